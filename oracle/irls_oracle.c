@@ -1,0 +1,844 @@
+/*
+ * irls_oracle.c — plain, slow, float64 CPU oracle for the IRLS s-t min-cut
+ * hot path of Zhu & Gleich, "A Parallel Min-Cut Algorithm using Iteratively
+ * Reweighted Least Squares" (arXiv 1501.03105).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference leg may load this library.  It
+ * shares no code, header, table or helper with the CUDA path
+ * (paper_1501_03105_b200/csrc); the two meet only in the seeded inputs of
+ * synthetic/generators.py.
+ *
+ * Citations: "P:Lnnn" = /root/reference/PAPER.md line nnn (equation numbers
+ * as in SURVEY.md §0); "S:Lnnn" = SPEC.md; "A<k>" / "O<k>" / "C<k>" =
+ * readings and arithmetic contract recorded in DESIGN.md §2 (taken from
+ * SURVEY.md §8(c)).
+ *
+ * Arithmetic: float64, compiled with -ffp-contract=off (C1: no FMA); sqrt and
+ * '/' are IEEE round-to-nearest.  Every sum follows the order stated at the
+ * point of use (C2 ascending neighbour id; C3 fixed reduction tree), so the
+ * results are a function of the inputs alone.
+ *
+ * Parity status: every function below is pinned by the
+ * `-m "not gpu"` tests in tests/test_oracle_*.py — closed forms, SPEC worked
+ * examples, dense numpy solves, brute-force cut enumeration, networkx max
+ * flow, invariants.  Functions with no independent pin say so in their
+ * comment ("parity unpinned").
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* status codes: numerically equal to irls_status in include/irls_mincut.h by
+ * specification; deliberately not shared. */
+enum {
+    ORC_OK = 0,
+    ORC_ERR_INVALID_ARGUMENT = 1,
+    ORC_ERR_SOURCE_EQUALS_SINK = 2,
+    ORC_ERR_BAD_CAPACITY = 3,
+    ORC_ERR_NOT_SYMMETRIC = 4,
+    ORC_ERR_SINGULAR = 5,
+    ORC_ERR_CG_BREAKDOWN = 6,
+    ORC_ERR_BAD_POTENTIAL = 7,
+    ORC_ERR_STATE = 8,
+    ORC_ERR_OOM = 11,
+};
+
+/* ------------------------------------------------------------------------- */
+/* Graph: the non-terminal graph G~ in reduced ids, plus the terminal */
+/* edges E^T as per-node capacities cs/ct and the direct s-t capacity (A5).  */
+/* ------------------------------------------------------------------------- */
+typedef struct {
+    int64_t n;          /* number of non-terminal nodes (n~) */
+    int64_t *adj_ptr;   /* n+1 */
+    int64_t *adj_idx;   /* neighbour reduced ids, strictly ascending (C2) */
+    double *adj_c;      /* n-link capacities, > 0 (A6: c = 0 is absent) */
+    double *cs, *ct;    /* terminal capacities (0 = absent) */
+    double c_st;        /* direct s-t capacity (A5) */
+    int64_t n_total;    /* ids in outputs: stencil N+2, CSR n */
+    int64_t *orig;      /* reduced id -> output id */
+    int64_t s_id, t_id; /* output ids of s and t */
+} orc_graph;
+
+static int is_bad_cap(double c) { return !(c >= 0.0) || isinf(c); }
+
+void orc_graph_free(orc_graph *g)
+{
+    if (!g) return;
+    free(g->adj_ptr); free(g->adj_idx); free(g->adj_c);
+    free(g->cs); free(g->ct); free(g->orig); free(g);
+}
+
+static orc_graph *graph_alloc(int64_t n, int64_t nnz)
+{
+    orc_graph *g = (orc_graph *)calloc(1, sizeof(orc_graph));
+    if (!g) return NULL;
+    g->n = n;
+    g->adj_ptr = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
+    g->adj_idx = (int64_t *)malloc(sizeof(int64_t) * (size_t)(nnz > 0 ? nnz : 1));
+    g->adj_c = (double *)malloc(sizeof(double) * (size_t)(nnz > 0 ? nnz : 1));
+    g->cs = (double *)calloc((size_t)(n > 0 ? n : 1), sizeof(double));
+    g->ct = (double *)calloc((size_t)(n > 0 ? n : 1), sizeof(double));
+    g->orig = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+    if (!g->adj_ptr || !g->adj_idx || !g->adj_c || !g->cs || !g->ct || !g->orig) {
+        orc_graph_free(g);
+        return NULL;
+    }
+    return g;
+}
+
+/* Stencil input: node u = x + nx*(y + ny*z); cx[u] = c(u,u+1),
+ * cy[u] = c(u,u+nx), cz[u] = c(u,u+nx*ny); entries past the grid edge are
+ * ignored.  s = N, t = N+1 are virtual.  Ascending neighbour order of a grid
+ * node is (-z, -y, -x, +x, +y, +z) (C2).  Zero capacities are absent (A6). */
+int orc_graph_from_stencil(orc_graph **out, int64_t nx, int64_t ny, int64_t nz,
+                           const double *cx, const double *cy, const double *cz,
+                           const double *cs, const double *ct)
+{
+    *out = NULL;
+    if (nx < 1 || ny < 1 || nz < 1) return ORC_ERR_INVALID_ARGUMENT;
+    int64_t N = nx * ny * nz, pl = nx * ny;
+    for (int64_t u = 0; u < N; u++) {
+        int64_t x = u % nx, y = (u / nx) % ny, z = u / pl;
+        if (x < nx - 1 && is_bad_cap(cx[u])) return ORC_ERR_BAD_CAPACITY;
+        if (y < ny - 1 && is_bad_cap(cy[u])) return ORC_ERR_BAD_CAPACITY;
+        if (z < nz - 1 && is_bad_cap(cz[u])) return ORC_ERR_BAD_CAPACITY;
+        if (is_bad_cap(cs[u]) || is_bad_cap(ct[u])) return ORC_ERR_BAD_CAPACITY;
+    }
+    orc_graph *g = graph_alloc(N, 6 * N);
+    if (!g) return ORC_ERR_OOM;
+    int64_t k = 0;
+    for (int64_t u = 0; u < N; u++) {
+        int64_t x = u % nx, y = (u / nx) % ny, z = u / pl;
+        g->adj_ptr[u] = k;
+#define PUSH(cond, v, c) do { if ((cond) && (c) > 0.0) { g->adj_idx[k] = (v); g->adj_c[k] = (c); k++; } } while (0)
+        PUSH(z > 0, u - pl, (z > 0 ? cz[u - pl] : 0.0));
+        PUSH(y > 0, u - nx, (y > 0 ? cy[u - nx] : 0.0));
+        PUSH(x > 0, u - 1, (x > 0 ? cx[u - 1] : 0.0));
+        PUSH(x < nx - 1, u + 1, cx[u]);
+        PUSH(y < ny - 1, u + nx, cy[u]);
+        PUSH(z < nz - 1, u + pl, cz[u]);
+#undef PUSH
+        g->cs[u] = cs[u];
+        g->ct[u] = ct[u];
+        g->orig[u] = u;
+    }
+    g->adj_ptr[N] = k;
+    g->c_st = 0.0;
+    g->n_total = N + 2;
+    g->s_id = N;
+    g->t_id = N + 1;
+    *out = g;
+    return ORC_OK;
+}
+
+typedef struct { int64_t col; int64_t pos; double w; } csr_ent;
+
+static int ent_cmp(const void *a, const void *b)
+{
+    const csr_ent *x = (const csr_ent *)a, *y = (const csr_ent *)b;
+    if (x->col != y->col) return x->col < y->col ? -1 : 1;
+    return x->pos < y->pos ? -1 : (x->pos > y->pos);
+}
+
+/* CSR input over all n nodes including s and t.  Duplicate
+ * entries of a row are merged by summation in CSR order (A7); self
+ * loops are rejected; the merged matrix must be exactly symmetric.  The edge
+ * {s,t} becomes the additive constant c_st (A5). */
+int orc_graph_from_csr(orc_graph **out, int64_t n, const int64_t *row_ptr,
+                       const int32_t *col, const double *w, int64_t s, int64_t t)
+{
+    *out = NULL;
+    if (n < 2 || s < 0 || t < 0 || s >= n || t >= n) return ORC_ERR_INVALID_ARGUMENT;
+    if (s == t) return ORC_ERR_SOURCE_EQUALS_SINK;
+    if (row_ptr[0] != 0) return ORC_ERR_INVALID_ARGUMENT;
+    for (int64_t u = 0; u < n; u++)
+        if (row_ptr[u + 1] < row_ptr[u]) return ORC_ERR_INVALID_ARGUMENT;
+    int64_t nnz = row_ptr[n];
+    for (int64_t e = 0; e < nnz; e++) {
+        if (col[e] < 0 || col[e] >= n) return ORC_ERR_INVALID_ARGUMENT;
+        if (is_bad_cap(w[e])) return ORC_ERR_BAD_CAPACITY;
+    }
+    for (int64_t u = 0; u < n; u++)
+        for (int64_t e = row_ptr[u]; e < row_ptr[u + 1]; e++)
+            if (col[e] == u) return ORC_ERR_INVALID_ARGUMENT;
+
+    /* merged rows: sort each row's entries by (col, position), sum runs */
+    int64_t *mptr = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
+    int64_t *mcol = (int64_t *)malloc(sizeof(int64_t) * (size_t)(nnz > 0 ? nnz : 1));
+    double *mw = (double *)malloc(sizeof(double) * (size_t)(nnz > 0 ? nnz : 1));
+    csr_ent *tmp = (csr_ent *)malloc(sizeof(csr_ent) * (size_t)(nnz > 0 ? nnz : 1));
+    if (!mptr || !mcol || !mw || !tmp) { free(mptr); free(mcol); free(mw); free(tmp); return ORC_ERR_OOM; }
+    int64_t m = 0;
+    for (int64_t u = 0; u < n; u++) {
+        int64_t a = row_ptr[u], b = row_ptr[u + 1];
+        for (int64_t e = a; e < b; e++) { tmp[e - a].col = col[e]; tmp[e - a].pos = e; tmp[e - a].w = w[e]; }
+        qsort(tmp, (size_t)(b - a), sizeof(csr_ent), ent_cmp);
+        mptr[u] = m;
+        for (int64_t i = 0; i < b - a; i++) {
+            if (i > 0 && tmp[i].col == tmp[i - 1].col) {
+                mw[m - 1] = mw[m - 1] + tmp[i].w;
+            } else {
+                mcol[m] = tmp[i].col; mw[m] = tmp[i].w; m++;
+            }
+        }
+    }
+    mptr[n] = m;
+    free(tmp);
+    /* exact symmetry of the merged matrix */
+    int rc = ORC_OK;
+    for (int64_t u = 0; u < n && rc == ORC_OK; u++) {
+        for (int64_t e = mptr[u]; e < mptr[u + 1]; e++) {
+            int64_t v = mcol[e];
+            int64_t lo = mptr[v], hi = mptr[v + 1], found = -1;
+            while (lo < hi) { int64_t mid = (lo + hi) / 2; if (mcol[mid] < u) lo = mid + 1; else hi = mid; }
+            if (lo < mptr[v + 1] && mcol[lo] == u) found = lo;
+            if (found < 0 || mw[found] != mw[e]) { rc = ORC_ERR_NOT_SYMMETRIC; break; }
+        }
+    }
+    if (rc != ORC_OK) { free(mptr); free(mcol); free(mw); return rc; }
+
+    int64_t nr = n - 2;
+    int64_t nn = 0;
+    for (int64_t u = 0; u < n; u++) {
+        if (u == s || u == t) continue;
+        for (int64_t e = mptr[u]; e < mptr[u + 1]; e++)
+            if (mcol[e] != s && mcol[e] != t && mw[e] > 0.0) nn++;
+    }
+    orc_graph *g = graph_alloc(nr, nn);
+    if (!g) { free(mptr); free(mcol); free(mw); return ORC_ERR_OOM; }
+    int64_t k = 0, r = 0;
+    for (int64_t u = 0; u < n; u++) {
+        if (u == s || u == t) continue;
+        g->adj_ptr[r] = k;
+        g->orig[r] = u;
+        for (int64_t e = mptr[u]; e < mptr[u + 1]; e++) {
+            int64_t v = mcol[e];
+            if (v == s) g->cs[r] = mw[e];
+            else if (v == t) g->ct[r] = mw[e];
+            else if (mw[e] > 0.0) {
+                g->adj_idx[k] = v - (v > s) - (v > t); /* reduced id, monotone in v */
+                g->adj_c[k] = mw[e];
+                k++;
+            }
+        }
+        r++;
+    }
+    g->adj_ptr[nr] = k;
+    g->c_st = 0.0;
+    for (int64_t e = mptr[s]; e < mptr[s + 1]; e++)
+        if (mcol[e] == t) g->c_st = mw[e];
+    g->n_total = n;
+    g->s_id = s;
+    g->t_id = t;
+    free(mptr); free(mcol); free(mw);
+    *out = g;
+    return ORC_OK;
+}
+
+int64_t orc_graph_n(const orc_graph *g) { return g->n; }
+int64_t orc_graph_n_total(const orc_graph *g) { return g->n_total; }
+int64_t orc_graph_nnz(const orc_graph *g) { return g->adj_ptr[g->n]; }
+double orc_graph_c_st(const orc_graph *g) { return g->c_st; }
+void orc_graph_orig_ids(const orc_graph *g, int64_t *out)
+{
+    for (int64_t u = 0; u < g->n; u++) out[u] = g->orig[u];
+}
+void orc_graph_terminals(const orc_graph *g, double *cs, double *ct)
+{
+    for (int64_t u = 0; u < g->n; u++) { cs[u] = g->cs[u]; ct[u] = g->ct[u]; }
+}
+
+/* Prop. 1 / A8: L~ is nonsingular iff every connected component
+ * of G~ (edges with c > 0) contains a node with a positive terminal edge.
+ * Plain BFS.  Returns ORC_OK or ORC_ERR_SINGULAR. */
+int orc_check_nonsingular(const orc_graph *g)
+{
+    int64_t n = g->n;
+    if (n == 0) return ORC_OK;
+    int64_t *queue = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    char *seen = (char *)calloc((size_t)n, 1);
+    if (!queue || !seen) { free(queue); free(seen); return ORC_ERR_OOM; }
+    int rc = ORC_OK;
+    for (int64_t r = 0; r < n && rc == ORC_OK; r++) {
+        if (seen[r]) continue;
+        int64_t head = 0, tail = 0; int anchored = 0;
+        queue[tail++] = r; seen[r] = 1;
+        while (head < tail) {
+            int64_t u = queue[head++];
+            if (g->cs[u] > 0.0 || g->ct[u] > 0.0) anchored = 1;
+            for (int64_t e = g->adj_ptr[u]; e < g->adj_ptr[u + 1]; e++) {
+                int64_t v = g->adj_idx[e];
+                if (!seen[v]) { seen[v] = 1; queue[tail++] = v; }
+            }
+        }
+        if (!anchored) rc = ORC_ERR_SINGULAR;
+    }
+    free(queue); free(seen);
+    return rc;
+}
+
+/* ------------------------------------------------------------------------- */
+/* C3: the fixed reduction tree (contract C3).                 */
+/* ------------------------------------------------------------------------- */
+#define C3_CHUNK 4096
+#define C3_THREADS 256
+#define C3_GROUPS 8
+
+/* One 4096-element chunk starting at `base` of v[0..n): "thread" t sums
+ * sequentially from +0.0 the elements base+2t+512j+v (j=0..7, v=0,1); the 32
+ * lanes of each warp combine by offsets 16,8,4,2,1 (lane i += lane i+off);
+ * the 8 warp sums by offsets 4,2,1.  Elements past n contribute nothing. */
+static double c3_chunk(const double *v, int64_t n, int64_t base)
+{
+    double th[C3_THREADS];
+    for (int t = 0; t < C3_THREADS; t++) {
+        double acc = 0.0;
+        for (int j = 0; j < 8; j++)
+            for (int q = 0; q < 2; q++) {
+                int64_t i = base + 2 * t + 512 * j + q;
+                if (i < n) acc = acc + v[i];
+            }
+        th[t] = acc;
+    }
+    double ws[8];
+    for (int w = 0; w < 8; w++) {
+        double *lane = th + 32 * w;
+        for (int off = 16; off >= 1; off /= 2)
+            for (int i = 0; i < off; i++) lane[i] = lane[i] + lane[i + off];
+        ws[w] = lane[0];
+    }
+    for (int off = 4; off >= 1; off /= 2)
+        for (int i = 0; i < off; i++) ws[i] = ws[i] + ws[i + off];
+    return ws[0];
+}
+
+/* A list of m values reduced chunk by chunk, repeated until one remains. */
+static double c3_list(double *a, int64_t m)
+{
+    if (m == 0) return 0.0;
+    while (m > 1) {
+        int64_t K = (m + C3_CHUNK - 1) / C3_CHUNK;
+        for (int64_t k = 0; k < K; k++) a[k] = c3_chunk(a, m, k * C3_CHUNK);
+        m = K;
+    }
+    return a[0];
+}
+
+/* Full C3 sum of v[0..n): chunk partials; 8 groups covering chunks
+ * [floor(gK/8), floor((g+1)K/8)); each group reduced as a fresh list; the 8
+ * group sums combined by offsets 4,2,1. */
+double orc_c3_sum(const double *v, int64_t n)
+{
+    int64_t K = (n + C3_CHUNK - 1) / C3_CHUNK;
+    double *part = (double *)malloc(sizeof(double) * (size_t)(K > 0 ? K : 1));
+    double gs[C3_GROUPS];
+    for (int64_t k = 0; k < K; k++) part[k] = c3_chunk(v, n, k * C3_CHUNK);
+    for (int g = 0; g < C3_GROUPS; g++) {
+        int64_t lo = (int64_t)g * K / C3_GROUPS, hi = (int64_t)(g + 1) * K / C3_GROUPS;
+        gs[g] = c3_list(part + lo, hi - lo);
+    }
+    free(part);
+    for (int off = 4; off >= 1; off /= 2)
+        for (int i = 0; i < off; i++) gs[i] = gs[i] + gs[i + off];
+    return gs[0];
+}
+
+/* Group sums only (the 8 values before the final tree), for the multi-rank
+ * slot-exact allreduce tests. */
+void orc_c3_group_sums(const double *v, int64_t n, double *out8)
+{
+    int64_t K = (n + C3_CHUNK - 1) / C3_CHUNK;
+    double *part = (double *)malloc(sizeof(double) * (size_t)(K > 0 ? K : 1));
+    for (int64_t k = 0; k < K; k++) part[k] = c3_chunk(v, n, k * C3_CHUNK);
+    for (int g = 0; g < C3_GROUPS; g++) {
+        int64_t lo = (int64_t)g * K / C3_GROUPS, hi = (int64_t)(g + 1) * K / C3_GROUPS;
+        out8[g] = c3_list(part + lo, hi - lo);
+    }
+    free(part);
+}
+
+/* ------------------------------------------------------------------------- */
+/* Assembly: Eq. 4 reweighting, Eq. 8 reweighted Laplacian, Eq. 7 reduction.  */
+/* ------------------------------------------------------------------------- */
+
+/* Eq. 4 with A2: w = sqrt((c*d)^2 + eps^2); Eq. 8:
+ * the edge's conductance in L^(l) is c^2 / w  (O3). */
+static double reweight_g(double c, double d, double eps2)
+{
+    double a = c * d;
+    double w = sqrt(a * a + eps2);
+    return (c * c) / w;
+}
+
+typedef struct {
+    const orc_graph *G;
+    double *g;     /* per adjacency entry conductance */
+    double *gs, *gt, *D, *Dinv;
+    double *x, *r, *z, *p, *q;
+    double *tmp;
+    double eps;
+    int32_t T, cg_max_iter, cg_norm, warm_start;
+    double cg_rtol;
+    int32_t step;  /* number of solves done (0 = none) */
+    double *cs, *ct; /* owned copy of terminal capacities (set_terminal_weights) */
+} orc_state;
+
+typedef struct {
+    double eps;
+    int32_t T;
+    double cg_rtol;
+    int32_t cg_max_iter;
+    int32_t cg_norm;      /* 0 = preconditioned (A9), 1 = unpreconditioned */
+    int32_t warm_start;
+} orc_options;
+
+typedef struct {
+    int32_t cg_iters, converged;
+    double rel_res;       /* recursive residual norm / ref at exit */
+    double true_rel_res;  /* ||b - A x|| (same norm) / ref */
+    double S_eps;         /* Eq. 9 at x^(l) */
+    double flow_value;    /* Prop. 3: x^T L^(l) x */
+    double current_s;     /* sum_u gs_u (1 - x_u) */
+    double x_min, x_max;
+    double ref;
+} orc_report;
+
+void orc_state_free(orc_state *S)
+{
+    if (!S) return;
+    free(S->g); free(S->gs); free(S->gt); free(S->D); free(S->Dinv);
+    free(S->x); free(S->r); free(S->z); free(S->p); free(S->q); free(S->tmp);
+    free(S->cs); free(S->ct); free(S);
+}
+
+orc_state *orc_state_new(const orc_graph *G, const orc_options *o)
+{
+    orc_state *S = (orc_state *)calloc(1, sizeof(orc_state));
+    if (!S) return NULL;
+    int64_t n = G->n > 0 ? G->n : 1, m = G->adj_ptr[G->n] > 0 ? G->adj_ptr[G->n] : 1;
+    S->G = G;
+    S->g = (double *)calloc((size_t)m, sizeof(double));
+    double **vecs[] = {&S->gs, &S->gt, &S->D, &S->Dinv, &S->x, &S->r, &S->z, &S->p, &S->q, &S->tmp, &S->cs, &S->ct};
+    for (size_t i = 0; i < sizeof(vecs) / sizeof(vecs[0]); i++) {
+        *vecs[i] = (double *)calloc((size_t)n, sizeof(double));
+        if (!*vecs[i]) { orc_state_free(S); return NULL; }
+    }
+    if (!S->g) { orc_state_free(S); return NULL; }
+    for (int64_t u = 0; u < G->n; u++) { S->cs[u] = G->cs[u]; S->ct[u] = G->ct[u]; }
+    S->eps = o->eps; S->T = o->T; S->cg_rtol = o->cg_rtol; S->cg_max_iter = o->cg_max_iter;
+    S->cg_norm = o->cg_norm; S->warm_start = o->warm_start;
+    S->step = 0;
+    return S;
+}
+
+/* O1 + O3/O4: conductances of every edge from x (or g = c when x == NULL,
+ * i.e. W^(0) = C), then D_u = ((sum_asc g_uv) + gs_u) + gt_u,
+ * Dinv_u = 1/D_u, b_u = gs_u (Eq. 7: b = -Z^T L e_s, x_s = 1, x_t = 0). */
+static void assemble(orc_state *S, const double *x)
+{
+    const orc_graph *G = S->G;
+    double eps2 = S->eps * S->eps;
+    for (int64_t u = 0; u < G->n; u++) {
+        double acc = 0.0;
+        for (int64_t e = G->adj_ptr[u]; e < G->adj_ptr[u + 1]; e++) {
+            double c = G->adj_c[e];
+            double gv = x ? reweight_g(c, x[u] - x[G->adj_idx[e]], eps2) : c;
+            S->g[e] = gv;
+            acc = acc + gv;
+        }
+        double cs = S->cs[u], ct = S->ct[u];
+        /* A3: terminal edges are reweighted with x_s = 1, x_t = 0 */
+        double gs = x ? reweight_g(cs, 1.0 - x[u], eps2) : cs;
+        double gt = x ? reweight_g(ct, x[u], eps2) : ct;
+        S->gs[u] = gs; S->gt[u] = gt;
+        S->D[u] = (acc + gs) + gt;
+        S->Dinv[u] = 1.0 / S->D[u];
+    }
+}
+
+/* O2: q = L~ p with acc = sum_asc g_uv p_v from +0.0, q_u = D_u p_u - acc. */
+static void matvec(const orc_state *S, const double *p, double *q)
+{
+    const orc_graph *G = S->G;
+    for (int64_t u = 0; u < G->n; u++) {
+        double acc = 0.0;
+        for (int64_t e = G->adj_ptr[u]; e < G->adj_ptr[u + 1]; e++)
+            acc = acc + S->g[e] * p[G->adj_idx[e]];
+        q[u] = S->D[u] * p[u] - acc;
+    }
+}
+
+static double dot_c3(orc_state *S, const double *a, const double *b)
+{
+    for (int64_t u = 0; u < S->G->n; u++) S->tmp[u] = a[u] * b[u];
+    return orc_c3_sum(S->tmp, S->G->n);
+}
+
+/* O5: Jacobi-preconditioned CG ("preconditioned conjugate gradient")
+ * on L~ v = b with M = diag(L~) (A12), Hestenes-Stiefel form, warm start x0
+ * = S->x, stopping test res <= rtol*ref before each iteration (A9,
+ * A13). */
+static int pcg(orc_state *S, orc_report *rep)
+{
+    const orc_graph *G = S->G;
+    int64_t n = G->n;
+    double *x = S->x, *r = S->r, *z = S->z, *p = S->p, *q = S->q;
+    /* r = b - A x0 */
+    matvec(S, x, q);
+    for (int64_t u = 0; u < n; u++) r[u] = S->gs[u] - q[u];
+    for (int64_t u = 0; u < n; u++) z[u] = r[u] * S->Dinv[u];
+    for (int64_t u = 0; u < n; u++) p[u] = z[u];
+    double rho = dot_c3(S, r, z);
+    double ref2;
+    if (S->cg_norm == 0) {
+        for (int64_t u = 0; u < n; u++) { double mb = S->gs[u] * S->Dinv[u]; S->tmp[u] = mb * mb; }
+        ref2 = orc_c3_sum(S->tmp, n);
+    } else {
+        ref2 = dot_c3(S, S->gs, S->gs);
+    }
+    double ref = sqrt(ref2);
+    rep->ref = ref;
+    if (ref == 0.0) { /* b = 0 => v = 0 */
+        for (int64_t u = 0; u < n; u++) x[u] = 0.0;
+        rep->cg_iters = 0; rep->converged = 1; rep->rel_res = 0.0;
+        return ORC_OK;
+    }
+    double res2 = S->cg_norm == 0 ? dot_c3(S, z, z) : dot_c3(S, r, r);
+    double res = sqrt(res2);
+    int32_t k = 0;
+    for (;;) {
+        if (res <= S->cg_rtol * ref || k == S->cg_max_iter) break;
+        matvec(S, p, q);
+        double pi = dot_c3(S, p, q);
+        if (!(pi > 0.0) || isinf(pi)) return ORC_ERR_CG_BREAKDOWN;
+        double alpha = rho / pi;
+        for (int64_t u = 0; u < n; u++) x[u] = x[u] + alpha * p[u];
+        for (int64_t u = 0; u < n; u++) r[u] = r[u] - alpha * q[u];
+        for (int64_t u = 0; u < n; u++) z[u] = r[u] * S->Dinv[u];
+        double rho1 = dot_c3(S, r, z);
+        res2 = S->cg_norm == 0 ? dot_c3(S, z, z) : dot_c3(S, r, r);
+        res = sqrt(res2);
+        double beta = rho1 / rho;
+        for (int64_t u = 0; u < n; u++) p[u] = z[u] + beta * p[u];
+        rho = rho1;
+        k++;
+        if (!isfinite(alpha) || !isfinite(beta) || !isfinite(res)) return ORC_ERR_CG_BREAKDOWN;
+    }
+    rep->cg_iters = k;
+    rep->converged = res <= S->cg_rtol * ref;
+    rep->rel_res = res / ref;
+    return ORC_OK;
+}
+
+/* O8 diagnostics at x = S->x with the step's conductances. */
+static void diagnostics(orc_state *S, orc_report *rep)
+{
+    const orc_graph *G = S->G;
+    int64_t n = G->n;
+    const double *x = S->x;
+    double eps2 = S->eps * S->eps;
+    /* Eq. 9: S_eps = sum over edges with c > 0 of w_e; node u
+     * owns its higher-id n-links (ascending) then its s- and t-links. */
+    for (int64_t u = 0; u < n; u++) {
+        double acc = 0.0;
+        for (int64_t e = G->adj_ptr[u]; e < G->adj_ptr[u + 1]; e++) {
+            int64_t v = G->adj_idx[e];
+            if (v < u) continue;
+            double a = G->adj_c[e] * (x[u] - x[v]);
+            acc = acc + sqrt(a * a + eps2);
+        }
+        if (S->cs[u] > 0.0) { double a = S->cs[u] * (1.0 - x[u]); acc = acc + sqrt(a * a + eps2); }
+        if (S->ct[u] > 0.0) { double a = S->ct[u] * x[u]; acc = acc + sqrt(a * a + eps2); }
+        S->tmp[u] = acc;
+    }
+    rep->S_eps = orc_c3_sum(S->tmp, n);
+    /* Prop. 3: flow value x^T L^(l) x = sum_e g_e d_e^2 */
+    for (int64_t u = 0; u < n; u++) {
+        double acc = 0.0;
+        for (int64_t e = G->adj_ptr[u]; e < G->adj_ptr[u + 1]; e++) {
+            int64_t v = G->adj_idx[e];
+            if (v < u) continue;
+            double d = x[u] - x[v];
+            acc = acc + S->g[e] * (d * d);
+        }
+        double ds = 1.0 - x[u];
+        acc = acc + S->gs[u] * (ds * ds);
+        acc = acc + S->gt[u] * (x[u] * x[u]);
+        S->tmp[u] = acc;
+    }
+    rep->flow_value = orc_c3_sum(S->tmp, n);
+    for (int64_t u = 0; u < n; u++) S->tmp[u] = S->gs[u] * (1.0 - x[u]);
+    rep->current_s = orc_c3_sum(S->tmp, n);
+    /* true residual in the stopping norm */
+    double *q = S->q;
+    matvec(S, x, q);
+    for (int64_t u = 0; u < n; u++) {
+        double rr = S->gs[u] - q[u];
+        double v = S->cg_norm == 0 ? rr * S->Dinv[u] : rr;
+        S->tmp[u] = v * v;
+    }
+    double tr = sqrt(orc_c3_sum(S->tmp, n));
+    rep->true_rel_res = rep->ref > 0.0 ? tr / rep->ref : 0.0;
+    double mn = n ? x[0] : 0.0, mx = n ? x[0] : 0.0;
+    for (int64_t u = 0; u < n; u++) { if (x[u] < mn) mn = x[u]; if (x[u] > mx) mx = x[u]; }
+    rep->x_min = mn; rep->x_max = mx;
+}
+
+/* Algorithm 1 step 2 / O4: x^(0) solves Eq. 5 with W^(0) = C, cold. */
+int orc_init(orc_state *S, orc_report *rep)
+{
+    memset(rep, 0, sizeof(*rep));
+    assemble(S, NULL);
+    for (int64_t u = 0; u < S->G->n; u++) S->x[u] = 0.0;
+    int rc = pcg(S, rep);
+    if (rc != ORC_OK) return rc;
+    diagnostics(S, rep);
+    S->step = 1;
+    return ORC_OK;
+}
+
+/* Algorithm 1 step 4 / O6: reweight from x^(l-1) (Eq. 4), then
+ * solve L~^(l) v = b^(l), warm-started from x^(l-1) or cold. */
+int orc_step(orc_state *S, orc_report *rep)
+{
+    memset(rep, 0, sizeof(*rep));
+    if (S->step == 0) return ORC_ERR_STATE;
+    assemble(S, S->x);
+    if (!S->warm_start)
+        for (int64_t u = 0; u < S->G->n; u++) S->x[u] = 0.0;
+    int rc = pcg(S, rep);
+    if (rc != ORC_OK) return rc;
+    diagnostics(S, rep);
+    S->step++;
+    return ORC_OK;
+}
+
+void orc_get_x(const orc_state *S, double *x)
+{
+    for (int64_t u = 0; u < S->G->n; u++) x[u] = S->x[u];
+}
+
+void orc_set_x(orc_state *S, const double *x)
+{
+    for (int64_t u = 0; u < S->G->n; u++) S->x[u] = x[u];
+    if (S->step == 0) S->step = 1;
+}
+
+/* A19 / P:L451: replace the terminal capacities, keep x. */
+int orc_set_terminal_weights(orc_state *S, const double *cs, const double *ct)
+{
+    for (int64_t u = 0; u < S->G->n; u++)
+        if (is_bad_cap(cs[u]) || is_bad_cap(ct[u])) return ORC_ERR_BAD_CAPACITY;
+    for (int64_t u = 0; u < S->G->n; u++) { S->cs[u] = cs[u]; S->ct[u] = ct[u]; }
+    return ORC_OK;
+}
+
+/* For unit pins: conductances, D, Dinv, b after assemble(x) (x NULL = init). */
+void orc_assemble_export(orc_state *S, const double *x, double *g, double *gs, double *gt,
+                         double *D, double *Dinv)
+{
+    assemble(S, x);
+    const orc_graph *G = S->G;
+    for (int64_t e = 0; e < G->adj_ptr[G->n]; e++) g[e] = S->g[e];
+    for (int64_t u = 0; u < G->n; u++) { gs[u] = S->gs[u]; gt[u] = S->gt[u]; D[u] = S->D[u]; Dinv[u] = S->Dinv[u]; }
+}
+
+/* Run a full solve (init + T steps), optionally recording x^(l) for l=0..T
+ * (xs has (T+1)*n entries) and the reports (T+1). */
+int orc_irls_run(orc_state *S, double *xs, orc_report *reps)
+{
+    orc_report rep;
+    int rc = orc_init(S, &rep);
+    if (rc) return rc;
+    if (reps) reps[0] = rep;
+    int64_t n = S->G->n;
+    if (xs) for (int64_t u = 0; u < n; u++) xs[u] = S->x[u];
+    for (int32_t l = 1; l <= S->T; l++) {
+        rc = orc_step(S, &rep);
+        if (rc) return rc;
+        if (reps) reps[l] = rep;
+        if (xs) for (int64_t u = 0; u < n; u++) xs[(int64_t)l * n + u] = S->x[u];
+    }
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Sweep cut ("sorting the nodes according to x^(T)").    */
+/* ------------------------------------------------------------------------- */
+typedef __int128 i128;
+
+static const double *sort_x;
+static int sweep_cmp(const void *a, const void *b)
+{
+    int64_t i = *(const int64_t *)a, j = *(const int64_t *)b;
+    double xi = sort_x[i], xj = sort_x[j];
+    if (xi > xj) return -1;   /* x descending */
+    if (xi < xj) return 1;
+    return (i > j) - (i < j); /* ties: id ascending (A14) */
+}
+
+/* A15: prefix sums of the sweep are exact integer sums of capacities in
+ * fixed point with F fractional bits, Q(c) = rint(c * 2^F), F = 124 - e - b
+ * where cmax < 2^e (frexp) and b = bit length of the number of positive
+ * capacities (n-links + s-links + t-links + direct s-t). */
+static int32_t sweep_F(const orc_graph *G, const double *cs, const double *ct)
+{
+    double cmax = G->c_st;
+    int64_t cnt = G->c_st > 0.0;
+    for (int64_t u = 0; u < G->n; u++) {
+        for (int64_t e = G->adj_ptr[u]; e < G->adj_ptr[u + 1]; e++)
+            if (G->adj_idx[e] > u) { cnt++; if (G->adj_c[e] > cmax) cmax = G->adj_c[e]; }
+        if (cs[u] > 0.0) { cnt++; if (cs[u] > cmax) cmax = cs[u]; }
+        if (ct[u] > 0.0) { cnt++; if (ct[u] > cmax) cmax = ct[u]; }
+    }
+    if (cmax == 0.0) return 0;
+    int e; frexp(cmax, &e);
+    int b = 0; while (b < 63 && (((int64_t)1) << b) <= cnt) b++;
+    return 124 - e - b;
+}
+
+static i128 Qfix(double c, int32_t F) { return (i128)rint(ldexp(c, F)); }
+
+/* O7: order non-terminals by (x desc, id asc); delta_v = sum over neighbours
+ * u of (+c if u is later in the order else -c) + ct_v - cs_v; P_0 = sum cs +
+ * c_st; P_i = P_{i-1} + delta_{order[i-1]} (exact, fixed point); k = first
+ * argmin of P_i over i = 0..n; S = {s} + order[0..k).  The reported cut value
+ * is recomputed from S by C3 ("recomputed, not trusted").
+ * side: n_total bytes (1 = source side); order: n output ids (or NULL);
+ * pk_words: P_k as (lo, hi) 64-bit words (or NULL). */
+int orc_sweep(const orc_state *S, const double *x, uint8_t *side, int64_t *order_out,
+              int64_t *k_out, double *cut_out, int32_t *F_out, uint64_t *pk_words)
+{
+    const orc_graph *G = S->G;
+    int64_t n = G->n;
+    for (int64_t u = 0; u < n; u++) if (isnan(x[u])) return ORC_ERR_BAD_POTENTIAL;
+    int64_t *order = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+    int64_t *rank = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+    i128 *delta = (i128 *)malloc(sizeof(i128) * (size_t)(n > 0 ? n : 1));
+    double *cross = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    if (!order || !rank || !delta || !cross) { free(order); free(rank); free(delta); free(cross); return ORC_ERR_OOM; }
+    for (int64_t u = 0; u < n; u++) order[u] = u;
+    sort_x = x;
+    qsort(order, (size_t)n, sizeof(int64_t), sweep_cmp);
+    for (int64_t i = 0; i < n; i++) rank[order[i]] = i;
+    int32_t F = sweep_F(G, S->cs, S->ct);
+    for (int64_t v = 0; v < n; v++) {
+        i128 d = 0;
+        for (int64_t e = G->adj_ptr[v]; e < G->adj_ptr[v + 1]; e++) {
+            int64_t u = G->adj_idx[e];
+            i128 qc = Qfix(G->adj_c[e], F);
+            d += rank[u] > rank[v] ? qc : -qc;
+        }
+        d += Qfix(S->ct[v], F);
+        d -= Qfix(S->cs[v], F);
+        delta[v] = d;
+    }
+    i128 P = Qfix(G->c_st, F);
+    for (int64_t v = 0; v < n; v++) P += Qfix(S->cs[v], F);
+    i128 best = P; int64_t k = 0;
+    for (int64_t i = 1; i <= n; i++) {
+        P += delta[order[i - 1]];
+        if (P < best) { best = P; k = i; }
+    }
+    /* membership and directly recomputed cut value */
+    for (int64_t id = 0; id < G->n_total; id++) side[id] = 0;
+    side[G->s_id] = 1;
+    for (int64_t i = 0; i < k; i++) side[G->orig[order[i]]] = 1;
+    for (int64_t v = 0; v < n; v++) {
+        if (rank[v] < k) {
+            double acc = 0.0;
+            for (int64_t e = G->adj_ptr[v]; e < G->adj_ptr[v + 1]; e++)
+                if (rank[G->adj_idx[e]] >= k) acc = acc + G->adj_c[e];
+            cross[v] = acc + S->ct[v];
+        } else {
+            cross[v] = S->cs[v];
+        }
+    }
+    double cut = orc_c3_sum(cross, n) + G->c_st;
+    if (order_out) for (int64_t i = 0; i < n; i++) order_out[i] = G->orig[order[i]];
+    *k_out = k;
+    *cut_out = cut;
+    if (F_out) *F_out = F;
+    if (pk_words) { pk_words[0] = (uint64_t)best; pk_words[1] = (uint64_t)(best >> 64); }
+    free(order); free(rank); free(delta); free(cross);
+    return ORC_OK;
+}
+
+/* cut(S, S-bar) by definition over the graph held by S (with its
+ * current terminal capacities); side indexed by output id. */
+double orc_cut_value(const orc_state *S, const uint8_t *side)
+{
+    const orc_graph *G = S->G;
+    double cut = 0.0;
+    int ss = side[G->s_id], st = side[G->t_id];
+    for (int64_t u = 0; u < G->n; u++) {
+        int su = side[G->orig[u]];
+        for (int64_t e = G->adj_ptr[u]; e < G->adj_ptr[u + 1]; e++) {
+            int64_t v = G->adj_idx[e];
+            if (v > u && su != side[G->orig[v]]) cut += G->adj_c[e];
+        }
+        if (su != ss) cut += S->cs[u];
+        if (su != st) cut += S->ct[u];
+    }
+    if (ss != st) cut += G->c_st;
+    return cut;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Exact min cut mu* by Edmonds-Karp (shortest augmenting paths) on the whole */
+/* graph, used to evaluate delta (Eq. 13).  Undirected edge {u,v} */
+/* = two arcs of capacity c, each the other's residual twin.                  */
+/* ------------------------------------------------------------------------- */
+int orc_maxflow_ek(const orc_state *S, double *flow_out, uint8_t *side)
+{
+    const orc_graph *G = S->G;
+    int64_t n = G->n, V = n + 2, s = n, t = n + 1;
+    int64_t m = G->adj_ptr[n] / 2 + 2 * n + 1; /* undirected edges (upper bound) */
+    int64_t *head = (int64_t *)malloc(sizeof(int64_t) * (size_t)V);
+    int64_t *nxt = (int64_t *)malloc(sizeof(int64_t) * (size_t)(2 * m));
+    int64_t *to = (int64_t *)malloc(sizeof(int64_t) * (size_t)(2 * m));
+    double *res = (double *)malloc(sizeof(double) * (size_t)(2 * m));
+    int64_t *prev = (int64_t *)malloc(sizeof(int64_t) * (size_t)V);
+    int64_t *queue = (int64_t *)malloc(sizeof(int64_t) * (size_t)V);
+    if (!head || !nxt || !to || !res || !prev || !queue) {
+        free(head); free(nxt); free(to); free(res); free(prev); free(queue); return ORC_ERR_OOM;
+    }
+    for (int64_t i = 0; i < V; i++) head[i] = -1;
+    int64_t A = 0;
+    double cmax = G->c_st;
+#define ADD_EDGE(a, b, c) do { to[A] = (b); res[A] = (c); nxt[A] = head[a]; head[a] = A; A++; \
+                               to[A] = (a); res[A] = (c); nxt[A] = head[b]; head[b] = A; A++; } while (0)
+    for (int64_t u = 0; u < n; u++) {
+        for (int64_t e = G->adj_ptr[u]; e < G->adj_ptr[u + 1]; e++)
+            if (G->adj_idx[e] > u) { ADD_EDGE(u, G->adj_idx[e], G->adj_c[e]); if (G->adj_c[e] > cmax) cmax = G->adj_c[e]; }
+        if (S->cs[u] > 0.0) { ADD_EDGE(s, u, S->cs[u]); if (S->cs[u] > cmax) cmax = S->cs[u]; }
+        if (S->ct[u] > 0.0) { ADD_EDGE(u, t, S->ct[u]); if (S->ct[u] > cmax) cmax = S->ct[u]; }
+    }
+    if (G->c_st > 0.0) ADD_EDGE(s, t, G->c_st);
+#undef ADD_EDGE
+    double tol = 1e-12 * cmax, flow = 0.0;
+    for (;;) {
+        for (int64_t i = 0; i < V; i++) prev[i] = -2;
+        int64_t qh = 0, qt = 0;
+        queue[qt++] = s; prev[s] = -1;
+        while (qh < qt && prev[t] == -2) {
+            int64_t u = queue[qh++];
+            for (int64_t a = head[u]; a >= 0; a = nxt[a])
+                if (res[a] > tol && prev[to[a]] == -2) { prev[to[a]] = a; queue[qt++] = to[a]; }
+        }
+        if (prev[t] == -2) break;
+        double b = INFINITY;
+        for (int64_t v = t; v != s; v = to[prev[v] ^ 1]) if (res[prev[v]] < b) b = res[prev[v]];
+        for (int64_t v = t; v != s; v = to[prev[v] ^ 1]) { res[prev[v]] -= b; res[prev[v] ^ 1] += b; }
+        flow += b;
+    }
+    /* reachable set from s in the final residual graph: prev != -2 */
+    for (int64_t id = 0; id < G->n_total; id++) side[id] = 0;
+    side[G->s_id] = 1;
+    for (int64_t u = 0; u < n; u++) if (prev[u] != -2) side[G->orig[u]] = 1;
+    *flow_out = flow;
+    free(head); free(nxt); free(to); free(res); free(prev); free(queue);
+    return ORC_OK;
+}
