@@ -1,0 +1,197 @@
+/*
+ * irls_mincut.h — C ABI of the B200-native IRLS s-t min-cut hot path.
+ *
+ * Method: Zhu & Gleich, "A Parallel Min-Cut Algorithm using Iteratively
+ * Reweighted Least Squares", arXiv 1501.03105.  Citations "P:Lnnn"
+ * are PAPER.md lines; readings A<k>, the oracle steps O<k> and the arithmetic
+ * contract C1-C3 are listed in DESIGN.md §2.
+ *
+ * What the library computes (Algorithm 1, without the partition
+ * step):
+ *   x^(0)  = solution of the constrained WLS Eq. 5 with W^(0) = C,
+ *   for l = 1..T:
+ *     w^(l) = sqrt((C B x^(l-1))^2 + eps^2)                 (Eq. 4)
+ *     L^(l) = B^T C (W^(l))^-1 C B                           (Eq. 8)
+ *     solve the reduced system L~^(l) v = b^(l)               (Eq. 7)
+ *       by Jacobi-preconditioned CG warm-started from v^(l-1)
+ *   sweep cut of x^(T): sort by potential, prefix-sum the per-node cut
+ *   deltas, take the first argmin
+ *
+ * Conventions shared by every entry point
+ *   - All floating point is IEEE float64 without FMA contraction (C1); all
+ *     sums follow C2/C3, so results are bitwise identical to the CPU oracle
+ *     and independent of the number of GPUs.
+ *   - Input arrays are HOST memory, copied at create; the caller keeps
+ *     ownership.  Output arrays are caller-owned HOST memory unless a
+ *     function says otherwise.  Device memory is owned by the context.
+ *   - Multi-GPU: one process per GPU; every call is collective (all ranks,
+ *     same order).  Only rank 0 fills sweep / potential outputs; other ranks
+ *     may pass NULL.
+ *   - Every call is stream-ordered on the context's stream and returns after
+ *     its results are final.
+ *   - Argument errors (IRLS_ERR_INVALID_ARGUMENT and the validation codes at
+ *     create) are detected on the host before device work.  After any other
+ *     error the context is poisoned: later calls return IRLS_ERR_STATE until
+ *     irls_mincut_destroy.  A non-converged CG is NOT an error: the
+ *     report says converged = 0.
+ *   - No C++ exception crosses this boundary.
+ */
+#ifndef IRLS_MINCUT_H
+#define IRLS_MINCUT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct irls_ctx irls_ctx; /* opaque; one per rank; not thread-safe */
+
+typedef enum {
+    IRLS_OK = 0,
+    IRLS_ERR_INVALID_ARGUMENT = 1,   /* bad sizes, NULL pointers, self loop, eps <= 0, ... */
+    IRLS_ERR_SOURCE_EQUALS_SINK = 2, /* s == t */
+    IRLS_ERR_BAD_CAPACITY = 3,       /* c < 0, NaN or Inf (P:L42 requires c >= 0; A6) */
+    IRLS_ERR_NOT_SYMMETRIC = 4,      /* CSR after duplicate merging is not symmetric */
+    IRLS_ERR_SINGULAR = 5,           /* a component of G~ has no positive terminal edge (Prop. 1; A8) */
+    IRLS_ERR_CG_BREAKDOWN = 6,       /* p'Ap <= 0 or a non-finite CG scalar */
+    IRLS_ERR_BAD_POTENTIAL = 7,      /* NaN in x at the sweep */
+    IRLS_ERR_STATE = 8,              /* wrong call order, or poisoned context */
+    IRLS_ERR_CUDA = 9,
+    IRLS_ERR_NCCL = 10,
+    IRLS_ERR_OOM = 11
+} irls_status;
+
+typedef enum { IRLS_NORM_PRECONDITIONED = 0, IRLS_NORM_UNPRECONDITIONED = 1 } irls_cg_norm;
+typedef enum { IRLS_LOOP_GRAPH = 0, IRLS_LOOP_HOST = 1 } irls_loop_mode;
+
+/* Solver options (A9-A13). */
+typedef struct {
+    double eps;          /* smoothing eps of Eq. 4, > 0; default 1e-6 */
+    int32_t T;           /* IRLS steps after x^(0) (A1); default 50 */
+    double cg_rtol;      /* stop when ||res|| <= cg_rtol * ||ref|| (A9); default 1e-3 */
+    int32_t cg_max_iter; /* PCG iteration cap per solve; default 50 */
+    int32_t cg_norm;     /* irls_cg_norm: PRECONDITIONED ||M^-1 r|| vs ||M^-1 b|| (default), or ||r|| vs ||b|| */
+    int32_t warm_start;  /* 1: CG starts from v^(l-1); 0: cold start from 0 */
+    int32_t record_trace;/* 1: fill S_eps / flow / true residual / x range in reports (extra passes) */
+    int32_t loop_mode;   /* irls_loop_mode: CUDA graph with device-side WHILE loop (default) or host loop */
+} irls_options;
+
+void irls_options_default(irls_options *opt);
+
+/* Process / device description.  world_size 1: nccl_unique_id may be NULL.
+ * cuda_stream: a cudaStream_t to run on, or NULL for a library-owned one. */
+typedef struct {
+    int32_t world_size, rank, device;
+    const uint8_t *nccl_unique_id; /* 128 bytes from irls_nccl_unique_id on rank 0, broadcast by the caller */
+    void *cuda_stream;
+} irls_comm_desc;
+
+/* Fill a fresh NCCL unique id (128 bytes) on rank 0. */
+irls_status irls_nccl_unique_id(uint8_t out[128]);
+
+/* Structured 2-D/3-D grid (the GraphCut / MRI configs).  N = nx*ny*nz
+ * non-terminal nodes, u = x + nx*(y + ny*z); s = N and t = N+1 are virtual.
+ * cx[u] = c(u, u+1) (ignored at x = nx-1), cy[u] = c(u, u+nx) (ignored at
+ * y = ny-1), cz[u] = c(u, u+nx*ny) (ignored at z = nz-1); cs[u] = c(s,u),
+ * ct[u] = c(u,t).  All arrays length N, host, float64, >= 0 (0 = absent edge,
+ * A6).  Multi-GPU: z-slab partition aligned to the C3 groups (every rank owns
+ * whole groups); world_size must divide 8 and the partition must be
+ * group-aligned, else IRLS_ERR_INVALID_ARGUMENT.  Every rank passes the full
+ * arrays. */
+irls_status irls_mincut_create_stencil(irls_ctx **ctx, const irls_comm_desc *comm,
+                                       int32_t nx, int32_t ny, int32_t nz,
+                                       const double *cx, const double *cy, const double *cz,
+                                       const double *cs, const double *ct,
+                                       const irls_options *opt);
+
+/* General undirected graph as CSR over all n nodes including s and t:
+ * row_ptr[n+1] (int64), col[row_ptr[n]] (int32), w (float64 >= 0).  Entries of
+ * a row with the same column are merged by summation in CSR order (A7); self
+ * loops are rejected; the merged matrix must be exactly symmetric.  The edge
+ * {s,t}, if present, is the additive constant c_st (A5).  Single GPU in this
+ * version (world_size 1). */
+irls_status irls_mincut_create_csr(irls_ctx **ctx, const irls_comm_desc *comm, int64_t n,
+                                   const int64_t *row_ptr, const int32_t *col, const double *w,
+                                   int64_t s, int64_t t, const irls_options *opt);
+
+/* Per-solve diagnostics. */
+typedef struct {
+    int32_t cg_iters, converged, status, reserved;
+    double rel_res;      /* recursive residual / ref at exit */
+    double true_rel_res; /* record_trace: ||b - A x|| / ref (same norm) */
+    double S_eps;        /* record_trace: Eq. 9 at x^(l) */
+    double flow_value;   /* record_trace: Prop. 3, x^T L^(l) x */
+    double current_s;    /* record_trace: sum_u g_su (1 - x_u) */
+    double x_min, x_max; /* record_trace */
+    double ref;          /* ||M^-1 b|| or ||b|| */
+    float ms;            /* device time of this solve */
+    float reserved2;
+} irls_step_report;
+
+/* x^(0): W = C, cold CG (Alg. 1 step 2).  report may be NULL. */
+irls_status irls_init(irls_ctx *ctx, irls_step_report *report);
+/* One IRLS step: reweight from the current x (Eq. 4), assemble (Eq. 7-8),
+ * PCG warm or cold per options.  Requires irls_init (or set_potentials). */
+irls_status irls_step(irls_ctx *ctx, irls_step_report *report);
+
+typedef enum { IRLS_FROM_SCRATCH = 0, IRLS_CONTINUE = 1 } irls_solve_mode;
+/* FROM_SCRATCH: irls_init then T steps (T+1 solves).  CONTINUE: T steps from
+ * the current x (a warm-started sequence of related problems).
+ * per_step: T+1 (FROM_SCRATCH) or T (CONTINUE) reports, or NULL. */
+irls_status irls_solve(irls_ctx *ctx, int32_t mode, irls_step_report *per_step,
+                       int64_t *total_cg_iters);
+
+/* Sweep cut of the current x (O7): order non-terminals by (x desc, id
+ * asc), prefix sums of per-node cut deltas in exact fixed point (A15), first
+ * argmin.  side: host bytes, one per output id (stencil N+2, CSR n), 1 =
+ * source side; order: host, n~ output ids in sweep order, or NULL; k: number
+ * of non-terminals on the source side; cut_value: recomputed from the set
+ * (C3).  side may be NULL: the result stays on the device (irls_get_side).
+ * Only rank 0 writes outputs. */
+irls_status irls_sweep_cut(irls_ctx *ctx, uint8_t *side, int32_t *order, int64_t *k,
+                           double *cut_value);
+irls_status irls_get_side(irls_ctx *ctx, uint8_t *side);
+
+/* Replace the terminal capacities (full arrays, length n~ in reduced order:
+ * stencil u, CSR ascending original id without s and t); keeps x. */
+irls_status irls_set_terminal_weights(irls_ctx *ctx, const double *cs, const double *ct);
+
+/* Potentials of the n~ non-terminals in reduced order (host). */
+irls_status irls_get_potentials(irls_ctx *ctx, double *x);
+irls_status irls_set_potentials(irls_ctx *ctx, const double *x);
+
+/* Counters of the last solve: kernel launches of this library and device
+ * time of the dominant kernels, for the roofline. */
+typedef struct {
+    int64_t launches;        /* kernels launched by the library in the last irls_solve / sweep */
+    int64_t cg_iters;        /* CG iterations in the last irls_solve */
+    int64_t n_nonterminal;   /* n~ (global) */
+    int64_t n_links;         /* |E~| with c > 0 (global) */
+    int64_t n_local;         /* non-terminals owned by this rank */
+} irls_stats;
+irls_status irls_get_stats(irls_ctx *ctx, irls_stats *stats);
+
+/* Kernel timing with CUDA events on the context's stream, on the current
+ * state: runs `reps` launches of kernel `which` (0 = CG SpMV+p-update K3,
+ * 1 = CG axpy+Jacobi K5, 2 = reweight+assemble K1) and returns the mean ms.
+ * The CG state is saved and restored, so the solve state is unchanged. */
+irls_status irls_time_kernel(irls_ctx *ctx, int32_t which, int32_t reps, float *mean_ms);
+
+void irls_mincut_destroy(irls_ctx *ctx);
+const char *irls_status_string(irls_status st);
+const char *irls_last_error(const irls_ctx *ctx);
+
+/* ---- host-only helpers of the multi-GPU plan (no device work) ----------- */
+/* C3 groups of a length-n index space: chunk count K = ceil(n/4096); group g
+ * covers chunks [floor(gK/8), floor((g+1)K/8)). */
+irls_status irls_plan_stencil(int32_t nx, int32_t ny, int32_t nz, int32_t world, int32_t rank,
+                              int32_t *z0, int32_t *z1, int32_t *g0, int32_t *g1);
+/* The fixed 8-leaf tree of C3 step 6: ((s0+s4)+(s2+s6))+((s1+s5)+(s3+s7)). */
+double irls_combine_slots(const double slots[8]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IRLS_MINCUT_H */

@@ -1,0 +1,1179 @@
+// api.cu — the C ABI (include/irls_mincut.h): validation, device memory,
+// the per-solve CUDA graph with a device-side WHILE loop, the host-loop and
+// multi-GPU paths, and the sweep orchestration.
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <queue>
+#include <string>
+#include <vector>
+
+#include "ctx.h"
+
+using namespace irls;
+
+// ---------------------------------------------------------------------------
+// error plumbing
+// ---------------------------------------------------------------------------
+static irls_status fail(irls_ctx *c, irls_status st, const std::string &msg)
+{
+    if (c) {
+        c->err = msg;
+        if (st != IRLS_ERR_INVALID_ARGUMENT && st != IRLS_ERR_BAD_POTENTIAL && st != IRLS_ERR_STATE) c->poisoned = true;
+    }
+    return st;
+}
+
+#define CK(call)                                                                                      \
+    do {                                                                                              \
+        cudaError_t e__ = (call);                                                                     \
+        if (e__ != cudaSuccess)                                                                       \
+            return fail(c, e__ == cudaErrorMemoryAllocation ? IRLS_ERR_OOM : IRLS_ERR_CUDA,           \
+                        std::string(#call) + ": " + cudaGetErrorString(e__));                         \
+    } while (0)
+
+#define NK(call)                                                                                      \
+    do {                                                                                              \
+        ncclResult_t r__ = (call);                                                                    \
+        if (r__ != ncclSuccess) return fail(c, IRLS_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r__)); \
+    } while (0)
+
+#define GUARD(c)                                                                  \
+    do {                                                                          \
+        if (!(c)) return IRLS_ERR_INVALID_ARGUMENT;                               \
+        if ((c)->poisoned) return IRLS_ERR_STATE;                                 \
+        if (cudaSetDevice((c)->device) != cudaSuccess) return IRLS_ERR_CUDA;      \
+    } while (0)
+
+static irls_status last_launch(irls_ctx *c, const char *what)
+{
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(c, IRLS_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    return IRLS_OK;
+}
+
+template <class T>
+static T *dalloc(irls_ctx *c, int64_t count)
+{
+    void *p = nullptr;
+    const size_t bytes = (size_t)std::max<int64_t>(count, 1) * sizeof(T);
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+    cudaMemset(p, 0, bytes);
+    c->allocs.push_back(p);
+    return (T *)p;
+}
+
+extern "C" void irls_options_default(irls_options *o)
+{
+    if (!o) return;
+    o->eps = 1e-6;
+    o->T = 50;
+    o->cg_rtol = 1e-3;
+    o->cg_max_iter = 50;
+    o->cg_norm = IRLS_NORM_PRECONDITIONED;
+    o->warm_start = 1;
+    o->record_trace = 0;
+    o->loop_mode = IRLS_LOOP_GRAPH;
+}
+
+extern "C" const char *irls_status_string(irls_status st)
+{
+    switch (st) {
+    case IRLS_OK: return "IRLS_OK";
+    case IRLS_ERR_INVALID_ARGUMENT: return "IRLS_ERR_INVALID_ARGUMENT";
+    case IRLS_ERR_SOURCE_EQUALS_SINK: return "IRLS_ERR_SOURCE_EQUALS_SINK";
+    case IRLS_ERR_BAD_CAPACITY: return "IRLS_ERR_BAD_CAPACITY";
+    case IRLS_ERR_NOT_SYMMETRIC: return "IRLS_ERR_NOT_SYMMETRIC";
+    case IRLS_ERR_SINGULAR: return "IRLS_ERR_SINGULAR";
+    case IRLS_ERR_CG_BREAKDOWN: return "IRLS_ERR_CG_BREAKDOWN";
+    case IRLS_ERR_BAD_POTENTIAL: return "IRLS_ERR_BAD_POTENTIAL";
+    case IRLS_ERR_STATE: return "IRLS_ERR_STATE";
+    case IRLS_ERR_CUDA: return "IRLS_ERR_CUDA";
+    case IRLS_ERR_NCCL: return "IRLS_ERR_NCCL";
+    case IRLS_ERR_OOM: return "IRLS_ERR_OOM";
+    }
+    return "IRLS_ERR_UNKNOWN";
+}
+
+extern "C" const char *irls_last_error(const irls_ctx *c) { return c ? c->err.c_str() : "null context"; }
+
+extern "C" irls_status irls_nccl_unique_id(uint8_t out[128])
+{
+    if (!out) return IRLS_ERR_INVALID_ARGUMENT;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return IRLS_ERR_NCCL;
+    static_assert(sizeof(id) == 128, "ncclUniqueId size");
+    memcpy(out, &id, 128);
+    return IRLS_OK;
+}
+
+// C3 step 6 on the host (slots after the slot-exact allreduce).
+extern "C" double irls_combine_slots(const double s[8])
+{
+    return ((s[0] + s[4]) + (s[2] + s[6])) + ((s[1] + s[5]) + (s[3] + s[7]));
+}
+
+static int count_nonempty(int32_t K, int g0, int g1)
+{
+    int n = 0;
+    for (int g = g0; g < g1; g++)
+        if (group_lo(g + 1, K) > group_lo(g, K)) n++;
+    return n;
+}
+
+// z-slab plan: rank r owns C3 groups [8r/W, 8(r+1)/W); the slab must start
+// and end on z-plane boundaries.
+extern "C" irls_status irls_plan_stencil(int32_t nx, int32_t ny, int32_t nz, int32_t world, int32_t rank,
+                                         int32_t *z0, int32_t *z1, int32_t *g0, int32_t *g1)
+{
+    if (nx < 1 || ny < 1 || nz < 1 || world < 1 || rank < 0 || rank >= world) return IRLS_ERR_INVALID_ARGUMENT;
+    if (8 % world != 0) return IRLS_ERR_INVALID_ARGUMENT;
+    const int64_t N = (int64_t)nx * ny * nz, P = (int64_t)nx * ny;
+    const int32_t K = (int32_t)((N + kChunk - 1) / kChunk);
+    const int a = rank * 8 / world, b = (rank + 1) * 8 / world;
+    const int64_t lo = std::min<int64_t>((int64_t)group_lo(a, K) * kChunk, N);
+    const int64_t hi = std::min<int64_t>((int64_t)group_lo(b, K) * kChunk, N);
+    if (lo % P != 0 || (hi % P != 0 && hi != N)) return IRLS_ERR_INVALID_ARGUMENT;
+    if (world > 1 && hi <= lo) return IRLS_ERR_INVALID_ARGUMENT;
+    if (z0) *z0 = (int32_t)(lo / P);
+    if (z1) *z1 = (int32_t)((hi + P - 1) / P);
+    if (g0) *g0 = a;
+    if (g1) *g1 = b;
+    return IRLS_OK;
+}
+
+static irls_status check_opts(const irls_options *o)
+{
+    if (!o) return IRLS_ERR_INVALID_ARGUMENT;
+    if (!(o->eps > 0.0) || isinf(o->eps) || o->T < 0 || !(o->cg_rtol >= 0.0) || o->cg_max_iter < 0 ||
+        (o->cg_norm != 0 && o->cg_norm != 1) || (o->loop_mode != 0 && o->loop_mode != 1))
+        return IRLS_ERR_INVALID_ARGUMENT;
+    return IRLS_OK;
+}
+
+static int32_t compute_F(double cmax, int64_t cnt)
+{
+    if (cmax == 0.0) return 0;
+    int e;
+    frexp(cmax, &e);
+    int b = 0;
+    while (b < 63 && (((int64_t)1) << b) <= cnt) b++;
+    return 124 - e - b;
+}
+
+// ---------------------------------------------------------------------------
+// argument blocks
+// ---------------------------------------------------------------------------
+static VecArgs vec_args(const irls_ctx *c)
+{
+    VecArgs v;
+    v.n_own = c->n_own;
+    v.chunk0 = c->chunk0;
+    v.x = c->x;
+    v.D = c->D;
+    v.Dinv = c->Dinv;
+    v.r = c->r;
+    v.q = c->q;
+    v.z = c->z;
+    v.p0 = c->p0;
+    v.p1 = c->p1;
+    return v;
+}
+
+static StencilArgs stencil_args(const irls_ctx *c, bool full)
+{
+    StencilArgs s;
+    s.nx = c->nx;
+    s.ny = c->ny;
+    s.nz = c->nz;
+    s.P = c->P;
+    s.lo = full ? 0 : c->lo;
+    s.fd_nx = make_fastdiv((uint32_t)c->nx);
+    s.fd_ny = make_fastdiv((uint32_t)c->ny);
+    s.lo_ghost = full ? 0 : (c->lo_ghost ? 1 : 0);
+    const int64_t off = full ? 0 : c->lo;  // capacity arrays are full-size on every rank
+    s.cx = c->cx + off;
+    s.cy = c->cy + off;
+    s.cz = c->cz + off;
+    s.cs = c->cs + off;
+    s.ct = c->ct + off;
+    s.gx = c->gx;
+    s.gy = c->gy;
+    s.gz = c->gz;
+    return s;
+}
+
+static SellArgs sell_args(const irls_ctx *c)
+{
+    SellArgs s;
+    s.n = c->n_glob;
+    s.slice_ptr = c->slice_ptr;
+    s.col = c->col;
+    s.c = c->cap;
+    s.g = c->gsell;
+    s.cs = c->cs;
+    s.ct = c->ct;
+    return s;
+}
+
+static RedArgs red_args(const irls_ctx *c)
+{
+    RedArgs r;
+    r.part = c->part;
+    r.slots = c->slots_local;
+    r.ctrl = c->ctrl;
+    r.K = c->K;
+    r.g0 = c->g0;
+    r.g1 = c->g1;
+    r.n_fin = c->n_fin;
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// multi-GPU collectives (NCCL over NVLink): halo planes, slot allreduce
+// ---------------------------------------------------------------------------
+static irls_status halo(irls_ctx *c, double *arr, cudaStream_t st)
+{
+    if (c->world == 1) return IRLS_OK;
+    const size_t P = (size_t)c->P;
+    NK(ncclGroupStart());
+    if (c->lo_ghost) {
+        NK(ncclSend(arr, P, ncclDouble, c->rank - 1, c->nccl, st));
+        NK(ncclRecv(arr - P, P, ncclDouble, c->rank - 1, c->nccl, st));
+    }
+    if (c->hi_ghost) {
+        NK(ncclSend(arr + c->n_own - P, P, ncclDouble, c->rank + 1, c->nccl, st));
+        NK(ncclRecv(arr + c->n_own, P, ncclDouble, c->rank + 1, c->nccl, st));
+    }
+    NK(ncclGroupEnd());
+    return IRLS_OK;
+}
+
+static irls_status allreduce_slots(irls_ctx *c, int nq, cudaStream_t st)
+{
+    if (c->world == 1) return IRLS_OK;
+    NK(ncclAllReduce(c->slots_local, c->slots_glob, (size_t)nq * kGroups, ncclDouble, ncclSum, c->nccl, st));
+    return IRLS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// enqueue pieces of one solve
+// ---------------------------------------------------------------------------
+static irls_status enq_assemble(irls_ctx *c, int mode, const CondArgs &cd, cudaStream_t st)
+{
+    const VecArgs v = vec_args(c);
+    const RedArgs ra = red_args(c);
+    if (c->kind == 0) {
+        if (mode != ASM_INIT) {
+            irls_status s = halo(c, c->x, st);
+            if (s) return s;
+        }
+        launch_stencil_assemble_ex(stencil_args(c, false), v, ra, cd, mode, c->opt.eps, c->gs_diag, c->gt_diag, st);
+    } else {
+        launch_sell_assemble_ex(sell_args(c), v, ra, cd, mode, c->opt.eps, c->gs_diag, c->gt_diag, st);
+    }
+    c->launches++;
+    if (c->world > 1) {
+        irls_status s = allreduce_slots(c, 5, st);
+        if (s) return s;
+        launch_finalize(PH_START, c->ctrl, c->slots_glob, cd, st);
+        c->launches++;
+        s = halo(c, c->z, st);
+        if (s) return s;
+    }
+    return last_launch(c, "assemble");
+}
+
+static irls_status enq_body(irls_ctx *c, const CondArgs &cd, cudaStream_t st)
+{
+    const VecArgs v = vec_args(c);
+    const RedArgs ra = red_args(c);
+    if (c->kind == 0) launch_stencil_pspmv(stencil_args(c, false), v, ra, cd, st);
+    else launch_sell_pspmv(sell_args(c), v, ra, cd, st);
+    c->launches++;
+    if (c->world > 1) {
+        launch_ghost_pupdate(v, c->lo_ghost, c->hi_ghost, c->P, c->ctrl, st);
+        irls_status s = allreduce_slots(c, 1, st);
+        if (s) return s;
+        launch_finalize(PH_PQ, c->ctrl, c->slots_glob, cd, st);
+        c->launches += 2;
+    }
+    launch_axpy_jacobi(v, ra, cd, st);
+    c->launches++;
+    if (c->world > 1) {
+        irls_status s = allreduce_slots(c, 3, st);
+        if (s) return s;
+        launch_finalize(PH_RZ, c->ctrl, c->slots_glob, cd, st);
+        c->launches++;
+        s = halo(c, c->z, st);
+        if (s) return s;
+    }
+    return last_launch(c, "cg body");
+}
+
+static irls_status enq_tail(irls_ctx *c, cudaStream_t st)
+{
+    const VecArgs v = vec_args(c);
+    launch_finish(v, c->ctrl, st);
+    launch_report(c->ctrl, c->reports, st);
+    c->launches += 2;
+    if (c->opt.record_trace) {
+        if (c->world > 1) {
+            irls_status s = halo(c, c->x, st);
+            if (s) return s;
+        }
+        const RedArgs ra = red_args(c);
+        if (c->kind == 0)
+            launch_stencil_diag_ex(stencil_args(c, false), v, ra, c->opt.eps, c->opt.cg_norm, c->gs_diag, c->gt_diag, st);
+        else
+            launch_sell_diag_ex(sell_args(c), v, ra, c->opt.eps, c->opt.cg_norm, c->gs_diag, c->gt_diag, st);
+        if (c->world > 1) {
+            irls_status s = allreduce_slots(c, 4, st);
+            if (s) return s;
+        }
+        launch_diag_finalize(c->ctrl, c->slots_glob, c->reports, c->opt.cg_norm, st);
+        c->launches += 2;
+    }
+    return last_launch(c, "tail");
+}
+
+// Per-solve CUDA graph: [x = 0] -> K1 (sets the WHILE condition) -> [x = 0]
+// -> WHILE { K3 ; K5 (sets the condition) } -> finish -> report [-> diag].
+static irls_status build_graph(irls_ctx *c, int mode)
+{
+    cudaStream_t st = c->stream;
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t graph;
+    const cudaGraphNode_t *deps = nullptr;
+    size_t nd = 0;
+    CK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &graph, &deps, &nd));
+    cudaGraphConditionalHandle h;
+    CK(cudaGraphConditionalHandleCreate(&h, graph, 0, 0));
+    CondArgs cd;
+    cd.handle = h;
+    cd.use = 1;
+    cd.finalize = 1;
+    const int64_t lsave = c->launches;
+    if (mode == ASM_INIT) CK(cudaMemsetAsync(c->x, 0, sizeof(double) * c->n_own, st));
+    irls_status s = enq_assemble(c, mode, cd, st);
+    if (s) { cudaGraph_t g; cudaStreamEndCapture(st, &g); if (g) cudaGraphDestroy(g); return s; }
+    if (mode == ASM_REWEIGHT_COLD) CK(cudaMemsetAsync(c->x, 0, sizeof(double) * c->n_own, st));
+    CK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &graph, &deps, &nd));
+    cudaGraphNodeParams p = {cudaGraphNodeTypeConditional};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = h;
+    p.conditional.type = cudaGraphCondTypeWhile;
+    p.conditional.size = 1;
+    cudaGraphNode_t cnode;
+    CK(cudaGraphAddNode(&cnode, graph, deps, nd, &p));
+    cudaGraph_t body = p.conditional.phGraph_out[0];
+    CK(cudaStreamUpdateCaptureDependencies(st, &cnode, 1, cudaStreamSetCaptureDependencies));
+    CK(cudaStreamBeginCaptureToGraph(c->side_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    s = enq_body(c, cd, c->side_stream);
+    cudaGraph_t bodyg;
+    CK(cudaStreamEndCapture(c->side_stream, &bodyg));
+    if (s) { cudaGraph_t g; cudaStreamEndCapture(st, &g); if (g) cudaGraphDestroy(g); return s; }
+    s = enq_tail(c, st);
+    cudaGraph_t full;
+    CK(cudaStreamEndCapture(st, &full));
+    if (s) { cudaGraphDestroy(full); return s; }
+    CK(cudaGraphInstantiate(&c->gexec[mode], full, 0));
+    cudaGraphDestroy(full);
+    c->launches = lsave;
+    return IRLS_OK;
+}
+
+// launches per solve in graph mode: assemble(1) + tail(2 or 4) + 2 per CG iteration
+static int64_t tail_launches(const irls_ctx *c) { return 1 + 2 + (c->opt.record_trace ? 2 : 0); }
+
+static irls_status enqueue_solve(irls_ctx *c, int mode)
+{
+    cudaStream_t st = c->stream;
+    if (c->opt.loop_mode == IRLS_LOOP_GRAPH && c->world == 1) {
+        if (!c->gexec[mode]) {
+            irls_status s = build_graph(c, mode);
+            if (s) return s;
+        }
+        CK(cudaGraphLaunch(c->gexec[mode], st));
+        c->launches += tail_launches(c);
+        return IRLS_OK;
+    }
+    // host loop: one 4-byte readback of the device "done" flag per iteration
+    CondArgs cd;
+    memset(&cd, 0, sizeof(cd));
+    cd.use = 0;
+    cd.finalize = c->world == 1 ? 1 : 0;
+    if (mode == ASM_INIT) CK(cudaMemsetAsync(c->x, 0, sizeof(double) * c->n_own, st));
+    irls_status s = enq_assemble(c, mode, cd, st);
+    if (s) return s;
+    if (mode == ASM_REWEIGHT_COLD) CK(cudaMemsetAsync(c->x, 0, sizeof(double) * c->n_own, st));
+    for (;;) {
+        CK(cudaMemcpyAsync(c->h_done, &c->ctrl->done, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (*c->h_done) break;
+        s = enq_body(c, cd, st);
+        if (s) return s;
+    }
+    return enq_tail(c, st);
+}
+
+static void copy_report(const DevReport &d, irls_step_report *o, float ms)
+{
+    o->cg_iters = d.cg_iters;
+    o->converged = d.converged;
+    o->status = d.status;
+    o->reserved = 0;
+    o->rel_res = d.rel_res;
+    o->true_rel_res = d.true_rel_res;
+    o->S_eps = d.S_eps;
+    o->flow_value = d.flow_value;
+    o->current_s = d.current_s;
+    o->x_min = d.x_min;
+    o->x_max = d.x_max;
+    o->ref = d.ref;
+    o->ms = ms;
+    o->reserved2 = 0.f;
+}
+
+// Run `count` solves (first one with mode0, the rest with mode_rest); fill reports.
+static irls_status run_solves(irls_ctx *c, int mode0, int mode_rest, int count, irls_step_report *reps,
+                              int64_t *total)
+{
+    cudaStream_t st = c->stream;
+    c->launches = 0;
+    CK(cudaMemsetAsync(&c->ctrl->step, 0, sizeof(int32_t), st));
+    std::vector<cudaEvent_t> ev(count + 1);
+    for (auto &e : ev) CK(cudaEventCreate(&e));
+    CK(cudaEventRecord(ev[0], st));
+    irls_status s = IRLS_OK;
+    for (int i = 0; i < count && !s; i++) {
+        s = enqueue_solve(c, i == 0 ? mode0 : mode_rest);
+        if (!s) {
+            cudaError_t e = cudaEventRecord(ev[i + 1], st);
+            if (e != cudaSuccess) s = fail(c, IRLS_ERR_CUDA, cudaGetErrorString(e));
+        }
+    }
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (!s && e != cudaSuccess) s = fail(c, IRLS_ERR_CUDA, std::string("solve: ") + cudaGetErrorString(e));
+    std::vector<DevReport> h(count);
+    if (!s) {
+        e = cudaMemcpy(h.data(), c->reports, sizeof(DevReport) * count, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) s = fail(c, IRLS_ERR_CUDA, cudaGetErrorString(e));
+    }
+    int64_t tot = 0;
+    if (!s) {
+        for (int i = 0; i < count; i++) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+            tot += h[i].cg_iters;
+            if (reps) copy_report(h[i], reps + i, ms);
+            if (h[i].status != 0 && !s) s = fail(c, (irls_status)h[i].status, "CG breakdown (p'Ap <= 0 or non-finite scalar)");
+        }
+        c->launches += 2 * tot;
+    }
+    for (auto &ee : ev) cudaEventDestroy(ee);
+    c->last_cg_iters = tot;
+    if (total) *total = tot;
+    if (!s) c->state = 1;
+    return s;
+}
+
+// ---------------------------------------------------------------------------
+// create
+// ---------------------------------------------------------------------------
+static irls_status common_setup(irls_ctx *c, const irls_comm_desc *comm, const irls_options *opt)
+{
+    c->opt = *opt;
+    c->world = comm ? comm->world_size : 1;
+    c->rank = comm ? comm->rank : 0;
+    c->device = comm ? comm->device : 0;
+    if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return IRLS_ERR_INVALID_ARGUMENT;
+    if (c->world > 1 && (!comm->nccl_unique_id || 8 % c->world != 0)) return IRLS_ERR_INVALID_ARGUMENT;
+    CK(cudaSetDevice(c->device));
+    if (comm && comm->cuda_stream) {
+        c->stream = (cudaStream_t)comm->cuda_stream;
+    } else {
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+    }
+    CK(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
+    CK(cudaMallocHost(&c->h_done, sizeof(int)));
+    return IRLS_OK;
+}
+
+static irls_status alloc_solver(irls_ctx *c, int64_t ghost)
+{
+    const int64_t npad = (int64_t)c->nchunks * kChunk;
+    const int64_t gpad = (ghost + 1) & ~(int64_t)1;  // keep the owned start 16-byte aligned
+    auto ghosted = [&](double *&ptr) -> bool {
+        double *b = dalloc<double>(c, npad + 2 * gpad);
+        if (!b) return false;
+        ptr = b + gpad;
+        return true;
+    };
+    if (!ghosted(c->x) || !ghosted(c->z) || !ghosted(c->p0) || !ghosted(c->p1)) return IRLS_ERR_OOM;
+    c->D = dalloc<double>(c, npad);
+    c->Dinv = dalloc<double>(c, npad);
+    c->r = dalloc<double>(c, npad);
+    c->q = dalloc<double>(c, npad);
+    c->ctrl = dalloc<DevCtrl>(c, 1);
+    c->part = dalloc<double>(c, (int64_t)kMaxQ * std::max<int32_t>(c->K, 1));
+    c->slots_local = dalloc<double>(c, kMaxQ * kGroups);
+    c->slots_glob = c->world > 1 ? dalloc<double>(c, kMaxQ * kGroups) : c->slots_local;
+    c->max_reports = std::max(c->opt.T + 1, 1);
+    c->reports = dalloc<DevReport>(c, c->max_reports);
+    if (!c->D || !c->Dinv || !c->r || !c->q || !c->ctrl || !c->part || !c->slots_local || !c->slots_glob || !c->reports)
+        return IRLS_ERR_OOM;
+    if (c->opt.record_trace) {
+        c->gs_diag = dalloc<double>(c, npad);
+        c->gt_diag = dalloc<double>(c, npad);
+        if (!c->gs_diag || !c->gt_diag) return IRLS_ERR_OOM;
+    }
+    DevCtrl h;
+    memset(&h, 0, sizeof(h));
+    h.rtol = c->opt.cg_rtol;
+    h.max_iter = c->opt.cg_max_iter;
+    h.norm = c->opt.cg_norm;
+    h.done = 1;
+    CK(cudaMemcpy(c->ctrl, &h, sizeof(h), cudaMemcpyHostToDevice));
+    return IRLS_OK;
+}
+
+static irls_status init_nccl(irls_ctx *c, const irls_comm_desc *comm)
+{
+    if (c->world == 1) return IRLS_OK;
+    ncclUniqueId id;
+    memcpy(&id, comm->nccl_unique_id, sizeof(id));
+    NK(ncclCommInitRank(&c->nccl, c->world, id, c->rank));
+    return IRLS_OK;
+}
+
+// Host BFS for Prop. 1 / A8 on a grid (used only when some n-link is zero).
+static bool grid_nonsingular(int32_t nx, int32_t ny, int32_t nz, const double *cx, const double *cy, const double *cz,
+                             const double *cs, const double *ct)
+{
+    const int64_t N = (int64_t)nx * ny * nz, P = (int64_t)nx * ny;
+    std::vector<uint8_t> seen(N, 0);
+    std::vector<int64_t> q;
+    q.reserve(1024);
+    for (int64_t r0 = 0; r0 < N; r0++) {
+        if (seen[r0]) continue;
+        bool anchored = false;
+        q.clear();
+        q.push_back(r0);
+        seen[r0] = 1;
+        for (size_t h = 0; h < q.size(); h++) {
+            const int64_t u = q[h];
+            if (cs[u] > 0.0 || ct[u] > 0.0) anchored = true;
+            const int64_t x = u % nx, y = (u / nx) % ny, z = u / P;
+            const int64_t nb[6] = {z > 0 && cz[u - P] > 0 ? u - P : -1, y > 0 && cy[u - nx] > 0 ? u - nx : -1,
+                                   x > 0 && cx[u - 1] > 0 ? u - 1 : -1, x < nx - 1 && cx[u] > 0 ? u + 1 : -1,
+                                   y < ny - 1 && cy[u] > 0 ? u + nx : -1, z < nz - 1 && cz[u] > 0 ? u + P : -1};
+            for (int k = 0; k < 6; k++)
+                if (nb[k] >= 0 && !seen[nb[k]]) { seen[nb[k]] = 1; q.push_back(nb[k]); }
+        }
+        if (!anchored) return false;
+    }
+    return true;
+}
+
+extern "C" irls_status irls_mincut_create_stencil(irls_ctx **out, const irls_comm_desc *comm, int32_t nx, int32_t ny,
+                                                  int32_t nz, const double *cx, const double *cy, const double *cz,
+                                                  const double *cs, const double *ct, const irls_options *opt)
+{
+    if (!out) return IRLS_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    if (check_opts(opt) || nx < 1 || ny < 1 || nz < 1 || !cx || !cy || !cz || !cs || !ct)
+        return IRLS_ERR_INVALID_ARGUMENT;
+    const int64_t N = (int64_t)nx * ny * nz;
+    if (N >= ((int64_t)1 << 31) - 2 * ((int64_t)nx * ny) - kChunk) return IRLS_ERR_INVALID_ARGUMENT;
+    irls_ctx *c = new irls_ctx();
+    irls_status s = common_setup(c, comm, opt);
+    if (!s) {
+        c->kind = 0;
+        c->nx = nx; c->ny = ny; c->nz = nz;
+        c->P = (int64_t)nx * ny;
+        c->n_glob = N;
+        c->n_total = N + 2;
+        c->s_id = N;
+        c->t_id = N + 1;
+        c->K = (int32_t)((N + kChunk - 1) / kChunk);
+        int32_t g0, g1, z0, z1;
+        s = irls_plan_stencil(nx, ny, nz, c->world, c->rank, &z0, &z1, &g0, &g1);
+        if (!s) {
+            c->g0 = g0; c->g1 = g1; c->z0 = z0; c->z1 = z1;
+            c->lo = (int64_t)z0 * c->P;
+            c->n_own = std::min<int64_t>((int64_t)z1 * c->P, N) - c->lo;
+            c->chunk0 = (int32_t)(c->lo / kChunk);
+            c->nchunks = (int32_t)((c->n_own + kChunk - 1) / kChunk);
+            c->n_fin = count_nonempty(c->K, g0, g1);
+            c->lo_ghost = c->world > 1 && c->rank > 0;
+            c->hi_ghost = c->world > 1 && c->rank < c->world - 1;
+            s = alloc_solver(c, c->world > 1 ? c->P : 0);
+        }
+        if (!s) {
+            // static capacities: full arrays on every rank (rank 0 sweeps the whole graph)
+            c->cx = dalloc<double>(c, N); c->cy = dalloc<double>(c, N); c->cz = dalloc<double>(c, N);
+            c->cs = dalloc<double>(c, N); c->ct = dalloc<double>(c, N);
+            c->gx = dalloc<double>(c, (int64_t)c->nchunks * kChunk);
+            c->gy = dalloc<double>(c, (int64_t)c->nchunks * kChunk);
+            const int64_t gp = c->lo_ghost ? ((c->P + 1) & ~(int64_t)1) : 0;
+            double *gzb = dalloc<double>(c, (int64_t)c->nchunks * kChunk + gp);
+            if (!c->cx || !c->cy || !c->cz || !c->cs || !c->ct || !c->gx || !c->gy || !gzb) s = IRLS_ERR_OOM;
+            else c->gz = gzb + gp;
+        }
+        if (!s) {
+            const size_t b = sizeof(double) * N;
+            cudaMemcpyAsync(c->cx, cx, b, cudaMemcpyHostToDevice, c->stream);
+            cudaMemcpyAsync(c->cy, cy, b, cudaMemcpyHostToDevice, c->stream);
+            cudaMemcpyAsync(c->cz, cz, b, cudaMemcpyHostToDevice, c->stream);
+            cudaMemcpyAsync(c->cs, cs, b, cudaMemcpyHostToDevice, c->stream);
+            cudaMemcpyAsync(c->ct, ct, b, cudaMemcpyHostToDevice, c->stream);
+            unsigned long long vo[5];
+            if (validate_stencil(nx, ny, nz, c->cx, c->cy, c->cz, c->cs, c->ct, vo, c->stream))
+                s = fail(c, IRLS_ERR_CUDA, "validate_stencil");
+            else if (vo[0]) s = IRLS_ERR_BAD_CAPACITY;
+            else {
+                bool ok = vo[1] == 0 ? (vo[2] > 0) : grid_nonsingular(nx, ny, nz, cx, cy, cz, cs, ct);
+                if (!ok) s = IRLS_ERR_SINGULAR;
+                double cmax;
+                memcpy(&cmax, &vo[4], sizeof(double));
+                c->F = compute_F(cmax, (int64_t)vo[3]);
+                c->n_links = 0;
+            }
+        }
+        if (!s) {
+            // |E~| with c > 0 for the GEdge/s metric (host count, once)
+            int64_t nl = 0;
+            for (int64_t u = 0; u < N; u++) {
+                const int64_t x = u % nx, y = (u / nx) % ny, z = u / c->P;
+                nl += (x < nx - 1 && cx[u] > 0) + (y < ny - 1 && cy[u] > 0) + (z < nz - 1 && cz[u] > 0);
+            }
+            c->n_links = nl;
+            s = init_nccl(c, comm);
+        }
+    }
+    if (s) {
+        irls_mincut_destroy(c);
+        return s;
+    }
+    *out = c;
+    return IRLS_OK;
+}
+
+struct Ent {
+    int32_t col;
+    int64_t pos;
+    double w;
+};
+
+extern "C" irls_status irls_mincut_create_csr(irls_ctx **out, const irls_comm_desc *comm, int64_t n,
+                                              const int64_t *row_ptr, const int32_t *col, const double *w, int64_t s_,
+                                              int64_t t_, const irls_options *opt)
+{
+    if (!out) return IRLS_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    if (check_opts(opt) || n < 2 || !row_ptr || !col || !w || s_ < 0 || t_ < 0 || s_ >= n || t_ >= n)
+        return IRLS_ERR_INVALID_ARGUMENT;
+    if (s_ == t_) return IRLS_ERR_SOURCE_EQUALS_SINK;
+    if (comm && comm->world_size != 1) return IRLS_ERR_INVALID_ARGUMENT;  // CSR: single GPU in this version
+    if (n >= ((int64_t)1 << 31)) return IRLS_ERR_INVALID_ARGUMENT;
+    if (row_ptr[0] != 0) return IRLS_ERR_INVALID_ARGUMENT;
+    for (int64_t u = 0; u < n; u++)
+        if (row_ptr[u + 1] < row_ptr[u]) return IRLS_ERR_INVALID_ARGUMENT;
+    const int64_t nnz = row_ptr[n];
+    for (int64_t e = 0; e < nnz; e++) {
+        if (col[e] < 0 || col[e] >= n) return IRLS_ERR_INVALID_ARGUMENT;
+        if (!(w[e] >= 0.0) || isinf(w[e])) return IRLS_ERR_BAD_CAPACITY;
+    }
+    for (int64_t u = 0; u < n; u++)
+        for (int64_t e = row_ptr[u]; e < row_ptr[u + 1]; e++)
+            if (col[e] == u) return IRLS_ERR_INVALID_ARGUMENT;
+    // merge duplicates in CSR order (A7); fast path when rows are strictly ascending
+    std::vector<int64_t> mptr(n + 1, 0);
+    std::vector<int32_t> mcol;
+    std::vector<double> mw;
+    mcol.reserve(nnz);
+    mw.reserve(nnz);
+    std::vector<Ent> tmp;
+    for (int64_t u = 0; u < n; u++) {
+        const int64_t a = row_ptr[u], b = row_ptr[u + 1];
+        bool sorted = true;
+        for (int64_t e = a + 1; e < b; e++)
+            if (col[e] <= col[e - 1]) { sorted = false; break; }
+        mptr[u] = (int64_t)mcol.size();
+        if (sorted) {
+            for (int64_t e = a; e < b; e++) { mcol.push_back(col[e]); mw.push_back(w[e]); }
+        } else {
+            tmp.clear();
+            for (int64_t e = a; e < b; e++) tmp.push_back({col[e], e, w[e]});
+            std::stable_sort(tmp.begin(), tmp.end(), [](const Ent &x, const Ent &y) { return x.col < y.col; });
+            for (size_t i = 0; i < tmp.size(); i++) {
+                if (i > 0 && tmp[i].col == tmp[i - 1].col) mw.back() = mw.back() + tmp[i].w;
+                else { mcol.push_back(tmp[i].col); mw.push_back(tmp[i].w); }
+            }
+        }
+    }
+    mptr[n] = (int64_t)mcol.size();
+    // exact symmetry
+    for (int64_t u = 0; u < n; u++)
+        for (int64_t e = mptr[u]; e < mptr[u + 1]; e++) {
+            const int32_t v = mcol[e];
+            const auto beg = mcol.begin() + mptr[v], end = mcol.begin() + mptr[v + 1];
+            const auto it = std::lower_bound(beg, end, (int32_t)u);
+            if (it == end || *it != u || mw[it - mcol.begin()] != mw[e]) return IRLS_ERR_NOT_SYMMETRIC;
+        }
+    const int64_t nr = n - 2;
+    auto red = [&](int64_t v) { return v - (v > s_) - (v > t_); };
+    std::vector<double> hcs(std::max<int64_t>(nr, 1), 0.0), hct(std::max<int64_t>(nr, 1), 0.0);
+    std::vector<int64_t> orig(std::max<int64_t>(nr, 1), 0);
+    std::vector<int64_t> aptr(nr + 1, 0);
+    std::vector<int32_t> aidx;
+    std::vector<double> ac;
+    double cst = 0.0;
+    for (int64_t e = mptr[s_]; e < mptr[s_ + 1]; e++)
+        if (mcol[e] == t_) cst = mw[e];
+    double cmax = cst;
+    int64_t cnt = cst > 0.0;
+    {
+        int64_t r = 0;
+        for (int64_t u = 0; u < n; u++) {
+            if (u == s_ || u == t_) continue;
+            aptr[r] = (int64_t)aidx.size();
+            orig[r] = u;
+            for (int64_t e = mptr[u]; e < mptr[u + 1]; e++) {
+                const int64_t v = mcol[e];
+                if (v == s_) hcs[r] = mw[e];
+                else if (v == t_) hct[r] = mw[e];
+                else if (mw[e] > 0.0) {
+                    aidx.push_back((int32_t)red(v));
+                    ac.push_back(mw[e]);
+                    if (v > u) { cnt++; cmax = std::max(cmax, mw[e]); }
+                }
+            }
+            if (hcs[r] > 0) { cnt++; cmax = std::max(cmax, hcs[r]); }
+            if (hct[r] > 0) { cnt++; cmax = std::max(cmax, hct[r]); }
+            r++;
+        }
+        aptr[nr] = (int64_t)aidx.size();
+    }
+    // Prop. 1 / A8: every component of G~ touches a positive terminal edge
+    {
+        std::vector<uint8_t> seen(std::max<int64_t>(nr, 1), 0);
+        std::vector<int64_t> q;
+        for (int64_t r0 = 0; r0 < nr; r0++) {
+            if (seen[r0]) continue;
+            bool anchored = false;
+            q.clear();
+            q.push_back(r0);
+            seen[r0] = 1;
+            for (size_t h = 0; h < q.size(); h++) {
+                const int64_t u = q[h];
+                if (hcs[u] > 0.0 || hct[u] > 0.0) anchored = true;
+                for (int64_t e = aptr[u]; e < aptr[u + 1]; e++)
+                    if (!seen[aidx[e]]) { seen[aidx[e]] = 1; q.push_back(aidx[e]); }
+            }
+            if (!anchored) return IRLS_ERR_SINGULAR;
+        }
+    }
+    // SELL-32 (slices of 32 consecutive rows, column-major inside a slice)
+    const int64_t nsl = (nr + 31) / 32;
+    std::vector<int64_t> sptr(nsl + 1, 0);
+    for (int64_t sl = 0; sl < nsl; sl++) {
+        int64_t wmax = 0;
+        for (int64_t r = sl * 32; r < std::min<int64_t>(nr, sl * 32 + 32); r++) wmax = std::max(wmax, aptr[r + 1] - aptr[r]);
+        sptr[sl + 1] = sptr[sl] + 32 * wmax;
+    }
+    const int64_t nent = sptr[nsl];
+    std::vector<int32_t> scol(std::max<int64_t>(nent, 1), -1);
+    std::vector<double> scap(std::max<int64_t>(nent, 1), 0.0);
+    for (int64_t r = 0; r < nr; r++) {
+        const int64_t sl = r >> 5, ln = r & 31;
+        for (int64_t k = 0; k < aptr[r + 1] - aptr[r]; k++) {
+            scol[sptr[sl] + 32 * k + ln] = aidx[aptr[r] + k];
+            scap[sptr[sl] + 32 * k + ln] = ac[aptr[r] + k];
+        }
+    }
+    irls_ctx *c = new irls_ctx();
+    irls_status st = common_setup(c, comm, opt);
+    if (!st) {
+        c->kind = 1;
+        c->n_glob = nr;
+        c->n_total = n;
+        c->s_id = s_;
+        c->t_id = t_;
+        c->c_st = cst;
+        c->K = (int32_t)((nr + kChunk - 1) / kChunk);
+        c->g0 = 0; c->g1 = 8;
+        c->lo = 0;
+        c->n_own = nr;
+        c->chunk0 = 0;
+        c->nchunks = c->K;
+        c->n_fin = count_nonempty(c->K, 0, 8);
+        c->n_links = (int64_t)aidx.size() / 2;
+        c->F = compute_F(cmax, cnt);
+        c->n_entries = nent;
+        st = alloc_solver(c, 0);
+    }
+    if (!st) {
+        const int64_t npad = (int64_t)c->nchunks * kChunk;
+        c->cs = dalloc<double>(c, npad);
+        c->ct = dalloc<double>(c, npad);
+        c->slice_ptr = dalloc<int64_t>(c, nsl + 1);
+        c->col = dalloc<int32_t>(c, nent);
+        c->cap = dalloc<double>(c, nent);
+        c->gsell = dalloc<double>(c, nent);
+        c->orig_dev = dalloc<int64_t>(c, std::max<int64_t>(nr, 1));
+        if (!c->cs || !c->ct || !c->slice_ptr || !c->col || !c->cap || !c->gsell || !c->orig_dev) st = IRLS_ERR_OOM;
+    }
+    if (!st && nr > 0) {
+        cudaMemcpy(c->cs, hcs.data(), sizeof(double) * nr, cudaMemcpyHostToDevice);
+        cudaMemcpy(c->ct, hct.data(), sizeof(double) * nr, cudaMemcpyHostToDevice);
+        cudaMemcpy(c->slice_ptr, sptr.data(), sizeof(int64_t) * (nsl + 1), cudaMemcpyHostToDevice);
+        cudaMemcpy(c->col, scol.data(), sizeof(int32_t) * nent, cudaMemcpyHostToDevice);
+        cudaMemcpy(c->cap, scap.data(), sizeof(double) * nent, cudaMemcpyHostToDevice);
+        cudaMemcpy(c->orig_dev, orig.data(), sizeof(int64_t) * nr, cudaMemcpyHostToDevice);
+        if (cudaDeviceSynchronize() != cudaSuccess) st = fail(c, IRLS_ERR_CUDA, "csr upload");
+    }
+    if (st) {
+        irls_mincut_destroy(c);
+        return st;
+    }
+    *out = c;
+    return IRLS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// solves
+// ---------------------------------------------------------------------------
+extern "C" irls_status irls_init(irls_ctx *c, irls_step_report *rep)
+{
+    GUARD(c);
+    if (c->n_glob == 0) { c->state = 1; return IRLS_OK; }
+    irls_step_report tmp;
+    return run_solves(c, ASM_INIT, ASM_INIT, 1, rep ? rep : &tmp, nullptr);
+}
+
+extern "C" irls_status irls_step(irls_ctx *c, irls_step_report *rep)
+{
+    GUARD(c);
+    if (c->state == 0) return fail(c, IRLS_ERR_STATE, "irls_step before irls_init / irls_set_potentials");
+    if (c->n_glob == 0) return IRLS_OK;
+    const int mode = c->opt.warm_start ? ASM_REWEIGHT_WARM : ASM_REWEIGHT_COLD;
+    irls_step_report tmp;
+    return run_solves(c, mode, mode, 1, rep ? rep : &tmp, nullptr);
+}
+
+extern "C" irls_status irls_solve(irls_ctx *c, int32_t mode, irls_step_report *per_step, int64_t *total)
+{
+    GUARD(c);
+    if (mode != IRLS_FROM_SCRATCH && mode != IRLS_CONTINUE) return IRLS_ERR_INVALID_ARGUMENT;
+    if (mode == IRLS_CONTINUE && c->state == 0) return fail(c, IRLS_ERR_STATE, "IRLS_CONTINUE without potentials");
+    if (c->n_glob == 0) { c->state = 1; if (total) *total = 0; return IRLS_OK; }
+    const int step_mode = c->opt.warm_start ? ASM_REWEIGHT_WARM : ASM_REWEIGHT_COLD;
+    if (mode == IRLS_FROM_SCRATCH) return run_solves(c, ASM_INIT, step_mode, c->opt.T + 1, per_step, total);
+    if (c->opt.T == 0) { if (total) *total = 0; return IRLS_OK; }
+    return run_solves(c, step_mode, step_mode, c->opt.T, per_step, total);
+}
+
+// ---------------------------------------------------------------------------
+// potentials / terminal weights
+// ---------------------------------------------------------------------------
+extern "C" irls_status irls_get_potentials(irls_ctx *c, double *x)
+{
+    GUARD(c);
+    if (c->state == 0) return fail(c, IRLS_ERR_STATE, "no potentials yet");
+    if (c->world > 1) return fail(c, IRLS_ERR_INVALID_ARGUMENT, "get_potentials: multi-GPU gather not supported");
+    if (!x) return IRLS_ERR_INVALID_ARGUMENT;
+    CK(cudaMemcpyAsync(x, c->x, sizeof(double) * c->n_own, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return IRLS_OK;
+}
+
+extern "C" irls_status irls_set_potentials(irls_ctx *c, const double *x)
+{
+    GUARD(c);
+    if (!x) return IRLS_ERR_INVALID_ARGUMENT;
+    CK(cudaMemcpyAsync(c->x, x + c->lo, sizeof(double) * c->n_own, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->state = 1;
+    c->sweep_valid = false;
+    return IRLS_OK;
+}
+
+extern "C" irls_status irls_set_terminal_weights(irls_ctx *c, const double *cs, const double *ct)
+{
+    GUARD(c);
+    if (!cs || !ct) return IRLS_ERR_INVALID_ARGUMENT;
+    const int64_t n = c->n_glob;
+    double cmax = c->c_st;
+    int64_t cnt = c->c_st > 0;
+    for (int64_t u = 0; u < n; u++) {
+        if (!(cs[u] >= 0.0) || isinf(cs[u]) || !(ct[u] >= 0.0) || isinf(ct[u])) return IRLS_ERR_BAD_CAPACITY;
+        if (cs[u] > 0) { cnt++; cmax = std::max(cmax, cs[u]); }
+        if (ct[u] > 0) { cnt++; cmax = std::max(cmax, ct[u]); }
+    }
+    // n-link part of F: recomputed from the device copies
+    if (c->kind == 0) {
+        unsigned long long vo[5];
+        CK(cudaMemcpyAsync(c->cs, cs, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->ct, ct, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+        if (validate_stencil(c->nx, c->ny, c->nz, c->cx, c->cy, c->cz, c->cs, c->ct, vo, c->stream))
+            return fail(c, IRLS_ERR_CUDA, "validate");
+        if (vo[1] != 0 || vo[2] == 0) {
+            // zero n-links present: full check on the host copy
+            std::vector<double> hx(n), hy(n), hz(n);
+            cudaMemcpy(hx.data(), c->cx, sizeof(double) * n, cudaMemcpyDeviceToHost);
+            cudaMemcpy(hy.data(), c->cy, sizeof(double) * n, cudaMemcpyDeviceToHost);
+            cudaMemcpy(hz.data(), c->cz, sizeof(double) * n, cudaMemcpyDeviceToHost);
+            if (!grid_nonsingular(c->nx, c->ny, c->nz, hx.data(), hy.data(), hz.data(), cs, ct))
+                return fail(c, IRLS_ERR_SINGULAR, "terminal weights make L~ singular");
+        }
+        double m;
+        memcpy(&m, &vo[4], sizeof(double));
+        c->F = compute_F(m, (int64_t)vo[3]);
+    } else {
+        std::vector<double> cp(c->n_entries);
+        std::vector<int32_t> cl(c->n_entries);
+        cudaMemcpy(cp.data(), c->cap, sizeof(double) * c->n_entries, cudaMemcpyDeviceToHost);
+        cudaMemcpy(cl.data(), c->col, sizeof(int32_t) * c->n_entries, cudaMemcpyDeviceToHost);
+        // each n-link appears twice (both rows): count once via v > u
+        std::vector<int64_t> sp((c->n_glob + 31) / 32 + 1);
+        cudaMemcpy(sp.data(), c->slice_ptr, sizeof(int64_t) * sp.size(), cudaMemcpyDeviceToHost);
+        for (int64_t sl = 0; sl + 1 < (int64_t)sp.size(); sl++)
+            for (int64_t e = sp[sl]; e < sp[sl + 1]; e++) {
+                const int64_t u = sl * 32 + ((e - sp[sl]) & 31);
+                if (cl[e] > u) { cnt++; cmax = std::max(cmax, cp[e]); }
+            }
+        c->F = compute_F(cmax, cnt);
+        CK(cudaMemcpyAsync(c->cs, cs, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->ct, ct, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    }
+    c->sweep_valid = false;
+    return IRLS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// sweep cut
+// ---------------------------------------------------------------------------
+static irls_status alloc_sweep(irls_ctx *c)
+{
+    if (c->sb.keys) return IRLS_OK;
+    SweepBuffers &b = c->sb;
+    const int64_t n = c->n_glob, nt = sweep_ntiles(n);
+    b.n = n;
+    b.keys = dalloc<unsigned long long>(c, n);
+    b.keys_alt = dalloc<unsigned long long>(c, n);
+    b.vals = dalloc<int32_t>(c, n);
+    b.vals_alt = dalloc<int32_t>(c, n);
+    b.rank = dalloc<int32_t>(c, n);
+    b.tile_hist = dalloc<int32_t>(c, 256 * nt);
+    b.tile_off = dalloc<int32_t>(c, 256 * nt);
+    b.scan_tmp = (int32_t *)dalloc<int64_t>(c, (256 * nt + 4095) / 4096 + 1);
+    b.digit_hist = dalloc<unsigned long long>(c, 8 * 256);
+    b.delta = dalloc<__int128>(c, n + 2);
+    b.tile_sum = dalloc<__int128>(c, nt);
+    b.tile_min = dalloc<__int128>(c, nt);
+    b.tile_argmin = dalloc<int64_t>(c, nt);
+    b.flags = dalloc<int32_t>(c, 4);
+    b.k_out = dalloc<int64_t>(c, 1);
+    b.side = dalloc<uint8_t>(c, c->n_total);
+    c->order_out = dalloc<int32_t>(c, n);
+    if (!b.keys || !b.keys_alt || !b.vals || !b.vals_alt || !b.rank || !b.tile_hist || !b.tile_off || !b.scan_tmp ||
+        !b.digit_hist || !b.delta || !b.tile_sum || !b.tile_min || !b.tile_argmin || !b.flags || !b.k_out || !b.side ||
+        !c->order_out)
+        return fail(c, IRLS_ERR_OOM, "sweep buffers");
+    return IRLS_OK;
+}
+
+extern "C" irls_status irls_sweep_cut(irls_ctx *c, uint8_t *side, int32_t *order, int64_t *k, double *cut_value)
+{
+    GUARD(c);
+    if (c->state == 0) return fail(c, IRLS_ERR_STATE, "sweep before solve");
+    if (c->world > 1) return fail(c, IRLS_ERR_INVALID_ARGUMENT, "multi-GPU sweep: gather not implemented");
+    cudaStream_t st = c->stream;
+    const int64_t n = c->n_glob;
+    irls_status s = alloc_sweep(c);
+    if (s) return s;
+    int launches = 0;
+    SweepBuffers &b = c->sb;
+    CK(cudaMemsetAsync(b.flags, 0, sizeof(int32_t) * 4, st));
+    sweep_keys(c->x, b, st);
+    launches++;
+    int32_t *ord = sweep_sort(b, st, &launches);
+    int32_t hflag = 0;
+    CK(cudaMemcpyAsync(&hflag, b.flags, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (hflag) return fail(c, IRLS_ERR_BAD_POTENTIAL, "NaN in potentials");
+    sweep_rank(ord, b, st);
+    launches++;
+    if (c->kind == 0) sweep_delta_stencil(stencil_args(c, true), n, c->F, b, st);
+    else sweep_delta_sell(sell_args(c), c->F, b, st);
+    launches++;
+    sweep_scan_argmin(b, qfix_host(c->c_st, c->F), st);
+    launches += 4;
+    RedArgs ra;
+    ra.part = c->part;
+    ra.slots = c->slots_local;
+    ra.ctrl = c->ctrl;
+    ra.K = (int32_t)((n + kChunk - 1) / kChunk);
+    ra.g0 = 0;
+    ra.g1 = 8;
+    ra.n_fin = count_nonempty(ra.K, 0, 8);
+    if (c->kind == 0) {
+        sweep_side_cross_stencil(stencil_args(c, true), n, b, ra, st);
+    } else {
+        CK(cudaMemsetAsync(b.side, 0, c->n_total, st));
+        sweep_side_cross_sell(sell_args(c), c->orig_dev, c->n_total, b, ra, st);
+        const uint8_t one = 1;
+        CK(cudaMemcpyAsync(b.side + c->s_id, &one, 1, cudaMemcpyHostToDevice, st));
+    }
+    launches++;
+    irls_status ls = last_launch(c, "sweep");
+    if (ls) return ls;
+    double slots[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int64_t hk = 0;
+    if (n > 0) CK(cudaMemcpyAsync(slots, c->slots_local, sizeof(slots), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&hk, b.k_out, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    if (order && n > 0) {
+        sweep_order_out(ord, c->kind == 1 ? c->orig_dev : nullptr, c->order_out, n, st);
+        launches++;
+        CK(cudaMemcpyAsync(order, c->order_out, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+    }
+    if (side) CK(cudaMemcpyAsync(side, b.side, c->n_total, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (n == 0) hk = 0;
+    c->sweep_k = hk;
+    c->sweep_cut = irls_combine_slots(slots) + c->c_st;
+    c->sweep_valid = true;
+    c->order_dev = ord;
+    c->launches += launches;
+    if (k) *k = hk;
+    if (cut_value) *cut_value = c->sweep_cut;
+    return IRLS_OK;
+}
+
+extern "C" irls_status irls_get_side(irls_ctx *c, uint8_t *side)
+{
+    GUARD(c);
+    if (!c->sweep_valid) return fail(c, IRLS_ERR_STATE, "no sweep result");
+    if (!side) return IRLS_ERR_INVALID_ARGUMENT;
+    CK(cudaMemcpy(side, c->sb.side, c->n_total, cudaMemcpyDeviceToHost));
+    return IRLS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// stats / kernel timing / destroy
+// ---------------------------------------------------------------------------
+extern "C" irls_status irls_get_stats(irls_ctx *c, irls_stats *o)
+{
+    if (!c || !o) return IRLS_ERR_INVALID_ARGUMENT;
+    o->launches = c->launches;
+    o->cg_iters = c->last_cg_iters;
+    o->n_nonterminal = c->n_glob;
+    o->n_links = c->n_links;
+    o->n_local = c->n_own;
+    return IRLS_OK;
+}
+
+extern "C" irls_status irls_time_kernel(irls_ctx *c, int32_t which, int32_t reps, float *mean_ms)
+{
+    GUARD(c);
+    if (!mean_ms || reps < 1 || which < 0 || which > 2) return IRLS_ERR_INVALID_ARGUMENT;
+    if (c->state == 0) return fail(c, IRLS_ERR_STATE, "time_kernel needs a solved state");
+    cudaStream_t st = c->stream;
+    const int64_t npad = (int64_t)c->nchunks * kChunk;
+    // snapshot everything the kernels write
+    double *arrs[] = {c->x, c->q, c->r, c->z, c->p0, c->p1, c->D, c->Dinv};
+    std::vector<double *> save;
+    for (double *a : arrs) {
+        double *b = nullptr;
+        if (cudaMalloc(&b, sizeof(double) * npad) != cudaSuccess) {
+            for (double *s2 : save) cudaFree(s2);
+            return fail(c, IRLS_ERR_OOM, "time_kernel snapshot");
+        }
+        cudaMemcpyAsync(b, a, sizeof(double) * npad, cudaMemcpyDeviceToDevice, st);
+        save.push_back(b);
+    }
+    double *gsave = nullptr;
+    const int64_t gbytes = c->kind == 0 ? 3 * npad : c->n_entries;
+    CK(cudaMalloc(&gsave, sizeof(double) * std::max<int64_t>(gbytes, 1)));
+    if (c->kind == 0) {
+        cudaMemcpyAsync(gsave, c->gx, sizeof(double) * npad, cudaMemcpyDeviceToDevice, st);
+        cudaMemcpyAsync(gsave + npad, c->gy, sizeof(double) * npad, cudaMemcpyDeviceToDevice, st);
+        cudaMemcpyAsync(gsave + 2 * npad, c->gz, sizeof(double) * npad, cudaMemcpyDeviceToDevice, st);
+    } else {
+        cudaMemcpyAsync(gsave, c->gsell, sizeof(double) * c->n_entries, cudaMemcpyDeviceToDevice, st);
+    }
+    DevCtrl hc;
+    CK(cudaMemcpyAsync(&hc, c->ctrl, sizeof(hc), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    DevCtrl tc = hc;
+    tc.k = 1;  // a steady-state iteration (p-update and lazy x update active)
+    if (!(tc.alpha == tc.alpha) || tc.alpha == 0.0) tc.alpha = 0.5;
+    if (!(tc.beta == tc.beta)) tc.beta = 0.5;
+    tc.done = 0;
+    CK(cudaMemcpyAsync(c->ctrl, &tc, sizeof(tc), cudaMemcpyHostToDevice, st));
+    CondArgs cd;
+    memset(&cd, 0, sizeof(cd));
+    const VecArgs v = vec_args(c);
+    const RedArgs ra = red_args(c);
+    const int mode = c->opt.warm_start ? ASM_REWEIGHT_WARM : ASM_REWEIGHT_COLD;
+    auto launch = [&]() {
+        if (which == 0) {
+            if (c->kind == 0) launch_stencil_pspmv(stencil_args(c, false), v, ra, cd, st);
+            else launch_sell_pspmv(sell_args(c), v, ra, cd, st);
+        } else if (which == 1) {
+            launch_axpy_jacobi(v, ra, cd, st);
+        } else {
+            if (c->kind == 0) launch_stencil_assemble(stencil_args(c, false), v, ra, cd, mode, c->opt.eps, st);
+            else launch_sell_assemble(sell_args(c), v, ra, cd, mode, c->opt.eps, st);
+        }
+    };
+    launch();  // warm-up
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, st));
+    for (int i = 0; i < reps; i++) launch();
+    CK(cudaEventRecord(e1, st));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *mean_ms = ms / reps;
+    // restore
+    for (size_t i = 0; i < save.size(); i++)
+        cudaMemcpyAsync(arrs[i], save[i], sizeof(double) * npad, cudaMemcpyDeviceToDevice, st);
+    if (c->kind == 0) {
+        cudaMemcpyAsync(c->gx, gsave, sizeof(double) * npad, cudaMemcpyDeviceToDevice, st);
+        cudaMemcpyAsync(c->gy, gsave + npad, sizeof(double) * npad, cudaMemcpyDeviceToDevice, st);
+        cudaMemcpyAsync(c->gz, gsave + 2 * npad, sizeof(double) * npad, cudaMemcpyDeviceToDevice, st);
+    } else {
+        cudaMemcpyAsync(c->gsell, gsave, sizeof(double) * c->n_entries, cudaMemcpyDeviceToDevice, st);
+    }
+    cudaMemcpyAsync(c->ctrl, &hc, sizeof(hc), cudaMemcpyHostToDevice, st);
+    CK(cudaStreamSynchronize(st));
+    for (double *s2 : save) cudaFree(s2);
+    cudaFree(gsave);
+    return last_launch(c, "time_kernel");
+}
+
+extern "C" void irls_mincut_destroy(irls_ctx *c)
+{
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    for (auto &g : c->gexec)
+        if (g) cudaGraphExecDestroy(g);
+    for (void *p : c->allocs) cudaFree(p);
+    if (c->h_done) cudaFreeHost(c->h_done);
+    if (c->nccl) ncclCommDestroy(c->nccl);
+    if (c->side_stream) cudaStreamDestroy(c->side_stream);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}

@@ -1,0 +1,77 @@
+// ctx.h — host-side context of one rank (internal).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/irls_mincut.h"
+#include "kernels.h"
+
+struct irls_ctx {
+    // ---- configuration
+    int kind = 0;  // 0 stencil, 1 csr
+    irls_options opt{};
+    int world = 1, rank = 0, device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    ncclComm_t nccl = nullptr;
+    std::string err;
+    bool poisoned = false;
+    int state = 0;  // 0 created, 1 potentials valid
+
+    // ---- sizes (reduced ids)
+    int64_t n_glob = 0;  // n~
+    int64_t n_own = 0, lo = 0;
+    int32_t K = 0, chunk0 = 0, nchunks = 0;
+    int32_t g0 = 0, g1 = 8, n_fin = 0;
+    int64_t n_links = 0;
+
+    // ---- stencil geometry
+    int32_t nx = 0, ny = 0, nz = 0, z0 = 0, z1 = 0;
+    int64_t P = 0;
+    bool lo_ghost = false, hi_ghost = false;
+
+    // ---- csr bookkeeping
+    int64_t n_total = 0, s_id = 0, t_id = 0;
+    double c_st = 0.0;
+    int64_t *orig_dev = nullptr;
+
+    // ---- sweep fixed point
+    int32_t F = 0;
+
+    // ---- device arrays
+    std::vector<void *> allocs;
+    double *x = nullptr, *z = nullptr, *p0 = nullptr, *p1 = nullptr;  // ghost arrays (offset)
+    double *D = nullptr, *Dinv = nullptr, *r = nullptr, *q = nullptr;
+    double *cx = nullptr, *cy = nullptr, *cz = nullptr, *cs = nullptr, *ct = nullptr;
+    double *gx = nullptr, *gy = nullptr, *gz = nullptr;
+    double *gs_diag = nullptr, *gt_diag = nullptr;
+    int64_t *slice_ptr = nullptr;
+    int32_t *col = nullptr;
+    double *cap = nullptr, *gsell = nullptr;
+    int64_t n_entries = 0;
+
+    irls::DevCtrl *ctrl = nullptr;
+    double *part = nullptr, *slots_local = nullptr, *slots_glob = nullptr;
+    irls::DevReport *reports = nullptr;
+    int max_reports = 0;
+    int *h_done = nullptr;  // pinned
+
+    // sweep
+    irls::SweepBuffers sb{};
+    int32_t *order_dev = nullptr;  // points into sb.vals / vals_alt after a sweep
+    int32_t *order_out = nullptr;
+    bool sweep_valid = false;
+    int64_t sweep_k = 0;
+    double sweep_cut = 0.0;
+
+    // ---- graphs
+    cudaGraphExec_t gexec[3] = {nullptr, nullptr, nullptr};  // by assemble mode
+    cudaStream_t side_stream = nullptr;
+
+    // ---- stats
+    int64_t launches = 0, last_cg_iters = 0;
+};

@@ -1,0 +1,133 @@
+// kernels.h — argument blocks and launchers of the IRLS kernels (internal).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace irls {
+
+// Which assembly to run (Algorithm 1: step 2 vs step 4).
+enum AssembleMode { ASM_INIT = 0, ASM_REWEIGHT_WARM = 1, ASM_REWEIGHT_COLD = 2 };
+
+// Per-node CG vectors (local indexing; owned nodes are [0, n_own); arrays
+// marked "ghost" also hold one plane below (negative indices) and above).
+struct VecArgs {
+    int64_t n_own;
+    int32_t chunk0;      // global chunk index of local chunk 0
+    double *x;           // ghost
+    double *D, *Dinv, *r, *q;
+    double *z;           // ghost
+    double *p0, *p1;     // ghost (ping-pong: iteration k reads p[k&1], writes p[(k+1)&1])
+};
+
+struct StencilArgs {
+    int32_t nx, ny, nz;
+    int64_t P;           // nx*ny
+    int64_t lo;          // global id of local node 0
+    FastDiv fd_nx, fd_ny;
+    int32_t lo_ghost;    // a rank below owns plane z0-1 (ghost planes valid)
+    const double *cx, *cy, *cz;  // cz: ghost below
+    const double *cs, *ct;
+    double *gx, *gy, *gz;        // gz: ghost below
+};
+
+struct SellArgs {
+    int64_t n;                   // rows
+    const int64_t *slice_ptr;    // [nslices+1] entry offsets (multiples of 32)
+    const int32_t *col;          // -1 = padding (always after the real entries)
+    const double *c;             // capacities
+    double *g;                   // conductances
+    const double *cs, *ct;
+};
+
+struct CondArgs {
+    cudaGraphConditionalHandle handle;
+    int32_t use;                 // 1: set the WHILE condition from device code
+    int32_t finalize;            // 1: world == 1, the last block finalizes the scalars
+};
+
+// assembly (K1 / K2): fills g*, D, Dinv, r, z and START reduction
+void launch_stencil_assemble(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
+                             int mode, double eps, cudaStream_t st);
+void launch_sell_assemble(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
+                          int mode, double eps, cudaStream_t st);
+// _ex: also store the terminal conductances gs/gt (record_trace diagnostics)
+void launch_stencil_assemble_ex(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
+                                int mode, double eps, double *gs_out, double *gt_out, cudaStream_t st);
+void launch_sell_assemble_ex(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
+                             int mode, double eps, double *gs_out, double *gt_out, cudaStream_t st);
+// K3: p = z + beta p_old (fused), lazy x += alpha p_old, q = L~ p, PQ reduction
+void launch_stencil_pspmv(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
+                          cudaStream_t st);
+void launch_sell_pspmv(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
+                       cudaStream_t st);
+// ghost planes of p for the next iteration (multi-GPU stencil)
+void launch_ghost_pupdate(const VecArgs &v, int64_t ghost_lo, int64_t ghost_hi, int64_t plane, DevCtrl *ctrl,
+                          cudaStream_t st);
+// K5: r -= alpha q, z = Dinv r, RZ reduction
+void launch_axpy_jacobi(const VecArgs &v, const RedArgs &ra, const CondArgs &cd, cudaStream_t st);
+// after the loop: x += alpha p_last (or x = 0 if b = 0)
+void launch_finish(const VecArgs &v, DevCtrl *ctrl, cudaStream_t st);
+// scalar finalizers for the multi-GPU path (after the slot allreduce)
+void launch_finalize(int phase, DevCtrl *ctrl, const double *slots, const CondArgs &cd, cudaStream_t st);
+// write the step report from the control block
+struct DevReport {
+    int32_t cg_iters, converged, status, pad;
+    double rel_res, true_rel_res, S_eps, flow_value, current_s, x_min, x_max, ref;
+};
+void launch_report(DevCtrl *ctrl, DevReport *reports, cudaStream_t st);
+// record_trace diagnostics: [S_eps, flow, current_s, true_res^2] + x range
+void launch_stencil_diag_ex(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, double eps, int norm,
+                            const double *gsv, const double *gtv, cudaStream_t st);
+void launch_sell_diag_ex(const SellArgs &s, const VecArgs &v, const RedArgs &ra, double eps, int norm,
+                         const double *gsv, const double *gtv, cudaStream_t st);
+void launch_diag_finalize(DevCtrl *ctrl, const double *slots, DevReport *reports, int norm, cudaStream_t st);
+
+enum { PH_START = 0, PH_PQ = 1, PH_RZ = 2 };
+
+// ---------------------------------------------------------------------------
+// Sweep cut (K8-K12)
+// ---------------------------------------------------------------------------
+struct SweepBuffers {
+    int64_t n;
+    unsigned long long *keys, *keys_alt;
+    int32_t *vals, *vals_alt;
+    int32_t *rank;
+    int32_t *tile_hist;      // [256][ntiles]
+    int32_t *tile_off;       // [256][ntiles]
+    int32_t *scan_tmp;       // scan block totals
+    unsigned long long *digit_hist;  // [8][256] global histograms
+    __int128 *delta;         // [n] in sweep order
+    __int128 *tile_sum;      // [ntiles]
+    __int128 *tile_min;      // [ntiles]
+    int64_t *tile_argmin;    // [ntiles]
+    int32_t *flags;          // [0] NaN seen
+    int64_t *k_out;
+    double *cross;
+    uint8_t *side;           // n_total
+};
+int64_t sweep_ntiles(int64_t n);
+void sweep_keys(const double *x, SweepBuffers &b, cudaStream_t st);
+// returns pointer to the sorted ids buffer (vals or vals_alt)
+int32_t *sweep_sort(SweepBuffers &b, cudaStream_t st, int *launches);
+void sweep_rank(const int32_t *order, SweepBuffers &b, cudaStream_t st);
+void sweep_delta_stencil(const StencilArgs &s, int64_t N, int32_t F, SweepBuffers &b, cudaStream_t st);
+void sweep_delta_sell(const SellArgs &s, int32_t F, SweepBuffers &b, cudaStream_t st);
+void sweep_scan_argmin(SweepBuffers &b, __int128 P0, cudaStream_t st);
+void sweep_side_cross_stencil(const StencilArgs &s, int64_t N, SweepBuffers &b, const RedArgs &ra,
+                              cudaStream_t st);
+void sweep_side_cross_sell(const SellArgs &s, const int64_t *orig, int64_t n_total, SweepBuffers &b,
+                           const RedArgs &ra, cudaStream_t st);
+void sweep_order_out(const int32_t *order, const int64_t *orig, int32_t *out, int64_t n, cudaStream_t st);
+__int128 qfix_host(double c, int32_t F);
+
+}  // namespace irls
+
+namespace irls {
+// validate.cu: out[0..4] = bad, zero interior n-links, nodes with a positive
+// terminal edge, positive capacities, bits of the max capacity
+int validate_stencil(int32_t nx, int32_t ny, int32_t nz, const double *cx, const double *cy, const double *cz,
+                     const double *cs, const double *ct, unsigned long long *out_host, cudaStream_t st);
+}  // namespace irls

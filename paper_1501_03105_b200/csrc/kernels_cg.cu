@@ -1,0 +1,546 @@
+// kernels_cg.cu — assembly, PCG and diagnostic kernels (stencil and SELL-32).
+//
+// One CTA of 256 threads owns one C3 chunk of 4096 consecutive node ids;
+// thread t handles nodes base + 2t + 512j + e (j = 0..7, e = 0,1) in that
+// order, so its running sums are exactly C3 step 2 and the block epilogue
+// (common.cuh) completes steps 3-6.  Per-node arithmetic follows O1-O5 of
+// DESIGN.md §2 operation for operation (no FMA: built with -fmad=false).
+#include "kernels.h"
+
+namespace irls {
+
+// ---------------------------------------------------------------------------
+// helpers
+// ---------------------------------------------------------------------------
+struct Coord {
+    int32_t x, y, z;
+};
+
+__device__ __forceinline__ Coord coord_of(const StencilArgs &s, int64_t ug)
+{
+    Coord c;
+    const uint32_t u = (uint32_t)ug;
+    const uint32_t t1 = fdiv(u, s.fd_nx);
+    c.x = (int32_t)(u - t1 * (uint32_t)s.nx);
+    const uint32_t zz = fdiv(t1, s.fd_ny);
+    c.y = (int32_t)(t1 - zz * (uint32_t)s.ny);
+    c.z = (int32_t)zz;
+    return c;
+}
+
+__device__ __forceinline__ void set_cond(const CondArgs &cd, const DevCtrl *c)
+{
+    if (cd.use) cudaGraphSetConditional(cd.handle, c->done ? 0u : 1u);
+}
+
+#define FOR_CHUNK_NODES(...)                                                     \
+    {                                                                             \
+        const int64_t base__ = (int64_t)blockIdx.x * kChunk;                      \
+        _Pragma("unroll 1") for (int j__ = 0; j__ < 8; j__++)                     \
+        {                                                                         \
+            _Pragma("unroll") for (int e__ = 0; e__ < 2; e__++)                   \
+            {                                                                     \
+                const int64_t u = base__ + 2 * (int64_t)threadIdx.x + 512 * j__ + e__; \
+                if (u < v.n_own) { __VA_ARGS__ }                                         \
+            }                                                                     \
+        }                                                                         \
+    }
+
+// ---------------------------------------------------------------------------
+// K1 / K2: reweight (Eq. 4) + assemble the reduced Laplacian (Eq. 7-8, O1),
+// initial residual r0 = b - L~ x0, z0 = Dinv r0 and the START reductions.
+// ---------------------------------------------------------------------------
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) k_stencil_assemble(StencilArgs s, VecArgs v, RedArgs ra, CondArgs cd,
+                                                               double eps2, double *gs_out, double *gt_out)
+{
+    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    const int64_t P = s.P;
+    FOR_CHUNK_NODES({
+        const Coord c = coord_of(s, s.lo + u);
+        const bool hz = c.z > 0, hy = c.y > 0, hx = c.x > 0;
+        const bool px = c.x < s.nx - 1, py = c.y < s.ny - 1, pz = c.z < s.nz - 1;
+        double xu = 0.0, xmz = 0.0, xmy = 0.0, xmx = 0.0, xpx = 0.0, xpy = 0.0, xpz = 0.0;
+        double gmz = 0.0, gmy = 0.0, gmx = 0.0, gpx = 0.0, gpy = 0.0, gpz = 0.0, gs, gt;
+        if (MODE == ASM_INIT) {  // W^(0) = C: g = c
+            if (hz) gmz = s.cz[u - P];
+            if (hy) gmy = s.cy[u - s.nx];
+            if (hx) gmx = s.cx[u - 1];
+            if (px) gpx = s.cx[u];
+            if (py) gpy = s.cy[u];
+            if (pz) gpz = s.cz[u];
+            gs = s.cs[u];
+            gt = s.ct[u];
+        } else {
+            xu = v.x[u];
+            if (hz) { xmz = v.x[u - P]; gmz = rw_g(s.cz[u - P], xmz - xu, eps2); }
+            if (hy) { xmy = v.x[u - s.nx]; gmy = rw_g(s.cy[u - s.nx], xmy - xu, eps2); }
+            if (hx) { xmx = v.x[u - 1]; gmx = rw_g(s.cx[u - 1], xmx - xu, eps2); }
+            if (px) { xpx = v.x[u + 1]; gpx = rw_g(s.cx[u], xu - xpx, eps2); }
+            if (py) { xpy = v.x[u + s.nx]; gpy = rw_g(s.cy[u], xu - xpy, eps2); }
+            if (pz) { xpz = v.x[u + P]; gpz = rw_g(s.cz[u], xu - xpz, eps2); }
+            gs = rw_g(s.cs[u], 1.0 - xu, eps2);  // A3: x_s = 1
+            gt = rw_g(s.ct[u], xu, eps2);        // A3: x_t = 0
+        }
+        // O1: D = ((sum_asc g) + gs) + gt, ascending = (-z,-y,-x,+x,+y,+z)
+        double a = 0.0;
+        if (hz) a = a + gmz;
+        if (hy) a = a + gmy;
+        if (hx) a = a + gmx;
+        if (px) a = a + gpx;
+        if (py) a = a + gpy;
+        if (pz) a = a + gpz;
+        const double D = (a + gs) + gt;
+        const double Dinv = 1.0 / D;
+        s.gx[u] = gpx;
+        s.gy[u] = gpy;
+        s.gz[u] = gpz;
+        if (s.lo_ghost && u < P) s.gz[u - P] = gmz;  // the -z edge of the first plane
+        v.D[u] = D;
+        v.Dinv[u] = Dinv;
+        if (gs_out) { gs_out[u] = gs; gt_out[u] = gt; }
+        double r;
+        if (MODE == ASM_REWEIGHT_WARM) {  // r0 = b - L~ x^(l-1)  (O2 with p = x)
+            double a2 = 0.0;
+            if (hz) a2 = a2 + gmz * xmz;
+            if (hy) a2 = a2 + gmy * xmy;
+            if (hx) a2 = a2 + gmx * xmx;
+            if (px) a2 = a2 + gpx * xpx;
+            if (py) a2 = a2 + gpy * xpy;
+            if (pz) a2 = a2 + gpz * xpz;
+            r = gs - (D * xu - a2);
+        } else {  // x0 = 0: r0 = b exactly
+            r = gs;
+        }
+        const double zr = r * Dinv;
+        v.r[u] = r;
+        v.z[u] = zr;
+        const double mb = gs * Dinv;
+        acc[0] = acc[0] + r * zr;
+        acc[1] = acc[1] + zr * zr;
+        acc[2] = acc[2] + r * r;
+        acc[3] = acc[3] + mb * mb;
+        acc[4] = acc[4] + gs * gs;
+    })
+    if (c3_chunk_epilogue<5>(acc, v.chunk0 + (int32_t)blockIdx.x, ra) && cd.finalize && threadIdx.x == 0) {
+        finalize_start(ra.ctrl, ra.slots);
+        set_cond(cd, ra.ctrl);
+    }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) k_sell_assemble(SellArgs s, VecArgs v, RedArgs ra, CondArgs cd,
+                                                            double eps2, double *gs_out, double *gt_out)
+{
+    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    FOR_CHUNK_NODES({
+        const int64_t sl = u >> 5;
+        const int64_t e0 = s.slice_ptr[sl] + (u & 31);
+        const int32_t W = (int32_t)((s.slice_ptr[sl + 1] - s.slice_ptr[sl]) >> 5);
+        const double xu = MODE == ASM_INIT ? 0.0 : v.x[u];
+        double a = 0.0, a2 = 0.0;
+        for (int32_t k = 0; k < W; k++) {
+            const int64_t idx = e0 + 32 * (int64_t)k;
+            const int32_t nb = s.col[idx];
+            if (nb < 0) break;
+            const double c = s.c[idx];
+            double g;
+            if (MODE == ASM_INIT) {
+                g = c;
+            } else {
+                const double xv = v.x[nb];
+                g = rw_g(c, xu - xv, eps2);
+                if (MODE == ASM_REWEIGHT_WARM) a2 = a2 + g * xv;
+            }
+            s.g[idx] = g;
+            a = a + g;
+        }
+        const double gs = MODE == ASM_INIT ? s.cs[u] : rw_g(s.cs[u], 1.0 - xu, eps2);
+        const double gt = MODE == ASM_INIT ? s.ct[u] : rw_g(s.ct[u], xu, eps2);
+        const double D = (a + gs) + gt;
+        const double Dinv = 1.0 / D;
+        v.D[u] = D;
+        v.Dinv[u] = Dinv;
+        if (gs_out) { gs_out[u] = gs; gt_out[u] = gt; }
+        const double r = MODE == ASM_REWEIGHT_WARM ? gs - (D * xu - a2) : gs;
+        const double zr = r * Dinv;
+        v.r[u] = r;
+        v.z[u] = zr;
+        const double mb = gs * Dinv;
+        acc[0] = acc[0] + r * zr;
+        acc[1] = acc[1] + zr * zr;
+        acc[2] = acc[2] + r * r;
+        acc[3] = acc[3] + mb * mb;
+        acc[4] = acc[4] + gs * gs;
+    })
+    if (c3_chunk_epilogue<5>(acc, v.chunk0 + (int32_t)blockIdx.x, ra) && cd.finalize && threadIdx.x == 0) {
+        finalize_start(ra.ctrl, ra.slots);
+        set_cond(cd, ra.ctrl);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K3: p = z + beta p_old (p = z at k = 0, O9(i)), recomputed for the node and
+// its neighbours (O9(ii)); lazy x += alpha_{k-1} p_{k-1}; q = L~ p (O2);
+// PQ reduction.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_stencil_pspmv(StencilArgs s, VecArgs v, RedArgs ra, CondArgs cd)
+{
+    const DevCtrl *ctrl = ra.ctrl;
+    const int32_t k = ctrl->k;
+    const bool first = (k == 0);
+    const double beta = ctrl->beta, alpha = ctrl->alpha;
+    const double *__restrict__ pold = (k & 1) ? v.p1 : v.p0;
+    double *__restrict__ pnew = (k & 1) ? v.p0 : v.p1;
+    const double *__restrict__ zv = v.z;
+    const int64_t P = s.P;
+    double acc[1] = {0.0};
+#define PVAL(w) (first ? zv[w] : zv[w] + beta * pold[w])
+    FOR_CHUNK_NODES({
+        const Coord c = coord_of(s, s.lo + u);
+        const double pu = PVAL(u);
+        double a = 0.0;
+        if (c.z > 0) a = a + s.gz[u - P] * PVAL(u - P);
+        if (c.y > 0) a = a + s.gy[u - s.nx] * PVAL(u - s.nx);
+        if (c.x > 0) a = a + s.gx[u - 1] * PVAL(u - 1);
+        if (c.x < s.nx - 1) a = a + s.gx[u] * PVAL(u + 1);
+        if (c.y < s.ny - 1) a = a + s.gy[u] * PVAL(u + s.nx);
+        if (c.z < s.nz - 1) a = a + s.gz[u] * PVAL(u + P);
+        const double qu = v.D[u] * pu - a;
+        pnew[u] = pu;
+        v.q[u] = qu;
+        if (!first) v.x[u] = v.x[u] + alpha * pold[u];
+        acc[0] = acc[0] + pu * qu;
+    })
+#undef PVAL
+    if (c3_chunk_epilogue<1>(acc, v.chunk0 + (int32_t)blockIdx.x, ra) && cd.finalize && threadIdx.x == 0) {
+        finalize_pq(ra.ctrl, ra.slots);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_sell_pspmv(SellArgs s, VecArgs v, RedArgs ra, CondArgs cd)
+{
+    const DevCtrl *ctrl = ra.ctrl;
+    const int32_t k = ctrl->k;
+    const bool first = (k == 0);
+    const double beta = ctrl->beta, alpha = ctrl->alpha;
+    const double *__restrict__ pold = (k & 1) ? v.p1 : v.p0;
+    double *__restrict__ pnew = (k & 1) ? v.p0 : v.p1;
+    const double *__restrict__ zv = v.z;
+    double acc[1] = {0.0};
+#define PVAL(w) (first ? zv[w] : zv[w] + beta * pold[w])
+    FOR_CHUNK_NODES({
+        const int64_t sl = u >> 5;
+        const int64_t e0 = s.slice_ptr[sl] + (u & 31);
+        const int32_t W = (int32_t)((s.slice_ptr[sl + 1] - s.slice_ptr[sl]) >> 5);
+        const double pu = PVAL(u);
+        double a = 0.0;
+        for (int32_t kk = 0; kk < W; kk++) {
+            const int64_t idx = e0 + 32 * (int64_t)kk;
+            const int32_t nb = s.col[idx];
+            if (nb < 0) break;
+            a = a + s.g[idx] * PVAL(nb);
+        }
+        const double qu = v.D[u] * pu - a;
+        pnew[u] = pu;
+        v.q[u] = qu;
+        if (!first) v.x[u] = v.x[u] + alpha * pold[u];
+        acc[0] = acc[0] + pu * qu;
+    })
+#undef PVAL
+    if (c3_chunk_epilogue<1>(acc, v.chunk0 + (int32_t)blockIdx.x, ra) && cd.finalize && threadIdx.x == 0) {
+        finalize_pq(ra.ctrl, ra.slots);
+    }
+}
+
+// Ghost planes of p (multi-GPU): the neighbour rank's boundary plane of p is
+// maintained locally from the exchanged z with the same update.
+__global__ void k_ghost_pupdate(VecArgs v, int64_t ghost_lo, int64_t ghost_hi, int64_t plane, const DevCtrl *ctrl)
+{
+    const int32_t k = ctrl->k;
+    const bool first = (k == 0);
+    const double beta = ctrl->beta;
+    const double *pold = (k & 1) ? v.p1 : v.p0;
+    double *pnew = (k & 1) ? v.p0 : v.p1;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nlo = ghost_lo ? plane : 0, nhi = ghost_hi ? plane : 0;
+    if (i < nlo) {
+        const int64_t w = i - plane;
+        pnew[w] = first ? v.z[w] : v.z[w] + beta * pold[w];
+    } else if (i < nlo + nhi) {
+        const int64_t w = v.n_own + (i - nlo);
+        pnew[w] = first ? v.z[w] : v.z[w] + beta * pold[w];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K5: r = r - alpha q; z = r Dinv (Jacobi, A12); RZ reduction.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_axpy_jacobi(VecArgs v, RedArgs ra, CondArgs cd)
+{
+    DevCtrl *ctrl = ra.ctrl;
+    if (ctrl->done) {  // breakdown flagged after q = A p
+        if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(cd, ctrl);
+        return;
+    }
+    const double alpha = ctrl->alpha;
+    double acc[3] = {0.0, 0.0, 0.0};
+    FOR_CHUNK_NODES({
+        const double r = v.r[u] - alpha * v.q[u];
+        const double zr = r * v.Dinv[u];
+        v.r[u] = r;
+        v.z[u] = zr;
+        acc[0] = acc[0] + r * zr;
+        acc[1] = acc[1] + zr * zr;
+        acc[2] = acc[2] + r * r;
+    })
+    if (c3_chunk_epilogue<3>(acc, v.chunk0 + (int32_t)blockIdx.x, ra) && cd.finalize && threadIdx.x == 0) {
+        finalize_rz(ctrl, ra.slots);
+        set_cond(cd, ctrl);
+    }
+}
+
+// After the loop: the deferred x += alpha_{k-1} p_{k-1}; or v = 0 when b = 0.
+__global__ void __launch_bounds__(kThreads) k_finish(VecArgs v, const DevCtrl *ctrl)
+{
+    const int32_t k = ctrl->k;
+    const bool zero = ctrl->zero_x != 0;
+    if (!zero && (k == 0 || ctrl->status != ST_OK)) return;
+    const double alpha = ctrl->alpha;
+    const double *pl = (k & 1) ? v.p1 : v.p0;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < v.n_own) v.x[i] = zero ? 0.0 : v.x[i] + alpha * pl[i];
+}
+
+__global__ void k_finalize(int phase, DevCtrl *ctrl, const double *slots, CondArgs cd)
+{
+    if (phase == PH_START) finalize_start(ctrl, slots);
+    else if (phase == PH_PQ) finalize_pq(ctrl, slots);
+    else finalize_rz(ctrl, slots);
+    if (phase != PH_PQ) set_cond(cd, ctrl);
+}
+
+__global__ void k_report(DevCtrl *ctrl, DevReport *reports)
+{
+    DevReport &R = reports[ctrl->step];
+    const double ref = ctrl->ref;
+    R.cg_iters = ctrl->k;
+    R.status = ctrl->status;
+    R.ref = ref;
+    R.rel_res = ref > 0.0 ? ctrl->res / ref : 0.0;
+    R.converged = ctrl->status == ST_OK && (ref == 0.0 || ctrl->res <= ctrl->rtol * ref);
+    R.true_rel_res = R.S_eps = R.flow_value = R.current_s = 0.0;
+    R.x_min = R.x_max = 0.0;
+    ctrl->step = ctrl->step + 1;
+    ctrl->xmin_key = ~0ull;
+    ctrl->xmax_key = 0ull;
+}
+
+// ---------------------------------------------------------------------------
+// record_trace diagnostics (O8): [S_eps, flow, current_s, ||res||^2] + range
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void range_update(DevCtrl *ctrl, double mn, double mx)
+{
+    // warp-aggregate then one atomic per warp
+    unsigned long long kmin = dkey_asc(mn), kmax = dkey_asc(mx);
+    for (int off = 16; off >= 1; off >>= 1) {
+        unsigned long long o1 = __shfl_down_sync(0xffffffffu, kmin, off);
+        unsigned long long o2 = __shfl_down_sync(0xffffffffu, kmax, off);
+        kmin = o1 < kmin ? o1 : kmin;
+        kmax = o2 > kmax ? o2 : kmax;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&ctrl->xmin_key, kmin);
+        atomicMax(&ctrl->xmax_key, kmax);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_stencil_diag(StencilArgs s, VecArgs v, RedArgs ra, double eps2,
+                                                           int norm, const double *gsv, const double *gtv)
+{
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    double mn = INFINITY, mx = -INFINITY;
+    const int64_t P = s.P;
+    FOR_CHUNK_NODES({
+        const Coord c = coord_of(s, s.lo + u);
+        const double xu = v.x[u];
+        mn = fmin(mn, xu);
+        mx = fmax(mx, xu);
+        double Se = 0.0, fl = 0.0;
+        // owned edges: +x, +y, +z (ascending), then s-link, t-link
+        const bool px = c.x < s.nx - 1, py = c.y < s.ny - 1, pz = c.z < s.nz - 1;
+        double xpx = 0.0, xpy = 0.0, xpz = 0.0;
+        if (px) { xpx = v.x[u + 1]; const double cc = s.cx[u]; if (cc > 0.0) { const double a = cc * (xu - xpx); Se = Se + sqrt(a * a + eps2); const double d = xu - xpx; fl = fl + s.gx[u] * (d * d); } }
+        if (py) { xpy = v.x[u + s.nx]; const double cc = s.cy[u]; if (cc > 0.0) { const double a = cc * (xu - xpy); Se = Se + sqrt(a * a + eps2); const double d = xu - xpy; fl = fl + s.gy[u] * (d * d); } }
+        if (pz) { xpz = v.x[u + P]; const double cc = s.cz[u]; if (cc > 0.0) { const double a = cc * (xu - xpz); Se = Se + sqrt(a * a + eps2); const double d = xu - xpz; fl = fl + s.gz[u] * (d * d); } }
+        if (s.cs[u] > 0.0) { const double a = s.cs[u] * (1.0 - xu); Se = Se + sqrt(a * a + eps2); }
+        if (s.ct[u] > 0.0) { const double a = s.ct[u] * xu; Se = Se + sqrt(a * a + eps2); }
+        const double ds = 1.0 - xu;
+        fl = fl + gsv[u] * (ds * ds);
+        fl = fl + gtv[u] * (xu * xu);
+        // true residual b - L~ x
+        double a2 = 0.0;
+        if (c.z > 0) a2 = a2 + s.gz[u - P] * v.x[u - P];
+        if (c.y > 0) a2 = a2 + s.gy[u - s.nx] * v.x[u - s.nx];
+        if (c.x > 0) a2 = a2 + s.gx[u - 1] * v.x[u - 1];
+        if (px) a2 = a2 + s.gx[u] * xpx;
+        if (py) a2 = a2 + s.gy[u] * xpy;
+        if (pz) a2 = a2 + s.gz[u] * xpz;
+        const double rr = gsv[u] - (v.D[u] * xu - a2);
+        const double tv = norm == 0 ? rr * v.Dinv[u] : rr;
+        acc[0] = acc[0] + Se;
+        acc[1] = acc[1] + fl;
+        acc[2] = acc[2] + gsv[u] * (1.0 - xu);
+        acc[3] = acc[3] + tv * tv;
+    })
+    range_update(ra.ctrl, mn, mx);
+    c3_chunk_epilogue<4>(acc, v.chunk0 + (int32_t)blockIdx.x, ra);
+}
+
+__global__ void __launch_bounds__(kThreads) k_sell_diag(SellArgs s, VecArgs v, RedArgs ra, double eps2, int norm,
+                                                        const double *gsv, const double *gtv)
+{
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    double mn = INFINITY, mx = -INFINITY;
+    FOR_CHUNK_NODES({
+        const int64_t sl = u >> 5;
+        const int64_t e0 = s.slice_ptr[sl] + (u & 31);
+        const int32_t W = (int32_t)((s.slice_ptr[sl + 1] - s.slice_ptr[sl]) >> 5);
+        const double xu = v.x[u];
+        mn = fmin(mn, xu);
+        mx = fmax(mx, xu);
+        double Se = 0.0, fl = 0.0, a2 = 0.0;
+        for (int32_t k = 0; k < W; k++) {
+            const int64_t idx = e0 + 32 * (int64_t)k;
+            const int32_t nb = s.col[idx];
+            if (nb < 0) break;
+            const double xv = v.x[nb];
+            a2 = a2 + s.g[idx] * xv;
+            if (nb > u) {
+                const double a = s.c[idx] * (xu - xv);
+                Se = Se + sqrt(a * a + eps2);
+                const double d = xu - xv;
+                fl = fl + s.g[idx] * (d * d);
+            }
+        }
+        if (s.cs[u] > 0.0) { const double a = s.cs[u] * (1.0 - xu); Se = Se + sqrt(a * a + eps2); }
+        if (s.ct[u] > 0.0) { const double a = s.ct[u] * xu; Se = Se + sqrt(a * a + eps2); }
+        const double ds = 1.0 - xu;
+        fl = fl + gsv[u] * (ds * ds);
+        fl = fl + gtv[u] * (xu * xu);
+        const double rr = gsv[u] - (v.D[u] * xu - a2);
+        const double tv = norm == 0 ? rr * v.Dinv[u] : rr;
+        acc[0] = acc[0] + Se;
+        acc[1] = acc[1] + fl;
+        acc[2] = acc[2] + gsv[u] * (1.0 - xu);
+        acc[3] = acc[3] + tv * tv;
+    })
+    range_update(ra.ctrl, mn, mx);
+    c3_chunk_epilogue<4>(acc, v.chunk0 + (int32_t)blockIdx.x, ra);
+}
+
+__global__ void k_diag_finalize(DevCtrl *ctrl, const double *slots, DevReport *reports, int norm)
+{
+    DevReport &R = reports[ctrl->step - 1];
+    R.S_eps = slot_total(slots, 0);
+    R.flow_value = slot_total(slots, 1);
+    R.current_s = slot_total(slots, 2);
+    const double tr = sqrt(slot_total(slots, 3));
+    R.true_rel_res = ctrl->ref > 0.0 ? tr / ctrl->ref : 0.0;
+    R.x_min = dkey_inv(ctrl->xmin_key);
+    R.x_max = dkey_inv(ctrl->xmax_key);
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+static inline unsigned nblocks(int64_t n_own) { return (unsigned)((n_own + kChunk - 1) / kChunk); }
+
+void launch_stencil_assemble(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
+                             int mode, double eps, cudaStream_t st)
+{
+    launch_stencil_assemble_ex(s, v, ra, cd, mode, eps, nullptr, nullptr, st);
+}
+
+void launch_stencil_assemble_ex(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
+                                int mode, double eps, double *gs_out, double *gt_out, cudaStream_t st)
+{
+    const double eps2 = eps * eps;
+    const unsigned nb = nblocks(v.n_own);
+    if (mode == ASM_INIT) k_stencil_assemble<ASM_INIT><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
+    else if (mode == ASM_REWEIGHT_WARM)
+        k_stencil_assemble<ASM_REWEIGHT_WARM><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
+    else k_stencil_assemble<ASM_REWEIGHT_COLD><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
+}
+
+void launch_sell_assemble(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, int mode,
+                          double eps, cudaStream_t st)
+{
+    launch_sell_assemble_ex(s, v, ra, cd, mode, eps, nullptr, nullptr, st);
+}
+
+void launch_sell_assemble_ex(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, int mode,
+                             double eps, double *gs_out, double *gt_out, cudaStream_t st)
+{
+    const double eps2 = eps * eps;
+    const unsigned nb = nblocks(v.n_own);
+    if (mode == ASM_INIT) k_sell_assemble<ASM_INIT><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
+    else if (mode == ASM_REWEIGHT_WARM)
+        k_sell_assemble<ASM_REWEIGHT_WARM><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
+    else k_sell_assemble<ASM_REWEIGHT_COLD><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
+}
+
+void launch_stencil_pspmv(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
+                          cudaStream_t st)
+{
+    k_stencil_pspmv<<<nblocks(v.n_own), kThreads, 0, st>>>(s, v, ra, cd);
+}
+
+void launch_sell_pspmv(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, cudaStream_t st)
+{
+    k_sell_pspmv<<<nblocks(v.n_own), kThreads, 0, st>>>(s, v, ra, cd);
+}
+
+void launch_ghost_pupdate(const VecArgs &v, int64_t ghost_lo, int64_t ghost_hi, int64_t plane, DevCtrl *ctrl,
+                          cudaStream_t st)
+{
+    const int64_t n = (ghost_lo ? plane : 0) + (ghost_hi ? plane : 0);
+    if (n == 0) return;
+    k_ghost_pupdate<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(v, ghost_lo, ghost_hi, plane, ctrl);
+}
+
+void launch_axpy_jacobi(const VecArgs &v, const RedArgs &ra, const CondArgs &cd, cudaStream_t st)
+{
+    k_axpy_jacobi<<<nblocks(v.n_own), kThreads, 0, st>>>(v, ra, cd);
+}
+
+void launch_finish(const VecArgs &v, DevCtrl *ctrl, cudaStream_t st)
+{
+    k_finish<<<(unsigned)((v.n_own + 255) / 256), 256, 0, st>>>(v, ctrl);
+}
+
+void launch_finalize(int phase, DevCtrl *ctrl, const double *slots, const CondArgs &cd, cudaStream_t st)
+{
+    k_finalize<<<1, 1, 0, st>>>(phase, ctrl, slots, cd);
+}
+
+void launch_report(DevCtrl *ctrl, DevReport *reports, cudaStream_t st) { k_report<<<1, 1, 0, st>>>(ctrl, reports); }
+
+void launch_stencil_diag_ex(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, double eps, int norm,
+                            const double *gsv, const double *gtv, cudaStream_t st)
+{
+    k_stencil_diag<<<nblocks(v.n_own), kThreads, 0, st>>>(s, v, ra, eps * eps, norm, gsv, gtv);
+}
+
+void launch_sell_diag_ex(const SellArgs &s, const VecArgs &v, const RedArgs &ra, double eps, int norm,
+                         const double *gsv, const double *gtv, cudaStream_t st)
+{
+    k_sell_diag<<<nblocks(v.n_own), kThreads, 0, st>>>(s, v, ra, eps * eps, norm, gsv, gtv);
+}
+
+void launch_diag_finalize(DevCtrl *ctrl, const double *slots, DevReport *reports, int norm, cudaStream_t st)
+{
+    k_diag_finalize<<<1, 1, 0, st>>>(ctrl, slots, reports, norm);
+}
+
+}  // namespace irls

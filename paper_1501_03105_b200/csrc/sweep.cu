@@ -1,0 +1,622 @@
+// sweep.cu — GPU sweep cut ("sorting the nodes according to x^(T)";
+// O7 / A14 / A15 in DESIGN.md §2).
+//
+//   keys      order-preserving 64-bit key of x (descending), ids as values
+//   sort      stable LSD radix sort, 8-bit digits; constant-digit passes skipped
+//   rank      rank[order[i]] = i
+//   delta     delta_v = sum_u (+-Q(c_uv)) + Q(ct_v) - Q(cs_v) in exact 128-bit
+//             fixed point (Q(c) = rint(c 2^F)), written at position rank[v]
+//   scan      P_i = P_0 + delta_0 + ... + delta_{i-1}; exact integer sums, so
+//             any parallel order equals the sequential definition
+//   argmin    first i in 0..n minimising P_i
+//   side/cut  side[v] = rank[v] < k; cut value recomputed by C3 (+ c_st)
+#include <algorithm>
+#include "kernels.h"
+
+namespace irls {
+
+typedef unsigned long long u64;
+typedef __int128 i128;
+
+constexpr int kTile = 4096;  // keys per tile (256 threads x 16)
+
+int64_t sweep_ntiles(int64_t n) { return (n + kTile - 1) / kTile; }
+
+__device__ __forceinline__ i128 qfix(double c, int32_t F)
+{
+    if (c == 0.0) return 0;
+    const double v = rint(scalbn(c, F));
+    const double hi = floor(v * 0x1p-64);
+    const double lo = v - hi * 0x1p64;
+    return ((i128)(long long)hi << 64) + (i128)(u64)lo;
+}
+
+__int128 qfix_host(double c, int32_t F)
+{
+    if (c == 0.0) return 0;
+    const double v = rint(ldexp(c, F));
+    return (__int128)v;
+}
+
+__device__ __forceinline__ i128 shfl_up_i128(i128 v, int off)
+{
+    u64 lo = (u64)v, hi = (u64)(v >> 64);
+    lo = __shfl_up_sync(0xffffffffu, lo, off);
+    hi = __shfl_up_sync(0xffffffffu, hi, off);
+    return ((i128)hi << 64) | (i128)lo;
+}
+__device__ __forceinline__ i128 shfl_down_i128(i128 v, int off)
+{
+    u64 lo = (u64)v, hi = (u64)(v >> 64);
+    lo = __shfl_down_sync(0xffffffffu, lo, off);
+    hi = __shfl_down_sync(0xffffffffu, hi, off);
+    return ((i128)hi << 64) | (i128)lo;
+}
+
+// ---------------------------------------------------------------------------
+// keys
+// ---------------------------------------------------------------------------
+__global__ void k_sweep_keys(const double *x, int64_t n, u64 *keys, int32_t *vals, int32_t *flags)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double xv = x[i];
+    if (isnan(xv)) flags[0] = 1;
+    if (xv == 0.0) xv = 0.0;  // -0.0 -> +0.0
+    keys[i] = ~dkey_asc(xv);  // ascending key order = x descending
+    vals[i] = (int32_t)i;     // ties keep ascending id (stable sort)
+}
+
+// ---------------------------------------------------------------------------
+// radix sort
+// ---------------------------------------------------------------------------
+__global__ void k_hist8(const u64 *keys, int64_t n, u64 *digit_hist)
+{
+    __shared__ unsigned h[8][256];
+    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&h[0][0])[i] = 0u;
+    __syncthreads();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const u64 k = keys[i];
+#pragma unroll
+        for (int d = 0; d < 8; d++) atomicAdd(&h[d][(k >> (8 * d)) & 255u], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) {
+        const unsigned c = (&h[0][0])[i];
+        if (c) atomicAdd(&digit_hist[i], (u64)c);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_tile_hist(const u64 *keys, int64_t n, int shift, int32_t *tile_hist,
+                                                   int64_t ntiles)
+{
+    __shared__ unsigned h[256];
+    h[threadIdx.x] = 0u;
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * kTile;
+#pragma unroll 4
+    for (int r = 0; r < 16; r++) {
+        const int64_t i = base + r * 256 + threadIdx.x;
+        if (i < n) atomicAdd(&h[(keys[i] >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    tile_hist[(int64_t)threadIdx.x * ntiles + blockIdx.x] = (int32_t)h[threadIdx.x];
+}
+
+// Stable scatter: warp w owns keys [base + 512 w, +512) in 16 rounds of 32.
+__global__ void __launch_bounds__(256) k_radix_scatter(const u64 *keys, const int32_t *vals, u64 *okeys,
+                                                       int32_t *ovals, int64_t n, int shift,
+                                                       const int32_t *tile_off, int64_t ntiles)
+{
+    __shared__ int32_t wh[8][256];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < 8 * 256; i += 256) (&wh[0][0])[i] = 0;
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * kTile + w * 512;
+    u64 k[16];
+    int32_t vv[16];
+    int dig[16];
+#pragma unroll
+    for (int r = 0; r < 16; r++) {
+        const int64_t i = base + r * 32 + lane;
+        if (i < n) {
+            k[r] = keys[i];
+            vv[r] = vals[i];
+            dig[r] = (int)((k[r] >> shift) & 255u);
+        } else {
+            k[r] = 0;
+            vv[r] = 0;
+            dig[r] = -1;
+        }
+    }
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int r = 0; r < 16; r++) {
+        const unsigned peers = __match_any_sync(0xffffffffu, dig[r]);
+        if (dig[r] >= 0 && (peers & lt) == 0u) wh[w][dig[r]] += __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    {
+        const int d = threadIdx.x;
+        int32_t run = tile_off[(int64_t)d * ntiles + blockIdx.x];
+#pragma unroll
+        for (int w2 = 0; w2 < 8; w2++) {
+            const int32_t c = wh[w2][d];
+            wh[w2][d] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 16; r++) {
+        const int d = dig[r];
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        int32_t pos = 0;
+        if (d >= 0) pos = wh[w][d] + __popc(peers & lt);
+        __syncwarp();
+        if (d >= 0) {
+            okeys[pos] = k[r];
+            ovals[pos] = vv[r];
+            if ((peers & lt) == 0u) wh[w][d] += __popc(peers);
+        }
+        __syncwarp();
+    }
+}
+
+// Exclusive scan of int32 counts (length m) -> out, via 4096-element blocks.
+__device__ __forceinline__ int64_t block_exscan_i64(int64_t v, int64_t *smem, int64_t &total)
+{
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int64_t inc = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int64_t o = __shfl_up_sync(0xffffffffu, inc, off);
+        if (lane >= off) inc += o;
+    }
+    if (lane == 31) smem[w] = inc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t run = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); i++) {
+            const int64_t c = smem[i];
+            smem[i] = run;
+            run += c;
+        }
+        smem[32] = run;
+    }
+    __syncthreads();
+    const int64_t ex = smem[w] + inc - v;
+    total = smem[32];
+    __syncthreads();
+    return ex;
+}
+
+__global__ void __launch_bounds__(256) k_scan_reduce(const int32_t *in, int64_t m, int64_t *bsum)
+{
+    __shared__ int64_t sm[33];
+    int64_t acc = 0;
+    const int64_t base = (int64_t)blockIdx.x * kTile;
+    for (int r = 0; r < 16; r++) {
+        const int64_t i = base + r * 256 + threadIdx.x;
+        if (i < m) acc += in[i];
+    }
+    int64_t tot;
+    block_exscan_i64(acc, sm, tot);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(256) k_scan_top(int64_t *bsum, int64_t nb)
+{
+    __shared__ int64_t sm[33];
+    int64_t carry = 0;
+    for (int64_t b0 = 0; b0 < nb; b0 += 256) {
+        const int64_t i = b0 + threadIdx.x;
+        const int64_t v = i < nb ? bsum[i] : 0;
+        int64_t tot;
+        const int64_t ex = block_exscan_i64(v, sm, tot);
+        if (i < nb) bsum[i] = carry + ex;
+        carry += tot;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_scan_down(const int32_t *in, int64_t m, const int64_t *bsum,
+                                                   int32_t *out)
+{
+    __shared__ int64_t sm[33];
+    int64_t carry = bsum[blockIdx.x];
+    const int64_t base = (int64_t)blockIdx.x * kTile;
+    for (int r = 0; r < 16; r++) {
+        const int64_t i = base + r * 256 + threadIdx.x;
+        const int64_t v = i < m ? in[i] : 0;
+        int64_t tot;
+        const int64_t ex = block_exscan_i64(v, sm, tot);
+        if (i < m) out[i] = (int32_t)(carry + ex);
+        carry += tot;
+    }
+}
+
+static void exclusive_scan_i32(const int32_t *in, int64_t m, int32_t *out, int64_t *tmp, cudaStream_t st,
+                               int *launches)
+{
+    const int64_t nb = (m + kTile - 1) / kTile;
+    k_scan_reduce<<<(unsigned)nb, 256, 0, st>>>(in, m, tmp);
+    k_scan_top<<<1, 256, 0, st>>>(tmp, nb);
+    k_scan_down<<<(unsigned)nb, 256, 0, st>>>(in, m, tmp, out);
+    *launches += 3;
+}
+
+void sweep_keys(const double *x, SweepBuffers &b, cudaStream_t st)
+{
+    if (b.n == 0) return;
+    k_sweep_keys<<<(unsigned)((b.n + 255) / 256), 256, 0, st>>>(x, b.n, b.keys, b.vals, b.flags);
+}
+
+int32_t *sweep_sort(SweepBuffers &b, cudaStream_t st, int *launches)
+{
+    const int64_t n = b.n;
+    if (n == 0) return b.vals;
+    const int64_t nt = sweep_ntiles(n);
+    cudaMemsetAsync(b.digit_hist, 0, sizeof(u64) * 8 * 256, st);
+    const int nbh = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    k_hist8<<<nbh, 256, 0, st>>>(b.keys, n, b.digit_hist);
+    *launches += 1;
+    u64 h[8 * 256];
+    cudaMemcpyAsync(h, b.digit_hist, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    u64 *ka = b.keys, *kb = b.keys_alt;
+    int32_t *va = b.vals, *vb = b.vals_alt;
+    for (int d = 0; d < 8; d++) {
+        bool trivial = false;
+        for (int i = 0; i < 256; i++)
+            if (h[d * 256 + i] == (u64)n) trivial = true;
+        if (trivial) continue;
+        k_tile_hist<<<(unsigned)nt, 256, 0, st>>>(ka, n, 8 * d, b.tile_hist, nt);
+        exclusive_scan_i32(b.tile_hist, 256 * nt, b.tile_off, (int64_t *)b.scan_tmp, st, launches);
+        k_radix_scatter<<<(unsigned)nt, 256, 0, st>>>(ka, va, kb, vb, n, 8 * d, b.tile_off, nt);
+        *launches += 2;
+        std::swap(ka, kb);
+        std::swap(va, vb);
+    }
+    return va;
+}
+
+__global__ void k_rank(const int32_t *order, int64_t n, int32_t *rank)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) rank[order[i]] = (int32_t)i;
+}
+
+void sweep_rank(const int32_t *order, SweepBuffers &b, cudaStream_t st)
+{
+    if (b.n == 0) return;
+    k_rank<<<(unsigned)((b.n + 255) / 256), 256, 0, st>>>(order, b.n, b.rank);
+}
+
+// ---------------------------------------------------------------------------
+// delta (exact fixed point) + per-tile sums of Q(cs) for P_0
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void tile_sum_i128(i128 v, i128 *out)
+{
+    __shared__ i128 sm[8];
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) v += shfl_down_i128(v, off);
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        i128 s = 0;
+        for (int i = 0; i < 8; i++) s += sm[i];
+        *out = s;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_delta_stencil(StencilArgs s, int64_t N, int32_t F, const int32_t *rank,
+                                                       i128 *delta, i128 *qcs_tile)
+{
+    i128 qcs = 0;
+    const int64_t base = (int64_t)blockIdx.x * kTile;
+    for (int r = 0; r < 16; r++) {
+        const int64_t v = base + r * 256 + threadIdx.x;
+        if (v >= N) break;
+        const uint32_t uv = (uint32_t)v;
+        const uint32_t t1 = fdiv(uv, s.fd_nx);
+        const int32_t x = (int32_t)(uv - t1 * (uint32_t)s.nx);
+        const uint32_t zz = fdiv(t1, s.fd_ny);
+        const int32_t y = (int32_t)(t1 - zz * (uint32_t)s.ny), z = (int32_t)zz;
+        const int32_t rv = rank[v];
+        i128 d = 0;
+#define NB(cond, w, cap) if (cond) { const i128 q = qfix(cap, F); d += rank[w] > rv ? q : -q; }
+        NB(z > 0, v - s.P, s.cz[v - s.P]);
+        NB(y > 0, v - s.nx, s.cy[v - s.nx]);
+        NB(x > 0, v - 1, s.cx[v - 1]);
+        NB(x < s.nx - 1, v + 1, s.cx[v]);
+        NB(y < s.ny - 1, v + s.nx, s.cy[v]);
+        NB(z < s.nz - 1, v + s.P, s.cz[v]);
+#undef NB
+        const i128 qs = qfix(s.cs[v], F);
+        d += qfix(s.ct[v], F);
+        d -= qs;
+        qcs += qs;
+        delta[rv] = d;
+    }
+    tile_sum_i128(qcs, qcs_tile + blockIdx.x);
+}
+
+__global__ void __launch_bounds__(256) k_delta_sell(SellArgs s, int32_t F, const int32_t *rank, i128 *delta,
+                                                    i128 *qcs_tile)
+{
+    i128 qcs = 0;
+    const int64_t base = (int64_t)blockIdx.x * kTile;
+    for (int r = 0; r < 16; r++) {
+        const int64_t v = base + r * 256 + threadIdx.x;
+        if (v >= s.n) break;
+        const int64_t sl = v >> 5;
+        const int64_t e0 = s.slice_ptr[sl] + (v & 31);
+        const int32_t W = (int32_t)((s.slice_ptr[sl + 1] - s.slice_ptr[sl]) >> 5);
+        const int32_t rv = rank[v];
+        i128 d = 0;
+        for (int32_t k = 0; k < W; k++) {
+            const int64_t idx = e0 + 32 * (int64_t)k;
+            const int32_t nb = s.col[idx];
+            if (nb < 0) break;
+            const i128 q = qfix(s.c[idx], F);
+            d += rank[nb] > rv ? q : -q;
+        }
+        const i128 qs = qfix(s.cs[v], F);
+        d += qfix(s.ct[v], F);
+        d -= qs;
+        qcs += qs;
+        delta[rv] = d;
+    }
+    tile_sum_i128(qcs, qcs_tile + blockIdx.x);
+}
+
+void sweep_delta_stencil(const StencilArgs &s, int64_t N, int32_t F, SweepBuffers &b, cudaStream_t st)
+{
+    if (N == 0) return;
+    k_delta_stencil<<<(unsigned)sweep_ntiles(N), 256, 0, st>>>(s, N, F, b.rank, b.delta, b.tile_min);
+}
+
+void sweep_delta_sell(const SellArgs &s, int32_t F, SweepBuffers &b, cudaStream_t st)
+{
+    if (s.n == 0) return;
+    k_delta_sell<<<(unsigned)sweep_ntiles(s.n), 256, 0, st>>>(s, F, b.rank, b.delta, b.tile_min);
+}
+
+// ---------------------------------------------------------------------------
+// scan + argmin
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_delta_tile_sum(const i128 *delta, int64_t n, i128 *tile_sum)
+{
+    i128 acc = 0;
+    const int64_t base = (int64_t)blockIdx.x * kTile;
+    for (int r = 0; r < 16; r++) {
+        const int64_t i = base + r * 256 + threadIdx.x;
+        if (i < n) acc += delta[i];
+    }
+    tile_sum_i128(acc, tile_sum + blockIdx.x);
+}
+
+// One block of 256: P0 = sum(qcs_tile) + Q(c_st); tile_sum -> P0 + exclusive prefix.
+__global__ void __launch_bounds__(256) k_tile_prefix(i128 *tile_sum, const i128 *qcs_tile, int64_t nt, i128 qcst,
+                                                     i128 *p0_out)
+{
+    __shared__ i128 sm[256];
+    const int64_t per = (nt + 255) / 256;
+    const int64_t lo = threadIdx.x * per, hi = lo + per < nt ? lo + per : nt;
+    i128 q = 0, t = 0;
+    for (int64_t i = lo; i < hi; i++) { q += qcs_tile[i]; t += tile_sum[i]; }
+    sm[threadIdx.x] = q;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        i128 p0 = qcst;
+        for (int i = 0; i < 256; i++) p0 += sm[i];
+        *p0_out = p0;
+        sm[0] = p0;
+    }
+    __syncthreads();
+    const i128 p0 = sm[0];
+    __syncthreads();
+    sm[threadIdx.x] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        i128 run = p0;
+        for (int i = 0; i < 256; i++) { const i128 c = sm[i]; sm[i] = run; run += c; }
+    }
+    __syncthreads();
+    i128 run = sm[threadIdx.x];
+    for (int64_t i = lo; i < hi; i++) { const i128 c = tile_sum[i]; tile_sum[i] = run; run += c; }
+}
+
+__device__ __forceinline__ bool lex_less(i128 a, int64_t ia, i128 b, int64_t ib)
+{
+    return a < b || (a == b && ia < ib);
+}
+
+// Per tile: inclusive prefixes P_{i+1} = prefix + delta_0..i, first minimum.
+__global__ void __launch_bounds__(256) k_tile_argmin(const i128 *delta, int64_t n, const i128 *tile_prefix,
+                                                     i128 *tile_min, int64_t *tile_arg)
+{
+    __shared__ i128 wsum[8];
+    __shared__ i128 smin[8];
+    __shared__ int64_t sarg[8];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t base = (int64_t)blockIdx.x * kTile;
+    i128 carry = tile_prefix[blockIdx.x];
+    i128 best = 0;
+    int64_t barg = INT64_MAX;
+    for (int r = 0; r < 16; r++) {
+        const int64_t i = base + r * 256 + threadIdx.x;
+        const i128 v = i < n ? delta[i] : (i128)0;
+        i128 inc = v;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const i128 o = shfl_up_i128(inc, off);
+            if (lane >= off) inc += o;
+        }
+        if (lane == 31) wsum[w] = inc;
+        __syncthreads();
+        i128 wpre = 0, tot = 0;
+        for (int k = 0; k < 8; k++) {
+            if (k < w) wpre += wsum[k];
+            tot += wsum[k];
+        }
+        if (i < n) {
+            const i128 P = carry + wpre + inc;  // P_{i+1}
+            if (lex_less(P, i + 1, best, barg)) { best = P; barg = i + 1; }
+        }
+        carry += tot;
+        __syncthreads();
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        const i128 ob = shfl_down_i128(best, off);
+        const int64_t oa = __shfl_down_sync(0xffffffffu, barg, off);
+        if (lex_less(ob, oa, best, barg)) { best = ob; barg = oa; }
+    }
+    if (lane == 0) { smin[w] = best; sarg[w] = barg; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < 8; k++)
+            if (lex_less(smin[k], sarg[k], best, barg)) { best = smin[k]; barg = sarg[k]; }
+        tile_min[blockIdx.x] = best;
+        tile_arg[blockIdx.x] = barg;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_final_argmin(const i128 *tile_min, const int64_t *tile_arg, int64_t nt,
+                                                      const i128 *p0, int64_t *k_out, i128 *pk_out)
+{
+    __shared__ i128 smin[256];
+    __shared__ int64_t sarg[256];
+    i128 best = *p0;
+    int64_t barg = 0;
+    for (int64_t i = threadIdx.x; i < nt; i += 256)
+        if (lex_less(tile_min[i], tile_arg[i], best, barg)) { best = tile_min[i]; barg = tile_arg[i]; }
+    smin[threadIdx.x] = best;
+    sarg[threadIdx.x] = barg;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < 256; k++)
+            if (lex_less(smin[k], sarg[k], best, barg)) { best = smin[k]; barg = sarg[k]; }
+        *k_out = barg;
+        *pk_out = best;
+    }
+}
+
+void sweep_scan_argmin(SweepBuffers &b, __int128 qcst, cudaStream_t st)
+{
+    const int64_t n = b.n, nt = sweep_ntiles(n);
+    // b.tile_min holds the per-tile sums of Q(cs) from the delta kernel
+    i128 *qcs_tile = b.tile_min;
+    i128 *p0 = b.delta + n;        // two spare slots at the end of delta
+    i128 *pk = b.delta + n + 1;
+    if (nt > 0) k_delta_tile_sum<<<(unsigned)nt, 256, 0, st>>>(b.delta, n, b.tile_sum);
+    k_tile_prefix<<<1, 256, 0, st>>>(b.tile_sum, qcs_tile, nt, qcst, p0);
+    if (nt > 0) k_tile_argmin<<<(unsigned)nt, 256, 0, st>>>(b.delta, n, b.tile_sum, b.tile_min, b.tile_argmin);
+    k_final_argmin<<<1, 256, 0, st>>>(b.tile_min, b.tile_argmin, nt, p0, b.k_out, pk);
+}
+
+// ---------------------------------------------------------------------------
+// side + directly recomputed cut value (O7 step 7), C3 over cross_v
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_side_cross_stencil(StencilArgs s, int64_t N, const int32_t *rank,
+                                                                 const int64_t *kptr, uint8_t *side, RedArgs ra)
+{
+    const int64_t k = *kptr;
+    double acc[1] = {0.0};
+    const int64_t base = (int64_t)blockIdx.x * kChunk;
+    for (int j = 0; j < 8; j++)
+        for (int e = 0; e < 2; e++) {
+            const int64_t v = base + 2 * (int64_t)threadIdx.x + 512 * j + e;
+            if (v >= N) continue;
+            const bool in = rank[v] < k;
+            side[v] = in ? 1 : 0;
+            double cr;
+            if (in) {
+                const uint32_t uv = (uint32_t)v;
+                const uint32_t t1 = fdiv(uv, s.fd_nx);
+                const int32_t x = (int32_t)(uv - t1 * (uint32_t)s.nx);
+                const uint32_t zz = fdiv(t1, s.fd_ny);
+                const int32_t y = (int32_t)(t1 - zz * (uint32_t)s.ny), z = (int32_t)zz;
+                double a = 0.0;
+                if (z > 0 && rank[v - s.P] >= k) a = a + s.cz[v - s.P];
+                if (y > 0 && rank[v - s.nx] >= k) a = a + s.cy[v - s.nx];
+                if (x > 0 && rank[v - 1] >= k) a = a + s.cx[v - 1];
+                if (x < s.nx - 1 && rank[v + 1] >= k) a = a + s.cx[v];
+                if (y < s.ny - 1 && rank[v + s.nx] >= k) a = a + s.cy[v];
+                if (z < s.nz - 1 && rank[v + s.P] >= k) a = a + s.cz[v];
+                cr = a + s.ct[v];
+            } else {
+                cr = s.cs[v];
+            }
+            acc[0] = acc[0] + cr;
+        }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        side[N] = 1;
+        side[N + 1] = 0;
+    }
+    c3_chunk_epilogue<1>(acc, (int32_t)blockIdx.x, ra);
+}
+
+__global__ void __launch_bounds__(kThreads) k_side_cross_sell(SellArgs s, const int32_t *rank, const int64_t *kptr,
+                                                              const int64_t *orig, uint8_t *side, RedArgs ra)
+{
+    const int64_t k = *kptr;
+    double acc[1] = {0.0};
+    const int64_t base = (int64_t)blockIdx.x * kChunk;
+    for (int j = 0; j < 8; j++)
+        for (int e = 0; e < 2; e++) {
+            const int64_t v = base + 2 * (int64_t)threadIdx.x + 512 * j + e;
+            if (v >= s.n) continue;
+            const bool in = rank[v] < k;
+            side[orig[v]] = in ? 1 : 0;
+            double cr;
+            if (in) {
+                const int64_t sl = v >> 5;
+                const int64_t e0 = s.slice_ptr[sl] + (v & 31);
+                const int32_t W = (int32_t)((s.slice_ptr[sl + 1] - s.slice_ptr[sl]) >> 5);
+                double a = 0.0;
+                for (int32_t kk = 0; kk < W; kk++) {
+                    const int64_t idx = e0 + 32 * (int64_t)kk;
+                    const int32_t nb = s.col[idx];
+                    if (nb < 0) break;
+                    if (rank[nb] >= k) a = a + s.c[idx];
+                }
+                cr = a + s.ct[v];
+            } else {
+                cr = s.cs[v];
+            }
+            acc[0] = acc[0] + cr;
+        }
+    c3_chunk_epilogue<1>(acc, (int32_t)blockIdx.x, ra);
+}
+
+void sweep_side_cross_stencil(const StencilArgs &s, int64_t N, SweepBuffers &b, const RedArgs &ra, cudaStream_t st)
+{
+    k_side_cross_stencil<<<(unsigned)((N + kChunk - 1) / kChunk), kThreads, 0, st>>>(s, N, b.rank, b.k_out, b.side,
+                                                                                    ra);
+}
+
+void sweep_side_cross_sell(const SellArgs &s, const int64_t *orig, int64_t n_total, SweepBuffers &b,
+                           const RedArgs &ra, cudaStream_t st)
+{
+    (void)n_total;
+    if (s.n == 0) return;
+    k_side_cross_sell<<<(unsigned)((s.n + kChunk - 1) / kChunk), kThreads, 0, st>>>(s, b.rank, b.k_out, orig,
+                                                                                   b.side, ra);
+}
+
+__global__ void k_order_out(const int32_t *order, const int64_t *orig, int32_t *out, int64_t n)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = orig ? (int32_t)orig[order[i]] : order[i];
+}
+
+void sweep_order_out(const int32_t *order, const int64_t *orig, int32_t *out, int64_t n, cudaStream_t st)
+{
+    if (n == 0) return;
+    k_order_out<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(order, orig, out, n);
+}
+
+}  // namespace irls

@@ -1,0 +1,285 @@
+"""Thin ctypes binding of include/irls_mincut.h (argument marshalling only).
+
+Every function keeps the C name; every step of the hot path runs in
+libirls_mincut.so.  There is no CPU fallback: if the library is missing the
+import of ``lib()`` raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libirls_mincut.so")
+
+IRLS_OK = 0
+STATUS_NAMES = {0: "IRLS_OK", 1: "IRLS_ERR_INVALID_ARGUMENT", 2: "IRLS_ERR_SOURCE_EQUALS_SINK",
+                3: "IRLS_ERR_BAD_CAPACITY", 4: "IRLS_ERR_NOT_SYMMETRIC", 5: "IRLS_ERR_SINGULAR",
+                6: "IRLS_ERR_CG_BREAKDOWN", 7: "IRLS_ERR_BAD_POTENTIAL", 8: "IRLS_ERR_STATE",
+                9: "IRLS_ERR_CUDA", 10: "IRLS_ERR_NCCL", 11: "IRLS_ERR_OOM"}
+IRLS_FROM_SCRATCH, IRLS_CONTINUE = 0, 1
+IRLS_NORM_PRECONDITIONED, IRLS_NORM_UNPRECONDITIONED = 0, 1
+IRLS_LOOP_GRAPH, IRLS_LOOP_HOST = 0, 1
+KERNEL_PSPMV, KERNEL_AXPY, KERNEL_ASSEMBLE = 0, 1, 2
+
+
+class irls_options(C.Structure):
+    _fields_ = [("eps", C.c_double), ("T", C.c_int32), ("cg_rtol", C.c_double), ("cg_max_iter", C.c_int32),
+                ("cg_norm", C.c_int32), ("warm_start", C.c_int32), ("record_trace", C.c_int32),
+                ("loop_mode", C.c_int32)]
+
+
+class irls_comm_desc(C.Structure):
+    _fields_ = [("world_size", C.c_int32), ("rank", C.c_int32), ("device", C.c_int32),
+                ("nccl_unique_id", C.c_void_p), ("cuda_stream", C.c_void_p)]
+
+
+class irls_step_report(C.Structure):
+    _fields_ = [("cg_iters", C.c_int32), ("converged", C.c_int32), ("status", C.c_int32), ("reserved", C.c_int32),
+                ("rel_res", C.c_double), ("true_rel_res", C.c_double), ("S_eps", C.c_double),
+                ("flow_value", C.c_double), ("current_s", C.c_double), ("x_min", C.c_double),
+                ("x_max", C.c_double), ("ref", C.c_double), ("ms", C.c_float), ("reserved2", C.c_float)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_ if not k.startswith("reserved")}
+
+
+class irls_stats(C.Structure):
+    _fields_ = [("launches", C.c_int64), ("cg_iters", C.c_int64), ("n_nonterminal", C.c_int64),
+                ("n_links", C.c_int64), ("n_local", C.c_int64)]
+
+
+_lib = None
+
+# exported symbols of include/irls_mincut.h
+SYMBOLS = ["irls_options_default", "irls_nccl_unique_id", "irls_mincut_create_stencil", "irls_mincut_create_csr",
+           "irls_init", "irls_step", "irls_solve", "irls_sweep_cut", "irls_get_side", "irls_set_terminal_weights",
+           "irls_get_potentials", "irls_set_potentials", "irls_get_stats", "irls_time_kernel",
+           "irls_mincut_destroy", "irls_status_string", "irls_last_error", "irls_plan_stencil",
+           "irls_combine_slots"]
+
+
+def lib():
+    """Load libirls_mincut.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} missing: run paper_1501_03105_b200.build.build() "
+                               "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        P = C.c_void_p
+        L.irls_options_default.argtypes = [C.POINTER(irls_options)]
+        L.irls_nccl_unique_id.argtypes = [C.c_char_p]
+        L.irls_mincut_create_stencil.argtypes = [C.POINTER(P), C.POINTER(irls_comm_desc), C.c_int32, C.c_int32,
+                                                 C.c_int32, P, P, P, P, P, C.POINTER(irls_options)]
+        L.irls_mincut_create_csr.argtypes = [C.POINTER(P), C.POINTER(irls_comm_desc), C.c_int64, P, P, P,
+                                             C.c_int64, C.c_int64, C.POINTER(irls_options)]
+        L.irls_init.argtypes = [P, C.POINTER(irls_step_report)]
+        L.irls_step.argtypes = [P, C.POINTER(irls_step_report)]
+        L.irls_solve.argtypes = [P, C.c_int32, P, C.POINTER(C.c_int64)]
+        L.irls_sweep_cut.argtypes = [P, P, P, C.POINTER(C.c_int64), C.POINTER(C.c_double)]
+        L.irls_get_side.argtypes = [P, P]
+        L.irls_set_terminal_weights.argtypes = [P, P, P]
+        L.irls_get_potentials.argtypes = [P, P]
+        L.irls_set_potentials.argtypes = [P, P]
+        L.irls_get_stats.argtypes = [P, C.POINTER(irls_stats)]
+        L.irls_time_kernel.argtypes = [P, C.c_int32, C.c_int32, C.POINTER(C.c_float)]
+        L.irls_mincut_destroy.argtypes = [P]
+        L.irls_mincut_destroy.restype = None
+        L.irls_status_string.argtypes = [C.c_int]
+        L.irls_status_string.restype = C.c_char_p
+        L.irls_last_error.argtypes = [P]
+        L.irls_last_error.restype = C.c_char_p
+        L.irls_plan_stencil.argtypes = [C.c_int32] * 5 + [C.POINTER(C.c_int32)] * 4
+        L.irls_combine_slots.argtypes = [P]
+        L.irls_combine_slots.restype = C.c_double
+        _lib = L
+    return _lib
+
+
+class IrlsError(RuntimeError):
+    def __init__(self, code, where, detail=""):
+        super().__init__(f"{where}: {STATUS_NAMES.get(code, code)} {detail}")
+        self.code = code
+
+
+def _ptr(a):
+    return a.ctypes.data_as(C.c_void_p) if a is not None else None
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def options(**kw) -> irls_options:
+    o = irls_options()
+    lib().irls_options_default(C.byref(o))
+    for k, v in kw.items():
+        if not hasattr(o, k):
+            raise TypeError(f"unknown option {k}")
+        setattr(o, k, v)
+    return o
+
+
+def comm_desc(world_size=1, rank=0, device=0, unique_id: bytes | None = None, stream=None):
+    d = irls_comm_desc()
+    d.world_size, d.rank, d.device = world_size, rank, device
+    d._uid = C.create_string_buffer(unique_id, 128) if unique_id is not None else None
+    d.nccl_unique_id = C.cast(d._uid, C.c_void_p) if d._uid is not None else None
+    d.cuda_stream = stream
+    return d
+
+
+# ---------------------------------------------------------------------------
+# functions with the C names
+# ---------------------------------------------------------------------------
+
+def irls_nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    rc = lib().irls_nccl_unique_id(buf)
+    if rc:
+        raise IrlsError(rc, "irls_nccl_unique_id")
+    return buf.raw
+
+
+def irls_plan_stencil(nx, ny, nz, world, rank):
+    out = [C.c_int32() for _ in range(4)]
+    rc = lib().irls_plan_stencil(nx, ny, nz, world, rank, *[C.byref(o) for o in out])
+    if rc:
+        raise IrlsError(rc, "irls_plan_stencil")
+    return tuple(o.value for o in out)  # z0, z1, g0, g1
+
+
+def irls_combine_slots(slots) -> float:
+    s = _f64(slots)
+    assert s.shape == (8,)
+    return lib().irls_combine_slots(_ptr(s))
+
+
+class MinCut:
+    """One context (one rank) of the IRLS min-cut library."""
+
+    def __init__(self, h, n, n_total):
+        self.h = h
+        self.n = n
+        self.n_total = n_total
+
+    # -- creation ----------------------------------------------------------
+    @classmethod
+    def irls_mincut_create_stencil(cls, nx, ny, nz, cx, cy, cz, cs, ct, opts: irls_options | None = None,
+                                   comm: irls_comm_desc | None = None):
+        arrs = [_f64(a) for a in (cx, cy, cz, cs, ct)]
+        N = nx * ny * nz
+        if any(a.shape[0] != N for a in arrs):
+            raise ValueError("capacity arrays must have nx*ny*nz entries")
+        opts = opts or options()
+        h = C.c_void_p()
+        rc = lib().irls_mincut_create_stencil(C.byref(h), C.byref(comm) if comm else None, nx, ny, nz,
+                                              *[_ptr(a) for a in arrs], C.byref(opts))
+        if rc:
+            raise IrlsError(rc, "irls_mincut_create_stencil")
+        return cls(h, N, N + 2)
+
+    @classmethod
+    def irls_mincut_create_csr(cls, n, row_ptr, col, w, s, t, opts: irls_options | None = None,
+                               comm: irls_comm_desc | None = None):
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        cl = np.ascontiguousarray(col, dtype=np.int32)
+        ww = _f64(w)
+        opts = opts or options()
+        h = C.c_void_p()
+        rc = lib().irls_mincut_create_csr(C.byref(h), C.byref(comm) if comm else None, n, _ptr(rp), _ptr(cl),
+                                          _ptr(ww), s, t, C.byref(opts))
+        if rc:
+            raise IrlsError(rc, "irls_mincut_create_csr")
+        return cls(h, n - 2, n)
+
+    @classmethod
+    def from_spec(cls, spec, opts=None, comm=None):
+        """Create from a synthetic.generators dict."""
+        if spec["kind"] == "stencil":
+            return cls.irls_mincut_create_stencil(spec["nx"], spec["ny"], spec["nz"], spec["cx"], spec["cy"],
+                                                  spec["cz"], spec["cs"], spec["ct"], opts, comm)
+        return cls.irls_mincut_create_csr(spec["n"], spec["row_ptr"], spec["col"], spec["w"], spec["s"],
+                                          spec["t"], opts, comm)
+
+    def _check(self, rc, where):
+        if rc:
+            detail = lib().irls_last_error(self.h) if self.h else b""
+            raise IrlsError(rc, where, detail.decode(errors="replace") if detail else "")
+
+    # -- solves ------------------------------------------------------------
+    def irls_init(self) -> dict:
+        r = irls_step_report()
+        self._check(lib().irls_init(self.h, C.byref(r)), "irls_init")
+        return r.as_dict()
+
+    def irls_step(self) -> dict:
+        r = irls_step_report()
+        self._check(lib().irls_step(self.h, C.byref(r)), "irls_step")
+        return r.as_dict()
+
+    def irls_solve(self, mode=IRLS_FROM_SCRATCH, T=None, reports=True):
+        nrep = (T + 1 if mode == IRLS_FROM_SCRATCH else T) if T is not None else None
+        buf = (irls_step_report * max(nrep, 1))() if (reports and nrep is not None) else None
+        total = C.c_int64()
+        self._check(lib().irls_solve(self.h, mode, C.cast(buf, C.c_void_p) if buf is not None else None,
+                                     C.byref(total)), "irls_solve")
+        return ([r.as_dict() for r in buf[:nrep]] if buf is not None else None), total.value
+
+    def irls_sweep_cut(self, side=True, order=False):
+        s = np.zeros(self.n_total, dtype=np.uint8) if side else None
+        o = np.zeros(max(self.n, 1), dtype=np.int32) if order else None
+        k = C.c_int64()
+        cut = C.c_double()
+        self._check(lib().irls_sweep_cut(self.h, _ptr(s), _ptr(o), C.byref(k), C.byref(cut)), "irls_sweep_cut")
+        return s, (o[: self.n] if o is not None else None), k.value, cut.value
+
+    def irls_get_side(self):
+        s = np.zeros(self.n_total, dtype=np.uint8)
+        self._check(lib().irls_get_side(self.h, _ptr(s)), "irls_get_side")
+        return s
+
+    def irls_set_terminal_weights(self, cs, ct):
+        a, b = _f64(cs), _f64(ct)
+        self._check(lib().irls_set_terminal_weights(self.h, _ptr(a), _ptr(b)), "irls_set_terminal_weights")
+
+    def irls_get_potentials(self):
+        x = np.zeros(max(self.n, 1))
+        self._check(lib().irls_get_potentials(self.h, _ptr(x)), "irls_get_potentials")
+        return x[: self.n]
+
+    def irls_set_potentials(self, x):
+        a = _f64(x)
+        self._check(lib().irls_set_potentials(self.h, _ptr(a)), "irls_set_potentials")
+
+    def irls_get_stats(self) -> dict:
+        s = irls_stats()
+        self._check(lib().irls_get_stats(self.h, C.byref(s)), "irls_get_stats")
+        return {k: getattr(s, k) for k, _ in s._fields_}
+
+    def irls_time_kernel(self, which, reps=10) -> float:
+        ms = C.c_float()
+        self._check(lib().irls_time_kernel(self.h, which, reps, C.byref(ms)), "irls_time_kernel")
+        return ms.value
+
+    def irls_mincut_destroy(self):
+        if self.h:
+            lib().irls_mincut_destroy(self.h)
+            self.h = None
+
+    close = irls_mincut_destroy
+
+    def __del__(self):
+        try:
+            self.irls_mincut_destroy()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.irls_mincut_destroy()
