@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(256) k_tile_argmin(const i128 *delta, int64_t 
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t base = (int64_t)blockIdx.x * kTile;
     i128 carry = tile_prefix[blockIdx.x];
-    i128 best = 0;
+    i128 best = (i128)(((unsigned __int128)1 << 127) - 1);  // +infinity
     int64_t barg = INT64_MAX;
     for (int r = 0; r < 16; r++) {
         const int64_t i = base + r * 256 + threadIdx.x;
