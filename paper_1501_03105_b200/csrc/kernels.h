@@ -87,6 +87,14 @@ void launch_diag_finalize(DevCtrl *ctrl, const double *slots, DevReport *reports
 
 enum { PH_START = 0, PH_PQ = 1, PH_RZ = 2 };
 
+// stencil_pair.cu (nx even): K1a+K1b, K3, K5, finish with 128-bit pair access
+void launch_pair_assemble(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, int mode,
+                          double eps, double *gs_out, double *gt_out, cudaStream_t st);
+void launch_pair_pspmv(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
+                       cudaStream_t st);
+void launch_pair_axpy(const VecArgs &v, const RedArgs &ra, const CondArgs &cd, cudaStream_t st);
+void launch_pair_finish(const VecArgs &v, DevCtrl *ctrl, cudaStream_t st);
+
 // ---------------------------------------------------------------------------
 // Sweep cut (K8-K12)
 // ---------------------------------------------------------------------------

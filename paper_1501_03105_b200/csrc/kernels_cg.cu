@@ -465,6 +465,7 @@ void launch_stencil_assemble(const StencilArgs &s, const VecArgs &v, const RedAr
 void launch_stencil_assemble_ex(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
                                 int mode, double eps, double *gs_out, double *gt_out, cudaStream_t st)
 {
+    if (s.nx % 2 == 0) return launch_pair_assemble(s, v, ra, cd, mode, eps, gs_out, gt_out, st);
     const double eps2 = eps * eps;
     const unsigned nb = nblocks(v.n_own);
     if (mode == ASM_INIT) k_stencil_assemble<ASM_INIT><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
@@ -493,6 +494,7 @@ void launch_sell_assemble_ex(const SellArgs &s, const VecArgs &v, const RedArgs 
 void launch_stencil_pspmv(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
                           cudaStream_t st)
 {
+    if (s.nx % 2 == 0) return launch_pair_pspmv(s, v, ra, cd, st);
     k_stencil_pspmv<<<nblocks(v.n_own), kThreads, 0, st>>>(s, v, ra, cd);
 }
 
@@ -511,12 +513,12 @@ void launch_ghost_pupdate(const VecArgs &v, int64_t ghost_lo, int64_t ghost_hi, 
 
 void launch_axpy_jacobi(const VecArgs &v, const RedArgs &ra, const CondArgs &cd, cudaStream_t st)
 {
-    k_axpy_jacobi<<<nblocks(v.n_own), kThreads, 0, st>>>(v, ra, cd);
+    launch_pair_axpy(v, ra, cd, st);
 }
 
 void launch_finish(const VecArgs &v, DevCtrl *ctrl, cudaStream_t st)
 {
-    k_finish<<<(unsigned)((v.n_own + 255) / 256), 256, 0, st>>>(v, ctrl);
+    launch_pair_finish(v, ctrl, st);
 }
 
 void launch_finalize(int phase, DevCtrl *ctrl, const double *slots, const CondArgs &cd, cudaStream_t st)

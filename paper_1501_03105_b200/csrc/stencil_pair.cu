@@ -1,0 +1,411 @@
+// stencil_pair.cu — pair-vectorised stencil kernels (nx even).
+//
+// Same C3 mapping as kernels_cg.cu (thread t owns nodes base + 2t + 512j + e),
+// but each thread moves its node pair (u0, u0+1) with 128-bit loads/stores
+// and takes the +-x neighbours from the adjacent lanes by warp shuffle.  With
+// nx even a pair never straddles a row, so both nodes share (y, z).
+//
+// K1 is split in two passes:
+//   K1a  edge pass: the conductance of every owned +x/+y/+z edge (Eq. 4, 8)
+//        -> gx, gy, gz  (3 sqrt+div per node instead of 6 in one pass)
+//   K1b  node pass: terminal conductances, D, Dinv (O1), r0 = b - L~ x0,
+//        z0 = Dinv r0 and the START reductions.
+// Absent neighbours contribute exact +0.0 products, which leaves every sum
+// bitwise unchanged (the accumulators are never -0.0), so these kernels give
+// the same bits as the scalar ones and as the oracle.
+#include <algorithm>
+#include "kernels.h"
+
+namespace irls {
+
+__device__ __forceinline__ double2 ldp(const double *__restrict__ a, int64_t i)
+{
+    return __ldg(reinterpret_cast<const double2 *>(a + i));
+}
+__device__ __forceinline__ double2 ldp_cg(const double *a, int64_t i)
+{
+    return *reinterpret_cast<const double2 *>(a + i);
+}
+__device__ __forceinline__ void stp(double *a, int64_t i, double2 v) { *reinterpret_cast<double2 *>(a + i) = v; }
+
+struct PairCoord {
+    int32_t x0, y, z;
+};
+
+__device__ __forceinline__ PairCoord pair_coord(const StencilArgs &s, int64_t ug0)
+{
+    PairCoord c;
+    const uint32_t u = (uint32_t)ug0;
+    const uint32_t t1 = fdiv(u, s.fd_nx);
+    c.x0 = (int32_t)(u - t1 * (uint32_t)s.nx);
+    const uint32_t zz = fdiv(t1, s.fd_ny);
+    c.y = (int32_t)(t1 - zz * (uint32_t)s.ny);
+    c.z = (int32_t)zz;
+    return c;
+}
+
+__device__ __forceinline__ void set_cond2(const CondArgs &cd, const DevCtrl *c)
+{
+    if (cd.use) cudaGraphSetConditional(cd.handle, c->done ? 0u : 1u);
+}
+
+// ---------------------------------------------------------------------------
+// K1a: owned edge conductances
+// ---------------------------------------------------------------------------
+template <bool INIT>
+__global__ void __launch_bounds__(kThreads) k_pair_edges(StencilArgs s, VecArgs v, double eps2)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t base = (int64_t)blockIdx.x * kChunk;
+    const int64_t P = s.P;
+    const double2 zero2 = make_double2(0.0, 0.0);
+#pragma unroll 1
+    for (int j = 0; j < 8; j++) {
+        const int64_t u0 = base + 2 * (int64_t)threadIdx.x + 512 * j;
+        const bool valid = u0 < v.n_own;
+        const PairCoord c = pair_coord(s, s.lo + u0);
+        const bool hasr = c.x0 + 1 < s.nx - 1;  // node u0+1 has a +x edge
+        const bool py = valid && c.y < s.ny - 1, pz = valid && c.z < s.nz - 1;
+        const bool gh = valid && s.lo_ghost && u0 < P;
+        // ---- loads first
+        const double2 x2 = INIT ? zero2 : ldp(v.x, u0);
+        const double2 cx2 = valid ? ldp(s.cx, u0) : zero2;
+        const double2 cy2 = py ? ldp(s.cy, u0) : zero2;
+        const double2 cz2 = pz ? ldp(s.cz, u0) : zero2;
+        const double2 xpy = (!INIT && py) ? ldp(v.x, u0 + s.nx) : zero2;
+        const double2 xpz = (!INIT && pz) ? ldp(v.x, u0 + P) : zero2;
+        const double2 czm = gh ? ldp(s.cz, u0 - P) : zero2;
+        const double2 xmz = (!INIT && gh) ? ldp(v.x, u0 - P) : zero2;
+        double xe = 0.0;
+        if (!INIT && valid && lane == 31 && hasr) xe = __ldg(v.x + u0 + 2);
+        double xr = __shfl_down_sync(0xffffffffu, x2.x, 1);
+        if (!valid) continue;
+        if (lane == 31) xr = xe;
+        double2 gx2, gy2, gz2;
+        if (INIT) {
+            gx2 = make_double2(cx2.x, hasr ? cx2.y : 0.0);
+            gy2 = cy2;
+            gz2 = cz2;
+        } else {
+            gx2.x = rw_g(cx2.x, x2.x - x2.y, eps2);
+            gx2.y = hasr ? rw_g(cx2.y, x2.y - xr, eps2) : 0.0;
+            gy2 = py ? make_double2(rw_g(cy2.x, x2.x - xpy.x, eps2), rw_g(cy2.y, x2.y - xpy.y, eps2)) : zero2;
+            gz2 = pz ? make_double2(rw_g(cz2.x, x2.x - xpz.x, eps2), rw_g(cz2.y, x2.y - xpz.y, eps2)) : zero2;
+        }
+        stp(s.gx, u0, gx2);
+        stp(s.gy, u0, gy2);
+        stp(s.gz, u0, gz2);
+        if (gh)  // the -z edge of the first owned plane (ghost slot)
+            stp(s.gz, u0 - P, INIT ? czm
+                                   : make_double2(rw_g(czm.x, xmz.x - x2.x, eps2), rw_g(czm.y, xmz.y - x2.y, eps2)));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K1b: terminals, D, Dinv, r0, z0, START reductions
+// ---------------------------------------------------------------------------
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) k_pair_nodes(StencilArgs s, VecArgs v, RedArgs ra, CondArgs cd,
+                                                         double eps2, double *gs_out, double *gt_out)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t base = (int64_t)blockIdx.x * kChunk;
+    const int64_t P = s.P;
+    const double2 zero2 = make_double2(0.0, 0.0);
+    constexpr bool WARM = MODE == ASM_REWEIGHT_WARM;
+    constexpr bool HASX = MODE != ASM_INIT;
+    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll 1
+    for (int j = 0; j < 8; j++) {
+        const int64_t u0 = base + 2 * (int64_t)threadIdx.x + 512 * j;
+        const bool valid = u0 < v.n_own;
+        const PairCoord c = pair_coord(s, s.lo + u0);
+        const bool hx = c.x0 > 0, hr = c.x0 + 1 < s.nx - 1;
+        const bool hy = valid && c.y > 0, py = valid && c.y < s.ny - 1;
+        const bool hz = valid && c.z > 0, pz = valid && c.z < s.nz - 1;
+        // ---- loads first
+        const double2 gx2 = ldp(s.gx, u0);
+        const double2 x2 = HASX ? ldp(v.x, u0) : zero2;
+        const double2 gy2 = valid ? ldp(s.gy, u0) : zero2, gz2 = valid ? ldp(s.gz, u0) : zero2;
+        const double2 gym = hy ? ldp(s.gy, u0 - s.nx) : zero2;
+        const double2 gzm = hz ? ldp(s.gz, u0 - P) : zero2;
+        const double2 cs2 = valid ? ldp(s.cs, u0) : zero2, ct2 = valid ? ldp(s.ct, u0) : zero2;
+        const double2 xmz = (WARM && hz) ? ldp(v.x, u0 - P) : zero2;
+        const double2 xmy = (WARM && hy) ? ldp(v.x, u0 - s.nx) : zero2;
+        const double2 xpy = (WARM && py) ? ldp(v.x, u0 + s.nx) : zero2;
+        const double2 xpz = (WARM && pz) ? ldp(v.x, u0 + P) : zero2;
+        double gxe = 0.0, xle = 0.0, xre = 0.0;
+        if (valid && lane == 0 && hx) {
+            gxe = __ldg(s.gx + u0 - 1);
+            if (WARM) xle = __ldg(v.x + u0 - 1);
+        }
+        if (WARM && valid && lane == 31 && hr) xre = __ldg(v.x + u0 + 2);
+        double gxl = __shfl_up_sync(0xffffffffu, gx2.y, 1);
+        double xl = __shfl_up_sync(0xffffffffu, x2.y, 1);
+        double xr = __shfl_down_sync(0xffffffffu, x2.x, 1);
+        if (!valid) continue;
+        if (lane == 0) { gxl = gxe; xl = xle; }
+        if (lane == 31) xr = xre;
+        if (!hx) { gxl = 0.0; xl = 0.0; }
+        if (!hr) xr = 0.0;
+        double2 gs2, gt2;
+        if (MODE == ASM_INIT) {
+            gs2 = cs2;
+            gt2 = ct2;
+        } else {
+            gs2 = make_double2(rw_g(cs2.x, 1.0 - x2.x, eps2), rw_g(cs2.y, 1.0 - x2.y, eps2));
+            gt2 = make_double2(rw_g(ct2.x, x2.x, eps2), rw_g(ct2.y, x2.y, eps2));
+        }
+        // O1, ascending (-z, -y, -x, +x, +y, +z); absent terms are +0.0
+        const double D0 = ((((((0.0 + gzm.x) + gym.x) + gxl) + gx2.x) + gy2.x) + gz2.x + gs2.x) + gt2.x;
+        const double D1 = ((((((0.0 + gzm.y) + gym.y) + gx2.x) + gx2.y) + gy2.y) + gz2.y + gs2.y) + gt2.y;
+        const double Di0 = 1.0 / D0, Di1 = 1.0 / D1;
+        double r0, r1;
+        if (WARM) {
+            double a = 0.0;
+            a = a + gzm.x * xmz.x;
+            a = a + gym.x * xmy.x;
+            a = a + gxl * xl;
+            a = a + gx2.x * x2.y;
+            a = a + gy2.x * xpy.x;
+            a = a + gz2.x * xpz.x;
+            r0 = gs2.x - (D0 * x2.x - a);
+            double b = 0.0;
+            b = b + gzm.y * xmz.y;
+            b = b + gym.y * xmy.y;
+            b = b + gx2.x * x2.x;
+            b = b + gx2.y * xr;
+            b = b + gy2.y * xpy.y;
+            b = b + gz2.y * xpz.y;
+            r1 = gs2.y - (D1 * x2.y - b);
+        } else {
+            r0 = gs2.x;
+            r1 = gs2.y;
+        }
+        const double z0 = r0 * Di0, z1 = r1 * Di1;
+        stp(v.D, u0, make_double2(D0, D1));
+        stp(v.Dinv, u0, make_double2(Di0, Di1));
+        stp(v.r, u0, make_double2(r0, r1));
+        stp(v.z, u0, make_double2(z0, z1));
+        if (gs_out) {
+            stp(gs_out, u0, gs2);
+            stp(gt_out, u0, gt2);
+        }
+        const double mb0 = gs2.x * Di0, mb1 = gs2.y * Di1;
+        acc[0] = acc[0] + r0 * z0;
+        acc[1] = acc[1] + z0 * z0;
+        acc[2] = acc[2] + r0 * r0;
+        acc[3] = acc[3] + mb0 * mb0;
+        acc[4] = acc[4] + gs2.x * gs2.x;
+        acc[0] = acc[0] + r1 * z1;
+        acc[1] = acc[1] + z1 * z1;
+        acc[2] = acc[2] + r1 * r1;
+        acc[3] = acc[3] + mb1 * mb1;
+        acc[4] = acc[4] + gs2.y * gs2.y;
+    }
+    if (c3_chunk_epilogue<5>(acc, v.chunk0 + (int32_t)blockIdx.x, ra) && cd.finalize && threadIdx.x == 0) {
+        finalize_start(ra.ctrl, ra.slots);
+        set_cond2(cd, ra.ctrl);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K3: p = z + beta p_old (recomputed for neighbours), lazy x update, q = L~ p
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_pair_pspmv(StencilArgs s, VecArgs v, RedArgs ra, CondArgs cd)
+{
+    const DevCtrl *ctrl = ra.ctrl;
+    const int32_t k = ctrl->k;
+    const bool first = (k == 0);
+    const double beta = ctrl->beta, alpha = ctrl->alpha;
+    const double *__restrict__ pold = (k & 1) ? v.p1 : v.p0;
+    double *__restrict__ pnew = (k & 1) ? v.p0 : v.p1;
+    const double *__restrict__ zv = v.z;
+    const int lane = threadIdx.x & 31;
+    const int64_t base = (int64_t)blockIdx.x * kChunk;
+    const int64_t P = s.P;
+    const double2 zero2 = make_double2(0.0, 0.0);
+    double acc[1] = {0.0};
+#pragma unroll 1
+    for (int j = 0; j < 8; j++) {
+        const int64_t u0 = base + 2 * (int64_t)threadIdx.x + 512 * j;
+        const bool valid = u0 < v.n_own;
+        const PairCoord c = pair_coord(s, s.lo + u0);
+        const bool hx = c.x0 > 0, hr = c.x0 + 1 < s.nx - 1;
+        const bool hy = valid && c.y > 0, py = valid && c.y < s.ny - 1;
+        const bool hz = valid && c.z > 0, pz = valid && c.z < s.nz - 1;
+        // ---- issue every load of this pair first (memory-level parallelism)
+        const double2 z2 = ldp(zv, u0);
+        const double2 zmz = hz ? ldp(zv, u0 - P) : zero2;
+        const double2 zmy = hy ? ldp(zv, u0 - s.nx) : zero2;
+        const double2 zpy = py ? ldp(zv, u0 + s.nx) : zero2;
+        const double2 zpz = pz ? ldp(zv, u0 + P) : zero2;
+        double2 po = zero2, pmz = zero2, pmy = zero2, ppy = zero2, ppz = zero2;
+        if (!first) {
+            po = ldp(pold, u0);
+            if (hz) pmz = ldp(pold, u0 - P);
+            if (hy) pmy = ldp(pold, u0 - s.nx);
+            if (py) ppy = ldp(pold, u0 + s.nx);
+            if (pz) ppz = ldp(pold, u0 + P);
+        }
+        const double2 gx2 = ldp(s.gx, u0);
+        const double2 gy2 = valid ? ldp(s.gy, u0) : zero2, gz2 = valid ? ldp(s.gz, u0) : zero2;
+        const double2 gym = hy ? ldp(s.gy, u0 - s.nx) : zero2;
+        const double2 gzm = hz ? ldp(s.gz, u0 - P) : zero2;
+        const double2 D2 = valid ? ldp(v.D, u0) : zero2;
+        double2 x2 = zero2;
+        if (!first && valid) x2 = ldp_cg(v.x, u0);
+        double zl = 0.0, pol = 0.0, gxe = 0.0, zr = 0.0, por = 0.0;
+        if (valid && lane == 0 && hx) {
+            zl = __ldg(zv + u0 - 1);
+            gxe = __ldg(s.gx + u0 - 1);
+            if (!first) pol = __ldg(pold + u0 - 1);
+        }
+        if (valid && lane == 31 && hr) {
+            zr = __ldg(zv + u0 + 2);
+            if (!first) por = __ldg(pold + u0 + 2);
+        }
+        // ---- p = z + beta p_old
+        double2 p2 = z2;
+        if (!first) p2 = make_double2(z2.x + beta * po.x, z2.y + beta * po.y);
+        double pl = __shfl_up_sync(0xffffffffu, p2.y, 1);
+        double pr = __shfl_down_sync(0xffffffffu, p2.x, 1);
+        double gxl = __shfl_up_sync(0xffffffffu, gx2.y, 1);
+        if (!valid) continue;
+        if (lane == 0) { pl = first ? zl : zl + beta * pol; gxl = gxe; }
+        if (lane == 31) pr = first ? zr : zr + beta * por;
+        if (!hx) { pl = 0.0; gxl = 0.0; }
+        if (!hr) pr = 0.0;
+        double2 qmz = zmz, qmy = zmy, qpy = zpy, qpz = zpz;
+        if (!first) {
+            qmz = make_double2(zmz.x + beta * pmz.x, zmz.y + beta * pmz.y);
+            qmy = make_double2(zmy.x + beta * pmy.x, zmy.y + beta * pmy.y);
+            qpy = make_double2(zpy.x + beta * ppy.x, zpy.y + beta * ppy.y);
+            qpz = make_double2(zpz.x + beta * ppz.x, zpz.y + beta * ppz.y);
+        }
+        double a = 0.0;
+        a = a + gzm.x * qmz.x;
+        a = a + gym.x * qmy.x;
+        a = a + gxl * pl;
+        a = a + gx2.x * p2.y;
+        a = a + gy2.x * qpy.x;
+        a = a + gz2.x * qpz.x;
+        double b = 0.0;
+        b = b + gzm.y * qmz.y;
+        b = b + gym.y * qmy.y;
+        b = b + gx2.x * p2.x;
+        b = b + gx2.y * pr;
+        b = b + gy2.y * qpy.y;
+        b = b + gz2.y * qpz.y;
+        const double q0 = D2.x * p2.x - a, q1 = D2.y * p2.y - b;
+        stp(pnew, u0, p2);
+        stp(v.q, u0, make_double2(q0, q1));
+        if (!first) stp(v.x, u0, make_double2(x2.x + alpha * po.x, x2.y + alpha * po.y));
+        acc[0] = acc[0] + p2.x * q0;
+        acc[0] = acc[0] + p2.y * q1;
+    }
+    if (c3_chunk_epilogue<1>(acc, v.chunk0 + (int32_t)blockIdx.x, ra) && cd.finalize && threadIdx.x == 0) {
+        finalize_pq(ra.ctrl, ra.slots);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K5 (vectorised; any graph): r -= alpha q, z = Dinv r, RZ reductions.
+// Requires n_own even or arrays padded (they are padded to whole chunks).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_pair_axpy(VecArgs v, RedArgs ra, CondArgs cd)
+{
+    DevCtrl *ctrl = ra.ctrl;
+    if (ctrl->done) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) set_cond2(cd, ctrl);
+        return;
+    }
+    const double alpha = ctrl->alpha;
+    const int64_t base = (int64_t)blockIdx.x * kChunk;
+    double acc[3] = {0.0, 0.0, 0.0};
+#pragma unroll 2
+    for (int j = 0; j < 8; j++) {
+        const int64_t u0 = base + 2 * (int64_t)threadIdx.x + 512 * j;
+        if (u0 >= v.n_own) break;
+        const double2 r2 = ldp_cg(v.r, u0), q2 = ldp(v.q, u0), d2 = ldp(v.Dinv, u0);
+        const double r0 = r2.x - alpha * q2.x, r1 = r2.y - alpha * q2.y;
+        const double z0 = r0 * d2.x, z1 = r1 * d2.y;
+        stp(v.r, u0, make_double2(r0, r1));
+        stp(v.z, u0, make_double2(z0, z1));
+        acc[0] = acc[0] + r0 * z0;
+        acc[1] = acc[1] + z0 * z0;
+        acc[2] = acc[2] + r0 * r0;
+        if (u0 + 1 < v.n_own) {
+            acc[0] = acc[0] + r1 * z1;
+            acc[1] = acc[1] + z1 * z1;
+            acc[2] = acc[2] + r1 * r1;
+        }
+    }
+    if (c3_chunk_epilogue<3>(acc, v.chunk0 + (int32_t)blockIdx.x, ra) && cd.finalize && threadIdx.x == 0) {
+        finalize_rz(ctrl, ra.slots);
+        set_cond2(cd, ctrl);
+    }
+}
+
+// After the loop: x += alpha_{k-1} p_{k-1} (or 0 when b = 0); grid-stride over
+// pairs with a small grid, so an idle call (k = 0) costs one short launch.
+__global__ void __launch_bounds__(256) k_pair_finish(VecArgs v, const DevCtrl *ctrl)
+{
+    const int32_t k = ctrl->k;
+    const bool zero = ctrl->zero_x != 0;
+    if (!zero && (k == 0 || ctrl->status != ST_OK)) return;
+    const double alpha = ctrl->alpha;
+    const double *pl = (k & 1) ? v.p1 : v.p0;
+    const int64_t npairs = (v.n_own + 1) / 2;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npairs; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t u0 = 2 * i;
+        if (zero) {
+            stp(v.x, u0, make_double2(0.0, 0.0));
+        } else {
+            const double2 x2 = ldp_cg(v.x, u0), p2 = ldp(pl, u0);
+            stp(v.x, u0, make_double2(x2.x + alpha * p2.x, x2.y + alpha * p2.y));
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+static inline unsigned nblk(int64_t n_own) { return (unsigned)((n_own + kChunk - 1) / kChunk); }
+
+void launch_pair_assemble(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, int mode,
+                          double eps, double *gs_out, double *gt_out, cudaStream_t st)
+{
+    const double eps2 = eps * eps;
+    const unsigned nb = nblk(v.n_own);
+    if (mode == ASM_INIT) {
+        k_pair_edges<true><<<nb, kThreads, 0, st>>>(s, v, eps2);
+        k_pair_nodes<ASM_INIT><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
+    } else {
+        k_pair_edges<false><<<nb, kThreads, 0, st>>>(s, v, eps2);
+        if (mode == ASM_REWEIGHT_WARM)
+            k_pair_nodes<ASM_REWEIGHT_WARM><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
+        else
+            k_pair_nodes<ASM_REWEIGHT_COLD><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
+    }
+}
+
+void launch_pair_pspmv(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
+                       cudaStream_t st)
+{
+    k_pair_pspmv<<<nblk(v.n_own), kThreads, 0, st>>>(s, v, ra, cd);
+}
+
+void launch_pair_axpy(const VecArgs &v, const RedArgs &ra, const CondArgs &cd, cudaStream_t st)
+{
+    k_pair_axpy<<<nblk(v.n_own), kThreads, 0, st>>>(v, ra, cd);
+}
+
+void launch_pair_finish(const VecArgs &v, DevCtrl *ctrl, cudaStream_t st)
+{
+    const int64_t npairs = (v.n_own + 1) / 2;
+    const unsigned nb = (unsigned)std::min<int64_t>((npairs + 255) / 256, 148 * 8);
+    k_pair_finish<<<nb > 0 ? nb : 1, 256, 0, st>>>(v, ctrl);
+}
+
+}  // namespace irls
