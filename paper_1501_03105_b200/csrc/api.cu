@@ -46,6 +46,14 @@ static irls_status fail(irls_ctx *c, irls_status st, const std::string &msg)
         if (cudaSetDevice((c)->device) != cudaSuccess) return IRLS_ERR_CUDA;      \
     } while (0)
 
+// Blocking copy ordered on the context stream (its allocations are stream-ordered).
+static cudaError_t memcpy_sync(irls_ctx *c, void *dst, const void *src, size_t n, cudaMemcpyKind k)
+{
+    cudaError_t e = cudaMemcpyAsync(dst, src, n, k, c->stream);
+    if (e != cudaSuccess) return e;
+    return cudaStreamSynchronize(c->stream);
+}
+
 static irls_status last_launch(irls_ctx *c, const char *what)
 {
     const cudaError_t e = cudaGetLastError();
@@ -53,13 +61,25 @@ static irls_status last_launch(irls_ctx *c, const char *what)
     return IRLS_OK;
 }
 
+// Device memory comes from the device's stream-ordered pool with an unbounded
+// release threshold: a create / destroy cycle maps HBM once and then reuses
+// it (sizes here are GBs; cudaMalloc / cudaFree would remap every time).
+static void setup_pool(int device)
+{
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+}
+
 template <class T>
 static T *dalloc(irls_ctx *c, int64_t count)
 {
     void *p = nullptr;
     const size_t bytes = (size_t)std::max<int64_t>(count, 1) * sizeof(T);
-    if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
-    cudaMemset(p, 0, bytes);
+    if (cudaMallocAsync(&p, bytes, c->stream) != cudaSuccess) return nullptr;
+    cudaMemsetAsync(p, 0, bytes, c->stream);
     c->allocs.push_back(p);
     return (T *)p;
 }
@@ -269,11 +289,11 @@ static irls_status enq_assemble(irls_ctx *c, int mode, const CondArgs &cd, cudaS
             irls_status s = halo(c, c->x, st);
             if (s) return s;
         }
-        launch_stencil_assemble_ex(stencil_args(c, false), v, ra, cd, mode, c->opt.eps, c->gs_diag, c->gt_diag, st);
+        c->launches +=
+            launch_stencil_assemble_ex(stencil_args(c, false), v, ra, cd, mode, c->opt.eps, c->gs_diag, c->gt_diag, st);
     } else {
-        launch_sell_assemble_ex(sell_args(c), v, ra, cd, mode, c->opt.eps, c->gs_diag, c->gt_diag, st);
+        c->launches += launch_sell_assemble_ex(sell_args(c), v, ra, cd, mode, c->opt.eps, c->gs_diag, c->gt_diag, st);
     }
-    c->launches++;
     if (c->world > 1) {
         irls_status s = allreduce_slots(c, 5, st);
         if (s) return s;
@@ -356,6 +376,7 @@ static irls_status build_graph(irls_ctx *c, int mode)
     cd.use = 1;
     cd.finalize = 1;
     const int64_t lsave = c->launches;
+    c->launches = 0;
     if (mode == ASM_INIT) CK(cudaMemsetAsync(c->x, 0, sizeof(double) * c->n_own, st));
     irls_status s = enq_assemble(c, mode, cd, st);
     if (s) { cudaGraph_t g; cudaStreamEndCapture(st, &g); if (g) cudaGraphDestroy(g); return s; }
@@ -371,7 +392,10 @@ static irls_status build_graph(irls_ctx *c, int mode)
     cudaGraph_t body = p.conditional.phGraph_out[0];
     CK(cudaStreamUpdateCaptureDependencies(st, &cnode, 1, cudaStreamSetCaptureDependencies));
     CK(cudaStreamBeginCaptureToGraph(c->side_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    const int64_t pre = c->launches;
     s = enq_body(c, cd, c->side_stream);
+    c->gl_body = c->launches - pre;
+    c->launches = pre;
     cudaGraph_t bodyg;
     CK(cudaStreamEndCapture(c->side_stream, &bodyg));
     if (s) { cudaGraph_t g; cudaStreamEndCapture(st, &g); if (g) cudaGraphDestroy(g); return s; }
@@ -381,12 +405,11 @@ static irls_status build_graph(irls_ctx *c, int mode)
     if (s) { cudaGraphDestroy(full); return s; }
     CK(cudaGraphInstantiate(&c->gexec[mode], full, 0));
     cudaGraphDestroy(full);
+    c->gl_fixed[mode] = c->launches;
     c->launches = lsave;
     return IRLS_OK;
 }
 
-// launches per solve in graph mode: assemble(1) + tail(2 or 4) + 2 per CG iteration
-static int64_t tail_launches(const irls_ctx *c) { return 1 + 2 + (c->opt.record_trace ? 2 : 0); }
 
 static irls_status enqueue_solve(irls_ctx *c, int mode)
 {
@@ -397,7 +420,8 @@ static irls_status enqueue_solve(irls_ctx *c, int mode)
             if (s) return s;
         }
         CK(cudaGraphLaunch(c->gexec[mode], st));
-        c->launches += tail_launches(c);
+        c->launches += c->gl_fixed[mode];
+        c->graph_iters_pending = true;
         return IRLS_OK;
     }
     // host loop: one 4-byte readback of the device "done" flag per iteration
@@ -459,7 +483,7 @@ static irls_status run_solves(irls_ctx *c, int mode0, int mode_rest, int count, 
     if (!s && e != cudaSuccess) s = fail(c, IRLS_ERR_CUDA, std::string("solve: ") + cudaGetErrorString(e));
     std::vector<DevReport> h(count);
     if (!s) {
-        e = cudaMemcpy(h.data(), c->reports, sizeof(DevReport) * count, cudaMemcpyDeviceToHost);
+        e = memcpy_sync(c, h.data(), c->reports, sizeof(DevReport) * count, cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) s = fail(c, IRLS_ERR_CUDA, cudaGetErrorString(e));
     }
     int64_t tot = 0;
@@ -471,7 +495,8 @@ static irls_status run_solves(irls_ctx *c, int mode0, int mode_rest, int count, 
             if (reps) copy_report(h[i], reps + i, ms);
             if (h[i].status != 0 && !s) s = fail(c, (irls_status)h[i].status, "CG breakdown (p'Ap <= 0 or non-finite scalar)");
         }
-        c->launches += 2 * tot;
+        if (c->graph_iters_pending) c->launches += c->gl_body * tot;
+        c->graph_iters_pending = false;
     }
     for (auto &ee : ev) cudaEventDestroy(ee);
     c->last_cg_iters = tot;
@@ -500,6 +525,7 @@ static irls_status common_setup(irls_ctx *c, const irls_comm_desc *comm, const i
     }
     CK(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
     CK(cudaMallocHost(&c->h_done, sizeof(int)));
+    setup_pool(c->device);
     return IRLS_OK;
 }
 
@@ -537,7 +563,7 @@ static irls_status alloc_solver(irls_ctx *c, int64_t ghost)
     h.max_iter = c->opt.cg_max_iter;
     h.norm = c->opt.cg_norm;
     h.done = 1;
-    CK(cudaMemcpy(c->ctrl, &h, sizeof(h), cudaMemcpyHostToDevice));
+    CK(memcpy_sync(c, c->ctrl, &h, sizeof(h), cudaMemcpyHostToDevice));
     return IRLS_OK;
 }
 
@@ -631,7 +657,7 @@ extern "C" irls_status irls_mincut_create_stencil(irls_ctx **out, const irls_com
             cudaMemcpyAsync(c->cz, cz, b, cudaMemcpyHostToDevice, c->stream);
             cudaMemcpyAsync(c->cs, cs, b, cudaMemcpyHostToDevice, c->stream);
             cudaMemcpyAsync(c->ct, ct, b, cudaMemcpyHostToDevice, c->stream);
-            unsigned long long vo[5];
+            unsigned long long vo[6];
             if (validate_stencil(nx, ny, nz, c->cx, c->cy, c->cz, c->cs, c->ct, vo, c->stream))
                 s = fail(c, IRLS_ERR_CUDA, "validate_stencil");
             else if (vo[0]) s = IRLS_ERR_BAD_CAPACITY;
@@ -641,19 +667,10 @@ extern "C" irls_status irls_mincut_create_stencil(irls_ctx **out, const irls_com
                 double cmax;
                 memcpy(&cmax, &vo[4], sizeof(double));
                 c->F = compute_F(cmax, (int64_t)vo[3]);
-                c->n_links = 0;
+                c->n_links = (int64_t)vo[5];  // |E~| with c > 0
             }
         }
-        if (!s) {
-            // |E~| with c > 0 for the GEdge/s metric (host count, once)
-            int64_t nl = 0;
-            for (int64_t u = 0; u < N; u++) {
-                const int64_t x = u % nx, y = (u / nx) % ny, z = u / c->P;
-                nl += (x < nx - 1 && cx[u] > 0) + (y < ny - 1 && cy[u] > 0) + (z < nz - 1 && cz[u] > 0);
-            }
-            c->n_links = nl;
-            s = init_nccl(c, comm);
-        }
+        if (!s) s = init_nccl(c, comm);
     }
     if (s) {
         irls_mincut_destroy(c);
@@ -829,13 +846,13 @@ extern "C" irls_status irls_mincut_create_csr(irls_ctx **out, const irls_comm_de
         if (!c->cs || !c->ct || !c->slice_ptr || !c->col || !c->cap || !c->gsell || !c->orig_dev) st = IRLS_ERR_OOM;
     }
     if (!st && nr > 0) {
-        cudaMemcpy(c->cs, hcs.data(), sizeof(double) * nr, cudaMemcpyHostToDevice);
-        cudaMemcpy(c->ct, hct.data(), sizeof(double) * nr, cudaMemcpyHostToDevice);
-        cudaMemcpy(c->slice_ptr, sptr.data(), sizeof(int64_t) * (nsl + 1), cudaMemcpyHostToDevice);
-        cudaMemcpy(c->col, scol.data(), sizeof(int32_t) * nent, cudaMemcpyHostToDevice);
-        cudaMemcpy(c->cap, scap.data(), sizeof(double) * nent, cudaMemcpyHostToDevice);
-        cudaMemcpy(c->orig_dev, orig.data(), sizeof(int64_t) * nr, cudaMemcpyHostToDevice);
-        if (cudaDeviceSynchronize() != cudaSuccess) st = fail(c, IRLS_ERR_CUDA, "csr upload");
+        memcpy_sync(c, c->cs, hcs.data(), sizeof(double) * nr, cudaMemcpyHostToDevice);
+        memcpy_sync(c, c->ct, hct.data(), sizeof(double) * nr, cudaMemcpyHostToDevice);
+        memcpy_sync(c, c->slice_ptr, sptr.data(), sizeof(int64_t) * (nsl + 1), cudaMemcpyHostToDevice);
+        memcpy_sync(c, c->col, scol.data(), sizeof(int32_t) * nent, cudaMemcpyHostToDevice);
+        memcpy_sync(c, c->cap, scap.data(), sizeof(double) * nent, cudaMemcpyHostToDevice);
+        memcpy_sync(c, c->orig_dev, orig.data(), sizeof(int64_t) * nr, cudaMemcpyHostToDevice);
+        if (cudaStreamSynchronize(c->stream) != cudaSuccess) st = fail(c, IRLS_ERR_CUDA, "csr upload");
     }
     if (st) {
         irls_mincut_destroy(c);
@@ -917,7 +934,7 @@ extern "C" irls_status irls_set_terminal_weights(irls_ctx *c, const double *cs, 
     }
     // n-link part of F: recomputed from the device copies
     if (c->kind == 0) {
-        unsigned long long vo[5];
+        unsigned long long vo[6];
         CK(cudaMemcpyAsync(c->cs, cs, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
         CK(cudaMemcpyAsync(c->ct, ct, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
         if (validate_stencil(c->nx, c->ny, c->nz, c->cx, c->cy, c->cz, c->cs, c->ct, vo, c->stream))
@@ -925,9 +942,9 @@ extern "C" irls_status irls_set_terminal_weights(irls_ctx *c, const double *cs, 
         if (vo[1] != 0 || vo[2] == 0) {
             // zero n-links present: full check on the host copy
             std::vector<double> hx(n), hy(n), hz(n);
-            cudaMemcpy(hx.data(), c->cx, sizeof(double) * n, cudaMemcpyDeviceToHost);
-            cudaMemcpy(hy.data(), c->cy, sizeof(double) * n, cudaMemcpyDeviceToHost);
-            cudaMemcpy(hz.data(), c->cz, sizeof(double) * n, cudaMemcpyDeviceToHost);
+            memcpy_sync(c, hx.data(), c->cx, sizeof(double) * n, cudaMemcpyDeviceToHost);
+            memcpy_sync(c, hy.data(), c->cy, sizeof(double) * n, cudaMemcpyDeviceToHost);
+            memcpy_sync(c, hz.data(), c->cz, sizeof(double) * n, cudaMemcpyDeviceToHost);
             if (!grid_nonsingular(c->nx, c->ny, c->nz, hx.data(), hy.data(), hz.data(), cs, ct))
                 return fail(c, IRLS_ERR_SINGULAR, "terminal weights make L~ singular");
         }
@@ -937,11 +954,11 @@ extern "C" irls_status irls_set_terminal_weights(irls_ctx *c, const double *cs, 
     } else {
         std::vector<double> cp(c->n_entries);
         std::vector<int32_t> cl(c->n_entries);
-        cudaMemcpy(cp.data(), c->cap, sizeof(double) * c->n_entries, cudaMemcpyDeviceToHost);
-        cudaMemcpy(cl.data(), c->col, sizeof(int32_t) * c->n_entries, cudaMemcpyDeviceToHost);
+        memcpy_sync(c, cp.data(), c->cap, sizeof(double) * c->n_entries, cudaMemcpyDeviceToHost);
+        memcpy_sync(c, cl.data(), c->col, sizeof(int32_t) * c->n_entries, cudaMemcpyDeviceToHost);
         // each n-link appears twice (both rows): count once via v > u
         std::vector<int64_t> sp((c->n_glob + 31) / 32 + 1);
-        cudaMemcpy(sp.data(), c->slice_ptr, sizeof(int64_t) * sp.size(), cudaMemcpyDeviceToHost);
+        memcpy_sync(c, sp.data(), c->slice_ptr, sizeof(int64_t) * sp.size(), cudaMemcpyDeviceToHost);
         for (int64_t sl = 0; sl + 1 < (int64_t)sp.size(); sl++)
             for (int64_t e = sp[sl]; e < sp[sl + 1]; e++) {
                 const int64_t u = sl * 32 + ((e - sp[sl]) & 31);
@@ -999,6 +1016,7 @@ extern "C" irls_status irls_sweep_cut(irls_ctx *c, uint8_t *side, int32_t *order
     irls_status s = alloc_sweep(c);
     if (s) return s;
     int launches = 0;
+    c->launches = 0;
     SweepBuffers &b = c->sb;
     CK(cudaMemsetAsync(b.flags, 0, sizeof(int32_t) * 4, st));
     sweep_keys(c->x, b, st);
@@ -1061,7 +1079,7 @@ extern "C" irls_status irls_get_side(irls_ctx *c, uint8_t *side)
     GUARD(c);
     if (!c->sweep_valid) return fail(c, IRLS_ERR_STATE, "no sweep result");
     if (!side) return IRLS_ERR_INVALID_ARGUMENT;
-    CK(cudaMemcpy(side, c->sb.side, c->n_total, cudaMemcpyDeviceToHost));
+    CK(memcpy_sync(c, side, c->sb.side, c->n_total, cudaMemcpyDeviceToHost));
     return IRLS_OK;
 }
 
@@ -1170,7 +1188,8 @@ extern "C" void irls_mincut_destroy(irls_ctx *c)
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (auto &g : c->gexec)
         if (g) cudaGraphExecDestroy(g);
-    for (void *p : c->allocs) cudaFree(p);
+    for (void *p : c->allocs) cudaFreeAsync(p, c->stream);
+    if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->h_done) cudaFreeHost(c->h_done);
     if (c->nccl) ncclCommDestroy(c->nccl);
     if (c->side_stream) cudaStreamDestroy(c->side_stream);

@@ -74,4 +74,7 @@ struct irls_ctx {
 
     // ---- stats
     int64_t launches = 0, last_cg_iters = 0;
+    int64_t gl_fixed[3] = {0, 0, 0};  // kernels per solve graph outside the WHILE body
+    int64_t gl_body = 0;              // kernels per CG iteration (WHILE body)
+    bool graph_iters_pending = false;
 };

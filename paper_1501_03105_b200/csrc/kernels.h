@@ -54,9 +54,9 @@ void launch_stencil_assemble(const StencilArgs &s, const VecArgs &v, const RedAr
 void launch_sell_assemble(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
                           int mode, double eps, cudaStream_t st);
 // _ex: also store the terminal conductances gs/gt (record_trace diagnostics)
-void launch_stencil_assemble_ex(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
+int launch_stencil_assemble_ex(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
                                 int mode, double eps, double *gs_out, double *gt_out, cudaStream_t st);
-void launch_sell_assemble_ex(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
+int launch_sell_assemble_ex(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
                              int mode, double eps, double *gs_out, double *gt_out, cudaStream_t st);
 // K3: p = z + beta p_old (fused), lazy x += alpha p_old, q = L~ p, PQ reduction
 void launch_stencil_pspmv(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
@@ -88,7 +88,7 @@ void launch_diag_finalize(DevCtrl *ctrl, const double *slots, DevReport *reports
 enum { PH_START = 0, PH_PQ = 1, PH_RZ = 2 };
 
 // stencil_pair.cu (nx even): K1a+K1b, K3, K5, finish with 128-bit pair access
-void launch_pair_assemble(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, int mode,
+int launch_pair_assemble(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, int mode,
                           double eps, double *gs_out, double *gt_out, cudaStream_t st);
 void launch_pair_pspmv(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
                        cudaStream_t st);
@@ -134,8 +134,8 @@ __int128 qfix_host(double c, int32_t F);
 }  // namespace irls
 
 namespace irls {
-// validate.cu: out[0..4] = bad, zero interior n-links, nodes with a positive
-// terminal edge, positive capacities, bits of the max capacity
+// validate.cu: out[0..5] = bad, zero interior n-links, nodes with a positive
+// terminal edge, positive capacities, bits of the max capacity, positive n-links
 int validate_stencil(int32_t nx, int32_t ny, int32_t nz, const double *cx, const double *cy, const double *cz,
                      const double *cs, const double *ct, unsigned long long *out_host, cudaStream_t st);
 }  // namespace irls

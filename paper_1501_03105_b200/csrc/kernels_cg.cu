@@ -462,7 +462,7 @@ void launch_stencil_assemble(const StencilArgs &s, const VecArgs &v, const RedAr
     launch_stencil_assemble_ex(s, v, ra, cd, mode, eps, nullptr, nullptr, st);
 }
 
-void launch_stencil_assemble_ex(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
+int launch_stencil_assemble_ex(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
                                 int mode, double eps, double *gs_out, double *gt_out, cudaStream_t st)
 {
     if (s.nx % 2 == 0) return launch_pair_assemble(s, v, ra, cd, mode, eps, gs_out, gt_out, st);
@@ -472,6 +472,7 @@ void launch_stencil_assemble_ex(const StencilArgs &s, const VecArgs &v, const Re
     else if (mode == ASM_REWEIGHT_WARM)
         k_stencil_assemble<ASM_REWEIGHT_WARM><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
     else k_stencil_assemble<ASM_REWEIGHT_COLD><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
+    return 1;
 }
 
 void launch_sell_assemble(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, int mode,
@@ -480,7 +481,7 @@ void launch_sell_assemble(const SellArgs &s, const VecArgs &v, const RedArgs &ra
     launch_sell_assemble_ex(s, v, ra, cd, mode, eps, nullptr, nullptr, st);
 }
 
-void launch_sell_assemble_ex(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, int mode,
+int launch_sell_assemble_ex(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, int mode,
                              double eps, double *gs_out, double *gt_out, cudaStream_t st)
 {
     const double eps2 = eps * eps;
@@ -489,6 +490,7 @@ void launch_sell_assemble_ex(const SellArgs &s, const VecArgs &v, const RedArgs 
     else if (mode == ASM_REWEIGHT_WARM)
         k_sell_assemble<ASM_REWEIGHT_WARM><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
     else k_sell_assemble<ASM_REWEIGHT_COLD><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
+    return 1;
 }
 
 void launch_stencil_pspmv(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,

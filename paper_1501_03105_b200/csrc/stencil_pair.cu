@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(256) k_pair_finish(VecArgs v, const DevCtrl *c
 // ---------------------------------------------------------------------------
 static inline unsigned nblk(int64_t n_own) { return (unsigned)((n_own + kChunk - 1) / kChunk); }
 
-void launch_pair_assemble(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, int mode,
+int launch_pair_assemble(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, int mode,
                           double eps, double *gs_out, double *gt_out, cudaStream_t st)
 {
     const double eps2 = eps * eps;
@@ -388,6 +388,7 @@ void launch_pair_assemble(const StencilArgs &s, const VecArgs &v, const RedArgs 
         else
             k_pair_nodes<ASM_REWEIGHT_COLD><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
     }
+    return 2;
 }
 
 void launch_pair_pspmv(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,

@@ -8,7 +8,7 @@
 namespace irls {
 
 struct ValidateOut {
-    unsigned long long bad, zero_nlinks, pos_terms, cnt_pos, cmax_bits;
+    unsigned long long bad, zero_nlinks, pos_terms, cnt_pos, cmax_bits, nlinks_pos;
 };
 
 __device__ __forceinline__ void vcheck(double c, bool present, unsigned long long &bad, unsigned long long &zero,
@@ -28,7 +28,7 @@ __global__ void k_validate_stencil(int32_t nx, int32_t ny, int32_t nz, FastDiv f
                                    const double *cy, const double *cz, const double *cs, const double *ct, int64_t N,
                                    ValidateOut *out)
 {
-    unsigned long long bad = 0, zero = 0, cnt = 0, pt = 0;
+    unsigned long long bad = 0, zero = 0, cnt = 0, pt = 0, nl = 0;
     double cmax = 0.0;
     for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < N; u += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t uu = (uint32_t)u;
@@ -36,9 +36,11 @@ __global__ void k_validate_stencil(int32_t nx, int32_t ny, int32_t nz, FastDiv f
         const int32_t x = (int32_t)(uu - t1 * (uint32_t)nx);
         const uint32_t zz = fdiv(t1, fdy);
         const int32_t y = (int32_t)(t1 - zz * (uint32_t)ny), z = (int32_t)zz;
+        const unsigned long long cb = cnt;
         vcheck(cx[u], x < nx - 1, bad, zero, cnt, cmax, true);
         vcheck(cy[u], y < ny - 1, bad, zero, cnt, cmax, true);
         vcheck(cz[u], z < nz - 1, bad, zero, cnt, cmax, true);
+        nl += cnt - cb;
         const unsigned long long c0 = cnt;
         vcheck(cs[u], true, bad, zero, cnt, cmax, false);
         vcheck(ct[u], true, bad, zero, cnt, cmax, false);
@@ -49,6 +51,7 @@ __global__ void k_validate_stencil(int32_t nx, int32_t ny, int32_t nz, FastDiv f
         zero += __shfl_down_sync(0xffffffffu, zero, off);
         cnt += __shfl_down_sync(0xffffffffu, cnt, off);
         pt += __shfl_down_sync(0xffffffffu, pt, off);
+        nl += __shfl_down_sync(0xffffffffu, nl, off);
         cmax = fmax(cmax, __shfl_down_sync(0xffffffffu, cmax, off));
     }
     if ((threadIdx.x & 31) == 0) {
@@ -56,6 +59,7 @@ __global__ void k_validate_stencil(int32_t nx, int32_t ny, int32_t nz, FastDiv f
         if (zero) atomicAdd(&out->zero_nlinks, zero);
         if (cnt) atomicAdd(&out->cnt_pos, cnt);
         if (pt) atomicAdd(&out->pos_terms, pt);
+        if (nl) atomicAdd(&out->nlinks_pos, nl);
         atomicMax(&out->cmax_bits, (unsigned long long)__double_as_longlong(cmax));  // cmax >= 0
     }
 }
@@ -65,7 +69,7 @@ int validate_stencil(int32_t nx, int32_t ny, int32_t nz, const double *cx, const
                      const double *cs, const double *ct, unsigned long long *out_host, cudaStream_t st)
 {
     ValidateOut *d = nullptr;
-    if (cudaMalloc(&d, sizeof(ValidateOut)) != cudaSuccess) return 1;
+    if (cudaMallocAsync((void **)&d, sizeof(ValidateOut), st) != cudaSuccess) return 1;
     cudaMemsetAsync(d, 0, sizeof(ValidateOut), st);
     const int64_t N = (int64_t)nx * ny * nz;
     const FastDiv fdx = make_fastdiv((uint32_t)nx), fdy = make_fastdiv((uint32_t)ny);
@@ -73,14 +77,15 @@ int validate_stencil(int32_t nx, int32_t ny, int32_t nz, const double *cx, const
     k_validate_stencil<<<(unsigned)nb, 256, 0, st>>>(nx, ny, nz, fdx, fdy, cx, cy, cz, cs, ct, N, d);
     ValidateOut h;
     cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(d, st);
     const cudaError_t e = cudaStreamSynchronize(st);
-    cudaFree(d);
     if (e != cudaSuccess) return 2;
     out_host[0] = h.bad;
     out_host[1] = h.zero_nlinks;
     out_host[2] = h.pos_terms;
     out_host[3] = h.cnt_pos;
     out_host[4] = h.cmax_bits;
+    out_host[5] = h.nlinks_pos;
     return 0;
 }
 
