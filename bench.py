@@ -283,6 +283,10 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.e2e_steps):
+        if world > 1:  # a fresh NCCL id per communicator (part of the user's create path)
+            obj = [I.irls_nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            comm = I.comm_desc(world, rank, local, obj[0], stream.cuda_stream)
         mm = I.MinCut.irls_mincut_create_stencil(spec["nx"], spec["ny"], spec["nz"], pinned["cx"], pinned["cy"],
                                                  pinned["cz"], pinned["cs"], pinned["ct"], opts, comm)
         _, tot = mm.irls_solve(I.IRLS_FROM_SCRATCH, T=T, reports=False)

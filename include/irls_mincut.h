@@ -188,6 +188,15 @@ const char *irls_last_error(const irls_ctx *ctx);
  * covers chunks [floor(gK/8), floor((g+1)K/8)). */
 irls_status irls_plan_stencil(int32_t nx, int32_t ny, int32_t nz, int32_t world, int32_t rank,
                               int32_t *z0, int32_t *z1, int32_t *g0, int32_t *g1);
+/* Halo plan of rank `rank`'s z-slab: element offsets relative to its first
+ * owned node (send_lo/send_hi: boundary planes sent to peer_lo/peer_hi;
+ * recv_lo/recv_hi: ghost planes received from them), count = nx*ny values
+ * per message; peers are -1 when absent. */
+typedef struct {
+    int64_t count, n_own, send_lo, recv_lo, send_hi, recv_hi;
+    int32_t peer_lo, peer_hi, first_plane, reserved;
+} irls_halo;
+irls_status irls_halo_plan(int32_t nx, int32_t ny, int32_t nz, int32_t world, int32_t rank, irls_halo *h);
 /* The fixed 8-leaf tree of C3 step 6: ((s0+s4)+(s2+s6))+((s1+s5)+(s3+s7)). */
 double irls_combine_slots(const double slots[8]);
 

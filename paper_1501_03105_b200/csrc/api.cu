@@ -253,20 +253,73 @@ static RedArgs red_args(const irls_ctx *c)
 // ---------------------------------------------------------------------------
 // multi-GPU collectives (NCCL over NVLink): halo planes, slot allreduce
 // ---------------------------------------------------------------------------
+// Halo plan of a z-slab (offsets relative to the first owned node): the
+// boundary planes go to the neighbour ranks and their planes land in the
+// ghost planes just outside [0, n_own).  Peers are -1 when absent.
+extern "C" irls_status irls_halo_plan(int32_t nx, int32_t ny, int32_t nz, int32_t world, int32_t rank,
+                                      irls_halo *h)
+{
+    if (!h) return IRLS_ERR_INVALID_ARGUMENT;
+    int32_t z0, z1;
+    irls_status s = irls_plan_stencil(nx, ny, nz, world, rank, &z0, &z1, nullptr, nullptr);
+    if (s) return s;
+    const int64_t P = (int64_t)nx * ny;
+    const int64_t n_own = (int64_t)(z1 - z0) * P;
+    h->count = P;
+    h->n_own = n_own;
+    h->first_plane = z0;
+    h->peer_lo = rank > 0 ? rank - 1 : -1;
+    h->peer_hi = rank < world - 1 ? rank + 1 : -1;
+    h->send_lo = 0;
+    h->recv_lo = -P;
+    h->send_hi = n_own - P;
+    h->recv_hi = n_own;
+    return IRLS_OK;
+}
+
 static irls_status halo(irls_ctx *c, double *arr, cudaStream_t st)
 {
     if (c->world == 1) return IRLS_OK;
-    const size_t P = (size_t)c->P;
+    const irls_halo &h = c->hplan;
     NK(ncclGroupStart());
-    if (c->lo_ghost) {
-        NK(ncclSend(arr, P, ncclDouble, c->rank - 1, c->nccl, st));
-        NK(ncclRecv(arr - P, P, ncclDouble, c->rank - 1, c->nccl, st));
+    if (h.peer_lo >= 0) {
+        NK(ncclSend(arr + h.send_lo, (size_t)h.count, ncclDouble, h.peer_lo, c->nccl, st));
+        NK(ncclRecv(arr + h.recv_lo, (size_t)h.count, ncclDouble, h.peer_lo, c->nccl, st));
     }
-    if (c->hi_ghost) {
-        NK(ncclSend(arr + c->n_own - P, P, ncclDouble, c->rank + 1, c->nccl, st));
-        NK(ncclRecv(arr + c->n_own, P, ncclDouble, c->rank + 1, c->nccl, st));
+    if (h.peer_hi >= 0) {
+        NK(ncclSend(arr + h.send_hi, (size_t)h.count, ncclDouble, h.peer_hi, c->nccl, st));
+        NK(ncclRecv(arr + h.recv_hi, (size_t)h.count, ncclDouble, h.peer_hi, c->nccl, st));
     }
     NK(ncclGroupEnd());
+    return IRLS_OK;
+}
+
+// Rank 0 receives every slab of x (Algorithm 1 step 5: "Gather the
+// voltage vector to the root process"); returns the full vector's pointer on
+// rank 0 (the local x when world == 1).
+static irls_status gather_x(irls_ctx *c, double **full)
+{
+    *full = c->x;
+    if (c->world == 1) return IRLS_OK;
+    cudaStream_t st = c->stream;
+    if (c->rank == 0 && !c->x_full) {
+        c->x_full = dalloc<double>(c, c->n_glob);
+        if (!c->x_full) return fail(c, IRLS_ERR_OOM, "x_full");
+    }
+    NK(ncclGroupStart());
+    if (c->rank == 0) {
+        for (int r = 1; r < c->world; r++) {
+            int32_t z0, z1;
+            irls_plan_stencil(c->nx, c->ny, c->nz, c->world, r, &z0, &z1, nullptr, nullptr);
+            const int64_t lo = (int64_t)z0 * c->P, n = std::min<int64_t>((int64_t)z1 * c->P, c->n_glob) - lo;
+            NK(ncclRecv(c->x_full + lo, (size_t)n, ncclDouble, r, c->nccl, st));
+        }
+    } else {
+        NK(ncclSend(c->x, (size_t)c->n_own, ncclDouble, 0, c->nccl, st));
+    }
+    NK(ncclGroupEnd());
+    if (c->rank == 0) CK(cudaMemcpyAsync(c->x_full, c->x, sizeof(double) * c->n_own, cudaMemcpyDeviceToDevice, st));
+    *full = c->x_full;
     return IRLS_OK;
 }
 
@@ -637,6 +690,9 @@ extern "C" irls_status irls_mincut_create_stencil(irls_ctx **out, const irls_com
             c->n_fin = count_nonempty(c->K, g0, g1);
             c->lo_ghost = c->world > 1 && c->rank > 0;
             c->hi_ghost = c->world > 1 && c->rank < c->world - 1;
+            if (c->world > 1) s = irls_halo_plan(nx, ny, nz, c->world, c->rank, &c->hplan);
+        }
+        if (!s) {
             s = alloc_solver(c, c->world > 1 ? c->P : 0);
         }
         if (!s) {
@@ -902,9 +958,11 @@ extern "C" irls_status irls_get_potentials(irls_ctx *c, double *x)
 {
     GUARD(c);
     if (c->state == 0) return fail(c, IRLS_ERR_STATE, "no potentials yet");
-    if (c->world > 1) return fail(c, IRLS_ERR_INVALID_ARGUMENT, "get_potentials: multi-GPU gather not supported");
-    if (!x) return IRLS_ERR_INVALID_ARGUMENT;
-    CK(cudaMemcpyAsync(x, c->x, sizeof(double) * c->n_own, cudaMemcpyDeviceToHost, c->stream));
+    if (c->rank == 0 && !x) return IRLS_ERR_INVALID_ARGUMENT;
+    double *full = nullptr;
+    irls_status s = gather_x(c, &full);
+    if (s) return s;
+    if (c->rank == 0) CK(cudaMemcpyAsync(x, full, sizeof(double) * c->n_glob, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return IRLS_OK;
 }
@@ -1006,11 +1064,48 @@ static irls_status alloc_sweep(irls_ctx *c)
     return IRLS_OK;
 }
 
+// Rank 0 result of the sweep, broadcast so every rank returns the same values.
+struct SweepResultMsg {
+    int64_t status, k;
+    double cut;
+};
+
+static irls_status sweep_rank0(irls_ctx *c, const double *xfull, uint8_t *side, int32_t *order, int64_t *k,
+                               double *cut_value);
+
 extern "C" irls_status irls_sweep_cut(irls_ctx *c, uint8_t *side, int32_t *order, int64_t *k, double *cut_value)
 {
     GUARD(c);
     if (c->state == 0) return fail(c, IRLS_ERR_STATE, "sweep before solve");
-    if (c->world > 1) return fail(c, IRLS_ERR_INVALID_ARGUMENT, "multi-GPU sweep: gather not implemented");
+    double *xfull = nullptr;
+    irls_status s = gather_x(c, &xfull);
+    if (s) return s;
+    SweepResultMsg msg{0, 0, 0.0};
+    if (c->rank == 0) {
+        s = sweep_rank0(c, xfull, side, order, &msg.k, &msg.cut);
+        msg.status = s;
+        if (s && s != IRLS_ERR_BAD_POTENTIAL && c->world == 1) return s;
+    }
+    if (c->world > 1) {
+        if (!c->msg_dev) {
+            c->msg_dev = dalloc<SweepResultMsg>(c, 1);
+            if (!c->msg_dev) return fail(c, IRLS_ERR_OOM, "sweep msg");
+        }
+        if (c->rank == 0)
+            CK(cudaMemcpyAsync(c->msg_dev, &msg, sizeof(msg), cudaMemcpyHostToDevice, c->stream));
+        NK(ncclBroadcast(c->msg_dev, c->msg_dev, sizeof(msg), ncclUint8, 0, c->nccl, c->stream));
+        CK(cudaMemcpyAsync(&msg, c->msg_dev, sizeof(msg), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    }
+    if (msg.status) return fail(c, (irls_status)msg.status, c->rank == 0 ? c->err : "sweep failed on rank 0");
+    if (k) *k = msg.k;
+    if (cut_value) *cut_value = msg.cut;
+    return IRLS_OK;
+}
+
+static irls_status sweep_rank0(irls_ctx *c, const double *xfull, uint8_t *side, int32_t *order, int64_t *k,
+                               double *cut_value)
+{
     cudaStream_t st = c->stream;
     const int64_t n = c->n_glob;
     irls_status s = alloc_sweep(c);
@@ -1019,7 +1114,7 @@ extern "C" irls_status irls_sweep_cut(irls_ctx *c, uint8_t *side, int32_t *order
     c->launches = 0;
     SweepBuffers &b = c->sb;
     CK(cudaMemsetAsync(b.flags, 0, sizeof(int32_t) * 4, st));
-    sweep_keys(c->x, b, st);
+    sweep_keys(xfull, b, st);
     launches++;
     int32_t *ord = sweep_sort(b, st, &launches);
     int32_t hflag = 0;

@@ -60,6 +60,11 @@ struct irls_ctx {
     int max_reports = 0;
     int *h_done = nullptr;  // pinned
 
+    // multi-GPU
+    irls_halo hplan{};
+    double *x_full = nullptr;     // rank 0: gathered potentials
+    void *msg_dev = nullptr;      // sweep result broadcast
+
     // sweep
     irls::SweepBuffers sb{};
     int32_t *order_dev = nullptr;  // points into sb.vals / vals_alt after a sweep

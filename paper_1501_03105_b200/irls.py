@@ -46,6 +46,12 @@ class irls_step_report(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_ if not k.startswith("reserved")}
 
 
+class irls_halo(C.Structure):
+    _fields_ = [("count", C.c_int64), ("n_own", C.c_int64), ("send_lo", C.c_int64), ("recv_lo", C.c_int64),
+                ("send_hi", C.c_int64), ("recv_hi", C.c_int64), ("peer_lo", C.c_int32), ("peer_hi", C.c_int32),
+                ("first_plane", C.c_int32), ("reserved", C.c_int32)]
+
+
 class irls_stats(C.Structure):
     _fields_ = [("launches", C.c_int64), ("cg_iters", C.c_int64), ("n_nonterminal", C.c_int64),
                 ("n_links", C.c_int64), ("n_local", C.c_int64)]
@@ -58,7 +64,7 @@ SYMBOLS = ["irls_options_default", "irls_nccl_unique_id", "irls_mincut_create_st
            "irls_init", "irls_step", "irls_solve", "irls_sweep_cut", "irls_get_side", "irls_set_terminal_weights",
            "irls_get_potentials", "irls_set_potentials", "irls_get_stats", "irls_time_kernel",
            "irls_mincut_destroy", "irls_status_string", "irls_last_error", "irls_plan_stencil",
-           "irls_combine_slots"]
+           "irls_halo_plan", "irls_combine_slots"]
 
 
 def lib():
@@ -93,6 +99,7 @@ def lib():
         L.irls_last_error.argtypes = [P]
         L.irls_last_error.restype = C.c_char_p
         L.irls_plan_stencil.argtypes = [C.c_int32] * 5 + [C.POINTER(C.c_int32)] * 4
+        L.irls_halo_plan.argtypes = [C.c_int32] * 5 + [C.POINTER(irls_halo)]
         L.irls_combine_slots.argtypes = [P]
         L.irls_combine_slots.restype = C.c_double
         _lib = L
@@ -150,6 +157,14 @@ def irls_plan_stencil(nx, ny, nz, world, rank):
     if rc:
         raise IrlsError(rc, "irls_plan_stencil")
     return tuple(o.value for o in out)  # z0, z1, g0, g1
+
+
+def irls_halo_plan(nx, ny, nz, world, rank) -> dict:
+    h = irls_halo()
+    rc = lib().irls_halo_plan(nx, ny, nz, world, rank, C.byref(h))
+    if rc:
+        raise IrlsError(rc, "irls_halo_plan")
+    return {k: getattr(h, k) for k, _ in h._fields_ if k != "reserved"}
 
 
 def irls_combine_slots(slots) -> float:

@@ -1,0 +1,146 @@
+"""Multi-rank host logic of the z-slab path, world_size 2 over gloo on CPU.
+
+The CUDA/NCCL data path needs GPUs; what is checked here is everything the
+ranks must agree on, using the library's own host plan functions:
+  - irls_plan_stencil: slabs tile the grid, start/end on plane boundaries and
+    own whole C3 groups;
+  - irls_halo_plan: exchanging the planned planes fills each ghost plane with
+    exactly the neighbour's boundary plane (the library's NCCL halo sends and
+    receives these offsets);
+  - slot-exact allreduce (C3 step 8): each rank contributes only the group
+    sums it owns, the cross-rank SUM is exact, and irls_combine_slots gives
+    the single-process C3 result bitwise;
+  - gather to rank 0 of the slabs reproduces the global vector.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import torch
+        import oracle
+        from paper_1501_03105_b200 import irls as I
+
+        out = {}
+        # ---- slab plans of the BASELINE grids and a small test grid
+        for dims in ((512, 512, 256), (128, 128, 128), (16, 16, 64)):
+            z0, z1, g0, g1 = I.irls_plan_stencil(*dims, world, rank)
+            plans = [None] * world
+            dist.all_gather_object(plans, (z0, z1, g0, g1))
+            out[dims] = plans
+
+        # ---- halo exchange with the library's plan
+        nx, ny, nz = 16, 16, 64
+        N, P = nx * ny * nz, nx * ny
+        glob = np.random.default_rng(7).standard_normal(N)
+        h = I.irls_halo_plan(nx, ny, nz, world, rank)
+        lo = h["first_plane"] * P
+        n_own = h["n_own"]
+        local = np.full(n_own + 2 * P, np.nan)
+        base = P  # local index 0 of the owned range
+        local[base:base + n_own] = glob[lo:lo + n_own]
+        reqs = []
+        bufs = {}
+        for side in ("lo", "hi"):
+            peer = h["peer_" + side]
+            if peer < 0:
+                continue
+            send = torch.from_numpy(local[base + h["send_" + side]: base + h["send_" + side] + h["count"]].copy())
+            bufs[side] = torch.empty(h["count"], dtype=torch.float64)
+            reqs.append(dist.isend(send, peer))
+            reqs.append(dist.irecv(bufs[side], peer))
+        for r in reqs:
+            r.wait()
+        for side, b in bufs.items():
+            off = base + h["recv_" + side]
+            local[off:off + h["count"]] = b.numpy()
+        ok_lo = h["peer_lo"] < 0 or np.array_equal(local[base - P:base], glob[lo - P:lo])
+        ok_hi = h["peer_hi"] < 0 or np.array_equal(local[base + n_own:base + n_own + P],
+                                                   glob[lo + n_own:lo + n_own + P])
+        out["halo"] = (ok_lo, ok_hi)
+
+        # ---- slot-exact allreduce of C3 group sums
+        v = np.random.default_rng(11).standard_normal(N) * 1e3
+        gs = oracle.c3_group_sums(v)
+        z0, z1, g0, g1 = I.irls_plan_stencil(nx, ny, nz, world, rank)
+        mine = np.zeros(8)
+        mine[g0:g1] = gs[g0:g1]
+        t = torch.from_numpy(mine.copy())
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        out["slots_exact"] = np.array_equal(t.numpy(), gs)
+        out["combined"] = I.irls_combine_slots(t.numpy()) == oracle.c3_sum(v)
+
+        # ---- gather of the slabs to rank 0
+        mine = torch.from_numpy(glob[lo:lo + n_own].copy())
+        if rank == 0:
+            full = np.empty(N)
+            full[lo:lo + n_own] = glob[lo:lo + n_own]
+            for r in range(1, world):
+                hr = I.irls_halo_plan(nx, ny, nz, world, r)
+                buf = torch.empty(hr["n_own"], dtype=torch.float64)
+                dist.recv(buf, r)
+                full[hr["first_plane"] * P: hr["first_plane"] * P + hr["n_own"]] = buf.numpy()
+            out["gather"] = np.array_equal(full, glob)
+        else:
+            dist.send(mine, 0)
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.fixture(scope="module")
+def results():
+    from paper_1501_03105_b200 import build
+    build.build()
+    import oracle
+    oracle.build()
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return res
+
+
+def test_slab_plans_tile_the_grid(results):
+    for dims in ((512, 512, 256), (128, 128, 128), (16, 16, 64)):
+        plans = results[0][dims]
+        assert plans == results[1][dims]
+        assert plans[0][0] == 0 and plans[-1][1] == dims[2]
+        assert plans[0][1] == plans[1][0]
+        assert [p[2:] for p in plans] == [(0, 4), (4, 8)]
+
+
+def test_halo_plan_exchange(results):
+    for r in (0, 1):
+        assert results[r]["halo"] == (True, True)
+
+
+def test_slot_exact_allreduce(results):
+    for r in (0, 1):
+        assert results[r]["slots_exact"] and results[r]["combined"]
+
+
+def test_gather_to_root(results):
+    assert results[0]["gather"]
