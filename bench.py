@@ -259,6 +259,13 @@ def main():
     t_k5 = m.irls_time_kernel(I.KERNEL_AXPY, 20)
     t_k1 = m.irls_time_kernel(I.KERNEL_ASSEMBLE, 10)
     ach = K3_BYTES_PER_NODE * n_own / (t_k3 * 1e-3) / 1e9
+    traffic = None
+    try:  # per-launch DRAM bytes of K3 from the committed ncu --set full capture (same config)
+        tj = json.load(open(os.path.join(ROOT, "profiles", "r01_k3_traffic.json")))
+        if args.config == "config4" and world == 1:
+            traffic = tj["traffic_GB_per_launch"] / (t_k3 * 1e-3)
+    except Exception:
+        pass
     kernels = {
         "K3_pspmv": {"ms": t_k3, "GBps": ach, "bytes_per_node": K3_BYTES_PER_NODE},
         "K5_axpy_jacobi": {"ms": t_k5, "GBps": K5_BYTES_PER_NODE * n_own / (t_k5 * 1e-3) / 1e9,
@@ -326,7 +333,9 @@ def main():
                    "parallelism": f"z-slab x{world}", "cut_value": cut, "k": k,
                    "cg_iter_ms_kernels": cg_iter_ms, "loop_mode": "graph" if args.loop_mode == 0 else "host"},
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                     "traffic": None, "kernel": "K3 fused p-update + SpMV + p.q (stencil)",
+                     "traffic": traffic, "traffic_note": "ncu dram__bytes_read+write per K3 launch "
+                     "(profiles/r01_k3_traffic.json) over the live K3 duration, GB/s; algorithmic bytes per launch "
+                     f"= {K3_BYTES_PER_NODE * n_own / 1e9:.3f} GB", "kernel": "K3 fused p-update + SpMV + p.q (stencil)",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks
                      else "fallback 6650 GB/s (B200_PROFILING.md)",
                      "frac_of_nominal_8TBps": ach / 8000.0, "kernels": kernels},
