@@ -1,0 +1,81 @@
+"""Full-size parity at BASELINE.json's sizes, in the configuration bench.py
+and tools/bench_configs.py time (graph loop, T=50, rtol 1e-3 preconditioned,
+cap 50, warm start):
+
+- config 2 (128^3): every x^(l), l = 0..50, and the sweep — bitwise;
+- config 3 (road-like CSR, 23.7M nodes): final x^(50), per-step iteration
+  counts and the sweep — bitwise;
+- config 4 (512x512x256, 67M nodes): x^(0) (the init solve the oracle finishes
+  in minutes) and the sweep of x^(0) — bitwise; the full 50-step trajectory is
+  checked by the invariants that hold at any size (box, sweep cut equals the
+  cut of the returned set).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from synthetic import generators as gen
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+@pytest.fixture(scope="module")
+def irls():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1501_03105_b200 import build, irls as I
+    build.build()
+    return I
+
+
+def _bitwise(a, b):
+    return np.array_equal(np.asarray(a).view(np.uint64), np.asarray(b).view(np.uint64))
+
+
+def test_config2_full_trajectory(irls):
+    spec = gen.config2()
+    m = irls.MinCut.from_spec(spec, irls.options(T=50))
+    S = oracle.Solver(oracle.Graph(spec), T=50)
+    for l in range(51):
+        rg = m.irls_init() if l == 0 else m.irls_step()
+        ro = S.init() if l == 0 else S.step()
+        assert rg["cg_iters"] == ro["cg_iters"], l
+        assert _bitwise(m.irls_get_potentials(), S.x()), l
+    side, order, k, cut = m.irls_sweep_cut(order=True)
+    sw = S.sweep()
+    assert k == sw.k and cut == sw.cut_value
+    assert np.array_equal(side, sw.side) and np.array_equal(order.astype(np.int64), sw.order)
+
+
+def test_config3_full_csr(irls):
+    spec = gen.config3()
+    m = irls.MinCut.from_spec(spec, irls.options(T=50))
+    reps, total = m.irls_solve(irls.IRLS_FROM_SCRATCH, T=50)
+    S = oracle.Solver(oracle.Graph(spec), T=50)
+    _, oreps = S.run(record=False)
+    assert [r["cg_iters"] for r in reps] == [r["cg_iters"] for r in oreps]
+    assert _bitwise(m.irls_get_potentials(), S.x())
+    side, _, k, cut = m.irls_sweep_cut()
+    sw = S.sweep()
+    assert k == sw.k and cut == sw.cut_value and np.array_equal(side, sw.side)
+
+
+def test_config4_init_and_invariants(irls):
+    spec = gen.config4()
+    m = irls.MinCut.from_spec(spec, irls.options(T=50))
+    r0 = m.irls_init()
+    S = oracle.Solver(oracle.Graph(spec), T=0)
+    ro = S.init()
+    assert r0["cg_iters"] == ro["cg_iters"]
+    assert _bitwise(m.irls_get_potentials(), S.x())
+    side, _, k, cut = m.irls_sweep_cut()
+    sw = S.sweep()
+    assert k == sw.k and cut == sw.cut_value and np.array_equal(side, sw.side)
+    del S
+    # full run: invariants at full size
+    reps, total = m.irls_solve(irls.IRLS_FROM_SCRATCH, T=50)
+    x = m.irls_get_potentials()
+    assert x.min() > -1e-2 and x.max() < 1 + 1e-2  # box up to the loose CG tolerance (A21)
+    side, _, k, cut = m.irls_sweep_cut()
+    assert side[-2] == 1 and side[-1] == 0 and int(side[:-2].sum()) == k
