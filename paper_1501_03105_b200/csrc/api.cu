@@ -234,6 +234,7 @@ static SellArgs sell_args(const irls_ctx *c)
     s.g = c->gsell;
     s.cs = c->cs;
     s.ct = c->ct;
+    s.wmax = c->sell_wmax;
     return s;
 }
 
@@ -851,22 +852,26 @@ extern "C" irls_status irls_mincut_create_csr(irls_ctx **out, const irls_comm_de
             if (!anchored) return IRLS_ERR_SINGULAR;
         }
     }
-    // SELL-32 (slices of 32 consecutive rows, column-major inside a slice)
-    const int64_t nsl = (nr + 31) / 32;
+    // SELL-64 (slices of 64 consecutive rows, column-major inside a slice: the
+    // k-th neighbour of rows 2t and 2t+1 are adjacent, one 128-bit load)
+    const int64_t nsl = (nr + kSell - 1) / kSell;
     std::vector<int64_t> sptr(nsl + 1, 0);
+    int64_t sell_wmax = 0;
     for (int64_t sl = 0; sl < nsl; sl++) {
         int64_t wmax = 0;
-        for (int64_t r = sl * 32; r < std::min<int64_t>(nr, sl * 32 + 32); r++) wmax = std::max(wmax, aptr[r + 1] - aptr[r]);
-        sptr[sl + 1] = sptr[sl] + 32 * wmax;
+        for (int64_t r = sl * kSell; r < std::min<int64_t>(nr, sl * kSell + kSell); r++)
+            wmax = std::max(wmax, aptr[r + 1] - aptr[r]);
+        sptr[sl + 1] = sptr[sl] + kSell * wmax;
+        sell_wmax = std::max(sell_wmax, wmax);
     }
     const int64_t nent = sptr[nsl];
     std::vector<int32_t> scol(std::max<int64_t>(nent, 1), -1);
     std::vector<double> scap(std::max<int64_t>(nent, 1), 0.0);
     for (int64_t r = 0; r < nr; r++) {
-        const int64_t sl = r >> 5, ln = r & 31;
+        const int64_t sl = r / kSell, ln = r % kSell;
         for (int64_t k = 0; k < aptr[r + 1] - aptr[r]; k++) {
-            scol[sptr[sl] + 32 * k + ln] = aidx[aptr[r] + k];
-            scap[sptr[sl] + 32 * k + ln] = ac[aptr[r] + k];
+            scol[sptr[sl] + kSell * k + ln] = aidx[aptr[r] + k];
+            scap[sptr[sl] + kSell * k + ln] = ac[aptr[r] + k];
         }
     }
     irls_ctx *c = new irls_ctx();
@@ -888,6 +893,7 @@ extern "C" irls_status irls_mincut_create_csr(irls_ctx **out, const irls_comm_de
         c->n_links = (int64_t)aidx.size() / 2;
         c->F = compute_F(cmax, cnt);
         c->n_entries = nent;
+        c->sell_wmax = (int32_t)sell_wmax;
         st = alloc_solver(c, 0);
     }
     if (!st) {
@@ -1015,11 +1021,11 @@ extern "C" irls_status irls_set_terminal_weights(irls_ctx *c, const double *cs, 
         memcpy_sync(c, cp.data(), c->cap, sizeof(double) * c->n_entries, cudaMemcpyDeviceToHost);
         memcpy_sync(c, cl.data(), c->col, sizeof(int32_t) * c->n_entries, cudaMemcpyDeviceToHost);
         // each n-link appears twice (both rows): count once via v > u
-        std::vector<int64_t> sp((c->n_glob + 31) / 32 + 1);
+        std::vector<int64_t> sp((c->n_glob + kSell - 1) / kSell + 1);
         memcpy_sync(c, sp.data(), c->slice_ptr, sizeof(int64_t) * sp.size(), cudaMemcpyDeviceToHost);
         for (int64_t sl = 0; sl + 1 < (int64_t)sp.size(); sl++)
             for (int64_t e = sp[sl]; e < sp[sl + 1]; e++) {
-                const int64_t u = sl * 32 + ((e - sp[sl]) & 31);
+                const int64_t u = sl * kSell + ((e - sp[sl]) % kSell);
                 if (cl[e] > u) { cnt++; cmax = std::max(cmax, cp[e]); }
             }
         c->F = compute_F(cmax, cnt);

@@ -16,6 +16,7 @@ constexpr int kChunk = 4096;    // C3 chunk: 256 threads x 8 rounds x double2
 constexpr int kThreads = 256;
 constexpr int kGroups = 8;
 constexpr int kMaxQ = 5;
+constexpr int kSell = 64;     // SELL slice height: thread t's rows 2t, 2t+1 hold adjacent slots
 
 // ---------------------------------------------------------------------------
 // Fast unsigned division for n < 2^31, d < 2^31: q = (n * m) >> sh with

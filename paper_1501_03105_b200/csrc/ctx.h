@@ -53,6 +53,7 @@ struct irls_ctx {
     int32_t *col = nullptr;
     double *cap = nullptr, *gsell = nullptr;
     int64_t n_entries = 0;
+    int32_t sell_wmax = 0;
 
     irls::DevCtrl *ctrl = nullptr;
     double *part = nullptr, *slots_local = nullptr, *slots_glob = nullptr;

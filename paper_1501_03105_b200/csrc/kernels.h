@@ -35,11 +35,12 @@ struct StencilArgs {
 
 struct SellArgs {
     int64_t n;                   // rows
-    const int64_t *slice_ptr;    // [nslices+1] entry offsets (multiples of 32)
+    const int64_t *slice_ptr;    // [nslices+1] entry offsets (multiples of kSell)
     const int32_t *col;          // -1 = padding (always after the real entries)
     const double *c;             // capacities
     double *g;                   // conductances
     const double *cs, *ct;
+    int32_t wmax;                // widest slice (max degree)
 };
 
 struct CondArgs {
@@ -94,6 +95,10 @@ void launch_pair_pspmv(const StencilArgs &s, const VecArgs &v, const RedArgs &ra
                        cudaStream_t st);
 void launch_pair_axpy(const VecArgs &v, const RedArgs &ra, const CondArgs &cd, cudaStream_t st);
 void launch_pair_finish(const VecArgs &v, DevCtrl *ctrl, cudaStream_t st);
+// sell_pair.cu (widest slice <= 8): false when the generic SELL kernel must run
+bool launch_sellp_assemble(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, int mode,
+                           double eps, double *gs_out, double *gt_out, cudaStream_t st);
+bool launch_sellp_pspmv(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, cudaStream_t st);
 
 // ---------------------------------------------------------------------------
 // Sweep cut (K8-K12)

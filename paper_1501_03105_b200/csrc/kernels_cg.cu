@@ -134,13 +134,13 @@ __global__ void __launch_bounds__(kThreads) k_sell_assemble(SellArgs s, VecArgs 
 {
     double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     FOR_CHUNK_NODES({
-        const int64_t sl = u >> 5;
-        const int64_t e0 = s.slice_ptr[sl] + (u & 31);
-        const int32_t W = (int32_t)((s.slice_ptr[sl + 1] - s.slice_ptr[sl]) >> 5);
+        const int64_t sl = u / kSell;
+        const int64_t e0 = s.slice_ptr[sl] + (u % kSell);
+        const int32_t W = (int32_t)((s.slice_ptr[sl + 1] - s.slice_ptr[sl]) / kSell);
         const double xu = MODE == ASM_INIT ? 0.0 : v.x[u];
         double a = 0.0, a2 = 0.0;
         for (int32_t k = 0; k < W; k++) {
-            const int64_t idx = e0 + 32 * (int64_t)k;
+            const int64_t idx = e0 + kSell * (int64_t)k;
             const int32_t nb = s.col[idx];
             if (nb < 0) break;
             const double c = s.c[idx];
@@ -230,13 +230,13 @@ __global__ void __launch_bounds__(kThreads) k_sell_pspmv(SellArgs s, VecArgs v, 
     double acc[1] = {0.0};
 #define PVAL(w) (first ? zv[w] : zv[w] + beta * pold[w])
     FOR_CHUNK_NODES({
-        const int64_t sl = u >> 5;
-        const int64_t e0 = s.slice_ptr[sl] + (u & 31);
-        const int32_t W = (int32_t)((s.slice_ptr[sl + 1] - s.slice_ptr[sl]) >> 5);
+        const int64_t sl = u / kSell;
+        const int64_t e0 = s.slice_ptr[sl] + (u % kSell);
+        const int32_t W = (int32_t)((s.slice_ptr[sl + 1] - s.slice_ptr[sl]) / kSell);
         const double pu = PVAL(u);
         double a = 0.0;
         for (int32_t kk = 0; kk < W; kk++) {
-            const int64_t idx = e0 + 32 * (int64_t)kk;
+            const int64_t idx = e0 + kSell * (int64_t)kk;
             const int32_t nb = s.col[idx];
             if (nb < 0) break;
             a = a + s.g[idx] * PVAL(nb);
@@ -403,15 +403,15 @@ __global__ void __launch_bounds__(kThreads) k_sell_diag(SellArgs s, VecArgs v, R
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     double mn = INFINITY, mx = -INFINITY;
     FOR_CHUNK_NODES({
-        const int64_t sl = u >> 5;
-        const int64_t e0 = s.slice_ptr[sl] + (u & 31);
-        const int32_t W = (int32_t)((s.slice_ptr[sl + 1] - s.slice_ptr[sl]) >> 5);
+        const int64_t sl = u / kSell;
+        const int64_t e0 = s.slice_ptr[sl] + (u % kSell);
+        const int32_t W = (int32_t)((s.slice_ptr[sl + 1] - s.slice_ptr[sl]) / kSell);
         const double xu = v.x[u];
         mn = fmin(mn, xu);
         mx = fmax(mx, xu);
         double Se = 0.0, fl = 0.0, a2 = 0.0;
         for (int32_t k = 0; k < W; k++) {
-            const int64_t idx = e0 + 32 * (int64_t)k;
+            const int64_t idx = e0 + kSell * (int64_t)k;
             const int32_t nb = s.col[idx];
             if (nb < 0) break;
             const double xv = v.x[nb];
@@ -484,6 +484,7 @@ void launch_sell_assemble(const SellArgs &s, const VecArgs &v, const RedArgs &ra
 int launch_sell_assemble_ex(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, int mode,
                              double eps, double *gs_out, double *gt_out, cudaStream_t st)
 {
+    if (launch_sellp_assemble(s, v, ra, cd, mode, eps, gs_out, gt_out, st)) return 1;
     const double eps2 = eps * eps;
     const unsigned nb = nblocks(v.n_own);
     if (mode == ASM_INIT) k_sell_assemble<ASM_INIT><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
@@ -502,6 +503,7 @@ void launch_stencil_pspmv(const StencilArgs &s, const VecArgs &v, const RedArgs 
 
 void launch_sell_pspmv(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, cudaStream_t st)
 {
+    if (launch_sellp_pspmv(s, v, ra, cd, st)) return;
     k_sell_pspmv<<<nblocks(v.n_own), kThreads, 0, st>>>(s, v, ra, cd);
 }
 

@@ -44,6 +44,20 @@ __device__ __forceinline__ PairCoord pair_coord(const StencilArgs &s, int64_t ug
     return c;
 }
 
+// Terminal conductances gs = rw(cs, 1 - x), gt = rw(ct, x) (Eq. 4/8, A3).
+// Most nodes have exactly one positive terminal capacity; computing that one
+// first keeps the warp convergent (one sqrt + div for every lane) and the
+// second pair only runs for nodes with both.  Same formula, same bits.
+__device__ __forceinline__ double terminal_g(double cs, double ct, double x, double eps2, double &gt)
+{
+    const bool s_first = cs > 0.0;
+    const double g1 = rw_g(s_first ? cs : ct, s_first ? 1.0 - x : x, eps2);
+    double gs = s_first ? g1 : 0.0;
+    gt = s_first ? 0.0 : g1;
+    if (s_first && ct > 0.0) gt = rw_g(ct, x, eps2);
+    return gs;
+}
+
 __device__ __forceinline__ void set_cond2(const CondArgs &cd, const DevCtrl *c)
 {
     if (cd.use) cudaGraphSetConditional(cd.handle, c->done ? 0u : 1u);
@@ -153,8 +167,8 @@ __global__ void __launch_bounds__(kThreads) k_pair_nodes(StencilArgs s, VecArgs 
             gs2 = cs2;
             gt2 = ct2;
         } else {
-            gs2 = make_double2(rw_g(cs2.x, 1.0 - x2.x, eps2), rw_g(cs2.y, 1.0 - x2.y, eps2));
-            gt2 = make_double2(rw_g(ct2.x, x2.x, eps2), rw_g(ct2.y, x2.y, eps2));
+            gs2.x = terminal_g(cs2.x, ct2.x, x2.x, eps2, gt2.x);
+            gs2.y = terminal_g(cs2.y, ct2.y, x2.y, eps2, gt2.y);
         }
         // O1, ascending (-z, -y, -x, +x, +y, +z); absent terms are +0.0
         const double D0 = ((((((0.0 + gzm.x) + gym.x) + gxl) + gx2.x) + gy2.x) + gz2.x + gs2.x) + gt2.x;

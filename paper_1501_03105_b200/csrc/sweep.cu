@@ -350,13 +350,13 @@ __global__ void __launch_bounds__(256) k_delta_sell(SellArgs s, int32_t F, const
     for (int r = 0; r < 16; r++) {
         const int64_t v = base + r * 256 + threadIdx.x;
         if (v >= s.n) break;
-        const int64_t sl = v >> 5;
-        const int64_t e0 = s.slice_ptr[sl] + (v & 31);
-        const int32_t W = (int32_t)((s.slice_ptr[sl + 1] - s.slice_ptr[sl]) >> 5);
+        const int64_t sl = v / kSell;
+        const int64_t e0 = s.slice_ptr[sl] + (v % kSell);
+        const int32_t W = (int32_t)((s.slice_ptr[sl + 1] - s.slice_ptr[sl]) / kSell);
         const int32_t rv = rank[v];
         i128 d = 0;
         for (int32_t k = 0; k < W; k++) {
-            const int64_t idx = e0 + 32 * (int64_t)k;
+            const int64_t idx = e0 + kSell * (int64_t)k;
             const int32_t nb = s.col[idx];
             if (nb < 0) break;
             const i128 q = qfix(s.c[idx], F);
@@ -573,12 +573,12 @@ __global__ void __launch_bounds__(kThreads) k_side_cross_sell(SellArgs s, const 
             side[orig[v]] = in ? 1 : 0;
             double cr;
             if (in) {
-                const int64_t sl = v >> 5;
-                const int64_t e0 = s.slice_ptr[sl] + (v & 31);
-                const int32_t W = (int32_t)((s.slice_ptr[sl + 1] - s.slice_ptr[sl]) >> 5);
+                const int64_t sl = v / kSell;
+                const int64_t e0 = s.slice_ptr[sl] + (v % kSell);
+                const int32_t W = (int32_t)((s.slice_ptr[sl + 1] - s.slice_ptr[sl]) / kSell);
                 double a = 0.0;
                 for (int32_t kk = 0; kk < W; kk++) {
-                    const int64_t idx = e0 + 32 * (int64_t)kk;
+                    const int64_t idx = e0 + kSell * (int64_t)kk;
                     const int32_t nb = s.col[idx];
                     if (nb < 0) break;
                     if (rank[nb] >= k) a = a + s.c[idx];
