@@ -127,6 +127,15 @@ def test_blob_grid_ragged(irls, loop_mode):
     check_sweep(m, S)
 
 
+@pytest.mark.parametrize("dims", [(64, 64, 20), (128, 64, 9), (128, 32, 6)])
+def test_blob_grid_chunk_planes(irls, dims):
+    """Planes that are whole C3 chunks (the geometry of configs 2, 4, 5)."""
+    spec = gen.blob_grid(*dims, seed=3, sigma=(3.0, 10.0))
+    m, S = lockstep(irls, spec, T=30, record=True)
+    check_sweep(m, S)
+    m2, S2 = lockstep(irls, spec, T=6, warm=False)
+
+
 def test_blob_grid_cold_start(irls):
     spec = gen.blob_grid(24, 20, 18, seed=7, sigma=(2.0, 6.0))
     m, S = lockstep(irls, spec, T=12, warm=False, record=True)
