@@ -103,16 +103,25 @@ __global__ void __launch_bounds__(256) k_tile_hist(const u64 *keys, int64_t n, i
     tile_hist[(int64_t)threadIdx.x * ntiles + blockIdx.x] = (int32_t)h[threadIdx.x];
 }
 
-// Stable scatter: warp w owns keys [base + 512 w, +512) in 16 rounds of 32.
+// Stable scatter.  Warp w owns keys [base + 512 w, +512) in 16 rounds of 32.
+// The tile is first ranked (stable, match_any per round) and staged in shared
+// memory in digit order, then written out so that consecutive threads write
+// consecutive positions of one bucket (coalesced runs instead of isolated
+// 8-byte writes).
 __global__ void __launch_bounds__(256) k_radix_scatter(const u64 *keys, const int32_t *vals, u64 *okeys,
                                                        int32_t *ovals, int64_t n, int shift,
                                                        const int32_t *tile_off, int64_t ntiles)
 {
-    __shared__ int32_t wh[8][256];
+    __shared__ int32_t wh[8][256];     // per-warp digit counts, then per-warp running tile positions
+    __shared__ int32_t gdelta[256];    // global start of the bucket minus its tile-local start
+    extern __shared__ __align__(16) unsigned char radix_dyn[];  // kTile keys + kTile values
+    u64 *skey = reinterpret_cast<u64 *>(radix_dyn);
+    int32_t *sval = reinterpret_cast<int32_t *>(radix_dyn + sizeof(u64) * kTile);
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < 8 * 256; i += 256) (&wh[0][0])[i] = 0;
     __syncthreads();
-    const int64_t base = (int64_t)blockIdx.x * kTile + w * 512;
+    const int64_t tbase = (int64_t)blockIdx.x * kTile;
+    const int64_t base = tbase + w * 512;
     u64 k[16];
     int32_t vv[16];
     int dig[16];
@@ -137,9 +146,26 @@ __global__ void __launch_bounds__(256) k_radix_scatter(const u64 *keys, const in
         __syncwarp();
     }
     __syncthreads();
+    // digit d (one per thread): tile total, exclusive scan over digits, per-warp starts
+    const int d = threadIdx.x;
+    int32_t tot = 0;
+#pragma unroll
+    for (int w2 = 0; w2 < 8; w2++) tot += wh[w2][d];
     {
-        const int d = threadIdx.x;
-        int32_t run = tile_off[(int64_t)d * ntiles + blockIdx.x];
+        int32_t inc = tot;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int32_t o = __shfl_up_sync(0xffffffffu, inc, off);
+            if (lane >= off) inc += o;
+        }
+        __shared__ int32_t wsum[8];
+        if (lane == 31) wsum[w] = inc;
+        __syncthreads();
+        int32_t pre = 0;
+        for (int i = 0; i < w; i++) pre += wsum[i];
+        const int32_t ex = pre + inc - tot;
+        gdelta[d] = tile_off[(int64_t)d * ntiles + blockIdx.x] - ex;
+        int32_t run = ex;
 #pragma unroll
         for (int w2 = 0; w2 < 8; w2++) {
             const int32_t c = wh[w2][d];
@@ -150,17 +176,26 @@ __global__ void __launch_bounds__(256) k_radix_scatter(const u64 *keys, const in
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < 16; r++) {
-        const int d = dig[r];
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const int dd = dig[r];
+        const unsigned peers = __match_any_sync(0xffffffffu, dd);
         int32_t pos = 0;
-        if (d >= 0) pos = wh[w][d] + __popc(peers & lt);
+        if (dd >= 0) pos = wh[w][dd] + __popc(peers & lt);
         __syncwarp();
-        if (d >= 0) {
-            okeys[pos] = k[r];
-            ovals[pos] = vv[r];
-            if ((peers & lt) == 0u) wh[w][d] += __popc(peers);
+        if (dd >= 0) {
+            skey[pos] = k[r];
+            sval[pos] = vv[r];
+            if ((peers & lt) == 0u) wh[w][dd] += __popc(peers);
         }
         __syncwarp();
+    }
+    __syncthreads();
+    const int32_t cnt = (int32_t)(n - tbase < kTile ? n - tbase : kTile);
+    for (int i = threadIdx.x; i < cnt; i += 256) {
+        const u64 key = skey[i];
+        const int dd = (int)((key >> shift) & 255u);
+        const int64_t g = (int64_t)gdelta[dd] + i;
+        okeys[g] = key;
+        ovals[g] = sval[i];
     }
 }
 
@@ -273,7 +308,13 @@ int32_t *sweep_sort(SweepBuffers &b, cudaStream_t st, int *launches)
         if (trivial) continue;
         k_tile_hist<<<(unsigned)nt, 256, 0, st>>>(ka, n, 8 * d, b.tile_hist, nt);
         exclusive_scan_i32(b.tile_hist, 256 * nt, b.tile_off, (int64_t *)b.scan_tmp, st, launches);
-        k_radix_scatter<<<(unsigned)nt, 256, 0, st>>>(ka, va, kb, vb, n, 8 * d, b.tile_off, nt);
+        const int dyn = (int)((sizeof(u64) + sizeof(int32_t)) * kTile);
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_radix_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+            attr = true;
+        }
+        k_radix_scatter<<<(unsigned)nt, 256, dyn, st>>>(ka, va, kb, vb, n, 8 * d, b.tile_off, nt);
         *launches += 2;
         std::swap(ka, kb);
         std::swap(va, vb);
@@ -337,7 +378,7 @@ __global__ void __launch_bounds__(256) k_delta_stencil(StencilArgs s, int64_t N,
         d += qfix(s.ct[v], F);
         d -= qs;
         qcs += qs;
-        delta[rv] = d;
+        delta[v] = d;  // id order (coalesced); gathered into sweep order later
     }
     tile_sum_i128(qcs, qcs_tile + blockIdx.x);
 }
@@ -366,21 +407,34 @@ __global__ void __launch_bounds__(256) k_delta_sell(SellArgs s, int32_t F, const
         d += qfix(s.ct[v], F);
         d -= qs;
         qcs += qs;
-        delta[rv] = d;
+        delta[v] = d;
     }
     tile_sum_i128(qcs, qcs_tile + blockIdx.x);
+}
+
+// delta in sweep order: ds[i] = delta[order[i]] (random 16-byte reads, coalesced writes)
+__global__ void k_delta_gather(const i128 *delta, const int32_t *order, int64_t n, i128 *ds)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) ds[i] = delta[order[i]];
+}
+
+void sweep_delta_order(const int32_t *order, SweepBuffers &b, cudaStream_t st)
+{
+    if (b.n == 0) return;
+    k_delta_gather<<<(unsigned)((b.n + 255) / 256), 256, 0, st>>>(b.delta_id, order, b.n, b.delta);
 }
 
 void sweep_delta_stencil(const StencilArgs &s, int64_t N, int32_t F, SweepBuffers &b, cudaStream_t st)
 {
     if (N == 0) return;
-    k_delta_stencil<<<(unsigned)sweep_ntiles(N), 256, 0, st>>>(s, N, F, b.rank, b.delta, b.tile_min);
+    k_delta_stencil<<<(unsigned)sweep_ntiles(N), 256, 0, st>>>(s, N, F, b.rank, b.delta_id, b.tile_min);
 }
 
 void sweep_delta_sell(const SellArgs &s, int32_t F, SweepBuffers &b, cudaStream_t st)
 {
     if (s.n == 0) return;
-    k_delta_sell<<<(unsigned)sweep_ntiles(s.n), 256, 0, st>>>(s, F, b.rank, b.delta, b.tile_min);
+    k_delta_sell<<<(unsigned)sweep_ntiles(s.n), 256, 0, st>>>(s, F, b.rank, b.delta_id, b.tile_min);
 }
 
 // ---------------------------------------------------------------------------
