@@ -183,6 +183,25 @@ void irls_mincut_destroy(irls_ctx *ctx);
 const char *irls_status_string(irls_status st);
 const char *irls_last_error(const irls_ctx *ctx);
 
+/* ---- virtual groups: the multi-GPU data path on ONE device --------------- */
+/* All `world` ranks of the z-slab partition of one grid, driven by one host
+ * thread on one device and one stream, phase by phase (every rank's kernel,
+ * then the collective, ...); halo exchange, slot allreduce and gather are
+ * device copies instead of NCCL.  Everything else — slabs, ghost planes,
+ * per-rank reductions, ghost p updates, finalize kernels, rank-0 sweep — is
+ * the multi-GPU code.  Used to test that path without several GPUs; results
+ * are bitwise those of world 1.  world must divide 8 and the slabs must be
+ * group-aligned (see irls_plan_stencil). */
+typedef struct irls_vgroup irls_vgroup;
+irls_status irls_vgroup_create_stencil(irls_vgroup **g, int32_t world, int32_t device, int32_t nx, int32_t ny,
+                                       int32_t nz, const double *cx, const double *cy, const double *cz,
+                                       const double *cs, const double *ct, const irls_options *opt);
+irls_status irls_vgroup_solve(irls_vgroup *g, int32_t mode, irls_step_report *per_step, int64_t *total_cg_iters);
+irls_status irls_vgroup_sweep_cut(irls_vgroup *g, uint8_t *side, int32_t *order, int64_t *k, double *cut_value);
+irls_status irls_vgroup_get_potentials(irls_vgroup *g, double *x);
+irls_status irls_vgroup_set_terminal_weights(irls_vgroup *g, const double *cs, const double *ct);
+void irls_vgroup_destroy(irls_vgroup *g);
+
 /* ---- host-only helpers of the multi-GPU plan (no device work) ----------- */
 /* C3 groups of a length-n index space: chunk count K = ceil(n/4096); group g
  * covers chunks [floor(gK/8), floor((g+1)K/8)). */

@@ -295,6 +295,20 @@ static irls_status halo(irls_ctx *c, double *arr, cudaStream_t st)
     return IRLS_OK;
 }
 
+// Virtual group: rank 0's x_full <- every rank's slab (device copies).
+static irls_status vgather_x(irls_vgroup *g, double **full)
+{
+    irls_ctx *c = g->ranks[0];
+    if (!c->x_full) {
+        c->x_full = dalloc<double>(c, c->n_glob);
+        if (!c->x_full) return fail(c, IRLS_ERR_OOM, "x_full");
+    }
+    for (irls_ctx *d : g->ranks)
+        CK(cudaMemcpyAsync(c->x_full + d->lo, d->x, sizeof(double) * d->n_own, cudaMemcpyDeviceToDevice, g->stream));
+    *full = c->x_full;
+    return IRLS_OK;
+}
+
 // Rank 0 receives every slab of x (Algorithm 1 step 5: "Gather the
 // voltage vector to the root process"); returns the full vector's pointer on
 // rank 0 (the local x when world == 1).
@@ -332,91 +346,164 @@ static irls_status allreduce_slots(irls_ctx *c, int nq, cudaStream_t st)
 }
 
 // ---------------------------------------------------------------------------
-// enqueue pieces of one solve
+// Collectives over the ranks a host thread drives: one rank with NCCL (one
+// process per GPU), or every rank of a virtual group (one process, one device,
+// one stream; the same data movement done with device copies).
 // ---------------------------------------------------------------------------
-static irls_status enq_assemble(irls_ctx *c, int mode, const CondArgs &cd, cudaStream_t st)
+typedef std::vector<irls_ctx *> Ranks;
+
+static irls_status coll_halo(Ranks &R, bool z_not_x, cudaStream_t st)
 {
-    const VecArgs v = vec_args(c);
-    const RedArgs ra = red_args(c);
-    if (c->kind == 0) {
-        if (mode != ASM_INIT) {
-            irls_status s = halo(c, c->x, st);
-            if (s) return s;
+    irls_ctx *c = R[0];
+    if (c->world == 1) return IRLS_OK;
+    if (!c->vg) return halo(c, z_not_x ? c->z : c->x, st);
+    for (irls_ctx *d : R) {
+        const irls_halo &h = d->hplan;
+        double *arr = z_not_x ? d->z : d->x;
+        const size_t bytes = sizeof(double) * (size_t)h.count;
+        if (h.peer_lo >= 0) {
+            irls_ctx *o = R[h.peer_lo];
+            CK(cudaMemcpyAsync(arr + h.recv_lo, (z_not_x ? o->z : o->x) + o->hplan.send_hi, bytes,
+                               cudaMemcpyDeviceToDevice, st));
         }
-        c->launches +=
-            launch_stencil_assemble_ex(stencil_args(c, false), v, ra, cd, mode, c->opt.eps, c->gs_diag, c->gt_diag, st);
-    } else {
-        c->launches += launch_sell_assemble_ex(sell_args(c), v, ra, cd, mode, c->opt.eps, c->gs_diag, c->gt_diag, st);
+        if (h.peer_hi >= 0) {
+            irls_ctx *o = R[h.peer_hi];
+            CK(cudaMemcpyAsync(arr + h.recv_hi, (z_not_x ? o->z : o->x) + o->hplan.send_lo, bytes,
+                               cudaMemcpyDeviceToDevice, st));
+        }
     }
-    if (c->world > 1) {
-        irls_status s = allreduce_slots(c, 5, st);
-        if (s) return s;
-        launch_finalize(PH_START, c->ctrl, c->slots_glob, cd, st);
-        c->launches++;
-        s = halo(c, c->z, st);
-        if (s) return s;
-    }
-    return last_launch(c, "assemble");
+    return IRLS_OK;
 }
 
-static irls_status enq_body(irls_ctx *c, const CondArgs &cd, cudaStream_t st)
+static irls_status coll_allreduce(Ranks &R, int nq, cudaStream_t st)
 {
-    const VecArgs v = vec_args(c);
-    const RedArgs ra = red_args(c);
-    if (c->kind == 0) launch_stencil_pspmv(stencil_args(c, false), v, ra, cd, st);
-    else launch_sell_pspmv(sell_args(c), v, ra, cd, st);
-    c->launches++;
-    if (c->world > 1) {
-        launch_ghost_pupdate(v, c->lo_ghost, c->hi_ghost, c->P, c->ctrl, st);
-        irls_status s = allreduce_slots(c, 1, st);
-        if (s) return s;
-        launch_finalize(PH_PQ, c->ctrl, c->slots_glob, cd, st);
-        c->launches += 2;
-    }
-    launch_axpy_jacobi(v, ra, cd, st);
-    c->launches++;
-    if (c->world > 1) {
-        irls_status s = allreduce_slots(c, 3, st);
-        if (s) return s;
-        launch_finalize(PH_RZ, c->ctrl, c->slots_glob, cd, st);
-        c->launches++;
-        s = halo(c, c->z, st);
-        if (s) return s;
-    }
-    return last_launch(c, "cg body");
+    irls_ctx *c = R[0];
+    if (c->world == 1) return IRLS_OK;
+    if (!c->vg) return allreduce_slots(c, nq, st);
+    // sum of every rank's slots in rank order (each slot has one non-zero
+    // contributor, so this is the same exact value NCCL's sum produces)
+    launch_vsum(c->vg->src_slots, (int)R.size(), nq * kGroups, R[0]->slots_glob, st);
+    for (size_t r = 1; r < R.size(); r++)
+        CK(cudaMemcpyAsync(R[r]->slots_glob, R[0]->slots_glob, sizeof(double) * nq * kGroups,
+                           cudaMemcpyDeviceToDevice, st));
+    return IRLS_OK;
 }
 
-static irls_status enq_tail(irls_ctx *c, cudaStream_t st)
+// x range of the diagnostics: min / max of the order-preserving keys.
+static irls_status coll_minmax(Ranks &R, cudaStream_t st)
 {
-    const VecArgs v = vec_args(c);
-    launch_finish(v, c->ctrl, st);
-    launch_report(c->ctrl, c->reports, st);
-    c->launches += 2;
-    if (c->opt.record_trace) {
-        if (c->world > 1) {
-            irls_status s = halo(c, c->x, st);
-            if (s) return s;
-        }
+    irls_ctx *c = R[0];
+    if (c->world == 1) return IRLS_OK;
+    if (!c->vg) {
+        NK(ncclGroupStart());
+        NK(ncclAllReduce(&c->ctrl->xmin_key, &c->ctrl->xmin_key, 1, ncclUint64, ncclMin, c->nccl, st));
+        NK(ncclAllReduce(&c->ctrl->xmax_key, &c->ctrl->xmax_key, 1, ncclUint64, ncclMax, c->nccl, st));
+        NK(ncclGroupEnd());
+        return IRLS_OK;
+    }
+    launch_vminmax(c->vg->src_ctrl, (int)R.size(), st);
+    return IRLS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// enqueue pieces of one solve (over the ranks this thread drives)
+// ---------------------------------------------------------------------------
+static irls_status enq_assemble(Ranks &R, int mode, const CondArgs &cd, cudaStream_t st)
+{
+    irls_status s;
+    if (R[0]->kind == 0 && mode != ASM_INIT && (s = coll_halo(R, false, st))) return s;
+    for (irls_ctx *c : R) {
+        const VecArgs v = vec_args(c);
         const RedArgs ra = red_args(c);
         if (c->kind == 0)
-            launch_stencil_diag_ex(stencil_args(c, false), v, ra, c->opt.eps, c->opt.cg_norm, c->gs_diag, c->gt_diag, st);
+            c->launches += launch_stencil_assemble_ex(stencil_args(c, false), v, ra, cd, mode, c->opt.eps, c->gs_diag,
+                                                      c->gt_diag, st);
         else
-            launch_sell_diag_ex(sell_args(c), v, ra, c->opt.eps, c->opt.cg_norm, c->gs_diag, c->gt_diag, st);
-        if (c->world > 1) {
-            irls_status s = allreduce_slots(c, 4, st);
-            if (s) return s;
-        }
-        launch_diag_finalize(c->ctrl, c->slots_glob, c->reports, c->opt.cg_norm, st);
-        c->launches += 2;
+            c->launches += launch_sell_assemble_ex(sell_args(c), v, ra, cd, mode, c->opt.eps, c->gs_diag, c->gt_diag, st);
     }
-    return last_launch(c, "tail");
+    if (R[0]->world > 1) {
+        if ((s = coll_allreduce(R, 5, st))) return s;
+        for (irls_ctx *c : R) {
+            launch_finalize(PH_START, c->ctrl, c->slots_glob, cd, st);
+            c->launches++;
+        }
+        if ((s = coll_halo(R, true, st))) return s;
+    }
+    return last_launch(R[0], "assemble");
 }
 
-// Per-solve CUDA graph: [x = 0] -> K1 (sets the WHILE condition) -> [x = 0]
-// -> WHILE { K3 ; K5 (sets the condition) } -> finish -> report [-> diag].
+static irls_status enq_body(Ranks &R, const CondArgs &cd, cudaStream_t st)
+{
+    irls_status s;
+    for (irls_ctx *c : R) {
+        const VecArgs v = vec_args(c);
+        const RedArgs ra = red_args(c);
+        if (c->kind == 0) launch_stencil_pspmv(stencil_args(c, false), v, ra, cd, st);
+        else launch_sell_pspmv(sell_args(c), v, ra, cd, st);
+        c->launches++;
+        if (c->world > 1) {
+            launch_ghost_pupdate(v, c->lo_ghost, c->hi_ghost, c->P, c->ctrl, st);
+            c->launches++;
+        }
+    }
+    if (R[0]->world > 1) {
+        if ((s = coll_allreduce(R, 1, st))) return s;
+        for (irls_ctx *c : R) {
+            launch_finalize(PH_PQ, c->ctrl, c->slots_glob, cd, st);
+            c->launches++;
+        }
+    }
+    for (irls_ctx *c : R) {
+        launch_axpy_jacobi(vec_args(c), red_args(c), cd, st);
+        c->launches++;
+    }
+    if (R[0]->world > 1) {
+        if ((s = coll_allreduce(R, 3, st))) return s;
+        for (irls_ctx *c : R) {
+            launch_finalize(PH_RZ, c->ctrl, c->slots_glob, cd, st);
+            c->launches++;
+        }
+        if ((s = coll_halo(R, true, st))) return s;
+    }
+    return last_launch(R[0], "cg body");
+}
+
+static irls_status enq_tail(Ranks &R, cudaStream_t st)
+{
+    irls_status s;
+    for (irls_ctx *c : R) {
+        launch_finish(vec_args(c), c->ctrl, st);
+        launch_report(c->ctrl, c->reports, st);
+        c->launches += 2;
+    }
+    if (R[0]->opt.record_trace) {
+        if (R[0]->world > 1 && (s = coll_halo(R, false, st))) return s;
+        for (irls_ctx *c : R) {
+            const VecArgs v = vec_args(c);
+            const RedArgs ra = red_args(c);
+            if (c->kind == 0)
+                launch_stencil_diag_ex(stencil_args(c, false), v, ra, c->opt.eps, c->opt.cg_norm, c->gs_diag,
+                                       c->gt_diag, st);
+            else
+                launch_sell_diag_ex(sell_args(c), v, ra, c->opt.eps, c->opt.cg_norm, c->gs_diag, c->gt_diag, st);
+        }
+        if (R[0]->world > 1 && (s = coll_allreduce(R, 4, st))) return s;
+        if ((s = coll_minmax(R, st))) return s;
+        for (irls_ctx *c : R) {
+            launch_diag_finalize(c->ctrl, c->slots_glob, c->reports, c->opt.cg_norm, st);
+            c->launches += 2;
+        }
+    }
+    return last_launch(R[0], "tail");
+}
+
+// Per-solve CUDA graph (one rank, world 1): [x = 0] -> K1 (sets the WHILE
+// condition) -> [x = 0] -> WHILE { K3 ; K5 (sets the condition) } -> finish
+// -> report [-> diag].
 static irls_status build_graph(irls_ctx *c, int mode)
 {
     cudaStream_t st = c->stream;
+    Ranks R{c};
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     cudaStreamCaptureStatus cs;
     cudaGraph_t graph;
@@ -432,7 +519,7 @@ static irls_status build_graph(irls_ctx *c, int mode)
     const int64_t lsave = c->launches;
     c->launches = 0;
     if (mode == ASM_INIT) CK(cudaMemsetAsync(c->x, 0, sizeof(double) * c->n_own, st));
-    irls_status s = enq_assemble(c, mode, cd, st);
+    irls_status s = enq_assemble(R, mode, cd, st);
     if (s) { cudaGraph_t g; cudaStreamEndCapture(st, &g); if (g) cudaGraphDestroy(g); return s; }
     if (mode == ASM_REWEIGHT_COLD) CK(cudaMemsetAsync(c->x, 0, sizeof(double) * c->n_own, st));
     CK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &graph, &deps, &nd));
@@ -447,13 +534,13 @@ static irls_status build_graph(irls_ctx *c, int mode)
     CK(cudaStreamUpdateCaptureDependencies(st, &cnode, 1, cudaStreamSetCaptureDependencies));
     CK(cudaStreamBeginCaptureToGraph(c->side_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
     const int64_t pre = c->launches;
-    s = enq_body(c, cd, c->side_stream);
+    s = enq_body(R, cd, c->side_stream);
     c->gl_body = c->launches - pre;
     c->launches = pre;
     cudaGraph_t bodyg;
     CK(cudaStreamEndCapture(c->side_stream, &bodyg));
     if (s) { cudaGraph_t g; cudaStreamEndCapture(st, &g); if (g) cudaGraphDestroy(g); return s; }
-    s = enq_tail(c, st);
+    s = enq_tail(R, st);
     cudaGraph_t full;
     CK(cudaStreamEndCapture(st, &full));
     if (s) { cudaGraphDestroy(full); return s; }
@@ -464,9 +551,9 @@ static irls_status build_graph(irls_ctx *c, int mode)
     return IRLS_OK;
 }
 
-
-static irls_status enqueue_solve(irls_ctx *c, int mode)
+static irls_status enqueue_solve(Ranks &R, int mode)
 {
+    irls_ctx *c = R[0];
     cudaStream_t st = c->stream;
     if (c->opt.loop_mode == IRLS_LOOP_GRAPH && c->world == 1) {
         if (!c->gexec[mode]) {
@@ -479,22 +566,25 @@ static irls_status enqueue_solve(irls_ctx *c, int mode)
         return IRLS_OK;
     }
     // host loop: one 4-byte readback of the device "done" flag per iteration
+    // (every rank computes the identical flag: the slot allreduce is exact)
     CondArgs cd;
     memset(&cd, 0, sizeof(cd));
     cd.use = 0;
     cd.finalize = c->world == 1 ? 1 : 0;
-    if (mode == ASM_INIT) CK(cudaMemsetAsync(c->x, 0, sizeof(double) * c->n_own, st));
-    irls_status s = enq_assemble(c, mode, cd, st);
+    if (mode == ASM_INIT)
+        for (irls_ctx *d : R) CK(cudaMemsetAsync(d->x, 0, sizeof(double) * d->n_own, st));
+    irls_status s = enq_assemble(R, mode, cd, st);
     if (s) return s;
-    if (mode == ASM_REWEIGHT_COLD) CK(cudaMemsetAsync(c->x, 0, sizeof(double) * c->n_own, st));
+    if (mode == ASM_REWEIGHT_COLD)
+        for (irls_ctx *d : R) CK(cudaMemsetAsync(d->x, 0, sizeof(double) * d->n_own, st));
     for (;;) {
         CK(cudaMemcpyAsync(c->h_done, &c->ctrl->done, sizeof(int), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         if (*c->h_done) break;
-        s = enq_body(c, cd, st);
+        s = enq_body(R, cd, st);
         if (s) return s;
     }
-    return enq_tail(c, st);
+    return enq_tail(R, st);
 }
 
 static void copy_report(const DevReport &d, irls_step_report *o, float ms)
@@ -515,19 +605,22 @@ static void copy_report(const DevReport &d, irls_step_report *o, float ms)
     o->reserved2 = 0.f;
 }
 
-// Run `count` solves (first one with mode0, the rest with mode_rest); fill reports.
-static irls_status run_solves(irls_ctx *c, int mode0, int mode_rest, int count, irls_step_report *reps,
-                              int64_t *total)
+// Run `count` solves (first one with mode0, the rest with mode_rest); fill
+// reports from rank 0 and check that every driven rank reports the same.
+static irls_status run_solves(Ranks &R, int mode0, int mode_rest, int count, irls_step_report *reps, int64_t *total)
 {
+    irls_ctx *c = R[0];
     cudaStream_t st = c->stream;
-    c->launches = 0;
-    CK(cudaMemsetAsync(&c->ctrl->step, 0, sizeof(int32_t), st));
+    for (irls_ctx *d : R) {
+        d->launches = 0;
+        CK(cudaMemsetAsync(&d->ctrl->step, 0, sizeof(int32_t), st));
+    }
     std::vector<cudaEvent_t> ev(count + 1);
     for (auto &e : ev) CK(cudaEventCreate(&e));
     CK(cudaEventRecord(ev[0], st));
     irls_status s = IRLS_OK;
     for (int i = 0; i < count && !s; i++) {
-        s = enqueue_solve(c, i == 0 ? mode0 : mode_rest);
+        s = enqueue_solve(R, i == 0 ? mode0 : mode_rest);
         if (!s) {
             cudaError_t e = cudaEventRecord(ev[i + 1], st);
             if (e != cudaSuccess) s = fail(c, IRLS_ERR_CUDA, cudaGetErrorString(e));
@@ -535,10 +628,17 @@ static irls_status run_solves(irls_ctx *c, int mode0, int mode_rest, int count, 
     }
     cudaError_t e = cudaStreamSynchronize(st);
     if (!s && e != cudaSuccess) s = fail(c, IRLS_ERR_CUDA, std::string("solve: ") + cudaGetErrorString(e));
-    std::vector<DevReport> h(count);
+    std::vector<DevReport> h(count), h2(count);
     if (!s) {
         e = memcpy_sync(c, h.data(), c->reports, sizeof(DevReport) * count, cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) s = fail(c, IRLS_ERR_CUDA, cudaGetErrorString(e));
+        for (size_t r = 1; r < R.size() && !s; r++) {
+            e = memcpy_sync(R[r], h2.data(), R[r]->reports, sizeof(DevReport) * count, cudaMemcpyDeviceToHost);
+            if (e != cudaSuccess) s = fail(c, IRLS_ERR_CUDA, cudaGetErrorString(e));
+            for (int i = 0; i < count && !s; i++)
+                if (h2[i].cg_iters != h[i].cg_iters || h2[i].status != h[i].status || h2[i].rel_res != h[i].rel_res)
+                    s = fail(c, IRLS_ERR_STATE, "ranks disagree on the CG scalars");
+        }
     }
     int64_t tot = 0;
     if (!s) {
@@ -553,9 +653,11 @@ static irls_status run_solves(irls_ctx *c, int mode0, int mode_rest, int count, 
         c->graph_iters_pending = false;
     }
     for (auto &ee : ev) cudaEventDestroy(ee);
-    c->last_cg_iters = tot;
+    for (irls_ctx *d : R) {
+        d->last_cg_iters = tot;
+        if (!s) d->state = 1;
+    }
     if (total) *total = tot;
-    if (!s) c->state = 1;
     return s;
 }
 
@@ -569,7 +671,7 @@ static irls_status common_setup(irls_ctx *c, const irls_comm_desc *comm, const i
     c->rank = comm ? comm->rank : 0;
     c->device = comm ? comm->device : 0;
     if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return IRLS_ERR_INVALID_ARGUMENT;
-    if (c->world > 1 && (!comm->nccl_unique_id || 8 % c->world != 0)) return IRLS_ERR_INVALID_ARGUMENT;
+    if (c->world > 1 && ((!comm->nccl_unique_id && !c->vg) || 8 % c->world != 0)) return IRLS_ERR_INVALID_ARGUMENT;
     CK(cudaSetDevice(c->device));
     if (comm && comm->cuda_stream) {
         c->stream = (cudaStream_t)comm->cuda_stream;
@@ -623,7 +725,7 @@ static irls_status alloc_solver(irls_ctx *c, int64_t ghost)
 
 static irls_status init_nccl(irls_ctx *c, const irls_comm_desc *comm)
 {
-    if (c->world == 1) return IRLS_OK;
+    if (c->world == 1 || c->vg) return IRLS_OK;
     ncclUniqueId id;
     memcpy(&id, comm->nccl_unique_id, sizeof(id));
     NK(ncclCommInitRank(&c->nccl, c->world, id, c->rank));
@@ -659,9 +761,20 @@ static bool grid_nonsingular(int32_t nx, int32_t ny, int32_t nz, const double *c
     return true;
 }
 
+static irls_status create_stencil_impl(irls_ctx **out, const irls_comm_desc *comm, int32_t nx, int32_t ny, int32_t nz,
+                                       const double *cx, const double *cy, const double *cz, const double *cs,
+                                       const double *ct, const irls_options *opt, irls_vgroup *vg);
+
 extern "C" irls_status irls_mincut_create_stencil(irls_ctx **out, const irls_comm_desc *comm, int32_t nx, int32_t ny,
                                                   int32_t nz, const double *cx, const double *cy, const double *cz,
                                                   const double *cs, const double *ct, const irls_options *opt)
+{
+    return create_stencil_impl(out, comm, nx, ny, nz, cx, cy, cz, cs, ct, opt, nullptr);
+}
+
+static irls_status create_stencil_impl(irls_ctx **out, const irls_comm_desc *comm, int32_t nx, int32_t ny, int32_t nz,
+                                       const double *cx, const double *cy, const double *cz, const double *cs,
+                                       const double *ct, const irls_options *opt, irls_vgroup *vg)
 {
     if (!out) return IRLS_ERR_INVALID_ARGUMENT;
     *out = nullptr;
@@ -670,6 +783,7 @@ extern "C" irls_status irls_mincut_create_stencil(irls_ctx **out, const irls_com
     const int64_t N = (int64_t)nx * ny * nz;
     if (N >= ((int64_t)1 << 31) - 2 * ((int64_t)nx * ny) - kChunk) return IRLS_ERR_INVALID_ARGUMENT;
     irls_ctx *c = new irls_ctx();
+    c->vg = vg;
     irls_status s = common_setup(c, comm, opt);
     if (!s) {
         c->kind = 0;
@@ -932,7 +1046,8 @@ extern "C" irls_status irls_init(irls_ctx *c, irls_step_report *rep)
     GUARD(c);
     if (c->n_glob == 0) { c->state = 1; return IRLS_OK; }
     irls_step_report tmp;
-    return run_solves(c, ASM_INIT, ASM_INIT, 1, rep ? rep : &tmp, nullptr);
+    Ranks R{c};
+    return run_solves(R, ASM_INIT, ASM_INIT, 1, rep ? rep : &tmp, nullptr);
 }
 
 extern "C" irls_status irls_step(irls_ctx *c, irls_step_report *rep)
@@ -942,7 +1057,8 @@ extern "C" irls_status irls_step(irls_ctx *c, irls_step_report *rep)
     if (c->n_glob == 0) return IRLS_OK;
     const int mode = c->opt.warm_start ? ASM_REWEIGHT_WARM : ASM_REWEIGHT_COLD;
     irls_step_report tmp;
-    return run_solves(c, mode, mode, 1, rep ? rep : &tmp, nullptr);
+    Ranks R{c};
+    return run_solves(R, mode, mode, 1, rep ? rep : &tmp, nullptr);
 }
 
 extern "C" irls_status irls_solve(irls_ctx *c, int32_t mode, irls_step_report *per_step, int64_t *total)
@@ -952,9 +1068,10 @@ extern "C" irls_status irls_solve(irls_ctx *c, int32_t mode, irls_step_report *p
     if (mode == IRLS_CONTINUE && c->state == 0) return fail(c, IRLS_ERR_STATE, "IRLS_CONTINUE without potentials");
     if (c->n_glob == 0) { c->state = 1; if (total) *total = 0; return IRLS_OK; }
     const int step_mode = c->opt.warm_start ? ASM_REWEIGHT_WARM : ASM_REWEIGHT_COLD;
-    if (mode == IRLS_FROM_SCRATCH) return run_solves(c, ASM_INIT, step_mode, c->opt.T + 1, per_step, total);
+    Ranks R{c};
+    if (mode == IRLS_FROM_SCRATCH) return run_solves(R, ASM_INIT, step_mode, c->opt.T + 1, per_step, total);
     if (c->opt.T == 0) { if (total) *total = 0; return IRLS_OK; }
-    return run_solves(c, step_mode, step_mode, c->opt.T, per_step, total);
+    return run_solves(R, step_mode, step_mode, c->opt.T, per_step, total);
 }
 
 // ---------------------------------------------------------------------------
@@ -1298,4 +1415,113 @@ extern "C" void irls_mincut_destroy(irls_ctx *c)
     if (c->side_stream) cudaStreamDestroy(c->side_stream);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
+}
+
+// ---------------------------------------------------------------------------
+// Virtual groups: every rank of the z-slab path in one process on one device.
+// ---------------------------------------------------------------------------
+extern "C" void irls_vgroup_destroy(irls_vgroup *g)
+{
+    if (!g) return;
+    for (irls_ctx *c : g->ranks) irls_mincut_destroy(c);
+    if (g->src_slots) cudaFree(g->src_slots);
+    if (g->src_ctrl) cudaFree(g->src_ctrl);
+    if (g->stream) cudaStreamDestroy(g->stream);
+    delete g;
+}
+
+extern "C" irls_status irls_vgroup_create_stencil(irls_vgroup **out, int32_t world, int32_t device, int32_t nx,
+                                                  int32_t ny, int32_t nz, const double *cx, const double *cy,
+                                                  const double *cz, const double *cs, const double *ct,
+                                                  const irls_options *opt)
+{
+    if (!out || world < 1 || 8 % world != 0) return IRLS_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    if (cudaSetDevice(device) != cudaSuccess) return IRLS_ERR_CUDA;
+    irls_vgroup *g = new irls_vgroup();
+    if (cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete g;
+        return IRLS_ERR_CUDA;
+    }
+    for (int r = 0; r < world; r++) {
+        irls_comm_desc comm;
+        comm.world_size = world;
+        comm.rank = r;
+        comm.device = device;
+        comm.nccl_unique_id = nullptr;
+        comm.cuda_stream = g->stream;
+        irls_ctx *c = nullptr;
+        irls_status s = create_stencil_impl(&c, &comm, nx, ny, nz, cx, cy, cz, cs, ct, opt, g);
+        if (s) {
+            irls_vgroup_destroy(g);
+            return s;
+        }
+        g->ranks.push_back(c);
+    }
+    std::vector<double *> src(world);
+    std::vector<DevCtrl *> ctl(world);
+    for (int r = 0; r < world; r++) {
+        src[r] = g->ranks[r]->slots_local;
+        ctl[r] = g->ranks[r]->ctrl;
+    }
+    if (cudaMalloc(&g->src_slots, sizeof(double *) * world) != cudaSuccess ||
+        cudaMemcpy(g->src_slots, src.data(), sizeof(double *) * world, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMalloc(&g->src_ctrl, sizeof(DevCtrl *) * world) != cudaSuccess ||
+        cudaMemcpy(g->src_ctrl, ctl.data(), sizeof(DevCtrl *) * world, cudaMemcpyHostToDevice) != cudaSuccess) {
+        irls_vgroup_destroy(g);
+        return IRLS_ERR_CUDA;
+    }
+    *out = g;
+    return IRLS_OK;
+}
+
+extern "C" irls_status irls_vgroup_solve(irls_vgroup *g, int32_t mode, irls_step_report *per_step, int64_t *total)
+{
+    if (!g) return IRLS_ERR_INVALID_ARGUMENT;
+    irls_ctx *c = g->ranks[0];
+    GUARD(c);
+    if (mode != IRLS_FROM_SCRATCH && mode != IRLS_CONTINUE) return IRLS_ERR_INVALID_ARGUMENT;
+    if (mode == IRLS_CONTINUE && c->state == 0) return fail(c, IRLS_ERR_STATE, "IRLS_CONTINUE without potentials");
+    const int step_mode = c->opt.warm_start ? ASM_REWEIGHT_WARM : ASM_REWEIGHT_COLD;
+    Ranks &R = g->ranks;
+    if (mode == IRLS_FROM_SCRATCH) return run_solves(R, ASM_INIT, step_mode, c->opt.T + 1, per_step, total);
+    if (c->opt.T == 0) { if (total) *total = 0; return IRLS_OK; }
+    return run_solves(R, step_mode, step_mode, c->opt.T, per_step, total);
+}
+
+extern "C" irls_status irls_vgroup_sweep_cut(irls_vgroup *g, uint8_t *side, int32_t *order, int64_t *k,
+                                             double *cut_value)
+{
+    if (!g) return IRLS_ERR_INVALID_ARGUMENT;
+    irls_ctx *c = g->ranks[0];
+    GUARD(c);
+    if (c->state == 0) return fail(c, IRLS_ERR_STATE, "sweep before solve");
+    double *full = nullptr;
+    irls_status s = vgather_x(g, &full);
+    if (s) return s;
+    return sweep_rank0(c, full, side, order, k, cut_value);
+}
+
+extern "C" irls_status irls_vgroup_get_potentials(irls_vgroup *g, double *x)
+{
+    if (!g || !x) return IRLS_ERR_INVALID_ARGUMENT;
+    irls_ctx *c = g->ranks[0];
+    GUARD(c);
+    if (c->state == 0) return fail(c, IRLS_ERR_STATE, "no potentials yet");
+    double *full = nullptr;
+    irls_status s = vgather_x(g, &full);
+    if (s) return s;
+    CK(cudaMemcpyAsync(x, full, sizeof(double) * c->n_glob, cudaMemcpyDeviceToHost, g->stream));
+    CK(cudaStreamSynchronize(g->stream));
+    return IRLS_OK;
+}
+
+extern "C" irls_status irls_vgroup_set_terminal_weights(irls_vgroup *g, const double *cs, const double *ct)
+{
+    if (!g) return IRLS_ERR_INVALID_ARGUMENT;
+    for (irls_ctx *c : g->ranks) {
+        irls_status s = irls_set_terminal_weights(c, cs, ct);
+        if (s) return s;
+    }
+    return IRLS_OK;
 }

@@ -10,6 +10,8 @@
 #include "../../include/irls_mincut.h"
 #include "kernels.h"
 
+struct irls_vgroup;
+
 struct irls_ctx {
     // ---- configuration
     int kind = 0;  // 0 stencil, 1 csr
@@ -63,6 +65,7 @@ struct irls_ctx {
 
     // multi-GPU
     irls_halo hplan{};
+    irls_vgroup *vg = nullptr;    // virtual group (one process drives every rank)
     double *x_full = nullptr;     // rank 0: gathered potentials
     void *msg_dev = nullptr;      // sweep result broadcast
 
@@ -83,4 +86,13 @@ struct irls_ctx {
     int64_t gl_fixed[3] = {0, 0, 0};  // kernels per solve graph outside the WHILE body
     int64_t gl_body = 0;              // kernels per CG iteration (WHILE body)
     bool graph_iters_pending = false;
+};
+
+// W ranks of one grid driven by one host thread on one device and one stream;
+// the collectives are device copies (testing the multi-GPU data path).
+struct irls_vgroup {
+    std::vector<irls_ctx *> ranks;
+    cudaStream_t stream = nullptr;
+    double **src_slots = nullptr;  // device array of every rank's slots_local
+    irls::DevCtrl **src_ctrl = nullptr;  // device array of every rank's control block
 };

@@ -87,6 +87,9 @@ void launch_sell_diag_ex(const SellArgs &s, const VecArgs &v, const RedArgs &ra,
 void launch_diag_finalize(DevCtrl *ctrl, const double *slots, DevReport *reports, int norm, cudaStream_t st);
 
 enum { PH_START = 0, PH_PQ = 1, PH_RZ = 2 };
+// virtual-group slot sum: dst[i] = sum_r src[r][i]
+void launch_vsum(double *const *src, int W, int n, double *dst, cudaStream_t st);
+void launch_vminmax(DevCtrl *const *ctrl, int W, cudaStream_t st);
 
 // stencil_pair.cu (nx even): K1a+K1b, K3, K5, finish with 128-bit pair access
 int launch_pair_assemble(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, int mode,

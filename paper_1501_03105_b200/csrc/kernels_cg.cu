@@ -451,9 +451,40 @@ __global__ void k_diag_finalize(DevCtrl *ctrl, const double *slots, DevReport *r
     R.x_max = dkey_inv(ctrl->xmax_key);
 }
 
+// Virtual-group "allreduce": dst = sum over ranks (rank order) of src[r].
+__global__ void k_vsum(const double *const *src, int W, int n, double *dst)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double acc = 0.0;
+    for (int r = 0; r < W; r++) acc = acc + src[r][i];
+    dst[i] = acc;
+}
+
+// Virtual-group min / max of the diagnostic x range over every rank.
+__global__ void k_vminmax(DevCtrl *const *ctrl, int W)
+{
+    unsigned long long mn = ~0ull, mx = 0ull;
+    for (int r = 0; r < W; r++) {
+        mn = ctrl[r]->xmin_key < mn ? ctrl[r]->xmin_key : mn;
+        mx = ctrl[r]->xmax_key > mx ? ctrl[r]->xmax_key : mx;
+    }
+    for (int r = 0; r < W; r++) {
+        ctrl[r]->xmin_key = mn;
+        ctrl[r]->xmax_key = mx;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
+void launch_vminmax(DevCtrl *const *ctrl, int W, cudaStream_t st) { k_vminmax<<<1, 1, 0, st>>>(ctrl, W); }
+
+void launch_vsum(double *const *src, int W, int n, double *dst, cudaStream_t st)
+{
+    k_vsum<<<(n + 127) / 128, 128, 0, st>>>(src, W, n, dst);
+}
+
 static inline unsigned nblocks(int64_t n_own) { return (unsigned)((n_own + kChunk - 1) / kChunk); }
 
 void launch_stencil_assemble(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,

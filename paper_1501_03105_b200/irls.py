@@ -64,7 +64,9 @@ SYMBOLS = ["irls_options_default", "irls_nccl_unique_id", "irls_mincut_create_st
            "irls_init", "irls_step", "irls_solve", "irls_sweep_cut", "irls_get_side", "irls_set_terminal_weights",
            "irls_get_potentials", "irls_set_potentials", "irls_get_stats", "irls_time_kernel",
            "irls_mincut_destroy", "irls_status_string", "irls_last_error", "irls_plan_stencil",
-           "irls_halo_plan", "irls_combine_slots"]
+           "irls_halo_plan", "irls_combine_slots", "irls_vgroup_create_stencil", "irls_vgroup_solve",
+           "irls_vgroup_sweep_cut", "irls_vgroup_get_potentials", "irls_vgroup_set_terminal_weights",
+           "irls_vgroup_destroy"]
 
 
 def lib():
@@ -100,6 +102,14 @@ def lib():
         L.irls_last_error.restype = C.c_char_p
         L.irls_plan_stencil.argtypes = [C.c_int32] * 5 + [C.POINTER(C.c_int32)] * 4
         L.irls_halo_plan.argtypes = [C.c_int32] * 5 + [C.POINTER(irls_halo)]
+        L.irls_vgroup_create_stencil.argtypes = [C.POINTER(P), C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                                 C.c_int32, P, P, P, P, P, C.POINTER(irls_options)]
+        L.irls_vgroup_solve.argtypes = [P, C.c_int32, P, C.POINTER(C.c_int64)]
+        L.irls_vgroup_sweep_cut.argtypes = [P, P, P, C.POINTER(C.c_int64), C.POINTER(C.c_double)]
+        L.irls_vgroup_get_potentials.argtypes = [P, P]
+        L.irls_vgroup_set_terminal_weights.argtypes = [P, P, P]
+        L.irls_vgroup_destroy.argtypes = [P]
+        L.irls_vgroup_destroy.restype = None
         L.irls_combine_slots.argtypes = [P]
         L.irls_combine_slots.restype = C.c_double
         _lib = L
@@ -298,3 +308,61 @@ class MinCut:
 
     def __exit__(self, *a):
         self.irls_mincut_destroy()
+
+
+class VGroup:
+    """W ranks of the z-slab multi-GPU path on one device (irls_vgroup_*)."""
+
+    def __init__(self, spec, world, opts: irls_options | None = None, device=0):
+        arrs = [_f64(spec[k]) for k in ("cx", "cy", "cz", "cs", "ct")]
+        self.opts = opts or options()
+        self.h = C.c_void_p()
+        self.n = spec["nx"] * spec["ny"] * spec["nz"]
+        rc = lib().irls_vgroup_create_stencil(C.byref(self.h), world, device, spec["nx"], spec["ny"], spec["nz"],
+                                              *[_ptr(a) for a in arrs], C.byref(self.opts))
+        if rc:
+            self.h = None
+            raise IrlsError(rc, "irls_vgroup_create_stencil")
+
+    def irls_vgroup_solve(self, mode=IRLS_FROM_SCRATCH, T=None):
+        nrep = (T + 1 if mode == IRLS_FROM_SCRATCH else T) if T is not None else None
+        buf = (irls_step_report * max(nrep, 1))() if nrep is not None else None
+        total = C.c_int64()
+        rc = lib().irls_vgroup_solve(self.h, mode, C.cast(buf, C.c_void_p) if buf is not None else None,
+                                     C.byref(total))
+        if rc:
+            raise IrlsError(rc, "irls_vgroup_solve")
+        return ([r.as_dict() for r in buf[:nrep]] if buf is not None else None), total.value
+
+    def irls_vgroup_sweep_cut(self, order=False):
+        side = np.zeros(self.n + 2, dtype=np.uint8)
+        o = np.zeros(self.n, dtype=np.int32) if order else None
+        k, cut = C.c_int64(), C.c_double()
+        rc = lib().irls_vgroup_sweep_cut(self.h, _ptr(side), _ptr(o), C.byref(k), C.byref(cut))
+        if rc:
+            raise IrlsError(rc, "irls_vgroup_sweep_cut")
+        return side, o, k.value, cut.value
+
+    def irls_vgroup_get_potentials(self):
+        x = np.zeros(self.n)
+        rc = lib().irls_vgroup_get_potentials(self.h, _ptr(x))
+        if rc:
+            raise IrlsError(rc, "irls_vgroup_get_potentials")
+        return x
+
+    def irls_vgroup_set_terminal_weights(self, cs, ct):
+        a, b = _f64(cs), _f64(ct)
+        rc = lib().irls_vgroup_set_terminal_weights(self.h, _ptr(a), _ptr(b))
+        if rc:
+            raise IrlsError(rc, "irls_vgroup_set_terminal_weights")
+
+    def close(self):
+        if self.h:
+            lib().irls_vgroup_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,99 @@
+"""The multi-GPU z-slab data path, executed on one GPU as a virtual group
+(irls_vgroup_*): W ranks' kernels, ghost planes, per-rank C3 group sums,
+slot-exact allreduce, ghost p updates, finalize kernels and the rank-0 sweep.
+Only NCCL is replaced (by device copies).  The bar is bitwise equality with
+one rank and with the oracle: the contract makes the result independent of W.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from synthetic import generators as gen
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def irls():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1501_03105_b200 import build, irls as I
+    build.build()
+    return I
+
+
+def single(I, spec, opts, T):
+    m = I.MinCut.from_spec(spec, opts)
+    reps, tot = m.irls_solve(I.IRLS_FROM_SCRATCH, T=T)
+    sw = m.irls_sweep_cut(order=True)
+    return m, reps, tot, sw
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_vgroup_equals_single_and_oracle(irls, world):
+    # 64x64x20: one chunk per plane, uneven slabs (2 or 3 planes per group)
+    spec = gen.blob_grid(64, 64, 20, seed=5, sigma=(3.0, 10.0))
+    T = 20
+    opts = irls.options(T=T, record_trace=1)
+    m, reps1, tot1, sw1 = single(irls, spec, opts, T)
+    g = irls.VGroup(spec, world, irls.options(T=T, record_trace=1))
+    reps, tot = g.irls_vgroup_solve(irls.IRLS_FROM_SCRATCH, T=T)
+    assert tot == tot1
+    for a, b in zip(reps, reps1):
+        for k in ("cg_iters", "converged", "rel_res", "S_eps", "flow_value", "current_s", "true_rel_res",
+                  "x_min", "x_max"):
+            assert a[k] == b[k], k
+    x = g.irls_vgroup_get_potentials()
+    assert np.array_equal(x, m.irls_get_potentials())
+    S = oracle.Solver(oracle.Graph(spec), T=T)
+    S.run(record=False)
+    assert np.array_equal(x, S.x())
+    side, order, k, cut = g.irls_vgroup_sweep_cut(order=True)
+    assert k == sw1[2] and cut == sw1[3]
+    assert np.array_equal(side, sw1[0]) and np.array_equal(order, sw1[1])
+    g.close()
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_vgroup_cold_and_sequence(irls, world):
+    spec = gen.blob_grid(64, 64, 16, seed=2, sigma=(3.0, 8.0))
+    T = 8
+    for warm in (0, 1):
+        opts = irls.options(T=T, warm_start=warm)
+        m = irls.MinCut.from_spec(spec, opts)
+        g = irls.VGroup(spec, world, irls.options(T=T, warm_start=warm))
+        _, t1 = m.irls_solve(irls.IRLS_FROM_SCRATCH, T=T)
+        _, t2 = g.irls_vgroup_solve(irls.IRLS_FROM_SCRATCH, T=T)
+        assert t1 == t2
+        cs, ct = spec["cs"].copy(), spec["ct"].copy()
+        for fs, ft in gen.config5_factors(cs.shape[0], n_problems=2, seed=4):
+            cs, ct = cs * fs, ct * ft
+            m.irls_set_terminal_weights(cs, ct)
+            g.irls_vgroup_set_terminal_weights(cs, ct)
+            _, t1 = m.irls_solve(irls.IRLS_CONTINUE, T=T)
+            _, t2 = g.irls_vgroup_solve(irls.IRLS_CONTINUE, T=T)
+            assert t1 == t2
+            assert np.array_equal(g.irls_vgroup_get_potentials(), m.irls_get_potentials())
+        g.close()
+
+
+@pytest.mark.slow
+def test_vgroup_config2_world8(irls):
+    """BASELINE config 2 (128^3), 8 virtual ranks of 16 planes each."""
+    spec = gen.config2()
+    opts = irls.options(T=50)
+    m, reps1, tot1, sw1 = single(irls, spec, opts, 50)
+    g = irls.VGroup(spec, 8, irls.options(T=50))
+    reps, tot = g.irls_vgroup_solve(irls.IRLS_FROM_SCRATCH, T=50)
+    assert [r["cg_iters"] for r in reps] == [r["cg_iters"] for r in reps1]
+    assert np.array_equal(g.irls_vgroup_get_potentials(), m.irls_get_potentials())
+    side, _, k, cut = g.irls_vgroup_sweep_cut()
+    assert k == sw1[2] and cut == sw1[3] and np.array_equal(side, sw1[0])
+    g.close()
+
+
+def test_vgroup_rejects_unaligned(irls):
+    spec = gen.blob_grid(40, 36, 29, seed=1)  # group boundaries fall inside planes
+    with pytest.raises(irls.IrlsError):
+        irls.VGroup(spec, 2)
