@@ -79,6 +79,12 @@ def lib():
                                 C.POINTER(C.c_int32), u64p]
         L.orc_cut_value.argtypes = [P, u8p]; L.orc_cut_value.restype = C.c_double
         L.orc_maxflow_ek.argtypes = [P, C.POINTER(C.c_double), u8p]
+        i8p = np.ctypeslib.ndpointer(np.int8, flags="C_CONTIGUOUS")
+        L.orc_kmeans2.argtypes = [P, dp, dp, C.POINTER(C.c_int32)]
+        L.orc_coarsen.argtypes = [P, dp, C.c_double, C.c_double, i8p, i64p, C.POINTER(C.c_int64), i64p, i64p,
+                                  u64p, u64p, u64p, u64p, C.POINTER(C.c_int32)]
+        L.orc_maxflow_coarse.argtypes = [C.c_int64, i64p, i64p, u64p, u64p, u64p, u64p, u8p, u64p]
+        L.orc_two_level.argtypes = [P, dp, u8p, C.POINTER(C.c_double), dp, i64p, u64p, C.POINTER(C.c_int32)]
         _lib = L
     return _lib
 
@@ -150,6 +156,48 @@ class Graph:
             self.h = None
 
 
+def q_to_int(words) -> int:
+    """128-bit two's complement (lo, hi) words -> Python int."""
+    v = int(words[0]) + (int(words[1]) << 64)
+    return v - (1 << 128) if v >= 1 << 127 else v
+
+
+def q_array(words) -> list:
+    w = np.asarray(words, dtype=np.uint64).reshape(-1, 2)
+    return [q_to_int(r) for r in w]
+
+
+@dataclass
+class Coarse:
+    cls: np.ndarray      # per reduced node: 0 = S0, 1 = S1, 2 = Sc
+    cid: np.ndarray      # coarse id (Sc) or -1
+    nc: int
+    ptr: np.ndarray      # [nc+1]
+    col: np.ndarray      # coarse ids, ascending per row
+    cap: list            # fixed-point integers per entry
+    qs: list             # s_c-link per coarse node
+    qt: list             # t_c-link per coarse node
+    qst: int             # s_c-t_c edge
+    F: int
+
+
+@dataclass
+class TwoLevelResult:
+    side: np.ndarray
+    cut_value: float
+    c0: float
+    c1: float
+    gamma0: float
+    gamma1: float
+    rounds: int
+    n0: int
+    n1: int
+    nc: int
+    coarse_entries: int
+    flow: int
+    F: int
+
+
 @dataclass
 class SweepResult:
     side: np.ndarray
@@ -219,16 +267,59 @@ class Solver:
         k = C.c_int64(); cut = C.c_double(); F = C.c_int32(); pk = np.zeros(2, dtype=np.uint64)
         _check(lib().orc_sweep(self.h, x, side, order.ctypes.data_as(C.c_void_p), C.byref(k),
                                C.byref(cut), C.byref(F), pk), "sweep")
-        pkv = int(pk[0]) + (int(pk[1]) << 64)
-        if pkv >= 1 << 127:
-            pkv -= 1 << 128
+        pkv = q_to_int(pk)
         return SweepResult(side, order[: self.n], k.value, cut.value, F.value, pkv)
 
     def cut_value(self, side) -> float:
         return lib().orc_cut_value(self.h, np.ascontiguousarray(side, dtype=np.uint8))
+
+    def kmeans2(self, x=None):
+        """A25: (c0, c1, gamma0, gamma1), rounds."""
+        x = self.x() if x is None else np.ascontiguousarray(x, dtype=np.float64)
+        out = np.zeros(4); r = C.c_int32()
+        _check(lib().orc_kmeans2(self.h, x, out, C.byref(r)), "kmeans2")
+        return tuple(float(v) for v in out), r.value
+
+    def coarsen(self, x, gamma0, gamma1) -> Coarse:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        n, nnz = self.n, max(self.graph.nnz, 1)
+        cls = np.zeros(max(n, 1), dtype=np.int8); cid = np.zeros(max(n, 1), dtype=np.int64)
+        ptr = np.zeros(n + 1, dtype=np.int64); col = np.zeros(nnz, dtype=np.int64)
+        cap = np.zeros(2 * nnz, dtype=np.uint64); qs = np.zeros(2 * max(n, 1), dtype=np.uint64)
+        qt = np.zeros(2 * max(n, 1), dtype=np.uint64); qst = np.zeros(2, dtype=np.uint64)
+        nc = C.c_int64(); F = C.c_int32()
+        _check(lib().orc_coarsen(self.h, x, gamma0, gamma1, cls, cid, C.byref(nc), ptr, col, cap, qs, qt, qst,
+                                 C.byref(F)), "coarsen")
+        nc = nc.value
+        m = int(ptr[nc])
+        return Coarse(cls[:n], cid[:n], nc, ptr[: nc + 1].copy(), col[:m].copy(), q_array(cap[: 2 * m]),
+                      q_array(qs[: 2 * nc]), q_array(qt[: 2 * nc]), q_to_int(qst), F.value)
+
+    def two_level(self, x=None) -> TwoLevelResult:
+        x = self.x() if x is None else np.ascontiguousarray(x, dtype=np.float64)
+        side = np.zeros(self.graph.n_total, dtype=np.uint8)
+        cut = C.c_double(); d = np.zeros(4); ii = np.zeros(5, dtype=np.int64)
+        fl = np.zeros(2, dtype=np.uint64); F = C.c_int32()
+        _check(lib().orc_two_level(self.h, x, side, C.byref(cut), d, ii, fl, C.byref(F)), "two_level")
+        return TwoLevelResult(side, cut.value, *[float(v) for v in d], *[int(v) for v in ii], q_to_int(fl), F.value)
 
     def maxflow(self):
         side = np.zeros(self.graph.n_total, dtype=np.uint8)
         flow = C.c_double()
         _check(lib().orc_maxflow_ek(self.h, C.byref(flow), side), "maxflow")
         return flow.value, side
+
+
+def maxflow_coarse(nc, ptr, col, cap, qs, qt, qst):
+    """Exact max-flow on a fixed-point coarse graph (A28): (flow, src[nc])."""
+    def words(vals):
+        w = np.zeros(2 * max(len(vals), 1), dtype=np.uint64)
+        for i, v in enumerate(vals):
+            v &= (1 << 128) - 1
+            w[2 * i] = v & ((1 << 64) - 1); w[2 * i + 1] = v >> 64
+        return w
+    src = np.zeros(max(nc, 1), dtype=np.uint8); fl = np.zeros(2, dtype=np.uint64)
+    _check(lib().orc_maxflow_coarse(nc, np.ascontiguousarray(ptr, dtype=np.int64),
+                                    np.ascontiguousarray(col, dtype=np.int64) if len(col) else np.zeros(1, np.int64),
+                                    words(cap), words(qs), words(qt), words([qst]), src, fl), "maxflow_coarse")
+    return q_to_int(fl), src[:nc]

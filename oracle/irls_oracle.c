@@ -842,3 +842,232 @@ int orc_maxflow_ek(const orc_state *S, double *flow_out, uint8_t *side)
     free(head); free(nxt); free(to); free(res); free(prev); free(queue);
     return ORC_OK;
 }
+
+/* ------------------------------------------------------------------------- */
+/* Two-level rounding ("A two-level rounding procedure";          */
+/* SURVEY §8(f) NEXT #1).  Readings A25-A30 in DESIGN.md §2.                  */
+/* ------------------------------------------------------------------------- */
+
+/* A25 ("the two centers returned from K-means on x^(T) (with initial
+ * guesses 0.1 and 0.9)"): Lloyd's algorithm, k = 2, on the components of
+ * x^(T) — the non-terminals plus x_s = 1 and x_t = 0.  Assignment: u goes to
+ * cluster 1 iff |x_u - c1| < |x_u - c0| (a tie goes to cluster 0).  Means:
+ * sum_j = C3 sum over the non-terminals of (x_u if u is in j, else +0.0),
+ * then + x_s if s is in j, then + x_t if t is in j; c_j = sum_j / |j| (an
+ * empty cluster keeps its centre).  Stop when both centres are unchanged,
+ * or after 100 rounds.  out4 = (c0, c1, gamma0 = c0 + 0.05, gamma1 = c1 - 0.05). */
+int orc_kmeans2(const orc_state *S, const double *x, double *out4, int32_t *rounds_out)
+{
+    const orc_graph *G = S->G;
+    int64_t n = G->n;
+    double *v0 = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    double *v1 = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    if (!v0 || !v1) { free(v0); free(v1); return ORC_ERR_OOM; }
+    double c0 = 0.1, c1 = 0.9;
+    int32_t r;
+    for (r = 1; r <= 100; r++) {
+        int64_t n1 = 0;
+        for (int64_t u = 0; u < n; u++) {
+            int in1 = fabs(x[u] - c1) < fabs(x[u] - c0);
+            v0[u] = in1 ? 0.0 : x[u];
+            v1[u] = in1 ? x[u] : 0.0;
+            n1 += in1;
+        }
+        double s0 = orc_c3_sum(v0, n), s1 = orc_c3_sum(v1, n);
+        const double xt[2] = {1.0, 0.0}; /* x_s, x_t */
+        for (int i = 0; i < 2; i++) {
+            if (fabs(xt[i] - c1) < fabs(xt[i] - c0)) { s1 = s1 + xt[i]; n1++; }
+            else s0 = s0 + xt[i];
+        }
+        int64_t n0 = n + 2 - n1;
+        double d0 = n0 > 0 ? s0 / (double)n0 : c0;
+        double d1 = n1 > 0 ? s1 / (double)n1 : c1;
+        int same = (d0 == c0) && (d1 == c1);
+        c0 = d0; c1 = d1;
+        if (same) break;
+    }
+    if (r > 100) r = 100;
+    out4[0] = c0; out4[1] = c1; out4[2] = c0 + 0.05; out4[3] = c1 - 0.05;
+    *rounds_out = r;
+    free(v0); free(v1);
+    return ORC_OK;
+}
+
+static void put_q(uint64_t *w, i128 v) { w[0] = (uint64_t)v; w[1] = (uint64_t)(v >> 64); }
+static i128 get_q(const uint64_t *w) { return (i128)(((unsigned __int128)w[1] << 64) | w[0]); }
+
+/* The partition and the coarsened graph G_c, in the fixed point
+ * of A15 (Q(c) = rint(c 2^F), the sweep's F), so every coarse capacity is an
+ * exact integer sum (A27).  cls[u] = 0 if x_u <= gamma0 (S0), else 1 if
+ * x_u >= gamma1 (S1), else 2 (Sc); s is in S1 and t in S0 by definition
+ * (they are what S1 and S0 contract into).  Coarse ids: Sc in ascending
+ * reduced id.  The four bullets of P:L278-281:
+ *   {u,v} in Sc x Sc:  Q(c_uv)                          (ccol / ccap, ascending)
+ *   {s_c,u}:           sum_{v in S1} Q(c_uv) + Q(cs_u)  (the s-link: s in S1)
+ *   {t_c,u}:           sum_{v in S0} Q(c_uv) + Q(ct_u)  (the t-link: t in S0)
+ *   {s_c,t_c}:         Q(c_st) + sum_{u in S1}(sum_{v in S0} Q(c_uv) + Q(ct_u))
+ *                      + sum_{u in S0} Q(cs_u)
+ * Caller buffers: cls, cid [n]; cptr [n+1]; ccol, ccap(2 words) [nnz];
+ * cqs, cqt (2 words) [n]; cqst [2].  Returns nc and the coarse entry count. */
+int orc_coarsen(const orc_state *S, const double *x, double g0, double g1, int8_t *cls, int64_t *cid,
+                int64_t *nc_out, int64_t *cptr, int64_t *ccol, uint64_t *ccap, uint64_t *cqs, uint64_t *cqt,
+                uint64_t *cqst, int32_t *F_out)
+{
+    const orc_graph *G = S->G;
+    int64_t n = G->n;
+    int32_t F = sweep_F(G, S->cs, S->ct);
+    int64_t nc = 0;
+    for (int64_t u = 0; u < n; u++) {
+        cls[u] = x[u] <= g0 ? 0 : (x[u] >= g1 ? 1 : 2);
+        cid[u] = cls[u] == 2 ? nc++ : -1;
+    }
+    i128 qst = Qfix(G->c_st, F);
+    int64_t m = 0;
+    cptr[0] = 0;
+    for (int64_t u = 0; u < n; u++) {
+        if (cls[u] == 2) {
+            i128 qs = 0, qt = 0;
+            for (int64_t e = G->adj_ptr[u]; e < G->adj_ptr[u + 1]; e++) {
+                int64_t v = G->adj_idx[e];
+                i128 q = Qfix(G->adj_c[e], F);
+                if (cls[v] == 2) { ccol[m] = cid[v]; put_q(ccap + 2 * m, q); m++; }
+                else if (cls[v] == 1) qs += q;
+                else qt += q;
+            }
+            put_q(cqs + 2 * cid[u], qs + Qfix(S->cs[u], F));
+            put_q(cqt + 2 * cid[u], qt + Qfix(S->ct[u], F));
+            cptr[cid[u] + 1] = m;
+        } else if (cls[u] == 1) {
+            for (int64_t e = G->adj_ptr[u]; e < G->adj_ptr[u + 1]; e++)
+                if (cls[G->adj_idx[e]] == 0) qst += Qfix(G->adj_c[e], F);
+            qst += Qfix(S->ct[u], F);
+        } else {
+            qst += Qfix(S->cs[u], F);
+        }
+    }
+    put_q(cqst, qst);
+    *nc_out = nc;
+    if (F_out) *F_out = F;
+    return ORC_OK;
+}
+
+/* Exact max-flow / min-cut on G_c (the paper's "combinatorial max-flow/
+ * min-cut solver") by Edmonds-Karp (shortest augmenting paths) in
+ * 128-bit integers.  Coarse nodes 0..nc-1, s_c = nc, t_c = nc+1; the direct
+ * s_c-t_c edge is in every cut and is added to the flow value.  src[u] = 1 iff
+ * u is reachable from s_c in the final residual graph: the source side of
+ * the minimal minimum cut, which is the same for every maximum flow (A28). */
+int orc_maxflow_coarse(int64_t nc, const int64_t *cptr, const int64_t *ccol, const uint64_t *ccap,
+                       const uint64_t *cqs, const uint64_t *cqt, const uint64_t *cqst, uint8_t *src,
+                       uint64_t *flow_out)
+{
+    int64_t V = nc + 2, s = nc, t = nc + 1;
+    int64_t m = cptr[nc] / 2 + 2 * nc + 1;
+    int64_t *head = (int64_t *)malloc(sizeof(int64_t) * (size_t)V);
+    int64_t *nxt = (int64_t *)malloc(sizeof(int64_t) * (size_t)(2 * m));
+    int64_t *to = (int64_t *)malloc(sizeof(int64_t) * (size_t)(2 * m));
+    i128 *res = (i128 *)malloc(sizeof(i128) * (size_t)(2 * m));
+    int64_t *prev = (int64_t *)malloc(sizeof(int64_t) * (size_t)V);
+    int64_t *queue = (int64_t *)malloc(sizeof(int64_t) * (size_t)V);
+    if (!head || !nxt || !to || !res || !prev || !queue) {
+        free(head); free(nxt); free(to); free(res); free(prev); free(queue); return ORC_ERR_OOM;
+    }
+    for (int64_t i = 0; i < V; i++) head[i] = -1;
+    int64_t A = 0;
+#define ADD_EDGE(a, b, c) do { to[A] = (b); res[A] = (c); nxt[A] = head[a]; head[a] = A; A++; \
+                               to[A] = (a); res[A] = (c); nxt[A] = head[b]; head[b] = A; A++; } while (0)
+    for (int64_t u = 0; u < nc; u++) {
+        for (int64_t e = cptr[u]; e < cptr[u + 1]; e++)
+            if (ccol[e] > u) ADD_EDGE(u, ccol[e], get_q(ccap + 2 * e));
+        i128 qs = get_q(cqs + 2 * u), qt = get_q(cqt + 2 * u);
+        if (qs > 0) ADD_EDGE(s, u, qs);
+        if (qt > 0) ADD_EDGE(u, t, qt);
+    }
+#undef ADD_EDGE
+    i128 flow = get_q(cqst);
+    for (;;) {
+        for (int64_t i = 0; i < V; i++) prev[i] = -2;
+        int64_t qh = 0, qt = 0;
+        queue[qt++] = s; prev[s] = -1;
+        while (qh < qt && prev[t] == -2) {
+            int64_t u = queue[qh++];
+            for (int64_t a = head[u]; a >= 0; a = nxt[a])
+                if (res[a] > 0 && prev[to[a]] == -2) { prev[to[a]] = a; queue[qt++] = to[a]; }
+        }
+        if (prev[t] == -2) break;
+        i128 b = -1;
+        for (int64_t v = t; v != s; v = to[prev[v] ^ 1]) if (b < 0 || res[prev[v]] < b) b = res[prev[v]];
+        for (int64_t v = t; v != s; v = to[prev[v] ^ 1]) { res[prev[v]] -= b; res[prev[v] ^ 1] += b; }
+        flow += b;
+    }
+    for (int64_t u = 0; u < nc; u++) src[u] = prev[u] != -2;
+    put_q(flow_out, flow);
+    free(head); free(nxt); free(to); free(res); free(prev); free(queue);
+    return ORC_OK;
+}
+
+/* The cut value of a node set by C3 (O7 step 7): cross_v = (v in S) ?
+ * (sum_asc over neighbours u not in S of c_uv) + ct_v : cs_v, plus c_st. */
+static double cut_c3(const orc_state *S, const uint8_t *in)
+{
+    const orc_graph *G = S->G;
+    int64_t n = G->n;
+    double *cross = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    if (!cross) return NAN;
+    for (int64_t v = 0; v < n; v++) {
+        if (in[v]) {
+            double acc = 0.0;
+            for (int64_t e = G->adj_ptr[v]; e < G->adj_ptr[v + 1]; e++)
+                if (!in[G->adj_idx[e]]) acc = acc + G->adj_c[e];
+            cross[v] = acc + S->ct[v];
+        } else {
+            cross[v] = S->cs[v];
+        }
+    }
+    double cut = orc_c3_sum(cross, n) + G->c_st;
+    free(cross);
+    return cut;
+}
+
+/* Two-level rounding of x: K-means thresholds (A25) -> S0/S1/Sc
+ * -> G_c (A27) -> exact min cut on G_c (A28) -> the induced cut on G
+ * ("An s-t cut on G_c induces an s-t cut on G"): S = {s} + S1 + the
+ * source side of G_c.  The cut value is recomputed on G by C3 (A29).
+ * dinfo = (c0, c1, gamma0, gamma1); iinfo = (rounds, |S0|, |S1|, |Sc|, coarse
+ * entries); flow = max-flow value on G_c in fixed point (2 words). */
+int orc_two_level(const orc_state *S, const double *x, uint8_t *side, double *cut_out, double *dinfo,
+                  int64_t *iinfo, uint64_t *flow, int32_t *F_out)
+{
+    const orc_graph *G = S->G;
+    int64_t n = G->n, nnz = G->adj_ptr[n];
+    for (int64_t u = 0; u < n; u++) if (isnan(x[u])) return ORC_ERR_BAD_POTENTIAL;
+    int32_t rounds;
+    int rc = orc_kmeans2(S, x, dinfo, &rounds);
+    if (rc) return rc;
+    size_t N1 = (size_t)(n > 0 ? n : 1), M1 = (size_t)(nnz > 0 ? nnz : 1);
+    int8_t *cls = (int8_t *)malloc(N1);
+    int64_t *cid = (int64_t *)malloc(sizeof(int64_t) * N1);
+    int64_t *cptr = (int64_t *)malloc(sizeof(int64_t) * (N1 + 1));
+    int64_t *ccol = (int64_t *)malloc(sizeof(int64_t) * M1);
+    uint64_t *ccap = (uint64_t *)malloc(16 * M1), *cqs = (uint64_t *)malloc(16 * N1),
+             *cqt = (uint64_t *)malloc(16 * N1), cqst[2];
+    uint8_t *src = (uint8_t *)malloc(N1), *in = (uint8_t *)malloc(N1);
+    if (!cls || !cid || !cptr || !ccol || !ccap || !cqs || !cqt || !src || !in) { rc = ORC_ERR_OOM; goto out; }
+    int64_t nc;
+    orc_coarsen(S, x, dinfo[2], dinfo[3], cls, cid, &nc, cptr, ccol, ccap, cqs, cqt, cqst, F_out);
+    rc = orc_maxflow_coarse(nc, cptr, ccol, ccap, cqs, cqt, cqst, src, flow);
+    if (rc) goto out;
+    int64_t n0 = 0, n1 = 0;
+    for (int64_t u = 0; u < n; u++) {
+        in[u] = cls[u] == 1 || (cls[u] == 2 && src[cid[u]]);
+        n0 += cls[u] == 0; n1 += cls[u] == 1;
+    }
+    for (int64_t id = 0; id < G->n_total; id++) side[id] = 0;
+    side[G->s_id] = 1;
+    for (int64_t u = 0; u < n; u++) if (in[u]) side[G->orig[u]] = 1;
+    *cut_out = cut_c3(S, in);
+    iinfo[0] = rounds; iinfo[1] = n0; iinfo[2] = n1; iinfo[3] = nc; iinfo[4] = cptr[nc];
+out:
+    free(cls); free(cid); free(cptr); free(ccol); free(ccap); free(cqs); free(cqt); free(src); free(in);
+    return rc;
+}
