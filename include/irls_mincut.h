@@ -154,6 +154,63 @@ irls_status irls_sweep_cut(irls_ctx *ctx, uint8_t *side, int32_t *order, int64_t
                            double *cut_value);
 irls_status irls_get_side(irls_ctx *ctx, uint8_t *side);
 
+/* ---- two-level rounding --------------
+ * Rounds the current x^(T) (gathered to rank 0) instead of the sweep:
+ *   1. K-means (Lloyd, k = 2) on the components of x^(T) — the non-terminals
+ *      plus x_s = 1, x_t = 0 — from centres 0.1 / 0.9 (A25): u joins
+ *      cluster 1 iff |x_u - c1| < |x_u - c0|; centres are C3 sums / counts;
+ *      stop when both centres repeat (<= 100 rounds).
+ *   2. gamma0 = c0 + 0.05, gamma1 = c1 - 0.05; S0 = {x <= gamma0},
+ *      S1 = {x >= gamma1} \ S0, Sc = the rest; s in S1, t in S0.
+ *   3. G_c: Sc + {s_c, t_c}, capacities per the four bullets of P:L278-281
+ *      in the sweep's 128-bit fixed point Q(c) = rint(c 2^F) (A27), built on
+ *      the GPU.
+ *   4. Exact max-flow on G_c on the HOST (Boykov-Kolmogorov, timed
+ *      separately, A28); source side = the set reachable from s_c in the
+ *      final residual graph (minimal min cut, unique).
+ *   5. S = {s} + S1 + that set ("an s-t cut on G_c induces an s-t cut on G",
+ *      P:L283); the cut value is recomputed on G by C3 (A29).
+ * side: n_total bytes on the host (as irls_sweep_cut) or NULL; rep: may be
+ * NULL.  Collective in multi-GPU mode; rank 0 computes, every rank returns
+ * the report.  Requires a solve (IRLS_ERR_STATE); NaN in x ->
+ * IRLS_ERR_BAD_POTENTIAL; a max-flow whose value differs from the cut value
+ * of its set (strong duality fails: an internal error) -> IRLS_ERR_CUDA. */
+typedef struct {
+    double c0, c1, gamma0, gamma1;   /* K-means centres and thresholds */
+    int32_t kmeans_rounds;
+    int32_t certified;               /* 1: max-flow value == cut value of the returned set on G_c */
+    int64_t n0, n1, nc;              /* |S0|, |S1|, |Sc| over the non-terminals */
+    int64_t coarse_nlinks;           /* n-links of G_c (undirected) */
+    int64_t augmentations;           /* max-flow augmenting paths */
+    int32_t F, pad;                  /* fixed-point fraction bits */
+    double coarse_flow;              /* max-flow value on G_c including the s_c-t_c edge (Q / 2^F) */
+    double cut_value;                /* cut of the returned set on G (C3) */
+    float ms_gpu;                    /* K-means + coarsening + lift + cut on the device */
+    float ms_copy;                   /* coarse graph to the host and source side back */
+    float ms_maxflow;                /* host max-flow (the paper's sequential second level) */
+    float ms_total;                  /* wall time of the call on rank 0 */
+} irls_two_level_report;
+irls_status irls_two_level_cut(irls_ctx *ctx, uint8_t *side, irls_two_level_report *rep);
+
+/* The coarse graph of the last irls_two_level_cut (rank 0, host copies), for
+ * parity tests: cls [n~] per reduced node (0 = S0, 1 = S1, 2 = Sc); ptr
+ * [nc+1], col [entries] (coarse ids, ascending; both directions stored), cap
+ * [entries] (capacity, float64); qs, qt [2*nc] and qst [2]: the s_c / t_c /
+ * s_c-t_c links as 128-bit fixed point (lo, hi) words.  Any pointer may be
+ * NULL; sizes from the report (entries = 2 * coarse_nlinks). */
+irls_status irls_two_level_get_coarse(irls_ctx *ctx, int8_t *cls, int32_t *ptr, int32_t *col, double *cap,
+                                      uint64_t *qs, uint64_t *qt, uint64_t *qst);
+
+/* Host-only: the library's exact max-flow on a coarse graph in fixed point
+ * (the one irls_two_level_cut runs), for CPU tests.  ptr [nc+1] / col:
+ * symmetric CSR with ascending columns; cap, qs, qt, flow: 128-bit (lo, hi)
+ * words; flow excludes any direct s_c-t_c edge.  src [nc]: 1 = reachable
+ * from s_c.  certified = 1 when the flow equals the cut of src.  Returns
+ * IRLS_ERR_INVALID_ARGUMENT for a non-symmetric graph. */
+irls_status irls_coarse_maxflow(int32_t nc, const int32_t *ptr, const int32_t *col, const uint64_t *cap,
+                                const uint64_t *qs, const uint64_t *qt, uint8_t *src, uint64_t *flow,
+                                int32_t *certified);
+
 /* Replace the terminal capacities (full arrays, length n~ in reduced order:
  * stencil u, CSR ascending original id without s and t); keeps x. */
 irls_status irls_set_terminal_weights(irls_ctx *ctx, const double *cs, const double *ct);
@@ -198,6 +255,7 @@ irls_status irls_vgroup_create_stencil(irls_vgroup **g, int32_t world, int32_t d
                                        const double *cs, const double *ct, const irls_options *opt);
 irls_status irls_vgroup_solve(irls_vgroup *g, int32_t mode, irls_step_report *per_step, int64_t *total_cg_iters);
 irls_status irls_vgroup_sweep_cut(irls_vgroup *g, uint8_t *side, int32_t *order, int64_t *k, double *cut_value);
+irls_status irls_vgroup_two_level_cut(irls_vgroup *g, uint8_t *side, irls_two_level_report *rep);
 irls_status irls_vgroup_get_potentials(irls_vgroup *g, double *x);
 irls_status irls_vgroup_set_terminal_weights(irls_vgroup *g, const double *cs, const double *ct);
 void irls_vgroup_destroy(irls_vgroup *g);

@@ -1525,3 +1525,360 @@ extern "C" irls_status irls_vgroup_set_terminal_weights(irls_vgroup *g, const do
     }
     return IRLS_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Two-level rounding (include/irls_mincut.h, DESIGN.md §2 A25-A29)
+// ---------------------------------------------------------------------------
+#include <chrono>
+
+static irls_status alloc_tl(irls_ctx *c)
+{
+    TLBuffers &b = c->tl;
+    if (b.st) return IRLS_OK;
+    const int64_t n = c->n_glob, K = (n + kChunk - 1) / kChunk, nt = tl_ntiles(n);
+    b.n = n;
+    b.st = dalloc<TLState>(c, 1);
+    b.part = dalloc<double>(c, 3 * K);
+    b.slots = dalloc<double>(c, 3 * kGroups);
+    b.ctrl = dalloc<DevCtrl>(c, 1);
+    b.cls = dalloc<int8_t>(c, n);
+    b.flag = dalloc<int32_t>(c, n);
+    b.cid = dalloc<int32_t>(c, n);
+    b.deg = dalloc<int32_t>(c, n);
+    b.eoff = dalloc<int32_t>(c, n);
+    b.scan_tmp = dalloc<int64_t>(c, nt + 1);
+    b.tile_a = dalloc<__int128>(c, nt);
+    b.cp = dalloc<int32_t>(c, n + 1);
+    b.cqs = dalloc<__int128>(c, n);
+    b.cqt = dalloc<__int128>(c, n);
+    b.src = dalloc<uint8_t>(c, n);
+    b.prank = dalloc<int32_t>(c, n);
+    b.one = dalloc<int64_t>(c, 1);
+    b.side = dalloc<uint8_t>(c, c->n_total);
+    b.ccol = nullptr;
+    b.ccap = nullptr;
+    b.cap_entries = 0;
+    if (!b.st || !b.part || !b.slots || !b.ctrl || !b.cls || !b.flag || !b.cid || !b.deg || !b.eoff || !b.scan_tmp ||
+        !b.tile_a || !b.cp || !b.cqs || !b.cqt || !b.src || !b.prank || !b.one || !b.side)
+        return fail(c, IRLS_ERR_OOM, "two-level buffers");
+    const int64_t one = 1;
+    CK(cudaMemcpyAsync(b.one, &one, sizeof(one), cudaMemcpyHostToDevice, c->stream));
+    return IRLS_OK;
+}
+
+// Coarse entry buffers grow to the largest coarse graph seen.
+static irls_status tl_reserve(irls_ctx *c, int64_t entries)
+{
+    TLBuffers &b = c->tl;
+    if (entries <= b.cap_entries && b.ccol) return IRLS_OK;
+    for (void *p : {(void *)b.ccol, (void *)b.ccap}) {
+        if (!p) continue;
+        CK(cudaFreeAsync(p, c->stream));
+        c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), p), c->allocs.end());
+    }
+    b.ccol = dalloc<int32_t>(c, entries);
+    b.ccap = dalloc<double>(c, entries);
+    if (!b.ccol || !b.ccap) return fail(c, IRLS_ERR_OOM, "coarse graph");
+    b.cap_entries = std::max<int64_t>(entries, 1);
+    return IRLS_OK;
+}
+
+static double q_to_double(__int128 q, int32_t F) { return ldexp((double)q, -F); }
+
+static irls_status two_level_rank0(irls_ctx *c, const double *xfull, uint8_t *side, irls_two_level_report *r)
+{
+    auto t_start = std::chrono::steady_clock::now();
+    cudaStream_t st = c->stream;
+    const int64_t n = c->n_glob;
+    irls_status s = alloc_tl(c);
+    if (s) return s;
+    TLBuffers &b = c->tl;
+    memset(r, 0, sizeof(*r));
+    r->F = c->F;
+    cudaEvent_t ev[4];
+    for (auto &e : ev) CK(cudaEventCreate(&e));
+    struct EvGuard {
+        cudaEvent_t *e;
+        ~EvGuard() { for (int i = 0; i < 4; i++) cudaEventDestroy(e[i]); }
+    } guard{ev};
+    int launches = 0;
+    CK(cudaEventRecord(ev[0], st));
+    // A NaN in x lands in cluster 0 (the comparison is false) and makes c0 NaN.
+    // 1. K-means (A25): batches of rounds, the device stops itself
+    TLState h{0.1, 0.9, 0, 0};
+    CK(cudaMemcpyAsync(b.st, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+    if (n > 0) {
+        RedArgs ra;
+        ra.part = b.part;
+        ra.slots = b.slots;
+        ra.ctrl = b.ctrl;
+        ra.K = (int32_t)((n + kChunk - 1) / kChunk);
+        ra.g0 = 0;
+        ra.g1 = kGroups;
+        ra.n_fin = count_nonempty(ra.K, 0, kGroups);
+        for (int batch = 0; batch < 13 && !h.done; batch++) {
+            for (int i = 0; i < 8; i++) tl_kmeans_round(xfull, n, b.st, ra, st);
+            launches += 8;
+            CK(cudaMemcpyAsync(&h, b.st, sizeof(h), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+        }
+    } else {  // only the terminals' values {1, 0}
+        for (h.rounds = 1; h.rounds <= 100; h.rounds++) {
+            double s0 = 0.0, s1 = 0.0;
+            int64_t n1 = 0;
+            const double xt[2] = {1.0, 0.0};
+            for (double v : xt) {
+                if (fabs(v - h.c1) < fabs(v - h.c0)) { s1 = s1 + v; n1++; } else { s0 = s0 + v; }
+            }
+            const double d0 = (2 - n1) > 0 ? s0 / (double)(2 - n1) : h.c0, d1 = n1 > 0 ? s1 / (double)n1 : h.c1;
+            const bool same = d0 == h.c0 && d1 == h.c1;
+            h.c0 = d0;
+            h.c1 = d1;
+            if (same) break;
+        }
+        if (h.rounds > 100) h.rounds = 100;
+    }
+    if (isnan(h.c0) || isnan(h.c1)) return fail(c, IRLS_ERR_BAD_POTENTIAL, "NaN in potentials");
+    r->c0 = h.c0;
+    r->c1 = h.c1;
+    r->gamma0 = h.c0 + 0.05;
+    r->gamma1 = h.c1 - 0.05;
+    r->kmeans_rounds = h.rounds;
+    // 2-3. classify, coarse ids / offsets, G_c
+    const int64_t nt = tl_ntiles(n);
+    int32_t last[4] = {0, 0, 0, 0};
+    std::vector<__int128> tiles((size_t)std::max<int64_t>(nt, 1));
+    if (n > 0) {
+        if (c->kind == 0) tl_classify_stencil(stencil_args(c, true), n, xfull, r->gamma0, r->gamma1, c->F, b, st);
+        else tl_classify_sell(sell_args(c), xfull, r->gamma0, r->gamma1, c->F, b, st);
+        exclusive_scan_i32(b.flag, n, b.cid, b.scan_tmp, st, &launches);
+        exclusive_scan_i32(b.deg, n, b.eoff, b.scan_tmp, st, &launches);
+        launches += 1;
+        CK(cudaMemcpyAsync(&last[0], b.cid + n - 1, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&last[1], b.flag + n - 1, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&last[2], b.eoff + n - 1, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&last[3], b.deg + n - 1, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(tiles.data(), b.tile_a, sizeof(__int128) * nt, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    const int64_t nc = (int64_t)last[0] + last[1], E = (int64_t)last[2] + last[3];
+    if (E > INT32_MAX - 1) return fail(c, IRLS_ERR_INVALID_ARGUMENT, "coarse graph too large");
+    s = tl_reserve(c, E);
+    if (s) return s;
+    __int128 qst = qfix_host(c->c_st, c->F);
+    for (int64_t i = 0; i < nt && n > 0; i++) qst += tiles[i];
+    if (nc > 0) {
+        if (c->kind == 0) tl_fill_stencil(stencil_args(c, true), n, xfull, r->gamma0, r->gamma1, c->F, b, st);
+        else tl_fill_sell(sell_args(c), c->F, b, st);
+        launches++;
+    }
+    irls_status ls = last_launch(c, "two-level coarsening");
+    if (ls) return ls;
+    CK(cudaEventRecord(ev[1], st));
+    c->h_cp.resize(nc + 1);
+    c->h_ccol.resize(E);
+    c->h_ccap.resize(E);
+    c->h_cqs.resize(nc);
+    c->h_cqt.resize(nc);
+    if (nc > 0) {
+        CK(cudaMemcpyAsync(c->h_cp.data(), b.cp, sizeof(int32_t) * nc, cudaMemcpyDeviceToHost, st));
+        if (E > 0) {
+            CK(cudaMemcpyAsync(c->h_ccol.data(), b.ccol, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(c->h_ccap.data(), b.ccap, sizeof(double) * E, cudaMemcpyDeviceToHost, st));
+        }
+        CK(cudaMemcpyAsync(c->h_cqs.data(), b.cqs, sizeof(__int128) * nc, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(c->h_cqt.data(), b.cqt, sizeof(__int128) * nc, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaEventRecord(ev[2], st));
+    CK(cudaStreamSynchronize(st));
+    c->h_cp[nc] = (int32_t)E;
+    c->h_qst = qst;
+    // 4. exact max-flow on G_c (host)
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<__int128> qcap(E);
+    for (int64_t e = 0; e < E; e++) qcap[e] = qfix_host(c->h_ccap[e], c->F);
+    std::vector<uint8_t> src((size_t)std::max<int64_t>(nc, 1), 0);
+    int64_t stats[3] = {0, 0, 0};
+    __int128 flow = 0;
+    if (nc > 0) {
+        flow = maxflow_bk((int32_t)nc, c->h_cp.data(), c->h_ccol.data(), qcap.data(), c->h_cqs.data(),
+                          c->h_cqt.data(), src.data(), stats);
+        if (stats[0] != 1) return fail(c, IRLS_ERR_CUDA, "coarse max-flow not certified (flow != cut)");
+    } else {
+        stats[0] = 1;
+    }
+    auto t1 = std::chrono::steady_clock::now();
+    r->ms_maxflow = (float)std::chrono::duration<double, std::milli>(t1 - t0).count();
+    r->certified = (int32_t)stats[0];
+    r->augmentations = stats[1];
+    r->coarse_flow = q_to_double(flow + qst, c->F);
+    // 5. lift + cut on G (C3)
+    CK(cudaEventRecord(ev[3], st));
+    if (nc > 0) CK(cudaMemcpyAsync(b.src, src.data(), nc, cudaMemcpyHostToDevice, st));
+    float ms_copy_back = 0.0f;
+    cudaEvent_t e4, e5;
+    CK(cudaEventCreate(&e4));
+    CK(cudaEventCreate(&e5));
+    CK(cudaEventRecord(e4, st));
+    tl_lift(b, st);
+    RedArgs ra;
+    ra.part = c->part;
+    ra.slots = c->slots_local;
+    ra.ctrl = c->ctrl;
+    ra.K = (int32_t)((n + kChunk - 1) / kChunk);
+    ra.g0 = 0;
+    ra.g1 = 8;
+    ra.n_fin = count_nonempty(ra.K, 0, 8);
+    SweepBuffers sb = c->sb;
+    sb.rank = b.prank;
+    sb.k_out = b.one;
+    sb.side = b.side;
+    if (n > 0) {
+        if (c->kind == 0) {
+            sweep_side_cross_stencil(stencil_args(c, true), n, sb, ra, st);
+        } else {
+            CK(cudaMemsetAsync(b.side, 0, c->n_total, st));
+            sweep_side_cross_sell(sell_args(c), c->orig_dev, c->n_total, sb, ra, st);
+            const uint8_t one = 1;
+            CK(cudaMemcpyAsync(b.side + c->s_id, &one, 1, cudaMemcpyHostToDevice, st));
+        }
+        launches += 2;
+    } else {
+        CK(cudaMemsetAsync(b.side, 0, c->n_total, st));
+        const uint8_t one = 1;
+        CK(cudaMemcpyAsync(b.side + (c->kind == 0 ? 0 : c->s_id), &one, 1, cudaMemcpyHostToDevice, st));
+    }
+    ls = last_launch(c, "two-level lift");
+    if (ls) return ls;
+    double slots[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (n > 0) CK(cudaMemcpyAsync(slots, c->slots_local, sizeof(slots), cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(e5, st));
+    if (side) CK(cudaMemcpyAsync(side, b.side, c->n_total, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    float ms_a = 0, ms_b = 0, ms_c = 0;
+    cudaEventElapsedTime(&ms_a, ev[0], ev[1]);
+    cudaEventElapsedTime(&ms_b, ev[1], ev[2]);
+    cudaEventElapsedTime(&ms_c, e4, e5);
+    cudaEventElapsedTime(&ms_copy_back, ev[3], e4);
+    cudaEventDestroy(e4);
+    cudaEventDestroy(e5);
+    r->ms_gpu = ms_a + ms_c;
+    r->ms_copy = ms_b + ms_copy_back;
+    int64_t n0 = 0, n1 = 0;
+    {
+        // |S0| and |S1| from the scan totals: nc is known; count S1 on the host
+        // from the classes (cheap relative to the max-flow; n bytes D2H)
+        std::vector<int8_t> cls((size_t)std::max<int64_t>(n, 1));
+        if (n > 0) CK(memcpy_sync(c, cls.data(), b.cls, n, cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < n; i++) n1 += cls[i] == 1;
+        n0 = n - n1 - nc;
+    }
+    r->n0 = n0;
+    r->n1 = n1;
+    r->nc = nc;
+    r->coarse_nlinks = E / 2;
+    r->cut_value = (n > 0 ? irls_combine_slots(slots) : 0.0) + c->c_st;
+    c->tl_valid = true;
+    c->launches = launches;
+    r->ms_total = (float)std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+    return IRLS_OK;
+}
+
+struct TwoLevelMsg {
+    int64_t status;
+    irls_two_level_report rep;
+};
+
+extern "C" irls_status irls_two_level_cut(irls_ctx *c, uint8_t *side, irls_two_level_report *rep)
+{
+    GUARD(c);
+    if (c->state == 0) return fail(c, IRLS_ERR_STATE, "two-level rounding before solve");
+    double *xfull = nullptr;
+    irls_status s = gather_x(c, &xfull);
+    if (s) return s;
+    TwoLevelMsg msg;
+    memset(&msg, 0, sizeof(msg));
+    if (c->rank == 0) {
+        s = two_level_rank0(c, xfull, side, &msg.rep);
+        msg.status = s;
+        if (s && c->world == 1) return s;
+    }
+    if (c->world > 1) {
+        void *dmsg = nullptr;
+        CK(cudaMallocAsync(&dmsg, sizeof(msg), c->stream));
+        if (c->rank == 0) CK(cudaMemcpyAsync(dmsg, &msg, sizeof(msg), cudaMemcpyHostToDevice, c->stream));
+        NK(ncclBroadcast(dmsg, dmsg, sizeof(msg), ncclUint8, 0, c->nccl, c->stream));
+        CK(cudaMemcpyAsync(&msg, dmsg, sizeof(msg), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaFreeAsync(dmsg, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    }
+    if (msg.status) return fail(c, (irls_status)msg.status, c->rank == 0 ? c->err : "two-level failed on rank 0");
+    if (rep) *rep = msg.rep;
+    return IRLS_OK;
+}
+
+extern "C" irls_status irls_vgroup_two_level_cut(irls_vgroup *g, uint8_t *side, irls_two_level_report *rep)
+{
+    if (!g) return IRLS_ERR_INVALID_ARGUMENT;
+    irls_ctx *c = g->ranks[0];
+    GUARD(c);
+    if (c->state == 0) return fail(c, IRLS_ERR_STATE, "two-level rounding before solve");
+    double *full = nullptr;
+    irls_status s = vgather_x(g, &full);
+    if (s) return s;
+    irls_two_level_report r;
+    s = two_level_rank0(c, full, side, &r);
+    if (s) return s;
+    if (rep) *rep = r;
+    return IRLS_OK;
+}
+
+static void put_words(uint64_t *w, __int128 v)
+{
+    w[0] = (uint64_t)v;
+    w[1] = (uint64_t)((unsigned __int128)v >> 64);
+}
+static __int128 get_words(const uint64_t *w) { return (__int128)(((unsigned __int128)w[1] << 64) | w[0]); }
+
+extern "C" irls_status irls_two_level_get_coarse(irls_ctx *c, int8_t *cls, int32_t *ptr, int32_t *col, double *cap,
+                                                 uint64_t *qs, uint64_t *qt, uint64_t *qst)
+{
+    GUARD(c);
+    if (!c->tl_valid) return fail(c, IRLS_ERR_STATE, "no two-level result");
+    const int64_t nc = (int64_t)c->h_cp.size() - 1, E = c->h_cp[nc];
+    if (cls && c->n_glob > 0) CK(memcpy_sync(c, cls, c->tl.cls, c->n_glob, cudaMemcpyDeviceToHost));
+    if (ptr) memcpy(ptr, c->h_cp.data(), sizeof(int32_t) * (nc + 1));
+    if (col && E) memcpy(col, c->h_ccol.data(), sizeof(int32_t) * E);
+    if (cap && E) memcpy(cap, c->h_ccap.data(), sizeof(double) * E);
+    for (int64_t i = 0; i < nc; i++) {
+        if (qs) put_words(qs + 2 * i, c->h_cqs[i]);
+        if (qt) put_words(qt + 2 * i, c->h_cqt[i]);
+    }
+    if (qst) put_words(qst, c->h_qst);
+    return IRLS_OK;
+}
+
+extern "C" irls_status irls_coarse_maxflow(int32_t nc, const int32_t *ptr, const int32_t *col, const uint64_t *cap,
+                                           const uint64_t *qs, const uint64_t *qt, uint8_t *src, uint64_t *flow,
+                                           int32_t *certified)
+{
+    if (nc < 0 || (nc > 0 && (!ptr || !qs || !qt || !src)) || !flow) return IRLS_ERR_INVALID_ARGUMENT;
+    if (nc == 0) {
+        put_words(flow, 0);
+        if (certified) *certified = 1;
+        return IRLS_OK;
+    }
+    const int32_t E = ptr[nc];
+    std::vector<__int128> qc(E), a(nc), b(nc);
+    for (int32_t e = 0; e < E; e++) qc[e] = get_words(cap + 2 * e);
+    for (int32_t u = 0; u < nc; u++) {
+        a[u] = get_words(qs + 2 * u);
+        b[u] = get_words(qt + 2 * u);
+    }
+    int64_t stats[3] = {0, 0, 0};
+    __int128 f = maxflow_bk(nc, ptr, col, qc.data(), a.data(), b.data(), src, stats);
+    if (stats[0] < 0) return IRLS_ERR_INVALID_ARGUMENT;
+    put_words(flow, f);
+    if (certified) *certified = (int32_t)stats[0];
+    return IRLS_OK;
+}

@@ -268,4 +268,14 @@ __device__ __forceinline__ double rw_g(double c, double d, double eps2)
     return (c * c) / w;
 }
 
+// A15 fixed point: Q(c) = rint(c 2^F) as an exact 128-bit integer (c >= 0).
+__device__ __forceinline__ __int128 qfix(double c, int32_t F)
+{
+    if (c == 0.0) return 0;
+    const double v = rint(scalbn(c, F));
+    const double hi = floor(v * 0x1p-64);
+    const double lo = v - hi * 0x1p64;
+    return ((__int128)(long long)hi << 64) + (__int128)(unsigned long long)lo;
+}
+
 }  // namespace irls

@@ -77,6 +77,14 @@ struct irls_ctx {
     int64_t sweep_k = 0;
     double sweep_cut = 0.0;
 
+    // two-level rounding (rank 0)
+    irls::TLBuffers tl{};
+    bool tl_valid = false;
+    std::vector<int32_t> h_cp, h_ccol;
+    std::vector<double> h_ccap;
+    std::vector<__int128> h_cqs, h_cqt;
+    __int128 h_qst = 0;
+
     // ---- graphs
     cudaGraphExec_t gexec[3] = {nullptr, nullptr, nullptr};  // by assemble mode
     cudaStream_t side_stream = nullptr;

@@ -140,6 +140,52 @@ void sweep_side_cross_sell(const SellArgs &s, const int64_t *orig, int64_t n_tot
                            const RedArgs &ra, cudaStream_t st);
 void sweep_order_out(const int32_t *order, const int64_t *orig, int32_t *out, int64_t n, cudaStream_t st);
 __int128 qfix_host(double c, int32_t F);
+void exclusive_scan_i32(const int32_t *in, int64_t m, int32_t *out, int64_t *tmp, cudaStream_t st, int *launches);
+
+// ---------------------------------------------------------------------------
+// Two-level rounding (twolevel.cu, maxflow.cu)
+// ---------------------------------------------------------------------------
+struct TLState {
+    double c0, c1;
+    int32_t done, rounds;
+};
+struct TLBuffers {
+    int64_t n;               // non-terminals
+    TLState *st;
+    double *part, *slots;    // private C3 scratch: [3][K], [3][8]
+    DevCtrl *ctrl;           // private group counters
+    int8_t *cls;             // [n] 0 = S0, 1 = S1, 2 = Sc
+    int32_t *flag, *cid;     // [n] Sc indicator, coarse id (exclusive scan)
+    int32_t *deg, *eoff;     // [n] coarse degree, coarse row offset (exclusive scan)
+    int64_t *scan_tmp;
+    __int128 *tile_a;        // [ntiles] s_c-t_c partials
+    int32_t *cp;             // [n+1] coarse row pointer
+    __int128 *cqs, *cqt;     // [n] coarse terminal links (by coarse id)
+    int32_t *ccol;           // [cap_entries]
+    double *ccap;
+    int64_t cap_entries;
+    uint8_t *src;            // [n] coarse source side (by coarse id)
+    int32_t *prank;          // [n] 0 = source side
+    int64_t *one;            // device constant 1 (the "k" of the side/cut kernel)
+    uint8_t *side;           // [n_total]
+};
+int64_t tl_ntiles(int64_t n);
+void tl_kmeans_round(const double *x, int64_t n, TLState *st, const RedArgs &ra, cudaStream_t stream);
+void tl_classify_stencil(const StencilArgs &s, int64_t N, const double *x, double g0, double g1, int32_t F,
+                         TLBuffers &b, cudaStream_t st);
+void tl_classify_sell(const SellArgs &s, const double *x, double g0, double g1, int32_t F, TLBuffers &b,
+                      cudaStream_t st);
+void tl_fill_stencil(const StencilArgs &s, int64_t N, const double *x, double g0, double g1, int32_t F,
+                     TLBuffers &b, cudaStream_t st);
+void tl_fill_sell(const SellArgs &s, int32_t F, TLBuffers &b, cudaStream_t st);
+void tl_lift(TLBuffers &b, cudaStream_t st);
+
+// Exact max-flow on the coarse graph (host; maxflow.cu).  Undirected coarse
+// CSR (nc nodes, symmetric, fixed-point capacities), terminal links qs/qt.
+// Returns the flow value (without the direct s_c-t_c edge) and src[u] = 1 iff
+// u is reachable from s_c in the final residual graph.
+__int128 maxflow_bk(int32_t nc, const int32_t *ptr, const int32_t *col, const __int128 *cap, const __int128 *qs,
+                    const __int128 *qt, uint8_t *src, int64_t *stats);
 
 }  // namespace irls
 

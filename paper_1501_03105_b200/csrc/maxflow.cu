@@ -1,0 +1,310 @@
+// maxflow.cu — exact max-flow / min-cut on the coarse graph G_c of the
+// two-level rounding (host code; "solve the undirected s-t min-cut
+// problem on the coarsened graph G_c using a combinatorial max-flow/min-cut
+// solver, e.g. [Boykov-Kolmogorov]"; the paper runs it sequentially on the
+// root, and the north_star keeps it off the GPU hot path).
+//
+// Algorithm: Boykov-Kolmogorov augmenting paths with two search trees (grown
+// from s_c and t_c; orphans re-adopted after each augmentation; the
+// timestamp/distance heuristic for choosing parents).  Capacities are the
+// exact 128-bit fixed-point integers of A15/A27, so the flow is exact.
+// After termination the source side is recomputed as the set reachable from
+// s_c in the residual graph (the minimal minimum cut, unique, A28) and the
+// cut value of that set is compared with the flow value (strong duality is
+// the certificate of optimality).
+#include <climits>
+#include <deque>
+#include <vector>
+
+#include "kernels.h"
+
+namespace irls {
+
+typedef __int128 i128;
+
+namespace {
+
+constexpr int32_t kNone = -1, kTerm = -2, kOrphan = -3;
+
+struct BK {
+    int32_t n;
+    const int32_t *first, *head;
+    std::vector<int32_t> sister;
+    std::vector<i128> rc, tr;
+    std::vector<int32_t> parent, ts, dist;
+    std::vector<uint8_t> tree, in_active;
+    std::deque<int32_t> active, orphans;
+    int32_t time = 0;
+    i128 flow = 0;
+    int64_t n_aug = 0, n_orphan = 0;
+
+    void activate(int32_t i)
+    {
+        if (!in_active[i]) {
+            in_active[i] = 1;
+            active.push_back(i);
+        }
+    }
+    void make_orphan(int32_t k)
+    {
+        parent[k] = kOrphan;
+        orphans.push_back(k);
+        n_orphan++;
+    }
+
+    // Growth stage: returns an arc from an S node to a T node with residual
+    // capacity, or -1 when no active node can grow (maximum flow reached).
+    int32_t grow()
+    {
+        while (!active.empty()) {
+            const int32_t i = active.front();
+            if (tree[i] == 0) {
+                active.pop_front();
+                in_active[i] = 0;
+                continue;
+            }
+            for (int32_t a = first[i]; a < first[i + 1]; a++) {
+                const int32_t j = head[a];
+                if (tree[i] == 1) {
+                    if (rc[a] == 0) continue;
+                    if (tree[j] == 0) {
+                        tree[j] = 1;
+                        parent[j] = sister[a];
+                        ts[j] = ts[i];
+                        dist[j] = dist[i] + 1;
+                        activate(j);
+                    } else if (tree[j] == 2) {
+                        return a;
+                    } else if (ts[j] <= ts[i] && dist[j] > dist[i]) {
+                        parent[j] = sister[a];
+                        ts[j] = ts[i];
+                        dist[j] = dist[i] + 1;
+                    }
+                } else {
+                    const int32_t sa = sister[a];
+                    if (rc[sa] == 0) continue;
+                    if (tree[j] == 0) {
+                        tree[j] = 2;
+                        parent[j] = sa;
+                        ts[j] = ts[i];
+                        dist[j] = dist[i] + 1;
+                        activate(j);
+                    } else if (tree[j] == 1) {
+                        return sa;
+                    } else if (ts[j] <= ts[i] && dist[j] > dist[i]) {
+                        parent[j] = sa;
+                        ts[j] = ts[i];
+                        dist[j] = dist[i] + 1;
+                    }
+                }
+            }
+            active.pop_front();
+            in_active[i] = 0;
+        }
+        return -1;
+    }
+
+    // Augmentation along s_c -> ... -> i -a-> j -> ... -> t_c.
+    void augment(int32_t a)
+    {
+        const int32_t i = head[sister[a]], j = head[a];
+        i128 b = rc[a];
+        for (int32_t k = i;;) {
+            const int32_t p = parent[k];
+            if (p == kTerm) {
+                if (tr[k] < b) b = tr[k];
+                break;
+            }
+            if (rc[sister[p]] < b) b = rc[sister[p]];
+            k = head[p];
+        }
+        for (int32_t k = j;;) {
+            const int32_t p = parent[k];
+            if (p == kTerm) {
+                if (-tr[k] < b) b = -tr[k];
+                break;
+            }
+            if (rc[p] < b) b = rc[p];
+            k = head[p];
+        }
+        rc[a] -= b;
+        rc[sister[a]] += b;
+        for (int32_t k = i;;) {
+            const int32_t p = parent[k];
+            if (p == kTerm) {
+                tr[k] -= b;
+                if (tr[k] == 0) make_orphan(k);
+                break;
+            }
+            const int32_t arc = sister[p], nxt = head[p];
+            rc[arc] -= b;
+            rc[p] += b;
+            if (rc[arc] == 0) make_orphan(k);
+            k = nxt;
+        }
+        for (int32_t k = j;;) {
+            const int32_t p = parent[k];
+            if (p == kTerm) {
+                tr[k] += b;
+                if (tr[k] == 0) make_orphan(k);
+                break;
+            }
+            const int32_t nxt = head[p];
+            rc[p] -= b;
+            rc[sister[p]] += b;
+            if (rc[p] == 0) make_orphan(k);
+            k = nxt;
+        }
+        flow += b;
+        n_aug++;
+    }
+
+    // Adoption stage: every orphan finds a parent in its own tree whose
+    // path reaches the terminal, or becomes free.
+    void adopt()
+    {
+        while (!orphans.empty()) {
+            const int32_t i = orphans.front();
+            orphans.pop_front();
+            const int t = tree[i];
+            int32_t best = kNone, dmin = INT_MAX;
+            for (int32_t a0 = first[i]; a0 < first[i + 1]; a0++) {
+                const int32_t j = head[a0];
+                if (tree[j] != t) continue;
+                if (!(t == 1 ? rc[sister[a0]] > 0 : rc[a0] > 0)) continue;
+                int32_t d = 0, k = j;
+                bool valid;
+                for (;;) {
+                    if (ts[k] == time) {
+                        d += dist[k];
+                        valid = true;
+                        break;
+                    }
+                    const int32_t p = parent[k];
+                    d++;
+                    if (p == kTerm) {
+                        ts[k] = time;
+                        dist[k] = 1;
+                        valid = true;
+                        break;
+                    }
+                    if (p < 0) {  // orphan
+                        valid = false;
+                        break;
+                    }
+                    k = head[p];
+                }
+                if (!valid) continue;
+                if (d < dmin) {
+                    best = a0;
+                    dmin = d;
+                }
+                for (k = j; ts[k] != time; k = head[parent[k]]) {
+                    ts[k] = time;
+                    dist[k] = d--;
+                }
+            }
+            if (best != kNone) {
+                parent[i] = best;
+                ts[i] = time;
+                dist[i] = dmin + 1;
+                continue;
+            }
+            for (int32_t a0 = first[i]; a0 < first[i + 1]; a0++) {
+                const int32_t j = head[a0];
+                if (tree[j] != t) continue;
+                if (t == 1 ? rc[sister[a0]] > 0 : rc[a0] > 0) activate(j);
+                const int32_t p = parent[j];
+                if (p >= 0 && head[p] == i) make_orphan(j);
+            }
+            tree[i] = 0;
+            parent[i] = kNone;
+        }
+    }
+};
+
+}  // namespace
+
+i128 maxflow_bk(int32_t nc, const int32_t *ptr, const int32_t *col, const i128 *cap, const i128 *qs, const i128 *qt,
+                uint8_t *src, int64_t *stats)
+{
+    BK g;
+    g.n = nc;
+    g.first = ptr;
+    g.head = col;
+    const int32_t m = ptr[nc];
+    g.sister.assign(m, -1);
+    g.rc.assign(cap, cap + m);
+    g.tr.resize(nc);
+    g.parent.assign(nc, kNone);
+    g.ts.assign(nc, 0);
+    g.dist.assign(nc, 0);
+    g.tree.assign(nc, 0);
+    g.in_active.assign(nc, 0);
+    // sister arcs: rows are sorted, so the entries (v, u) with u < v are the
+    // leading entries of row v in ascending u
+    {
+        std::vector<int32_t> fill(ptr, ptr + nc);
+        for (int32_t u = 0; u < nc; u++)
+            for (int32_t a = ptr[u]; a < ptr[u + 1]; a++) {
+                const int32_t v = col[a];
+                if (v <= u) continue;
+                const int32_t s = fill[v]++;
+                if (s >= ptr[v + 1] || col[s] != u) {  // not symmetric
+                    if (stats) stats[0] = -1;
+                    return -1;
+                }
+                g.sister[a] = s;
+                g.sister[s] = a;
+            }
+    }
+    for (int32_t u = 0; u < nc; u++) {
+        const i128 a = qs[u], b = qt[u];
+        g.flow += a < b ? a : b;
+        g.tr[u] = a - b;
+        if (g.tr[u] != 0) {
+            g.tree[u] = g.tr[u] > 0 ? 1 : 2;
+            g.parent[u] = kTerm;
+            g.dist[u] = 1;
+            g.activate(u);
+        }
+    }
+    for (;;) {
+        const int32_t a = g.grow();
+        if (a < 0) break;
+        g.time++;
+        g.augment(a);
+        g.adopt();
+    }
+    // minimal source side: residual reachability from s_c
+    std::vector<int32_t> q;
+    q.reserve(nc);
+    for (int32_t u = 0; u < nc; u++) {
+        src[u] = g.tr[u] > 0;
+        if (src[u]) q.push_back(u);
+    }
+    for (size_t h = 0; h < q.size(); h++) {
+        const int32_t u = q[h];
+        for (int32_t a = ptr[u]; a < ptr[u + 1]; a++)
+            if (g.rc[a] > 0 && !src[col[a]]) {
+                src[col[a]] = 1;
+                q.push_back(col[a]);
+            }
+    }
+    // certificate: cut(src) on the original capacities == flow value
+    i128 cut = 0;
+    for (int32_t u = 0; u < nc; u++) {
+        cut += src[u] ? qt[u] : qs[u];
+        if (src[u])
+            for (int32_t a = ptr[u]; a < ptr[u + 1]; a++)
+                if (!src[col[a]]) cut += cap[a];
+    }
+    if (stats) {
+        stats[0] = cut == g.flow ? 1 : 0;
+        stats[1] = g.n_aug;
+        stats[2] = g.n_orphan;
+    }
+    return g.flow;
+}
+
+}  // namespace irls

@@ -22,14 +22,6 @@ constexpr int kTile = 4096;  // keys per tile (256 threads x 16)
 
 int64_t sweep_ntiles(int64_t n) { return (n + kTile - 1) / kTile; }
 
-__device__ __forceinline__ i128 qfix(double c, int32_t F)
-{
-    if (c == 0.0) return 0;
-    const double v = rint(scalbn(c, F));
-    const double hi = floor(v * 0x1p-64);
-    const double lo = v - hi * 0x1p64;
-    return ((i128)(long long)hi << 64) + (i128)(u64)lo;
-}
 
 __int128 qfix_host(double c, int32_t F)
 {
@@ -271,8 +263,8 @@ __global__ void __launch_bounds__(256) k_scan_down(const int32_t *in, int64_t m,
     }
 }
 
-static void exclusive_scan_i32(const int32_t *in, int64_t m, int32_t *out, int64_t *tmp, cudaStream_t st,
-                               int *launches)
+void exclusive_scan_i32(const int32_t *in, int64_t m, int32_t *out, int64_t *tmp, cudaStream_t st,
+                        int *launches)
 {
     const int64_t nb = (m + kTile - 1) / kTile;
     k_scan_reduce<<<(unsigned)nb, 256, 0, st>>>(in, m, tmp);

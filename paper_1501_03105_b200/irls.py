@@ -52,6 +52,17 @@ class irls_halo(C.Structure):
                 ("first_plane", C.c_int32), ("reserved", C.c_int32)]
 
 
+class irls_two_level_report(C.Structure):
+    _fields_ = [("c0", C.c_double), ("c1", C.c_double), ("gamma0", C.c_double), ("gamma1", C.c_double),
+                ("kmeans_rounds", C.c_int32), ("certified", C.c_int32), ("n0", C.c_int64), ("n1", C.c_int64),
+                ("nc", C.c_int64), ("coarse_nlinks", C.c_int64), ("augmentations", C.c_int64), ("F", C.c_int32),
+                ("pad", C.c_int32), ("coarse_flow", C.c_double), ("cut_value", C.c_double), ("ms_gpu", C.c_float),
+                ("ms_copy", C.c_float), ("ms_maxflow", C.c_float), ("ms_total", C.c_float)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad"}
+
+
 class irls_stats(C.Structure):
     _fields_ = [("launches", C.c_int64), ("cg_iters", C.c_int64), ("n_nonterminal", C.c_int64),
                 ("n_links", C.c_int64), ("n_local", C.c_int64)]
@@ -66,7 +77,8 @@ SYMBOLS = ["irls_options_default", "irls_nccl_unique_id", "irls_mincut_create_st
            "irls_mincut_destroy", "irls_status_string", "irls_last_error", "irls_plan_stencil",
            "irls_halo_plan", "irls_combine_slots", "irls_vgroup_create_stencil", "irls_vgroup_solve",
            "irls_vgroup_sweep_cut", "irls_vgroup_get_potentials", "irls_vgroup_set_terminal_weights",
-           "irls_vgroup_destroy"]
+           "irls_vgroup_destroy", "irls_two_level_cut", "irls_two_level_get_coarse", "irls_coarse_maxflow",
+           "irls_vgroup_two_level_cut"]
 
 
 def lib():
@@ -109,6 +121,10 @@ def lib():
         L.irls_vgroup_get_potentials.argtypes = [P, P]
         L.irls_vgroup_set_terminal_weights.argtypes = [P, P, P]
         L.irls_vgroup_destroy.argtypes = [P]
+        L.irls_two_level_cut.argtypes = [P, P, C.POINTER(irls_two_level_report)]
+        L.irls_vgroup_two_level_cut.argtypes = [P, P, C.POINTER(irls_two_level_report)]
+        L.irls_two_level_get_coarse.argtypes = [P] * 8
+        L.irls_coarse_maxflow.argtypes = [C.c_int32, P, P, P, P, P, P, P, C.POINTER(C.c_int32)]
         L.irls_vgroup_destroy.restype = None
         L.irls_combine_slots.argtypes = [P]
         L.irls_combine_slots.restype = C.c_double
@@ -181,6 +197,40 @@ def irls_combine_slots(slots) -> float:
     s = _f64(slots)
     assert s.shape == (8,)
     return lib().irls_combine_slots(_ptr(s))
+
+
+def words_to_ints(w) -> list:
+    """128-bit two's complement (lo, hi) uint64 pairs -> Python ints."""
+    w = np.asarray(w, dtype=np.uint64).reshape(-1, 2)
+    out = []
+    for lo, hi in w:
+        v = int(lo) + (int(hi) << 64)
+        out.append(v - (1 << 128) if v >= 1 << 127 else v)
+    return out
+
+
+def ints_to_words(vals) -> np.ndarray:
+    w = np.zeros(2 * max(len(vals), 1), dtype=np.uint64)
+    for i, v in enumerate(vals):
+        v &= (1 << 128) - 1
+        w[2 * i] = v & ((1 << 64) - 1)
+        w[2 * i + 1] = v >> 64
+    return w
+
+
+def irls_coarse_maxflow(nc, ptr, col, cap, qs, qt):
+    """The library's exact coarse max-flow (host): (flow int, src uint8[nc], certified)."""
+    p = np.ascontiguousarray(ptr, dtype=np.int32)
+    c = np.ascontiguousarray(col, dtype=np.int32) if len(col) else np.zeros(1, np.int32)
+    src = np.zeros(max(nc, 1), dtype=np.uint8)
+    fl = np.zeros(2, dtype=np.uint64)
+    cert = C.c_int32()
+    cw, sw, tw = ints_to_words(list(cap)), ints_to_words(list(qs)), ints_to_words(list(qt))
+    rc = lib().irls_coarse_maxflow(nc, _ptr(p), _ptr(c), _ptr(cw), _ptr(sw), _ptr(tw), _ptr(src), _ptr(fl),
+                                   C.byref(cert))
+    if rc:
+        raise IrlsError(rc, "irls_coarse_maxflow")
+    return words_to_ints(fl)[0], src[:nc], cert.value
 
 
 class MinCut:
@@ -262,6 +312,26 @@ class MinCut:
         self._check(lib().irls_sweep_cut(self.h, _ptr(s), _ptr(o), C.byref(k), C.byref(cut)), "irls_sweep_cut")
         return s, (o[: self.n] if o is not None else None), k.value, cut.value
 
+    def irls_two_level_cut(self, side=True):
+        """Two-level rounding: (side or None, report dict)."""
+        sd = np.zeros(self.n_total, dtype=np.uint8) if side else None
+        r = irls_two_level_report()
+        self._check(lib().irls_two_level_cut(self.h, _ptr(sd), C.byref(r)), "irls_two_level_cut")
+        return sd, r.as_dict()
+
+    def irls_two_level_get_coarse(self, nc, entries):
+        cls = np.zeros(max(self.n, 1), dtype=np.int8)
+        ptr = np.zeros(nc + 1, dtype=np.int32)
+        col = np.zeros(max(entries, 1), dtype=np.int32)
+        cap = np.zeros(max(entries, 1))
+        qs = np.zeros(2 * max(nc, 1), dtype=np.uint64)
+        qt = np.zeros(2 * max(nc, 1), dtype=np.uint64)
+        qst = np.zeros(2, dtype=np.uint64)
+        self._check(lib().irls_two_level_get_coarse(self.h, _ptr(cls), _ptr(ptr), _ptr(col), _ptr(cap), _ptr(qs),
+                                                    _ptr(qt), _ptr(qst)), "irls_two_level_get_coarse")
+        return dict(cls=cls[: self.n], ptr=ptr, col=col[:entries], cap=cap[:entries], qs=words_to_ints(qs[: 2 * nc]),
+                    qt=words_to_ints(qt[: 2 * nc]), qst=words_to_ints(qst)[0])
+
     def irls_get_side(self):
         s = np.zeros(self.n_total, dtype=np.uint8)
         self._check(lib().irls_get_side(self.h, _ptr(s)), "irls_get_side")
@@ -342,6 +412,14 @@ class VGroup:
         if rc:
             raise IrlsError(rc, "irls_vgroup_sweep_cut")
         return side, o, k.value, cut.value
+
+    def irls_vgroup_two_level_cut(self):
+        side = np.zeros(self.n + 2, dtype=np.uint8)
+        r = irls_two_level_report()
+        rc = lib().irls_vgroup_two_level_cut(self.h, _ptr(side), C.byref(r))
+        if rc:
+            raise IrlsError(rc, "irls_vgroup_two_level_cut")
+        return side, r.as_dict()
 
     def irls_vgroup_get_potentials(self):
         x = np.zeros(self.n)
