@@ -192,6 +192,12 @@ typedef struct {
 } irls_two_level_report;
 irls_status irls_two_level_cut(irls_ctx *ctx, uint8_t *side, irls_two_level_report *rep);
 
+/* mu*, the exact minimum cut of G, by the same pipeline with no contraction
+ * (gamma0 = -inf, gamma1 = +inf: G_c = G, the no-coarsening limit of S:L384)
+ * — the denominator of delta = (mu - mu*) / mu* (Eq. 13).  Needs
+ * no solve; single process only; host memory ~60 B per n-link. */
+irls_status irls_exact_min_cut(irls_ctx *ctx, uint8_t *side, irls_two_level_report *rep);
+
 /* The coarse graph of the last irls_two_level_cut (rank 0, host copies), for
  * parity tests: cls [n~] per reduced node (0 = S0, 1 = S1, 2 = Sc); ptr
  * [nc+1], col [entries] (coarse ids, ascending; both directions stored), cap

@@ -80,6 +80,7 @@ def lib():
         L.orc_cut_value.argtypes = [P, u8p]; L.orc_cut_value.restype = C.c_double
         L.orc_maxflow_ek.argtypes = [P, C.POINTER(C.c_double), u8p]
         i8p = np.ctypeslib.ndpointer(np.int8, flags="C_CONTIGUOUS")
+        L.orc_lambda2.argtypes = [P, C.c_double, C.c_int32, C.c_int32, dp, C.POINTER(C.c_int32), P]
         L.orc_kmeans2.argtypes = [P, dp, dp, C.POINTER(C.c_int32)]
         L.orc_coarsen.argtypes = [P, dp, C.c_double, C.c_double, i8p, i64p, C.POINTER(C.c_int64), i64p, i64p,
                                   u64p, u64p, u64p, u64p, C.POINTER(C.c_int32)]
@@ -302,6 +303,15 @@ class Solver:
         fl = np.zeros(2, dtype=np.uint64); F = C.c_int32()
         _check(lib().orc_two_level(self.h, x, side, C.byref(cut), d, ii, fl, C.byref(F)), "two_level")
         return TwoLevelResult(side, cut.value, *[float(v) for v in d], *[int(v) for v in ii], q_to_int(fl), F.value)
+
+    def lambda2(self, rtol=1e-12, max_iter=100000, norm=1, want_x=False):
+        """A30: (lambda_2, x^T L x, C, cg_iters[, v])."""
+        out = np.zeros(3); it = C.c_int32()
+        xo = np.zeros(max(self.n, 1)) if want_x else None
+        _check(lib().orc_lambda2(self.h, rtol, max_iter, norm, out, C.byref(it),
+                                 xo.ctypes.data_as(C.c_void_p) if want_x else None), "lambda2")
+        res = (float(out[0]), float(out[1]), float(out[2]), it.value)
+        return res + (xo[: self.n],) if want_x else res
 
     def maxflow(self):
         side = np.zeros(self.graph.n_total, dtype=np.uint8)

@@ -383,6 +383,7 @@ typedef struct {
     double cg_rtol;
     int32_t step;  /* number of solves done (0 = none) */
     double *cs, *ct; /* owned copy of terminal capacities (set_terminal_weights) */
+    const double *bvec; /* right-hand side override (lambda2); NULL: b = gs (Eq. 7) */
 } orc_state;
 
 typedef struct {
@@ -487,16 +488,17 @@ static int pcg(orc_state *S, orc_report *rep)
     double *x = S->x, *r = S->r, *z = S->z, *p = S->p, *q = S->q;
     /* r = b - A x0 */
     matvec(S, x, q);
-    for (int64_t u = 0; u < n; u++) r[u] = S->gs[u] - q[u];
+    const double *b = S->bvec ? S->bvec : S->gs;
+    for (int64_t u = 0; u < n; u++) r[u] = b[u] - q[u];
     for (int64_t u = 0; u < n; u++) z[u] = r[u] * S->Dinv[u];
     for (int64_t u = 0; u < n; u++) p[u] = z[u];
     double rho = dot_c3(S, r, z);
     double ref2;
     if (S->cg_norm == 0) {
-        for (int64_t u = 0; u < n; u++) { double mb = S->gs[u] * S->Dinv[u]; S->tmp[u] = mb * mb; }
+        for (int64_t u = 0; u < n; u++) { double mb = b[u] * S->Dinv[u]; S->tmp[u] = mb * mb; }
         ref2 = orc_c3_sum(S->tmp, n);
     } else {
-        ref2 = dot_c3(S, S->gs, S->gs);
+        ref2 = dot_c3(S, b, b);
     }
     double ref = sqrt(ref2);
     rep->ref = ref;
@@ -1069,5 +1071,71 @@ int orc_two_level(const orc_state *S, const double *x, uint8_t *side, double *cu
     iinfo[0] = rounds; iinfo[1] = n0; iinfo[2] = n1; iinfo[3] = nc; iinfo[4] = cptr[nc];
 out:
     free(cls); free(cid); free(cptr); free(ccol); free(ccap); free(cqs); free(cqt); free(src); free(in);
+    return rc;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Cheeger-type diagnostic lambda_2 (Theorem 4; characterised by  */
+/* the constrained WLS of P:L543-551; reading A30).     */
+/* ------------------------------------------------------------------------- */
+
+/* lambda_2 = min (1/2C) x^T L x s.t. x_s = 1, x_t = -1 (Eq. lambda2-
+ * constrained-wls), L the Laplacian of G with the capacities c
+ * (W = C) and C = 2 sum_e c_e.  Reduced system as Eq. 7 with
+ * f = (1, -1): L~ v = b, b_u = cs_u - ct_u, solved by the same Jacobi-PCG
+ * (O5) from x0 = 0 with the given rtol / cap / norm.  Then
+ *   x^T L x = C3 over u of own_u, plus 4 c_st, where own_u = sum over the
+ *     higher-id neighbours v (ascending) of c_uv * (d * d), d = x_u - x_v,
+ *     then + cs_u * (ds * ds), ds = 1 - x_u, then + ct_u * (dt * dt),
+ *     dt = x_u + 1;
+ *   C = 2 * (C3 over u of (sum_{v > u, asc} c_uv + cs_u + ct_u) + c_st);
+ *   lambda_2 = x^T L x / (2 C).
+ * out3 = (lambda_2, x^T L x, C); x_out (may be NULL) = v.  The IRLS state
+ * (x) is restored. */
+int orc_lambda2(orc_state *S, double rtol, int32_t max_iter, int32_t norm, double *out3, int32_t *iters,
+                double *x_out)
+{
+    const orc_graph *G = S->G;
+    int64_t n = G->n;
+    size_t N1 = (size_t)(n > 0 ? n : 1);
+    double *xs = (double *)malloc(sizeof(double) * N1), *b = (double *)malloc(sizeof(double) * N1);
+    double *own = (double *)malloc(sizeof(double) * N1), *cap = (double *)malloc(sizeof(double) * N1);
+    if (!xs || !b || !own || !cap) { free(xs); free(b); free(own); free(cap); return ORC_ERR_OOM; }
+    memcpy(xs, S->x, sizeof(double) * (size_t)n);
+    double r0 = S->cg_rtol; int32_t m0 = S->cg_max_iter, n0 = S->cg_norm;
+    S->cg_rtol = rtol; S->cg_max_iter = max_iter; S->cg_norm = norm;
+    assemble(S, NULL);
+    for (int64_t u = 0; u < n; u++) { b[u] = S->gs[u] - S->gt[u]; S->x[u] = 0.0; }
+    S->bvec = b;
+    orc_report rep;
+    memset(&rep, 0, sizeof(rep));
+    int rc = pcg(S, &rep);
+    S->bvec = NULL;
+    S->cg_rtol = r0; S->cg_max_iter = m0; S->cg_norm = n0;
+    if (rc == ORC_OK) {
+        const double *x = S->x;
+        for (int64_t u = 0; u < n; u++) {
+            double q = 0.0, c = 0.0;
+            for (int64_t e = G->adj_ptr[u]; e < G->adj_ptr[u + 1]; e++) {
+                int64_t v = G->adj_idx[e];
+                if (v < u) continue;
+                double d = x[u] - x[v];
+                q = q + G->adj_c[e] * (d * d);
+                c = c + G->adj_c[e];
+            }
+            double ds = 1.0 - x[u], dt = x[u] + 1.0;
+            q = q + S->cs[u] * (ds * ds);
+            q = q + S->ct[u] * (dt * dt);
+            own[u] = q;
+            cap[u] = (c + S->cs[u]) + S->ct[u];
+        }
+        double xLx = orc_c3_sum(own, n) + 4.0 * G->c_st;
+        double C = 2.0 * (orc_c3_sum(cap, n) + G->c_st);
+        out3[0] = xLx / (2.0 * C); out3[1] = xLx; out3[2] = C;
+        *iters = rep.cg_iters;
+        if (x_out) memcpy(x_out, S->x, sizeof(double) * (size_t)n);
+    }
+    memcpy(S->x, xs, sizeof(double) * (size_t)n);
+    free(xs); free(b); free(own); free(cap);
     return rc;
 }

@@ -1585,7 +1585,10 @@ static irls_status tl_reserve(irls_ctx *c, int64_t entries)
 
 static double q_to_double(__int128 q, int32_t F) { return ldexp((double)q, -F); }
 
-static irls_status two_level_rank0(irls_ctx *c, const double *xfull, uint8_t *side, irls_two_level_report *r)
+// exact: no contraction (gamma0 = -inf, gamma1 = +inf, every node in Sc): the
+// exact min cut mu* of G by the same pipeline (for delta, Eq. 13).
+static irls_status two_level_rank0(irls_ctx *c, const double *xfull, uint8_t *side, irls_two_level_report *r,
+                                   bool exact = false)
 {
     auto t_start = std::chrono::steady_clock::now();
     cudaStream_t st = c->stream;
@@ -1607,7 +1610,9 @@ static irls_status two_level_rank0(irls_ctx *c, const double *xfull, uint8_t *si
     // 1. K-means (A25): batches of rounds, the device stops itself
     TLState h{0.1, 0.9, 0, 0};
     CK(cudaMemcpyAsync(b.st, &h, sizeof(h), cudaMemcpyHostToDevice, st));
-    if (n > 0) {
+    if (exact) {
+        h.done = 1;
+    } else if (n > 0) {
         RedArgs ra;
         ra.part = b.part;
         ra.slots = b.slots;
@@ -1622,7 +1627,7 @@ static irls_status two_level_rank0(irls_ctx *c, const double *xfull, uint8_t *si
             CK(cudaMemcpyAsync(&h, b.st, sizeof(h), cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
         }
-    } else {  // only the terminals' values {1, 0}
+    } else if (!exact) {  // only the terminals' values {1, 0}
         for (h.rounds = 1; h.rounds <= 100; h.rounds++) {
             double s0 = 0.0, s1 = 0.0;
             int64_t n1 = 0;
@@ -1638,11 +1643,12 @@ static irls_status two_level_rank0(irls_ctx *c, const double *xfull, uint8_t *si
         }
         if (h.rounds > 100) h.rounds = 100;
     }
+    if (exact) h.rounds = 0;
     if (isnan(h.c0) || isnan(h.c1)) return fail(c, IRLS_ERR_BAD_POTENTIAL, "NaN in potentials");
     r->c0 = h.c0;
     r->c1 = h.c1;
-    r->gamma0 = h.c0 + 0.05;
-    r->gamma1 = h.c1 - 0.05;
+    r->gamma0 = exact ? -INFINITY : h.c0 + 0.05;
+    r->gamma1 = exact ? INFINITY : h.c1 - 0.05;
     r->kmeans_rounds = h.rounds;
     // 2-3. classify, coarse ids / offsets, G_c
     const int64_t nt = tl_ntiles(n);
@@ -1814,6 +1820,17 @@ extern "C" irls_status irls_two_level_cut(irls_ctx *c, uint8_t *side, irls_two_l
     }
     if (msg.status) return fail(c, (irls_status)msg.status, c->rank == 0 ? c->err : "two-level failed on rank 0");
     if (rep) *rep = msg.rep;
+    return IRLS_OK;
+}
+
+extern "C" irls_status irls_exact_min_cut(irls_ctx *c, uint8_t *side, irls_two_level_report *rep)
+{
+    GUARD(c);
+    if (c->world > 1) return fail(c, IRLS_ERR_INVALID_ARGUMENT, "irls_exact_min_cut is single-process");
+    irls_two_level_report r;
+    irls_status s = two_level_rank0(c, c->x, side, &r, true);
+    if (s) return s;
+    if (rep) *rep = r;
     return IRLS_OK;
 }
 

@@ -78,7 +78,7 @@ SYMBOLS = ["irls_options_default", "irls_nccl_unique_id", "irls_mincut_create_st
            "irls_halo_plan", "irls_combine_slots", "irls_vgroup_create_stencil", "irls_vgroup_solve",
            "irls_vgroup_sweep_cut", "irls_vgroup_get_potentials", "irls_vgroup_set_terminal_weights",
            "irls_vgroup_destroy", "irls_two_level_cut", "irls_two_level_get_coarse", "irls_coarse_maxflow",
-           "irls_vgroup_two_level_cut"]
+           "irls_vgroup_two_level_cut", "irls_exact_min_cut"]
 
 
 def lib():
@@ -122,6 +122,7 @@ def lib():
         L.irls_vgroup_set_terminal_weights.argtypes = [P, P, P]
         L.irls_vgroup_destroy.argtypes = [P]
         L.irls_two_level_cut.argtypes = [P, P, C.POINTER(irls_two_level_report)]
+        L.irls_exact_min_cut.argtypes = [P, P, C.POINTER(irls_two_level_report)]
         L.irls_vgroup_two_level_cut.argtypes = [P, P, C.POINTER(irls_two_level_report)]
         L.irls_two_level_get_coarse.argtypes = [P] * 8
         L.irls_coarse_maxflow.argtypes = [C.c_int32, P, P, P, P, P, P, P, C.POINTER(C.c_int32)]
@@ -317,6 +318,13 @@ class MinCut:
         sd = np.zeros(self.n_total, dtype=np.uint8) if side else None
         r = irls_two_level_report()
         self._check(lib().irls_two_level_cut(self.h, _ptr(sd), C.byref(r)), "irls_two_level_cut")
+        return sd, r.as_dict()
+
+    def irls_exact_min_cut(self, side=True):
+        """mu* of the whole graph (no contraction): (side or None, report dict)."""
+        sd = np.zeros(self.n_total, dtype=np.uint8) if side else None
+        r = irls_two_level_report()
+        self._check(lib().irls_exact_min_cut(self.h, _ptr(sd), C.byref(r)), "irls_exact_min_cut")
         return sd, r.as_dict()
 
     def irls_two_level_get_coarse(self, nc, entries):
