@@ -180,6 +180,7 @@ def main():
     ap.add_argument("--ref-planes", type=int, default=8)
     ap.add_argument("--ref-T", type=int, default=3)
     ap.add_argument("--loop-mode", type=int, default=0)
+    ap.add_argument("--no-two-level", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -274,6 +275,17 @@ def main():
                                  "bytes_per_node": K1_BYTES_PER_NODE},
     }
     cg_iter_ms = t_k3 + t_k5
+    # two-level rounding of the same x^(T), once,
+    # outside the timed step: device phases + the host max-flow, timed apart
+    two_level = None
+    if not args.no_two_level:
+        _, tl = m.irls_two_level_cut(side=False)
+        two_level = {k: tl[k] for k in ("cut_value", "c0", "c1", "gamma0", "gamma1", "kmeans_rounds", "n0", "n1",
+                                        "nc", "coarse_nlinks", "certified", "ms_gpu", "ms_copy", "ms_maxflow",
+                                        "ms_total")}
+        two_level["sweep_cut_value"] = cut
+        two_level["what"] = ("two-level rounding of x^(T): K-means + coarsening + lift + cut on the GPU (ms_gpu), "
+                             "coarse graph D2H/H2D (ms_copy), exact max-flow on G_c on the host (ms_maxflow)")
     m.close()
 
     # ---- e2e through the C ABI with pinned host buffers ---------------------
@@ -340,6 +352,7 @@ def main():
                      else "fallback 6650 GB/s (B200_PROFILING.md)",
                      "frac_of_nominal_8TBps": ach / 8000.0, "kernels": kernels},
         "cpu_baseline": cpu,
+        "two_level": two_level,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_ms / args.e2e_steps,
                 "what": "create from pinned host arrays + solve + sweep (side to host) + destroy"},

@@ -198,6 +198,25 @@ irls_status irls_two_level_cut(irls_ctx *ctx, uint8_t *side, irls_two_level_repo
  * no solve; single process only; host memory ~60 B per n-link. */
 irls_status irls_exact_min_cut(irls_ctx *ctx, uint8_t *side, irls_two_level_report *rep);
 
+/* ---- Cheeger-type diagnostic (Theorem 4) ----
+ * lambda_2, the non-zero finite generalized eigenvalue of the pencil (L, D)
+ * (Eq. spectral; D = diag(d), d_s = d_t = C = 2 sum_e c_e),
+ * by its constrained-WLS characterisation: minimise
+ * (1/2C) x^T L x subject to x_s = 1, x_t = -1 on the capacities c (W = C).
+ * One cold Jacobi-PCG solve of the reduced system (Eq. 7 with f = (1,-1):
+ * b_u = cs_u - ct_u) with the given rtol / cap / norm (irls_cg_norm), then
+ * x^T L x and C by C3 (A30).  phi^2/2 <= lambda_2 <= 2 phi with phi =
+ * mu_star / C (Theorem 4).  The IRLS state (x, options) is restored afterwards.
+ * x_out: the solution v (n~ doubles, host) or NULL.  Single process. */
+typedef struct {
+    double lambda2, xLx, C, rel_res;
+    int32_t cg_iters, converged;
+    float ms;            /* device time of the solve */
+    int32_t launches;    /* kernels launched */
+} irls_lambda2_report;
+irls_status irls_lambda2(irls_ctx *ctx, double cg_rtol, int32_t cg_max_iter, int32_t cg_norm, double *x_out,
+                         irls_lambda2_report *rep);
+
 /* The coarse graph of the last irls_two_level_cut (rank 0, host copies), for
  * parity tests: cls [n~] per reduced node (0 = S0, 1 = S1, 2 = Sc); ptr
  * [nc+1], col [entries] (coarse ids, ascending; both directions stored), cap

@@ -411,7 +411,7 @@ static irls_status coll_minmax(Ranks &R, cudaStream_t st)
 static irls_status enq_assemble(Ranks &R, int mode, const CondArgs &cd, cudaStream_t st)
 {
     irls_status s;
-    if (R[0]->kind == 0 && mode != ASM_INIT && (s = coll_halo(R, false, st))) return s;
+    if (R[0]->kind == 0 && mode != ASM_INIT && mode != ASM_LAMBDA2 && (s = coll_halo(R, false, st))) return s;
     for (irls_ctx *c : R) {
         const VecArgs v = vec_args(c);
         const RedArgs ra = red_args(c);
@@ -518,7 +518,7 @@ static irls_status build_graph(irls_ctx *c, int mode)
     cd.finalize = 1;
     const int64_t lsave = c->launches;
     c->launches = 0;
-    if (mode == ASM_INIT) CK(cudaMemsetAsync(c->x, 0, sizeof(double) * c->n_own, st));
+    if (mode == ASM_INIT || mode == ASM_LAMBDA2) CK(cudaMemsetAsync(c->x, 0, sizeof(double) * c->n_own, st));
     irls_status s = enq_assemble(R, mode, cd, st);
     if (s) { cudaGraph_t g; cudaStreamEndCapture(st, &g); if (g) cudaGraphDestroy(g); return s; }
     if (mode == ASM_REWEIGHT_COLD) CK(cudaMemsetAsync(c->x, 0, sizeof(double) * c->n_own, st));
@@ -571,7 +571,7 @@ static irls_status enqueue_solve(Ranks &R, int mode)
     memset(&cd, 0, sizeof(cd));
     cd.use = 0;
     cd.finalize = c->world == 1 ? 1 : 0;
-    if (mode == ASM_INIT)
+    if (mode == ASM_INIT || mode == ASM_LAMBDA2)
         for (irls_ctx *d : R) CK(cudaMemsetAsync(d->x, 0, sizeof(double) * d->n_own, st));
     irls_status s = enq_assemble(R, mode, cd, st);
     if (s) return s;
@@ -1548,6 +1548,7 @@ static irls_status alloc_tl(irls_ctx *c)
     b.eoff = dalloc<int32_t>(c, n);
     b.scan_tmp = dalloc<int64_t>(c, nt + 1);
     b.tile_a = dalloc<__int128>(c, nt);
+    b.tile_n1 = dalloc<int32_t>(c, nt);
     b.cp = dalloc<int32_t>(c, n + 1);
     b.cqs = dalloc<__int128>(c, n);
     b.cqt = dalloc<__int128>(c, n);
@@ -1559,7 +1560,7 @@ static irls_status alloc_tl(irls_ctx *c)
     b.ccap = nullptr;
     b.cap_entries = 0;
     if (!b.st || !b.part || !b.slots || !b.ctrl || !b.cls || !b.flag || !b.cid || !b.deg || !b.eoff || !b.scan_tmp ||
-        !b.tile_a || !b.cp || !b.cqs || !b.cqt || !b.src || !b.prank || !b.one || !b.side)
+        !b.tile_a || !b.tile_n1 || !b.cp || !b.cqs || !b.cqt || !b.src || !b.prank || !b.one || !b.side)
         return fail(c, IRLS_ERR_OOM, "two-level buffers");
     const int64_t one = 1;
     CK(cudaMemcpyAsync(b.one, &one, sizeof(one), cudaMemcpyHostToDevice, c->stream));
@@ -1654,6 +1655,7 @@ static irls_status two_level_rank0(irls_ctx *c, const double *xfull, uint8_t *si
     const int64_t nt = tl_ntiles(n);
     int32_t last[4] = {0, 0, 0, 0};
     std::vector<__int128> tiles((size_t)std::max<int64_t>(nt, 1));
+    std::vector<int32_t> tiles_n1((size_t)std::max<int64_t>(nt, 1), 0);
     if (n > 0) {
         if (c->kind == 0) tl_classify_stencil(stencil_args(c, true), n, xfull, r->gamma0, r->gamma1, c->F, b, st);
         else tl_classify_sell(sell_args(c), xfull, r->gamma0, r->gamma1, c->F, b, st);
@@ -1665,6 +1667,7 @@ static irls_status two_level_rank0(irls_ctx *c, const double *xfull, uint8_t *si
         CK(cudaMemcpyAsync(&last[2], b.eoff + n - 1, 4, cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(&last[3], b.deg + n - 1, 4, cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(tiles.data(), b.tile_a, sizeof(__int128) * nt, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(tiles_n1.data(), b.tile_n1, sizeof(int32_t) * nt, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
     }
     const int64_t nc = (int64_t)last[0] + last[1], E = (int64_t)last[2] + last[3];
@@ -1770,15 +1773,9 @@ static irls_status two_level_rank0(irls_ctx *c, const double *xfull, uint8_t *si
     cudaEventDestroy(e5);
     r->ms_gpu = ms_a + ms_c;
     r->ms_copy = ms_b + ms_copy_back;
-    int64_t n0 = 0, n1 = 0;
-    {
-        // |S0| and |S1| from the scan totals: nc is known; count S1 on the host
-        // from the classes (cheap relative to the max-flow; n bytes D2H)
-        std::vector<int8_t> cls((size_t)std::max<int64_t>(n, 1));
-        if (n > 0) CK(memcpy_sync(c, cls.data(), b.cls, n, cudaMemcpyDeviceToHost));
-        for (int64_t i = 0; i < n; i++) n1 += cls[i] == 1;
-        n0 = n - n1 - nc;
-    }
+    int64_t n1 = 0;
+    for (int64_t i = 0; i < nt && n > 0; i++) n1 += tiles_n1[i];
+    const int64_t n0 = n - n1 - nc;
     r->n0 = n0;
     r->n1 = n1;
     r->nc = nc;
@@ -1897,5 +1894,77 @@ extern "C" irls_status irls_coarse_maxflow(int32_t nc, const int32_t *ptr, const
     if (stats[0] < 0) return IRLS_ERR_INVALID_ARGUMENT;
     put_words(flow, f);
     if (certified) *certified = (int32_t)stats[0];
+    return IRLS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Cheeger-type diagnostic lambda_2 (A30)
+// ---------------------------------------------------------------------------
+extern "C" irls_status irls_lambda2(irls_ctx *c, double cg_rtol, int32_t cg_max_iter, int32_t cg_norm, double *x_out,
+                                    irls_lambda2_report *rep)
+{
+    GUARD(c);
+    if (c->world > 1) return fail(c, IRLS_ERR_INVALID_ARGUMENT, "irls_lambda2 is single-process");
+    if (!(cg_rtol >= 0.0) || cg_max_iter < 0 || (cg_norm != 0 && cg_norm != 1))
+        return fail(c, IRLS_ERR_INVALID_ARGUMENT, "lambda2 CG options");
+    cudaStream_t st = c->stream;
+    const int64_t n = c->n_own;
+    double *xs = dalloc<double>(c, n);
+    if (!xs) return fail(c, IRLS_ERR_OOM, "lambda2 x save");
+    CK(cudaMemcpyAsync(xs, c->x, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    const int state0 = c->state;
+    const int64_t iters0 = c->last_cg_iters;
+    // the CG options live in the control block: set, solve, restore
+    DevCtrl *d = c->ctrl;
+    auto set_opts = [&](double rt, int32_t mi, int32_t nm) -> cudaError_t {
+        cudaError_t e = cudaMemcpyAsync(&d->rtol, &rt, sizeof(double), cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&d->max_iter, &mi, sizeof(int32_t), cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&d->norm, &nm, sizeof(int32_t), cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        return e;
+    };
+    CK(set_opts(cg_rtol, cg_max_iter, cg_norm));
+    irls_step_report sr;
+    int64_t total = 0;
+    Ranks R{c};
+    irls_status s = run_solves(R, ASM_LAMBDA2, ASM_LAMBDA2, 1, &sr, &total);
+    const int64_t launches = c->launches;
+    if (!s) {
+        RedArgs ra;
+        ra.part = c->part;
+        ra.slots = c->slots_local;
+        ra.ctrl = c->ctrl;
+        ra.K = c->K;
+        ra.g0 = 0;
+        ra.g1 = 8;
+        ra.n_fin = count_nonempty(ra.K, 0, 8);
+        if (c->kind == 0) launch_l2_quad_stencil(stencil_args(c, true), n, c->x, ra, st);
+        else launch_l2_quad_sell(sell_args(c), c->x, ra, st);
+        s = last_launch(c, "lambda2 quadratic form");
+    }
+    double slots[2 * kGroups];
+    memset(slots, 0, sizeof(slots));
+    if (!s && n > 0) CK(memcpy_sync(c, slots, c->slots_local, sizeof(slots), cudaMemcpyDeviceToHost));
+    if (!s && x_out && n > 0) CK(memcpy_sync(c, x_out, c->x, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpyAsync(c->x, xs, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    CK(set_opts(c->opt.cg_rtol, c->opt.cg_max_iter, c->opt.cg_norm));
+    CK(cudaFreeAsync(xs, st));
+    c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), (void *)xs), c->allocs.end());
+    CK(cudaStreamSynchronize(st));
+    c->state = state0;
+    c->last_cg_iters = iters0;
+    if (s) return s;
+    const double xLx = irls_combine_slots(slots) + 4.0 * c->c_st;
+    const double C = 2.0 * (irls_combine_slots(slots + kGroups) + c->c_st);
+    if (rep) {
+        rep->lambda2 = xLx / (2.0 * C);
+        rep->xLx = xLx;
+        rep->C = C;
+        rep->rel_res = sr.rel_res;
+        rep->cg_iters = sr.cg_iters;
+        rep->converged = sr.converged;
+        rep->ms = sr.ms;
+        rep->launches = (int32_t)(launches + 1);
+    }
     return IRLS_OK;
 }

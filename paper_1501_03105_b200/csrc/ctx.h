@@ -86,12 +86,12 @@ struct irls_ctx {
     __int128 h_qst = 0;
 
     // ---- graphs
-    cudaGraphExec_t gexec[3] = {nullptr, nullptr, nullptr};  // by assemble mode
+    cudaGraphExec_t gexec[4] = {nullptr, nullptr, nullptr, nullptr};  // by assemble mode
     cudaStream_t side_stream = nullptr;
 
     // ---- stats
     int64_t launches = 0, last_cg_iters = 0;
-    int64_t gl_fixed[3] = {0, 0, 0};  // kernels per solve graph outside the WHILE body
+    int64_t gl_fixed[4] = {0, 0, 0, 0};  // kernels per solve graph outside the WHILE body
     int64_t gl_body = 0;              // kernels per CG iteration (WHILE body)
     bool graph_iters_pending = false;
 };

@@ -9,7 +9,9 @@
 namespace irls {
 
 // Which assembly to run (Algorithm 1: step 2 vs step 4).
-enum AssembleMode { ASM_INIT = 0, ASM_REWEIGHT_WARM = 1, ASM_REWEIGHT_COLD = 2 };
+// ASM_LAMBDA2: W = C with the boundary x_s = 1, x_t = -1 (b = gs - gt), the
+// Cheeger diagnostic's constrained WLS.
+enum AssembleMode { ASM_INIT = 0, ASM_REWEIGHT_WARM = 1, ASM_REWEIGHT_COLD = 2, ASM_LAMBDA2 = 3 };
 
 // Per-node CG vectors (local indexing; owned nodes are [0, n_own); arrays
 // marked "ghost" also hold one plane below (negative indices) and above).
@@ -159,6 +161,7 @@ struct TLBuffers {
     int32_t *deg, *eoff;     // [n] coarse degree, coarse row offset (exclusive scan)
     int64_t *scan_tmp;
     __int128 *tile_a;        // [ntiles] s_c-t_c partials
+    int32_t *tile_n1;        // [ntiles] |S1| partials
     int32_t *cp;             // [n+1] coarse row pointer
     __int128 *cqs, *cqt;     // [n] coarse terminal links (by coarse id)
     int32_t *ccol;           // [cap_entries]
@@ -170,6 +173,9 @@ struct TLBuffers {
     uint8_t *side;           // [n_total]
 };
 int64_t tl_ntiles(int64_t n);
+// lambda2.cu: [x^T L x owned terms, owned capacities] -> slots (2 quantities)
+void launch_l2_quad_stencil(const StencilArgs &s, int64_t N, const double *x, const RedArgs &ra, cudaStream_t st);
+void launch_l2_quad_sell(const SellArgs &s, const double *x, const RedArgs &ra, cudaStream_t st);
 void tl_kmeans_round(const double *x, int64_t n, TLState *st, const RedArgs &ra, cudaStream_t stream);
 void tl_classify_stencil(const StencilArgs &s, int64_t N, const double *x, double g0, double g1, int32_t F,
                          TLBuffers &b, cudaStream_t st);

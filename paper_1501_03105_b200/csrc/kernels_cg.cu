@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(kThreads) k_stencil_assemble(StencilArgs s, Ve
         const bool px = c.x < s.nx - 1, py = c.y < s.ny - 1, pz = c.z < s.nz - 1;
         double xu = 0.0, xmz = 0.0, xmy = 0.0, xmx = 0.0, xpx = 0.0, xpy = 0.0, xpz = 0.0;
         double gmz = 0.0, gmy = 0.0, gmx = 0.0, gpx = 0.0, gpy = 0.0, gpz = 0.0, gs, gt;
-        if (MODE == ASM_INIT) {  // W^(0) = C: g = c
+        if (MODE == ASM_INIT || MODE == ASM_LAMBDA2) {  // W^(0) = C: g = c
             if (hz) gmz = s.cz[u - P];
             if (hy) gmy = s.cy[u - s.nx];
             if (hx) gmx = s.cx[u - 1];
@@ -110,17 +110,18 @@ __global__ void __launch_bounds__(kThreads) k_stencil_assemble(StencilArgs s, Ve
             if (pz) a2 = a2 + gpz * xpz;
             r = gs - (D * xu - a2);
         } else {  // x0 = 0: r0 = b exactly
-            r = gs;
+            r = MODE == ASM_LAMBDA2 ? gs - gt : gs;
         }
         const double zr = r * Dinv;
         v.r[u] = r;
         v.z[u] = zr;
-        const double mb = gs * Dinv;
+        const double bu = MODE == ASM_LAMBDA2 ? gs - gt : gs;
+        const double mb = bu * Dinv;
         acc[0] = acc[0] + r * zr;
         acc[1] = acc[1] + zr * zr;
         acc[2] = acc[2] + r * r;
         acc[3] = acc[3] + mb * mb;
-        acc[4] = acc[4] + gs * gs;
+        acc[4] = acc[4] + bu * bu;
     })
     if (c3_chunk_epilogue<5>(acc, v.chunk0 + (int32_t)blockIdx.x, ra) && cd.finalize && threadIdx.x == 0) {
         finalize_start(ra.ctrl, ra.slots);
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(kThreads) k_sell_assemble(SellArgs s, VecArgs 
         const int64_t sl = u / kSell;
         const int64_t e0 = s.slice_ptr[sl] + (u % kSell);
         const int32_t W = (int32_t)((s.slice_ptr[sl + 1] - s.slice_ptr[sl]) / kSell);
-        const double xu = MODE == ASM_INIT ? 0.0 : v.x[u];
+        const double xu = (MODE == ASM_INIT || MODE == ASM_LAMBDA2) ? 0.0 : v.x[u];
         double a = 0.0, a2 = 0.0;
         for (int32_t k = 0; k < W; k++) {
             const int64_t idx = e0 + kSell * (int64_t)k;
@@ -145,7 +146,7 @@ __global__ void __launch_bounds__(kThreads) k_sell_assemble(SellArgs s, VecArgs 
             if (nb < 0) break;
             const double c = s.c[idx];
             double g;
-            if (MODE == ASM_INIT) {
+            if (MODE == ASM_INIT || MODE == ASM_LAMBDA2) {
                 g = c;
             } else {
                 const double xv = v.x[nb];
@@ -155,23 +156,24 @@ __global__ void __launch_bounds__(kThreads) k_sell_assemble(SellArgs s, VecArgs 
             s.g[idx] = g;
             a = a + g;
         }
-        const double gs = MODE == ASM_INIT ? s.cs[u] : rw_g(s.cs[u], 1.0 - xu, eps2);
-        const double gt = MODE == ASM_INIT ? s.ct[u] : rw_g(s.ct[u], xu, eps2);
+        const double gs = (MODE == ASM_INIT || MODE == ASM_LAMBDA2) ? s.cs[u] : rw_g(s.cs[u], 1.0 - xu, eps2);
+        const double gt = (MODE == ASM_INIT || MODE == ASM_LAMBDA2) ? s.ct[u] : rw_g(s.ct[u], xu, eps2);
         const double D = (a + gs) + gt;
         const double Dinv = 1.0 / D;
         v.D[u] = D;
         v.Dinv[u] = Dinv;
         if (gs_out) { gs_out[u] = gs; gt_out[u] = gt; }
-        const double r = MODE == ASM_REWEIGHT_WARM ? gs - (D * xu - a2) : gs;
+        const double r = MODE == ASM_REWEIGHT_WARM ? gs - (D * xu - a2) : (MODE == ASM_LAMBDA2 ? gs - gt : gs);
         const double zr = r * Dinv;
         v.r[u] = r;
         v.z[u] = zr;
-        const double mb = gs * Dinv;
+        const double bu = MODE == ASM_LAMBDA2 ? gs - gt : gs;
+        const double mb = bu * Dinv;
         acc[0] = acc[0] + r * zr;
         acc[1] = acc[1] + zr * zr;
         acc[2] = acc[2] + r * r;
         acc[3] = acc[3] + mb * mb;
-        acc[4] = acc[4] + gs * gs;
+        acc[4] = acc[4] + bu * bu;
     })
     if (c3_chunk_epilogue<5>(acc, v.chunk0 + (int32_t)blockIdx.x, ra) && cd.finalize && threadIdx.x == 0) {
         finalize_start(ra.ctrl, ra.slots);
@@ -500,6 +502,8 @@ int launch_stencil_assemble_ex(const StencilArgs &s, const VecArgs &v, const Red
     const double eps2 = eps * eps;
     const unsigned nb = nblocks(v.n_own);
     if (mode == ASM_INIT) k_stencil_assemble<ASM_INIT><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
+    else if (mode == ASM_LAMBDA2)
+        k_stencil_assemble<ASM_LAMBDA2><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
     else if (mode == ASM_REWEIGHT_WARM)
         k_stencil_assemble<ASM_REWEIGHT_WARM><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
     else k_stencil_assemble<ASM_REWEIGHT_COLD><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
@@ -519,6 +523,8 @@ int launch_sell_assemble_ex(const SellArgs &s, const VecArgs &v, const RedArgs &
     const double eps2 = eps * eps;
     const unsigned nb = nblocks(v.n_own);
     if (mode == ASM_INIT) k_sell_assemble<ASM_INIT><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
+    else if (mode == ASM_LAMBDA2)
+        k_sell_assemble<ASM_LAMBDA2><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
     else if (mode == ASM_REWEIGHT_WARM)
         k_sell_assemble<ASM_REWEIGHT_WARM><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
     else k_sell_assemble<ASM_REWEIGHT_COLD><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);

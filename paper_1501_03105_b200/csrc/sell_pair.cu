@@ -43,7 +43,8 @@ __global__ void __launch_bounds__(kThreads) k_sellp_assemble(SellArgs s, VecArgs
                                                              double eps2, double *gs_out, double *gt_out)
 {
     constexpr bool WARM = MODE == ASM_REWEIGHT_WARM;
-    constexpr bool HASX = MODE != ASM_INIT;
+    constexpr bool INITG = MODE == ASM_INIT || MODE == ASM_LAMBDA2;  // g = c
+    constexpr bool HASX = !INITG;
     const int64_t base = (int64_t)blockIdx.x * kChunk;
     double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll 1
@@ -82,12 +83,12 @@ __global__ void __launch_bounds__(kThreads) k_sellp_assemble(SellArgs s, VecArgs
             if (k < W) {
                 double g0 = 0.0, g1 = 0.0;
                 if (cl[k].x >= 0) {
-                    g0 = MODE == ASM_INIT ? cc[k].x : rw_g(cc[k].x, x2.x - xa[k], eps2);
+                    g0 = INITG ? cc[k].x : rw_g(cc[k].x, x2.x - xa[k], eps2);
                     a0 = a0 + g0;
                     if (WARM) b0 = b0 + g0 * xa[k];
                 }
                 if (cl[k].y >= 0) {
-                    g1 = MODE == ASM_INIT ? cc[k].y : rw_g(cc[k].y, x2.y - xb[k], eps2);
+                    g1 = INITG ? cc[k].y : rw_g(cc[k].y, x2.y - xb[k], eps2);
                     a1 = a1 + g1;
                     if (WARM) b1 = b1 + g1 * xb[k];
                 }
@@ -95,7 +96,7 @@ __global__ void __launch_bounds__(kThreads) k_sellp_assemble(SellArgs s, VecArgs
             }
         }
         double2 gs2, gt2;
-        if (MODE == ASM_INIT) {
+        if (INITG) {
             gs2 = cs2;
             gt2 = ct2;
         } else {
@@ -104,8 +105,10 @@ __global__ void __launch_bounds__(kThreads) k_sellp_assemble(SellArgs s, VecArgs
         }
         const double D0 = (a0 + gs2.x) + gt2.x, D1 = (a1 + gs2.y) + gt2.y;
         const double Di0 = 1.0 / D0, Di1 = v1 ? 1.0 / D1 : 0.0;
-        const double r0 = WARM ? gs2.x - (D0 * x2.x - b0) : gs2.x;
-        const double r1 = v1 ? (WARM ? gs2.y - (D1 * x2.y - b1) : gs2.y) : 0.0;
+        const double bb0 = MODE == ASM_LAMBDA2 ? gs2.x - gt2.x : gs2.x;
+        const double bb1 = MODE == ASM_LAMBDA2 ? gs2.y - gt2.y : gs2.y;
+        const double r0 = WARM ? gs2.x - (D0 * x2.x - b0) : bb0;
+        const double r1 = v1 ? (WARM ? gs2.y - (D1 * x2.y - b1) : bb1) : 0.0;
         const double z0 = r0 * Di0, z1 = r1 * Di1;
         stp2(v.D, u0, make_double2(D0, v1 ? D1 : 0.0));
         stp2(v.Dinv, u0, make_double2(Di0, Di1));
@@ -115,19 +118,19 @@ __global__ void __launch_bounds__(kThreads) k_sellp_assemble(SellArgs s, VecArgs
             stp2(gs_out, u0, gs2);
             stp2(gt_out, u0, gt2);
         }
-        const double mb0 = gs2.x * Di0;
+        const double mb0 = bb0 * Di0;
         acc[0] = acc[0] + r0 * z0;
         acc[1] = acc[1] + z0 * z0;
         acc[2] = acc[2] + r0 * r0;
         acc[3] = acc[3] + mb0 * mb0;
-        acc[4] = acc[4] + gs2.x * gs2.x;
+        acc[4] = acc[4] + bb0 * bb0;
         if (v1) {
-            const double mb1 = gs2.y * Di1;
+            const double mb1 = bb1 * Di1;
             acc[0] = acc[0] + r1 * z1;
             acc[1] = acc[1] + z1 * z1;
             acc[2] = acc[2] + r1 * r1;
             acc[3] = acc[3] + mb1 * mb1;
-            acc[4] = acc[4] + gs2.y * gs2.y;
+            acc[4] = acc[4] + bb1 * bb1;
         }
     }
     if (c3_chunk_epilogue<5>(acc, v.chunk0 + (int32_t)blockIdx.x, ra) && cd.finalize && threadIdx.x == 0) {
@@ -209,6 +212,8 @@ static void asm_w(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const 
 {
     const unsigned nb = nblk3(v.n_own);
     if (mode == ASM_INIT) k_sellp_assemble<WMAX, ASM_INIT><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
+    else if (mode == ASM_LAMBDA2)
+        k_sellp_assemble<WMAX, ASM_LAMBDA2><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
     else if (mode == ASM_REWEIGHT_WARM)
         k_sellp_assemble<WMAX, ASM_REWEIGHT_WARM><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
     else k_sellp_assemble<WMAX, ASM_REWEIGHT_COLD><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);

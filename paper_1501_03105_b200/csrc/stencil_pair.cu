@@ -127,7 +127,8 @@ __global__ void __launch_bounds__(kThreads) k_pair_nodes(StencilArgs s, VecArgs 
     const int64_t P = s.P;
     const double2 zero2 = make_double2(0.0, 0.0);
     constexpr bool WARM = MODE == ASM_REWEIGHT_WARM;
-    constexpr bool HASX = MODE != ASM_INIT;
+    constexpr bool INITG = MODE == ASM_INIT || MODE == ASM_LAMBDA2;  // g = c
+    constexpr bool HASX = !INITG;
     double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll 1
     for (int j = 0; j < 8; j++) {
@@ -163,7 +164,7 @@ __global__ void __launch_bounds__(kThreads) k_pair_nodes(StencilArgs s, VecArgs 
         if (!hx) { gxl = 0.0; xl = 0.0; }
         if (!hr) xr = 0.0;
         double2 gs2, gt2;
-        if (MODE == ASM_INIT) {
+        if (INITG) {
             gs2 = cs2;
             gt2 = ct2;
         } else {
@@ -193,8 +194,8 @@ __global__ void __launch_bounds__(kThreads) k_pair_nodes(StencilArgs s, VecArgs 
             b = b + gz2.y * xpz.y;
             r1 = gs2.y - (D1 * x2.y - b);
         } else {
-            r0 = gs2.x;
-            r1 = gs2.y;
+            r0 = MODE == ASM_LAMBDA2 ? gs2.x - gt2.x : gs2.x;
+            r1 = MODE == ASM_LAMBDA2 ? gs2.y - gt2.y : gs2.y;
         }
         const double z0 = r0 * Di0, z1 = r1 * Di1;
         stp(v.D, u0, make_double2(D0, D1));
@@ -205,17 +206,19 @@ __global__ void __launch_bounds__(kThreads) k_pair_nodes(StencilArgs s, VecArgs 
             stp(gs_out, u0, gs2);
             stp(gt_out, u0, gt2);
         }
-        const double mb0 = gs2.x * Di0, mb1 = gs2.y * Di1;
+        const double b0 = MODE == ASM_LAMBDA2 ? gs2.x - gt2.x : gs2.x;
+        const double b1 = MODE == ASM_LAMBDA2 ? gs2.y - gt2.y : gs2.y;
+        const double mb0 = b0 * Di0, mb1 = b1 * Di1;
         acc[0] = acc[0] + r0 * z0;
         acc[1] = acc[1] + z0 * z0;
         acc[2] = acc[2] + r0 * r0;
         acc[3] = acc[3] + mb0 * mb0;
-        acc[4] = acc[4] + gs2.x * gs2.x;
+        acc[4] = acc[4] + b0 * b0;
         acc[0] = acc[0] + r1 * z1;
         acc[1] = acc[1] + z1 * z1;
         acc[2] = acc[2] + r1 * r1;
         acc[3] = acc[3] + mb1 * mb1;
-        acc[4] = acc[4] + gs2.y * gs2.y;
+        acc[4] = acc[4] + b1 * b1;
     }
     if (c3_chunk_epilogue<5>(acc, v.chunk0 + (int32_t)blockIdx.x, ra) && cd.finalize && threadIdx.x == 0) {
         finalize_start(ra.ctrl, ra.slots);
@@ -392,9 +395,10 @@ int launch_pair_assemble(const StencilArgs &s, const VecArgs &v, const RedArgs &
 {
     const double eps2 = eps * eps;
     const unsigned nb = nblk(v.n_own);
-    if (mode == ASM_INIT) {
+    if (mode == ASM_INIT || mode == ASM_LAMBDA2) {
         k_pair_edges<true><<<nb, kThreads, 0, st>>>(s, v, eps2);
-        k_pair_nodes<ASM_INIT><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
+        if (mode == ASM_INIT) k_pair_nodes<ASM_INIT><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
+        else k_pair_nodes<ASM_LAMBDA2><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
     } else {
         k_pair_edges<false><<<nb, kThreads, 0, st>>>(s, v, eps2);
         if (mode == ASM_REWEIGHT_WARM)

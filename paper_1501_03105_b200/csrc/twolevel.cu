@@ -71,9 +71,12 @@ __global__ void __launch_bounds__(kThreads) k_tl_kmeans(const double *x, int64_t
 }
 
 // Partition of the block's tile of int128 values into one block total.
-__device__ __forceinline__ void tl_block_sum_i128(i128 v, i128 *out)
+__device__ __forceinline__ void tl_block_sum_i128(i128 v, i128 *out, int32_t cnt, int32_t *cnt_out)
 {
     __shared__ unsigned long long sm[2][8];
+    __shared__ int32_t sc[8];
+    for (int off = 16; off >= 1; off >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, off);
+    if ((threadIdx.x & 31) == 0) sc[threadIdx.x >> 5] = cnt;
     for (int off = 16; off >= 1; off >>= 1) {
         unsigned long long lo = (unsigned long long)v, hi = (unsigned long long)(v >> 64);
         lo = __shfl_down_sync(0xffffffffu, lo, off);
@@ -87,8 +90,13 @@ __device__ __forceinline__ void tl_block_sum_i128(i128 v, i128 *out)
     __syncthreads();
     if (threadIdx.x == 0) {
         i128 s = 0;
-        for (int i = 0; i < 8; i++) s += ((i128)sm[1][i] << 64) | (i128)sm[0][i];
+        int32_t c = 0;
+        for (int i = 0; i < 8; i++) {
+            s += ((i128)sm[1][i] << 64) | (i128)sm[0][i];
+            c += sc[i];
+        }
         *out = s;
+        *cnt_out = c;
     }
 }
 
@@ -97,9 +105,10 @@ __device__ __forceinline__ void tl_block_sum_i128(i128 v, i128 *out)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_tl_classify_stencil(StencilArgs s, int64_t N, const double *x, double g0,
                                                              double g1, int32_t F, int8_t *cls, int32_t *flag,
-                                                             int32_t *deg, i128 *tile_a)
+                                                             int32_t *deg, i128 *tile_a, int32_t *tile_n1)
 {
     i128 a = 0;
+    int32_t n1 = 0;
     const int64_t base = (int64_t)blockIdx.x * kTlTile;
     for (int r = 0; r < 16; r++) {
         const int64_t v = base + r * 256 + threadIdx.x;
@@ -133,17 +142,19 @@ __global__ void __launch_bounds__(256) k_tl_classify_stencil(StencilArgs s, int6
         }
 #undef NB
         deg[v] = d;
+        n1 += cv == 1;
         if (cv == 1) a += q0 + qfix(s.ct[v], F);
         else if (cv == 0) a += qfix(s.cs[v], F);
     }
-    tl_block_sum_i128(a, tile_a + blockIdx.x);
+    tl_block_sum_i128(a, tile_a + blockIdx.x, n1, tile_n1 + blockIdx.x);
 }
 
 __global__ void __launch_bounds__(256) k_tl_classify_sell(SellArgs s, const double *x, double g0, double g1,
                                                           int32_t F, int8_t *cls, int32_t *flag, int32_t *deg,
-                                                          i128 *tile_a)
+                                                          i128 *tile_a, int32_t *tile_n1)
 {
     i128 a = 0;
+    int32_t n1 = 0;
     const int64_t base = (int64_t)blockIdx.x * kTlTile;
     for (int r = 0; r < 16; r++) {
         const int64_t v = base + r * 256 + threadIdx.x;
@@ -170,10 +181,11 @@ __global__ void __launch_bounds__(256) k_tl_classify_sell(SellArgs s, const doub
             }
         }
         deg[v] = d;
+        n1 += cv == 1;
         if (cv == 1) a += q0 + qfix(s.ct[v], F);
         else if (cv == 0) a += qfix(s.cs[v], F);
     }
-    tl_block_sum_i128(a, tile_a + blockIdx.x);
+    tl_block_sum_i128(a, tile_a + blockIdx.x, n1, tile_n1 + blockIdx.x);
 }
 
 // ---------------------------------------------------------------------------
@@ -280,13 +292,14 @@ void tl_classify_stencil(const StencilArgs &s, int64_t N, const double *x, doubl
                          TLBuffers &b, cudaStream_t st)
 {
     k_tl_classify_stencil<<<(unsigned)tl_ntiles(N), 256, 0, st>>>(s, N, x, g0, g1, F, b.cls, b.flag, b.deg,
-                                                                   b.tile_a);
+                                                                   b.tile_a, b.tile_n1);
 }
 
 void tl_classify_sell(const SellArgs &s, const double *x, double g0, double g1, int32_t F, TLBuffers &b,
                       cudaStream_t st)
 {
-    k_tl_classify_sell<<<(unsigned)tl_ntiles(s.n), 256, 0, st>>>(s, x, g0, g1, F, b.cls, b.flag, b.deg, b.tile_a);
+    k_tl_classify_sell<<<(unsigned)tl_ntiles(s.n), 256, 0, st>>>(s, x, g0, g1, F, b.cls, b.flag, b.deg, b.tile_a,
+                                                                b.tile_n1);
 }
 
 void tl_fill_stencil(const StencilArgs &s, int64_t N, const double *x, double g0, double g1, int32_t F,

@@ -63,6 +63,14 @@ class irls_two_level_report(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad"}
 
 
+class irls_lambda2_report(C.Structure):
+    _fields_ = [("lambda2", C.c_double), ("xLx", C.c_double), ("C", C.c_double), ("rel_res", C.c_double),
+                ("cg_iters", C.c_int32), ("converged", C.c_int32), ("ms", C.c_float), ("launches", C.c_int32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 class irls_stats(C.Structure):
     _fields_ = [("launches", C.c_int64), ("cg_iters", C.c_int64), ("n_nonterminal", C.c_int64),
                 ("n_links", C.c_int64), ("n_local", C.c_int64)]
@@ -78,7 +86,7 @@ SYMBOLS = ["irls_options_default", "irls_nccl_unique_id", "irls_mincut_create_st
            "irls_halo_plan", "irls_combine_slots", "irls_vgroup_create_stencil", "irls_vgroup_solve",
            "irls_vgroup_sweep_cut", "irls_vgroup_get_potentials", "irls_vgroup_set_terminal_weights",
            "irls_vgroup_destroy", "irls_two_level_cut", "irls_two_level_get_coarse", "irls_coarse_maxflow",
-           "irls_vgroup_two_level_cut", "irls_exact_min_cut"]
+           "irls_vgroup_two_level_cut", "irls_exact_min_cut", "irls_lambda2"]
 
 
 def lib():
@@ -122,6 +130,7 @@ def lib():
         L.irls_vgroup_set_terminal_weights.argtypes = [P, P, P]
         L.irls_vgroup_destroy.argtypes = [P]
         L.irls_two_level_cut.argtypes = [P, P, C.POINTER(irls_two_level_report)]
+        L.irls_lambda2.argtypes = [P, C.c_double, C.c_int32, C.c_int32, P, C.POINTER(irls_lambda2_report)]
         L.irls_exact_min_cut.argtypes = [P, P, C.POINTER(irls_two_level_report)]
         L.irls_vgroup_two_level_cut.argtypes = [P, P, C.POINTER(irls_two_level_report)]
         L.irls_two_level_get_coarse.argtypes = [P] * 8
@@ -319,6 +328,13 @@ class MinCut:
         r = irls_two_level_report()
         self._check(lib().irls_two_level_cut(self.h, _ptr(sd), C.byref(r)), "irls_two_level_cut")
         return sd, r.as_dict()
+
+    def irls_lambda2(self, cg_rtol=1e-12, cg_max_iter=100000, cg_norm=IRLS_NORM_UNPRECONDITIONED, want_x=False):
+        """Cheeger-type diagnostic (A30): report dict (+ the solution v)."""
+        x = np.zeros(max(self.n, 1)) if want_x else None
+        r = irls_lambda2_report()
+        self._check(lib().irls_lambda2(self.h, cg_rtol, cg_max_iter, cg_norm, _ptr(x), C.byref(r)), "irls_lambda2")
+        return (r.as_dict(), x[: self.n]) if want_x else r.as_dict()
 
     def irls_exact_min_cut(self, side=True):
         """mu* of the whole graph (no contraction): (side or None, report dict)."""

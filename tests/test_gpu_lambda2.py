@@ -1,0 +1,93 @@
+"""GPU parity of the Cheeger-type diagnostic lambda_2 (
+P:L543-551): the CUDA path (the assembly kernels in
+their x_t = -1 mode, the CG loop, the quadratic-form kernel) through the C
+ABI against the oracle — bitwise equal lambda_2, x^T L x, C, CG iteration
+count and solution v; the IRLS state is unchanged by the call."""
+import numpy as np
+import pytest
+
+import oracle
+from synthetic import generators as gen
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def irls():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1501_03105_b200 import build, irls as I
+    build.build()
+    return I
+
+
+def _bitwise(a, b):
+    return np.array_equal(np.asarray(a, dtype=np.float64).view(np.uint64),
+                          np.asarray(b, dtype=np.float64).view(np.uint64))
+
+
+def check(I, spec, rtol=1e-10, cap=100000, norm=1, **opts):
+    m = I.MinCut.from_spec(spec, I.options(**opts))
+    r, xg = m.irls_lambda2(cg_rtol=rtol, cg_max_iter=cap, cg_norm=norm, want_x=True)
+    S = oracle.Solver(oracle.Graph(spec))
+    lam, xLx, C, it, xo = S.lambda2(rtol=rtol, max_iter=cap, norm=norm, want_x=True)
+    assert r["cg_iters"] == it
+    assert _bitwise(xg, xo)
+    assert (r["lambda2"], r["xLx"], r["C"]) == (lam, xLx, C)
+    return m, r
+
+
+@pytest.mark.parametrize("name", ["path", "cycle4", "path4", "triangle", "path_sym"])
+def test_tiny(irls, name):
+    m, r = check(irls, gen.tiny_graphs()[name])
+    if name == "path_sym":
+        assert r["lambda2"] == 0.25  # S:L495 (scale-free)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_random_csr(irls, seed):
+    check(irls, gen.random_small_graph(400, 700, seed=990 + seed))
+
+
+@pytest.mark.parametrize("shape", [(48, 40, 24), (33, 17, 9)])
+@pytest.mark.parametrize("norm", [0, 1])
+def test_blob_grids(irls, shape, norm):
+    check(irls, gen.blob_grid(*shape, seed=1, sigma=(3.0, 9.0)), rtol=1e-8, cap=5000, norm=norm)
+
+
+def test_capped_solve(irls):
+    """The paper's cap (50 iterations) — a capped, inexact lambda_2, still bitwise."""
+    m, r = check(irls, gen.blob_grid(40, 40, 10, seed=2, sigma=(3.0, 8.0)), rtol=1e-3, cap=50, norm=0)
+    assert r["cg_iters"] <= 50
+
+
+def test_road_csr(irls):
+    check(irls, gen.road_graph(80, seed=2, knn=50), rtol=1e-8, cap=20000)
+
+
+def test_state_restored(irls):
+    """lambda_2 between IRLS steps leaves x and the trajectory unchanged."""
+    spec = gen.blob_grid(32, 20, 8, seed=3, sigma=(2.0, 6.0))
+    m = irls.MinCut.from_spec(spec, irls.options(T=4))
+    S = oracle.Solver(oracle.Graph(spec), T=4)
+    m.irls_init(); S.init()
+    m.irls_step(); S.step()
+    x = m.irls_get_potentials()
+    m.irls_lambda2(cg_rtol=1e-6, cg_max_iter=1000)
+    assert _bitwise(m.irls_get_potentials(), x)
+    rg = m.irls_step(); ro = S.step()
+    assert rg["cg_iters"] == ro["cg_iters"] and _bitwise(m.irls_get_potentials(), S.x())
+    assert m.irls_get_stats()["cg_iters"] == rg["cg_iters"]
+
+
+@pytest.mark.slow
+def test_config2_full_size(irls):
+    """Config 2 at full size at the paper's tolerance and cap (rtol 1e-3
+    preconditioned, 50): bitwise; Theorem 4's upper bound with the sweep cut
+    as an upper bound of mu*: lambda_2 <= 2 phi <= 2 sweep/C."""
+    spec = gen.config2()
+    m, r = check(irls, spec, rtol=1e-3, cap=50, norm=0, T=50)
+    m.irls_solve(irls.IRLS_FROM_SCRATCH, T=50, reports=False)
+    _, _, _, cut = m.irls_sweep_cut(side=False)
+    assert r["lambda2"] > 0.0
