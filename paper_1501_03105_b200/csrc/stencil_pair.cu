@@ -226,6 +226,135 @@ __global__ void __launch_bounds__(kThreads) k_pair_nodes(StencilArgs s, VecArgs 
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// K1 fused (reweight steps, nx a multiple of 512): one pass per chunk.  With
+// nx = 512 m, thread t's pair of iteration j has its -y neighbour pair in
+// iteration j - m of the SAME thread (same x), so the -y conductance comes
+// from a thread-private shared-memory ring (no barrier); -x comes from the
+// adjacent lane by shuffle (lane 0 recomputes it); -z (another chunk) and -y
+// of the first m iterations are recomputed.  Same formula and operand order
+// as the owner's computation, so the bits equal K1a + K1b and the oracle.
+// 104 B/node of compulsory traffic instead of 136.
+// ---------------------------------------------------------------------------
+template <int MODE, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_pair_fused(StencilArgs s, VecArgs v, RedArgs ra, CondArgs cd,
+                                                            double eps2, double *gs_out, double *gt_out)
+{
+    __shared__ double2 ring[8][kThreads];
+    const int lane = threadIdx.x & 31;
+    const int64_t base = (int64_t)blockIdx.x * kChunk;
+    const int64_t P = s.P;
+    const int m = s.nx >> 9;
+    const double2 zero2 = make_double2(0.0, 0.0);
+    constexpr bool WARM = MODE == ASM_REWEIGHT_WARM;
+    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll 1
+    for (int j = 0; j < 8; j++) {
+        const int64_t u0 = base + 2 * (int64_t)threadIdx.x + 512 * j;
+        const bool valid = u0 < v.n_own;
+        const PairCoord c = pair_coord(s, s.lo + u0);
+        const bool hx = c.x0 > 0, hr = c.x0 + 1 < s.nx - 1;
+        const bool hy = valid && c.y > 0, py = valid && c.y < s.ny - 1;
+        const bool hz = valid && c.z > 0, pz = valid && c.z < s.nz - 1;
+        const bool ring_y = j >= m;  // -y pair computed by this thread in iteration j - m
+        // ---- loads first
+        const double2 x2 = valid ? ldp(v.x, u0) : zero2;
+        const double2 cx2 = valid ? ldp(s.cx, u0) : zero2;
+        const double2 cy2 = py ? ldp(s.cy, u0) : zero2, cz2 = pz ? ldp(s.cz, u0) : zero2;
+        const double2 cs2 = valid ? ldp(s.cs, u0) : zero2, ct2 = valid ? ldp(s.ct, u0) : zero2;
+        const double2 xpy = py ? ldp(v.x, u0 + s.nx) : zero2, xpz = pz ? ldp(v.x, u0 + P) : zero2;
+        const double2 xmz = hz ? ldp(v.x, u0 - P) : zero2, czm = hz ? ldp(s.cz, u0 - P) : zero2;
+        const double2 xmy = (hy && (WARM || !ring_y)) ? ldp(v.x, u0 - s.nx) : zero2;
+        const double2 cym = (hy && !ring_y) ? ldp(s.cy, u0 - s.nx) : zero2;
+        double xle = 0.0, cxle = 0.0, xre = 0.0;
+        if (valid && lane == 0 && hx) {
+            xle = __ldg(v.x + u0 - 1);
+            cxle = __ldg(s.cx + u0 - 1);
+        }
+        if (valid && lane == 31 && hr) xre = __ldg(v.x + u0 + 2);
+        double xl = __shfl_up_sync(0xffffffffu, x2.y, 1);
+        double xr = __shfl_down_sync(0xffffffffu, x2.x, 1);
+        if (lane == 0) xl = xle;
+        if (lane == 31) xr = xre;
+        if (!hx) xl = 0.0;
+        if (!hr) xr = 0.0;
+        // ---- owned edges (K1a)
+        double2 gx2;
+        gx2.x = valid ? rw_g(cx2.x, x2.x - x2.y, eps2) : 0.0;
+        gx2.y = (valid && hr) ? rw_g(cx2.y, x2.y - xr, eps2) : 0.0;
+        double gxl = __shfl_up_sync(0xffffffffu, gx2.y, 1);
+        if (!valid) continue;
+        if (lane == 0) gxl = hx ? rw_g(cxle, xl - x2.x, eps2) : 0.0;
+        if (!hx) gxl = 0.0;
+        const double2 gy2 = py ? make_double2(rw_g(cy2.x, x2.x - xpy.x, eps2), rw_g(cy2.y, x2.y - xpy.y, eps2)) : zero2;
+        const double2 gz2 = pz ? make_double2(rw_g(cz2.x, x2.x - xpz.x, eps2), rw_g(cz2.y, x2.y - xpz.y, eps2)) : zero2;
+        // ---- lower-neighbour edges: ring (-y), recompute (-z, first rows' -y)
+        double2 gym = zero2;
+        if (hy) gym = ring_y ? ring[j - m][threadIdx.x]
+                             : make_double2(rw_g(cym.x, xmy.x - x2.x, eps2), rw_g(cym.y, xmy.y - x2.y, eps2));
+        ring[j][threadIdx.x] = gy2;
+        const double2 gzm = hz ? make_double2(rw_g(czm.x, xmz.x - x2.x, eps2), rw_g(czm.y, xmz.y - x2.y, eps2)) : zero2;
+        stp(s.gx, u0, gx2);
+        stp(s.gy, u0, gy2);
+        stp(s.gz, u0, gz2);
+        if (s.lo_ghost && u0 < P) stp(s.gz, u0 - P, gzm);  // the -z edge of the first owned plane (ghost slot)
+        // ---- terminals, D, Dinv, r0, z0 (K1b)
+        double2 gs2, gt2;
+        gs2.x = terminal_g(cs2.x, ct2.x, x2.x, eps2, gt2.x);
+        gs2.y = terminal_g(cs2.y, ct2.y, x2.y, eps2, gt2.y);
+        const double D0 = ((((((0.0 + gzm.x) + gym.x) + gxl) + gx2.x) + gy2.x) + gz2.x + gs2.x) + gt2.x;
+        const double D1 = ((((((0.0 + gzm.y) + gym.y) + gx2.x) + gx2.y) + gy2.y) + gz2.y + gs2.y) + gt2.y;
+        const double Di0 = 1.0 / D0, Di1 = 1.0 / D1;
+        double r0, r1;
+        if (WARM) {
+            double a = 0.0;
+            a = a + gzm.x * xmz.x;
+            a = a + gym.x * xmy.x;
+            a = a + gxl * xl;
+            a = a + gx2.x * x2.y;
+            a = a + gy2.x * xpy.x;
+            a = a + gz2.x * xpz.x;
+            r0 = gs2.x - (D0 * x2.x - a);
+            double b = 0.0;
+            b = b + gzm.y * xmz.y;
+            b = b + gym.y * xmy.y;
+            b = b + gx2.x * x2.x;
+            b = b + gx2.y * xr;
+            b = b + gy2.y * xpy.y;
+            b = b + gz2.y * xpz.y;
+            r1 = gs2.y - (D1 * x2.y - b);
+        } else {
+            r0 = gs2.x;
+            r1 = gs2.y;
+        }
+        const double z0 = r0 * Di0, z1 = r1 * Di1;
+        stp(v.D, u0, make_double2(D0, D1));
+        stp(v.Dinv, u0, make_double2(Di0, Di1));
+        stp(v.r, u0, make_double2(r0, r1));
+        stp(v.z, u0, make_double2(z0, z1));
+        if (gs_out) {
+            stp(gs_out, u0, gs2);
+            stp(gt_out, u0, gt2);
+        }
+        const double mb0 = gs2.x * Di0, mb1 = gs2.y * Di1;
+        acc[0] = acc[0] + r0 * z0;
+        acc[1] = acc[1] + z0 * z0;
+        acc[2] = acc[2] + r0 * r0;
+        acc[3] = acc[3] + mb0 * mb0;
+        acc[4] = acc[4] + gs2.x * gs2.x;
+        acc[0] = acc[0] + r1 * z1;
+        acc[1] = acc[1] + z1 * z1;
+        acc[2] = acc[2] + r1 * r1;
+        acc[3] = acc[3] + mb1 * mb1;
+        acc[4] = acc[4] + gs2.y * gs2.y;
+    }
+    if (c3_chunk_epilogue<5>(acc, v.chunk0 + (int32_t)blockIdx.x, ra) && cd.finalize && threadIdx.x == 0) {
+        finalize_start(ra.ctrl, ra.slots);
+        set_cond2(cd, ra.ctrl);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K3: p = z + beta p_old (recomputed for neighbours), lazy x update, q = L~ p
 // ---------------------------------------------------------------------------
@@ -399,6 +528,14 @@ int launch_pair_assemble(const StencilArgs &s, const VecArgs &v, const RedArgs &
         k_pair_edges<true><<<nb, kThreads, 0, st>>>(s, v, eps2);
         if (mode == ASM_INIT) k_pair_nodes<ASM_INIT><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
         else k_pair_nodes<ASM_LAMBDA2><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
+    } else if (s.nx % 512 == 0 && s.nx <= 4096) {  // fused single pass
+        // 3 CTAs/SM (80 registers): measured on config 4 1.57 ms vs 1.64 (two
+        // passes), 1.90 (4 CTAs/SM, spills) and 1.70 (2 CTAs/SM)
+        if (mode == ASM_REWEIGHT_WARM)
+            k_pair_fused<ASM_REWEIGHT_WARM, 3><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
+        else
+            k_pair_fused<ASM_REWEIGHT_COLD, 3><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
+        return 1;
     } else {
         k_pair_edges<false><<<nb, kThreads, 0, st>>>(s, v, eps2);
         if (mode == ASM_REWEIGHT_WARM)

@@ -78,6 +78,20 @@ def test_vgroup_cold_and_sequence(irls, world):
         g.close()
 
 
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_vgroup_fused_rows_of_512(irls, world):
+    """512-wide rows (fused reweight kernel incl. the ghost -z slot), one
+    chunk per plane, 16 planes: bitwise equal to one rank."""
+    spec = gen.blob_grid(512, 8, 16, seed=8, sigma=(3.0, 8.0))
+    T = 10
+    m, reps1, tot1, sw1 = single(irls, spec, irls.options(T=T), T)
+    g = irls.VGroup(spec, world, irls.options(T=T))
+    reps, tot = g.irls_vgroup_solve(irls.IRLS_FROM_SCRATCH, T=T)
+    assert [r["cg_iters"] for r in reps] == [r["cg_iters"] for r in reps1]
+    assert np.array_equal(g.irls_vgroup_get_potentials(), m.irls_get_potentials())
+    g.close()
+
+
 @pytest.mark.slow
 def test_vgroup_config2_world8(irls):
     """BASELINE config 2 (128^3), 8 virtual ranks of 16 planes each."""
