@@ -76,6 +76,11 @@ typedef struct {
     int32_t warm_start;  /* 1: CG starts from v^(l-1); 0: cold start from 0 */
     int32_t record_trace;/* 1: fill S_eps / flow / true residual / x range in reports (extra passes) */
     int32_t loop_mode;   /* irls_loop_mode: CUDA graph with device-side WHILE loop (default) or host loop */
+    int32_t fixed_point_exit; /* 1: within one irls_solve, once a warm reweight step stops before its first
+                                 CG iteration (x unchanged), the remaining steps repeat it bit for bit and are
+                                 skipped on the device (their reports are copies).  x^(T) and the reports are
+                                 identical to running every step; default 0 (every step executed). */
+    int32_t reserved;
 } irls_options;
 
 void irls_options_default(irls_options *opt);

@@ -95,6 +95,8 @@ extern "C" void irls_options_default(irls_options *o)
     o->warm_start = 1;
     o->record_trace = 0;
     o->loop_mode = IRLS_LOOP_GRAPH;
+    o->fixed_point_exit = 0;
+    o->reserved = 0;
 }
 
 extern "C" const char *irls_status_string(irls_status st)
@@ -167,7 +169,8 @@ static irls_status check_opts(const irls_options *o)
 {
     if (!o) return IRLS_ERR_INVALID_ARGUMENT;
     if (!(o->eps > 0.0) || isinf(o->eps) || o->T < 0 || !(o->cg_rtol >= 0.0) || o->cg_max_iter < 0 ||
-        (o->cg_norm != 0 && o->cg_norm != 1) || (o->loop_mode != 0 && o->loop_mode != 1))
+        (o->cg_norm != 0 && o->cg_norm != 1) || (o->loop_mode != 0 && o->loop_mode != 1) ||
+        (o->fixed_point_exit != 0 && o->fixed_point_exit != 1))
         return IRLS_ERR_INVALID_ARGUMENT;
     return IRLS_OK;
 }
@@ -198,6 +201,7 @@ static VecArgs vec_args(const irls_ctx *c)
     v.z = c->z;
     v.p0 = c->p0;
     v.p1 = c->p1;
+    v.frozen = &c->ctrl->frozen;
     return v;
 }
 
@@ -468,13 +472,22 @@ static irls_status enq_body(Ranks &R, const CondArgs &cd, cudaStream_t st)
     return last_launch(R[0], "cg body");
 }
 
-static irls_status enq_tail(Ranks &R, cudaStream_t st)
+static void enq_finish(Ranks &R, cudaStream_t st)
 {
-    irls_status s;
     for (irls_ctx *c : R) {
         launch_finish(vec_args(c), c->ctrl, st);
-        launch_report(c->ctrl, c->reports, st);
-        c->launches += 2;
+        c->launches += 1;
+    }
+}
+
+// report (+ record_trace diagnostics); `finish` = also enqueue the x update
+static irls_status enq_tail(Ranks &R, int mode, cudaStream_t st, bool finish = true)
+{
+    irls_status s;
+    if (finish) enq_finish(R, st);
+    for (irls_ctx *c : R) {
+        launch_report(c->ctrl, c->reports, mode == ASM_REWEIGHT_WARM && c->opt.fixed_point_exit ? 1 : 0, st);
+        c->launches += 1;
     }
     if (R[0]->opt.record_trace) {
         if (R[0]->world > 1 && (s = coll_halo(R, false, st))) return s;
@@ -499,28 +512,26 @@ static irls_status enq_tail(Ranks &R, cudaStream_t st)
 
 // Per-solve CUDA graph (one rank, world 1): [x = 0] -> K1 (sets the WHILE
 // condition) -> [x = 0] -> WHILE { K3 ; K5 (sets the condition) } -> finish
-// -> report [-> diag].
-static irls_status build_graph(irls_ctx *c, int mode)
+// -> report [-> diag].  With fixed_point_exit, a warm reweight solve is
+// wrapped as  gate -> IF (not frozen) { K1 -> WHILE {...} -> finish } ->
+// report: a frozen solve costs one graph launch and two one-thread kernels.
+static irls_status capture_solve_body(irls_ctx *c, Ranks &R, int mode, cudaStream_t st)
 {
-    cudaStream_t st = c->stream;
-    Ranks R{c};
-    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     cudaStreamCaptureStatus cs;
     cudaGraph_t graph;
     const cudaGraphNode_t *deps = nullptr;
     size_t nd = 0;
     CK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &graph, &deps, &nd));
     cudaGraphConditionalHandle h;
-    CK(cudaGraphConditionalHandleCreate(&h, graph, 0, 0));
+    // default 0 at every launch: the assembly's last block turns the loop on
+    CK(cudaGraphConditionalHandleCreate(&h, graph, 0, cudaGraphCondAssignDefault));
     CondArgs cd;
     cd.handle = h;
     cd.use = 1;
     cd.finalize = 1;
-    const int64_t lsave = c->launches;
-    c->launches = 0;
     if (mode == ASM_INIT || mode == ASM_LAMBDA2) CK(cudaMemsetAsync(c->x, 0, sizeof(double) * c->n_own, st));
     irls_status s = enq_assemble(R, mode, cd, st);
-    if (s) { cudaGraph_t g; cudaStreamEndCapture(st, &g); if (g) cudaGraphDestroy(g); return s; }
+    if (s) return s;
     if (mode == ASM_REWEIGHT_COLD) CK(cudaMemsetAsync(c->x, 0, sizeof(double) * c->n_own, st));
     CK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &graph, &deps, &nd));
     cudaGraphNodeParams p = {cudaGraphNodeTypeConditional};
@@ -539,11 +550,62 @@ static irls_status build_graph(irls_ctx *c, int mode)
     c->launches = pre;
     cudaGraph_t bodyg;
     CK(cudaStreamEndCapture(c->side_stream, &bodyg));
-    if (s) { cudaGraph_t g; cudaStreamEndCapture(st, &g); if (g) cudaGraphDestroy(g); return s; }
-    s = enq_tail(R, st);
-    cudaGraph_t full;
-    CK(cudaStreamEndCapture(st, &full));
-    if (s) { cudaGraphDestroy(full); return s; }
+    return s;
+}
+
+static irls_status build_graph(irls_ctx *c, int mode)
+{
+    cudaStream_t st = c->stream;
+    Ranks R{c};
+    const bool gated = c->opt.fixed_point_exit && mode == ASM_REWEIGHT_WARM;
+    const int64_t lsave = c->launches;
+    c->launches = 0;
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    irls_status s = IRLS_OK;
+    if (!gated) {
+        s = capture_solve_body(c, R, mode, st);
+        if (!s) s = enq_tail(R, mode, st);
+    } else {
+        cudaStreamCaptureStatus cs;
+        cudaGraph_t graph;
+        const cudaGraphNode_t *deps = nullptr;
+        size_t nd = 0;
+        cudaGraphConditionalHandle hif;
+        cudaError_t e = cudaStreamGetCaptureInfo(st, &cs, nullptr, &graph, &deps, &nd);
+        if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&hif, graph, 0, cudaGraphCondAssignDefault);
+        if (e == cudaSuccess) {
+            launch_gate(c->ctrl, hif, st);
+            c->launches++;
+            e = cudaStreamGetCaptureInfo(st, &cs, nullptr, &graph, &deps, &nd);
+        }
+        cudaGraphNodeParams p = {cudaGraphNodeTypeConditional};
+        cudaGraphNode_t ifnode;
+        if (e == cudaSuccess) {
+            p.type = cudaGraphNodeTypeConditional;
+            p.conditional.handle = hif;
+            p.conditional.type = cudaGraphCondTypeIf;
+            p.conditional.size = 1;
+            e = cudaGraphAddNode(&ifnode, graph, deps, nd, &p);
+        }
+        if (e == cudaSuccess) e = cudaStreamUpdateCaptureDependencies(st, &ifnode, 1, cudaStreamSetCaptureDependencies);
+        if (e == cudaSuccess)
+            e = cudaStreamBeginCaptureToGraph(c->side_stream2, p.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                              cudaStreamCaptureModeThreadLocal);
+        if (e != cudaSuccess) {
+            s = fail(c, IRLS_ERR_CUDA, std::string("gated graph: ") + cudaGetErrorString(e));
+        } else {
+            s = capture_solve_body(c, R, mode, c->side_stream2);
+            if (!s) enq_finish(R, c->side_stream2);
+            cudaGraph_t ifg;
+            e = cudaStreamEndCapture(c->side_stream2, &ifg);
+            if (!s && e != cudaSuccess) s = fail(c, IRLS_ERR_CUDA, std::string("gated graph: ") + cudaGetErrorString(e));
+            if (!s) s = enq_tail(R, mode, st, false);
+        }
+    }
+    cudaGraph_t full = nullptr;
+    cudaError_t e = cudaStreamEndCapture(st, &full);
+    if (s) { if (full) cudaGraphDestroy(full); c->launches = lsave; return s; }
+    CK(e);
     CK(cudaGraphInstantiate(&c->gexec[mode], full, 0));
     cudaGraphDestroy(full);
     c->gl_fixed[mode] = c->launches;
@@ -584,7 +646,7 @@ static irls_status enqueue_solve(Ranks &R, int mode)
         s = enq_body(R, cd, st);
         if (s) return s;
     }
-    return enq_tail(R, st);
+    return enq_tail(R, mode, st);
 }
 
 static void copy_report(const DevReport &d, irls_step_report *o, float ms)
@@ -613,7 +675,7 @@ static irls_status run_solves(Ranks &R, int mode0, int mode_rest, int count, irl
     cudaStream_t st = c->stream;
     for (irls_ctx *d : R) {
         d->launches = 0;
-        CK(cudaMemsetAsync(&d->ctrl->step, 0, sizeof(int32_t), st));
+        CK(cudaMemsetAsync(&d->ctrl->step, 0, 2 * sizeof(int32_t), st));  // step, frozen
     }
     std::vector<cudaEvent_t> ev(count + 1);
     for (auto &e : ev) CK(cudaEventCreate(&e));
@@ -680,6 +742,7 @@ static irls_status common_setup(irls_ctx *c, const irls_comm_desc *comm, const i
         c->own_stream = true;
     }
     CK(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->side_stream2, cudaStreamNonBlocking));
     CK(cudaMallocHost(&c->h_done, sizeof(int)));
     setup_pool(c->device);
     return IRLS_OK;
@@ -1354,6 +1417,7 @@ extern "C" irls_status irls_time_kernel(irls_ctx *c, int32_t which, int32_t reps
     if (!(tc.alpha == tc.alpha) || tc.alpha == 0.0) tc.alpha = 0.5;
     if (!(tc.beta == tc.beta)) tc.beta = 0.5;
     tc.done = 0;
+    tc.frozen = 0;  // time the real kernels even after a fixed-point exit
     CK(cudaMemcpyAsync(c->ctrl, &tc, sizeof(tc), cudaMemcpyHostToDevice, st));
     CondArgs cd;
     memset(&cd, 0, sizeof(cd));
@@ -1413,6 +1477,7 @@ extern "C" void irls_mincut_destroy(irls_ctx *c)
     if (c->h_done) cudaFreeHost(c->h_done);
     if (c->nccl) ncclCommDestroy(c->nccl);
     if (c->side_stream) cudaStreamDestroy(c->side_stream);
+    if (c->side_stream2) cudaStreamDestroy(c->side_stream2);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }

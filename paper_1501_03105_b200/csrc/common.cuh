@@ -49,7 +49,7 @@ __device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv &f)
 struct DevCtrl {
     double rho, alpha, beta, ref, res, rtol;
     int32_t k, max_iter, norm, done;
-    int32_t status, zero_x, step, pad0;
+    int32_t status, zero_x, step, frozen;  // frozen: fixed point reached (fixed_point_exit)
     unsigned grp_cnt[kGroups];
     unsigned fin_cnt, pad1;
     unsigned long long xmin_key, xmax_key;

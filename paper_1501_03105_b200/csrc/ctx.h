@@ -87,7 +87,7 @@ struct irls_ctx {
 
     // ---- graphs
     cudaGraphExec_t gexec[4] = {nullptr, nullptr, nullptr, nullptr};  // by assemble mode
-    cudaStream_t side_stream = nullptr;
+    cudaStream_t side_stream = nullptr, side_stream2 = nullptr;
 
     // ---- stats
     int64_t launches = 0, last_cg_iters = 0;

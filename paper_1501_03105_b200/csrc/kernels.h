@@ -22,6 +22,7 @@ struct VecArgs {
     double *D, *Dinv, *r, *q;
     double *z;           // ghost
     double *p0, *p1;     // ghost (ping-pong: iteration k reads p[k&1], writes p[(k+1)&1])
+    const int32_t *frozen;  // DevCtrl::frozen: assembly kernels skip a step that repeats a fixed point
 };
 
 struct StencilArgs {
@@ -80,7 +81,11 @@ struct DevReport {
     int32_t cg_iters, converged, status, pad;
     double rel_res, true_rel_res, S_eps, flow_value, current_s, x_min, x_max, ref;
 };
-void launch_report(DevCtrl *ctrl, DevReport *reports, cudaStream_t st);
+// freeze: set DevCtrl::frozen when this (warm reweight) solve ended with 0 CG
+// iterations and x unchanged (fixed_point_exit)
+void launch_report(DevCtrl *ctrl, DevReport *reports, int freeze, cudaStream_t st);
+// fixed_point_exit graph gate: IF condition = !frozen
+void launch_gate(const DevCtrl *ctrl, cudaGraphConditionalHandle h, cudaStream_t st);
 // record_trace diagnostics: [S_eps, flow, current_s, true_res^2] + x range
 void launch_stencil_diag_ex(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, double eps, int norm,
                             const double *gsv, const double *gtv, cudaStream_t st);

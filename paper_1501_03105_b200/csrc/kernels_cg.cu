@@ -54,6 +54,7 @@ template <int MODE>
 __global__ void __launch_bounds__(kThreads) k_stencil_assemble(StencilArgs s, VecArgs v, RedArgs ra, CondArgs cd,
                                                                double eps2, double *gs_out, double *gt_out)
 {
+    if (v.frozen && *(const volatile int32_t *)v.frozen) return;  // fixed point: this step repeats the last one
     double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     const int64_t P = s.P;
     FOR_CHUNK_NODES({
@@ -133,6 +134,7 @@ template <int MODE>
 __global__ void __launch_bounds__(kThreads) k_sell_assemble(SellArgs s, VecArgs v, RedArgs ra, CondArgs cd,
                                                             double eps2, double *gs_out, double *gt_out)
 {
+    if (v.frozen && *(const volatile int32_t *)v.frozen) return;  // fixed point: this step repeats the last one
     double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     FOR_CHUNK_NODES({
         const int64_t sl = u / kSell;
@@ -322,8 +324,12 @@ __global__ void k_finalize(int phase, DevCtrl *ctrl, const double *slots, CondAr
     if (phase != PH_PQ) set_cond(cd, ctrl);
 }
 
-__global__ void k_report(DevCtrl *ctrl, DevReport *reports)
+__global__ void k_report(DevCtrl *ctrl, DevReport *reports, int freeze)
 {
+    // A warm reweight step that stopped before its first CG iteration left x
+    // unchanged (no update, b != 0): every later step of this solve reweights
+    // from the same x and repeats it bit for bit, so they may be skipped.
+    if (freeze && ctrl->k == 0 && ctrl->zero_x == 0 && ctrl->status == ST_OK) ctrl->frozen = 1;
     DevReport &R = reports[ctrl->step];
     const double ref = ctrl->ref;
     R.cg_iters = ctrl->k;
@@ -567,7 +573,20 @@ void launch_finalize(int phase, DevCtrl *ctrl, const double *slots, const CondAr
     k_finalize<<<1, 1, 0, st>>>(phase, ctrl, slots, cd);
 }
 
-void launch_report(DevCtrl *ctrl, DevReport *reports, cudaStream_t st) { k_report<<<1, 1, 0, st>>>(ctrl, reports); }
+__global__ void k_gate(const DevCtrl *ctrl, cudaGraphConditionalHandle h)
+{
+    cudaGraphSetConditional(h, ctrl->frozen ? 0u : 1u);
+}
+
+void launch_gate(const DevCtrl *ctrl, cudaGraphConditionalHandle h, cudaStream_t st)
+{
+    k_gate<<<1, 1, 0, st>>>(ctrl, h);
+}
+
+void launch_report(DevCtrl *ctrl, DevReport *reports, int freeze, cudaStream_t st)
+{
+    k_report<<<1, 1, 0, st>>>(ctrl, reports, freeze);
+}
 
 void launch_stencil_diag_ex(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, double eps, int norm,
                             const double *gsv, const double *gtv, cudaStream_t st)

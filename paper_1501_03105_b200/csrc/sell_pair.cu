@@ -42,6 +42,7 @@ template <int WMAX, int MODE>
 __global__ void __launch_bounds__(kThreads) k_sellp_assemble(SellArgs s, VecArgs v, RedArgs ra, CondArgs cd,
                                                              double eps2, double *gs_out, double *gt_out)
 {
+    if (v.frozen && *(const volatile int32_t *)v.frozen) return;  // fixed point: this step repeats the last one
     constexpr bool WARM = MODE == ASM_REWEIGHT_WARM;
     constexpr bool INITG = MODE == ASM_INIT || MODE == ASM_LAMBDA2;  // g = c
     constexpr bool HASX = !INITG;

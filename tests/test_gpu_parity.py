@@ -294,3 +294,53 @@ def test_time_kernel_restores_state(irls):
     S = oracle.Solver(oracle.Graph(spec), T=4)
     S.run(record=False)
     assert np.array_equal(m.irls_get_potentials(), S.x())
+
+
+# --------------------------------------------------------------------------
+# fixed_point_exit: skipped repeats of a frozen step give the same bits
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("kind", ["stencil_fused", "stencil_pair", "stencil_odd", "csr"])
+@pytest.mark.parametrize("loop_mode", [0, 1])
+def test_fixed_point_exit_bitwise(irls, kind, loop_mode):
+    """A warm reweight step with 0 CG iterations leaves x unchanged, so every
+    later step repeats it; with fixed_point_exit the library skips them on
+    the device.  x^(T), every report and the sweep equal the oracle that
+    runs all T steps."""
+    spec = {"stencil_fused": lambda: gen.blob_grid(512, 8, 6, seed=4, sigma=(3.0, 8.0)),
+            "stencil_pair": lambda: gen.blob_grid(64, 40, 12, seed=4, sigma=(3.0, 8.0)),
+            "stencil_odd": lambda: gen.blob_grid(33, 17, 9, seed=4, sigma=(3.0, 8.0)),
+            "csr": lambda: gen.road_graph(80, seed=2, knn=50)}[kind]()
+    T = 30
+    m = irls.MinCut.from_spec(spec, irls.options(T=T, fixed_point_exit=1, loop_mode=loop_mode, record_trace=1))
+    reps, tot = m.irls_solve(irls.IRLS_FROM_SCRATCH, T=T)
+    S = oracle.Solver(oracle.Graph(spec), T=T)
+    _, oreps = S.run(record=False)
+    assert [r["cg_iters"] for r in reps] == [r["cg_iters"] for r in oreps]
+    assert any(r["cg_iters"] == 0 for r in oreps[1:]), "test case never freezes"
+    for a, b in zip(reps, oreps):
+        for k in ("rel_res", "S_eps", "flow_value", "x_min", "x_max"):
+            assert a[k] == b[k], k
+    assert np.array_equal(m.irls_get_potentials().view(np.uint64), S.x().view(np.uint64))
+    check_sweep(m, S)
+    # the kernel timer still times real work after a frozen solve
+    assert m.irls_time_kernel(irls.KERNEL_ASSEMBLE, 2) > 0.0
+
+
+def test_fixed_point_exit_sequence(irls):
+    """Config-5 style sequence: every IRLS_CONTINUE after new terminal weights
+    runs its first step; results equal the default (every step executed)."""
+    spec = gen.blob_grid(64, 64, 16, seed=2, sigma=(3.0, 8.0))
+    a = irls.MinCut.from_spec(spec, irls.options(T=10, fixed_point_exit=1))
+    b = irls.MinCut.from_spec(spec, irls.options(T=10))
+    ra, _ = a.irls_solve(irls.IRLS_FROM_SCRATCH, T=10)
+    rb, _ = b.irls_solve(irls.IRLS_FROM_SCRATCH, T=10)
+    cs, ct = spec["cs"].copy(), spec["ct"].copy()
+    for fs, ft in gen.config5_factors(cs.shape[0], n_problems=3, seed=4):
+        cs, ct = cs * fs, ct * ft
+        for m in (a, b):
+            m.irls_set_terminal_weights(cs, ct)
+        ra, ta = a.irls_solve(irls.IRLS_CONTINUE, T=10)
+        rb, tb = b.irls_solve(irls.IRLS_CONTINUE, T=10)
+        assert [r["cg_iters"] for r in ra] == [r["cg_iters"] for r in rb]
+        assert np.array_equal(a.irls_get_potentials(), b.irls_get_potentials())
