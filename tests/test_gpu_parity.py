@@ -136,11 +136,13 @@ def test_blob_grid_chunk_planes(irls, dims):
     m2, S2 = lockstep(irls, spec, T=6, warm=False)
 
 
-@pytest.mark.parametrize("dims", [(512, 12, 6), (512, 7, 3), (1024, 5, 4), (1536, 3, 4)])
+@pytest.mark.parametrize("dims", [(512, 12, 6), (512, 7, 3), (1024, 5, 4), (1536, 3, 4), (512, 16, 5), (512, 8, 37),
+                                  (512, 24, 1)])
 def test_fused_reweight_rows_of_512(irls, dims):
     """nx a multiple of 512 (config 4's rows): the single-pass fused reweight
     kernel (-y conductance from the thread's own earlier row, -x by shuffle,
-    -z recomputed), warm and cold, graph and host loop, trace diagnostics."""
+    -z recomputed), with ragged chunks, whole-chunk planes and single planes;
+    warm and cold, graph and host loop, trace diagnostics."""
     spec = gen.blob_grid(*dims, seed=6, sigma=(3.0, 9.0))
     m, S = lockstep(irls, spec, T=20, record=True)
     check_sweep(m, S)
