@@ -38,8 +38,8 @@ __device__ __forceinline__ double term_g(double cs, double ct, double x, double 
     return gs;
 }
 
-template <int WMAX, int MODE>
-__global__ void __launch_bounds__(kThreads) k_sellp_assemble(SellArgs s, VecArgs v, RedArgs ra, CondArgs cd,
+template <int WMAX, int MODE, int MINB = 1>
+__global__ void __launch_bounds__(kThreads, MINB) k_sellp_assemble(SellArgs s, VecArgs v, RedArgs ra, CondArgs cd,
                                                              double eps2, double *gs_out, double *gt_out)
 {
     if (v.frozen && *(const volatile int32_t *)v.frozen) return;  // fixed point: this step repeats the last one
@@ -140,8 +140,8 @@ __global__ void __launch_bounds__(kThreads) k_sellp_assemble(SellArgs s, VecArgs
     }
 }
 
-template <int WMAX>
-__global__ void __launch_bounds__(kThreads) k_sellp_pspmv(SellArgs s, VecArgs v, RedArgs ra, CondArgs cd)
+template <int WMAX, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_sellp_pspmv(SellArgs s, VecArgs v, RedArgs ra, CondArgs cd)
 {
     const DevCtrl *ctrl = ra.ctrl;
     const int32_t it = ctrl->k;
@@ -212,6 +212,15 @@ static void asm_w(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const 
                   double *gs_out, double *gt_out, cudaStream_t st)
 {
     const unsigned nb = nblk3(v.n_own);
+    // reweight steps at 3 CTAs/SM: config 3 0.62 ms vs 0.72 ms at 1, 2 or 4
+    if (WMAX == 4 && mode == ASM_REWEIGHT_WARM) {
+        k_sellp_assemble<WMAX, ASM_REWEIGHT_WARM, 3><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
+        return;
+    }
+    if (WMAX == 4 && mode == ASM_REWEIGHT_COLD) {
+        k_sellp_assemble<WMAX, ASM_REWEIGHT_COLD, 3><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
+        return;
+    }
     if (mode == ASM_INIT) k_sellp_assemble<WMAX, ASM_INIT><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
     else if (mode == ASM_LAMBDA2)
         k_sellp_assemble<WMAX, ASM_LAMBDA2><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
@@ -232,8 +241,10 @@ bool launch_sellp_assemble(const SellArgs &s, const VecArgs &v, const RedArgs &r
 
 bool launch_sellp_pspmv(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, cudaStream_t st)
 {
-    if (s.wmax <= 4) k_sellp_pspmv<4><<<nblk3(v.n_own), kThreads, 0, st>>>(s, v, ra, cd);
-    else if (s.wmax <= 8) k_sellp_pspmv<8><<<nblk3(v.n_own), kThreads, 0, st>>>(s, v, ra, cd);
+    // 3 CTAs/SM (80 registers, 48 B spilled): config 3 0.47 ms vs 0.52 ms at
+    // 2 CTAs/SM (105 registers) and 0.49 ms at 4 (64 registers)
+    if (s.wmax <= 4) k_sellp_pspmv<4, 3><<<nblk3(v.n_own), kThreads, 0, st>>>(s, v, ra, cd);
+    else if (s.wmax <= 8) k_sellp_pspmv<8, 1><<<nblk3(v.n_own), kThreads, 0, st>>>(s, v, ra, cd);
     else return false;
     return true;
 }
