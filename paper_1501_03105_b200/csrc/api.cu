@@ -1129,7 +1129,16 @@ extern "C" irls_status irls_solve(irls_ctx *c, int32_t mode, irls_step_report *p
     GUARD(c);
     if (mode != IRLS_FROM_SCRATCH && mode != IRLS_CONTINUE) return IRLS_ERR_INVALID_ARGUMENT;
     if (mode == IRLS_CONTINUE && c->state == 0) return fail(c, IRLS_ERR_STATE, "IRLS_CONTINUE without potentials");
-    if (c->n_glob == 0) { c->state = 1; if (total) *total = 0; return IRLS_OK; }
+    if (c->n_glob == 0) {  // no unknowns: every solve is trivially converged (b = 0, v = [])
+        c->state = 1;
+        if (total) *total = 0;
+        const int count = mode == IRLS_FROM_SCRATCH ? c->opt.T + 1 : c->opt.T;
+        for (int i = 0; per_step && i < count; i++) {
+            memset(per_step + i, 0, sizeof(irls_step_report));
+            per_step[i].converged = 1;
+        }
+        return IRLS_OK;
+    }
     const int step_mode = c->opt.warm_start ? ASM_REWEIGHT_WARM : ASM_REWEIGHT_COLD;
     Ranks R{c};
     if (mode == IRLS_FROM_SCRATCH) return run_solves(R, ASM_INIT, step_mode, c->opt.T + 1, per_step, total);
@@ -1974,6 +1983,16 @@ extern "C" irls_status irls_lambda2(irls_ctx *c, double cg_rtol, int32_t cg_max_
         return fail(c, IRLS_ERR_INVALID_ARGUMENT, "lambda2 CG options");
     cudaStream_t st = c->stream;
     const int64_t n = c->n_own;
+    if (n == 0) {  // only s and t: x = (1, -1), x^T L x = 4 c_st, C = 2 c_st
+        if (rep) {
+            memset(rep, 0, sizeof(*rep));
+            rep->xLx = 4.0 * c->c_st;
+            rep->C = 2.0 * c->c_st;
+            rep->lambda2 = rep->xLx / (2.0 * rep->C);
+            rep->converged = 1;
+        }
+        return IRLS_OK;
+    }
     double *xs = dalloc<double>(c, n);
     if (!xs) return fail(c, IRLS_ERR_OOM, "lambda2 x save");
     CK(cudaMemcpyAsync(xs, c->x, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));

@@ -44,6 +44,13 @@ def test_spec_unit_path():
     assert lam == 0.25 and C == 4.0 and xLx == 2.0 and x.tolist() == [0.0]
 
 
+def test_spec_single_edge():
+    """a single edge s-t of weight c -> C = 2c, x^T L x = 4c, lambda_2 = 1."""
+    spec = gen._csr_edges(2, [(0, 1, 3.0)], 0, 1)
+    lam, xLx, C, it = solver(spec).lambda2()
+    assert (lam, xLx, C, it) == (1.0, 12.0, 6.0, 0)
+
+
 def test_spec_single_edge_via_path_limit():
     """a single edge s-t -> lambda_2 = 1.  Here as the direct s-t
     constant c_st (A5) next to a non-terminal hanging off s: x_a = 1, so
