@@ -85,7 +85,10 @@ typedef struct {
 
 void irls_options_default(irls_options *opt);
 
-/* Process / device description.  world_size 1: nccl_unique_id may be NULL.
+/* Process / device description.  world_size 1: nccl_unique_id may be NULL;
+ * a stencil context given world_size 1 AND an id runs the multi-rank code
+ * path over a 1-rank NCCL communicator (host loop, slot allreduce, finalize
+ * kernels, gather / broadcast) — a self-test of the NCCL plumbing on one GPU.
  * cuda_stream: a cudaStream_t to run on, or NULL for a library-owned one. */
 typedef struct {
     int32_t world_size, rank, device;

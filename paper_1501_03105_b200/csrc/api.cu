@@ -284,7 +284,7 @@ extern "C" irls_status irls_halo_plan(int32_t nx, int32_t ny, int32_t nz, int32_
 
 static irls_status halo(irls_ctx *c, double *arr, cudaStream_t st)
 {
-    if (c->world == 1) return IRLS_OK;
+    if (!c->multi) return IRLS_OK;
     const irls_halo &h = c->hplan;
     NK(ncclGroupStart());
     if (h.peer_lo >= 0) {
@@ -319,7 +319,7 @@ static irls_status vgather_x(irls_vgroup *g, double **full)
 static irls_status gather_x(irls_ctx *c, double **full)
 {
     *full = c->x;
-    if (c->world == 1) return IRLS_OK;
+    if (!c->multi) return IRLS_OK;
     cudaStream_t st = c->stream;
     if (c->rank == 0 && !c->x_full) {
         c->x_full = dalloc<double>(c, c->n_glob);
@@ -344,7 +344,7 @@ static irls_status gather_x(irls_ctx *c, double **full)
 
 static irls_status allreduce_slots(irls_ctx *c, int nq, cudaStream_t st)
 {
-    if (c->world == 1) return IRLS_OK;
+    if (!c->multi) return IRLS_OK;
     NK(ncclAllReduce(c->slots_local, c->slots_glob, (size_t)nq * kGroups, ncclDouble, ncclSum, c->nccl, st));
     return IRLS_OK;
 }
@@ -359,7 +359,7 @@ typedef std::vector<irls_ctx *> Ranks;
 static irls_status coll_halo(Ranks &R, bool z_not_x, cudaStream_t st)
 {
     irls_ctx *c = R[0];
-    if (c->world == 1) return IRLS_OK;
+    if (!c->multi) return IRLS_OK;
     if (!c->vg) return halo(c, z_not_x ? c->z : c->x, st);
     for (irls_ctx *d : R) {
         const irls_halo &h = d->hplan;
@@ -382,7 +382,7 @@ static irls_status coll_halo(Ranks &R, bool z_not_x, cudaStream_t st)
 static irls_status coll_allreduce(Ranks &R, int nq, cudaStream_t st)
 {
     irls_ctx *c = R[0];
-    if (c->world == 1) return IRLS_OK;
+    if (!c->multi) return IRLS_OK;
     if (!c->vg) return allreduce_slots(c, nq, st);
     // sum of every rank's slots in rank order (each slot has one non-zero
     // contributor, so this is the same exact value NCCL's sum produces)
@@ -397,7 +397,7 @@ static irls_status coll_allreduce(Ranks &R, int nq, cudaStream_t st)
 static irls_status coll_minmax(Ranks &R, cudaStream_t st)
 {
     irls_ctx *c = R[0];
-    if (c->world == 1) return IRLS_OK;
+    if (!c->multi) return IRLS_OK;
     if (!c->vg) {
         NK(ncclGroupStart());
         NK(ncclAllReduce(&c->ctrl->xmin_key, &c->ctrl->xmin_key, 1, ncclUint64, ncclMin, c->nccl, st));
@@ -425,7 +425,7 @@ static irls_status enq_assemble(Ranks &R, int mode, const CondArgs &cd, cudaStre
         else
             c->launches += launch_sell_assemble_ex(sell_args(c), v, ra, cd, mode, c->opt.eps, c->gs_diag, c->gt_diag, st);
     }
-    if (R[0]->world > 1) {
+    if (R[0]->multi) {
         if ((s = coll_allreduce(R, 5, st))) return s;
         for (irls_ctx *c : R) {
             launch_finalize(PH_START, c->ctrl, c->slots_glob, cd, st);
@@ -445,12 +445,12 @@ static irls_status enq_body(Ranks &R, const CondArgs &cd, cudaStream_t st)
         if (c->kind == 0) launch_stencil_pspmv(stencil_args(c, false), v, ra, cd, st);
         else launch_sell_pspmv(sell_args(c), v, ra, cd, st);
         c->launches++;
-        if (c->world > 1) {
+        if (c->multi) {
             launch_ghost_pupdate(v, c->lo_ghost, c->hi_ghost, c->P, c->ctrl, st);
             c->launches++;
         }
     }
-    if (R[0]->world > 1) {
+    if (R[0]->multi) {
         if ((s = coll_allreduce(R, 1, st))) return s;
         for (irls_ctx *c : R) {
             launch_finalize(PH_PQ, c->ctrl, c->slots_glob, cd, st);
@@ -461,7 +461,7 @@ static irls_status enq_body(Ranks &R, const CondArgs &cd, cudaStream_t st)
         launch_axpy_jacobi(vec_args(c), red_args(c), cd, st);
         c->launches++;
     }
-    if (R[0]->world > 1) {
+    if (R[0]->multi) {
         if ((s = coll_allreduce(R, 3, st))) return s;
         for (irls_ctx *c : R) {
             launch_finalize(PH_RZ, c->ctrl, c->slots_glob, cd, st);
@@ -490,7 +490,7 @@ static irls_status enq_tail(Ranks &R, int mode, cudaStream_t st, bool finish = t
         c->launches += 1;
     }
     if (R[0]->opt.record_trace) {
-        if (R[0]->world > 1 && (s = coll_halo(R, false, st))) return s;
+        if (R[0]->multi && (s = coll_halo(R, false, st))) return s;
         for (irls_ctx *c : R) {
             const VecArgs v = vec_args(c);
             const RedArgs ra = red_args(c);
@@ -500,7 +500,7 @@ static irls_status enq_tail(Ranks &R, int mode, cudaStream_t st, bool finish = t
             else
                 launch_sell_diag_ex(sell_args(c), v, ra, c->opt.eps, c->opt.cg_norm, c->gs_diag, c->gt_diag, st);
         }
-        if (R[0]->world > 1 && (s = coll_allreduce(R, 4, st))) return s;
+        if (R[0]->multi && (s = coll_allreduce(R, 4, st))) return s;
         if ((s = coll_minmax(R, st))) return s;
         for (irls_ctx *c : R) {
             launch_diag_finalize(c->ctrl, c->slots_glob, c->reports, c->opt.cg_norm, st);
@@ -617,7 +617,7 @@ static irls_status enqueue_solve(Ranks &R, int mode)
 {
     irls_ctx *c = R[0];
     cudaStream_t st = c->stream;
-    if (c->opt.loop_mode == IRLS_LOOP_GRAPH && c->world == 1) {
+    if (c->opt.loop_mode == IRLS_LOOP_GRAPH && !c->multi) {
         if (!c->gexec[mode]) {
             irls_status s = build_graph(c, mode);
             if (s) return s;
@@ -632,7 +632,7 @@ static irls_status enqueue_solve(Ranks &R, int mode)
     CondArgs cd;
     memset(&cd, 0, sizeof(cd));
     cd.use = 0;
-    cd.finalize = c->world == 1 ? 1 : 0;
+    cd.finalize = c->multi ? 0 : 1;
     if (mode == ASM_INIT || mode == ASM_LAMBDA2)
         for (irls_ctx *d : R) CK(cudaMemsetAsync(d->x, 0, sizeof(double) * d->n_own, st));
     irls_status s = enq_assemble(R, mode, cd, st);
@@ -734,6 +734,9 @@ static irls_status common_setup(irls_ctx *c, const irls_comm_desc *comm, const i
     c->device = comm ? comm->device : 0;
     if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return IRLS_ERR_INVALID_ARGUMENT;
     if (c->world > 1 && ((!comm->nccl_unique_id && !c->vg) || 8 % c->world != 0)) return IRLS_ERR_INVALID_ARGUMENT;
+    // world 1 with an NCCL id: the multi-rank code path over a 1-rank
+    // communicator (host loop, slot allreduce, finalize kernels, broadcasts)
+    c->multi = c->world > 1 || c->vg != nullptr || (comm && comm->nccl_unique_id != nullptr);
     CK(cudaSetDevice(c->device));
     if (comm && comm->cuda_stream) {
         c->stream = (cudaStream_t)comm->cuda_stream;
@@ -766,7 +769,7 @@ static irls_status alloc_solver(irls_ctx *c, int64_t ghost)
     c->ctrl = dalloc<DevCtrl>(c, 1);
     c->part = dalloc<double>(c, (int64_t)kMaxQ * std::max<int32_t>(c->K, 1));
     c->slots_local = dalloc<double>(c, kMaxQ * kGroups);
-    c->slots_glob = c->world > 1 ? dalloc<double>(c, kMaxQ * kGroups) : c->slots_local;
+    c->slots_glob = c->multi ? dalloc<double>(c, kMaxQ * kGroups) : c->slots_local;
     c->max_reports = std::max(c->opt.T + 1, 1);
     c->reports = dalloc<DevReport>(c, c->max_reports);
     if (!c->D || !c->Dinv || !c->r || !c->q || !c->ctrl || !c->part || !c->slots_local || !c->slots_glob || !c->reports)
@@ -788,7 +791,7 @@ static irls_status alloc_solver(irls_ctx *c, int64_t ghost)
 
 static irls_status init_nccl(irls_ctx *c, const irls_comm_desc *comm)
 {
-    if (c->world == 1 || c->vg) return IRLS_OK;
+    if (!c->multi || c->vg) return IRLS_OK;
     ncclUniqueId id;
     memcpy(&id, comm->nccl_unique_id, sizeof(id));
     NK(ncclCommInitRank(&c->nccl, c->world, id, c->rank));
@@ -868,7 +871,7 @@ static irls_status create_stencil_impl(irls_ctx **out, const irls_comm_desc *com
             c->n_fin = count_nonempty(c->K, g0, g1);
             c->lo_ghost = c->world > 1 && c->rank > 0;
             c->hi_ghost = c->world > 1 && c->rank < c->world - 1;
-            if (c->world > 1) s = irls_halo_plan(nx, ny, nz, c->world, c->rank, &c->hplan);
+            if (c->multi) s = irls_halo_plan(nx, ny, nz, c->world, c->rank, &c->hplan);
         }
         if (!s) {
             s = alloc_solver(c, c->world > 1 ? c->P : 0);
@@ -1053,6 +1056,7 @@ extern "C" irls_status irls_mincut_create_csr(irls_ctx **out, const irls_comm_de
     }
     irls_ctx *c = new irls_ctx();
     irls_status st = common_setup(c, comm, opt);
+    c->multi = false;  // CSR: single GPU, no communicator
     if (!st) {
         c->kind = 1;
         c->n_glob = nr;
@@ -1280,9 +1284,9 @@ extern "C" irls_status irls_sweep_cut(irls_ctx *c, uint8_t *side, int32_t *order
     if (c->rank == 0) {
         s = sweep_rank0(c, xfull, side, order, &msg.k, &msg.cut);
         msg.status = s;
-        if (s && s != IRLS_ERR_BAD_POTENTIAL && c->world == 1) return s;
+        if (s && s != IRLS_ERR_BAD_POTENTIAL && !c->multi) return s;
     }
-    if (c->world > 1) {
+    if (c->multi) {
         if (!c->msg_dev) {
             c->msg_dev = dalloc<SweepResultMsg>(c, 1);
             if (!c->msg_dev) return fail(c, IRLS_ERR_OOM, "sweep msg");
@@ -1878,9 +1882,9 @@ extern "C" irls_status irls_two_level_cut(irls_ctx *c, uint8_t *side, irls_two_l
     if (c->rank == 0) {
         s = two_level_rank0(c, xfull, side, &msg.rep);
         msg.status = s;
-        if (s && c->world == 1) return s;
+        if (s && !c->multi) return s;
     }
-    if (c->world > 1) {
+    if (c->multi) {
         void *dmsg = nullptr;
         CK(cudaMallocAsync(&dmsg, sizeof(msg), c->stream));
         if (c->rank == 0) CK(cudaMemcpyAsync(dmsg, &msg, sizeof(msg), cudaMemcpyHostToDevice, c->stream));

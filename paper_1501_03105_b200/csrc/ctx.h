@@ -17,6 +17,7 @@ struct irls_ctx {
     int kind = 0;  // 0 stencil, 1 csr
     irls_options opt{};
     int world = 1, rank = 0, device = 0;
+    bool multi = false;  // the multi-rank (NCCL) code path: world > 1, or a 1-rank communicator (self-test)
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     ncclComm_t nccl = nullptr;

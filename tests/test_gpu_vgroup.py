@@ -111,3 +111,28 @@ def test_vgroup_rejects_unaligned(irls):
     spec = gen.blob_grid(40, 36, 29, seed=1)  # group boundaries fall inside planes
     with pytest.raises(irls.IrlsError):
         irls.VGroup(spec, 2)
+
+
+def test_nccl_one_rank_communicator(irls):
+    """The NCCL code path on one GPU: world_size 1 with an NCCL id runs the
+    multi-rank host loop, ncclAllReduce of the slots, the finalize kernels,
+    the gather and the ncclBroadcast of the sweep / two-level results over a
+    1-rank communicator.  Bitwise equal to the plain single-GPU path."""
+    import torch
+    spec = gen.blob_grid(64, 64, 16, seed=3, sigma=(3.0, 8.0))
+    T = 12
+    m, reps1, tot1, sw1 = single(irls, spec, irls.options(T=T, record_trace=1), T)
+    comm = irls.comm_desc(1, 0, 0, irls.irls_nccl_unique_id(), torch.cuda.current_stream().cuda_stream)
+    g = irls.MinCut.from_spec(spec, irls.options(T=T, record_trace=1), comm)
+    reps, tot = g.irls_solve(irls.IRLS_FROM_SCRATCH, T=T)
+    assert tot == tot1
+    for a, b in zip(reps, reps1):
+        for k in ("cg_iters", "rel_res", "S_eps", "flow_value", "x_min", "x_max"):
+            assert a[k] == b[k], k
+    assert np.array_equal(g.irls_get_potentials(), m.irls_get_potentials())
+    side, order, k, cut = g.irls_sweep_cut(order=True)
+    assert k == sw1[2] and cut == sw1[3] and np.array_equal(side, sw1[0])
+    s2, r2 = g.irls_two_level_cut()
+    s1, r1 = m.irls_two_level_cut()
+    assert np.array_equal(s1, s2) and r1["cut_value"] == r2["cut_value"]
+    g.close()
