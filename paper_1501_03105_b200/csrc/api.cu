@@ -613,6 +613,70 @@ static irls_status build_graph(irls_ctx *c, int mode)
     return IRLS_OK;
 }
 
+// T reweight steps of one irls_solve in ONE graph (world 1): mark ->
+// WHILE_outer (T times, or until a fixed point with fixed_point_exit) {
+// K1 -> WHILE_cg {K3; K5} -> finish -> report -> next } -> fill reports.
+// One graph launch per irls_solve instead of one per IRLS step.
+static irls_status build_graph_multi(irls_ctx *c, int mode)
+{
+    cudaStream_t st = c->stream;
+    Ranks R{c};
+    const int count = c->opt.T;
+    const int fpx = c->opt.fixed_point_exit && mode == ASM_REWEIGHT_WARM ? 1 : 0;
+    const int64_t lsave = c->launches;
+    c->launches = 0;
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    irls_status s = IRLS_OK;
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t graph;
+    const cudaGraphNode_t *deps = nullptr;
+    size_t nd = 0;
+    cudaGraphConditionalHandle hout;
+    cudaError_t e = cudaStreamGetCaptureInfo(st, &cs, nullptr, &graph, &deps, &nd);
+    if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&hout, graph, 0, cudaGraphCondAssignDefault);
+    if (e == cudaSuccess) {
+        launch_outer_init(c->ctrl, hout, count, st);
+        e = cudaStreamGetCaptureInfo(st, &cs, nullptr, &graph, &deps, &nd);
+    }
+    cudaGraphNodeParams p = {cudaGraphNodeTypeConditional};
+    cudaGraphNode_t wnode;
+    if (e == cudaSuccess) {
+        p.type = cudaGraphNodeTypeConditional;
+        p.conditional.handle = hout;
+        p.conditional.type = cudaGraphCondTypeWhile;
+        p.conditional.size = 1;
+        e = cudaGraphAddNode(&wnode, graph, deps, nd, &p);
+    }
+    if (e == cudaSuccess) e = cudaStreamUpdateCaptureDependencies(st, &wnode, 1, cudaStreamSetCaptureDependencies);
+    if (e == cudaSuccess)
+        e = cudaStreamBeginCaptureToGraph(c->side_stream2, p.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                          cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) {
+        s = fail(c, IRLS_ERR_CUDA, std::string("multi-step graph: ") + cudaGetErrorString(e));
+    } else {
+        s = capture_solve_body(c, R, mode, c->side_stream2);
+        if (!s) s = enq_tail(R, mode, c->side_stream2);
+        if (!s) {
+            launch_outer_next(c->ctrl, hout, fpx, c->side_stream2);
+            c->launches++;
+        }
+        cudaGraph_t bg;
+        e = cudaStreamEndCapture(c->side_stream2, &bg);
+        if (!s && e != cudaSuccess) s = fail(c, IRLS_ERR_CUDA, std::string("multi-step graph: ") + cudaGetErrorString(e));
+    }
+    const int64_t per_step = c->launches;
+    if (!s && fpx) launch_fill_reports(c->ctrl, c->reports, st);
+    cudaGraph_t full = nullptr;
+    e = cudaStreamEndCapture(st, &full);
+    if (s) { if (full) cudaGraphDestroy(full); c->launches = lsave; return s; }
+    CK(e);
+    CK(cudaGraphInstantiate(&c->gmulti[mode], full, 0));
+    cudaGraphDestroy(full);
+    c->gm_fixed[mode] = per_step;
+    c->launches = lsave;
+    return IRLS_OK;
+}
+
 static irls_status enqueue_solve(Ranks &R, int mode)
 {
     irls_ctx *c = R[0];
@@ -681,11 +745,26 @@ static irls_status run_solves(Ranks &R, int mode0, int mode_rest, int count, irl
     for (auto &e : ev) CK(cudaEventCreate(&e));
     CK(cudaEventRecord(ev[0], st));
     irls_status s = IRLS_OK;
-    for (int i = 0; i < count && !s; i++) {
-        s = enqueue_solve(R, i == 0 ? mode0 : mode_rest);
+    // graph mode, one rank: the T reweight steps run as ONE graph (outer WHILE);
+    // per-step times then come from device timestamps in the reports
+    const int nrest = mode0 == mode_rest ? count : count - 1;
+    const bool multi_graph = c->opt.loop_mode == IRLS_LOOP_GRAPH && !c->multi && R.size() == 1 && nrest == c->opt.T &&
+                             nrest >= 2 && (mode_rest == ASM_REWEIGHT_WARM || mode_rest == ASM_REWEIGHT_COLD);
+    if (multi_graph) {
+        launch_mark(c->ctrl, st);
+        if (mode0 != mode_rest) s = enqueue_solve(R, mode0);
+        if (!s && !c->gmulti[mode_rest]) s = build_graph_multi(c, mode_rest);
         if (!s) {
-            cudaError_t e = cudaEventRecord(ev[i + 1], st);
-            if (e != cudaSuccess) s = fail(c, IRLS_ERR_CUDA, cudaGetErrorString(e));
+            CK(cudaGraphLaunch(c->gmulti[mode_rest], st));
+            c->graph_iters_pending = true;
+        }
+    } else {
+        for (int i = 0; i < count && !s; i++) {
+            s = enqueue_solve(R, i == 0 ? mode0 : mode_rest);
+            if (!s) {
+                cudaError_t e = cudaEventRecord(ev[i + 1], st);
+                if (e != cudaSuccess) s = fail(c, IRLS_ERR_CUDA, cudaGetErrorString(e));
+            }
         }
     }
     cudaError_t e = cudaStreamSynchronize(st);
@@ -703,10 +782,27 @@ static irls_status run_solves(Ranks &R, int mode0, int mode_rest, int count, irl
         }
     }
     int64_t tot = 0;
+    unsigned long long t0 = 0;
+    if (!s && multi_graph) {
+        DevCtrl hc;
+        e = memcpy_sync(c, &hc, c->ctrl, sizeof(hc), cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) s = fail(c, IRLS_ERR_CUDA, cudaGetErrorString(e));
+        t0 = hc.t_mark;
+        // kernels: the first (init) graph's fixed part, then per executed step
+        int executed = 0;
+        for (int i = (mode0 != mode_rest ? 1 : 0); i < count; i++)
+            if (i == 0 || h[i].t_end != h[i - 1].t_end) executed++;
+        c->launches += (int64_t)executed * c->gm_fixed[mode_rest] + 2;
+    }
     if (!s) {
         for (int i = 0; i < count; i++) {
             float ms = 0.f;
-            cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+            if (multi_graph) {
+                const unsigned long long prev = i == 0 ? t0 : h[i - 1].t_end;
+                ms = h[i].t_end > prev ? (float)((double)(h[i].t_end - prev) * 1e-6) : 0.f;
+            } else {
+                cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+            }
             tot += h[i].cg_iters;
             if (reps) copy_report(h[i], reps + i, ms);
             if (h[i].status != 0 && !s) s = fail(c, (irls_status)h[i].status, "CG breakdown (p'Ap <= 0 or non-finite scalar)");
@@ -1484,6 +1580,8 @@ extern "C" void irls_mincut_destroy(irls_ctx *c)
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (auto &g : c->gexec)
+        if (g) cudaGraphExecDestroy(g);
+    for (auto &g : c->gmulti)
         if (g) cudaGraphExecDestroy(g);
     for (void *p : c->allocs) cudaFreeAsync(p, c->stream);
     if (c->stream) cudaStreamSynchronize(c->stream);

@@ -51,9 +51,20 @@ struct DevCtrl {
     int32_t k, max_iter, norm, done;
     int32_t status, zero_x, step, frozen;  // frozen: fixed point reached (fixed_point_exit)
     unsigned grp_cnt[kGroups];
-    unsigned fin_cnt, pad1;
+    unsigned fin_cnt;
+    int32_t outer_left;  // IRLS steps left in a multi-step graph
+    int32_t outer_end;   // report index one past its last step
+    int32_t pad2;
     unsigned long long xmin_key, xmax_key;
+    unsigned long long t_mark;  // %globaltimer (ns) at the start of a solve sequence
 };
+
+__device__ __forceinline__ unsigned long long global_ns()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 enum { ST_OK = 0, ST_BREAKDOWN = 6 };
 

@@ -88,6 +88,8 @@ struct irls_ctx {
 
     // ---- graphs
     cudaGraphExec_t gexec[4] = {nullptr, nullptr, nullptr, nullptr};  // by assemble mode
+    cudaGraphExec_t gmulti[4] = {nullptr, nullptr, nullptr, nullptr};  // T reweight steps in one graph, by mode
+    int64_t gm_fixed[4] = {0, 0, 0, 0};  // kernels per step of the multi-step graph (outside the CG body)
     cudaStream_t side_stream = nullptr, side_stream2 = nullptr;
 
     // ---- stats

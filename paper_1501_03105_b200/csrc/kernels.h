@@ -80,12 +80,19 @@ void launch_finalize(int phase, DevCtrl *ctrl, const double *slots, const CondAr
 struct DevReport {
     int32_t cg_iters, converged, status, pad;
     double rel_res, true_rel_res, S_eps, flow_value, current_s, x_min, x_max, ref;
+    unsigned long long t_end;  // %globaltimer (ns) when the solve's report was written
 };
 // freeze: set DevCtrl::frozen when this (warm reweight) solve ended with 0 CG
 // iterations and x unchanged (fixed_point_exit)
 void launch_report(DevCtrl *ctrl, DevReport *reports, int freeze, cudaStream_t st);
 // fixed_point_exit graph gate: IF condition = !frozen
 void launch_gate(const DevCtrl *ctrl, cudaGraphConditionalHandle h, cudaStream_t st);
+// multi-step graph: time mark; outer WHILE over `count` IRLS steps (stops
+// early at a fixed point when freeze_exit); copies of the frozen report
+void launch_mark(DevCtrl *ctrl, cudaStream_t st);
+void launch_outer_init(DevCtrl *ctrl, cudaGraphConditionalHandle h, int count, cudaStream_t st);
+void launch_outer_next(DevCtrl *ctrl, cudaGraphConditionalHandle h, int freeze_exit, cudaStream_t st);
+void launch_fill_reports(DevCtrl *ctrl, DevReport *reports, cudaStream_t st);
 // record_trace diagnostics: [S_eps, flow, current_s, true_res^2] + x range
 void launch_stencil_diag_ex(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, double eps, int norm,
                             const double *gsv, const double *gtv, cudaStream_t st);

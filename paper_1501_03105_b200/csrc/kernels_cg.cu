@@ -339,6 +339,7 @@ __global__ void k_report(DevCtrl *ctrl, DevReport *reports, int freeze)
     R.converged = ctrl->status == ST_OK && (ref == 0.0 || ctrl->res <= ctrl->rtol * ref);
     R.true_rel_res = R.S_eps = R.flow_value = R.current_s = 0.0;
     R.x_min = R.x_max = 0.0;
+    R.t_end = global_ns();
     ctrl->step = ctrl->step + 1;
     ctrl->xmin_key = ~0ull;
     ctrl->xmax_key = 0ull;
@@ -581,6 +582,47 @@ __global__ void k_gate(const DevCtrl *ctrl, cudaGraphConditionalHandle h)
 void launch_gate(const DevCtrl *ctrl, cudaGraphConditionalHandle h, cudaStream_t st)
 {
     k_gate<<<1, 1, 0, st>>>(ctrl, h);
+}
+
+__global__ void k_mark(DevCtrl *ctrl) { ctrl->t_mark = global_ns(); }
+
+__global__ void k_outer_init(DevCtrl *ctrl, cudaGraphConditionalHandle h, int count)
+{
+    ctrl->outer_left = count;
+    ctrl->outer_end = ctrl->step + count;
+    cudaGraphSetConditional(h, count > 0 ? 1u : 0u);
+}
+
+__global__ void k_outer_next(DevCtrl *ctrl, cudaGraphConditionalHandle h, int freeze_exit)
+{
+    const int left = ctrl->outer_left - 1;
+    ctrl->outer_left = left;
+    cudaGraphSetConditional(h, (left > 0 && !(freeze_exit && ctrl->frozen)) ? 1u : 0u);
+}
+
+// after a fixed-point exit: the skipped steps' reports are the frozen one's
+__global__ void k_fill_reports(DevCtrl *ctrl, DevReport *reports)
+{
+    const int end = ctrl->outer_end;
+    int step = ctrl->step;
+    if (step <= 0) return;
+    const DevReport last = reports[step - 1];
+    for (; step < end; step++) reports[step] = last;
+    ctrl->step = step;
+}
+
+void launch_mark(DevCtrl *ctrl, cudaStream_t st) { k_mark<<<1, 1, 0, st>>>(ctrl); }
+void launch_outer_init(DevCtrl *ctrl, cudaGraphConditionalHandle h, int count, cudaStream_t st)
+{
+    k_outer_init<<<1, 1, 0, st>>>(ctrl, h, count);
+}
+void launch_outer_next(DevCtrl *ctrl, cudaGraphConditionalHandle h, int freeze_exit, cudaStream_t st)
+{
+    k_outer_next<<<1, 1, 0, st>>>(ctrl, h, freeze_exit);
+}
+void launch_fill_reports(DevCtrl *ctrl, DevReport *reports, cudaStream_t st)
+{
+    k_fill_reports<<<1, 1, 0, st>>>(ctrl, reports);
 }
 
 void launch_report(DevCtrl *ctrl, DevReport *reports, int freeze, cudaStream_t st)
