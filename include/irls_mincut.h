@@ -118,8 +118,12 @@ irls_status irls_mincut_create_stencil(irls_ctx **ctx, const irls_comm_desc *com
  * row_ptr[n+1] (int64), col[row_ptr[n]] (int32), w (float64 >= 0).  Entries of
  * a row with the same column are merged by summation in CSR order (A7); self
  * loops are rejected; the merged matrix must be exactly symmetric.  The edge
- * {s,t}, if present, is the additive constant c_st (A5).  Single GPU in this
- * version (world_size 1). */
+ * {s,t}, if present, is the additive constant c_st (A5).  Multi-GPU: id
+ * strips — rank r owns the reduced ids of C3 groups [8r/W, 8(r+1)/W) (chunk
+ * boundaries; W must divide 8 and the graph must have >= 8 chunks of 4096
+ * non-terminals); its rows keep their neighbours' values in a ghost block
+ * refreshed by one grouped NCCL exchange per halo (send lists follow from the
+ * symmetry of G~); every rank passes the full CSR. */
 irls_status irls_mincut_create_csr(irls_ctx **ctx, const irls_comm_desc *comm, int64_t n,
                                    const int64_t *row_ptr, const int32_t *col, const double *w,
                                    int64_t s, int64_t t, const irls_options *opt);
@@ -286,11 +290,18 @@ typedef struct irls_vgroup irls_vgroup;
 irls_status irls_vgroup_create_stencil(irls_vgroup **g, int32_t world, int32_t device, int32_t nx, int32_t ny,
                                        int32_t nz, const double *cx, const double *cy, const double *cz,
                                        const double *cs, const double *ct, const irls_options *opt);
+/* The CSR graph's id strips (rank r owns C3 groups [8r/W, 8(r+1)/W): reduced
+ * ids on chunk boundaries; W > 1 needs >= 8 chunks), ghost blocks and halo
+ * lists, as irls_mincut_create_csr builds them on each of W processes. */
+irls_status irls_vgroup_create_csr(irls_vgroup **g, int32_t world, int32_t device, int64_t n, const int64_t *row_ptr,
+                                   const int32_t *col, const double *w, int64_t s, int64_t t,
+                                   const irls_options *opt);
 irls_status irls_vgroup_solve(irls_vgroup *g, int32_t mode, irls_step_report *per_step, int64_t *total_cg_iters);
 irls_status irls_vgroup_sweep_cut(irls_vgroup *g, uint8_t *side, int32_t *order, int64_t *k, double *cut_value);
 irls_status irls_vgroup_two_level_cut(irls_vgroup *g, uint8_t *side, irls_two_level_report *rep);
 irls_status irls_vgroup_get_potentials(irls_vgroup *g, double *x);
 irls_status irls_vgroup_set_terminal_weights(irls_vgroup *g, const double *cs, const double *ct);
+const char *irls_vgroup_last_error(const irls_vgroup *g);  /* first rank's error detail */
 void irls_vgroup_destroy(irls_vgroup *g);
 
 /* ---- host-only helpers of the multi-GPU plan (no device work) ----------- */
@@ -298,6 +309,10 @@ void irls_vgroup_destroy(irls_vgroup *g);
  * covers chunks [floor(gK/8), floor((g+1)K/8)). */
 irls_status irls_plan_stencil(int32_t nx, int32_t ny, int32_t nz, int32_t world, int32_t rank,
                               int32_t *z0, int32_t *z1, int32_t *g0, int32_t *g1);
+/* Id strip of rank `rank` of a CSR graph with nr non-terminals: reduced ids
+ * [lo, hi) = the chunks of C3 groups [g0, g1) = [8r/W, 8(r+1)/W); W > 1 needs
+ * every rank to own >= 1 chunk (else IRLS_ERR_INVALID_ARGUMENT). */
+irls_status irls_plan_csr(int64_t nr, int32_t world, int32_t rank, int64_t *lo, int64_t *hi, int32_t *g0, int32_t *g1);
 /* Halo plan of rank `rank`'s z-slab: element offsets relative to its first
  * owned node (send_lo/send_hi: boundary planes sent to peer_lo/peer_hi;
  * recv_lo/recv_hi: ghost planes received from them), count = nx*ny values

@@ -2,6 +2,8 @@
 // the per-solve CUDA graph with a device-side WHILE loop, the host-loop and
 // multi-GPU paths, and the sweep orchestration.
 #include <math.h>
+#include <cstdio>
+#include <cstdlib>
 #include <string.h>
 
 #include <algorithm>
@@ -228,7 +230,25 @@ static StencilArgs stencil_args(const irls_ctx *c, bool full)
     return s;
 }
 
+// The solve's rows (local strip with ghost columns; the whole graph on one rank).
 static SellArgs sell_args(const irls_ctx *c)
+{
+    SellArgs s;
+    s.n = c->n_own;
+    s.slice_ptr = c->lslice_ptr;
+    s.col = c->lcol;
+    s.c = c->lcap;
+    s.g = c->lg;
+    s.cs = c->lcs;
+    s.ct = c->lct;
+    s.wmax = c->lwmax;
+    s.gbase = c->multi ? c->npad_own : INT64_MAX;
+    s.glow = c->multi ? c->recv_off[c->rank] : 0;
+    return s;
+}
+
+// The whole graph in reduced ids (rank 0's sweep, two-level rounding, lambda_2).
+static SellArgs sell_args_full(const irls_ctx *c)
 {
     SellArgs s;
     s.n = c->n_glob;
@@ -239,6 +259,8 @@ static SellArgs sell_args(const irls_ctx *c)
     s.cs = c->cs;
     s.ct = c->ct;
     s.wmax = c->sell_wmax;
+    s.gbase = INT64_MAX;
+    s.glow = 0;
     return s;
 }
 
@@ -282,9 +304,26 @@ extern "C" irls_status irls_halo_plan(int32_t nx, int32_t ny, int32_t nz, int32_
     return IRLS_OK;
 }
 
+// CSR: pack the owned values the peers need, then one grouped exchange; the
+// peers' values land in the ghost block (contiguous per peer, ascending ids).
+static irls_status halo_csr(irls_ctx *c, double *arr, cudaStream_t st)
+{
+    const int64_t ns = c->send_off[c->world];
+    if (ns > 0) launch_halo_pack(arr, c->send_idx, ns, c->sendbuf, st);
+    NK(ncclGroupStart());
+    for (int q = 0; q < c->world; q++) {
+        const int64_t sc = c->send_off[q + 1] - c->send_off[q], rc = c->recv_off[q + 1] - c->recv_off[q];
+        if (sc > 0) NK(ncclSend(c->sendbuf + c->send_off[q], (size_t)sc, ncclDouble, q, c->nccl, st));
+        if (rc > 0) NK(ncclRecv(arr + c->npad_own + c->recv_off[q], (size_t)rc, ncclDouble, q, c->nccl, st));
+    }
+    NK(ncclGroupEnd());
+    return IRLS_OK;
+}
+
 static irls_status halo(irls_ctx *c, double *arr, cudaStream_t st)
 {
     if (!c->multi) return IRLS_OK;
+    if (c->kind == 1) return halo_csr(c, arr, st);
     const irls_halo &h = c->hplan;
     NK(ncclGroupStart());
     if (h.peer_lo >= 0) {
@@ -328,12 +367,10 @@ static irls_status gather_x(irls_ctx *c, double **full)
     NK(ncclGroupStart());
     if (c->rank == 0) {
         for (int r = 1; r < c->world; r++) {
-            int32_t z0, z1;
-            irls_plan_stencil(c->nx, c->ny, c->nz, c->world, r, &z0, &z1, nullptr, nullptr);
-            const int64_t lo = (int64_t)z0 * c->P, n = std::min<int64_t>((int64_t)z1 * c->P, c->n_glob) - lo;
-            NK(ncclRecv(c->x_full + lo, (size_t)n, ncclDouble, r, c->nccl, st));
+            const int64_t lo = c->rank_lo[r], n = c->rank_lo[r + 1] - lo;
+            if (n > 0) NK(ncclRecv(c->x_full + lo, (size_t)n, ncclDouble, r, c->nccl, st));
         }
-    } else {
+    } else if (c->n_own > 0) {
         NK(ncclSend(c->x, (size_t)c->n_own, ncclDouble, 0, c->nccl, st));
     }
     NK(ncclGroupEnd());
@@ -361,6 +398,21 @@ static irls_status coll_halo(Ranks &R, bool z_not_x, cudaStream_t st)
     irls_ctx *c = R[0];
     if (!c->multi) return IRLS_OK;
     if (!c->vg) return halo(c, z_not_x ? c->z : c->x, st);
+    if (c->kind == 1) {  // pack on every rank, then the same copies NCCL would make
+        for (irls_ctx *d : R) {
+            const int64_t ns = d->send_off[d->world];
+            if (ns > 0) launch_halo_pack(z_not_x ? d->z : d->x, d->send_idx, ns, d->sendbuf, st);
+        }
+        for (irls_ctx *d : R)
+            for (int q = 0; q < d->world; q++) {
+                const int64_t rc = d->recv_off[q + 1] - d->recv_off[q];
+                if (rc == 0) continue;
+                irls_ctx *o = R[q];
+                CK(cudaMemcpyAsync((z_not_x ? d->z : d->x) + d->npad_own + d->recv_off[q], o->sendbuf + o->send_off[d->rank],
+                                   sizeof(double) * rc, cudaMemcpyDeviceToDevice, st));
+            }
+        return IRLS_OK;
+    }
     for (irls_ctx *d : R) {
         const irls_halo &h = d->hplan;
         double *arr = z_not_x ? d->z : d->x;
@@ -415,7 +467,7 @@ static irls_status coll_minmax(Ranks &R, cudaStream_t st)
 static irls_status enq_assemble(Ranks &R, int mode, const CondArgs &cd, cudaStream_t st)
 {
     irls_status s;
-    if (R[0]->kind == 0 && mode != ASM_INIT && mode != ASM_LAMBDA2 && (s = coll_halo(R, false, st))) return s;
+    if (mode != ASM_INIT && mode != ASM_LAMBDA2 && (s = coll_halo(R, false, st))) return s;
     for (irls_ctx *c : R) {
         const VecArgs v = vec_args(c);
         const RedArgs ra = red_args(c);
@@ -445,8 +497,11 @@ static irls_status enq_body(Ranks &R, const CondArgs &cd, cudaStream_t st)
         if (c->kind == 0) launch_stencil_pspmv(stencil_args(c, false), v, ra, cd, st);
         else launch_sell_pspmv(sell_args(c), v, ra, cd, st);
         c->launches++;
-        if (c->multi) {
+        if (c->multi && c->kind == 0) {
             launch_ghost_pupdate(v, c->lo_ghost, c->hi_ghost, c->P, c->ctrl, st);
+            c->launches++;
+        } else if (c->multi && c->n_ghost > 0) {
+            launch_ghost_range_pupdate(v, c->npad_own, c->n_ghost, c->ctrl, st);
             c->launches++;
         }
     }
@@ -967,6 +1022,12 @@ static irls_status create_stencil_impl(irls_ctx **out, const irls_comm_desc *com
             c->n_fin = count_nonempty(c->K, g0, g1);
             c->lo_ghost = c->world > 1 && c->rank > 0;
             c->hi_ghost = c->world > 1 && c->rank < c->world - 1;
+            c->rank_lo.assign(c->world + 1, N);
+            for (int r = 0; r < c->world; r++) {
+                int32_t a0, a1;
+                irls_plan_stencil(nx, ny, nz, c->world, r, &a0, &a1, nullptr, nullptr);
+                c->rank_lo[r] = std::min<int64_t>((int64_t)a0 * c->P, N);
+            }
             if (c->multi) s = irls_halo_plan(nx, ny, nz, c->world, c->rank, &c->hplan);
         }
         if (!s) {
@@ -1019,16 +1080,54 @@ struct Ent {
     double w;
 };
 
+static irls_status create_csr_impl(irls_ctx **out, const irls_comm_desc *comm, int64_t n, const int64_t *row_ptr,
+                                   const int32_t *col, const double *w, int64_t s_, int64_t t_, const irls_options *opt,
+                                   irls_vgroup *vg);
+
 extern "C" irls_status irls_mincut_create_csr(irls_ctx **out, const irls_comm_desc *comm, int64_t n,
                                               const int64_t *row_ptr, const int32_t *col, const double *w, int64_t s_,
                                               int64_t t_, const irls_options *opt)
+{
+    return create_csr_impl(out, comm, n, row_ptr, col, w, s_, t_, opt, nullptr);
+}
+
+// Id-strip plan of a CSR graph with nr non-terminals over `world` ranks:
+// rank r owns C3 groups [8r/W, 8(r+1)/W), i.e. reduced ids [lo, hi) on chunk
+// boundaries; every rank needs at least one chunk.
+static bool csr_strips(int64_t nr, int world, std::vector<int64_t> &lo)
+{
+    const int32_t K = (int32_t)((nr + kChunk - 1) / kChunk);
+    lo.assign(world + 1, nr);
+    for (int r = 0; r < world; r++) {
+        const int64_t c0 = group_lo(kGroups * r / world, K), c1 = group_lo(kGroups * (r + 1) / world, K);
+        if (world > 1 && c1 <= c0) return false;
+        lo[r] = std::min<int64_t>(c0 * kChunk, nr);
+    }
+    return true;
+}
+
+extern "C" irls_status irls_plan_csr(int64_t nr, int32_t world, int32_t rank, int64_t *lo, int64_t *hi, int32_t *g0,
+                                     int32_t *g1)
+{
+    if (nr < 0 || world < 1 || 8 % world != 0 || rank < 0 || rank >= world) return IRLS_ERR_INVALID_ARGUMENT;
+    std::vector<int64_t> v;
+    if (!csr_strips(nr, world, v)) return IRLS_ERR_INVALID_ARGUMENT;
+    if (lo) *lo = v[rank];
+    if (hi) *hi = v[rank + 1];
+    if (g0) *g0 = kGroups * rank / world;
+    if (g1) *g1 = kGroups * (rank + 1) / world;
+    return IRLS_OK;
+}
+
+static irls_status create_csr_impl(irls_ctx **out, const irls_comm_desc *comm, int64_t n, const int64_t *row_ptr,
+                                   const int32_t *col, const double *w, int64_t s_, int64_t t_, const irls_options *opt,
+                                   irls_vgroup *vg)
 {
     if (!out) return IRLS_ERR_INVALID_ARGUMENT;
     *out = nullptr;
     if (check_opts(opt) || n < 2 || !row_ptr || !col || !w || s_ < 0 || t_ < 0 || s_ >= n || t_ >= n)
         return IRLS_ERR_INVALID_ARGUMENT;
     if (s_ == t_) return IRLS_ERR_SOURCE_EQUALS_SINK;
-    if (comm && comm->world_size != 1) return IRLS_ERR_INVALID_ARGUMENT;  // CSR: single GPU in this version
     if (n >= ((int64_t)1 << 31)) return IRLS_ERR_INVALID_ARGUMENT;
     if (row_ptr[0] != 0) return IRLS_ERR_INVALID_ARGUMENT;
     for (int64_t u = 0; u < n; u++)
@@ -1151,8 +1250,10 @@ extern "C" irls_status irls_mincut_create_csr(irls_ctx **out, const irls_comm_de
         }
     }
     irls_ctx *c = new irls_ctx();
+    c->vg = vg;
     irls_status st = common_setup(c, comm, opt);
-    c->multi = false;  // CSR: single GPU, no communicator
+    if (!st && c->multi && !csr_strips(nr, c->world, c->rank_lo)) st = IRLS_ERR_INVALID_ARGUMENT;
+    if (!st && !c->multi) c->rank_lo = {0, nr};
     if (!st) {
         c->kind = 1;
         c->n_glob = nr;
@@ -1161,22 +1262,90 @@ extern "C" irls_status irls_mincut_create_csr(irls_ctx **out, const irls_comm_de
         c->t_id = t_;
         c->c_st = cst;
         c->K = (int32_t)((nr + kChunk - 1) / kChunk);
-        c->g0 = 0; c->g1 = 8;
-        c->lo = 0;
-        c->n_own = nr;
-        c->chunk0 = 0;
-        c->nchunks = c->K;
-        c->n_fin = count_nonempty(c->K, 0, 8);
+        c->g0 = kGroups * c->rank / c->world;
+        c->g1 = kGroups * (c->rank + 1) / c->world;
+        c->lo = c->rank_lo[c->rank];
+        c->n_own = c->rank_lo[c->rank + 1] - c->lo;
+        c->chunk0 = (int32_t)(c->lo / kChunk);
+        c->nchunks = (int32_t)((c->n_own + kChunk - 1) / kChunk);
+        c->n_fin = count_nonempty(c->K, c->g0, c->g1);
         c->n_links = (int64_t)aidx.size() / 2;
         c->F = compute_F(cmax, cnt);
         c->n_entries = nent;
         c->sell_wmax = (int32_t)sell_wmax;
-        st = alloc_solver(c, 0);
+        c->npad_own = (int64_t)c->nchunks * kChunk;
     }
+    // the strip's local SELL: owned neighbours -> v - lo, others -> ghost block
+    // (ascending global id, hence grouped by owner rank); send lists by the
+    // symmetry of G~: u goes to peer q iff u has a neighbour owned by q
+    std::vector<int64_t> lsptr;
+    std::vector<int32_t> lscol, lsend;
+    std::vector<double> lscap;
+    int64_t lwmax = 0;
+    if (!st && c->multi) {
+        const int64_t lo = c->lo, hi = c->lo + c->n_own, W = c->world;
+        auto owner = [&](int64_t v) {
+            return (int)(std::upper_bound(c->rank_lo.begin(), c->rank_lo.end() - 1, v) - c->rank_lo.begin()) - 1;
+        };
+        std::vector<int32_t> ghosts;
+        for (int64_t r = lo; r < hi; r++)
+            for (int64_t e = aptr[r]; e < aptr[r + 1]; e++)
+                if (aidx[e] < lo || aidx[e] >= hi) ghosts.push_back(aidx[e]);
+        std::sort(ghosts.begin(), ghosts.end());
+        ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
+        c->n_ghost = (int64_t)ghosts.size();
+        c->recv_off.assign(W + 1, 0);
+        for (int32_t v : ghosts) c->recv_off[owner(v) + 1]++;
+        for (int q = 0; q < W; q++) c->recv_off[q + 1] += c->recv_off[q];
+        std::vector<std::vector<int32_t>> sendq(W);
+        for (int64_t r = lo; r < hi; r++) {
+            int peers[16], np = 0;
+            for (int64_t e = aptr[r]; e < aptr[r + 1]; e++) {
+                const int64_t v = aidx[e];
+                if (v >= lo && v < hi) continue;
+                const int q = owner(v);
+                bool seen = false;
+                for (int i = 0; i < np; i++) seen |= peers[i] == q;
+                if (!seen && np < 16) peers[np++] = q;
+            }
+            for (int i = 0; i < np; i++) sendq[peers[i]].push_back((int32_t)(r - lo));
+        }
+        c->send_off.assign(W + 1, 0);
+        for (int q = 0; q < W; q++) {
+            c->send_off[q + 1] = c->send_off[q] + (int64_t)sendq[q].size();
+            lsend.insert(lsend.end(), sendq[q].begin(), sendq[q].end());
+        }
+        const int64_t nl = c->n_own, lnsl = (nl + kSell - 1) / kSell;
+        lsptr.assign(lnsl + 1, 0);
+        for (int64_t sl = 0; sl < lnsl; sl++) {
+            int64_t wm = 0;
+            for (int64_t r = sl * kSell; r < std::min<int64_t>(nl, sl * kSell + kSell); r++)
+                wm = std::max(wm, aptr[lo + r + 1] - aptr[lo + r]);
+            lsptr[sl + 1] = lsptr[sl] + kSell * wm;
+            lwmax = std::max(lwmax, wm);
+        }
+        lscol.assign(std::max<int64_t>(lsptr[lnsl], 1), -1);
+        lscap.assign(std::max<int64_t>(lsptr[lnsl], 1), 0.0);
+        for (int64_t r = 0; r < nl; r++) {
+            const int64_t sl = r / kSell, ln = r % kSell, gr = lo + r;
+            for (int64_t k = 0; k < aptr[gr + 1] - aptr[gr]; k++) {
+                const int64_t v = aidx[aptr[gr] + k];
+                const int64_t lv = (v >= lo && v < hi)
+                                       ? v - lo
+                                       : c->npad_own + (std::lower_bound(ghosts.begin(), ghosts.end(), (int32_t)v) - ghosts.begin());
+                lscol[lsptr[sl] + kSell * k + ln] = (int32_t)lv;
+                lscap[lsptr[sl] + kSell * k + ln] = ac[aptr[gr] + k];
+            }
+        }
+        c->ln_entries = lsptr[lnsl];
+        c->lwmax = (int32_t)lwmax;
+        if (c->npad_own + c->n_ghost >= ((int64_t)1 << 31)) st = IRLS_ERR_INVALID_ARGUMENT;
+    }
+    if (!st) st = alloc_solver(c, c->multi ? c->n_ghost : 0);
     if (!st) {
-        const int64_t npad = (int64_t)c->nchunks * kChunk;
-        c->cs = dalloc<double>(c, npad);
-        c->ct = dalloc<double>(c, npad);
+        const int64_t gpad = (int64_t)c->K * kChunk;  // the whole graph (rank 0 sweeps it)
+        c->cs = dalloc<double>(c, gpad);
+        c->ct = dalloc<double>(c, gpad);
         c->slice_ptr = dalloc<int64_t>(c, nsl + 1);
         c->col = dalloc<int32_t>(c, nent);
         c->cap = dalloc<double>(c, nent);
@@ -1184,14 +1353,56 @@ extern "C" irls_status irls_mincut_create_csr(irls_ctx **out, const irls_comm_de
         c->orig_dev = dalloc<int64_t>(c, std::max<int64_t>(nr, 1));
         if (!c->cs || !c->ct || !c->slice_ptr || !c->col || !c->cap || !c->gsell || !c->orig_dev) st = IRLS_ERR_OOM;
     }
+    if (!st && !c->multi) {  // one rank: the solve runs on the global structure
+        c->lslice_ptr = c->slice_ptr;
+        c->lcol = c->col;
+        c->lcap = c->cap;
+        c->lg = c->gsell;
+        c->lcs = c->cs;
+        c->lct = c->ct;
+        c->lwmax = c->sell_wmax;
+        c->ln_entries = c->n_entries;
+    } else if (!st) {
+        const int64_t npad = c->npad_own, le = std::max<int64_t>(c->ln_entries, 1);
+        c->lslice_ptr = dalloc<int64_t>(c, (int64_t)lsptr.size());
+        c->lcol = dalloc<int32_t>(c, le);
+        c->lcap = dalloc<double>(c, le);
+        c->lg = dalloc<double>(c, le);
+        c->lcs = dalloc<double>(c, npad);
+        c->lct = dalloc<double>(c, npad);
+        c->send_idx = dalloc<int32_t>(c, std::max<int64_t>((int64_t)lsend.size(), 1));
+        c->sendbuf = dalloc<double>(c, std::max<int64_t>((int64_t)lsend.size(), 1));
+        if (!c->lslice_ptr || !c->lcol || !c->lcap || !c->lg || !c->lcs || !c->lct || !c->send_idx || !c->sendbuf)
+            st = IRLS_ERR_OOM;
+        cudaError_t e = cudaSuccess;
+        auto up = [&](void *dst, const void *src, size_t bytes) {
+            if (e == cudaSuccess && bytes > 0) e = memcpy_sync(c, dst, src, bytes, cudaMemcpyHostToDevice);
+        };
+        if (!st) {
+            up(c->lslice_ptr, lsptr.data(), sizeof(int64_t) * lsptr.size());
+            up(c->lcol, lscol.data(), sizeof(int32_t) * lscol.size());
+            up(c->lcap, lscap.data(), sizeof(double) * lscap.size());
+            if (c->n_own > 0) {
+                up(c->lcs, hcs.data() + c->lo, sizeof(double) * c->n_own);
+                up(c->lct, hct.data() + c->lo, sizeof(double) * c->n_own);
+            }
+            up(c->send_idx, lsend.data(), sizeof(int32_t) * lsend.size());
+            if (e != cudaSuccess) st = fail(c, IRLS_ERR_CUDA, std::string("csr strip upload: ") + cudaGetErrorString(e));
+        }
+    }
+    if (!st) st = init_nccl(c, comm);
     if (!st && nr > 0) {
-        memcpy_sync(c, c->cs, hcs.data(), sizeof(double) * nr, cudaMemcpyHostToDevice);
-        memcpy_sync(c, c->ct, hct.data(), sizeof(double) * nr, cudaMemcpyHostToDevice);
-        memcpy_sync(c, c->slice_ptr, sptr.data(), sizeof(int64_t) * (nsl + 1), cudaMemcpyHostToDevice);
-        memcpy_sync(c, c->col, scol.data(), sizeof(int32_t) * nent, cudaMemcpyHostToDevice);
-        memcpy_sync(c, c->cap, scap.data(), sizeof(double) * nent, cudaMemcpyHostToDevice);
-        memcpy_sync(c, c->orig_dev, orig.data(), sizeof(int64_t) * nr, cudaMemcpyHostToDevice);
-        if (cudaStreamSynchronize(c->stream) != cudaSuccess) st = fail(c, IRLS_ERR_CUDA, "csr upload");
+        cudaError_t e = cudaSuccess;
+        auto up = [&](void *dst, const void *src, size_t bytes) {
+            if (e == cudaSuccess && bytes > 0) e = memcpy_sync(c, dst, src, bytes, cudaMemcpyHostToDevice);
+        };
+        up(c->cs, hcs.data(), sizeof(double) * nr);
+        up(c->ct, hct.data(), sizeof(double) * nr);
+        up(c->slice_ptr, sptr.data(), sizeof(int64_t) * (nsl + 1));
+        up(c->col, scol.data(), sizeof(int32_t) * nent);
+        up(c->cap, scap.data(), sizeof(double) * nent);
+        up(c->orig_dev, orig.data(), sizeof(int64_t) * nr);
+        if (e != cudaSuccess) st = fail(c, IRLS_ERR_CUDA, std::string("csr upload: ") + cudaGetErrorString(e));
     }
     if (st) {
         irls_mincut_destroy(c);
@@ -1320,6 +1531,10 @@ extern "C" irls_status irls_set_terminal_weights(irls_ctx *c, const double *cs, 
         c->F = compute_F(cmax, cnt);
         CK(cudaMemcpyAsync(c->cs, cs, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
         CK(cudaMemcpyAsync(c->ct, ct, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+        if (c->lcs != c->cs && c->n_own > 0) {  // the strip's own copy
+            CK(cudaMemcpyAsync(c->lcs, cs + c->lo, sizeof(double) * c->n_own, cudaMemcpyHostToDevice, c->stream));
+            CK(cudaMemcpyAsync(c->lct, ct + c->lo, sizeof(double) * c->n_own, cudaMemcpyHostToDevice, c->stream));
+        }
         CK(cudaStreamSynchronize(c->stream));
     }
     c->sweep_valid = false;
@@ -1420,7 +1635,7 @@ static irls_status sweep_rank0(irls_ctx *c, const double *xfull, uint8_t *side, 
     sweep_rank(ord, b, st);
     launches++;
     if (c->kind == 0) sweep_delta_stencil(stencil_args(c, true), n, c->F, b, st);
-    else sweep_delta_sell(sell_args(c), c->F, b, st);
+    else sweep_delta_sell(sell_args_full(c), c->F, b, st);
     sweep_delta_order(ord, b, st);
     launches += 2;
     sweep_scan_argmin(b, qfix_host(c->c_st, c->F), st);
@@ -1437,7 +1652,7 @@ static irls_status sweep_rank0(irls_ctx *c, const double *xfull, uint8_t *side, 
         sweep_side_cross_stencil(stencil_args(c, true), n, b, ra, st);
     } else {
         CK(cudaMemsetAsync(b.side, 0, c->n_total, st));
-        sweep_side_cross_sell(sell_args(c), c->orig_dev, c->n_total, b, ra, st);
+        sweep_side_cross_sell(sell_args_full(c), c->orig_dev, c->n_total, b, ra, st);
         const uint8_t one = 1;
         CK(cudaMemcpyAsync(b.side + c->s_id, &one, 1, cudaMemcpyHostToDevice, st));
     }
@@ -1509,14 +1724,14 @@ extern "C" irls_status irls_time_kernel(irls_ctx *c, int32_t which, int32_t reps
         save.push_back(b);
     }
     double *gsave = nullptr;
-    const int64_t gbytes = c->kind == 0 ? 3 * npad : c->n_entries;
+    const int64_t gbytes = c->kind == 0 ? 3 * npad : c->ln_entries;
     CK(cudaMalloc(&gsave, sizeof(double) * std::max<int64_t>(gbytes, 1)));
     if (c->kind == 0) {
         cudaMemcpyAsync(gsave, c->gx, sizeof(double) * npad, cudaMemcpyDeviceToDevice, st);
         cudaMemcpyAsync(gsave + npad, c->gy, sizeof(double) * npad, cudaMemcpyDeviceToDevice, st);
         cudaMemcpyAsync(gsave + 2 * npad, c->gz, sizeof(double) * npad, cudaMemcpyDeviceToDevice, st);
     } else {
-        cudaMemcpyAsync(gsave, c->gsell, sizeof(double) * c->n_entries, cudaMemcpyDeviceToDevice, st);
+        cudaMemcpyAsync(gsave, c->lg, sizeof(double) * c->ln_entries, cudaMemcpyDeviceToDevice, st);
     }
     DevCtrl hc;
     CK(cudaMemcpyAsync(&hc, c->ctrl, sizeof(hc), cudaMemcpyDeviceToHost, st));
@@ -1565,7 +1780,7 @@ extern "C" irls_status irls_time_kernel(irls_ctx *c, int32_t which, int32_t reps
         cudaMemcpyAsync(c->gy, gsave + npad, sizeof(double) * npad, cudaMemcpyDeviceToDevice, st);
         cudaMemcpyAsync(c->gz, gsave + 2 * npad, sizeof(double) * npad, cudaMemcpyDeviceToDevice, st);
     } else {
-        cudaMemcpyAsync(c->gsell, gsave, sizeof(double) * c->n_entries, cudaMemcpyDeviceToDevice, st);
+        cudaMemcpyAsync(c->lg, gsave, sizeof(double) * c->ln_entries, cudaMemcpyDeviceToDevice, st);
     }
     cudaMemcpyAsync(c->ctrl, &hc, sizeof(hc), cudaMemcpyHostToDevice, st);
     CK(cudaStreamSynchronize(st));
@@ -1606,10 +1821,10 @@ extern "C" void irls_vgroup_destroy(irls_vgroup *g)
     delete g;
 }
 
-extern "C" irls_status irls_vgroup_create_stencil(irls_vgroup **out, int32_t world, int32_t device, int32_t nx,
-                                                  int32_t ny, int32_t nz, const double *cx, const double *cy,
-                                                  const double *cz, const double *cs, const double *ct,
-                                                  const irls_options *opt)
+// W contexts of one graph on one device and one stream (every rank's strip
+// or slab), plus the device arrays the virtual collectives read.
+template <class MakeRank>
+static irls_status vgroup_create(irls_vgroup **out, int32_t world, int32_t device, MakeRank make)
 {
     if (!out || world < 1 || 8 % world != 0) return IRLS_ERR_INVALID_ARGUMENT;
     *out = nullptr;
@@ -1627,7 +1842,7 @@ extern "C" irls_status irls_vgroup_create_stencil(irls_vgroup **out, int32_t wor
         comm.nccl_unique_id = nullptr;
         comm.cuda_stream = g->stream;
         irls_ctx *c = nullptr;
-        irls_status s = create_stencil_impl(&c, &comm, nx, ny, nz, cx, cy, cz, cs, ct, opt, g);
+        irls_status s = make(&c, &comm, g);
         if (s) {
             irls_vgroup_destroy(g);
             return s;
@@ -1649,6 +1864,33 @@ extern "C" irls_status irls_vgroup_create_stencil(irls_vgroup **out, int32_t wor
     }
     *out = g;
     return IRLS_OK;
+}
+
+extern "C" irls_status irls_vgroup_create_stencil(irls_vgroup **out, int32_t world, int32_t device, int32_t nx,
+                                                  int32_t ny, int32_t nz, const double *cx, const double *cy,
+                                                  const double *cz, const double *cs, const double *ct,
+                                                  const irls_options *opt)
+{
+    return vgroup_create(out, world, device, [&](irls_ctx **c, const irls_comm_desc *comm, irls_vgroup *g) {
+        return create_stencil_impl(c, comm, nx, ny, nz, cx, cy, cz, cs, ct, opt, g);
+    });
+}
+
+extern "C" const char *irls_vgroup_last_error(const irls_vgroup *g)
+{
+    if (!g || g->ranks.empty()) return "null group";
+    for (const irls_ctx *c : g->ranks)
+        if (!c->err.empty()) return c->err.c_str();
+    return "";
+}
+
+extern "C" irls_status irls_vgroup_create_csr(irls_vgroup **out, int32_t world, int32_t device, int64_t n,
+                                              const int64_t *row_ptr, const int32_t *col, const double *w, int64_t s,
+                                              int64_t t, const irls_options *opt)
+{
+    return vgroup_create(out, world, device, [&](irls_ctx **c, const irls_comm_desc *comm, irls_vgroup *g) {
+        return create_csr_impl(c, comm, n, row_ptr, col, w, s, t, opt, g);
+    });
 }
 
 extern "C" irls_status irls_vgroup_solve(irls_vgroup *g, int32_t mode, irls_step_report *per_step, int64_t *total)
@@ -1834,7 +2076,7 @@ static irls_status two_level_rank0(irls_ctx *c, const double *xfull, uint8_t *si
     std::vector<int32_t> tiles_n1((size_t)std::max<int64_t>(nt, 1), 0);
     if (n > 0) {
         if (c->kind == 0) tl_classify_stencil(stencil_args(c, true), n, xfull, r->gamma0, r->gamma1, c->F, b, st);
-        else tl_classify_sell(sell_args(c), xfull, r->gamma0, r->gamma1, c->F, b, st);
+        else tl_classify_sell(sell_args_full(c), xfull, r->gamma0, r->gamma1, c->F, b, st);
         exclusive_scan_i32(b.flag, n, b.cid, b.scan_tmp, st, &launches);
         exclusive_scan_i32(b.deg, n, b.eoff, b.scan_tmp, st, &launches);
         launches += 1;
@@ -1854,7 +2096,7 @@ static irls_status two_level_rank0(irls_ctx *c, const double *xfull, uint8_t *si
     for (int64_t i = 0; i < nt && n > 0; i++) qst += tiles[i];
     if (nc > 0) {
         if (c->kind == 0) tl_fill_stencil(stencil_args(c, true), n, xfull, r->gamma0, r->gamma1, c->F, b, st);
-        else tl_fill_sell(sell_args(c), c->F, b, st);
+        else tl_fill_sell(sell_args_full(c), c->F, b, st);
         launches++;
     }
     irls_status ls = last_launch(c, "two-level coarsening");
@@ -1923,7 +2165,7 @@ static irls_status two_level_rank0(irls_ctx *c, const double *xfull, uint8_t *si
             sweep_side_cross_stencil(stencil_args(c, true), n, sb, ra, st);
         } else {
             CK(cudaMemsetAsync(b.side, 0, c->n_total, st));
-            sweep_side_cross_sell(sell_args(c), c->orig_dev, c->n_total, sb, ra, st);
+            sweep_side_cross_sell(sell_args_full(c), c->orig_dev, c->n_total, sb, ra, st);
             const uint8_t one = 1;
             CK(cudaMemcpyAsync(b.side + c->s_id, &one, 1, cudaMemcpyHostToDevice, st));
         }
@@ -2125,7 +2367,7 @@ extern "C" irls_status irls_lambda2(irls_ctx *c, double cg_rtol, int32_t cg_max_
         ra.g1 = 8;
         ra.n_fin = count_nonempty(ra.K, 0, 8);
         if (c->kind == 0) launch_l2_quad_stencil(stencil_args(c, true), n, c->x, ra, st);
-        else launch_l2_quad_sell(sell_args(c), c->x, ra, st);
+        else launch_l2_quad_sell(sell_args_full(c), c->x, ra, st);
         s = last_launch(c, "lambda2 quadratic form");
     }
     double slots[2 * kGroups];

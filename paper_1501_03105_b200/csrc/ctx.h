@@ -42,6 +42,20 @@ struct irls_ctx {
     double c_st = 0.0;
     int64_t *orig_dev = nullptr;
 
+    // ---- CSR multi-rank (id strips): the solve's local SELL (rows [lo, lo+n_own),
+    // columns remapped: owned v -> v - lo, ghost -> npad_own + ghost index) and
+    // the halo lists; aliases of the global arrays when the path is single-rank
+    int64_t *lslice_ptr = nullptr;
+    int32_t *lcol = nullptr;
+    double *lcap = nullptr, *lg = nullptr, *lcs = nullptr, *lct = nullptr;
+    int32_t lwmax = 0;
+    int64_t ln_entries = 0;
+    int64_t n_ghost = 0, npad_own = 0;       // ghost values at [npad_own, npad_own + n_ghost)
+    std::vector<int64_t> send_off, recv_off;  // [world + 1]: per-peer ranges of send_idx / the ghost block
+    int32_t *send_idx = nullptr;             // local ids packed for the peers (device)
+    double *sendbuf = nullptr;
+    std::vector<int64_t> rank_lo;            // [world + 1]: first reduced id owned by every rank
+
     // ---- sweep fixed point
     int32_t F = 0;
 

@@ -44,6 +44,7 @@ struct SellArgs {
     double *g;                   // conductances
     const double *cs, *ct;
     int32_t wmax;                // widest slice (max degree)
+    int64_t gbase, glow;         // strips: columns >= gbase are ghosts; the first glow ghosts have lower ids
 };
 
 struct CondArgs {
@@ -70,6 +71,9 @@ void launch_sell_pspmv(const SellArgs &s, const VecArgs &v, const RedArgs &ra, c
 // ghost planes of p for the next iteration (multi-GPU stencil)
 void launch_ghost_pupdate(const VecArgs &v, int64_t ghost_lo, int64_t ghost_hi, int64_t plane, DevCtrl *ctrl,
                           cudaStream_t st);
+// CSR multi-rank: ghost block of p updated from the exchanged z; halo packing
+void launch_ghost_range_pupdate(const VecArgs &v, int64_t start, int64_t count, DevCtrl *ctrl, cudaStream_t st);
+void launch_halo_pack(const double *arr, const int32_t *idx, int64_t n, double *out, cudaStream_t st);
 // K5: r -= alpha q, z = Dinv r, RZ reduction
 void launch_axpy_jacobi(const VecArgs &v, const RedArgs &ra, const CondArgs &cd, cudaStream_t st);
 // after the loop: x += alpha p_last (or x = 0 if b = 0)

@@ -277,6 +277,39 @@ __global__ void k_ghost_pupdate(VecArgs v, int64_t ghost_lo, int64_t ghost_hi, i
     }
 }
 
+// CSR strips: the ghost block [start, start + count) of p, same update.
+__global__ void k_ghost_range_pupdate(VecArgs v, int64_t start, int64_t count, const DevCtrl *ctrl)
+{
+    const int32_t k = ctrl->k;
+    const bool first = (k == 0);
+    const double beta = ctrl->beta;
+    const double *pold = (k & 1) ? v.p1 : v.p0;
+    double *pnew = (k & 1) ? v.p0 : v.p1;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) {
+        const int64_t w = start + i;
+        pnew[w] = first ? v.z[w] : v.z[w] + beta * pold[w];
+    }
+}
+
+__global__ void k_halo_pack(const double *arr, const int32_t *idx, int64_t n, double *out)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = arr[idx[i]];
+}
+
+void launch_ghost_range_pupdate(const VecArgs &v, int64_t start, int64_t count, DevCtrl *ctrl, cudaStream_t st)
+{
+    if (count <= 0) return;
+    k_ghost_range_pupdate<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(v, start, count, ctrl);
+}
+
+void launch_halo_pack(const double *arr, const int32_t *idx, int64_t n, double *out, cudaStream_t st)
+{
+    if (n <= 0) return;
+    k_halo_pack<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(arr, idx, n, out);
+}
+
 // ---------------------------------------------------------------------------
 // K5: r = r - alpha q; z = r Dinv (Jacobi, A12); RZ reduction.
 // ---------------------------------------------------------------------------
@@ -425,7 +458,7 @@ __global__ void __launch_bounds__(kThreads) k_sell_diag(SellArgs s, VecArgs v, R
             if (nb < 0) break;
             const double xv = v.x[nb];
             a2 = a2 + s.g[idx] * xv;
-            if (nb > u) {
+            if (nb < s.gbase ? nb > u : nb - s.gbase >= s.glow) {  // owned edge: higher global id
                 const double a = s.c[idx] * (xu - xv);
                 Se = Se + sqrt(a * a + eps2);
                 const double d = xu - xv;

@@ -86,7 +86,7 @@ SYMBOLS = ["irls_options_default", "irls_nccl_unique_id", "irls_mincut_create_st
            "irls_halo_plan", "irls_combine_slots", "irls_vgroup_create_stencil", "irls_vgroup_solve",
            "irls_vgroup_sweep_cut", "irls_vgroup_get_potentials", "irls_vgroup_set_terminal_weights",
            "irls_vgroup_destroy", "irls_two_level_cut", "irls_two_level_get_coarse", "irls_coarse_maxflow",
-           "irls_vgroup_two_level_cut", "irls_exact_min_cut", "irls_lambda2"]
+           "irls_vgroup_two_level_cut", "irls_exact_min_cut", "irls_lambda2", "irls_vgroup_create_csr", "irls_vgroup_last_error", "irls_plan_csr"]
 
 
 def lib():
@@ -124,6 +124,12 @@ def lib():
         L.irls_halo_plan.argtypes = [C.c_int32] * 5 + [C.POINTER(irls_halo)]
         L.irls_vgroup_create_stencil.argtypes = [C.POINTER(P), C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                                  C.c_int32, P, P, P, P, P, C.POINTER(irls_options)]
+        L.irls_vgroup_create_csr.argtypes = [C.POINTER(P), C.c_int32, C.c_int32, C.c_int64, P, P, P, C.c_int64,
+                                             C.c_int64, C.POINTER(irls_options)]
+        L.irls_plan_csr.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                    C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+        L.irls_vgroup_last_error.argtypes = [P]
+        L.irls_vgroup_last_error.restype = C.c_char_p
         L.irls_vgroup_solve.argtypes = [P, C.c_int32, P, C.POINTER(C.c_int64)]
         L.irls_vgroup_sweep_cut.argtypes = [P, P, P, C.POINTER(C.c_int64), C.POINTER(C.c_double)]
         L.irls_vgroup_get_potentials.argtypes = [P, P]
@@ -201,6 +207,15 @@ def irls_halo_plan(nx, ny, nz, world, rank) -> dict:
     if rc:
         raise IrlsError(rc, "irls_halo_plan")
     return {k: getattr(h, k) for k, _ in h._fields_ if k != "reserved"}
+
+
+def irls_plan_csr(nr, world, rank):
+    """Host-only: (lo, hi, g0, g1) of rank's id strip."""
+    lo, hi, g0, g1 = C.c_int64(), C.c_int64(), C.c_int32(), C.c_int32()
+    rc = lib().irls_plan_csr(nr, world, rank, C.byref(lo), C.byref(hi), C.byref(g0), C.byref(g1))
+    if rc:
+        raise IrlsError(rc, "irls_plan_csr")
+    return lo.value, hi.value, g0.value, g1.value
 
 
 def irls_combine_slots(slots) -> float:
@@ -405,18 +420,29 @@ class MinCut:
 
 
 class VGroup:
-    """W ranks of the z-slab multi-GPU path on one device (irls_vgroup_*)."""
+    """W ranks of the multi-GPU path (z-slabs of a grid, id strips of a CSR
+    graph) on one device (irls_vgroup_*)."""
 
     def __init__(self, spec, world, opts: irls_options | None = None, device=0):
-        arrs = [_f64(spec[k]) for k in ("cx", "cy", "cz", "cs", "ct")]
         self.opts = opts or options()
         self.h = C.c_void_p()
-        self.n = spec["nx"] * spec["ny"] * spec["nz"]
-        rc = lib().irls_vgroup_create_stencil(C.byref(self.h), world, device, spec["nx"], spec["ny"], spec["nz"],
-                                              *[_ptr(a) for a in arrs], C.byref(self.opts))
+        if spec["kind"] == "stencil":
+            arrs = [_f64(spec[k]) for k in ("cx", "cy", "cz", "cs", "ct")]
+            self.n = spec["nx"] * spec["ny"] * spec["nz"]
+            self.n_total = self.n + 2
+            rc = lib().irls_vgroup_create_stencil(C.byref(self.h), world, device, spec["nx"], spec["ny"], spec["nz"],
+                                                  *[_ptr(a) for a in arrs], C.byref(self.opts))
+        else:
+            rp = np.ascontiguousarray(spec["row_ptr"], dtype=np.int64)
+            cl = np.ascontiguousarray(spec["col"], dtype=np.int32)
+            ww = _f64(spec["w"])
+            self.n = spec["n"] - 2
+            self.n_total = spec["n"]
+            rc = lib().irls_vgroup_create_csr(C.byref(self.h), world, device, spec["n"], _ptr(rp), _ptr(cl), _ptr(ww),
+                                              spec["s"], spec["t"], C.byref(self.opts))
         if rc:
             self.h = None
-            raise IrlsError(rc, "irls_vgroup_create_stencil")
+            raise IrlsError(rc, "irls_vgroup_create")
 
     def irls_vgroup_solve(self, mode=IRLS_FROM_SCRATCH, T=None):
         nrep = (T + 1 if mode == IRLS_FROM_SCRATCH else T) if T is not None else None
@@ -425,12 +451,12 @@ class VGroup:
         rc = lib().irls_vgroup_solve(self.h, mode, C.cast(buf, C.c_void_p) if buf is not None else None,
                                      C.byref(total))
         if rc:
-            raise IrlsError(rc, "irls_vgroup_solve")
+            raise IrlsError(rc, "irls_vgroup_solve", lib().irls_vgroup_last_error(self.h).decode(errors="replace"))
         return ([r.as_dict() for r in buf[:nrep]] if buf is not None else None), total.value
 
     def irls_vgroup_sweep_cut(self, order=False):
-        side = np.zeros(self.n + 2, dtype=np.uint8)
-        o = np.zeros(self.n, dtype=np.int32) if order else None
+        side = np.zeros(self.n_total, dtype=np.uint8)
+        o = np.zeros(max(self.n, 1), dtype=np.int32) if order else None
         k, cut = C.c_int64(), C.c_double()
         rc = lib().irls_vgroup_sweep_cut(self.h, _ptr(side), _ptr(o), C.byref(k), C.byref(cut))
         if rc:
@@ -438,7 +464,7 @@ class VGroup:
         return side, o, k.value, cut.value
 
     def irls_vgroup_two_level_cut(self):
-        side = np.zeros(self.n + 2, dtype=np.uint8)
+        side = np.zeros(self.n_total, dtype=np.uint8)
         r = irls_two_level_report()
         rc = lib().irls_vgroup_two_level_cut(self.h, _ptr(side), C.byref(r))
         if rc:

@@ -44,6 +44,21 @@ def _worker(rank, world, port, q):
             dist.all_gather_object(plans, (z0, z1, g0, g1))
             out[dims] = plans
 
+        # ---- CSR id strips (config 3's n~, a ragged one, exactly 8 chunks)
+        for nr in (23734786, 39469, 8 * 4096):
+            strip = I.irls_plan_csr(nr, world, rank)
+            plans = [None] * world
+            dist.all_gather_object(plans, strip)
+            out[("csr", nr)] = plans
+            # slot-exact allreduce over the strip's own C3 groups
+            v = np.random.default_rng(nr % 1000).standard_normal(nr)
+            gs = oracle.c3_group_sums(v)
+            mine = np.zeros(8)
+            mine[strip[2]:strip[3]] = gs[strip[2]:strip[3]]
+            t = torch.from_numpy(mine.copy())
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            out[("csr_sum", nr)] = I.irls_combine_slots(t.numpy()) == oracle.c3_sum(v)
+
         # ---- halo exchange with the library's plan
         nx, ny, nz = 16, 16, 64
         N, P = nx * ny * nz, nx * ny
@@ -130,6 +145,20 @@ def test_slab_plans_tile_the_grid(results):
         assert plans[0][0] == 0 and plans[-1][1] == dims[2]
         assert plans[0][1] == plans[1][0]
         assert [p[2:] for p in plans] == [(0, 4), (4, 8)]
+
+
+def test_csr_strips(results):
+    """Id strips tile [0, n~), start on chunk (4096) boundaries, own the C3
+    groups [4r, 4r + 4), and the slot allreduce over them is the one-process
+    C3 sum bitwise."""
+    for nr in (23734786, 39469, 8 * 4096):
+        plans = results[0][("csr", nr)]
+        assert plans == results[1][("csr", nr)]
+        assert plans[0][0] == 0 and plans[-1][1] == nr and plans[0][1] == plans[1][0]
+        assert all(p[0] % 4096 == 0 for p in plans)
+        assert [p[2:] for p in plans] == [(0, 4), (4, 8)]
+        for r in (0, 1):
+            assert results[r][("csr_sum", nr)]
 
 
 def test_halo_plan_exchange(results):

@@ -136,3 +136,72 @@ def test_nccl_one_rank_communicator(irls):
     s1, r1 = m.irls_two_level_cut()
     assert np.array_equal(s1, s2) and r1["cut_value"] == r2["cut_value"]
     g.close()
+    # the same through a 1-rank communicator on a CSR graph (id strips, W = 1)
+    spec = gen.road_graph(120, seed=2, knn=50)
+    m, reps1, tot1, sw1 = single(irls, spec, irls.options(T=T), T)
+    comm = irls.comm_desc(1, 0, 0, irls.irls_nccl_unique_id(), torch.cuda.current_stream().cuda_stream)  # one id per comm
+    g = irls.MinCut.from_spec(spec, irls.options(T=T), comm)
+    _, tot = g.irls_solve(irls.IRLS_FROM_SCRATCH, T=T)
+    assert tot == tot1 and np.array_equal(g.irls_get_potentials(), m.irls_get_potentials())
+    side, _, k, cut = g.irls_sweep_cut()
+    assert k == sw1[2] and cut == sw1[3] and np.array_equal(side, sw1[0])
+    g.close()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_vgroup_csr_strips(irls, world):
+    """CSR id strips (SURVEY §8(e), config 3's partition): every rank's rows
+    with a ghost block refreshed by the halo (packed send lists), per-rank C3
+    groups, slot allreduce, ghost p update, gather and the rank-0 sweep and
+    two-level rounding: bitwise equal to one rank and to the oracle."""
+    spec = gen.road_graph(200, seed=2, knn=60)  # 39,469 non-terminals: 9.6 chunks, ragged strips
+    T = 12
+    m, reps1, tot1, sw1 = single(irls, spec, irls.options(T=T, record_trace=1), T)
+    g = irls.VGroup(spec, world, irls.options(T=T, record_trace=1))
+    reps, tot = g.irls_vgroup_solve(irls.IRLS_FROM_SCRATCH, T=T)
+    assert tot == tot1
+    for a, b in zip(reps, reps1):
+        for k in ("cg_iters", "converged", "rel_res", "S_eps", "flow_value", "true_rel_res", "x_min", "x_max"):
+            assert a[k] == b[k], k
+    x = g.irls_vgroup_get_potentials()
+    assert np.array_equal(x, m.irls_get_potentials())
+    S = oracle.Solver(oracle.Graph(spec), T=T)
+    S.run(record=False)
+    assert np.array_equal(x, S.x())
+    side, order, k, cut = g.irls_vgroup_sweep_cut(order=True)
+    assert k == sw1[2] and cut == sw1[3] and np.array_equal(side, sw1[0])
+    s2, r2 = g.irls_vgroup_two_level_cut()
+    s1, r1 = m.irls_two_level_cut()
+    assert np.array_equal(s1, s2) and r1["cut_value"] == r2["cut_value"]
+    # a config-5 style sequence on the strips (terminal weights of every strip)
+    cs, ct = S.graph.terminals()
+    for fs, ft in gen.config5_factors(cs.shape[0], n_problems=2, seed=4):
+        cs, ct = cs * fs, ct * ft
+        m.irls_set_terminal_weights(cs, ct)
+        g.irls_vgroup_set_terminal_weights(cs, ct)
+        _, t1 = m.irls_solve(irls.IRLS_CONTINUE, T=T)
+        _, t2 = g.irls_vgroup_solve(irls.IRLS_CONTINUE, T=T)
+        assert t1 == t2
+        assert np.array_equal(g.irls_vgroup_get_potentials(), m.irls_get_potentials())
+    g.close()
+
+
+@pytest.mark.slow
+def test_vgroup_config3_world8(irls):
+    """BASELINE config 3 (road-like CSR, 23.7M nodes) as 8 id strips: every
+    step's iteration count, x^(50) and the sweep equal one rank bitwise."""
+    spec = gen.config3()
+    m, reps1, tot1, sw1 = single(irls, spec, irls.options(T=50), 50)
+    g = irls.VGroup(spec, 8, irls.options(T=50))
+    reps, tot = g.irls_vgroup_solve(irls.IRLS_FROM_SCRATCH, T=50)
+    assert [r["cg_iters"] for r in reps] == [r["cg_iters"] for r in reps1]
+    assert np.array_equal(g.irls_vgroup_get_potentials(), m.irls_get_potentials())
+    side, _, k, cut = g.irls_vgroup_sweep_cut()
+    assert k == sw1[2] and cut == sw1[3] and np.array_equal(side, sw1[0])
+    g.close()
+
+
+def test_vgroup_csr_rejects_too_few_chunks(irls):
+    spec = gen.road_graph(60, seed=2, knn=40)  # < 8 chunks
+    with pytest.raises(irls.IrlsError):
+        irls.VGroup(spec, 2)
