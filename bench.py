@@ -55,6 +55,8 @@ def workload(name):
     from synthetic import generators as gen
     if name == "config4":
         return gen.config4(), "config4: 512x512x256 6-neighbour blob grid (BASELINE configs[3]), seed 3"
+    if name == "config3":
+        return gen.config3(), "config3: 4900^2 road-like CSR graph, 30% edges deleted, LCC (BASELINE configs[2]), seed 2"
     if name == "config2":
         return gen.config2(), "config2: 128^3 6-neighbour blob grid (BASELINE configs[1]), seed 1"
     if name == "config1":
@@ -119,6 +121,20 @@ def oracle_sample(spec, planes=8, T=3):
     `planes` z-planes of the grid, init + T IRLS steps (cap 50, rtol 1e-3).
     Returns (GEdge/s, seconds, description)."""
     import oracle
+    if spec["kind"] == "csr":  # config 3: the same generator at 1000^2 (a bounded instance of the recipe)
+        from synthetic import generators as gen
+        sub = gen.road_graph(1000, seed=2, knn=200)
+        G = oracle.Graph(sub)
+        S = oracle.Solver(G, T=T)
+        links = G.nnz // 2
+        t0 = time.perf_counter()
+        _, reps = S.run(record=False)
+        S.sweep()
+        dt = time.perf_counter() - t0
+        iters = sum(r["cg_iters"] for r in reps)
+        desc = (f"oracle (plain C, 1 thread) on the config-3 recipe at 1000^2 ({G.n} nodes, {links} n-links), "
+                f"init + {T} IRLS steps + sweep: {iters} CG iterations in {dt:.1f} s")
+        return links * iters / dt / 1e9, dt, desc
     nx, ny = spec["nx"], spec["ny"]
     n = nx * ny * planes
     sub = dict(spec)
@@ -291,7 +307,13 @@ def main():
     t_k3 = m.irls_time_kernel(I.KERNEL_PSPMV, 20)
     t_k5 = m.irls_time_kernel(I.KERNEL_AXPY, 20)
     t_k1 = m.irls_time_kernel(I.KERNEL_ASSEMBLE, 10)
-    ach = K3_BYTES_PER_NODE * n_own / (t_k3 * 1e-3) / 1e9
+    csr = spec["kind"] == "csr"
+    # algorithmic bytes per launch; CSR: K3 56 B/node + 12 B per
+    # stored entry, K1 56 B/node + 20 B per entry (this rank's rows)
+    ent = 2 * n_links * n_own / max(st["n_nonterminal"], 1)
+    k3_bytes = (56 * n_own + 12 * ent) if csr else K3_BYTES_PER_NODE * n_own
+    k1_bytes = (56 * n_own + 20 * ent) if csr else K1_BYTES_PER_NODE * n_own
+    ach = k3_bytes / (t_k3 * 1e-3) / 1e9
     traffic = None
     try:  # per-launch DRAM bytes of K3 from the committed ncu --set full capture (same config)
         tj = json.load(open(os.path.join(ROOT, "profiles", "r01_k3_traffic.json")))
@@ -300,10 +322,10 @@ def main():
     except Exception:
         pass
     kernels = {
-        "K3_pspmv": {"ms": t_k3, "GBps": ach, "bytes_per_node": K3_BYTES_PER_NODE},
+        "K3_pspmv": {"ms": t_k3, "GBps": ach, "bytes_per_launch": k3_bytes},
         "K5_axpy_jacobi": {"ms": t_k5, "GBps": K5_BYTES_PER_NODE * n_own / (t_k5 * 1e-3) / 1e9,
                            "bytes_per_node": K5_BYTES_PER_NODE},
-        "K1_reweight_assemble": {"ms": t_k1, "GBps": K1_BYTES_PER_NODE * n_own / (t_k1 * 1e-3) / 1e9,
+        "K1_reweight_assemble": {"ms": t_k1, "GBps": k1_bytes / (t_k1 * 1e-3) / 1e9,
                                  "bytes_per_node": K1_BYTES_PER_NODE},
     }
     cg_iter_ms = t_k3 + t_k5
@@ -322,12 +344,15 @@ def main():
 
     # ---- e2e through the C ABI with pinned host buffers ---------------------
     pinned = {}
-    for name in ("cx", "cy", "cz", "cs", "ct"):
-        t = torch.empty(spec[name].shape[0], dtype=torch.float64, pin_memory=True)
-        t.numpy()[:] = spec[name]
+    arrays = ("row_ptr", "col", "w") if csr else ("cx", "cy", "cz", "cs", "ct")
+    for name in arrays:
+        a = np.ascontiguousarray(spec[name])
+        t = torch.empty(a.shape[0], dtype=getattr(torch, str(a.dtype)), pin_memory=True)
+        t.numpy()[:] = a
         pinned[name] = t.numpy()
-    side_host = torch.empty(spec["nx"] * spec["ny"] * spec["nz"] + 2, dtype=torch.uint8, pin_memory=True).numpy()
-    h2d = 5 * 8 * pinned["cx"].shape[0]
+    n_total = spec["n"] if csr else spec["nx"] * spec["ny"] * spec["nz"] + 2
+    side_host = torch.empty(n_total, dtype=torch.uint8, pin_memory=True).numpy()
+    h2d = sum(a.nbytes for a in pinned.values())
     d2h = side_host.shape[0] if rank == 0 else 0
     e2e_iters = 0
     barrier()
@@ -338,8 +363,12 @@ def main():
             obj = [I.irls_nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(obj, src=0)
             comm = I.comm_desc(world, rank, local, obj[0], stream.cuda_stream)
-        mm = I.MinCut.irls_mincut_create_stencil(spec["nx"], spec["ny"], spec["nz"], pinned["cx"], pinned["cy"],
-                                                 pinned["cz"], pinned["cs"], pinned["ct"], opts, comm)
+        if csr:
+            mm = I.MinCut.irls_mincut_create_csr(spec["n"], pinned["row_ptr"], pinned["col"], pinned["w"], spec["s"],
+                                                 spec["t"], opts, comm)
+        else:
+            mm = I.MinCut.irls_mincut_create_stencil(spec["nx"], spec["ny"], spec["nz"], pinned["cx"], pinned["cy"],
+                                                     pinned["cz"], pinned["cs"], pinned["ct"], opts, comm)
         _, tot = mm.irls_solve(I.IRLS_FROM_SCRATCH, T=T, reports=False)
         import ctypes as C
         kk, cc = C.c_int64(), C.c_double()
@@ -379,7 +408,8 @@ def main():
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                      "traffic": traffic, "traffic_note": "ncu dram__bytes_read+write per K3 launch "
                      "(profiles/r01_k3_traffic.json) over the live K3 duration, GB/s; algorithmic bytes per launch "
-                     f"= {K3_BYTES_PER_NODE * n_own / 1e9:.3f} GB", "kernel": "K3 fused p-update + SpMV + p.q (stencil)",
+                     f"= {k3_bytes / 1e9:.3f} GB", "kernel": "K3 fused p-update + SpMV + p.q "
+                     + ("(SELL-64 CSR)" if csr else "(stencil)"),
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks
                      else "fallback 6650 GB/s (B200_PROFILING.md)",
                      "frac_of_nominal_8TBps": ach / 8000.0, "kernels": kernels},
