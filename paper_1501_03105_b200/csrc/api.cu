@@ -2,6 +2,9 @@
 // the per-solve CUDA graph with a device-side WHILE loop, the host-loop and
 // multi-GPU paths, and the sweep orchestration.
 #include <math.h>
+#include <atomic>
+#include <memory>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <string.h>
@@ -1074,6 +1077,39 @@ static irls_status create_stencil_impl(irls_ctx **out, const irls_comm_desc *com
     return IRLS_OK;
 }
 
+// Uninitialised host array (filled in parallel; avoids serial zeroing).
+template <class T>
+struct HostBuf {
+    std::unique_ptr<T[]> p;
+    explicit HostBuf(int64_t n) : p(new T[(size_t)std::max<int64_t>(n, 1)]) {}
+    T &operator[](int64_t i) { return p[i]; }
+    const T &operator[](int64_t i) const { return p[i]; }
+    T *data() { return p.get(); }
+    const T *data() const { return p.get(); }
+};
+
+// Host thread pool for create-time preparation (row blocks).
+static int host_threads(int64_t n)
+{
+    if (n < 200000) return 1;
+    const unsigned hc = std::thread::hardware_concurrency();
+    return (int)std::min<unsigned>(std::max(1u, hc), 32u);
+}
+
+template <class F>
+static void parallel_for(int64_t n, F f)
+{
+    const int nt = host_threads(n);
+    if (nt == 1) {
+        f(0, (int64_t)0, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (int i = 0; i < nt; i++)
+        th.emplace_back([&, i]() { f(i, n * i / nt, n * (i + 1) / nt); });
+    for (auto &t : th) t.join();
+}
+
 struct Ent {
     int32_t col;
     int64_t pos;
@@ -1133,99 +1169,188 @@ static irls_status create_csr_impl(irls_ctx **out, const irls_comm_desc *comm, i
     for (int64_t u = 0; u < n; u++)
         if (row_ptr[u + 1] < row_ptr[u]) return IRLS_ERR_INVALID_ARGUMENT;
     const int64_t nnz = row_ptr[n];
-    for (int64_t e = 0; e < nnz; e++) {
-        if (col[e] < 0 || col[e] >= n) return IRLS_ERR_INVALID_ARGUMENT;
-        if (!(w[e] >= 0.0) || isinf(w[e])) return IRLS_ERR_BAD_CAPACITY;
+    // Host preparation runs on the host threads (row blocks); every result is
+    // independent of the thread count (first offending entry wins, integer
+    // counts, per-row sums in CSR order).
+    {
+        std::vector<int64_t> bad(host_threads(nnz), INT64_MAX);
+        std::vector<int> code(bad.size(), 0);
+        parallel_for(nnz, [&](int i, int64_t a, int64_t b) {
+            for (int64_t e = a; e < b; e++) {
+                if (col[e] < 0 || col[e] >= n) { bad[i] = e; code[i] = IRLS_ERR_INVALID_ARGUMENT; return; }
+                if (!(w[e] >= 0.0) || isinf(w[e])) { bad[i] = e; code[i] = IRLS_ERR_BAD_CAPACITY; return; }
+            }
+        });
+        for (size_t i = 0; i < bad.size(); i++)
+            if (bad[i] != INT64_MAX) return (irls_status)code[i];
+        std::vector<uint8_t> loop(host_threads(n), 0);
+        parallel_for(n, [&](int i, int64_t a, int64_t b) {
+            for (int64_t u = a; u < b && !loop[i]; u++)
+                for (int64_t e = row_ptr[u]; e < row_ptr[u + 1]; e++)
+                    if (col[e] == u) { loop[i] = 1; break; }
+        });
+        for (uint8_t l : loop)
+            if (l) return IRLS_ERR_INVALID_ARGUMENT;
     }
-    for (int64_t u = 0; u < n; u++)
-        for (int64_t e = row_ptr[u]; e < row_ptr[u + 1]; e++)
-            if (col[e] == u) return IRLS_ERR_INVALID_ARGUMENT;
-    // merge duplicates in CSR order (A7); fast path when rows are strictly ascending
+    // merge duplicates in CSR order (A7): count per row, then fill
     std::vector<int64_t> mptr(n + 1, 0);
-    std::vector<int32_t> mcol;
-    std::vector<double> mw;
-    mcol.reserve(nnz);
-    mw.reserve(nnz);
-    std::vector<Ent> tmp;
-    for (int64_t u = 0; u < n; u++) {
+    auto merge_row = [&](int64_t u, std::vector<Ent> &tmp, int32_t *oc, double *ow) -> int64_t {
         const int64_t a = row_ptr[u], b = row_ptr[u + 1];
         bool sorted = true;
         for (int64_t e = a + 1; e < b; e++)
             if (col[e] <= col[e - 1]) { sorted = false; break; }
-        mptr[u] = (int64_t)mcol.size();
         if (sorted) {
-            for (int64_t e = a; e < b; e++) { mcol.push_back(col[e]); mw.push_back(w[e]); }
-        } else {
-            tmp.clear();
-            for (int64_t e = a; e < b; e++) tmp.push_back({col[e], e, w[e]});
-            std::stable_sort(tmp.begin(), tmp.end(), [](const Ent &x, const Ent &y) { return x.col < y.col; });
-            for (size_t i = 0; i < tmp.size(); i++) {
-                if (i > 0 && tmp[i].col == tmp[i - 1].col) mw.back() = mw.back() + tmp[i].w;
-                else { mcol.push_back(tmp[i].col); mw.push_back(tmp[i].w); }
+            if (oc)
+                for (int64_t e = a; e < b; e++) { oc[e - a] = col[e]; ow[e - a] = w[e]; }
+            return b - a;
+        }
+        tmp.clear();
+        for (int64_t e = a; e < b; e++) tmp.push_back({col[e], e, w[e]});
+        std::stable_sort(tmp.begin(), tmp.end(), [](const Ent &x, const Ent &y) { return x.col < y.col; });
+        int64_t m = 0;
+        double last = 0.0;
+        for (size_t i = 0; i < tmp.size(); i++) {
+            if (i > 0 && tmp[i].col == tmp[i - 1].col) {
+                last = last + tmp[i].w;
+                if (ow) ow[m - 1] = last;
+            } else {
+                last = tmp[i].w;
+                if (oc) { oc[m] = tmp[i].col; ow[m] = last; }
+                m++;
             }
         }
-    }
-    mptr[n] = (int64_t)mcol.size();
+        return m;
+    };
+    parallel_for(n, [&](int, int64_t a, int64_t b) {
+        std::vector<Ent> tmp;
+        for (int64_t u = a; u < b; u++) mptr[u + 1] = merge_row(u, tmp, nullptr, nullptr);
+    });
+    for (int64_t u = 0; u < n; u++) mptr[u + 1] += mptr[u];
+    HostBuf<int32_t> mcol(mptr[n]);
+    HostBuf<double> mw(mptr[n]);
+    parallel_for(n, [&](int, int64_t a, int64_t b) {
+        std::vector<Ent> tmp;
+        for (int64_t u = a; u < b; u++) merge_row(u, tmp, mcol.data() + mptr[u], mw.data() + mptr[u]);
+    });
     // exact symmetry
-    for (int64_t u = 0; u < n; u++)
-        for (int64_t e = mptr[u]; e < mptr[u + 1]; e++) {
-            const int32_t v = mcol[e];
-            const auto beg = mcol.begin() + mptr[v], end = mcol.begin() + mptr[v + 1];
-            const auto it = std::lower_bound(beg, end, (int32_t)u);
-            if (it == end || *it != u || mw[it - mcol.begin()] != mw[e]) return IRLS_ERR_NOT_SYMMETRIC;
-        }
+    {
+        std::vector<uint8_t> asym(host_threads(n), 0);
+        parallel_for(n, [&](int i, int64_t a, int64_t b) {
+            for (int64_t u = a; u < b && !asym[i]; u++)
+                for (int64_t e = mptr[u]; e < mptr[u + 1]; e++) {
+                    const int32_t v = mcol[e];
+                    const int32_t *beg = mcol.data() + mptr[v], *end = mcol.data() + mptr[v + 1];
+                    const int32_t *it = std::lower_bound(beg, end, (int32_t)u);
+                    if (it == end || *it != u || mw[it - mcol.data()] != mw[e]) { asym[i] = 1; break; }
+                }
+        });
+        for (uint8_t a : asym)
+            if (a) return IRLS_ERR_NOT_SYMMETRIC;
+    }
     const int64_t nr = n - 2;
     auto red = [&](int64_t v) { return v - (v > s_) - (v > t_); };
+    auto orig_of = [&](int64_t r) {  // reduced id -> original id
+        int64_t u = r;
+        const int64_t lo2 = std::min(s_, t_), hi2 = std::max(s_, t_);
+        if (u >= lo2) u++;
+        if (u >= hi2) u++;
+        return u;
+    };
     std::vector<double> hcs(std::max<int64_t>(nr, 1), 0.0), hct(std::max<int64_t>(nr, 1), 0.0);
     std::vector<int64_t> orig(std::max<int64_t>(nr, 1), 0);
     std::vector<int64_t> aptr(nr + 1, 0);
-    std::vector<int32_t> aidx;
-    std::vector<double> ac;
     double cst = 0.0;
     for (int64_t e = mptr[s_]; e < mptr[s_ + 1]; e++)
         if (mcol[e] == t_) cst = mw[e];
-    double cmax = cst;
-    int64_t cnt = cst > 0.0;
-    {
-        int64_t r = 0;
-        for (int64_t u = 0; u < n; u++) {
-            if (u == s_ || u == t_) continue;
-            aptr[r] = (int64_t)aidx.size();
+    parallel_for(nr, [&](int, int64_t a, int64_t b) {
+        for (int64_t r = a; r < b; r++) {
+            const int64_t u = orig_of(r);
             orig[r] = u;
+            int64_t k = 0;
             for (int64_t e = mptr[u]; e < mptr[u + 1]; e++) {
                 const int64_t v = mcol[e];
                 if (v == s_) hcs[r] = mw[e];
                 else if (v == t_) hct[r] = mw[e];
-                else if (mw[e] > 0.0) {
-                    aidx.push_back((int32_t)red(v));
-                    ac.push_back(mw[e]);
-                    if (v > u) { cnt++; cmax = std::max(cmax, mw[e]); }
-                }
+                else if (mw[e] > 0.0) k++;
             }
-            if (hcs[r] > 0) { cnt++; cmax = std::max(cmax, hcs[r]); }
-            if (hct[r] > 0) { cnt++; cmax = std::max(cmax, hct[r]); }
-            r++;
+            aptr[r + 1] = k;
         }
-        aptr[nr] = (int64_t)aidx.size();
-    }
-    // Prop. 1 / A8: every component of G~ touches a positive terminal edge
+    });
+    for (int64_t r = 0; r < nr; r++) aptr[r + 1] += aptr[r];
+    HostBuf<int32_t> aidx(aptr[nr]);
+    HostBuf<double> ac(aptr[nr]);
+    std::vector<int64_t> tcnt(host_threads(nr), 0);
+    std::vector<double> tmax(tcnt.size(), 0.0);
+    parallel_for(nr, [&](int i, int64_t a, int64_t b) {
+        int64_t cn = 0;
+        double cm = 0.0;
+        for (int64_t r = a; r < b; r++) {
+            const int64_t u = orig[r];
+            int64_t k = aptr[r];
+            for (int64_t e = mptr[u]; e < mptr[u + 1]; e++) {
+                const int64_t v = mcol[e];
+                if (v == s_ || v == t_ || !(mw[e] > 0.0)) continue;
+                aidx[k] = (int32_t)red(v);
+                ac[k] = mw[e];
+                k++;
+                if (v > u) { cn++; cm = std::max(cm, mw[e]); }
+            }
+            if (hcs[r] > 0) { cn++; cm = std::max(cm, hcs[r]); }
+            if (hct[r] > 0) { cn++; cm = std::max(cm, hct[r]); }
+        }
+        tcnt[i] = cn;
+        tmax[i] = cm;
+    });
+    double cmax = cst;
+    int64_t cnt = cst > 0.0;
+    for (size_t i = 0; i < tcnt.size(); i++) { cnt += tcnt[i]; cmax = std::max(cmax, tmax[i]); }
+    // Prop. 1 / A8: every component of G~ touches a positive terminal edge.
+    // Lock-free union-find over the edges (the components do not depend on
+    // the union order), then every component's root must be anchored.
     {
-        std::vector<uint8_t> seen(std::max<int64_t>(nr, 1), 0);
-        std::vector<int64_t> q;
-        for (int64_t r0 = 0; r0 < nr; r0++) {
-            if (seen[r0]) continue;
-            bool anchored = false;
-            q.clear();
-            q.push_back(r0);
-            seen[r0] = 1;
-            for (size_t h = 0; h < q.size(); h++) {
-                const int64_t u = q[h];
-                if (hcs[u] > 0.0 || hct[u] > 0.0) anchored = true;
-                for (int64_t e = aptr[u]; e < aptr[u + 1]; e++)
-                    if (!seen[aidx[e]]) { seen[aidx[e]] = 1; q.push_back(aidx[e]); }
+        std::unique_ptr<std::atomic<int32_t>[]> par(new std::atomic<int32_t>[(size_t)std::max<int64_t>(nr, 1)]);
+        std::unique_ptr<std::atomic<uint8_t>[]> anc(new std::atomic<uint8_t>[(size_t)std::max<int64_t>(nr, 1)]);
+        parallel_for(nr, [&](int, int64_t a, int64_t b) {
+            for (int64_t r = a; r < b; r++) {
+                par[r].store((int32_t)r, std::memory_order_relaxed);
+                anc[r].store(0, std::memory_order_relaxed);
             }
-            if (!anchored) return IRLS_ERR_SINGULAR;
-        }
+        });
+        auto find = [&](int32_t x) {
+            for (;;) {
+                int32_t p = par[x].load(std::memory_order_relaxed);
+                if (p == x) return x;
+                const int32_t gp = par[p].load(std::memory_order_relaxed);
+                if (gp != p) par[x].compare_exchange_weak(p, gp, std::memory_order_relaxed);
+                x = gp;
+            }
+        };
+        parallel_for(nr, [&](int, int64_t a, int64_t b) {
+            for (int64_t r = a; r < b; r++)
+                for (int64_t e = aptr[r]; e < aptr[r + 1]; e++) {
+                    if (aidx[e] < r) continue;
+                    int32_t x = (int32_t)r, y = aidx[e];
+                    for (;;) {
+                        x = find(x);
+                        y = find(y);
+                        if (x == y) break;
+                        if (x < y) std::swap(x, y);  // link the larger root below the smaller
+                        int32_t expect = x;
+                        if (par[x].compare_exchange_strong(expect, y, std::memory_order_relaxed)) break;
+                    }
+                }
+        });
+        parallel_for(nr, [&](int, int64_t a, int64_t b) {
+            for (int64_t r = a; r < b; r++)
+                if (hcs[r] > 0.0 || hct[r] > 0.0) anc[find((int32_t)r)].store(1, std::memory_order_relaxed);
+        });
+        std::vector<uint8_t> lonely(host_threads(nr), 0);
+        parallel_for(nr, [&](int i, int64_t a, int64_t b) {
+            for (int64_t r = a; r < b && !lonely[i]; r++)
+                if (!anc[find((int32_t)r)].load(std::memory_order_relaxed)) lonely[i] = 1;
+        });
+        for (uint8_t l : lonely)
+            if (l) return IRLS_ERR_SINGULAR;
     }
     // SELL-64 (slices of 64 consecutive rows, column-major inside a slice: the
     // k-th neighbour of rows 2t and 2t+1 are adjacent, one 128-bit load)
@@ -1240,15 +1365,20 @@ static irls_status create_csr_impl(irls_ctx **out, const irls_comm_desc *comm, i
         sell_wmax = std::max(sell_wmax, wmax);
     }
     const int64_t nent = sptr[nsl];
-    std::vector<int32_t> scol(std::max<int64_t>(nent, 1), -1);
-    std::vector<double> scap(std::max<int64_t>(nent, 1), 0.0);
-    for (int64_t r = 0; r < nr; r++) {
-        const int64_t sl = r / kSell, ln = r % kSell;
-        for (int64_t k = 0; k < aptr[r + 1] - aptr[r]; k++) {
-            scol[sptr[sl] + kSell * k + ln] = aidx[aptr[r] + k];
-            scap[sptr[sl] + kSell * k + ln] = ac[aptr[r] + k];
+    HostBuf<int32_t> scol(nent);
+    HostBuf<double> scap(nent);
+    parallel_for(nsl, [&](int, int64_t a, int64_t b) {  // padding slots: col -1, c 0
+        for (int64_t e = sptr[a]; e < sptr[b]; e++) { scol[e] = -1; scap[e] = 0.0; }
+    });
+    parallel_for(nr, [&](int, int64_t a, int64_t b) {
+        for (int64_t r = a; r < b; r++) {
+            const int64_t sl = r / kSell, ln = r % kSell;
+            for (int64_t k = 0; k < aptr[r + 1] - aptr[r]; k++) {
+                scol[sptr[sl] + kSell * k + ln] = aidx[aptr[r] + k];
+                scap[sptr[sl] + kSell * k + ln] = ac[aptr[r] + k];
+            }
         }
-    }
+    });
     irls_ctx *c = new irls_ctx();
     c->vg = vg;
     irls_status st = common_setup(c, comm, opt);
@@ -1269,7 +1399,7 @@ static irls_status create_csr_impl(irls_ctx **out, const irls_comm_desc *comm, i
         c->chunk0 = (int32_t)(c->lo / kChunk);
         c->nchunks = (int32_t)((c->n_own + kChunk - 1) / kChunk);
         c->n_fin = count_nonempty(c->K, c->g0, c->g1);
-        c->n_links = (int64_t)aidx.size() / 2;
+        c->n_links = aptr[nr] / 2;
         c->F = compute_F(cmax, cnt);
         c->n_entries = nent;
         c->sell_wmax = (int32_t)sell_wmax;
