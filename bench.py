@@ -229,7 +229,9 @@ def main():
         obj = [I.irls_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
-    comm = I.comm_desc(world, rank, local, uid, stream.cuda_stream)
+    # device memory: torch's caching allocator owns every array of the contexts
+    mem = I.TorchDeviceMemory(local)
+    comm = I.comm_desc(world, rank, local, uid, stream.cuda_stream, memory=mem)
 
     def barrier():
         if world > 1:
@@ -354,15 +356,14 @@ def main():
     side_host = torch.empty(n_total, dtype=torch.uint8, pin_memory=True).numpy()
     h2d = sum(a.nbytes for a in pinned.values())
     d2h = side_host.shape[0] if rank == 0 else 0
-    e2e_iters = 0
-    barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.e2e_steps):
+    import ctypes as C
+
+    def e2e_step():
+        nonlocal comm
         if world > 1:  # a fresh NCCL id per communicator (part of the user's create path)
             obj = [I.irls_nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(obj, src=0)
-            comm = I.comm_desc(world, rank, local, obj[0], stream.cuda_stream)
+            comm = I.comm_desc(world, rank, local, obj[0], stream.cuda_stream, memory=mem)
         if csr:
             mm = I.MinCut.irls_mincut_create_csr(spec["n"], pinned["row_ptr"], pinned["col"], pinned["w"], spec["s"],
                                                  spec["t"], opts, comm)
@@ -370,14 +371,21 @@ def main():
             mm = I.MinCut.irls_mincut_create_stencil(spec["nx"], spec["ny"], spec["nz"], pinned["cx"], pinned["cy"],
                                                      pinned["cz"], pinned["cs"], pinned["ct"], opts, comm)
         _, tot = mm.irls_solve(I.IRLS_FROM_SCRATCH, T=T, reports=False)
-        import ctypes as C
         kk, cc = C.c_int64(), C.c_double()
         rc = I.lib().irls_sweep_cut(mm.h, side_host.ctypes.data_as(C.c_void_p) if rank == 0 else None, None,
                                     C.byref(kk), C.byref(cc))
         if rc:
             raise I.IrlsError(rc, "irls_sweep_cut")
         mm.close()
-        e2e_iters += tot
+        return tot
+
+    e2e_step()  # warm-up (first-touch of the allocator's blocks for the sweep buffers)
+    e2e_iters = 0
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.e2e_steps):
+        e2e_iters += e2e_step()
     e1.record(stream)
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1))

@@ -89,11 +89,21 @@ void irls_options_default(irls_options *opt);
  * a stencil context given world_size 1 AND an id runs the multi-rank code
  * path over a 1-rank NCCL communicator (host loop, slot allreduce, finalize
  * kernels, gather / broadcast) — a self-test of the NCCL plumbing on one GPU.
- * cuda_stream: a cudaStream_t to run on, or NULL for a library-owned one. */
+ * cuda_stream: a cudaStream_t to run on, or NULL for a library-owned one.
+ * device_alloc / device_free: the caller's device memory (e.g. torch
+ * tensors from its caching allocator) for every array the context owns —
+ * called at create, on the first sweep / two-level rounding and when the
+ * coarse graph grows, with the context's stream; freed at destroy.  NULL:
+ * the library's stream-ordered pool.  alloc_user is passed through. */
+typedef void *(*irls_device_alloc_fn)(size_t bytes, void *stream, void *user);
+typedef void (*irls_device_free_fn)(void *ptr, void *stream, void *user);
 typedef struct {
     int32_t world_size, rank, device;
     const uint8_t *nccl_unique_id; /* 128 bytes from irls_nccl_unique_id on rank 0, broadcast by the caller */
     void *cuda_stream;
+    irls_device_alloc_fn device_alloc;
+    irls_device_free_fn device_free;
+    void *alloc_user;
 } irls_comm_desc;
 
 /* Fill a fresh NCCL unique id (128 bytes) on rank 0. */

@@ -82,11 +82,27 @@ template <class T>
 static T *dalloc(irls_ctx *c, int64_t count)
 {
     void *p = nullptr;
-    const size_t bytes = (size_t)std::max<int64_t>(count, 1) * sizeof(T);
-    if (cudaMallocAsync(&p, bytes, c->stream) != cudaSuccess) return nullptr;
+    const size_t bytes = ((size_t)std::max<int64_t>(count, 1) * sizeof(T) + 255) & ~(size_t)255;
+    if (c->dev_alloc) {
+        p = c->dev_alloc(bytes, (void *)c->stream, c->alloc_user);
+        if (!p) return nullptr;
+    } else if (cudaMallocAsync(&p, bytes, c->stream) != cudaSuccess) {
+        return nullptr;
+    }
     cudaMemsetAsync(p, 0, bytes, c->stream);
     c->allocs.push_back(p);
     return (T *)p;
+}
+
+// Release one of the context's arrays (stream-ordered for the pool).
+static cudaError_t dfree(irls_ctx *c, void *p)
+{
+    c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), p), c->allocs.end());
+    if (c->dev_free) {
+        c->dev_free(p, (void *)c->stream, c->alloc_user);
+        return cudaSuccess;
+    }
+    return cudaFreeAsync(p, c->stream);
 }
 
 extern "C" void irls_options_default(irls_options *o)
@@ -886,6 +902,10 @@ static irls_status common_setup(irls_ctx *c, const irls_comm_desc *comm, const i
     c->world = comm ? comm->world_size : 1;
     c->rank = comm ? comm->rank : 0;
     c->device = comm ? comm->device : 0;
+    if (comm && (!comm->device_alloc) != (!comm->device_free)) return IRLS_ERR_INVALID_ARGUMENT;
+    c->dev_alloc = comm ? comm->device_alloc : nullptr;
+    c->dev_free = comm ? comm->device_free : nullptr;
+    c->alloc_user = comm ? comm->alloc_user : nullptr;
     if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return IRLS_ERR_INVALID_ARGUMENT;
     if (c->world > 1 && ((!comm->nccl_unique_id && !c->vg) || 8 % c->world != 0)) return IRLS_ERR_INVALID_ARGUMENT;
     // world 1 with an NCCL id: the multi-rank code path over a 1-rank
@@ -1928,7 +1948,7 @@ extern "C" void irls_mincut_destroy(irls_ctx *c)
         if (g) cudaGraphExecDestroy(g);
     for (auto &g : c->gmulti)
         if (g) cudaGraphExecDestroy(g);
-    for (void *p : c->allocs) cudaFreeAsync(p, c->stream);
+    for (void *p : std::vector<void *>(c->allocs)) dfree(c, p);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->h_done) cudaFreeHost(c->h_done);
     if (c->nccl) ncclCommDestroy(c->nccl);
@@ -1971,6 +1991,9 @@ static irls_status vgroup_create(irls_vgroup **out, int32_t world, int32_t devic
         comm.device = device;
         comm.nccl_unique_id = nullptr;
         comm.cuda_stream = g->stream;
+        comm.device_alloc = nullptr;
+        comm.device_free = nullptr;
+        comm.alloc_user = nullptr;
         irls_ctx *c = nullptr;
         irls_status s = make(&c, &comm, g);
         if (s) {
@@ -2122,8 +2145,7 @@ static irls_status tl_reserve(irls_ctx *c, int64_t entries)
     if (entries <= b.cap_entries && b.ccol) return IRLS_OK;
     for (void *p : {(void *)b.ccol, (void *)b.ccap}) {
         if (!p) continue;
-        CK(cudaFreeAsync(p, c->stream));
-        c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), p), c->allocs.end());
+        CK(dfree(c, p));
     }
     b.ccol = dalloc<int32_t>(c, entries);
     b.ccap = dalloc<double>(c, entries);
@@ -2506,8 +2528,7 @@ extern "C" irls_status irls_lambda2(irls_ctx *c, double cg_rtol, int32_t cg_max_
     if (!s && x_out && n > 0) CK(memcpy_sync(c, x_out, c->x, sizeof(double) * n, cudaMemcpyDeviceToHost));
     CK(cudaMemcpyAsync(c->x, xs, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     CK(set_opts(c->opt.cg_rtol, c->opt.cg_max_iter, c->opt.cg_norm));
-    CK(cudaFreeAsync(xs, st));
-    c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), (void *)xs), c->allocs.end());
+    CK(dfree(c, xs));
     CK(cudaStreamSynchronize(st));
     c->state = state0;
     c->last_cg_iters = iters0;

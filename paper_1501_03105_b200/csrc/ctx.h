@@ -20,6 +20,9 @@ struct irls_ctx {
     bool multi = false;  // the multi-rank (NCCL) code path: world > 1, or a 1-rank communicator (self-test)
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    irls_device_alloc_fn dev_alloc = nullptr;  // caller's allocator (irls_comm_desc), or the pool
+    irls_device_free_fn dev_free = nullptr;
+    void *alloc_user = nullptr;
     ncclComm_t nccl = nullptr;
     std::string err;
     bool poisoned = false;

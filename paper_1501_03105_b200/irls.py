@@ -31,9 +31,43 @@ class irls_options(C.Structure):
                 ("loop_mode", C.c_int32), ("fixed_point_exit", C.c_int32), ("reserved", C.c_int32)]
 
 
+DEVICE_ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+DEVICE_FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p)
+
+
 class irls_comm_desc(C.Structure):
     _fields_ = [("world_size", C.c_int32), ("rank", C.c_int32), ("device", C.c_int32),
-                ("nccl_unique_id", C.c_void_p), ("cuda_stream", C.c_void_p)]
+                ("nccl_unique_id", C.c_void_p), ("cuda_stream", C.c_void_p),
+                ("device_alloc", DEVICE_ALLOC_FN), ("device_free", DEVICE_FREE_FN), ("alloc_user", C.c_void_p)]
+
+
+class TorchDeviceMemory:
+    """device_alloc / device_free backed by torch's caching allocator: every
+    array of a context is a torch uint8 tensor held here until it is freed
+    (argument marshalling only; the library owns the layout)."""
+
+    def __init__(self, device=0):
+        import torch
+        self._torch = torch
+        self.device = device
+        self.tensors = {}
+        self.alloc = DEVICE_ALLOC_FN(self._alloc)
+        self.free = DEVICE_FREE_FN(self._free)
+
+    def _alloc(self, nbytes, stream, user):
+        try:
+            t = self._torch.empty(int(nbytes), dtype=self._torch.uint8, device=f"cuda:{self.device}")
+        except Exception:
+            return None
+        self.tensors[t.data_ptr()] = t
+        return t.data_ptr()
+
+    def _free(self, ptr, stream, user):
+        self.tensors.pop(ptr, None)
+
+    @property
+    def bytes_held(self):
+        return sum(t.numel() for t in self.tensors.values())
 
 
 class irls_step_report(C.Structure):
@@ -172,12 +206,18 @@ def options(**kw) -> irls_options:
     return o
 
 
-def comm_desc(world_size=1, rank=0, device=0, unique_id: bytes | None = None, stream=None):
+def comm_desc(world_size=1, rank=0, device=0, unique_id: bytes | None = None, stream=None,
+              memory: "TorchDeviceMemory | None" = None):
+    """irls_comm_desc; memory: a TorchDeviceMemory to make torch own the
+    context's device arrays (it must outlive the context)."""
     d = irls_comm_desc()
     d.world_size, d.rank, d.device = world_size, rank, device
     d._uid = C.create_string_buffer(unique_id, 128) if unique_id is not None else None
     d.nccl_unique_id = C.cast(d._uid, C.c_void_p) if d._uid is not None else None
     d.cuda_stream = stream
+    if memory is not None:
+        d.device_alloc, d.device_free = memory.alloc, memory.free
+        d._memory = memory
     return d
 
 
@@ -280,7 +320,9 @@ class MinCut:
                                               *[_ptr(a) for a in arrs], C.byref(opts))
         if rc:
             raise IrlsError(rc, "irls_mincut_create_stencil")
-        return cls(h, N, N + 2)
+        m = cls(h, N, N + 2)
+        m._comm = comm  # keeps a caller allocator's callbacks alive
+        return m
 
     @classmethod
     def irls_mincut_create_csr(cls, n, row_ptr, col, w, s, t, opts: irls_options | None = None,
@@ -294,7 +336,9 @@ class MinCut:
                                           _ptr(ww), s, t, C.byref(opts))
         if rc:
             raise IrlsError(rc, "irls_mincut_create_csr")
-        return cls(h, n - 2, n)
+        m = cls(h, n - 2, n)
+        m._comm = comm
+        return m
 
     @classmethod
     def from_spec(cls, spec, opts=None, comm=None):

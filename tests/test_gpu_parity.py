@@ -346,3 +346,31 @@ def test_fixed_point_exit_sequence(irls):
         rb, tb = b.irls_solve(irls.IRLS_CONTINUE, T=10)
         assert [r["cg_iters"] for r in ra] == [r["cg_iters"] for r in rb]
         assert np.array_equal(a.irls_get_potentials(), b.irls_get_potentials())
+
+
+def test_torch_owned_device_memory(irls):
+    """device_alloc / device_free (irls_comm_desc): every array of the context
+    is a torch tensor; results bitwise equal to the library pool; everything
+    is returned at destroy."""
+    import torch
+    spec = gen.blob_grid(64, 40, 12, seed=4, sigma=(3.0, 8.0))
+    a = irls.MinCut.from_spec(spec, irls.options(T=8))
+    ra, ta = a.irls_solve(irls.IRLS_FROM_SCRATCH, T=8)
+    sa = a.irls_sweep_cut()
+    mem = irls.TorchDeviceMemory(0)
+    comm = irls.comm_desc(1, 0, 0, None, torch.cuda.current_stream().cuda_stream, memory=mem)
+    b = irls.MinCut.from_spec(spec, irls.options(T=8), comm)
+    held = mem.bytes_held
+    assert held > 0
+    rb, tb = b.irls_solve(irls.IRLS_FROM_SCRATCH, T=8)
+    sb = b.irls_sweep_cut()
+    tl_b = b.irls_two_level_cut()
+    lam_b = b.irls_lambda2(cg_rtol=1e-8, cg_max_iter=10000)
+    assert mem.bytes_held > held  # sweep / two-level buffers came from torch too
+    assert ta == tb and np.array_equal(a.irls_get_potentials(), b.irls_get_potentials())
+    assert sa[2:] == sb[2:] and np.array_equal(sa[0], sb[0])
+    assert tl_b[1]["cut_value"] == a.irls_two_level_cut()[1]["cut_value"]
+    assert lam_b["lambda2"] == a.irls_lambda2(cg_rtol=1e-8, cg_max_iter=10000)["lambda2"]
+    b.close()
+    torch.cuda.synchronize()
+    assert mem.bytes_held == 0 and not mem.tensors
