@@ -1,0 +1,115 @@
+"""Command line: IRLS s-t min cut of a BASELINE config or a graph file.
+
+    python -m paper_1501_03105_b200 --config 2 --rounding both --trace trace.csv
+    python -m paper_1501_03105_b200 --graph g.npz --lambda2 --exact
+
+A graph file is an .npz with either a grid (kind="stencil": nx, ny, nz, cx,
+cy, cz, cs, ct) or a CSR graph over all nodes incl. s and t (kind="csr": n,
+row_ptr, col, w, s, t), as synthetic/generators.py builds them.  The trace
+is the per-step report (SPEC's IrlsTrace: step, CG iterations, converged,
+residuals, S_eps, flow value, x range, ms) as CSV.  Every step runs in the
+CUDA library; this module only parses arguments and prints.
+"""
+from __future__ import annotations
+
+import argparse
+import csv
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+from . import build, irls as I
+
+
+def load_graph(args):
+    if args.graph:
+        z = np.load(args.graph, allow_pickle=False)
+        spec = {k: z[k] for k in z.files}
+        spec["kind"] = str(spec["kind"])
+        for k in ("nx", "ny", "nz", "n", "s", "t"):
+            if k in spec:
+                spec[k] = int(spec[k])
+        return spec, args.graph
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if root not in sys.path:
+        sys.path.insert(0, root)
+    from synthetic import generators as gen
+    make = {1: gen.config1, 2: gen.config2, 3: gen.config3, 4: gen.config4, 5: gen.config2}[args.config]
+    return make(), f"BASELINE config {args.config}"
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(prog="python -m paper_1501_03105_b200", description=__doc__.split("\n\n")[0])
+    src = ap.add_mutually_exclusive_group(required=True)
+    src.add_argument("--config", type=int, choices=[1, 2, 3, 4, 5])
+    src.add_argument("--graph", help=".npz graph file")
+    ap.add_argument("--T", type=int, default=50)
+    ap.add_argument("--eps", type=float, default=1e-6)
+    ap.add_argument("--rtol", type=float, default=None, help="CG relative tolerance (default 1e-3; config 1: 1e-10)")
+    ap.add_argument("--cap", type=int, default=None, help="CG iteration cap (default 50; config 1: 100000)")
+    ap.add_argument("--norm", choices=["preconditioned", "unpreconditioned"], default=None)
+    ap.add_argument("--cold", action="store_true", help="cold-start every CG solve")
+    ap.add_argument("--fixed-point-exit", action="store_true")
+    ap.add_argument("--rounding", choices=["sweep", "two_level", "both"], default="sweep")
+    ap.add_argument("--lambda2", action="store_true", help="Cheeger-type lambda_2 (P:L207-226)")
+    ap.add_argument("--exact", action="store_true", help="exact min cut mu* and delta (Eq. 13)")
+    ap.add_argument("--trace", help="write the per-step report as CSV")
+    ap.add_argument("--side", help="write the source-side indicator (uint8, one per node) as .npy")
+    args = ap.parse_args(argv)
+
+    build.build()
+    spec, what = load_graph(args)
+    c1 = args.config == 1
+    rtol = args.rtol if args.rtol is not None else (1e-10 if c1 else 1e-3)
+    cap = args.cap if args.cap is not None else (100000 if c1 else 50)
+    norm = args.norm or ("unpreconditioned" if c1 else "preconditioned")
+    opts = I.options(T=args.T, eps=args.eps, cg_rtol=rtol, cg_max_iter=cap,
+                     cg_norm=I.IRLS_NORM_UNPRECONDITIONED if norm == "unpreconditioned" else I.IRLS_NORM_PRECONDITIONED,
+                     warm_start=0 if args.cold else 1, fixed_point_exit=1 if args.fixed_point_exit else 0,
+                     record_trace=1 if args.trace else 0)
+    t0 = time.perf_counter()
+    m = I.MinCut.from_spec(spec, opts)
+    st = m.irls_get_stats()
+    out = {"graph": what, "nodes": st["n_nonterminal"], "n_links": st["n_links"],
+           "create_s": time.perf_counter() - t0}
+    t0 = time.perf_counter()
+    reps, iters = m.irls_solve(I.IRLS_FROM_SCRATCH, T=args.T)
+    out.update({"solve_s": time.perf_counter() - t0, "cg_iters": iters})
+    side = None
+    if args.rounding in ("sweep", "both"):
+        t0 = time.perf_counter()
+        side, _, k, cut = m.irls_sweep_cut()
+        out["sweep"] = {"cut": cut, "k": k, "s": time.perf_counter() - t0}
+    if args.rounding in ("two_level", "both"):
+        side2, rep = m.irls_two_level_cut()
+        out["two_level"] = {"cut": rep["cut_value"], "coarse_nodes": rep["nc"], "ms_gpu": rep["ms_gpu"],
+                            "ms_maxflow": rep["ms_maxflow"]}
+        if args.rounding == "two_level" or rep["cut_value"] < out["sweep"]["cut"]:
+            side = side2
+    if args.lambda2:
+        out["lambda2"] = m.irls_lambda2()["lambda2"]
+    if args.exact:
+        _, ex = m.irls_exact_min_cut(side=False)
+        mu = ex["cut_value"]
+        out["mu_star"] = mu
+        for key in ("sweep", "two_level"):
+            if key in out and mu > 0:
+                out[key]["delta"] = (out[key]["cut"] - mu) / mu
+    if args.trace:
+        with open(args.trace, "w", newline="") as f:
+            w = csv.writer(f)
+            cols = ["cg_iters", "converged", "rel_res", "true_rel_res", "S_eps", "flow_value", "x_min", "x_max", "ms"]
+            w.writerow(["step"] + cols)
+            for i, r in enumerate(reps):
+                w.writerow([i] + [r[c] for c in cols])
+    if args.side and side is not None:
+        np.save(args.side, side)
+    m.close()
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()

@@ -14,9 +14,18 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "ctx.h"
 
 using namespace irls;
+
+// NVTX ranges around every entry point and phase (header-only NVTX 3: a
+// profiler that injects itself sees them; otherwise they cost a branch).
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 // ---------------------------------------------------------------------------
 // error plumbing
@@ -1016,6 +1025,7 @@ static irls_status create_stencil_impl(irls_ctx **out, const irls_comm_desc *com
                                        const double *cx, const double *cy, const double *cz, const double *cs,
                                        const double *ct, const irls_options *opt, irls_vgroup *vg)
 {
+    NvtxRange nvtx_("irls_mincut_create_stencil");
     if (!out) return IRLS_ERR_INVALID_ARGUMENT;
     *out = nullptr;
     if (check_opts(opt) || nx < 1 || ny < 1 || nz < 1 || !cx || !cy || !cz || !cs || !ct)
@@ -1179,6 +1189,7 @@ static irls_status create_csr_impl(irls_ctx **out, const irls_comm_desc *comm, i
                                    const int32_t *col, const double *w, int64_t s_, int64_t t_, const irls_options *opt,
                                    irls_vgroup *vg)
 {
+    NvtxRange nvtx_("irls_mincut_create_csr");
     if (!out) return IRLS_ERR_INVALID_ARGUMENT;
     *out = nullptr;
     if (check_opts(opt) || n < 2 || !row_ptr || !col || !w || s_ < 0 || t_ < 0 || s_ >= n || t_ >= n)
@@ -1567,6 +1578,7 @@ static irls_status create_csr_impl(irls_ctx **out, const irls_comm_desc *comm, i
 // ---------------------------------------------------------------------------
 extern "C" irls_status irls_init(irls_ctx *c, irls_step_report *rep)
 {
+    NvtxRange nvtx_("irls_init");
     GUARD(c);
     if (c->n_glob == 0) { c->state = 1; return IRLS_OK; }
     irls_step_report tmp;
@@ -1576,6 +1588,7 @@ extern "C" irls_status irls_init(irls_ctx *c, irls_step_report *rep)
 
 extern "C" irls_status irls_step(irls_ctx *c, irls_step_report *rep)
 {
+    NvtxRange nvtx_("irls_step");
     GUARD(c);
     if (c->state == 0) return fail(c, IRLS_ERR_STATE, "irls_step before irls_init / irls_set_potentials");
     if (c->n_glob == 0) return IRLS_OK;
@@ -1587,6 +1600,7 @@ extern "C" irls_status irls_step(irls_ctx *c, irls_step_report *rep)
 
 extern "C" irls_status irls_solve(irls_ctx *c, int32_t mode, irls_step_report *per_step, int64_t *total)
 {
+    NvtxRange nvtx_("irls_solve");
     GUARD(c);
     if (mode != IRLS_FROM_SCRATCH && mode != IRLS_CONTINUE) return IRLS_ERR_INVALID_ARGUMENT;
     if (mode == IRLS_CONTINUE && c->state == 0) return fail(c, IRLS_ERR_STATE, "IRLS_CONTINUE without potentials");
@@ -1736,6 +1750,7 @@ static irls_status sweep_rank0(irls_ctx *c, const double *xfull, uint8_t *side, 
 
 extern "C" irls_status irls_sweep_cut(irls_ctx *c, uint8_t *side, int32_t *order, int64_t *k, double *cut_value)
 {
+    NvtxRange nvtx_("irls_sweep_cut");
     GUARD(c);
     if (c->state == 0) return fail(c, IRLS_ERR_STATE, "sweep before solve");
     double *xfull = nullptr;
@@ -2280,6 +2295,7 @@ static irls_status two_level_rank0(irls_ctx *c, const double *xfull, uint8_t *si
     int64_t stats[3] = {0, 0, 0};
     __int128 flow = 0;
     if (nc > 0) {
+        NvtxRange nvtx_mf("two_level: host max-flow");
         flow = maxflow_bk((int32_t)nc, c->h_cp.data(), c->h_ccol.data(), qcap.data(), c->h_cqs.data(),
                           c->h_cqt.data(), src.data(), stats);
         if (stats[0] != 1) return fail(c, IRLS_ERR_CUDA, "coarse max-flow not certified (flow != cut)");
@@ -2364,6 +2380,7 @@ struct TwoLevelMsg {
 
 extern "C" irls_status irls_two_level_cut(irls_ctx *c, uint8_t *side, irls_two_level_report *rep)
 {
+    NvtxRange nvtx_("irls_two_level_cut");
     GUARD(c);
     if (c->state == 0) return fail(c, IRLS_ERR_STATE, "two-level rounding before solve");
     double *xfull = nullptr;
@@ -2392,6 +2409,7 @@ extern "C" irls_status irls_two_level_cut(irls_ctx *c, uint8_t *side, irls_two_l
 
 extern "C" irls_status irls_exact_min_cut(irls_ctx *c, uint8_t *side, irls_two_level_report *rep)
 {
+    NvtxRange nvtx_("irls_exact_min_cut");
     GUARD(c);
     if (c->world > 1) return fail(c, IRLS_ERR_INVALID_ARGUMENT, "irls_exact_min_cut is single-process");
     irls_two_level_report r;
@@ -2473,6 +2491,7 @@ extern "C" irls_status irls_coarse_maxflow(int32_t nc, const int32_t *ptr, const
 extern "C" irls_status irls_lambda2(irls_ctx *c, double cg_rtol, int32_t cg_max_iter, int32_t cg_norm, double *x_out,
                                     irls_lambda2_report *rep)
 {
+    NvtxRange nvtx_("irls_lambda2");
     GUARD(c);
     if (c->world > 1) return fail(c, IRLS_ERR_INVALID_ARGUMENT, "irls_lambda2 is single-process");
     if (!(cg_rtol >= 0.0) || cg_max_iter < 0 || (cg_norm != 0 && cg_norm != 1))
