@@ -12,8 +12,12 @@
 // s_c in the residual graph (the minimal minimum cut, unique, A28) and the
 // cut value of that set is compared with the flow value (strong duality is
 // the certificate of optimality).
+#include <algorithm>
+#include <atomic>
+#include <cstdlib>
 #include <climits>
 #include <deque>
+#include <thread>
 #include <vector>
 
 #include "kernels.h"
@@ -225,8 +229,8 @@ struct BK {
 
 }  // namespace
 
-i128 maxflow_bk(int32_t nc, const int32_t *ptr, const int32_t *col, const i128 *cap, const i128 *qs, const i128 *qt,
-                uint8_t *src, int64_t *stats)
+static i128 maxflow_bk_one(int32_t nc, const int32_t *ptr, const int32_t *col, const i128 *cap, const i128 *qs,
+                           const i128 *qt, uint8_t *src, int64_t *stats)
 {
     BK g;
     g.n = nc;
@@ -325,6 +329,115 @@ i128 maxflow_bk(int32_t nc, const int32_t *ptr, const int32_t *col, const i128 *
         stats[2] = g.n_orphan;
     }
     return g.flow;
+}
+
+}  // namespace irls
+
+namespace irls {
+
+// The connected components of G_c (coarse n-links only) are independent
+// max-flow problems joined by s_c and t_c: their flows add and their minimal
+// source sides unite.  Components are solved by host threads, largest first;
+// the result does not depend on the thread count.
+i128 maxflow_bk(int32_t nc, const int32_t *ptr, const int32_t *col, const i128 *cap, const i128 *qs, const i128 *qt,
+                uint8_t *src, int64_t *stats)
+{
+    if (nc <= 0) {
+        if (stats) stats[0] = 1, stats[1] = 0, stats[2] = 0;
+        return 0;
+    }
+    // components by BFS
+    std::vector<int32_t> comp(nc, -1), order;
+    order.reserve(nc);
+    std::vector<int64_t> cstart;
+    int32_t ncomp = 0;
+    for (int32_t r = 0; r < nc; r++) {
+        if (comp[r] >= 0) continue;
+        cstart.push_back((int64_t)order.size());
+        comp[r] = ncomp;
+        order.push_back(r);
+        for (size_t h = cstart.back(); h < order.size(); h++) {
+            const int32_t u = order[h];
+            for (int32_t a = ptr[u]; a < ptr[u + 1]; a++)
+                if (comp[col[a]] < 0) {
+                    comp[col[a]] = ncomp;
+                    order.push_back(col[a]);
+                }
+        }
+        ncomp++;
+    }
+    cstart.push_back(nc);
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    int64_t largest = 0;
+    for (int32_t k = 0; k < ncomp; k++) largest = std::max<int64_t>(largest, cstart[k + 1] - cstart[k]);
+    // one dominant component (or a small graph): no parallelism to gain
+    static const int64_t par_min = [] {
+        const char *e = getenv("IRLS_MAXFLOW_PAR_MIN");  // test hook: threaded path on small graphs
+        return e ? atoll(e) : (int64_t)100000;
+    }();
+    if (ncomp == 1 || hw == 1 || nc < par_min || largest * 10 > (int64_t)nc * 9)
+        return maxflow_bk_one(nc, ptr, col, cap, qs, qt, src, stats);
+    // local ids: ascending original id inside each component (rows stay sorted)
+    for (int32_t k = 0; k < ncomp; k++) std::sort(order.begin() + cstart[k], order.begin() + cstart[k + 1]);
+    std::vector<int32_t> lid(nc);
+    for (int32_t k = 0; k < ncomp; k++)
+        for (int64_t i = cstart[k]; i < cstart[k + 1]; i++) lid[order[i]] = (int32_t)(i - cstart[k]);
+    std::vector<int32_t> byk(ncomp);
+    for (int32_t k = 0; k < ncomp; k++) byk[k] = k;
+    std::sort(byk.begin(), byk.end(), [&](int32_t a, int32_t b) {
+        return cstart[a + 1] - cstart[a] > cstart[b + 1] - cstart[b];
+    });
+    std::vector<i128> flows(ncomp, 0);
+    std::vector<int64_t> st(3 * (size_t)ncomp, 0);
+    std::atomic<int32_t> next{0};
+    auto worker = [&]() {
+        std::vector<int32_t> lp, lc;
+        std::vector<i128> lcap, lqs, lqt;
+        std::vector<uint8_t> lsrc;
+        for (;;) {
+            const int32_t j = next.fetch_add(1);
+            if (j >= ncomp) return;
+            const int32_t k = byk[j];
+            const int64_t b0 = cstart[k], m = cstart[k + 1] - b0;
+            lp.assign(m + 1, 0);
+            lc.clear();
+            lcap.clear();
+            lqs.resize(m);
+            lqt.resize(m);
+            for (int64_t i = 0; i < m; i++) {
+                const int32_t u = order[b0 + i];
+                for (int32_t a = ptr[u]; a < ptr[u + 1]; a++) {
+                    lc.push_back(lid[col[a]]);
+                    lcap.push_back(cap[a]);
+                }
+                lp[i + 1] = (int32_t)lc.size();
+                lqs[i] = qs[u];
+                lqt[i] = qt[u];
+            }
+            lsrc.assign(m, 0);
+            flows[k] = maxflow_bk_one((int32_t)m, lp.data(), lc.data(), lcap.data(), lqs.data(), lqt.data(),
+                                      lsrc.data(), &st[3 * (size_t)k]);
+            for (int64_t i = 0; i < m; i++) src[order[b0 + i]] = lsrc[i];
+        }
+    };
+    const unsigned nt = std::min<unsigned>(hw, (unsigned)ncomp);
+    std::vector<std::thread> th;
+    for (unsigned i = 0; i < nt; i++) th.emplace_back(worker);
+    for (auto &t : th) t.join();
+    i128 flow = 0;
+    int64_t cert = 1, aug = 0, orph = 0;
+    for (int32_t k = 0; k < ncomp; k++) {
+        flow += flows[k];
+        cert = std::min<int64_t>(cert, st[3 * (size_t)k]);
+        aug += st[3 * (size_t)k + 1];
+        orph += st[3 * (size_t)k + 2];
+    }
+    if (stats) {
+        stats[0] = cert;
+        stats[1] = aug;
+        stats[2] = orph;
+    }
+    return flow;
 }
 
 }  // namespace irls

@@ -64,3 +64,35 @@ def test_bk_ties_and_zero_graph(L):
 def test_bk_rejects_asymmetric(L):
     with pytest.raises(L.IrlsError):
         L.irls_coarse_maxflow(2, np.array([0, 1, 1], np.int32), np.array([1], np.int32), [5], [1, 0], [0, 1])
+
+
+def test_bk_components_in_parallel(L):
+    """Many components solved on host threads (the path large coarse graphs
+    take; enabled here for a small graph through IRLS_MAXFLOW_PAR_MIN, read
+    once per process — set by conftest for the whole session): the same flow
+    and minimal source side as the oracle's Edmonds-Karp."""
+    import numpy as np
+    parts, off = [], 0
+    for k in range(8):
+        sp = gen.blob_grid(40, 25, 2, seed=100 + k, n_blobs=3, sigma=(2.0, 6.0))
+        parts.append((sp, off))
+        off += 40 * 25 * 2
+    # one block-diagonal coarse graph: every node in Sc, components = the grids
+    cos = []
+    for sp, o in parts:
+        co = coarse_of(sp, np.full(40 * 25 * 2, 0.5), 0.1, 0.9)
+        cos.append((co, o))
+    nc = off
+    ptr = [0]
+    col, cap, qs, qt = [], [], [], []
+    for co, o in cos:
+        for u in range(co.nc):
+            for e in range(co.ptr[u], co.ptr[u + 1]):
+                col.append(int(co.col[e]) + o)
+                cap.append(co.cap[e])
+            ptr.append(len(col))
+        qs += co.qs
+        qt += co.qt
+    f_l, src_l, cert = L.irls_coarse_maxflow(nc, np.array(ptr, np.int32), np.array(col, np.int32), cap, qs, qt)
+    f_o, src_o = oracle.maxflow_coarse(nc, np.array(ptr), np.array(col), cap, qs, qt, 0)
+    assert cert == 1 and f_l == f_o and src_l.tolist() == src_o.tolist()

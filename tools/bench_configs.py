@@ -66,8 +66,23 @@ def run_config(cid, reps=3):
             cold_iters += tot
             cold_ms += ms
         _, _, k, cut = m.irls_sweep_cut(side=False)
+        # the same warm sequence with the exact fixed-point exit
+        mf = I.MinCut.from_spec(spec, I.options(T=50, fixed_point_exit=1), comm)
+        mf.irls_solve(I.IRLS_FROM_SCRATCH, T=50, reports=False)
+        cs, ct = spec["cs"].copy(), spec["ct"].copy()
+        fp_iters, fp_ms = 0, 0.0
+        for fs, ft in gen.config5_factors(cs.shape[0], n_problems=10, seed=4):
+            cs, ct = cs * fs, ct * ft
+            mf.irls_set_terminal_weights(cs, ct)
+            (r, tot), ms = timed(lambda: mf.irls_solve(I.IRLS_CONTINUE, T=50, reports=False))
+            fp_iters += tot
+            fp_ms += ms
+        _, _, kf, cutf = mf.irls_sweep_cut(side=False)
+        mf.close()
         res.update({"warm_total_cg_iters": warm_iters, "warm_ms": warm_ms, "cold_total_cg_iters": cold_iters,
-                    "cold_ms": cold_ms, "final_k": k, "final_cut": cut})
+                    "cold_ms": cold_ms, "final_k": k, "final_cut": cut,
+                    "warm_fixed_point_exit_ms": fp_ms, "warm_fixed_point_exit_iters": fp_iters,
+                    "fixed_point_exit_same_cut": bool(kf == k and cutf == cut)})
         mc.close()
         m.close()
         return res
