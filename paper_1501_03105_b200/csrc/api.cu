@@ -617,7 +617,7 @@ static irls_status capture_solve_body(irls_ctx *c, Ranks &R, int mode, cudaStrea
     if (s) return s;
     if (mode == ASM_REWEIGHT_COLD) CK(cudaMemsetAsync(c->x, 0, sizeof(double) * c->n_own, st));
     CK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &graph, &deps, &nd));
-    cudaGraphNodeParams p = {cudaGraphNodeTypeConditional};
+    cudaGraphNodeParams p{};
     p.type = cudaGraphNodeTypeConditional;
     p.conditional.handle = h;
     p.conditional.type = cudaGraphCondTypeWhile;
@@ -661,7 +661,7 @@ static irls_status build_graph(irls_ctx *c, int mode)
             c->launches++;
             e = cudaStreamGetCaptureInfo(st, &cs, nullptr, &graph, &deps, &nd);
         }
-        cudaGraphNodeParams p = {cudaGraphNodeTypeConditional};
+        cudaGraphNodeParams p{};
         cudaGraphNode_t ifnode;
         if (e == cudaSuccess) {
             p.type = cudaGraphNodeTypeConditional;
@@ -721,7 +721,7 @@ static irls_status build_graph_multi(irls_ctx *c, int mode)
         launch_outer_init(c->ctrl, hout, count, st);
         e = cudaStreamGetCaptureInfo(st, &cs, nullptr, &graph, &deps, &nd);
     }
-    cudaGraphNodeParams p = {cudaGraphNodeTypeConditional};
+    cudaGraphNodeParams p{};
     cudaGraphNode_t wnode;
     if (e == cudaSuccess) {
         p.type = cudaGraphNodeTypeConditional;
@@ -2262,7 +2262,7 @@ static irls_status two_level_rank0(irls_ctx *c, const double *xfull, uint8_t *si
     __int128 qst = qfix_host(c->c_st, c->F);
     for (int64_t i = 0; i < nt && n > 0; i++) qst += tiles[i];
     if (nc > 0) {
-        if (c->kind == 0) tl_fill_stencil(stencil_args(c, true), n, xfull, r->gamma0, r->gamma1, c->F, b, st);
+        if (c->kind == 0) tl_fill_stencil(stencil_args(c, true), n, c->F, b, st);
         else tl_fill_sell(sell_args_full(c), c->F, b, st);
         launches++;
     }

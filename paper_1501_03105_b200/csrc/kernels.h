@@ -197,8 +197,7 @@ void tl_classify_stencil(const StencilArgs &s, int64_t N, const double *x, doubl
                          TLBuffers &b, cudaStream_t st);
 void tl_classify_sell(const SellArgs &s, const double *x, double g0, double g1, int32_t F, TLBuffers &b,
                       cudaStream_t st);
-void tl_fill_stencil(const StencilArgs &s, int64_t N, const double *x, double g0, double g1, int32_t F,
-                     TLBuffers &b, cudaStream_t st);
+void tl_fill_stencil(const StencilArgs &s, int64_t N, int32_t F, TLBuffers &b, cudaStream_t st);
 void tl_fill_sell(const SellArgs &s, int32_t F, TLBuffers &b, cudaStream_t st);
 void tl_lift(TLBuffers &b, cudaStream_t st);
 

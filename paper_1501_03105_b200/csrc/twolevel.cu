@@ -191,10 +191,9 @@ __global__ void __launch_bounds__(256) k_tl_classify_sell(SellArgs s, const doub
 // ---------------------------------------------------------------------------
 // fill: coarse CSR rows of the Sc nodes
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_tl_fill_stencil(StencilArgs s, int64_t N, const double *x, double g0,
-                                                         double g1, int32_t F, const int8_t *cls, const int32_t *cid,
-                                                         const int32_t *eoff, int32_t *cp, int32_t *ccol,
-                                                         double *ccap, i128 *cqs, i128 *cqt)
+__global__ void __launch_bounds__(256) k_tl_fill_stencil(StencilArgs s, int64_t N, int32_t F, const int8_t *cls,
+                                                         const int32_t *cid, const int32_t *eoff, int32_t *cp,
+                                                         int32_t *ccol, double *ccap, i128 *cqs, i128 *cqt)
 {
     const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= N || cls[v] != 2) return;
@@ -302,11 +301,10 @@ void tl_classify_sell(const SellArgs &s, const double *x, double g0, double g1, 
                                                                 b.tile_n1);
 }
 
-void tl_fill_stencil(const StencilArgs &s, int64_t N, const double *x, double g0, double g1, int32_t F,
-                     TLBuffers &b, cudaStream_t st)
+void tl_fill_stencil(const StencilArgs &s, int64_t N, int32_t F, TLBuffers &b, cudaStream_t st)
 {
-    k_tl_fill_stencil<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(s, N, x, g0, g1, F, b.cls, b.cid, b.eoff, b.cp,
-                                                                    b.ccol, b.ccap, b.cqs, b.cqt);
+    k_tl_fill_stencil<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(s, N, F, b.cls, b.cid, b.eoff, b.cp, b.ccol,
+                                                                    b.ccap, b.cqs, b.cqt);
 }
 
 void tl_fill_sell(const SellArgs &s, int32_t F, TLBuffers &b, cudaStream_t st)
