@@ -64,7 +64,12 @@ typedef enum {
 } irls_status;
 
 typedef enum { IRLS_NORM_PRECONDITIONED = 0, IRLS_NORM_UNPRECONDITIONED = 1 } irls_cg_norm;
-typedef enum { IRLS_LOOP_GRAPH = 0, IRLS_LOOP_HOST = 1 } irls_loop_mode;
+/* GRAPH: CUDA graphs with device-side WHILE loops on one rank (multi-rank
+ * contexts fall back to the host loop: one 4-byte readback per CG
+ * iteration); GRAPH_NCCL: graphs also on a communicator, the NCCL
+ * collectives captured inside the loop bodies (no host round trip per
+ * iteration; exercised on one GPU through a 1-rank communicator). */
+typedef enum { IRLS_LOOP_GRAPH = 0, IRLS_LOOP_HOST = 1, IRLS_LOOP_GRAPH_NCCL = 2 } irls_loop_mode;
 
 /* Solver options (A9-A13). */
 typedef struct {

@@ -199,7 +199,7 @@ static irls_status check_opts(const irls_options *o)
 {
     if (!o) return IRLS_ERR_INVALID_ARGUMENT;
     if (!(o->eps > 0.0) || isinf(o->eps) || o->T < 0 || !(o->cg_rtol >= 0.0) || o->cg_max_iter < 0 ||
-        (o->cg_norm != 0 && o->cg_norm != 1) || (o->loop_mode != 0 && o->loop_mode != 1) ||
+        (o->cg_norm != 0 && o->cg_norm != 1) || (o->loop_mode < 0 || o->loop_mode > 2) ||
         (o->fixed_point_exit != 0 && o->fixed_point_exit != 1))
         return IRLS_ERR_INVALID_ARGUMENT;
     return IRLS_OK;
@@ -598,6 +598,19 @@ static irls_status enq_tail(Ranks &R, int mode, cudaStream_t st, bool finish = t
 // -> report [-> diag].  With fixed_point_exit, a warm reweight solve is
 // wrapped as  gate -> IF (not frozen) { K1 -> WHILE {...} -> finish } ->
 // report: a frozen solve costs one graph launch and two one-thread kernels.
+// One-block CG loop (small.cu) for a single rank whose graph is one C3 chunk.
+static bool small_path(const irls_ctx *c) { return !c->multi && c->n_own > 0 && c->n_own <= kChunk; }
+
+static void enq_small(irls_ctx *c, cudaStream_t st)
+{
+    SellArgs sl{};
+    StencilArgs sa{};
+    if (c->kind == 0) sa = stencil_args(c, false);
+    else sl = sell_args(c);
+    launch_small_cg(c->kind, sa, sl, vec_args(c), c->ctrl, c->slots_local, st);
+    c->launches++;
+}
+
 static irls_status capture_solve_body(irls_ctx *c, Ranks &R, int mode, cudaStream_t st)
 {
     cudaStreamCaptureStatus cs;
@@ -605,17 +618,23 @@ static irls_status capture_solve_body(irls_ctx *c, Ranks &R, int mode, cudaStrea
     const cudaGraphNode_t *deps = nullptr;
     size_t nd = 0;
     CK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &graph, &deps, &nd));
-    cudaGraphConditionalHandle h;
+    const bool small = small_path(c);
+    cudaGraphConditionalHandle h{};
     // default 0 at every launch: the assembly's last block turns the loop on
-    CK(cudaGraphConditionalHandleCreate(&h, graph, 0, cudaGraphCondAssignDefault));
+    if (!small) CK(cudaGraphConditionalHandleCreate(&h, graph, 0, cudaGraphCondAssignDefault));
     CondArgs cd;
     cd.handle = h;
-    cd.use = 1;
-    cd.finalize = 1;
+    cd.use = small ? 0 : 1;
+    cd.finalize = c->multi ? 0 : 1;  // multi-rank: the finalize kernels after the slot allreduce
     if (mode == ASM_INIT || mode == ASM_LAMBDA2) CK(cudaMemsetAsync(c->x, 0, sizeof(double) * c->n_own, st));
     irls_status s = enq_assemble(R, mode, cd, st);
     if (s) return s;
     if (mode == ASM_REWEIGHT_COLD) CK(cudaMemsetAsync(c->x, 0, sizeof(double) * c->n_own, st));
+    if (small) {  // no WHILE node: the block loops itself
+        enq_small(c, st);
+        c->gl_body = 0;
+        return last_launch(c, "small cg");
+    }
     CK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &graph, &deps, &nd));
     cudaGraphNodeParams p{};
     p.type = cudaGraphNodeTypeConditional;
@@ -760,11 +779,20 @@ static irls_status build_graph_multi(irls_ctx *c, int mode)
     return IRLS_OK;
 }
 
+// CUDA-graph loops: one rank without collectives, or (IRLS_LOOP_GRAPH_NCCL)
+// a rank of a communicator, whose NCCL calls are captured into the graphs.
+static bool graph_mode(const irls_ctx *c)
+{
+    if (c->vg) return false;
+    if (!c->multi) return c->opt.loop_mode == IRLS_LOOP_GRAPH || c->opt.loop_mode == IRLS_LOOP_GRAPH_NCCL;
+    return c->opt.loop_mode == IRLS_LOOP_GRAPH_NCCL;
+}
+
 static irls_status enqueue_solve(Ranks &R, int mode)
 {
     irls_ctx *c = R[0];
     cudaStream_t st = c->stream;
-    if (c->opt.loop_mode == IRLS_LOOP_GRAPH && !c->multi) {
+    if (graph_mode(c) && R.size() == 1) {
         if (!c->gexec[mode]) {
             irls_status s = build_graph(c, mode);
             if (s) return s;
@@ -786,6 +814,7 @@ static irls_status enqueue_solve(Ranks &R, int mode)
     if (s) return s;
     if (mode == ASM_REWEIGHT_COLD)
         for (irls_ctx *d : R) CK(cudaMemsetAsync(d->x, 0, sizeof(double) * d->n_own, st));
+    if (R.size() == 1 && small_path(c)) enq_small(c, st);
     for (;;) {
         CK(cudaMemcpyAsync(c->h_done, &c->ctrl->done, sizeof(int), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
@@ -831,7 +860,7 @@ static irls_status run_solves(Ranks &R, int mode0, int mode_rest, int count, irl
     // graph mode, one rank: the T reweight steps run as ONE graph (outer WHILE);
     // per-step times then come from device timestamps in the reports
     const int nrest = mode0 == mode_rest ? count : count - 1;
-    const bool multi_graph = c->opt.loop_mode == IRLS_LOOP_GRAPH && !c->multi && R.size() == 1 && nrest == c->opt.T &&
+    const bool multi_graph = graph_mode(c) && R.size() == 1 && nrest == c->opt.T &&
                              nrest >= 2 && (mode_rest == ASM_REWEIGHT_WARM || mode_rest == ASM_REWEIGHT_COLD);
     if (multi_graph) {
         launch_mark(c->ctrl, st);
@@ -931,6 +960,7 @@ static irls_status common_setup(irls_ctx *c, const irls_comm_desc *comm, const i
     CK(cudaStreamCreateWithFlags(&c->side_stream2, cudaStreamNonBlocking));
     CK(cudaMallocHost(&c->h_done, sizeof(int)));
     setup_pool(c->device);
+    small_cg_prepare();
     return IRLS_OK;
 }
 
@@ -2269,11 +2299,9 @@ static irls_status two_level_rank0(irls_ctx *c, const double *xfull, uint8_t *si
     irls_status ls = last_launch(c, "two-level coarsening");
     if (ls) return ls;
     CK(cudaEventRecord(ev[1], st));
-    c->h_cp.resize(nc + 1);
-    c->h_ccol.resize(E);
-    c->h_ccap.resize(E);
-    c->h_cqs.resize(nc);
-    c->h_cqt.resize(nc);
+    if (!c->h_cp.resize(nc + 1) || !c->h_ccol.resize(E) || !c->h_ccap.resize(E) || !c->h_cqs.resize(nc) ||
+        !c->h_cqt.resize(nc))
+        return fail(c, IRLS_ERR_OOM, "pinned coarse-graph buffers");
     if (nc > 0) {
         CK(cudaMemcpyAsync(c->h_cp.data(), b.cp, sizeof(int32_t) * nc, cudaMemcpyDeviceToHost, st));
         if (E > 0) {
@@ -2289,8 +2317,10 @@ static irls_status two_level_rank0(irls_ctx *c, const double *xfull, uint8_t *si
     c->h_qst = qst;
     // 4. exact max-flow on G_c (host)
     auto t0 = std::chrono::steady_clock::now();
-    std::vector<__int128> qcap(E);
-    for (int64_t e = 0; e < E; e++) qcap[e] = qfix_host(c->h_ccap[e], c->F);
+    HostBuf<__int128> qcap(E);
+    parallel_for(E, [&](int, int64_t a, int64_t b2) {
+        for (int64_t e = a; e < b2; e++) qcap[e] = qfix_host(c->h_ccap[e], c->F);
+    });
     std::vector<uint8_t> src((size_t)std::max<int64_t>(nc, 1), 0);
     int64_t stats[3] = {0, 0, 0};
     __int128 flow = 0;

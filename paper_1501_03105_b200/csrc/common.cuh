@@ -228,9 +228,10 @@ __device__ __forceinline__ void finalize_start(DevCtrl *c, const double *slots)
 }
 
 // After q = A p (phase PQ): quantity [pq].
-__device__ __forceinline__ void finalize_pq(DevCtrl *c, const double *slots)
+// (the _t forms take the totals; C = DevCtrl or a register copy of it)
+template <class C>
+__device__ __forceinline__ void finalize_pq_t(C *c, double pi)
 {
-    const double pi = slot_total(slots, 0);
     if (!(pi > 0.0) || isinf(pi)) {
         c->status = ST_BREAKDOWN;
         c->done = 1;
@@ -239,10 +240,12 @@ __device__ __forceinline__ void finalize_pq(DevCtrl *c, const double *slots)
     c->alpha = c->rho / pi;
 }
 
+__device__ __forceinline__ void finalize_pq(DevCtrl *c, const double *slots) { finalize_pq_t(c, slot_total(slots, 0)); }
+
 // After r -= alpha q, z = M^-1 r (phase RZ): quantities [rz, zz, rr].
-__device__ __forceinline__ void finalize_rz(DevCtrl *c, const double *slots)
+template <class C>
+__device__ __forceinline__ void finalize_rz_t(C *c, double rz, double zz, double rr)
 {
-    const double rz = slot_total(slots, 0), zz = slot_total(slots, 1), rr = slot_total(slots, 2);
     const double res = sqrt(c->norm == 0 ? zz : rr);
     const double beta = rz / c->rho;
     c->res = res;
@@ -255,6 +258,11 @@ __device__ __forceinline__ void finalize_rz(DevCtrl *c, const double *slots)
         return;
     }
     c->done = (res <= c->rtol * c->ref) || (c->k == c->max_iter);
+}
+
+__device__ __forceinline__ void finalize_rz(DevCtrl *c, const double *slots)
+{
+    finalize_rz_t(c, slot_total(slots, 0), slot_total(slots, 1), slot_total(slots, 2));
 }
 
 // Order-preserving 64-bit key of a double (ascending).

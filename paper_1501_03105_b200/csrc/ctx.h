@@ -12,6 +12,38 @@
 
 struct irls_vgroup;
 
+// Page-locked host array (fast D2H of the coarse graph); grows, never shrinks.
+template <class T>
+struct PinnedBuf {
+    T *p = nullptr;
+    size_t n = 0, cap = 0;
+    PinnedBuf() = default;
+    PinnedBuf(const PinnedBuf &) = delete;
+    PinnedBuf &operator=(const PinnedBuf &) = delete;
+    ~PinnedBuf()
+    {
+        if (p) cudaFreeHost(p);
+    }
+    bool resize(size_t m)
+    {
+        if (m > cap) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            cap = 0;
+            const size_t c2 = m + m / 4 + 16;
+            if (cudaMallocHost((void **)&p, c2 * sizeof(T)) != cudaSuccess) return false;
+            cap = c2;
+        }
+        n = m;
+        return true;
+    }
+    size_t size() const { return n; }
+    T *data() { return p; }
+    const T *data() const { return p; }
+    T &operator[](size_t i) { return p[i]; }
+    const T &operator[](size_t i) const { return p[i]; }
+};
+
 struct irls_ctx {
     // ---- configuration
     int kind = 0;  // 0 stencil, 1 csr
@@ -98,9 +130,9 @@ struct irls_ctx {
     // two-level rounding (rank 0)
     irls::TLBuffers tl{};
     bool tl_valid = false;
-    std::vector<int32_t> h_cp, h_ccol;
-    std::vector<double> h_ccap;
-    std::vector<__int128> h_cqs, h_cqt;
+    PinnedBuf<int32_t> h_cp, h_ccol;
+    PinnedBuf<double> h_ccap;
+    PinnedBuf<__int128> h_cqs, h_cqt;
     __int128 h_qst = 0;
 
     // ---- graphs

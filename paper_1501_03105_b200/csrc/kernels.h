@@ -68,6 +68,11 @@ void launch_stencil_pspmv(const StencilArgs &s, const VecArgs &v, const RedArgs 
                           cudaStream_t st);
 void launch_sell_pspmv(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
                        cudaStream_t st);
+// small.cu: the whole CG loop of a <= one-chunk graph in one block (kind 0
+// stencil, 1 SELL); runs after the assembly, before finish / report
+void small_cg_prepare();  // once per process, outside stream capture (128 KB dynamic shared memory)
+void launch_small_cg(int kind, const StencilArgs &s, const SellArgs &sl, const VecArgs &v, DevCtrl *ctrl,
+                     double *slots, cudaStream_t st);
 // ghost planes of p for the next iteration (multi-GPU stencil)
 void launch_ghost_pupdate(const VecArgs &v, int64_t ghost_lo, int64_t ghost_hi, int64_t plane, DevCtrl *ctrl,
                           cudaStream_t st);

@@ -113,7 +113,8 @@ def test_vgroup_rejects_unaligned(irls):
         irls.VGroup(spec, 2)
 
 
-def test_nccl_one_rank_communicator(irls):
+@pytest.mark.parametrize("loop_mode", [1, 2])
+def test_nccl_one_rank_communicator(irls, loop_mode):
     """The NCCL code path on one GPU: world_size 1 with an NCCL id runs the
     multi-rank host loop, ncclAllReduce of the slots, the finalize kernels,
     the gather and the ncclBroadcast of the sweep / two-level results over a
@@ -123,7 +124,7 @@ def test_nccl_one_rank_communicator(irls):
     T = 12
     m, reps1, tot1, sw1 = single(irls, spec, irls.options(T=T, record_trace=1), T)
     comm = irls.comm_desc(1, 0, 0, irls.irls_nccl_unique_id(), torch.cuda.current_stream().cuda_stream)
-    g = irls.MinCut.from_spec(spec, irls.options(T=T, record_trace=1), comm)
+    g = irls.MinCut.from_spec(spec, irls.options(T=T, record_trace=1, loop_mode=loop_mode), comm)
     reps, tot = g.irls_solve(irls.IRLS_FROM_SCRATCH, T=T)
     assert tot == tot1
     for a, b in zip(reps, reps1):
@@ -140,7 +141,7 @@ def test_nccl_one_rank_communicator(irls):
     spec = gen.road_graph(120, seed=2, knn=50)
     m, reps1, tot1, sw1 = single(irls, spec, irls.options(T=T), T)
     comm = irls.comm_desc(1, 0, 0, irls.irls_nccl_unique_id(), torch.cuda.current_stream().cuda_stream)  # one id per comm
-    g = irls.MinCut.from_spec(spec, irls.options(T=T), comm)
+    g = irls.MinCut.from_spec(spec, irls.options(T=T, loop_mode=loop_mode), comm)
     _, tot = g.irls_solve(irls.IRLS_FROM_SCRATCH, T=T)
     assert tot == tot1 and np.array_equal(g.irls_get_potentials(), m.irls_get_potentials())
     side, _, k, cut = g.irls_sweep_cut()
