@@ -29,10 +29,11 @@
  *     may pass NULL.
  *   - Every call is stream-ordered on the context's stream and returns after
  *     its results are final.
- *   - Argument errors (IRLS_ERR_INVALID_ARGUMENT and the validation codes at
- *     create) are detected on the host before device work.  After any other
- *     error the context is poisoned: later calls return IRLS_ERR_STATE until
- *     irls_mincut_destroy.  A non-converged CG is NOT an error: the
+ *   - Argument errors (IRLS_ERR_INVALID_ARGUMENT and the validation codes
+ *     BAD_CAPACITY / SINGULAR, at create or irls_set_terminal_weights) are
+ *     detected on the host before device work and leave the context usable.
+ *     After any other error the context is poisoned: later calls return
+ *     IRLS_ERR_STATE until irls_mincut_destroy.  A non-converged CG is NOT an error: the
  *     report says converged = 0.
  *   - No C++ exception crosses this boundary.
  */

@@ -34,7 +34,10 @@ static irls_status fail(irls_ctx *c, irls_status st, const std::string &msg)
 {
     if (c) {
         c->err = msg;
-        if (st != IRLS_ERR_INVALID_ARGUMENT && st != IRLS_ERR_BAD_POTENTIAL && st != IRLS_ERR_STATE) c->poisoned = true;
+        // host-side validation errors leave the context usable
+        if (st != IRLS_ERR_INVALID_ARGUMENT && st != IRLS_ERR_BAD_POTENTIAL && st != IRLS_ERR_STATE &&
+            st != IRLS_ERR_SINGULAR && st != IRLS_ERR_BAD_CAPACITY)
+            c->poisoned = true;
     }
     return st;
 }
@@ -1255,6 +1258,7 @@ static irls_status create_csr_impl(irls_ctx **out, const irls_comm_desc *comm, i
     }
     // merge duplicates in CSR order (A7): count per row, then fill
     std::vector<int64_t> mptr(n + 1, 0);
+    std::vector<int32_t> comp_root;
     auto merge_row = [&](int64_t u, std::vector<Ent> &tmp, int32_t *oc, double *ow) -> int64_t {
         const int64_t a = row_ptr[u], b = row_ptr[u + 1];
         bool sorted = true;
@@ -1406,9 +1410,13 @@ static irls_status create_csr_impl(irls_ctx **out, const irls_comm_desc *comm, i
                 if (hcs[r] > 0.0 || hct[r] > 0.0) anc[find((int32_t)r)].store(1, std::memory_order_relaxed);
         });
         std::vector<uint8_t> lonely(host_threads(nr), 0);
+        comp_root.resize(std::max<int64_t>(nr, 1));
         parallel_for(nr, [&](int i, int64_t a, int64_t b) {
-            for (int64_t r = a; r < b && !lonely[i]; r++)
-                if (!anc[find((int32_t)r)].load(std::memory_order_relaxed)) lonely[i] = 1;
+            for (int64_t r = a; r < b; r++) {
+                const int32_t root = find((int32_t)r);
+                comp_root[r] = root;  // kept: the components of G~ never change (A8 at set_terminal_weights)
+                if (!anc[root].load(std::memory_order_relaxed)) lonely[i] = 1;
+            }
         });
         for (uint8_t l : lonely)
             if (l) return IRLS_ERR_SINGULAR;
@@ -1465,6 +1473,7 @@ static irls_status create_csr_impl(irls_ctx **out, const irls_comm_desc *comm, i
         c->n_entries = nent;
         c->sell_wmax = (int32_t)sell_wmax;
         c->npad_own = (int64_t)c->nchunks * kChunk;
+        c->comp_root = std::move(comp_root);
     }
     // the strip's local SELL: owned neighbours -> v - lo, others -> ghost block
     // (ascending global id, hence grouped by owner rank); send lists by the
@@ -1722,6 +1731,14 @@ extern "C" irls_status irls_set_terminal_weights(irls_ctx *c, const double *cs, 
                 const int64_t u = sl * kSell + ((e - sp[sl]) % kSell);
                 if (cl[e] > u) { cnt++; cmax = std::max(cmax, cp[e]); }
             }
+        // Prop. 1 / A8 with the new terminals: every component keeps an anchor
+        if (!c->comp_root.empty() && n > 0) {
+            std::vector<uint8_t> anch(n, 0);
+            for (int64_t u = 0; u < n; u++)
+                if (cs[u] > 0.0 || ct[u] > 0.0) anch[c->comp_root[u]] = 1;
+            for (int64_t u = 0; u < n; u++)
+                if (!anch[c->comp_root[u]]) return fail(c, IRLS_ERR_SINGULAR, "terminal weights make L~ singular");
+        }
         c->F = compute_F(cmax, cnt);
         CK(cudaMemcpyAsync(c->cs, cs, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
         CK(cudaMemcpyAsync(c->ct, ct, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));

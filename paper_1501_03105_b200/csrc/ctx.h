@@ -90,6 +90,7 @@ struct irls_ctx {
     int32_t *send_idx = nullptr;             // local ids packed for the peers (device)
     double *sendbuf = nullptr;
     std::vector<int64_t> rank_lo;            // [world + 1]: first reduced id owned by every rank
+    std::vector<int32_t> comp_root;          // component (root id) of every non-terminal in G~ (host)
 
     // ---- sweep fixed point
     int32_t F = 0;

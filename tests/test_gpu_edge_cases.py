@@ -81,3 +81,19 @@ def test_all_nlinks_absent(irls):
 def test_thin_grids(irls, dims):
     spec = gen.blob_grid(*dims, seed=9, sigma=(1.0, 3.0))
     both(irls, spec, T=6)
+
+
+def test_csr_terminal_update_singular(irls):
+    """A8 at irls_set_terminal_weights on a CSR graph: removing the last
+    terminal edge of a component is rejected (IRLS_ERR_SINGULAR), as the
+    oracle's nonsingularity check rejects that graph."""
+    spec = gen._csr_edges(6, [(0, 1, 1.0), (1, 2, 2.0), (3, 4, 1.5), (4, 5, 1.0)], 0, 5)
+    m = irls.MinCut.from_spec(spec, irls.options(T=3))
+    m.irls_solve(irls.IRLS_FROM_SCRATCH, T=3)
+    cs, ct = oracle.Graph(spec).terminals()
+    bad_cs, bad_ct = cs.copy(), ct.copy()
+    bad_cs[0] = 0.0  # node 1 (reduced 0) loses its s-link: component {1, 2} keeps no anchor
+    with pytest.raises(irls.IrlsError) as e:
+        m.irls_set_terminal_weights(bad_cs, bad_ct)
+    assert e.value.code == 5
+    m.irls_set_terminal_weights(cs * 2.0, ct * 3.0)  # still anchored: accepted
