@@ -1,0 +1,664 @@
+// api_create.cu — context creation: validation of the
+// inputs (A6-A8), the stencil slab plan, the CSR preparation (duplicate
+// merging, symmetry, terminal split, Prop. 1, SELL-64, id strips with ghost
+// blocks and send lists) on host threads, device allocation and upload.
+#include "api_internal.h"
+
+// Device memory comes from the device's stream-ordered pool with an unbounded
+// release threshold: a create / destroy cycle maps HBM once and then reuses
+// it (sizes here are GBs; cudaMalloc / cudaFree would remap every time).
+static void setup_pool(int device)
+{
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+}
+
+
+// ---------------------------------------------------------------------------
+// create
+// ---------------------------------------------------------------------------
+static irls_status common_setup(irls_ctx *c, const irls_comm_desc *comm, const irls_options *opt)
+{
+    c->opt = *opt;
+    c->world = comm ? comm->world_size : 1;
+    c->rank = comm ? comm->rank : 0;
+    c->device = comm ? comm->device : 0;
+    if (comm && (!comm->device_alloc) != (!comm->device_free)) return IRLS_ERR_INVALID_ARGUMENT;
+    c->dev_alloc = comm ? comm->device_alloc : nullptr;
+    c->dev_free = comm ? comm->device_free : nullptr;
+    c->alloc_user = comm ? comm->alloc_user : nullptr;
+    if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return IRLS_ERR_INVALID_ARGUMENT;
+    if (c->world > 1 && ((!comm->nccl_unique_id && !c->vg) || 8 % c->world != 0)) return IRLS_ERR_INVALID_ARGUMENT;
+    // world 1 with an NCCL id: the multi-rank code path over a 1-rank
+    // communicator (host loop, slot allreduce, finalize kernels, broadcasts)
+    c->multi = c->world > 1 || c->vg != nullptr || (comm && comm->nccl_unique_id != nullptr);
+    CK(cudaSetDevice(c->device));
+    if (comm && comm->cuda_stream) {
+        c->stream = (cudaStream_t)comm->cuda_stream;
+    } else {
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+    }
+    CK(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->side_stream2, cudaStreamNonBlocking));
+    CK(cudaMallocHost(&c->h_done, sizeof(int)));
+    setup_pool(c->device);
+    small_cg_prepare();
+    return IRLS_OK;
+}
+
+static irls_status alloc_solver(irls_ctx *c, int64_t ghost)
+{
+    const int64_t npad = (int64_t)c->nchunks * kChunk;
+    const int64_t gpad = (ghost + 1) & ~(int64_t)1;  // keep the owned start 16-byte aligned
+    auto ghosted = [&](double *&ptr) -> bool {
+        double *b = dalloc<double>(c, npad + 2 * gpad);
+        if (!b) return false;
+        ptr = b + gpad;
+        return true;
+    };
+    if (!ghosted(c->x) || !ghosted(c->z) || !ghosted(c->p0) || !ghosted(c->p1)) return IRLS_ERR_OOM;
+    c->D = dalloc<double>(c, npad);
+    c->Dinv = dalloc<double>(c, npad);
+    c->r = dalloc<double>(c, npad);
+    c->q = dalloc<double>(c, npad);
+    c->ctrl = dalloc<DevCtrl>(c, 1);
+    c->part = dalloc<double>(c, (int64_t)kMaxQ * std::max<int32_t>(c->K, 1));
+    c->slots_local = dalloc<double>(c, kMaxQ * kGroups);
+    c->slots_glob = c->multi ? dalloc<double>(c, kMaxQ * kGroups) : c->slots_local;
+    c->max_reports = std::max(c->opt.T + 1, 1);
+    c->reports = dalloc<DevReport>(c, c->max_reports);
+    if (!c->D || !c->Dinv || !c->r || !c->q || !c->ctrl || !c->part || !c->slots_local || !c->slots_glob || !c->reports)
+        return IRLS_ERR_OOM;
+    if (c->opt.record_trace) {
+        c->gs_diag = dalloc<double>(c, npad);
+        c->gt_diag = dalloc<double>(c, npad);
+        if (!c->gs_diag || !c->gt_diag) return IRLS_ERR_OOM;
+    }
+    DevCtrl h;
+    memset(&h, 0, sizeof(h));
+    h.rtol = c->opt.cg_rtol;
+    h.max_iter = c->opt.cg_max_iter;
+    h.norm = c->opt.cg_norm;
+    h.done = 1;
+    CK(memcpy_sync(c, c->ctrl, &h, sizeof(h), cudaMemcpyHostToDevice));
+    return IRLS_OK;
+}
+
+static irls_status init_nccl(irls_ctx *c, const irls_comm_desc *comm)
+{
+    if (!c->multi || c->vg) return IRLS_OK;
+    ncclUniqueId id;
+    memcpy(&id, comm->nccl_unique_id, sizeof(id));
+    NK(ncclCommInitRank(&c->nccl, c->world, id, c->rank));
+    return IRLS_OK;
+}
+
+// Host BFS for Prop. 1 / A8 on a grid (used only when some n-link is zero).
+bool grid_nonsingular(int32_t nx, int32_t ny, int32_t nz, const double *cx, const double *cy, const double *cz,
+                             const double *cs, const double *ct)
+{
+    const int64_t N = (int64_t)nx * ny * nz, P = (int64_t)nx * ny;
+    std::vector<uint8_t> seen(N, 0);
+    std::vector<int64_t> q;
+    q.reserve(1024);
+    for (int64_t r0 = 0; r0 < N; r0++) {
+        if (seen[r0]) continue;
+        bool anchored = false;
+        q.clear();
+        q.push_back(r0);
+        seen[r0] = 1;
+        for (size_t h = 0; h < q.size(); h++) {
+            const int64_t u = q[h];
+            if (cs[u] > 0.0 || ct[u] > 0.0) anchored = true;
+            const int64_t x = u % nx, y = (u / nx) % ny, z = u / P;
+            const int64_t nb[6] = {z > 0 && cz[u - P] > 0 ? u - P : -1, y > 0 && cy[u - nx] > 0 ? u - nx : -1,
+                                   x > 0 && cx[u - 1] > 0 ? u - 1 : -1, x < nx - 1 && cx[u] > 0 ? u + 1 : -1,
+                                   y < ny - 1 && cy[u] > 0 ? u + nx : -1, z < nz - 1 && cz[u] > 0 ? u + P : -1};
+            for (int k = 0; k < 6; k++)
+                if (nb[k] >= 0 && !seen[nb[k]]) { seen[nb[k]] = 1; q.push_back(nb[k]); }
+        }
+        if (!anchored) return false;
+    }
+    return true;
+}
+
+irls_status create_stencil_impl(irls_ctx **out, const irls_comm_desc *comm, int32_t nx, int32_t ny, int32_t nz,
+                                       const double *cx, const double *cy, const double *cz, const double *cs,
+                                       const double *ct, const irls_options *opt, irls_vgroup *vg);
+
+extern "C" irls_status irls_mincut_create_stencil(irls_ctx **out, const irls_comm_desc *comm, int32_t nx, int32_t ny,
+                                                  int32_t nz, const double *cx, const double *cy, const double *cz,
+                                                  const double *cs, const double *ct, const irls_options *opt)
+{
+    return create_stencil_impl(out, comm, nx, ny, nz, cx, cy, cz, cs, ct, opt, nullptr);
+}
+
+irls_status create_stencil_impl(irls_ctx **out, const irls_comm_desc *comm, int32_t nx, int32_t ny, int32_t nz,
+                                       const double *cx, const double *cy, const double *cz, const double *cs,
+                                       const double *ct, const irls_options *opt, irls_vgroup *vg)
+{
+    NvtxRange nvtx_("irls_mincut_create_stencil");
+    if (!out) return IRLS_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    if (check_opts(opt) || nx < 1 || ny < 1 || nz < 1 || !cx || !cy || !cz || !cs || !ct)
+        return IRLS_ERR_INVALID_ARGUMENT;
+    const int64_t N = (int64_t)nx * ny * nz;
+    if (N >= ((int64_t)1 << 31) - 2 * ((int64_t)nx * ny) - kChunk) return IRLS_ERR_INVALID_ARGUMENT;
+    irls_ctx *c = new irls_ctx();
+    c->vg = vg;
+    irls_status s = common_setup(c, comm, opt);
+    if (!s) {
+        c->kind = 0;
+        c->nx = nx; c->ny = ny; c->nz = nz;
+        c->P = (int64_t)nx * ny;
+        c->n_glob = N;
+        c->n_total = N + 2;
+        c->s_id = N;
+        c->t_id = N + 1;
+        c->K = (int32_t)((N + kChunk - 1) / kChunk);
+        int32_t g0, g1, z0, z1;
+        s = irls_plan_stencil(nx, ny, nz, c->world, c->rank, &z0, &z1, &g0, &g1);
+        if (!s) {
+            c->g0 = g0; c->g1 = g1; c->z0 = z0; c->z1 = z1;
+            c->lo = (int64_t)z0 * c->P;
+            c->n_own = std::min<int64_t>((int64_t)z1 * c->P, N) - c->lo;
+            c->chunk0 = (int32_t)(c->lo / kChunk);
+            c->nchunks = (int32_t)((c->n_own + kChunk - 1) / kChunk);
+            c->n_fin = count_nonempty(c->K, g0, g1);
+            c->lo_ghost = c->world > 1 && c->rank > 0;
+            c->hi_ghost = c->world > 1 && c->rank < c->world - 1;
+            c->rank_lo.assign(c->world + 1, N);
+            for (int r = 0; r < c->world; r++) {
+                int32_t a0, a1;
+                irls_plan_stencil(nx, ny, nz, c->world, r, &a0, &a1, nullptr, nullptr);
+                c->rank_lo[r] = std::min<int64_t>((int64_t)a0 * c->P, N);
+            }
+            if (c->multi) s = irls_halo_plan(nx, ny, nz, c->world, c->rank, &c->hplan);
+        }
+        if (!s) {
+            s = alloc_solver(c, c->world > 1 ? c->P : 0);
+        }
+        if (!s) {
+            // static capacities: full arrays on every rank (rank 0 sweeps the whole graph)
+            c->cx = dalloc<double>(c, N); c->cy = dalloc<double>(c, N); c->cz = dalloc<double>(c, N);
+            c->cs = dalloc<double>(c, N); c->ct = dalloc<double>(c, N);
+            c->gx = dalloc<double>(c, (int64_t)c->nchunks * kChunk);
+            c->gy = dalloc<double>(c, (int64_t)c->nchunks * kChunk);
+            const int64_t gp = c->lo_ghost ? ((c->P + 1) & ~(int64_t)1) : 0;
+            double *gzb = dalloc<double>(c, (int64_t)c->nchunks * kChunk + gp);
+            if (!c->cx || !c->cy || !c->cz || !c->cs || !c->ct || !c->gx || !c->gy || !gzb) s = IRLS_ERR_OOM;
+            else c->gz = gzb + gp;
+        }
+        if (!s) {
+            const size_t b = sizeof(double) * N;
+            cudaMemcpyAsync(c->cx, cx, b, cudaMemcpyHostToDevice, c->stream);
+            cudaMemcpyAsync(c->cy, cy, b, cudaMemcpyHostToDevice, c->stream);
+            cudaMemcpyAsync(c->cz, cz, b, cudaMemcpyHostToDevice, c->stream);
+            cudaMemcpyAsync(c->cs, cs, b, cudaMemcpyHostToDevice, c->stream);
+            cudaMemcpyAsync(c->ct, ct, b, cudaMemcpyHostToDevice, c->stream);
+            unsigned long long vo[6];
+            if (validate_stencil(nx, ny, nz, c->cx, c->cy, c->cz, c->cs, c->ct, vo, c->stream))
+                s = fail(c, IRLS_ERR_CUDA, "validate_stencil");
+            else if (vo[0]) s = IRLS_ERR_BAD_CAPACITY;
+            else {
+                bool ok = vo[1] == 0 ? (vo[2] > 0) : grid_nonsingular(nx, ny, nz, cx, cy, cz, cs, ct);
+                if (!ok) s = IRLS_ERR_SINGULAR;
+                double cmax;
+                memcpy(&cmax, &vo[4], sizeof(double));
+                c->F = compute_F(cmax, (int64_t)vo[3]);
+                c->n_links = (int64_t)vo[5];  // |E~| with c > 0
+            }
+        }
+        if (!s) s = init_nccl(c, comm);
+    }
+    if (s) {
+        irls_mincut_destroy(c);
+        return s;
+    }
+    *out = c;
+    return IRLS_OK;
+}
+
+struct Ent {
+    int32_t col;
+    int64_t pos;
+    double w;
+};
+
+irls_status create_csr_impl(irls_ctx **out, const irls_comm_desc *comm, int64_t n, const int64_t *row_ptr,
+                                   const int32_t *col, const double *w, int64_t s_, int64_t t_, const irls_options *opt,
+                                   irls_vgroup *vg);
+
+extern "C" irls_status irls_mincut_create_csr(irls_ctx **out, const irls_comm_desc *comm, int64_t n,
+                                              const int64_t *row_ptr, const int32_t *col, const double *w, int64_t s_,
+                                              int64_t t_, const irls_options *opt)
+{
+    return create_csr_impl(out, comm, n, row_ptr, col, w, s_, t_, opt, nullptr);
+}
+
+// Id-strip plan of a CSR graph with nr non-terminals over `world` ranks:
+// rank r owns C3 groups [8r/W, 8(r+1)/W), i.e. reduced ids [lo, hi) on chunk
+// boundaries; every rank needs at least one chunk.
+static bool csr_strips(int64_t nr, int world, std::vector<int64_t> &lo)
+{
+    const int32_t K = (int32_t)((nr + kChunk - 1) / kChunk);
+    lo.assign(world + 1, nr);
+    for (int r = 0; r < world; r++) {
+        const int64_t c0 = group_lo(kGroups * r / world, K), c1 = group_lo(kGroups * (r + 1) / world, K);
+        if (world > 1 && c1 <= c0) return false;
+        lo[r] = std::min<int64_t>(c0 * kChunk, nr);
+    }
+    return true;
+}
+
+extern "C" irls_status irls_plan_csr(int64_t nr, int32_t world, int32_t rank, int64_t *lo, int64_t *hi, int32_t *g0,
+                                     int32_t *g1)
+{
+    if (nr < 0 || world < 1 || 8 % world != 0 || rank < 0 || rank >= world) return IRLS_ERR_INVALID_ARGUMENT;
+    std::vector<int64_t> v;
+    if (!csr_strips(nr, world, v)) return IRLS_ERR_INVALID_ARGUMENT;
+    if (lo) *lo = v[rank];
+    if (hi) *hi = v[rank + 1];
+    if (g0) *g0 = kGroups * rank / world;
+    if (g1) *g1 = kGroups * (rank + 1) / world;
+    return IRLS_OK;
+}
+
+irls_status create_csr_impl(irls_ctx **out, const irls_comm_desc *comm, int64_t n, const int64_t *row_ptr,
+                                   const int32_t *col, const double *w, int64_t s_, int64_t t_, const irls_options *opt,
+                                   irls_vgroup *vg)
+{
+    NvtxRange nvtx_("irls_mincut_create_csr");
+    if (!out) return IRLS_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    if (check_opts(opt) || n < 2 || !row_ptr || !col || !w || s_ < 0 || t_ < 0 || s_ >= n || t_ >= n)
+        return IRLS_ERR_INVALID_ARGUMENT;
+    if (s_ == t_) return IRLS_ERR_SOURCE_EQUALS_SINK;
+    if (n >= ((int64_t)1 << 31)) return IRLS_ERR_INVALID_ARGUMENT;
+    if (row_ptr[0] != 0) return IRLS_ERR_INVALID_ARGUMENT;
+    for (int64_t u = 0; u < n; u++)
+        if (row_ptr[u + 1] < row_ptr[u]) return IRLS_ERR_INVALID_ARGUMENT;
+    const int64_t nnz = row_ptr[n];
+    // Host preparation runs on the host threads (row blocks); every result is
+    // independent of the thread count (first offending entry wins, integer
+    // counts, per-row sums in CSR order).
+    {
+        std::vector<int64_t> bad(host_threads(nnz), INT64_MAX);
+        std::vector<int> code(bad.size(), 0);
+        parallel_for(nnz, [&](int i, int64_t a, int64_t b) {
+            for (int64_t e = a; e < b; e++) {
+                if (col[e] < 0 || col[e] >= n) { bad[i] = e; code[i] = IRLS_ERR_INVALID_ARGUMENT; return; }
+                if (!(w[e] >= 0.0) || isinf(w[e])) { bad[i] = e; code[i] = IRLS_ERR_BAD_CAPACITY; return; }
+            }
+        });
+        for (size_t i = 0; i < bad.size(); i++)
+            if (bad[i] != INT64_MAX) return (irls_status)code[i];
+        std::vector<uint8_t> loop(host_threads(n), 0);
+        parallel_for(n, [&](int i, int64_t a, int64_t b) {
+            for (int64_t u = a; u < b && !loop[i]; u++)
+                for (int64_t e = row_ptr[u]; e < row_ptr[u + 1]; e++)
+                    if (col[e] == u) { loop[i] = 1; break; }
+        });
+        for (uint8_t l : loop)
+            if (l) return IRLS_ERR_INVALID_ARGUMENT;
+    }
+    // merge duplicates in CSR order (A7): count per row, then fill
+    std::vector<int64_t> mptr(n + 1, 0);
+    std::vector<int32_t> comp_root;
+    auto merge_row = [&](int64_t u, std::vector<Ent> &tmp, int32_t *oc, double *ow) -> int64_t {
+        const int64_t a = row_ptr[u], b = row_ptr[u + 1];
+        bool sorted = true;
+        for (int64_t e = a + 1; e < b; e++)
+            if (col[e] <= col[e - 1]) { sorted = false; break; }
+        if (sorted) {
+            if (oc)
+                for (int64_t e = a; e < b; e++) { oc[e - a] = col[e]; ow[e - a] = w[e]; }
+            return b - a;
+        }
+        tmp.clear();
+        for (int64_t e = a; e < b; e++) tmp.push_back({col[e], e, w[e]});
+        std::stable_sort(tmp.begin(), tmp.end(), [](const Ent &x, const Ent &y) { return x.col < y.col; });
+        int64_t m = 0;
+        double last = 0.0;
+        for (size_t i = 0; i < tmp.size(); i++) {
+            if (i > 0 && tmp[i].col == tmp[i - 1].col) {
+                last = last + tmp[i].w;
+                if (ow) ow[m - 1] = last;
+            } else {
+                last = tmp[i].w;
+                if (oc) { oc[m] = tmp[i].col; ow[m] = last; }
+                m++;
+            }
+        }
+        return m;
+    };
+    parallel_for(n, [&](int, int64_t a, int64_t b) {
+        std::vector<Ent> tmp;
+        for (int64_t u = a; u < b; u++) mptr[u + 1] = merge_row(u, tmp, nullptr, nullptr);
+    });
+    for (int64_t u = 0; u < n; u++) mptr[u + 1] += mptr[u];
+    HostBuf<int32_t> mcol(mptr[n]);
+    HostBuf<double> mw(mptr[n]);
+    parallel_for(n, [&](int, int64_t a, int64_t b) {
+        std::vector<Ent> tmp;
+        for (int64_t u = a; u < b; u++) merge_row(u, tmp, mcol.data() + mptr[u], mw.data() + mptr[u]);
+    });
+    // exact symmetry
+    {
+        std::vector<uint8_t> asym(host_threads(n), 0);
+        parallel_for(n, [&](int i, int64_t a, int64_t b) {
+            for (int64_t u = a; u < b && !asym[i]; u++)
+                for (int64_t e = mptr[u]; e < mptr[u + 1]; e++) {
+                    const int32_t v = mcol[e];
+                    const int32_t *beg = mcol.data() + mptr[v], *end = mcol.data() + mptr[v + 1];
+                    const int32_t *it = std::lower_bound(beg, end, (int32_t)u);
+                    if (it == end || *it != u || mw[it - mcol.data()] != mw[e]) { asym[i] = 1; break; }
+                }
+        });
+        for (uint8_t a : asym)
+            if (a) return IRLS_ERR_NOT_SYMMETRIC;
+    }
+    const int64_t nr = n - 2;
+    auto red = [&](int64_t v) { return v - (v > s_) - (v > t_); };
+    auto orig_of = [&](int64_t r) {  // reduced id -> original id
+        int64_t u = r;
+        const int64_t lo2 = std::min(s_, t_), hi2 = std::max(s_, t_);
+        if (u >= lo2) u++;
+        if (u >= hi2) u++;
+        return u;
+    };
+    std::vector<double> hcs(std::max<int64_t>(nr, 1), 0.0), hct(std::max<int64_t>(nr, 1), 0.0);
+    std::vector<int64_t> orig(std::max<int64_t>(nr, 1), 0);
+    std::vector<int64_t> aptr(nr + 1, 0);
+    double cst = 0.0;
+    for (int64_t e = mptr[s_]; e < mptr[s_ + 1]; e++)
+        if (mcol[e] == t_) cst = mw[e];
+    parallel_for(nr, [&](int, int64_t a, int64_t b) {
+        for (int64_t r = a; r < b; r++) {
+            const int64_t u = orig_of(r);
+            orig[r] = u;
+            int64_t k = 0;
+            for (int64_t e = mptr[u]; e < mptr[u + 1]; e++) {
+                const int64_t v = mcol[e];
+                if (v == s_) hcs[r] = mw[e];
+                else if (v == t_) hct[r] = mw[e];
+                else if (mw[e] > 0.0) k++;
+            }
+            aptr[r + 1] = k;
+        }
+    });
+    for (int64_t r = 0; r < nr; r++) aptr[r + 1] += aptr[r];
+    HostBuf<int32_t> aidx(aptr[nr]);
+    HostBuf<double> ac(aptr[nr]);
+    std::vector<int64_t> tcnt(host_threads(nr), 0);
+    std::vector<double> tmax(tcnt.size(), 0.0);
+    parallel_for(nr, [&](int i, int64_t a, int64_t b) {
+        int64_t cn = 0;
+        double cm = 0.0;
+        for (int64_t r = a; r < b; r++) {
+            const int64_t u = orig[r];
+            int64_t k = aptr[r];
+            for (int64_t e = mptr[u]; e < mptr[u + 1]; e++) {
+                const int64_t v = mcol[e];
+                if (v == s_ || v == t_ || !(mw[e] > 0.0)) continue;
+                aidx[k] = (int32_t)red(v);
+                ac[k] = mw[e];
+                k++;
+                if (v > u) { cn++; cm = std::max(cm, mw[e]); }
+            }
+            if (hcs[r] > 0) { cn++; cm = std::max(cm, hcs[r]); }
+            if (hct[r] > 0) { cn++; cm = std::max(cm, hct[r]); }
+        }
+        tcnt[i] = cn;
+        tmax[i] = cm;
+    });
+    double cmax = cst;
+    int64_t cnt = cst > 0.0;
+    for (size_t i = 0; i < tcnt.size(); i++) { cnt += tcnt[i]; cmax = std::max(cmax, tmax[i]); }
+    // Prop. 1 / A8: every component of G~ touches a positive terminal edge.
+    // Lock-free union-find over the edges (the components do not depend on
+    // the union order), then every component's root must be anchored.
+    {
+        std::unique_ptr<std::atomic<int32_t>[]> par(new std::atomic<int32_t>[(size_t)std::max<int64_t>(nr, 1)]);
+        std::unique_ptr<std::atomic<uint8_t>[]> anc(new std::atomic<uint8_t>[(size_t)std::max<int64_t>(nr, 1)]);
+        parallel_for(nr, [&](int, int64_t a, int64_t b) {
+            for (int64_t r = a; r < b; r++) {
+                par[r].store((int32_t)r, std::memory_order_relaxed);
+                anc[r].store(0, std::memory_order_relaxed);
+            }
+        });
+        auto find = [&](int32_t x) {
+            for (;;) {
+                int32_t p = par[x].load(std::memory_order_relaxed);
+                if (p == x) return x;
+                const int32_t gp = par[p].load(std::memory_order_relaxed);
+                if (gp != p) par[x].compare_exchange_weak(p, gp, std::memory_order_relaxed);
+                x = gp;
+            }
+        };
+        parallel_for(nr, [&](int, int64_t a, int64_t b) {
+            for (int64_t r = a; r < b; r++)
+                for (int64_t e = aptr[r]; e < aptr[r + 1]; e++) {
+                    if (aidx[e] < r) continue;
+                    int32_t x = (int32_t)r, y = aidx[e];
+                    for (;;) {
+                        x = find(x);
+                        y = find(y);
+                        if (x == y) break;
+                        if (x < y) std::swap(x, y);  // link the larger root below the smaller
+                        int32_t expect = x;
+                        if (par[x].compare_exchange_strong(expect, y, std::memory_order_relaxed)) break;
+                    }
+                }
+        });
+        parallel_for(nr, [&](int, int64_t a, int64_t b) {
+            for (int64_t r = a; r < b; r++)
+                if (hcs[r] > 0.0 || hct[r] > 0.0) anc[find((int32_t)r)].store(1, std::memory_order_relaxed);
+        });
+        std::vector<uint8_t> lonely(host_threads(nr), 0);
+        comp_root.resize(std::max<int64_t>(nr, 1));
+        parallel_for(nr, [&](int i, int64_t a, int64_t b) {
+            for (int64_t r = a; r < b; r++) {
+                const int32_t root = find((int32_t)r);
+                comp_root[r] = root;  // kept: the components of G~ never change (A8 at set_terminal_weights)
+                if (!anc[root].load(std::memory_order_relaxed)) lonely[i] = 1;
+            }
+        });
+        for (uint8_t l : lonely)
+            if (l) return IRLS_ERR_SINGULAR;
+    }
+    // SELL-64 (slices of 64 consecutive rows, column-major inside a slice: the
+    // k-th neighbour of rows 2t and 2t+1 are adjacent, one 128-bit load)
+    const int64_t nsl = (nr + kSell - 1) / kSell;
+    std::vector<int64_t> sptr(nsl + 1, 0);
+    int64_t sell_wmax = 0;
+    for (int64_t sl = 0; sl < nsl; sl++) {
+        int64_t wmax = 0;
+        for (int64_t r = sl * kSell; r < std::min<int64_t>(nr, sl * kSell + kSell); r++)
+            wmax = std::max(wmax, aptr[r + 1] - aptr[r]);
+        sptr[sl + 1] = sptr[sl] + kSell * wmax;
+        sell_wmax = std::max(sell_wmax, wmax);
+    }
+    const int64_t nent = sptr[nsl];
+    HostBuf<int32_t> scol(nent);
+    HostBuf<double> scap(nent);
+    parallel_for(nsl, [&](int, int64_t a, int64_t b) {  // padding slots: col -1, c 0
+        for (int64_t e = sptr[a]; e < sptr[b]; e++) { scol[e] = -1; scap[e] = 0.0; }
+    });
+    parallel_for(nr, [&](int, int64_t a, int64_t b) {
+        for (int64_t r = a; r < b; r++) {
+            const int64_t sl = r / kSell, ln = r % kSell;
+            for (int64_t k = 0; k < aptr[r + 1] - aptr[r]; k++) {
+                scol[sptr[sl] + kSell * k + ln] = aidx[aptr[r] + k];
+                scap[sptr[sl] + kSell * k + ln] = ac[aptr[r] + k];
+            }
+        }
+    });
+    irls_ctx *c = new irls_ctx();
+    c->vg = vg;
+    irls_status st = common_setup(c, comm, opt);
+    if (!st && c->multi && !csr_strips(nr, c->world, c->rank_lo)) st = IRLS_ERR_INVALID_ARGUMENT;
+    if (!st && !c->multi) c->rank_lo = {0, nr};
+    if (!st) {
+        c->kind = 1;
+        c->n_glob = nr;
+        c->n_total = n;
+        c->s_id = s_;
+        c->t_id = t_;
+        c->c_st = cst;
+        c->K = (int32_t)((nr + kChunk - 1) / kChunk);
+        c->g0 = kGroups * c->rank / c->world;
+        c->g1 = kGroups * (c->rank + 1) / c->world;
+        c->lo = c->rank_lo[c->rank];
+        c->n_own = c->rank_lo[c->rank + 1] - c->lo;
+        c->chunk0 = (int32_t)(c->lo / kChunk);
+        c->nchunks = (int32_t)((c->n_own + kChunk - 1) / kChunk);
+        c->n_fin = count_nonempty(c->K, c->g0, c->g1);
+        c->n_links = aptr[nr] / 2;
+        c->F = compute_F(cmax, cnt);
+        c->n_entries = nent;
+        c->sell_wmax = (int32_t)sell_wmax;
+        c->npad_own = (int64_t)c->nchunks * kChunk;
+        c->comp_root = std::move(comp_root);
+    }
+    // the strip's local SELL: owned neighbours -> v - lo, others -> ghost block
+    // (ascending global id, hence grouped by owner rank); send lists by the
+    // symmetry of G~: u goes to peer q iff u has a neighbour owned by q
+    std::vector<int64_t> lsptr;
+    std::vector<int32_t> lscol, lsend;
+    std::vector<double> lscap;
+    int64_t lwmax = 0;
+    if (!st && c->multi) {
+        const int64_t lo = c->lo, hi = c->lo + c->n_own, W = c->world;
+        auto owner = [&](int64_t v) {
+            return (int)(std::upper_bound(c->rank_lo.begin(), c->rank_lo.end() - 1, v) - c->rank_lo.begin()) - 1;
+        };
+        std::vector<int32_t> ghosts;
+        for (int64_t r = lo; r < hi; r++)
+            for (int64_t e = aptr[r]; e < aptr[r + 1]; e++)
+                if (aidx[e] < lo || aidx[e] >= hi) ghosts.push_back(aidx[e]);
+        std::sort(ghosts.begin(), ghosts.end());
+        ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
+        c->n_ghost = (int64_t)ghosts.size();
+        c->recv_off.assign(W + 1, 0);
+        for (int32_t v : ghosts) c->recv_off[owner(v) + 1]++;
+        for (int q = 0; q < W; q++) c->recv_off[q + 1] += c->recv_off[q];
+        std::vector<std::vector<int32_t>> sendq(W);
+        for (int64_t r = lo; r < hi; r++) {
+            int peers[16], np = 0;
+            for (int64_t e = aptr[r]; e < aptr[r + 1]; e++) {
+                const int64_t v = aidx[e];
+                if (v >= lo && v < hi) continue;
+                const int q = owner(v);
+                bool seen = false;
+                for (int i = 0; i < np; i++) seen |= peers[i] == q;
+                if (!seen && np < 16) peers[np++] = q;
+            }
+            for (int i = 0; i < np; i++) sendq[peers[i]].push_back((int32_t)(r - lo));
+        }
+        c->send_off.assign(W + 1, 0);
+        for (int q = 0; q < W; q++) {
+            c->send_off[q + 1] = c->send_off[q] + (int64_t)sendq[q].size();
+            lsend.insert(lsend.end(), sendq[q].begin(), sendq[q].end());
+        }
+        const int64_t nl = c->n_own, lnsl = (nl + kSell - 1) / kSell;
+        lsptr.assign(lnsl + 1, 0);
+        for (int64_t sl = 0; sl < lnsl; sl++) {
+            int64_t wm = 0;
+            for (int64_t r = sl * kSell; r < std::min<int64_t>(nl, sl * kSell + kSell); r++)
+                wm = std::max(wm, aptr[lo + r + 1] - aptr[lo + r]);
+            lsptr[sl + 1] = lsptr[sl] + kSell * wm;
+            lwmax = std::max(lwmax, wm);
+        }
+        lscol.assign(std::max<int64_t>(lsptr[lnsl], 1), -1);
+        lscap.assign(std::max<int64_t>(lsptr[lnsl], 1), 0.0);
+        for (int64_t r = 0; r < nl; r++) {
+            const int64_t sl = r / kSell, ln = r % kSell, gr = lo + r;
+            for (int64_t k = 0; k < aptr[gr + 1] - aptr[gr]; k++) {
+                const int64_t v = aidx[aptr[gr] + k];
+                const int64_t lv = (v >= lo && v < hi)
+                                       ? v - lo
+                                       : c->npad_own + (std::lower_bound(ghosts.begin(), ghosts.end(), (int32_t)v) - ghosts.begin());
+                lscol[lsptr[sl] + kSell * k + ln] = (int32_t)lv;
+                lscap[lsptr[sl] + kSell * k + ln] = ac[aptr[gr] + k];
+            }
+        }
+        c->ln_entries = lsptr[lnsl];
+        c->lwmax = (int32_t)lwmax;
+        if (c->npad_own + c->n_ghost >= ((int64_t)1 << 31)) st = IRLS_ERR_INVALID_ARGUMENT;
+    }
+    if (!st) st = alloc_solver(c, c->multi ? c->n_ghost : 0);
+    if (!st) {
+        const int64_t gpad = (int64_t)c->K * kChunk;  // the whole graph (rank 0 sweeps it)
+        c->cs = dalloc<double>(c, gpad);
+        c->ct = dalloc<double>(c, gpad);
+        c->slice_ptr = dalloc<int64_t>(c, nsl + 1);
+        c->col = dalloc<int32_t>(c, nent);
+        c->cap = dalloc<double>(c, nent);
+        c->gsell = dalloc<double>(c, nent);
+        c->orig_dev = dalloc<int64_t>(c, std::max<int64_t>(nr, 1));
+        if (!c->cs || !c->ct || !c->slice_ptr || !c->col || !c->cap || !c->gsell || !c->orig_dev) st = IRLS_ERR_OOM;
+    }
+    if (!st && !c->multi) {  // one rank: the solve runs on the global structure
+        c->lslice_ptr = c->slice_ptr;
+        c->lcol = c->col;
+        c->lcap = c->cap;
+        c->lg = c->gsell;
+        c->lcs = c->cs;
+        c->lct = c->ct;
+        c->lwmax = c->sell_wmax;
+        c->ln_entries = c->n_entries;
+    } else if (!st) {
+        const int64_t npad = c->npad_own, le = std::max<int64_t>(c->ln_entries, 1);
+        c->lslice_ptr = dalloc<int64_t>(c, (int64_t)lsptr.size());
+        c->lcol = dalloc<int32_t>(c, le);
+        c->lcap = dalloc<double>(c, le);
+        c->lg = dalloc<double>(c, le);
+        c->lcs = dalloc<double>(c, npad);
+        c->lct = dalloc<double>(c, npad);
+        c->send_idx = dalloc<int32_t>(c, std::max<int64_t>((int64_t)lsend.size(), 1));
+        c->sendbuf = dalloc<double>(c, std::max<int64_t>((int64_t)lsend.size(), 1));
+        if (!c->lslice_ptr || !c->lcol || !c->lcap || !c->lg || !c->lcs || !c->lct || !c->send_idx || !c->sendbuf)
+            st = IRLS_ERR_OOM;
+        cudaError_t e = cudaSuccess;
+        auto up = [&](void *dst, const void *src, size_t bytes) {
+            if (e == cudaSuccess && bytes > 0) e = memcpy_sync(c, dst, src, bytes, cudaMemcpyHostToDevice);
+        };
+        if (!st) {
+            up(c->lslice_ptr, lsptr.data(), sizeof(int64_t) * lsptr.size());
+            up(c->lcol, lscol.data(), sizeof(int32_t) * lscol.size());
+            up(c->lcap, lscap.data(), sizeof(double) * lscap.size());
+            if (c->n_own > 0) {
+                up(c->lcs, hcs.data() + c->lo, sizeof(double) * c->n_own);
+                up(c->lct, hct.data() + c->lo, sizeof(double) * c->n_own);
+            }
+            up(c->send_idx, lsend.data(), sizeof(int32_t) * lsend.size());
+            if (e != cudaSuccess) st = fail(c, IRLS_ERR_CUDA, std::string("csr strip upload: ") + cudaGetErrorString(e));
+        }
+    }
+    if (!st) st = init_nccl(c, comm);
+    if (!st && nr > 0) {
+        cudaError_t e = cudaSuccess;
+        auto up = [&](void *dst, const void *src, size_t bytes) {
+            if (e == cudaSuccess && bytes > 0) e = memcpy_sync(c, dst, src, bytes, cudaMemcpyHostToDevice);
+        };
+        up(c->cs, hcs.data(), sizeof(double) * nr);
+        up(c->ct, hct.data(), sizeof(double) * nr);
+        up(c->slice_ptr, sptr.data(), sizeof(int64_t) * (nsl + 1));
+        up(c->col, scol.data(), sizeof(int32_t) * nent);
+        up(c->cap, scap.data(), sizeof(double) * nent);
+        up(c->orig_dev, orig.data(), sizeof(int64_t) * nr);
+        if (e != cudaSuccess) st = fail(c, IRLS_ERR_CUDA, std::string("csr upload: ") + cudaGetErrorString(e));
+    }
+    if (st) {
+        irls_mincut_destroy(c);
+        return st;
+    }
+    *out = c;
+    return IRLS_OK;
+}
+

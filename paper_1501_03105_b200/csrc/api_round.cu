@@ -1,0 +1,611 @@
+// api_round.cu — rounding of x^(T): the GPU sweep cut, the
+// two-level rounding with the host max-flow, the exact min cut
+// (mu* for delta, Eq. 13), and the Cheeger-type lambda_2.
+#include <chrono>
+
+#include "api_internal.h"
+
+// ---------------------------------------------------------------------------
+// sweep cut
+// ---------------------------------------------------------------------------
+static irls_status alloc_sweep(irls_ctx *c)
+{
+    if (c->sb.keys) return IRLS_OK;
+    SweepBuffers &b = c->sb;
+    const int64_t n = c->n_glob, nt = sweep_ntiles(n);
+    b.n = n;
+    b.keys = dalloc<unsigned long long>(c, n);
+    b.keys_alt = dalloc<unsigned long long>(c, n);
+    b.vals = dalloc<int32_t>(c, n);
+    b.vals_alt = dalloc<int32_t>(c, n);
+    b.rank = dalloc<int32_t>(c, n);
+    b.tile_hist = dalloc<int32_t>(c, 256 * nt);
+    b.tile_off = dalloc<int32_t>(c, 256 * nt);
+    b.scan_tmp = (int32_t *)dalloc<int64_t>(c, (256 * nt + 4095) / 4096 + 1);
+    b.digit_hist = dalloc<unsigned long long>(c, 8 * 256);
+    b.delta = dalloc<__int128>(c, n + 2);
+    b.delta_id = dalloc<__int128>(c, n);
+    b.tile_sum = dalloc<__int128>(c, nt);
+    b.tile_min = dalloc<__int128>(c, nt);
+    b.tile_argmin = dalloc<int64_t>(c, nt);
+    b.flags = dalloc<int32_t>(c, 4);
+    b.k_out = dalloc<int64_t>(c, 1);
+    b.side = dalloc<uint8_t>(c, c->n_total);
+    c->order_out = dalloc<int32_t>(c, n);
+    if (!b.keys || !b.keys_alt || !b.vals || !b.vals_alt || !b.rank || !b.tile_hist || !b.tile_off || !b.scan_tmp ||
+        !b.digit_hist || !b.delta || !b.delta_id || !b.tile_sum || !b.tile_min || !b.tile_argmin || !b.flags || !b.k_out || !b.side ||
+        !c->order_out)
+        return fail(c, IRLS_ERR_OOM, "sweep buffers");
+    return IRLS_OK;
+}
+
+// Rank 0 result of the sweep, broadcast so every rank returns the same values.
+struct SweepResultMsg {
+    int64_t status, k;
+    double cut;
+};
+
+irls_status sweep_rank0(irls_ctx *c, const double *xfull, uint8_t *side, int32_t *order, int64_t *k,
+                               double *cut_value);
+
+extern "C" irls_status irls_sweep_cut(irls_ctx *c, uint8_t *side, int32_t *order, int64_t *k, double *cut_value)
+{
+    NvtxRange nvtx_("irls_sweep_cut");
+    GUARD(c);
+    if (c->state == 0) return fail(c, IRLS_ERR_STATE, "sweep before solve");
+    double *xfull = nullptr;
+    irls_status s = gather_x(c, &xfull);
+    if (s) return s;
+    SweepResultMsg msg{0, 0, 0.0};
+    if (c->rank == 0) {
+        s = sweep_rank0(c, xfull, side, order, &msg.k, &msg.cut);
+        msg.status = s;
+        if (s && s != IRLS_ERR_BAD_POTENTIAL && !c->multi) return s;
+    }
+    if (c->multi) {
+        if (!c->msg_dev) {
+            c->msg_dev = dalloc<SweepResultMsg>(c, 1);
+            if (!c->msg_dev) return fail(c, IRLS_ERR_OOM, "sweep msg");
+        }
+        if (c->rank == 0)
+            CK(cudaMemcpyAsync(c->msg_dev, &msg, sizeof(msg), cudaMemcpyHostToDevice, c->stream));
+        NK(ncclBroadcast(c->msg_dev, c->msg_dev, sizeof(msg), ncclUint8, 0, c->nccl, c->stream));
+        CK(cudaMemcpyAsync(&msg, c->msg_dev, sizeof(msg), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    }
+    if (msg.status) return fail(c, (irls_status)msg.status, c->rank == 0 ? c->err : "sweep failed on rank 0");
+    if (k) *k = msg.k;
+    if (cut_value) *cut_value = msg.cut;
+    return IRLS_OK;
+}
+
+irls_status sweep_rank0(irls_ctx *c, const double *xfull, uint8_t *side, int32_t *order, int64_t *k,
+                               double *cut_value)
+{
+    cudaStream_t st = c->stream;
+    const int64_t n = c->n_glob;
+    irls_status s = alloc_sweep(c);
+    if (s) return s;
+    int launches = 0;
+    c->launches = 0;
+    SweepBuffers &b = c->sb;
+    CK(cudaMemsetAsync(b.flags, 0, sizeof(int32_t) * 4, st));
+    sweep_keys(xfull, b, st);
+    launches++;
+    int32_t *ord = sweep_sort(b, st, &launches);
+    int32_t hflag = 0;
+    CK(cudaMemcpyAsync(&hflag, b.flags, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (hflag) return fail(c, IRLS_ERR_BAD_POTENTIAL, "NaN in potentials");
+    sweep_rank(ord, b, st);
+    launches++;
+    if (c->kind == 0) sweep_delta_stencil(stencil_args(c, true), n, c->F, b, st);
+    else sweep_delta_sell(sell_args_full(c), c->F, b, st);
+    sweep_delta_order(ord, b, st);
+    launches += 2;
+    sweep_scan_argmin(b, qfix_host(c->c_st, c->F), st);
+    launches += 4;
+    RedArgs ra;
+    ra.part = c->part;
+    ra.slots = c->slots_local;
+    ra.ctrl = c->ctrl;
+    ra.K = (int32_t)((n + kChunk - 1) / kChunk);
+    ra.g0 = 0;
+    ra.g1 = 8;
+    ra.n_fin = count_nonempty(ra.K, 0, 8);
+    if (c->kind == 0) {
+        sweep_side_cross_stencil(stencil_args(c, true), n, b, ra, st);
+    } else {
+        CK(cudaMemsetAsync(b.side, 0, c->n_total, st));
+        sweep_side_cross_sell(sell_args_full(c), c->orig_dev, c->n_total, b, ra, st);
+        const uint8_t one = 1;
+        CK(cudaMemcpyAsync(b.side + c->s_id, &one, 1, cudaMemcpyHostToDevice, st));
+    }
+    launches++;
+    irls_status ls = last_launch(c, "sweep");
+    if (ls) return ls;
+    double slots[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int64_t hk = 0;
+    if (n > 0) CK(cudaMemcpyAsync(slots, c->slots_local, sizeof(slots), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&hk, b.k_out, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    if (order && n > 0) {
+        sweep_order_out(ord, c->kind == 1 ? c->orig_dev : nullptr, c->order_out, n, st);
+        launches++;
+        CK(cudaMemcpyAsync(order, c->order_out, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+    }
+    if (side) CK(cudaMemcpyAsync(side, b.side, c->n_total, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (n == 0) hk = 0;
+    c->sweep_k = hk;
+    c->sweep_cut = irls_combine_slots(slots) + c->c_st;
+    c->sweep_valid = true;
+    c->order_dev = ord;
+    c->launches += launches;
+    if (k) *k = hk;
+    if (cut_value) *cut_value = c->sweep_cut;
+    return IRLS_OK;
+}
+
+extern "C" irls_status irls_get_side(irls_ctx *c, uint8_t *side)
+{
+    GUARD(c);
+    if (!c->sweep_valid) return fail(c, IRLS_ERR_STATE, "no sweep result");
+    if (!side) return IRLS_ERR_INVALID_ARGUMENT;
+    CK(memcpy_sync(c, side, c->sb.side, c->n_total, cudaMemcpyDeviceToHost));
+    return IRLS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Two-level rounding (include/irls_mincut.h, DESIGN.md §2 A25-A29)
+// ---------------------------------------------------------------------------
+
+static irls_status alloc_tl(irls_ctx *c)
+{
+    TLBuffers &b = c->tl;
+    if (b.st) return IRLS_OK;
+    const int64_t n = c->n_glob, K = (n + kChunk - 1) / kChunk, nt = tl_ntiles(n);
+    b.n = n;
+    b.st = dalloc<TLState>(c, 1);
+    b.part = dalloc<double>(c, 3 * K);
+    b.slots = dalloc<double>(c, 3 * kGroups);
+    b.ctrl = dalloc<DevCtrl>(c, 1);
+    b.cls = dalloc<int8_t>(c, n);
+    b.flag = dalloc<int32_t>(c, n);
+    b.cid = dalloc<int32_t>(c, n);
+    b.deg = dalloc<int32_t>(c, n);
+    b.eoff = dalloc<int32_t>(c, n);
+    b.scan_tmp = dalloc<int64_t>(c, nt + 1);
+    b.tile_a = dalloc<__int128>(c, nt);
+    b.tile_n1 = dalloc<int32_t>(c, nt);
+    b.cp = dalloc<int32_t>(c, n + 1);
+    b.cqs = dalloc<__int128>(c, n);
+    b.cqt = dalloc<__int128>(c, n);
+    b.src = dalloc<uint8_t>(c, n);
+    b.prank = dalloc<int32_t>(c, n);
+    b.one = dalloc<int64_t>(c, 1);
+    b.side = dalloc<uint8_t>(c, c->n_total);
+    b.ccol = nullptr;
+    b.ccap = nullptr;
+    b.cap_entries = 0;
+    if (!b.st || !b.part || !b.slots || !b.ctrl || !b.cls || !b.flag || !b.cid || !b.deg || !b.eoff || !b.scan_tmp ||
+        !b.tile_a || !b.tile_n1 || !b.cp || !b.cqs || !b.cqt || !b.src || !b.prank || !b.one || !b.side)
+        return fail(c, IRLS_ERR_OOM, "two-level buffers");
+    const int64_t one = 1;
+    CK(cudaMemcpyAsync(b.one, &one, sizeof(one), cudaMemcpyHostToDevice, c->stream));
+    return IRLS_OK;
+}
+
+// Coarse entry buffers grow to the largest coarse graph seen.
+static irls_status tl_reserve(irls_ctx *c, int64_t entries)
+{
+    TLBuffers &b = c->tl;
+    if (entries <= b.cap_entries && b.ccol) return IRLS_OK;
+    for (void *p : {(void *)b.ccol, (void *)b.ccap}) {
+        if (!p) continue;
+        CK(dfree(c, p));
+    }
+    b.ccol = dalloc<int32_t>(c, entries);
+    b.ccap = dalloc<double>(c, entries);
+    if (!b.ccol || !b.ccap) return fail(c, IRLS_ERR_OOM, "coarse graph");
+    b.cap_entries = std::max<int64_t>(entries, 1);
+    return IRLS_OK;
+}
+
+static double q_to_double(__int128 q, int32_t F) { return ldexp((double)q, -F); }
+
+// exact: no contraction (gamma0 = -inf, gamma1 = +inf, every node in Sc): the
+// exact min cut mu* of G by the same pipeline (for delta, Eq. 13).
+irls_status two_level_rank0(irls_ctx *c, const double *xfull, uint8_t *side, irls_two_level_report *r,
+                                   bool exact)
+{
+    auto t_start = std::chrono::steady_clock::now();
+    cudaStream_t st = c->stream;
+    const int64_t n = c->n_glob;
+    irls_status s = alloc_tl(c);
+    if (s) return s;
+    TLBuffers &b = c->tl;
+    memset(r, 0, sizeof(*r));
+    r->F = c->F;
+    cudaEvent_t ev[4];
+    for (auto &e : ev) CK(cudaEventCreate(&e));
+    struct EvGuard {
+        cudaEvent_t *e;
+        ~EvGuard() { for (int i = 0; i < 4; i++) cudaEventDestroy(e[i]); }
+    } guard{ev};
+    int launches = 0;
+    CK(cudaEventRecord(ev[0], st));
+    // A NaN in x lands in cluster 0 (the comparison is false) and makes c0 NaN.
+    // 1. K-means (A25): batches of rounds, the device stops itself
+    TLState h{0.1, 0.9, 0, 0};
+    CK(cudaMemcpyAsync(b.st, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+    if (exact) {
+        h.done = 1;
+    } else if (n > 0) {
+        RedArgs ra;
+        ra.part = b.part;
+        ra.slots = b.slots;
+        ra.ctrl = b.ctrl;
+        ra.K = (int32_t)((n + kChunk - 1) / kChunk);
+        ra.g0 = 0;
+        ra.g1 = kGroups;
+        ra.n_fin = count_nonempty(ra.K, 0, kGroups);
+        for (int batch = 0; batch < 13 && !h.done; batch++) {
+            for (int i = 0; i < 8; i++) tl_kmeans_round(xfull, n, b.st, ra, st);
+            launches += 8;
+            CK(cudaMemcpyAsync(&h, b.st, sizeof(h), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+        }
+    } else if (!exact) {  // only the terminals' values {1, 0}
+        for (h.rounds = 1; h.rounds <= 100; h.rounds++) {
+            double s0 = 0.0, s1 = 0.0;
+            int64_t n1 = 0;
+            const double xt[2] = {1.0, 0.0};
+            for (double v : xt) {
+                if (fabs(v - h.c1) < fabs(v - h.c0)) { s1 = s1 + v; n1++; } else { s0 = s0 + v; }
+            }
+            const double d0 = (2 - n1) > 0 ? s0 / (double)(2 - n1) : h.c0, d1 = n1 > 0 ? s1 / (double)n1 : h.c1;
+            const bool same = d0 == h.c0 && d1 == h.c1;
+            h.c0 = d0;
+            h.c1 = d1;
+            if (same) break;
+        }
+        if (h.rounds > 100) h.rounds = 100;
+    }
+    if (exact) h.rounds = 0;
+    if (isnan(h.c0) || isnan(h.c1)) return fail(c, IRLS_ERR_BAD_POTENTIAL, "NaN in potentials");
+    r->c0 = h.c0;
+    r->c1 = h.c1;
+    r->gamma0 = exact ? -INFINITY : h.c0 + 0.05;
+    r->gamma1 = exact ? INFINITY : h.c1 - 0.05;
+    r->kmeans_rounds = h.rounds;
+    // 2-3. classify, coarse ids / offsets, G_c
+    const int64_t nt = tl_ntiles(n);
+    int32_t last[4] = {0, 0, 0, 0};
+    std::vector<__int128> tiles((size_t)std::max<int64_t>(nt, 1));
+    std::vector<int32_t> tiles_n1((size_t)std::max<int64_t>(nt, 1), 0);
+    if (n > 0) {
+        if (c->kind == 0) tl_classify_stencil(stencil_args(c, true), n, xfull, r->gamma0, r->gamma1, c->F, b, st);
+        else tl_classify_sell(sell_args_full(c), xfull, r->gamma0, r->gamma1, c->F, b, st);
+        exclusive_scan_i32(b.flag, n, b.cid, b.scan_tmp, st, &launches);
+        exclusive_scan_i32(b.deg, n, b.eoff, b.scan_tmp, st, &launches);
+        launches += 1;
+        CK(cudaMemcpyAsync(&last[0], b.cid + n - 1, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&last[1], b.flag + n - 1, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&last[2], b.eoff + n - 1, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&last[3], b.deg + n - 1, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(tiles.data(), b.tile_a, sizeof(__int128) * nt, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(tiles_n1.data(), b.tile_n1, sizeof(int32_t) * nt, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    const int64_t nc = (int64_t)last[0] + last[1], E = (int64_t)last[2] + last[3];
+    if (E > INT32_MAX - 1) return fail(c, IRLS_ERR_INVALID_ARGUMENT, "coarse graph too large");
+    s = tl_reserve(c, E);
+    if (s) return s;
+    __int128 qst = qfix_host(c->c_st, c->F);
+    for (int64_t i = 0; i < nt && n > 0; i++) qst += tiles[i];
+    if (nc > 0) {
+        if (c->kind == 0) tl_fill_stencil(stencil_args(c, true), n, c->F, b, st);
+        else tl_fill_sell(sell_args_full(c), c->F, b, st);
+        launches++;
+    }
+    irls_status ls = last_launch(c, "two-level coarsening");
+    if (ls) return ls;
+    CK(cudaEventRecord(ev[1], st));
+    if (!c->h_cp.resize(nc + 1) || !c->h_ccol.resize(E) || !c->h_ccap.resize(E) || !c->h_cqs.resize(nc) ||
+        !c->h_cqt.resize(nc))
+        return fail(c, IRLS_ERR_OOM, "pinned coarse-graph buffers");
+    if (nc > 0) {
+        CK(cudaMemcpyAsync(c->h_cp.data(), b.cp, sizeof(int32_t) * nc, cudaMemcpyDeviceToHost, st));
+        if (E > 0) {
+            CK(cudaMemcpyAsync(c->h_ccol.data(), b.ccol, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(c->h_ccap.data(), b.ccap, sizeof(double) * E, cudaMemcpyDeviceToHost, st));
+        }
+        CK(cudaMemcpyAsync(c->h_cqs.data(), b.cqs, sizeof(__int128) * nc, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(c->h_cqt.data(), b.cqt, sizeof(__int128) * nc, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaEventRecord(ev[2], st));
+    CK(cudaStreamSynchronize(st));
+    c->h_cp[nc] = (int32_t)E;
+    c->h_qst = qst;
+    // 4. exact max-flow on G_c (host)
+    auto t0 = std::chrono::steady_clock::now();
+    HostBuf<__int128> qcap(E);
+    parallel_for(E, [&](int, int64_t a, int64_t b2) {
+        for (int64_t e = a; e < b2; e++) qcap[e] = qfix_host(c->h_ccap[e], c->F);
+    });
+    std::vector<uint8_t> src((size_t)std::max<int64_t>(nc, 1), 0);
+    int64_t stats[3] = {0, 0, 0};
+    __int128 flow = 0;
+    if (nc > 0) {
+        NvtxRange nvtx_mf("two_level: host max-flow");
+        flow = maxflow_bk((int32_t)nc, c->h_cp.data(), c->h_ccol.data(), qcap.data(), c->h_cqs.data(),
+                          c->h_cqt.data(), src.data(), stats);
+        if (stats[0] != 1) return fail(c, IRLS_ERR_CUDA, "coarse max-flow not certified (flow != cut)");
+    } else {
+        stats[0] = 1;
+    }
+    auto t1 = std::chrono::steady_clock::now();
+    r->ms_maxflow = (float)std::chrono::duration<double, std::milli>(t1 - t0).count();
+    r->certified = (int32_t)stats[0];
+    r->augmentations = stats[1];
+    r->coarse_flow = q_to_double(flow + qst, c->F);
+    // 5. lift + cut on G (C3)
+    CK(cudaEventRecord(ev[3], st));
+    if (nc > 0) CK(cudaMemcpyAsync(b.src, src.data(), nc, cudaMemcpyHostToDevice, st));
+    float ms_copy_back = 0.0f;
+    cudaEvent_t e4, e5;
+    CK(cudaEventCreate(&e4));
+    CK(cudaEventCreate(&e5));
+    CK(cudaEventRecord(e4, st));
+    tl_lift(b, st);
+    RedArgs ra;
+    ra.part = c->part;
+    ra.slots = c->slots_local;
+    ra.ctrl = c->ctrl;
+    ra.K = (int32_t)((n + kChunk - 1) / kChunk);
+    ra.g0 = 0;
+    ra.g1 = 8;
+    ra.n_fin = count_nonempty(ra.K, 0, 8);
+    SweepBuffers sb = c->sb;
+    sb.rank = b.prank;
+    sb.k_out = b.one;
+    sb.side = b.side;
+    if (n > 0) {
+        if (c->kind == 0) {
+            sweep_side_cross_stencil(stencil_args(c, true), n, sb, ra, st);
+        } else {
+            CK(cudaMemsetAsync(b.side, 0, c->n_total, st));
+            sweep_side_cross_sell(sell_args_full(c), c->orig_dev, c->n_total, sb, ra, st);
+            const uint8_t one = 1;
+            CK(cudaMemcpyAsync(b.side + c->s_id, &one, 1, cudaMemcpyHostToDevice, st));
+        }
+        launches += 2;
+    } else {
+        CK(cudaMemsetAsync(b.side, 0, c->n_total, st));
+        const uint8_t one = 1;
+        CK(cudaMemcpyAsync(b.side + (c->kind == 0 ? 0 : c->s_id), &one, 1, cudaMemcpyHostToDevice, st));
+    }
+    ls = last_launch(c, "two-level lift");
+    if (ls) return ls;
+    double slots[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (n > 0) CK(cudaMemcpyAsync(slots, c->slots_local, sizeof(slots), cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(e5, st));
+    if (side) CK(cudaMemcpyAsync(side, b.side, c->n_total, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    float ms_a = 0, ms_b = 0, ms_c = 0;
+    cudaEventElapsedTime(&ms_a, ev[0], ev[1]);
+    cudaEventElapsedTime(&ms_b, ev[1], ev[2]);
+    cudaEventElapsedTime(&ms_c, e4, e5);
+    cudaEventElapsedTime(&ms_copy_back, ev[3], e4);
+    cudaEventDestroy(e4);
+    cudaEventDestroy(e5);
+    r->ms_gpu = ms_a + ms_c;
+    r->ms_copy = ms_b + ms_copy_back;
+    int64_t n1 = 0;
+    for (int64_t i = 0; i < nt && n > 0; i++) n1 += tiles_n1[i];
+    const int64_t n0 = n - n1 - nc;
+    r->n0 = n0;
+    r->n1 = n1;
+    r->nc = nc;
+    r->coarse_nlinks = E / 2;
+    r->cut_value = (n > 0 ? irls_combine_slots(slots) : 0.0) + c->c_st;
+    c->tl_valid = true;
+    c->launches = launches;
+    r->ms_total = (float)std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+    return IRLS_OK;
+}
+
+struct TwoLevelMsg {
+    int64_t status;
+    irls_two_level_report rep;
+};
+
+extern "C" irls_status irls_two_level_cut(irls_ctx *c, uint8_t *side, irls_two_level_report *rep)
+{
+    NvtxRange nvtx_("irls_two_level_cut");
+    GUARD(c);
+    if (c->state == 0) return fail(c, IRLS_ERR_STATE, "two-level rounding before solve");
+    double *xfull = nullptr;
+    irls_status s = gather_x(c, &xfull);
+    if (s) return s;
+    TwoLevelMsg msg;
+    memset(&msg, 0, sizeof(msg));
+    if (c->rank == 0) {
+        s = two_level_rank0(c, xfull, side, &msg.rep);
+        msg.status = s;
+        if (s && !c->multi) return s;
+    }
+    if (c->multi) {
+        void *dmsg = nullptr;
+        CK(cudaMallocAsync(&dmsg, sizeof(msg), c->stream));
+        if (c->rank == 0) CK(cudaMemcpyAsync(dmsg, &msg, sizeof(msg), cudaMemcpyHostToDevice, c->stream));
+        NK(ncclBroadcast(dmsg, dmsg, sizeof(msg), ncclUint8, 0, c->nccl, c->stream));
+        CK(cudaMemcpyAsync(&msg, dmsg, sizeof(msg), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaFreeAsync(dmsg, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    }
+    if (msg.status) return fail(c, (irls_status)msg.status, c->rank == 0 ? c->err : "two-level failed on rank 0");
+    if (rep) *rep = msg.rep;
+    return IRLS_OK;
+}
+
+extern "C" irls_status irls_exact_min_cut(irls_ctx *c, uint8_t *side, irls_two_level_report *rep)
+{
+    NvtxRange nvtx_("irls_exact_min_cut");
+    GUARD(c);
+    if (c->world > 1) return fail(c, IRLS_ERR_INVALID_ARGUMENT, "irls_exact_min_cut is single-process");
+    irls_two_level_report r;
+    irls_status s = two_level_rank0(c, c->x, side, &r, true);
+    if (s) return s;
+    if (rep) *rep = r;
+    return IRLS_OK;
+}
+
+extern "C" irls_status irls_vgroup_two_level_cut(irls_vgroup *g, uint8_t *side, irls_two_level_report *rep)
+{
+    if (!g) return IRLS_ERR_INVALID_ARGUMENT;
+    irls_ctx *c = g->ranks[0];
+    GUARD(c);
+    if (c->state == 0) return fail(c, IRLS_ERR_STATE, "two-level rounding before solve");
+    double *full = nullptr;
+    irls_status s = vgather_x(g, &full);
+    if (s) return s;
+    irls_two_level_report r;
+    s = two_level_rank0(c, full, side, &r);
+    if (s) return s;
+    if (rep) *rep = r;
+    return IRLS_OK;
+}
+
+static void put_words(uint64_t *w, __int128 v)
+{
+    w[0] = (uint64_t)v;
+    w[1] = (uint64_t)((unsigned __int128)v >> 64);
+}
+static __int128 get_words(const uint64_t *w) { return (__int128)(((unsigned __int128)w[1] << 64) | w[0]); }
+
+extern "C" irls_status irls_two_level_get_coarse(irls_ctx *c, int8_t *cls, int32_t *ptr, int32_t *col, double *cap,
+                                                 uint64_t *qs, uint64_t *qt, uint64_t *qst)
+{
+    GUARD(c);
+    if (!c->tl_valid) return fail(c, IRLS_ERR_STATE, "no two-level result");
+    const int64_t nc = (int64_t)c->h_cp.size() - 1, E = c->h_cp[nc];
+    if (cls && c->n_glob > 0) CK(memcpy_sync(c, cls, c->tl.cls, c->n_glob, cudaMemcpyDeviceToHost));
+    if (ptr) memcpy(ptr, c->h_cp.data(), sizeof(int32_t) * (nc + 1));
+    if (col && E) memcpy(col, c->h_ccol.data(), sizeof(int32_t) * E);
+    if (cap && E) memcpy(cap, c->h_ccap.data(), sizeof(double) * E);
+    for (int64_t i = 0; i < nc; i++) {
+        if (qs) put_words(qs + 2 * i, c->h_cqs[i]);
+        if (qt) put_words(qt + 2 * i, c->h_cqt[i]);
+    }
+    if (qst) put_words(qst, c->h_qst);
+    return IRLS_OK;
+}
+
+extern "C" irls_status irls_coarse_maxflow(int32_t nc, const int32_t *ptr, const int32_t *col, const uint64_t *cap,
+                                           const uint64_t *qs, const uint64_t *qt, uint8_t *src, uint64_t *flow,
+                                           int32_t *certified)
+{
+    if (nc < 0 || (nc > 0 && (!ptr || !qs || !qt || !src)) || !flow) return IRLS_ERR_INVALID_ARGUMENT;
+    if (nc == 0) {
+        put_words(flow, 0);
+        if (certified) *certified = 1;
+        return IRLS_OK;
+    }
+    const int32_t E = ptr[nc];
+    std::vector<__int128> qc(E), a(nc), b(nc);
+    for (int32_t e = 0; e < E; e++) qc[e] = get_words(cap + 2 * e);
+    for (int32_t u = 0; u < nc; u++) {
+        a[u] = get_words(qs + 2 * u);
+        b[u] = get_words(qt + 2 * u);
+    }
+    int64_t stats[3] = {0, 0, 0};
+    __int128 f = maxflow_bk(nc, ptr, col, qc.data(), a.data(), b.data(), src, stats);
+    if (stats[0] < 0) return IRLS_ERR_INVALID_ARGUMENT;
+    put_words(flow, f);
+    if (certified) *certified = (int32_t)stats[0];
+    return IRLS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Cheeger-type diagnostic lambda_2 (A30)
+// ---------------------------------------------------------------------------
+extern "C" irls_status irls_lambda2(irls_ctx *c, double cg_rtol, int32_t cg_max_iter, int32_t cg_norm, double *x_out,
+                                    irls_lambda2_report *rep)
+{
+    NvtxRange nvtx_("irls_lambda2");
+    GUARD(c);
+    if (c->world > 1) return fail(c, IRLS_ERR_INVALID_ARGUMENT, "irls_lambda2 is single-process");
+    if (!(cg_rtol >= 0.0) || cg_max_iter < 0 || (cg_norm != 0 && cg_norm != 1))
+        return fail(c, IRLS_ERR_INVALID_ARGUMENT, "lambda2 CG options");
+    cudaStream_t st = c->stream;
+    const int64_t n = c->n_own;
+    if (n == 0) {  // only s and t: x = (1, -1), x^T L x = 4 c_st, C = 2 c_st
+        if (rep) {
+            memset(rep, 0, sizeof(*rep));
+            rep->xLx = 4.0 * c->c_st;
+            rep->C = 2.0 * c->c_st;
+            rep->lambda2 = rep->xLx / (2.0 * rep->C);
+            rep->converged = 1;
+        }
+        return IRLS_OK;
+    }
+    double *xs = dalloc<double>(c, n);
+    if (!xs) return fail(c, IRLS_ERR_OOM, "lambda2 x save");
+    CK(cudaMemcpyAsync(xs, c->x, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    const int state0 = c->state;
+    const int64_t iters0 = c->last_cg_iters;
+    // the CG options live in the control block: set, solve, restore
+    DevCtrl *d = c->ctrl;
+    auto set_opts = [&](double rt, int32_t mi, int32_t nm) -> cudaError_t {
+        cudaError_t e = cudaMemcpyAsync(&d->rtol, &rt, sizeof(double), cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&d->max_iter, &mi, sizeof(int32_t), cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&d->norm, &nm, sizeof(int32_t), cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        return e;
+    };
+    CK(set_opts(cg_rtol, cg_max_iter, cg_norm));
+    irls_step_report sr;
+    int64_t total = 0;
+    Ranks R{c};
+    irls_status s = run_solves(R, ASM_LAMBDA2, ASM_LAMBDA2, 1, &sr, &total);
+    const int64_t launches = c->launches;
+    if (!s) {
+        RedArgs ra;
+        ra.part = c->part;
+        ra.slots = c->slots_local;
+        ra.ctrl = c->ctrl;
+        ra.K = c->K;
+        ra.g0 = 0;
+        ra.g1 = 8;
+        ra.n_fin = count_nonempty(ra.K, 0, 8);
+        if (c->kind == 0) launch_l2_quad_stencil(stencil_args(c, true), n, c->x, ra, st);
+        else launch_l2_quad_sell(sell_args_full(c), c->x, ra, st);
+        s = last_launch(c, "lambda2 quadratic form");
+    }
+    double slots[2 * kGroups];
+    memset(slots, 0, sizeof(slots));
+    if (!s && n > 0) CK(memcpy_sync(c, slots, c->slots_local, sizeof(slots), cudaMemcpyDeviceToHost));
+    if (!s && x_out && n > 0) CK(memcpy_sync(c, x_out, c->x, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpyAsync(c->x, xs, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    CK(set_opts(c->opt.cg_rtol, c->opt.cg_max_iter, c->opt.cg_norm));
+    CK(dfree(c, xs));
+    CK(cudaStreamSynchronize(st));
+    c->state = state0;
+    c->last_cg_iters = iters0;
+    if (s) return s;
+    const double xLx = irls_combine_slots(slots) + 4.0 * c->c_st;
+    const double C = 2.0 * (irls_combine_slots(slots + kGroups) + c->c_st);
+    if (rep) {
+        rep->lambda2 = xLx / (2.0 * C);
+        rep->xLx = xLx;
+        rep->C = C;
+        rep->rel_res = sr.rel_res;
+        rep->cg_iters = sr.cg_iters;
+        rep->converged = sr.converged;
+        rep->ms = sr.ms;
+        rep->launches = (int32_t)(launches + 1);
+    }
+    return IRLS_OK;
+}
+
