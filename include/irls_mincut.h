@@ -60,7 +60,7 @@ typedef enum {
     IRLS_ERR_BAD_POTENTIAL = 7,      /* NaN in x at the sweep */
     IRLS_ERR_STATE = 8,              /* wrong call order, or poisoned context */
     IRLS_ERR_CUDA = 9,
-    IRLS_ERR_NCCL = 10,
+    IRLS_ERR_NCCL = 10,              /* an NCCL call or a peer-memory collective (p2p wait timeout) failed */
     IRLS_ERR_OOM = 11
 } irls_status;
 
@@ -86,7 +86,17 @@ typedef struct {
                                  CG iteration (x unchanged), the remaining steps repeat it bit for bit and are
                                  skipped on the device (their reports are copies).  x^(T) and the reports are
                                  identical to running every step; default 0 (every step executed). */
-    int32_t reserved;
+    int32_t p2p;         /* multi-rank contexts (world > 1, or world 1 with an NCCL id): 1 = the per-iteration
+                            collectives go over peer memory, fused into the kernels that produce their data
+                            (DESIGN.md §6): each group owner stores its C3 slot sums straight into every
+                            rank's slot buffer and bumps an arrival counter that the finalize kernel waits
+                            on (no slot allreduce), and on z-slabs K5 also stores z's boundary planes into
+                            the neighbours' ghost planes (no per-iteration halo exchange).  Peer buffers
+                            are exchanged at create with CUDA IPC handles over NCCL (allocated with
+                            cudaMalloc, outside device_alloc); virtual groups use the other ranks' buffers
+                            directly.  Results are bit-identical to p2p = 0.  A wait longer than 10 s
+                            ends the solve with IRLS_ERR_NCCL.  Ignored on a single-rank context.
+                            Default 0 (NCCL). */
 } irls_options;
 
 void irls_options_default(irls_options *opt);

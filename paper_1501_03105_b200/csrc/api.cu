@@ -34,7 +34,7 @@ extern "C" void irls_options_default(irls_options *o)
     o->record_trace = 0;
     o->loop_mode = IRLS_LOOP_GRAPH;
     o->fixed_point_exit = 0;
-    o->reserved = 0;
+    o->p2p = 0;
 }
 
 extern "C" const char *irls_status_string(irls_status st)
@@ -251,7 +251,7 @@ static irls_status coll_halo(Ranks &R, bool z_not_x, cudaStream_t st)
 static irls_status coll_allreduce(Ranks &R, int nq, cudaStream_t st)
 {
     irls_ctx *c = R[0];
-    if (!c->multi) return IRLS_OK;
+    if (!c->multi || c->p2p) return IRLS_OK;  // p2p: the producers already stored every slot
     if (!c->vg) return allreduce_slots(c, nq, st);
     // sum of every rank's slots in rank order (each slot has one non-zero
     // contributor, so this is the same exact value NCCL's sum produces)
@@ -281,13 +281,35 @@ static irls_status coll_minmax(Ranks &R, cudaStream_t st)
 // ---------------------------------------------------------------------------
 // enqueue pieces of one solve (over the ranks this thread drives)
 // ---------------------------------------------------------------------------
+// The p2p consumer side of one rank (an inactive wait when p2p is off).
+static P2PWait p2p_wait_args(const irls_ctx *c)
+{
+    P2PWait pw;
+    pw.buf = c->p2p ? c->p2p_buf : nullptr;
+    pw.cnt = c->p2p ? (const unsigned long long *)(c->p2p_buf + 2 * kMaxQ * kGroups) : nullptr;
+    pw.n_groups = c->n_groups_all;
+    return pw;
+}
+
+// RedArgs of the solve's reductions: with p2p the owner blocks push to peers.
+static RedArgs red_args_solve(const irls_ctx *c)
+{
+    RedArgs ra = red_args(c);
+    if (c->p2p) {
+        ra.pslots = c->d_pslots;
+        ra.pcnt = c->d_pcnt;
+        ra.world = c->world;
+    }
+    return ra;
+}
+
 static irls_status enq_assemble(Ranks &R, int mode, const CondArgs &cd, cudaStream_t st)
 {
     irls_status s;
     if (mode != ASM_INIT && mode != ASM_LAMBDA2 && (s = coll_halo(R, false, st))) return s;
     for (irls_ctx *c : R) {
         const VecArgs v = vec_args(c);
-        const RedArgs ra = red_args(c);
+        const RedArgs ra = red_args_solve(c);
         if (c->kind == 0)
             c->launches += launch_stencil_assemble_ex(stencil_args(c, false), v, ra, cd, mode, c->opt.eps, c->gs_diag,
                                                       c->gt_diag, st);
@@ -297,7 +319,7 @@ static irls_status enq_assemble(Ranks &R, int mode, const CondArgs &cd, cudaStre
     if (R[0]->multi) {
         if ((s = coll_allreduce(R, 5, st))) return s;
         for (irls_ctx *c : R) {
-            launch_finalize(PH_START, c->ctrl, c->slots_glob, cd, st);
+            launch_finalize(PH_START, c->ctrl, c->slots_glob, cd, p2p_wait_args(c), st);
             c->launches++;
         }
         if ((s = coll_halo(R, true, st))) return s;
@@ -310,7 +332,7 @@ static irls_status enq_body(Ranks &R, const CondArgs &cd, cudaStream_t st)
     irls_status s;
     for (irls_ctx *c : R) {
         const VecArgs v = vec_args(c);
-        const RedArgs ra = red_args(c);
+        const RedArgs ra = red_args_solve(c);
         if (c->kind == 0) launch_stencil_pspmv(stencil_args(c, false), v, ra, cd, st);
         else launch_sell_pspmv(sell_args(c), v, ra, cd, st);
         c->launches++;
@@ -325,21 +347,27 @@ static irls_status enq_body(Ranks &R, const CondArgs &cd, cudaStream_t st)
     if (R[0]->multi) {
         if ((s = coll_allreduce(R, 1, st))) return s;
         for (irls_ctx *c : R) {
-            launch_finalize(PH_PQ, c->ctrl, c->slots_glob, cd, st);
+            launch_finalize(PH_PQ, c->ctrl, c->slots_glob, cd, p2p_wait_args(c), st);
             c->launches++;
         }
     }
     for (irls_ctx *c : R) {
-        launch_axpy_jacobi(vec_args(c), red_args(c), cd, st);
+        VecArgs v = vec_args(c);
+        if (c->p2p && c->kind == 0) {  // the z halo fused into K5 (peer stores)
+            v.zpeer_lo = c->zpeer_lo;
+            v.zpeer_hi = c->zpeer_hi;
+            v.plane = c->P;
+        }
+        launch_axpy_jacobi(v, red_args_solve(c), cd, st);
         c->launches++;
     }
     if (R[0]->multi) {
         if ((s = coll_allreduce(R, 3, st))) return s;
         for (irls_ctx *c : R) {
-            launch_finalize(PH_RZ, c->ctrl, c->slots_glob, cd, st);
+            launch_finalize(PH_RZ, c->ctrl, c->slots_glob, cd, p2p_wait_args(c), st);
             c->launches++;
         }
-        if ((s = coll_halo(R, true, st))) return s;
+        if (!(R[0]->p2p && R[0]->kind == 0) && (s = coll_halo(R, true, st))) return s;
     }
     return last_launch(R[0], "cg body");
 }
@@ -365,7 +393,7 @@ static irls_status enq_tail(Ranks &R, int mode, cudaStream_t st, bool finish = t
         if (R[0]->multi && (s = coll_halo(R, false, st))) return s;
         for (irls_ctx *c : R) {
             const VecArgs v = vec_args(c);
-            const RedArgs ra = red_args(c);
+            const RedArgs ra = red_args_solve(c);
             if (c->kind == 0)
                 launch_stencil_diag_ex(stencil_args(c, false), v, ra, c->opt.eps, c->opt.cg_norm, c->gs_diag,
                                        c->gt_diag, st);
@@ -375,7 +403,7 @@ static irls_status enq_tail(Ranks &R, int mode, cudaStream_t st, bool finish = t
         if (R[0]->multi && (s = coll_allreduce(R, 4, st))) return s;
         if ((s = coll_minmax(R, st))) return s;
         for (irls_ctx *c : R) {
-            launch_diag_finalize(c->ctrl, c->slots_glob, c->reports, c->opt.cg_norm, st);
+            launch_diag_finalize(c->ctrl, c->slots_glob, c->reports, c->opt.cg_norm, p2p_wait_args(c), st);
             c->launches += 2;
         }
     }
@@ -706,7 +734,10 @@ irls_status run_solves(Ranks &R, int mode0, int mode_rest, int count, irls_step_
             }
             tot += h[i].cg_iters;
             if (reps) copy_report(h[i], reps + i, ms);
-            if (h[i].status != 0 && !s) s = fail(c, (irls_status)h[i].status, "CG breakdown (p'Ap <= 0 or non-finite scalar)");
+            if (h[i].status != 0 && !s)
+                s = fail(c, (irls_status)h[i].status,
+                         h[i].status == ST_P2P_TIMEOUT ? "peer-memory collective: wait timed out (10 s)"
+                                                       : "CG breakdown (p'Ap <= 0 or non-finite scalar)");
         }
         if (c->graph_iters_pending) c->launches += c->gl_body * tot;
         c->graph_iters_pending = false;
@@ -970,6 +1001,8 @@ extern "C" void irls_mincut_destroy(irls_ctx *c)
         if (g) cudaGraphExecDestroy(g);
     for (void *p : std::vector<void *>(c->allocs)) dfree(c, p);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    for (void *p : c->ipc_open) cudaIpcCloseMemHandle(p);
+    for (void *p : c->raw_allocs) cudaFree(p);
     if (c->h_done) cudaFreeHost(c->h_done);
     if (c->nccl) ncclCommDestroy(c->nccl);
     if (c->side_stream) cudaStreamDestroy(c->side_stream);
@@ -1034,6 +1067,26 @@ static irls_status vgroup_create(irls_vgroup **out, int32_t world, int32_t devic
         cudaMemcpy(g->src_ctrl, ctl.data(), sizeof(DevCtrl *) * world, cudaMemcpyHostToDevice) != cudaSuccess) {
         irls_vgroup_destroy(g);
         return IRLS_ERR_CUDA;
+    }
+    if (g->ranks[0]->p2p) {  // peer memory = the other ranks' buffers on this device
+        std::vector<double *> bufs(world);
+        for (int r = 0; r < world; r++) bufs[r] = g->ranks[r]->p2p_buf;
+        for (int r = 0; r < world; r++) {
+            irls_ctx *c = g->ranks[r];
+            irls_status s = p2p_set_peers(c, bufs);
+            if (s) {
+                irls_vgroup_destroy(g);
+                return s;
+            }
+            if (c->kind == 0 && c->hplan.peer_lo >= 0) {
+                irls_ctx *o = g->ranks[c->hplan.peer_lo];
+                c->zpeer_lo = o->z + o->hplan.recv_hi;
+            }
+            if (c->kind == 0 && c->hplan.peer_hi >= 0) {
+                irls_ctx *o = g->ranks[c->hplan.peer_hi];
+                c->zpeer_hi = o->z + o->hplan.recv_lo;
+            }
+        }
     }
     *out = g;
     return IRLS_OK;

@@ -35,6 +35,7 @@ static irls_status common_setup(irls_ctx *c, const irls_comm_desc *comm, const i
     // world 1 with an NCCL id: the multi-rank code path over a 1-rank
     // communicator (host loop, slot allreduce, finalize kernels, broadcasts)
     c->multi = c->world > 1 || c->vg != nullptr || (comm && comm->nccl_unique_id != nullptr);
+    c->p2p = c->multi && opt->p2p != 0;
     CK(cudaSetDevice(c->device));
     if (comm && comm->cuda_stream) {
         c->stream = (cudaStream_t)comm->cuda_stream;
@@ -54,13 +55,34 @@ static irls_status alloc_solver(irls_ctx *c, int64_t ghost)
 {
     const int64_t npad = (int64_t)c->nchunks * kChunk;
     const int64_t gpad = (ghost + 1) & ~(int64_t)1;  // keep the owned start 16-byte aligned
-    auto ghosted = [&](double *&ptr) -> bool {
-        double *b = dalloc<double>(c, npad + 2 * gpad);
+    // multi-process p2p: buffers that peers open through CUDA IPC come from
+    // cudaMalloc (pool and caller-allocator memory cannot be exported)
+    const bool ipc = c->p2p && !c->vg;
+    auto raw = [&](int64_t count) -> double * {
+        void *p = nullptr;
+        if (cudaMalloc(&p, sizeof(double) * (size_t)std::max<int64_t>(count, 1)) != cudaSuccess) return nullptr;
+        c->raw_allocs.push_back(p);
+        return (double *)p;
+    };
+    auto ghosted = [&](double *&ptr, bool export_) -> bool {
+        double *b = export_ ? raw(npad + 2 * gpad) : dalloc<double>(c, npad + 2 * gpad);
         if (!b) return false;
         ptr = b + gpad;
+        if (export_) c->z_base = b;
         return true;
     };
-    if (!ghosted(c->x) || !ghosted(c->z) || !ghosted(c->p0) || !ghosted(c->p1)) return IRLS_ERR_OOM;
+    if (!ghosted(c->x, false) || !ghosted(c->z, ipc && c->kind == 0) || !ghosted(c->p0, false) ||
+        !ghosted(c->p1, false))
+        return IRLS_ERR_OOM;
+    if (c->p2p) {
+        const int64_t nb = 2 * kMaxQ * kGroups + 1;  // slots by parity + the arrival counter
+        c->p2p_buf = ipc ? raw(nb) : dalloc<double>(c, nb);
+        c->d_pslots = (double **)dalloc<double *>(c, c->world);
+        c->d_pcnt = (unsigned long long **)dalloc<unsigned long long *>(c, c->world);
+        if (!c->p2p_buf || !c->d_pslots || !c->d_pcnt) return IRLS_ERR_OOM;
+        CK(cudaMemsetAsync(c->p2p_buf, 0, sizeof(double) * nb, c->stream));
+        c->n_groups_all = count_nonempty(c->K, 0, kGroups);
+    }
     c->D = dalloc<double>(c, npad);
     c->Dinv = dalloc<double>(c, npad);
     c->r = dalloc<double>(c, npad);
@@ -88,12 +110,83 @@ static irls_status alloc_solver(irls_ctx *c, int64_t ghost)
     return IRLS_OK;
 }
 
+// Every rank's p2p slot buffer / counter (and, on z-slabs, the neighbours'
+// z ghost planes) as device pointers usable by this rank's kernels.
+irls_status p2p_set_peers(irls_ctx *c, const std::vector<double *> &bufs)
+{
+    std::vector<unsigned long long *> cnt(bufs.size());
+    for (size_t w = 0; w < bufs.size(); w++) cnt[w] = (unsigned long long *)(bufs[w] + 2 * kMaxQ * kGroups);
+    CK(memcpy_sync(c, c->d_pslots, bufs.data(), sizeof(double *) * bufs.size(), cudaMemcpyHostToDevice));
+    CK(memcpy_sync(c, c->d_pcnt, cnt.data(), sizeof(unsigned long long *) * cnt.size(), cudaMemcpyHostToDevice));
+    return IRLS_OK;
+}
+
+// One rank's exported buffers, exchanged with an NCCL all-gather at create.
+struct PeerRec {
+    cudaIpcMemHandle_t hbuf, hz;
+    int64_t zoff_recv_lo, zoff_recv_hi;  // ghost planes, in doubles from z's allocation start
+};
+
+static irls_status p2p_exchange(irls_ctx *c)
+{
+    const int W = c->world;
+    PeerRec mine;
+    memset(&mine, 0, sizeof(mine));
+    CK(cudaIpcGetMemHandle(&mine.hbuf, c->p2p_buf));
+    if (c->kind == 0) {
+        CK(cudaIpcGetMemHandle(&mine.hz, c->z_base));
+        mine.zoff_recv_lo = (c->z - c->z_base) + c->hplan.recv_lo;
+        mine.zoff_recv_hi = (c->z - c->z_base) + c->hplan.recv_hi;
+    }
+    std::vector<PeerRec> all(W);
+    void *dev = nullptr;
+    CK(cudaMalloc(&dev, sizeof(PeerRec) * W));
+    char *slot = (char *)dev + sizeof(PeerRec) * c->rank;
+    cudaError_t e = cudaMemcpyAsync(slot, &mine, sizeof(mine), cudaMemcpyHostToDevice, c->stream);
+    ncclResult_t nr = e == cudaSuccess ? ncclAllGather(slot, dev, sizeof(PeerRec), ncclUint8, c->nccl, c->stream)
+                                       : ncclSuccess;
+    if (e == cudaSuccess && nr == ncclSuccess)
+        e = cudaMemcpyAsync(all.data(), dev, sizeof(PeerRec) * W, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    cudaFree(dev);
+    if (nr != ncclSuccess) return fail(c, IRLS_ERR_NCCL, std::string("p2p exchange: ") + ncclGetErrorString(nr));
+    CK(e);
+    auto open = [&](const cudaIpcMemHandle_t &h, double **out) -> irls_status {
+        void *p = nullptr;
+        cudaError_t oe = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+        if (oe != cudaSuccess) return fail(c, IRLS_ERR_CUDA, std::string("p2p: cudaIpcOpenMemHandle: ") +
+                                                                 cudaGetErrorString(oe));
+        c->ipc_open.push_back(p);
+        *out = (double *)p;
+        return IRLS_OK;
+    };
+    std::vector<double *> bufs(W);
+    irls_status s;
+    for (int w = 0; w < W; w++) {
+        if (w == c->rank) bufs[w] = c->p2p_buf;
+        else if ((s = open(all[w].hbuf, &bufs[w]))) return s;
+    }
+    if (c->kind == 0) {
+        double *b;
+        if (c->hplan.peer_lo >= 0) {
+            if ((s = open(all[c->hplan.peer_lo].hz, &b))) return s;
+            c->zpeer_lo = b + all[c->hplan.peer_lo].zoff_recv_hi;
+        }
+        if (c->hplan.peer_hi >= 0) {
+            if ((s = open(all[c->hplan.peer_hi].hz, &b))) return s;
+            c->zpeer_hi = b + all[c->hplan.peer_hi].zoff_recv_lo;
+        }
+    }
+    return p2p_set_peers(c, bufs);
+}
+
 static irls_status init_nccl(irls_ctx *c, const irls_comm_desc *comm)
 {
     if (!c->multi || c->vg) return IRLS_OK;
     ncclUniqueId id;
     memcpy(&id, comm->nccl_unique_id, sizeof(id));
     NK(ncclCommInitRank(&c->nccl, c->world, id, c->rank));
+    if (c->p2p) return p2p_exchange(c);
     return IRLS_OK;
 }
 

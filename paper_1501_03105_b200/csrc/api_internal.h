@@ -109,7 +109,7 @@ static inline irls_status check_opts(const irls_options *o)
     if (!o) return IRLS_ERR_INVALID_ARGUMENT;
     if (!(o->eps > 0.0) || isinf(o->eps) || o->T < 0 || !(o->cg_rtol >= 0.0) || o->cg_max_iter < 0 ||
         (o->cg_norm != 0 && o->cg_norm != 1) || (o->loop_mode < 0 || o->loop_mode > 2) ||
-        (o->fixed_point_exit != 0 && o->fixed_point_exit != 1))
+        (o->fixed_point_exit != 0 && o->fixed_point_exit != 1) || (o->p2p != 0 && o->p2p != 1))
         return IRLS_ERR_INVALID_ARGUMENT;
     return IRLS_OK;
 }
@@ -266,5 +266,6 @@ bool grid_nonsingular(int32_t nx, int32_t ny, int32_t nz, const double *cx, cons
 // api_round.cu
 irls_status sweep_rank0(irls_ctx *c, const double *xfull, uint8_t *side, int32_t *order, int64_t *k,
                         double *cut_value);
+irls_status p2p_set_peers(irls_ctx *c, const std::vector<double *> &bufs);
 irls_status two_level_rank0(irls_ctx *c, const double *xfull, uint8_t *side, irls_two_level_report *r,
                             bool exact = false);

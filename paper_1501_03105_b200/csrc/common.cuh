@@ -54,7 +54,7 @@ struct DevCtrl {
     unsigned fin_cnt;
     int32_t outer_left;  // IRLS steps left in a multi-step graph
     int32_t outer_end;   // report index one past its last step
-    int32_t pad2;
+    uint32_t red_seq;    // peer-memory collectives: reductions consumed so far (slot parity, arrival target)
     unsigned long long xmin_key, xmax_key;
     unsigned long long t_mark;  // %globaltimer (ns) at the start of a solve sequence
 };
@@ -76,6 +76,13 @@ struct RedArgs {
     int32_t K;           // global chunk count
     int32_t g0, g1;      // owned groups [g0, g1)
     int32_t n_fin;       // non-empty owned groups
+    // peer-memory slot collective (irls_options.p2p, world > 1; nullptr: local
+    // slots + an allreduce afterwards): the owner block of a group stores its
+    // sums straight into every rank's slot buffer (parity red_seq & 1) and
+    // bumps every rank's arrival counter
+    double *const *pslots = nullptr;            // [world] -> [2][kMaxQ][8]
+    unsigned long long *const *pcnt = nullptr;  // [world] -> arrival counter
+    int32_t world = 0;
 };
 
 // ---------------------------------------------------------------------------
@@ -178,8 +185,17 @@ __device__ bool c3_chunk_epilogue(double (&v)[NQ], int32_t chunk, const RedArgs 
     double gsum[NQ];
     c3_list_sum<NQ>(ra.part, ra.K, glo, ghi - glo, gsum, smem);
     if (threadIdx.x == 0) {
+        if (ra.pslots) {  // fused collective: push the group sum to every rank over peer memory
+            const int off = (int)(ra.ctrl->red_seq & 1u) * (kMaxQ * kGroups) + g;
+            for (int w = 0; w < ra.world; w++)
 #pragma unroll
-        for (int q = 0; q < NQ; q++) ra.slots[q * kGroups + g] = gsum[q];
+                for (int q = 0; q < NQ; q++) ra.pslots[w][off + q * kGroups] = gsum[q];
+            __threadfence_system();
+            for (int w = 0; w < ra.world; w++) atomicAdd_system(ra.pcnt[w], 1ull);
+        } else {
+#pragma unroll
+            for (int q = 0; q < NQ; q++) ra.slots[q * kGroups + g] = gsum[q];
+        }
         ra.ctrl->grp_cnt[g] = 0u;
         __threadfence();
         const unsigned prev = atomicAdd(&ra.ctrl->fin_cnt, 1u);
@@ -202,6 +218,44 @@ __device__ __forceinline__ double slot_total(const double *slots, int q)
 #pragma unroll
     for (int g = 0; g < kGroups; g++) s[g] = ldslot(slots, q, g);
     return tree8(s);
+}
+
+// Peer-memory slot collective, consumer side (one thread): wait until every
+// non-empty group of this reduction has arrived (counter >= (red_seq + 1) *
+// n_groups), consume it (red_seq + 1) and return its parity buffer.  A wait
+// longer than 10 s (a peer died or the ranks fell out of step) sets status
+// ST_P2P_TIMEOUT, ends the solve and returns nullptr.
+enum { ST_P2P_TIMEOUT = 10 };  // = IRLS_ERR_NCCL (a collective failed)
+struct P2PWait {
+    const double *buf;               // this rank's [2][kMaxQ][8] slot buffer (nullptr: not in use)
+    const unsigned long long *cnt;   // this rank's arrival counter
+    int32_t n_groups;                // non-empty groups over all ranks
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ inline const double *p2p_wait(DevCtrl *c, const P2PWait &pw)
+{
+    const unsigned long long target = ((unsigned long long)c->red_seq + 1ull) * (unsigned long long)pw.n_groups;
+    if (ld_acquire_sys(pw.cnt) < target) {
+        const unsigned long long t0 = global_ns();
+        while (ld_acquire_sys(pw.cnt) < target) {
+            if (global_ns() - t0 > 10000000000ull) {
+                c->status = ST_P2P_TIMEOUT;
+                c->done = 1;
+                return nullptr;
+            }
+            __nanosleep(64);
+        }
+    }
+    const double *slots = pw.buf + (c->red_seq & 1u) * (kMaxQ * kGroups);
+    c->red_seq = c->red_seq + 1u;
+    return slots;
 }
 
 // After assembly (phase START): quantities [rz, zz, rr, mbmb, bb].

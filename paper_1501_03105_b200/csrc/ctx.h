@@ -120,6 +120,17 @@ struct irls_ctx {
     double *x_full = nullptr;     // rank 0: gathered potentials
     void *msg_dev = nullptr;      // sweep result broadcast
 
+    // peer-memory collectives (irls_options.p2p on a multi-rank context)
+    bool p2p = false;
+    double *p2p_buf = nullptr;    // [2][kMaxQ][8] slot sums by parity, then one u64 arrival counter
+    double **d_pslots = nullptr;  // device [world]: every rank's p2p_buf
+    unsigned long long **d_pcnt = nullptr;  // device [world]: every rank's arrival counter
+    int32_t n_groups_all = 0;     // non-empty C3 groups over all ranks (arrivals per reduction)
+    double *zpeer_lo = nullptr, *zpeer_hi = nullptr;  // neighbours' z ghost planes (z-slabs)
+    double *z_base = nullptr;     // start of z's allocation (IPC export)
+    std::vector<void *> raw_allocs;  // cudaMalloc'd, IPC-exportable (multi-process p2p)
+    std::vector<void *> ipc_open;    // peers' allocations opened with cudaIpcOpenMemHandle
+
     // sweep
     irls::SweepBuffers sb{};
     int32_t *order_dev = nullptr;  // points into sb.vals / vals_alt after a sweep

@@ -23,6 +23,12 @@ struct VecArgs {
     double *z;           // ghost
     double *p0, *p1;     // ghost (ping-pong: iteration k reads p[k&1], writes p[(k+1)&1])
     const int32_t *frozen;  // DevCtrl::frozen: assembly kernels skip a step that repeats a fixed point
+    // K5 only, z-slabs with irls_options.p2p: the boundary planes of z are also
+    // stored into the neighbours' ghost planes over peer memory (the halo
+    // exchange fused into the kernel that produces z)
+    double *zpeer_lo = nullptr;  // lower neighbour's upper ghost plane <- my first owned plane
+    double *zpeer_hi = nullptr;  // upper neighbour's lower ghost plane <- my last owned plane
+    int64_t plane = 0;           // nx * ny
 };
 
 struct StencilArgs {
@@ -84,7 +90,8 @@ void launch_axpy_jacobi(const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
 // after the loop: x += alpha p_last (or x = 0 if b = 0)
 void launch_finish(const VecArgs &v, DevCtrl *ctrl, cudaStream_t st);
 // scalar finalizers for the multi-GPU path (after the slot allreduce)
-void launch_finalize(int phase, DevCtrl *ctrl, const double *slots, const CondArgs &cd, cudaStream_t st);
+void launch_finalize(int phase, DevCtrl *ctrl, const double *slots, const CondArgs &cd, const P2PWait &pw,
+                     cudaStream_t st);
 // write the step report from the control block
 struct DevReport {
     int32_t cg_iters, converged, status, pad;
@@ -107,7 +114,8 @@ void launch_stencil_diag_ex(const StencilArgs &s, const VecArgs &v, const RedArg
                             const double *gsv, const double *gtv, cudaStream_t st);
 void launch_sell_diag_ex(const SellArgs &s, const VecArgs &v, const RedArgs &ra, double eps, int norm,
                          const double *gsv, const double *gtv, cudaStream_t st);
-void launch_diag_finalize(DevCtrl *ctrl, const double *slots, DevReport *reports, int norm, cudaStream_t st);
+void launch_diag_finalize(DevCtrl *ctrl, const double *slots, DevReport *reports, int norm, const P2PWait &pw,
+                          cudaStream_t st);
 
 enum { PH_START = 0, PH_PQ = 1, PH_RZ = 2 };
 // virtual-group slot sum: dst[i] = sum_r src[r][i]

@@ -349,8 +349,19 @@ __global__ void __launch_bounds__(kThreads) k_finish(VecArgs v, const DevCtrl *c
     if (i < v.n_own) v.x[i] = zero ? 0.0 : v.x[i] + alpha * pl[i];
 }
 
-__global__ void k_finalize(int phase, DevCtrl *ctrl, const double *slots, CondArgs cd)
+__global__ void k_finalize(int phase, DevCtrl *ctrl, const double *slots, CondArgs cd, P2PWait pw)
 {
+    // phases whose producers did not run (as on one rank, where the skipped
+    // kernel's fused finalize is skipped with it): a fixed-point step's
+    // assembly, and K5 after a breakdown in the PQ phase
+    if ((phase == PH_START && ctrl->frozen) || (phase == PH_RZ && ctrl->done)) {
+        set_cond(cd, ctrl);
+        return;
+    }
+    if (pw.buf && !(slots = p2p_wait(ctrl, pw))) {
+        set_cond(cd, ctrl);
+        return;
+    }
     if (phase == PH_START) finalize_start(ctrl, slots);
     else if (phase == PH_PQ) finalize_pq(ctrl, slots);
     else finalize_rz(ctrl, slots);
@@ -481,9 +492,13 @@ __global__ void __launch_bounds__(kThreads) k_sell_diag(SellArgs s, VecArgs v, R
     c3_chunk_epilogue<4>(acc, v.chunk0 + (int32_t)blockIdx.x, ra);
 }
 
-__global__ void k_diag_finalize(DevCtrl *ctrl, const double *slots, DevReport *reports, int norm)
+__global__ void k_diag_finalize(DevCtrl *ctrl, const double *slots, DevReport *reports, int norm, P2PWait pw)
 {
     DevReport &R = reports[ctrl->step - 1];
+    if (pw.buf && !(slots = p2p_wait(ctrl, pw))) {
+        R.status = ctrl->status;
+        return;
+    }
     R.S_eps = slot_total(slots, 0);
     R.flow_value = slot_total(slots, 1);
     R.current_s = slot_total(slots, 2);
@@ -602,9 +617,10 @@ void launch_finish(const VecArgs &v, DevCtrl *ctrl, cudaStream_t st)
     launch_pair_finish(v, ctrl, st);
 }
 
-void launch_finalize(int phase, DevCtrl *ctrl, const double *slots, const CondArgs &cd, cudaStream_t st)
+void launch_finalize(int phase, DevCtrl *ctrl, const double *slots, const CondArgs &cd, const P2PWait &pw,
+                     cudaStream_t st)
 {
-    k_finalize<<<1, 1, 0, st>>>(phase, ctrl, slots, cd);
+    k_finalize<<<1, 1, 0, st>>>(phase, ctrl, slots, cd, pw);
 }
 
 __global__ void k_gate(const DevCtrl *ctrl, cudaGraphConditionalHandle h)
@@ -675,9 +691,10 @@ void launch_sell_diag_ex(const SellArgs &s, const VecArgs &v, const RedArgs &ra,
     k_sell_diag<<<nblocks(v.n_own), kThreads, 0, st>>>(s, v, ra, eps * eps, norm, gsv, gtv);
 }
 
-void launch_diag_finalize(DevCtrl *ctrl, const double *slots, DevReport *reports, int norm, cudaStream_t st)
+void launch_diag_finalize(DevCtrl *ctrl, const double *slots, DevReport *reports, int norm, const P2PWait &pw,
+                          cudaStream_t st)
 {
-    k_diag_finalize<<<1, 1, 0, st>>>(ctrl, slots, reports, norm);
+    k_diag_finalize<<<1, 1, 0, st>>>(ctrl, slots, reports, norm, pw);
 }
 
 }  // namespace irls

@@ -472,6 +472,7 @@ __global__ void __launch_bounds__(kThreads) k_pair_axpy(VecArgs v, RedArgs ra, C
     const double alpha = ctrl->alpha;
     const int64_t base = (int64_t)blockIdx.x * kChunk;
     double acc[3] = {0.0, 0.0, 0.0};
+    bool peer = false;
 #pragma unroll 2
     for (int j = 0; j < 8; j++) {
         const int64_t u0 = base + 2 * (int64_t)threadIdx.x + 512 * j;
@@ -481,6 +482,17 @@ __global__ void __launch_bounds__(kThreads) k_pair_axpy(VecArgs v, RedArgs ra, C
         const double z0 = r0 * d2.x, z1 = r1 * d2.y;
         stp(v.r, u0, make_double2(r0, r1));
         stp(v.z, u0, make_double2(z0, z1));
+        if (v.zpeer_lo && u0 < v.plane) {  // fused halo: first owned plane -> lower neighbour
+            v.zpeer_lo[u0] = z0;
+            if (u0 + 1 < v.plane) v.zpeer_lo[u0 + 1] = z1;
+            peer = true;
+        }
+        if (v.zpeer_hi && u0 + 1 >= v.n_own - v.plane) {  // last owned plane -> upper neighbour
+            const int64_t b = v.n_own - v.plane;
+            if (u0 >= b) v.zpeer_hi[u0 - b] = z0;
+            if (u0 + 1 < v.n_own) v.zpeer_hi[u0 + 1 - b] = z1;
+            peer = true;
+        }
         acc[0] = acc[0] + r0 * z0;
         acc[1] = acc[1] + z0 * z0;
         acc[2] = acc[2] + r0 * r0;
@@ -490,6 +502,9 @@ __global__ void __launch_bounds__(kThreads) k_pair_axpy(VecArgs v, RedArgs ra, C
             acc[2] = acc[2] + r1 * r1;
         }
     }
+    // the peer stores are visible system-wide before this block's partial
+    // (and so before the group's arrival at any peer) is published
+    if (peer) __threadfence_system();
     if (c3_chunk_epilogue<3>(acc, v.chunk0 + (int32_t)blockIdx.x, ra) && cd.finalize && threadIdx.x == 0) {
         finalize_rz(ctrl, ra.slots);
         set_cond2(cd, ctrl);

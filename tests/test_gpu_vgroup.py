@@ -3,6 +3,10 @@
 slot-exact allreduce, ghost p updates, finalize kernels and the rank-0 sweep.
 Only NCCL is replaced (by device copies).  The bar is bitwise equality with
 one rank and with the oracle: the contract makes the result independent of W.
+p2p=1 runs the peer-memory collectives instead (group owners store their
+slot sums into every rank's buffer + arrival counters the finalize kernels
+wait on; K5 stores z's boundary planes into the neighbours' ghost planes):
+the same bits again.
 """
 import numpy as np
 import pytest
@@ -30,14 +34,15 @@ def single(I, spec, opts, T):
     return m, reps, tot, sw
 
 
+@pytest.mark.parametrize("p2p", [0, 1])
 @pytest.mark.parametrize("world", [2, 4, 8])
-def test_vgroup_equals_single_and_oracle(irls, world):
+def test_vgroup_equals_single_and_oracle(irls, world, p2p):
     # 64x64x20: one chunk per plane, uneven slabs (2 or 3 planes per group)
     spec = gen.blob_grid(64, 64, 20, seed=5, sigma=(3.0, 10.0))
     T = 20
     opts = irls.options(T=T, record_trace=1)
     m, reps1, tot1, sw1 = single(irls, spec, opts, T)
-    g = irls.VGroup(spec, world, irls.options(T=T, record_trace=1))
+    g = irls.VGroup(spec, world, irls.options(T=T, record_trace=1, p2p=p2p))
     reps, tot = g.irls_vgroup_solve(irls.IRLS_FROM_SCRATCH, T=T)
     assert tot == tot1
     for a, b in zip(reps, reps1):
@@ -55,14 +60,15 @@ def test_vgroup_equals_single_and_oracle(irls, world):
     g.close()
 
 
+@pytest.mark.parametrize("p2p", [0, 1])
 @pytest.mark.parametrize("world", [2, 8])
-def test_vgroup_cold_and_sequence(irls, world):
+def test_vgroup_cold_and_sequence(irls, world, p2p):
     spec = gen.blob_grid(64, 64, 16, seed=2, sigma=(3.0, 8.0))
     T = 8
     for warm in (0, 1):
         opts = irls.options(T=T, warm_start=warm)
         m = irls.MinCut.from_spec(spec, opts)
-        g = irls.VGroup(spec, world, irls.options(T=T, warm_start=warm))
+        g = irls.VGroup(spec, world, irls.options(T=T, warm_start=warm, p2p=p2p))
         _, t1 = m.irls_solve(irls.IRLS_FROM_SCRATCH, T=T)
         _, t2 = g.irls_vgroup_solve(irls.IRLS_FROM_SCRATCH, T=T)
         assert t1 == t2
@@ -78,14 +84,15 @@ def test_vgroup_cold_and_sequence(irls, world):
         g.close()
 
 
+@pytest.mark.parametrize("p2p", [0, 1])
 @pytest.mark.parametrize("world", [2, 4, 8])
-def test_vgroup_fused_rows_of_512(irls, world):
+def test_vgroup_fused_rows_of_512(irls, world, p2p):
     """512-wide rows (fused reweight kernel incl. the ghost -z slot), one
     chunk per plane, 16 planes: bitwise equal to one rank."""
     spec = gen.blob_grid(512, 8, 16, seed=8, sigma=(3.0, 8.0))
     T = 10
     m, reps1, tot1, sw1 = single(irls, spec, irls.options(T=T), T)
-    g = irls.VGroup(spec, world, irls.options(T=T))
+    g = irls.VGroup(spec, world, irls.options(T=T, p2p=p2p))
     reps, tot = g.irls_vgroup_solve(irls.IRLS_FROM_SCRATCH, T=T)
     assert [r["cg_iters"] for r in reps] == [r["cg_iters"] for r in reps1]
     assert np.array_equal(g.irls_vgroup_get_potentials(), m.irls_get_potentials())
@@ -93,12 +100,13 @@ def test_vgroup_fused_rows_of_512(irls, world):
 
 
 @pytest.mark.slow
-def test_vgroup_config2_world8(irls):
+@pytest.mark.parametrize("p2p", [0, 1])
+def test_vgroup_config2_world8(irls, p2p):
     """BASELINE config 2 (128^3), 8 virtual ranks of 16 planes each."""
     spec = gen.config2()
     opts = irls.options(T=50)
     m, reps1, tot1, sw1 = single(irls, spec, opts, 50)
-    g = irls.VGroup(spec, 8, irls.options(T=50))
+    g = irls.VGroup(spec, 8, irls.options(T=50, p2p=p2p))
     reps, tot = g.irls_vgroup_solve(irls.IRLS_FROM_SCRATCH, T=50)
     assert [r["cg_iters"] for r in reps] == [r["cg_iters"] for r in reps1]
     assert np.array_equal(g.irls_vgroup_get_potentials(), m.irls_get_potentials())
@@ -113,8 +121,9 @@ def test_vgroup_rejects_unaligned(irls):
         irls.VGroup(spec, 2)
 
 
+@pytest.mark.parametrize("p2p", [0, 1])
 @pytest.mark.parametrize("loop_mode", [1, 2])
-def test_nccl_one_rank_communicator(irls, loop_mode):
+def test_nccl_one_rank_communicator(irls, loop_mode, p2p):
     """The NCCL code path on one GPU: world_size 1 with an NCCL id runs the
     multi-rank host loop, ncclAllReduce of the slots, the finalize kernels,
     the gather and the ncclBroadcast of the sweep / two-level results over a
@@ -124,7 +133,7 @@ def test_nccl_one_rank_communicator(irls, loop_mode):
     T = 12
     m, reps1, tot1, sw1 = single(irls, spec, irls.options(T=T, record_trace=1), T)
     comm = irls.comm_desc(1, 0, 0, irls.irls_nccl_unique_id(), torch.cuda.current_stream().cuda_stream)
-    g = irls.MinCut.from_spec(spec, irls.options(T=T, record_trace=1, loop_mode=loop_mode), comm)
+    g = irls.MinCut.from_spec(spec, irls.options(T=T, record_trace=1, loop_mode=loop_mode, p2p=p2p), comm)
     reps, tot = g.irls_solve(irls.IRLS_FROM_SCRATCH, T=T)
     assert tot == tot1
     for a, b in zip(reps, reps1):
@@ -141,7 +150,7 @@ def test_nccl_one_rank_communicator(irls, loop_mode):
     spec = gen.road_graph(120, seed=2, knn=50)
     m, reps1, tot1, sw1 = single(irls, spec, irls.options(T=T), T)
     comm = irls.comm_desc(1, 0, 0, irls.irls_nccl_unique_id(), torch.cuda.current_stream().cuda_stream)  # one id per comm
-    g = irls.MinCut.from_spec(spec, irls.options(T=T, loop_mode=loop_mode), comm)
+    g = irls.MinCut.from_spec(spec, irls.options(T=T, loop_mode=loop_mode, p2p=p2p), comm)
     _, tot = g.irls_solve(irls.IRLS_FROM_SCRATCH, T=T)
     assert tot == tot1 and np.array_equal(g.irls_get_potentials(), m.irls_get_potentials())
     side, _, k, cut = g.irls_sweep_cut()
@@ -149,8 +158,9 @@ def test_nccl_one_rank_communicator(irls, loop_mode):
     g.close()
 
 
+@pytest.mark.parametrize("p2p", [0, 1])
 @pytest.mark.parametrize("world", [2, 4, 8])
-def test_vgroup_csr_strips(irls, world):
+def test_vgroup_csr_strips(irls, world, p2p):
     """CSR id strips (SURVEY §8(e), config 3's partition): every rank's rows
     with a ghost block refreshed by the halo (packed send lists), per-rank C3
     groups, slot allreduce, ghost p update, gather and the rank-0 sweep and
@@ -158,7 +168,7 @@ def test_vgroup_csr_strips(irls, world):
     spec = gen.road_graph(200, seed=2, knn=60)  # 39,469 non-terminals: 9.6 chunks, ragged strips
     T = 12
     m, reps1, tot1, sw1 = single(irls, spec, irls.options(T=T, record_trace=1), T)
-    g = irls.VGroup(spec, world, irls.options(T=T, record_trace=1))
+    g = irls.VGroup(spec, world, irls.options(T=T, record_trace=1, p2p=p2p))
     reps, tot = g.irls_vgroup_solve(irls.IRLS_FROM_SCRATCH, T=T)
     assert tot == tot1
     for a, b in zip(reps, reps1):
@@ -206,3 +216,31 @@ def test_vgroup_csr_rejects_too_few_chunks(irls):
     spec = gen.road_graph(60, seed=2, knn=40)  # < 8 chunks
     with pytest.raises(irls.IrlsError):
         irls.VGroup(spec, 2)
+
+
+@pytest.mark.parametrize("p2p", [0, 1])
+@pytest.mark.parametrize("world", [2, 4])
+def test_vgroup_fixed_point_exit(irls, world, p2p):
+    """fixed_point_exit on W ranks (host loop): a frozen step skips its
+    assembly on every rank and its START finalize with it (no producer ran,
+    so with p2p there is nothing to wait for); reports and x^(T) equal one
+    rank with the same option and one rank without it."""
+    spec = gen.blob_grid(64, 64, 16, seed=9, sigma=(3.0, 8.0))
+    T = 40
+    m, reps1, tot1, _ = single(irls, spec, irls.options(T=T), T)
+    mf, repsf, totf, _ = single(irls, spec, irls.options(T=T, fixed_point_exit=1), T)
+    assert totf == tot1
+    assert any(r["cg_iters"] == 0 for r in reps1[1:]), "case must reach a fixed point"
+    g = irls.VGroup(spec, world, irls.options(T=T, fixed_point_exit=1, p2p=p2p))
+    reps, tot = g.irls_vgroup_solve(irls.IRLS_FROM_SCRATCH, T=T)
+    assert tot == tot1
+    assert [r["cg_iters"] for r in reps] == [r["cg_iters"] for r in reps1]
+    assert [r["rel_res"] for r in reps] == [r["rel_res"] for r in repsf]
+    assert np.array_equal(g.irls_vgroup_get_potentials(), m.irls_get_potentials())
+    g.close()
+
+
+def test_vgroup_p2p_rejects_bad_flag(irls):
+    spec = gen.blob_grid(64, 64, 16, seed=9)
+    with pytest.raises(irls.IrlsError):
+        irls.VGroup(spec, 2, irls.options(p2p=2))
