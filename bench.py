@@ -333,6 +333,23 @@ def main():
                                  "bytes_per_node": K1_BYTES_PER_NODE},
     }
     cg_iter_ms = t_k3 + t_k5
+    # ---- N > 1: the z halo against the NVLink roofline (the bytes each rank
+    # sends per CG iteration over the measured 770 GB/s per-direction peer
+    # bandwidth of B200_PROFILING.md; 900 GB/s nominal)
+    nvlink = None
+    if world > 1:
+        t_halo = max_over_ranks(m.irls_time_kernel(I.KERNEL_HALO, 20))
+        if not csr:
+            h = I.irls_halo_plan(spec["nx"], spec["ny"], spec["nz"], world, rank)
+            sent = max_over_ranks(8.0 * h["count"] * ((h["peer_lo"] >= 0) + (h["peer_hi"] >= 0)))
+            nv_ach = sent / (t_halo * 1e-3) / 1e9
+            nvlink = {"bound": "nvlink", "achieved": nv_ach, "peak": 770.0, "unit": "GB/s", "frac": nv_ach / 770.0,
+                      "bytes_per_cg_iter_per_rank": sent, "halo_ms": t_halo,
+                      "peak_source": "B200_PROFILING.md measured peer copy per direction (900 nominal)",
+                      "what": "one z halo (a plane to each neighbour, ncclSend/Recv), max over ranks"}
+        else:
+            nvlink = {"halo_ms": t_halo, "achieved": None,
+                      "what": "CSR strips: halo time only (send-list bytes not exported)"}
     # two-level rounding of the same x^(T), once,
     # outside the timed step: device phases + the host max-flow, timed apart
     two_level = None
@@ -425,6 +442,7 @@ def main():
                      else "fallback 6650 GB/s (B200_PROFILING.md)",
                      "frac_of_nominal_8TBps": ach / 8000.0, "kernels": kernels},
         "cpu_baseline": cpu,
+        "nvlink": nvlink,
         "two_level": two_level,
         "fixed_point_exit": fpx,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

@@ -296,7 +296,11 @@ irls_status irls_get_stats(irls_ctx *ctx, irls_stats *stats);
 /* Kernel timing with CUDA events on the context's stream, on the current
  * state: runs `reps` launches of kernel `which` (0 = CG SpMV+p-update K3,
  * 1 = CG axpy+Jacobi K5, 2 = reweight+assemble K1) and returns the mean ms.
- * The CG state is saved and restored, so the solve state is unchanged. */
+ * The CG state is saved and restored, so the solve state is unchanged.
+ * which = 3 (multi-rank NCCL contexts only; COLLECTIVE: every rank calls it
+ * with the same reps): the per-CG-iteration z halo exchange (one plane / the
+ * packed send lists to each neighbour over NCCL), timed on this rank; it only
+ * rewrites z's ghost entries with the values they already hold. */
 irls_status irls_time_kernel(irls_ctx *ctx, int32_t which, int32_t reps, float *mean_ms);
 
 void irls_mincut_destroy(irls_ctx *ctx);

@@ -908,9 +908,28 @@ extern "C" irls_status irls_get_stats(irls_ctx *c, irls_stats *o)
 extern "C" irls_status irls_time_kernel(irls_ctx *c, int32_t which, int32_t reps, float *mean_ms)
 {
     GUARD(c);
-    if (!mean_ms || reps < 1 || which < 0 || which > 2) return IRLS_ERR_INVALID_ARGUMENT;
+    if (!mean_ms || reps < 1 || which < 0 || which > 3) return IRLS_ERR_INVALID_ARGUMENT;
     if (c->state == 0) return fail(c, IRLS_ERR_STATE, "time_kernel needs a solved state");
     cudaStream_t st = c->stream;
+    if (which == 3) {  // the z halo (NCCL), collective
+        if (!c->multi || c->vg) return fail(c, IRLS_ERR_INVALID_ARGUMENT, "halo timing needs an NCCL context");
+        Ranks R{c};
+        irls_status s = coll_halo(R, true, st);  // warm-up
+        if (s) return s;
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e0, st));
+        for (int i = 0; i < reps && !s; i++) s = coll_halo(R, true, st);
+        CK(cudaEventRecord(e1, st));
+        CK(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        *mean_ms = ms / reps;
+        return s;
+    }
     const int64_t npad = (int64_t)c->nchunks * kChunk;
     // snapshot everything the kernels write
     double *arrs[] = {c->x, c->q, c->r, c->z, c->p0, c->p1, c->D, c->Dinv};

@@ -22,7 +22,7 @@ STATUS_NAMES = {0: "IRLS_OK", 1: "IRLS_ERR_INVALID_ARGUMENT", 2: "IRLS_ERR_SOURC
 IRLS_FROM_SCRATCH, IRLS_CONTINUE = 0, 1
 IRLS_NORM_PRECONDITIONED, IRLS_NORM_UNPRECONDITIONED = 0, 1
 IRLS_LOOP_GRAPH, IRLS_LOOP_HOST, IRLS_LOOP_GRAPH_NCCL = 0, 1, 2
-KERNEL_PSPMV, KERNEL_AXPY, KERNEL_ASSEMBLE = 0, 1, 2
+KERNEL_PSPMV, KERNEL_AXPY, KERNEL_ASSEMBLE, KERNEL_HALO = 0, 1, 2, 3
 
 
 class irls_options(C.Structure):

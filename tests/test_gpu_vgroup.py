@@ -244,3 +244,23 @@ def test_vgroup_p2p_rejects_bad_flag(irls):
     spec = gen.blob_grid(64, 64, 16, seed=9)
     with pytest.raises(irls.IrlsError):
         irls.VGroup(spec, 2, irls.options(p2p=2))
+
+
+def test_halo_timing_entry(irls):
+    """irls_time_kernel(KERNEL_HALO) (bench's NVLink line at N > 1): runs on
+    an NCCL context (here a 1-rank communicator: no peers, an empty exchange)
+    without changing the state; refused on a plain single-GPU context."""
+    import torch
+    spec = gen.blob_grid(64, 64, 16, seed=3, sigma=(3.0, 8.0))
+    comm = irls.comm_desc(1, 0, 0, irls.irls_nccl_unique_id(), torch.cuda.current_stream().cuda_stream)
+    g = irls.MinCut.from_spec(spec, irls.options(T=4, loop_mode=1), comm)
+    g.irls_solve(irls.IRLS_FROM_SCRATCH, T=4)
+    x0 = g.irls_get_potentials()
+    assert g.irls_time_kernel(irls.KERNEL_HALO, 5) >= 0.0
+    assert np.array_equal(g.irls_get_potentials(), x0)
+    g.close()
+    m = irls.MinCut.from_spec(spec, irls.options(T=4))
+    m.irls_solve(irls.IRLS_FROM_SCRATCH, T=4)
+    with pytest.raises(irls.IrlsError):
+        m.irls_time_kernel(irls.KERNEL_HALO, 5)
+    m.close()
