@@ -32,7 +32,8 @@ _lib = None
 
 class Options(C.Structure):
     _fields_ = [("eps", C.c_double), ("T", C.c_int32), ("cg_rtol", C.c_double),
-                ("cg_max_iter", C.c_int32), ("cg_norm", C.c_int32), ("warm_start", C.c_int32)]
+                ("cg_max_iter", C.c_int32), ("cg_norm", C.c_int32), ("warm_start", C.c_int32),
+                ("cg_variant", C.c_int32)]
 
 
 class Report(C.Structure):
@@ -213,9 +214,9 @@ class Solver:
     """IRLS state over a Graph (Algorithm 1)."""
 
     def __init__(self, graph: Graph, eps=1e-6, T=50, cg_rtol=1e-3, cg_max_iter=50,
-                 cg_norm=0, warm_start=True):
+                 cg_norm=0, warm_start=True, cg_variant=0):
         self.graph = graph
-        self.opts = Options(eps, T, cg_rtol, cg_max_iter, cg_norm, int(bool(warm_start)))
+        self.opts = Options(eps, T, cg_rtol, cg_max_iter, cg_norm, int(bool(warm_start)), int(cg_variant))
         self.h = lib().orc_state_new(graph.h, C.byref(self.opts))
         if not self.h:
             raise MemoryError("orc_state_new")

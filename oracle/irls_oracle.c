@@ -377,9 +377,10 @@ typedef struct {
     double *g;     /* per adjacency entry conductance */
     double *gs, *gt, *D, *Dinv;
     double *x, *r, *z, *p, *q;
+    double *w, *sv;  /* CG-CG: w = A z, s = A p */
     double *tmp;
     double eps;
-    int32_t T, cg_max_iter, cg_norm, warm_start;
+    int32_t T, cg_max_iter, cg_norm, warm_start, cg_variant;
     double cg_rtol;
     int32_t step;  /* number of solves done (0 = none) */
     double *cs, *ct; /* owned copy of terminal capacities (set_terminal_weights) */
@@ -393,6 +394,7 @@ typedef struct {
     int32_t cg_max_iter;
     int32_t cg_norm;      /* 0 = preconditioned (A9), 1 = unpreconditioned */
     int32_t warm_start;
+    int32_t cg_variant;   /* 0 = Hestenes-Stiefel (O5), 1 = Chronopoulos-Gear (O5', A31) */
 } orc_options;
 
 typedef struct {
@@ -410,7 +412,7 @@ void orc_state_free(orc_state *S)
 {
     if (!S) return;
     free(S->g); free(S->gs); free(S->gt); free(S->D); free(S->Dinv);
-    free(S->x); free(S->r); free(S->z); free(S->p); free(S->q); free(S->tmp);
+    free(S->x); free(S->r); free(S->z); free(S->p); free(S->q); free(S->w); free(S->sv); free(S->tmp);
     free(S->cs); free(S->ct); free(S);
 }
 
@@ -421,7 +423,8 @@ orc_state *orc_state_new(const orc_graph *G, const orc_options *o)
     int64_t n = G->n > 0 ? G->n : 1, m = G->adj_ptr[G->n] > 0 ? G->adj_ptr[G->n] : 1;
     S->G = G;
     S->g = (double *)calloc((size_t)m, sizeof(double));
-    double **vecs[] = {&S->gs, &S->gt, &S->D, &S->Dinv, &S->x, &S->r, &S->z, &S->p, &S->q, &S->tmp, &S->cs, &S->ct};
+    double **vecs[] = {&S->gs, &S->gt, &S->D, &S->Dinv, &S->x, &S->r, &S->z, &S->p, &S->q, &S->w, &S->sv,
+                       &S->tmp, &S->cs, &S->ct};
     for (size_t i = 0; i < sizeof(vecs) / sizeof(vecs[0]); i++) {
         *vecs[i] = (double *)calloc((size_t)n, sizeof(double));
         if (!*vecs[i]) { orc_state_free(S); return NULL; }
@@ -429,7 +432,7 @@ orc_state *orc_state_new(const orc_graph *G, const orc_options *o)
     if (!S->g) { orc_state_free(S); return NULL; }
     for (int64_t u = 0; u < G->n; u++) { S->cs[u] = G->cs[u]; S->ct[u] = G->ct[u]; }
     S->eps = o->eps; S->T = o->T; S->cg_rtol = o->cg_rtol; S->cg_max_iter = o->cg_max_iter;
-    S->cg_norm = o->cg_norm; S->warm_start = o->warm_start;
+    S->cg_norm = o->cg_norm; S->warm_start = o->warm_start; S->cg_variant = o->cg_variant;
     S->step = 0;
     return S;
 }
@@ -534,6 +537,86 @@ static int pcg(orc_state *S, orc_report *rep)
     return ORC_OK;
 }
 
+/* O5' (A31): the same Jacobi-PCG in the Chronopoulos-Gear form (SURVEY
+ * §8(f) NEXT #3, single-reduction CG: Chronopoulos & Gear 1989), which
+ * carries w = A z and s = A p so that one iteration needs one global
+ * reduction instead of two.  In exact arithmetic its iterates equal O5's.
+ * Setup, ref, the b = 0 case and the stopping test (res <= rtol*ref before
+ * each iteration) are O5's.  Then, if the loop runs at all: w = A z,
+ * delta = <z, w> (breakdown if not > 0 or inf), alpha = rho / delta.
+ * Iteration k:  p = z (k = 0) | z + beta p;  s = w (k = 0) | w + beta s;
+ * x += alpha p;  r -= alpha s;  z = r Dinv;  w = A z (O2);
+ * gamma = <r, z>, delta = <z, w>, res = sqrt(<z,z> | <r,r>) (C3 each);
+ * k += 1;  beta = gamma / rho;  den = delta - (beta gamma) / alpha;
+ * rho = gamma;  breakdown if alpha, beta or res is not finite;  if the loop
+ * continues: breakdown unless den > 0 and finite, alpha = gamma / den. */
+static int pcg_cgcg(orc_state *S, orc_report *rep)
+{
+    const orc_graph *G = S->G;
+    int64_t n = G->n;
+    double *x = S->x, *r = S->r, *z = S->z, *p = S->p, *q = S->q, *w = S->w, *sv = S->sv;
+    matvec(S, x, q);
+    const double *b = S->bvec ? S->bvec : S->gs;
+    for (int64_t u = 0; u < n; u++) r[u] = b[u] - q[u];
+    for (int64_t u = 0; u < n; u++) z[u] = r[u] * S->Dinv[u];
+    double rho = dot_c3(S, r, z);
+    double ref2;
+    if (S->cg_norm == 0) {
+        for (int64_t u = 0; u < n; u++) { double mb = b[u] * S->Dinv[u]; S->tmp[u] = mb * mb; }
+        ref2 = orc_c3_sum(S->tmp, n);
+    } else {
+        ref2 = dot_c3(S, b, b);
+    }
+    double ref = sqrt(ref2);
+    rep->ref = ref;
+    if (ref == 0.0) {
+        for (int64_t u = 0; u < n; u++) x[u] = 0.0;
+        rep->cg_iters = 0; rep->converged = 1; rep->rel_res = 0.0;
+        return ORC_OK;
+    }
+    double res = sqrt(S->cg_norm == 0 ? dot_c3(S, z, z) : dot_c3(S, r, r));
+    int32_t k = 0;
+    double alpha = 0.0, beta = 0.0;
+    if (!(res <= S->cg_rtol * ref || k == S->cg_max_iter)) {
+        matvec(S, z, w);
+        double delta = dot_c3(S, z, w);
+        if (!(delta > 0.0) || isinf(delta)) return ORC_ERR_CG_BREAKDOWN;
+        alpha = rho / delta;
+    }
+    for (;;) {
+        if (res <= S->cg_rtol * ref || k == S->cg_max_iter) break;
+        for (int64_t u = 0; u < n; u++) p[u] = k == 0 ? z[u] : z[u] + beta * p[u];
+        for (int64_t u = 0; u < n; u++) sv[u] = k == 0 ? w[u] : w[u] + beta * sv[u];
+        for (int64_t u = 0; u < n; u++) x[u] = x[u] + alpha * p[u];
+        for (int64_t u = 0; u < n; u++) r[u] = r[u] - alpha * sv[u];
+        for (int64_t u = 0; u < n; u++) z[u] = r[u] * S->Dinv[u];
+        matvec(S, z, w);
+        double gamma = dot_c3(S, r, z);
+        double delta = dot_c3(S, z, w);
+        res = sqrt(S->cg_norm == 0 ? dot_c3(S, z, z) : dot_c3(S, r, r));
+        k++;
+        beta = gamma / rho;
+        double t = beta * gamma;
+        t = t / alpha;
+        double den = delta - t;
+        rho = gamma;
+        if (!isfinite(alpha) || !isfinite(beta) || !isfinite(res)) return ORC_ERR_CG_BREAKDOWN;
+        if (!(res <= S->cg_rtol * ref || k == S->cg_max_iter)) {
+            if (!(den > 0.0) || isinf(den)) return ORC_ERR_CG_BREAKDOWN;
+            alpha = gamma / den;
+        }
+    }
+    rep->cg_iters = k;
+    rep->converged = res <= S->cg_rtol * ref;
+    rep->rel_res = res / ref;
+    return ORC_OK;
+}
+
+static int solve(orc_state *S, orc_report *rep)
+{
+    return S->cg_variant == 1 ? pcg_cgcg(S, rep) : pcg(S, rep);
+}
+
 /* O8 diagnostics at x = S->x with the step's conductances. */
 static void diagnostics(orc_state *S, orc_report *rep)
 {
@@ -594,7 +677,7 @@ int orc_init(orc_state *S, orc_report *rep)
     memset(rep, 0, sizeof(*rep));
     assemble(S, NULL);
     for (int64_t u = 0; u < S->G->n; u++) S->x[u] = 0.0;
-    int rc = pcg(S, rep);
+    int rc = solve(S, rep);
     if (rc != ORC_OK) return rc;
     diagnostics(S, rep);
     S->step = 1;
@@ -610,7 +693,7 @@ int orc_step(orc_state *S, orc_report *rep)
     assemble(S, S->x);
     if (!S->warm_start)
         for (int64_t u = 0; u < S->G->n; u++) S->x[u] = 0.0;
-    int rc = pcg(S, rep);
+    int rc = solve(S, rep);
     if (rc != ORC_OK) return rc;
     diagnostics(S, rep);
     S->step++;
@@ -1109,7 +1192,7 @@ int orc_lambda2(orc_state *S, double rtol, int32_t max_iter, int32_t norm, doubl
     S->bvec = b;
     orc_report rep;
     memset(&rep, 0, sizeof(rep));
-    int rc = pcg(S, &rep);
+    int rc = solve(S, &rep);
     S->bvec = NULL;
     S->cg_rtol = r0; S->cg_max_iter = m0; S->cg_norm = n0;
     if (rc == ORC_OK) {
