@@ -71,6 +71,11 @@ typedef enum { IRLS_NORM_PRECONDITIONED = 0, IRLS_NORM_UNPRECONDITIONED = 1 } ir
  * collectives captured inside the loop bodies (no host round trip per
  * iteration; exercised on one GPU through a 1-rank communicator). */
 typedef enum { IRLS_LOOP_GRAPH = 0, IRLS_LOOP_HOST = 1, IRLS_LOOP_GRAPH_NCCL = 2 } irls_loop_mode;
+/* PCG form (A31): Hestenes-Stiefel (O5, two reductions per iteration) or
+ * Chronopoulos-Gear (O5': one reduction per iteration,
+ * one kernel per iteration on one GPU; iterates equal O5's in exact
+ * arithmetic, bitwise equal to the oracle's O5'). */
+typedef enum { IRLS_CG_HS = 0, IRLS_CG_CG = 1 } irls_cg_variant;
 
 /* Solver options (A9-A13). */
 typedef struct {
@@ -97,6 +102,8 @@ typedef struct {
                             directly.  Results are bit-identical to p2p = 0.  A wait longer than 10 s
                             ends the solve with IRLS_ERR_NCCL.  Ignored on a single-rank context.
                             Default 0 (NCCL). */
+    int32_t cg_variant;  /* irls_cg_variant; default IRLS_CG_HS */
+    int32_t reserved;
 } irls_options;
 
 void irls_options_default(irls_options *opt);

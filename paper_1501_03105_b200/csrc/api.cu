@@ -35,6 +35,8 @@ extern "C" void irls_options_default(irls_options *o)
     o->loop_mode = IRLS_LOOP_GRAPH;
     o->fixed_point_exit = 0;
     o->p2p = 0;
+    o->cg_variant = IRLS_CG_HS;
+    o->reserved = 0;
 }
 
 extern "C" const char *irls_status_string(irls_status st)
@@ -210,42 +212,54 @@ static irls_status allreduce_slots(irls_ctx *c, int nq, cudaStream_t st)
 // one stream; the same data movement done with device copies).
 // ---------------------------------------------------------------------------
 
-static irls_status coll_halo(Ranks &R, bool z_not_x, cudaStream_t st)
+// The array of a ghosted vector on one rank (halo exchanges name it this way).
+typedef double *(*ArrSel)(irls_ctx *);
+static double *sel_x(irls_ctx *c) { return c->x; }
+static double *sel_z(irls_ctx *c) { return c->z; }
+static double *sel_r(irls_ctx *c) { return c->r; }
+static double *sel_dinv(irls_ctx *c) { return c->Dinv; }
+static double *sel_w0(irls_ctx *c) { return c->cg_w[0]; }
+static double *sel_w1(irls_ctx *c) { return c->cg_w[1]; }
+
+static irls_status coll_halo_sel(Ranks &R, ArrSel sel, cudaStream_t st)
 {
     irls_ctx *c = R[0];
     if (!c->multi) return IRLS_OK;
-    if (!c->vg) return halo(c, z_not_x ? c->z : c->x, st);
+    if (!c->vg) return halo(c, sel(c), st);
     if (c->kind == 1) {  // pack on every rank, then the same copies NCCL would make
         for (irls_ctx *d : R) {
             const int64_t ns = d->send_off[d->world];
-            if (ns > 0) launch_halo_pack(z_not_x ? d->z : d->x, d->send_idx, ns, d->sendbuf, st);
+            if (ns > 0) launch_halo_pack(sel(d), d->send_idx, ns, d->sendbuf, st);
         }
         for (irls_ctx *d : R)
             for (int q = 0; q < d->world; q++) {
                 const int64_t rc = d->recv_off[q + 1] - d->recv_off[q];
                 if (rc == 0) continue;
                 irls_ctx *o = R[q];
-                CK(cudaMemcpyAsync((z_not_x ? d->z : d->x) + d->npad_own + d->recv_off[q], o->sendbuf + o->send_off[d->rank],
+                CK(cudaMemcpyAsync(sel(d) + d->npad_own + d->recv_off[q], o->sendbuf + o->send_off[d->rank],
                                    sizeof(double) * rc, cudaMemcpyDeviceToDevice, st));
             }
         return IRLS_OK;
     }
     for (irls_ctx *d : R) {
         const irls_halo &h = d->hplan;
-        double *arr = z_not_x ? d->z : d->x;
+        double *arr = sel(d);
         const size_t bytes = sizeof(double) * (size_t)h.count;
         if (h.peer_lo >= 0) {
             irls_ctx *o = R[h.peer_lo];
-            CK(cudaMemcpyAsync(arr + h.recv_lo, (z_not_x ? o->z : o->x) + o->hplan.send_hi, bytes,
-                               cudaMemcpyDeviceToDevice, st));
+            CK(cudaMemcpyAsync(arr + h.recv_lo, sel(o) + o->hplan.send_hi, bytes, cudaMemcpyDeviceToDevice, st));
         }
         if (h.peer_hi >= 0) {
             irls_ctx *o = R[h.peer_hi];
-            CK(cudaMemcpyAsync(arr + h.recv_hi, (z_not_x ? o->z : o->x) + o->hplan.send_lo, bytes,
-                               cudaMemcpyDeviceToDevice, st));
+            CK(cudaMemcpyAsync(arr + h.recv_hi, sel(o) + o->hplan.send_lo, bytes, cudaMemcpyDeviceToDevice, st));
         }
     }
     return IRLS_OK;
+}
+
+static irls_status coll_halo(Ranks &R, bool z_not_x, cudaStream_t st)
+{
+    return coll_halo_sel(R, z_not_x ? sel_z : sel_x, st);
 }
 
 static irls_status coll_allreduce(Ranks &R, int nq, cudaStream_t st)
@@ -324,11 +338,64 @@ static irls_status enq_assemble(Ranks &R, int mode, const CondArgs &cd, cudaStre
         }
         if ((s = coll_halo(R, true, st))) return s;
     }
+    if (R[0]->cgcg) {  // CG-CG: w0 = A z0 and alpha_0 = rho / <z0, w0> (a K3 pass at k = 0 into w[0])
+        if (R[0]->multi && ((s = coll_halo_sel(R, sel_r, st)) || (s = coll_halo_sel(R, sel_dinv, st)))) return s;
+        for (irls_ctx *c : R) {
+            VecArgs v = vec_args(c);
+            v.q = c->cg_w[0];
+            if (c->kind == 0) launch_stencil_pspmv(stencil_args(c, false), v, red_args_solve(c), cd, st);
+            else launch_sell_pspmv(sell_args(c), v, red_args_solve(c), cd, st);
+            c->launches++;
+        }
+        if (R[0]->multi) {
+            if ((s = coll_allreduce(R, 1, st))) return s;
+            for (irls_ctx *c : R) {
+                launch_finalize(PH_W0, c->ctrl, c->slots_glob, cd, p2p_wait_args(c), st);
+                c->launches++;
+            }
+            if ((s = coll_halo_sel(R, sel_w0, st))) return s;
+        }
+    }
     return last_launch(R[0], "assemble");
+}
+
+// Chronopoulos-Gear body: TWO iterations (k even, then k odd) so that the
+// ping-pong buffer each halo moves is fixed at capture time; the second one
+// is skipped on the device when the first one stopped.
+static irls_status enq_body_cgcg(Ranks &R, const CondArgs &cd, cudaStream_t st)
+{
+    irls_status s;
+    for (int half = 0; half < 2; half++) {
+        for (irls_ctx *c : R) {
+            const VecArgs v = vec_args(c);
+            const CgArgs g = cg_args(c);
+            if (c->kind == 0) launch_stencil_cgcg(stencil_args(c, false), v, g, red_args_solve(c), cd, st);
+            else launch_sell_cgcg(sell_args(c), v, g, red_args_solve(c), cd, st);
+            c->launches++;
+            if (c->multi && c->kind == 0) {
+                if (c->lo_ghost) launch_cgcg_ghost(g, -c->P, c->P, c->ctrl, st);
+                if (c->hi_ghost) launch_cgcg_ghost(g, c->n_own, c->P, c->ctrl, st);
+                c->launches += (c->lo_ghost ? 1 : 0) + (c->hi_ghost ? 1 : 0);
+            } else if (c->multi && c->n_ghost > 0) {
+                launch_cgcg_ghost(g, c->npad_own, c->n_ghost, c->ctrl, st);
+                c->launches++;
+            }
+        }
+        if (R[0]->multi) {
+            if ((s = coll_allreduce(R, 4, st))) return s;
+            for (irls_ctx *c : R) {
+                launch_finalize(PH_CG, c->ctrl, c->slots_glob, cd, p2p_wait_args(c), st);
+                c->launches++;
+            }
+            if ((s = coll_halo_sel(R, half == 0 ? sel_w1 : sel_w0, st))) return s;
+        }
+    }
+    return last_launch(R[0], "cg-cg body");
 }
 
 static irls_status enq_body(Ranks &R, const CondArgs &cd, cudaStream_t st)
 {
+    if (R[0]->cgcg) return enq_body_cgcg(R, cd, st);
     irls_status s;
     for (irls_ctx *c : R) {
         const VecArgs v = vec_args(c);
@@ -375,7 +442,8 @@ static irls_status enq_body(Ranks &R, const CondArgs &cd, cudaStream_t st)
 static void enq_finish(Ranks &R, cudaStream_t st)
 {
     for (irls_ctx *c : R) {
-        launch_finish(vec_args(c), c->ctrl, st);
+        if (c->cgcg) launch_cgcg_finish(vec_args(c), c->ctrl, st);
+        else launch_finish(vec_args(c), c->ctrl, st);
         c->launches += 1;
     }
 }
@@ -416,7 +484,7 @@ static irls_status enq_tail(Ranks &R, int mode, cudaStream_t st, bool finish = t
 // wrapped as  gate -> IF (not frozen) { K1 -> WHILE {...} -> finish } ->
 // report: a frozen solve costs one graph launch and two one-thread kernels.
 // One-block CG loop (small.cu) for a single rank whose graph is one C3 chunk.
-static bool small_path(const irls_ctx *c) { return !c->multi && c->n_own > 0 && c->n_own <= kChunk; }
+static bool small_path(const irls_ctx *c) { return !c->multi && !c->cgcg && c->n_own > 0 && c->n_own <= kChunk; }
 
 static void enq_small(irls_ctx *c, cudaStream_t st)
 {
@@ -465,7 +533,7 @@ static irls_status capture_solve_body(irls_ctx *c, Ranks &R, int mode, cudaStrea
     CK(cudaStreamBeginCaptureToGraph(c->side_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
     const int64_t pre = c->launches;
     s = enq_body(R, cd, c->side_stream);
-    c->gl_body = c->launches - pre;
+    c->gl_body = (c->launches - pre) / (c->cgcg ? 2 : 1);  // CG-CG bodies hold two iterations
     c->launches = pre;
     cudaGraph_t bodyg;
     CK(cudaStreamEndCapture(c->side_stream, &bodyg));

@@ -72,7 +72,11 @@ static irls_status alloc_solver(irls_ctx *c, int64_t ghost)
         return true;
     };
     if (!ghosted(c->x, false) || !ghosted(c->z, ipc && c->kind == 0) || !ghosted(c->p0, false) ||
-        !ghosted(c->p1, false))
+        !ghosted(c->p1, false) || !ghosted(c->r, false) || !ghosted(c->Dinv, false))
+        return IRLS_ERR_OOM;
+    c->cgcg = c->opt.cg_variant == IRLS_CG_CG;
+    if (c->cgcg && (!ghosted(c->cg_r2, false) || !ghosted(c->cg_w[0], false) || !ghosted(c->cg_w[1], false) ||
+                    !ghosted(c->cg_s[0], false) || !ghosted(c->cg_s[1], false)))
         return IRLS_ERR_OOM;
     if (c->p2p) {
         const int64_t nb = 2 * kMaxQ * kGroups + 1;  // slots by parity + the arrival counter
@@ -84,8 +88,6 @@ static irls_status alloc_solver(irls_ctx *c, int64_t ghost)
         c->n_groups_all = count_nonempty(c->K, 0, kGroups);
     }
     c->D = dalloc<double>(c, npad);
-    c->Dinv = dalloc<double>(c, npad);
-    c->r = dalloc<double>(c, npad);
     c->q = dalloc<double>(c, npad);
     c->ctrl = dalloc<DevCtrl>(c, 1);
     c->part = dalloc<double>(c, (int64_t)kMaxQ * std::max<int32_t>(c->K, 1));

@@ -109,7 +109,8 @@ static inline irls_status check_opts(const irls_options *o)
     if (!o) return IRLS_ERR_INVALID_ARGUMENT;
     if (!(o->eps > 0.0) || isinf(o->eps) || o->T < 0 || !(o->cg_rtol >= 0.0) || o->cg_max_iter < 0 ||
         (o->cg_norm != 0 && o->cg_norm != 1) || (o->loop_mode < 0 || o->loop_mode > 2) ||
-        (o->fixed_point_exit != 0 && o->fixed_point_exit != 1) || (o->p2p != 0 && o->p2p != 1))
+        (o->fixed_point_exit != 0 && o->fixed_point_exit != 1) || (o->p2p != 0 && o->p2p != 1) ||
+        (o->cg_variant != IRLS_CG_HS && o->cg_variant != IRLS_CG_CG))
         return IRLS_ERR_INVALID_ARGUMENT;
     return IRLS_OK;
 }
@@ -212,6 +213,19 @@ static inline RedArgs red_args(const irls_ctx *c)
     r.g1 = c->g1;
     r.n_fin = c->n_fin;
     return r;
+}
+
+static inline CgArgs cg_args(const irls_ctx *c)
+{
+    CgArgs g;
+    g.r[0] = c->r;
+    g.r[1] = c->cg_r2;
+    g.w[0] = c->cg_w[0];
+    g.w[1] = c->cg_w[1];
+    g.s[0] = c->cg_s[0];
+    g.s[1] = c->cg_s[1];
+    g.p = c->p0;
+    return g;
 }
 
 typedef std::vector<irls_ctx *> Ranks;

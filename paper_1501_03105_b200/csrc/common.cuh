@@ -319,6 +319,42 @@ __device__ __forceinline__ void finalize_rz(DevCtrl *c, const double *slots)
     finalize_rz_t(c, slot_total(slots, 0), slot_total(slots, 1), slot_total(slots, 2));
 }
 
+// Chronopoulos-Gear PCG (O5', A31): after iteration k, quantities
+// [gamma = <r,z>, delta = <z,w>, <z,z>, <r,r>] of the new r, z, w.
+template <class C>
+__device__ __forceinline__ void finalize_cgcg_t(C *c, double gamma, double delta, double zz, double rr)
+{
+    const double res = sqrt(c->norm == 0 ? zz : rr);
+    const double alpha = c->alpha;
+    const double beta = gamma / c->rho;
+    double t = beta * gamma;
+    t = t / alpha;
+    const double den = delta - t;
+    c->res = res;
+    c->beta = beta;
+    c->rho = gamma;
+    c->k = c->k + 1;
+    if (!isfinite(alpha) || !isfinite(beta) || !isfinite(res)) {
+        c->status = ST_BREAKDOWN;
+        c->done = 1;
+        return;
+    }
+    c->done = (res <= c->rtol * c->ref) || (c->k == c->max_iter);
+    if (!c->done) {
+        if (!(den > 0.0) || isinf(den)) {
+            c->status = ST_BREAKDOWN;
+            c->done = 1;
+            return;
+        }
+        c->alpha = gamma / den;
+    }
+}
+
+__device__ __forceinline__ void finalize_cgcg(DevCtrl *c, const double *slots)
+{
+    finalize_cgcg_t(c, slot_total(slots, 0), slot_total(slots, 1), slot_total(slots, 2), slot_total(slots, 3));
+}
+
 // Order-preserving 64-bit key of a double (ascending).
 __device__ __forceinline__ unsigned long long dkey_asc(double x)
 {

@@ -120,6 +120,10 @@ struct irls_ctx {
     double *x_full = nullptr;     // rank 0: gathered potentials
     void *msg_dev = nullptr;      // sweep result broadcast
 
+    // Chronopoulos-Gear PCG (irls_options.cg_variant = IRLS_CG_CG)
+    bool cgcg = false;
+    double *cg_r2 = nullptr, *cg_w[2] = {nullptr, nullptr}, *cg_s[2] = {nullptr, nullptr};  // ghosted
+
     // peer-memory collectives (irls_options.p2p on a multi-rank context)
     bool p2p = false;
     double *p2p_buf = nullptr;    // [2][kMaxQ][8] slot sums by parity, then one u64 arrival counter

@@ -31,6 +31,14 @@ struct VecArgs {
     int64_t plane = 0;           // nx * ny
 };
 
+// Chronopoulos-Gear PCG (irls_options.cg_variant = IRLS_CG_CG): iteration k
+// reads r[k&1], w[k&1], s[(k+1)&1] (also at neighbours, incl. ghosts) and
+// writes r[(k+1)&1], w[(k+1)&1], s[k&1]; p and x are updated in place.
+struct CgArgs {
+    double *r[2], *w[2], *s[2];  // ghosted like x
+    double *p;
+};
+
 struct StencilArgs {
     int32_t nx, ny, nz;
     int64_t P;           // nx*ny
@@ -90,6 +98,15 @@ void launch_axpy_jacobi(const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
 // after the loop: x += alpha p_last (or x = 0 if b = 0)
 void launch_finish(const VecArgs &v, DevCtrl *ctrl, cudaStream_t st);
 // scalar finalizers for the multi-GPU path (after the slot allreduce)
+// Chronopoulos-Gear iteration (one kernel; C3 quantities [<r,z>, <z,w>,
+// <z,z>, <r,r>]; world 1: the last block finalizes and sets the condition)
+void launch_stencil_cgcg(const StencilArgs &s, const VecArgs &v, const CgArgs &g, const RedArgs &ra,
+                         const CondArgs &cd, cudaStream_t st);
+void launch_sell_cgcg(const SellArgs &s, const VecArgs &v, const CgArgs &g, const RedArgs &ra, const CondArgs &cd,
+                      cudaStream_t st);
+// ghost entries [lo, lo + n): s = w + beta s_old, r = r - alpha s (the owner's formulas)
+void launch_cgcg_ghost(const CgArgs &g, int64_t lo, int64_t n, const DevCtrl *ctrl, cudaStream_t st);
+void launch_cgcg_finish(const VecArgs &v, const DevCtrl *ctrl, cudaStream_t st);
 void launch_finalize(int phase, DevCtrl *ctrl, const double *slots, const CondArgs &cd, const P2PWait &pw,
                      cudaStream_t st);
 // write the step report from the control block
@@ -117,7 +134,7 @@ void launch_sell_diag_ex(const SellArgs &s, const VecArgs &v, const RedArgs &ra,
 void launch_diag_finalize(DevCtrl *ctrl, const double *slots, DevReport *reports, int norm, const P2PWait &pw,
                           cudaStream_t st);
 
-enum { PH_START = 0, PH_PQ = 1, PH_RZ = 2 };
+enum { PH_START = 0, PH_PQ = 1, PH_RZ = 2, PH_W0 = 3, PH_CG = 4 };
 // virtual-group slot sum: dst[i] = sum_r src[r][i]
 void launch_vsum(double *const *src, int W, int n, double *dst, cudaStream_t st);
 void launch_vminmax(DevCtrl *const *ctrl, int W, cudaStream_t st);

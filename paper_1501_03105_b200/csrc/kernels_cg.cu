@@ -5,6 +5,8 @@
 // order, so its running sums are exactly C3 step 2 and the block epilogue
 // (common.cuh) completes steps 3-6.  Per-node arithmetic follows O1-O5 of
 // DESIGN.md §2 operation for operation (no FMA: built with -fmad=false).
+#include <algorithm>
+
 #include "kernels.h"
 
 namespace irls {
@@ -191,6 +193,7 @@ __global__ void __launch_bounds__(kThreads) k_sell_assemble(SellArgs s, VecArgs 
 __global__ void __launch_bounds__(kThreads) k_stencil_pspmv(StencilArgs s, VecArgs v, RedArgs ra, CondArgs cd)
 {
     const DevCtrl *ctrl = ra.ctrl;
+    if (ctrl->done) return;  // CG-CG's w0 pass after a START that stopped
     const int32_t k = ctrl->k;
     const bool first = (k == 0);
     const double beta = ctrl->beta, alpha = ctrl->alpha;
@@ -219,12 +222,14 @@ __global__ void __launch_bounds__(kThreads) k_stencil_pspmv(StencilArgs s, VecAr
 #undef PVAL
     if (c3_chunk_epilogue<1>(acc, v.chunk0 + (int32_t)blockIdx.x, ra) && cd.finalize && threadIdx.x == 0) {
         finalize_pq(ra.ctrl, ra.slots);
+        set_cond(cd, ra.ctrl);
     }
 }
 
 __global__ void __launch_bounds__(kThreads) k_sell_pspmv(SellArgs s, VecArgs v, RedArgs ra, CondArgs cd)
 {
     const DevCtrl *ctrl = ra.ctrl;
+    if (ctrl->done) return;  // CG-CG's w0 pass after a START that stopped
     const int32_t k = ctrl->k;
     const bool first = (k == 0);
     const double beta = ctrl->beta, alpha = ctrl->alpha;
@@ -254,6 +259,7 @@ __global__ void __launch_bounds__(kThreads) k_sell_pspmv(SellArgs s, VecArgs v, 
 #undef PVAL
     if (c3_chunk_epilogue<1>(acc, v.chunk0 + (int32_t)blockIdx.x, ra) && cd.finalize && threadIdx.x == 0) {
         finalize_pq(ra.ctrl, ra.slots);
+        set_cond(cd, ra.ctrl);
     }
 }
 
@@ -354,7 +360,7 @@ __global__ void k_finalize(int phase, DevCtrl *ctrl, const double *slots, CondAr
     // phases whose producers did not run (as on one rank, where the skipped
     // kernel's fused finalize is skipped with it): a fixed-point step's
     // assembly, and K5 after a breakdown in the PQ phase
-    if ((phase == PH_START && ctrl->frozen) || (phase == PH_RZ && ctrl->done)) {
+    if ((phase == PH_START && ctrl->frozen) || ((phase == PH_RZ || phase == PH_W0 || phase == PH_CG) && ctrl->done)) {
         set_cond(cd, ctrl);
         return;
     }
@@ -363,7 +369,8 @@ __global__ void k_finalize(int phase, DevCtrl *ctrl, const double *slots, CondAr
         return;
     }
     if (phase == PH_START) finalize_start(ctrl, slots);
-    else if (phase == PH_PQ) finalize_pq(ctrl, slots);
+    else if (phase == PH_PQ || phase == PH_W0) finalize_pq(ctrl, slots);  // W0: alpha_0 = rho / <z, A z>
+    else if (phase == PH_CG) finalize_cgcg(ctrl, slots);
     else finalize_rz(ctrl, slots);
     if (phase != PH_PQ) set_cond(cd, ctrl);
 }
@@ -506,6 +513,150 @@ __global__ void k_diag_finalize(DevCtrl *ctrl, const double *slots, DevReport *r
     R.true_rel_res = ctrl->ref > 0.0 ? tr / ctrl->ref : 0.0;
     R.x_min = dkey_inv(ctrl->xmin_key);
     R.x_max = dkey_inv(ctrl->xmax_key);
+}
+
+// ---------------------------------------------------------------------------
+// Chronopoulos-Gear PCG (O5', A31): ONE kernel and ONE
+// C3 reduction per iteration.  Node u at iteration k (alpha = alpha_k, beta =
+// beta_k; k = 0: p = z, s = w):
+//   s = w + beta s_old;  z = r Dinv;  p = z + beta p;  x += alpha p;
+//   r' = r - alpha s;  z' = r' Dinv;  w' = D z' - sum_asc g z'_nbr   (O2)
+// with every neighbour's z' recomputed from its r, w, s_old and Dinv by the
+// same formulas (same bits as the owner's, O9 (ii)); quantities
+// [<r',z'>, <z',w'>, <z',z'>, <r',r'>].
+// ---------------------------------------------------------------------------
+#define CG_SVAL(i) (first ? wk[i] : wk[i] + beta * so[i])
+#define CG_ZNEW(i) ((rk[i] - alpha * CG_SVAL(i)) * di[i])
+#define CG_NODE_TAIL()                                                            \
+    const double su = CG_SVAL(u);                                                 \
+    const double zu = rk[u] * di[u];                                              \
+    const double pu = first ? zu : zu + beta * g.p[u];                            \
+    const double ru = rk[u] - alpha * su;                                         \
+    const double zn = ru * di[u];                                                 \
+    const double wu = v.D[u] * zn - a;                                            \
+    g.p[u] = pu;                                                                  \
+    sn[u] = su;                                                                   \
+    v.x[u] = v.x[u] + alpha * pu;                                                 \
+    rn[u] = ru;                                                                   \
+    wn[u] = wu;                                                                   \
+    acc[0] = acc[0] + ru * zn;                                                    \
+    acc[1] = acc[1] + zn * wu;                                                    \
+    acc[2] = acc[2] + zn * zn;                                                    \
+    acc[3] = acc[3] + ru * ru;
+
+#define CG_PROLOGUE()                                                             \
+    DevCtrl *ctrl = ra.ctrl;                                                      \
+    if (ctrl->done) {                                                             \
+        if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(cd, ctrl);              \
+        return;                                                                   \
+    }                                                                             \
+    const int32_t k = ctrl->k;                                                    \
+    const bool first = (k == 0);                                                  \
+    const double alpha = ctrl->alpha, beta = ctrl->beta;                          \
+    const double *__restrict__ rk = g.r[k & 1];                                   \
+    const double *__restrict__ wk = g.w[k & 1];                                   \
+    const double *__restrict__ so = g.s[(k + 1) & 1];                             \
+    double *__restrict__ rn = g.r[(k + 1) & 1];                                   \
+    double *__restrict__ wn = g.w[(k + 1) & 1];                                   \
+    double *__restrict__ sn = g.s[k & 1];                                         \
+    const double *__restrict__ di = v.Dinv;                                       \
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+
+#define CG_EPILOGUE()                                                             \
+    if (c3_chunk_epilogue<4>(acc, v.chunk0 + (int32_t)blockIdx.x, ra) && cd.finalize && threadIdx.x == 0) { \
+        finalize_cgcg(ra.ctrl, ra.slots);                                         \
+        set_cond(cd, ra.ctrl);                                                    \
+    }
+
+__global__ void __launch_bounds__(kThreads) k_cgcg_stencil(StencilArgs s, VecArgs v, CgArgs g, RedArgs ra,
+                                                           CondArgs cd)
+{
+    CG_PROLOGUE()
+    const int64_t P = s.P;
+    FOR_CHUNK_NODES({
+        const Coord c = coord_of(s, s.lo + u);
+        double a = 0.0;
+        if (c.z > 0) a = a + s.gz[u - P] * CG_ZNEW(u - P);
+        if (c.y > 0) a = a + s.gy[u - s.nx] * CG_ZNEW(u - s.nx);
+        if (c.x > 0) a = a + s.gx[u - 1] * CG_ZNEW(u - 1);
+        if (c.x < s.nx - 1) a = a + s.gx[u] * CG_ZNEW(u + 1);
+        if (c.y < s.ny - 1) a = a + s.gy[u] * CG_ZNEW(u + s.nx);
+        if (c.z < s.nz - 1) a = a + s.gz[u] * CG_ZNEW(u + P);
+        CG_NODE_TAIL()
+    })
+    CG_EPILOGUE()
+}
+
+__global__ void __launch_bounds__(kThreads) k_cgcg_sell(SellArgs s, VecArgs v, CgArgs g, RedArgs ra, CondArgs cd)
+{
+    CG_PROLOGUE()
+    FOR_CHUNK_NODES({
+        const int64_t sl = u / kSell;
+        const int64_t e0 = s.slice_ptr[sl] + (u % kSell);
+        const int32_t W = (int32_t)((s.slice_ptr[sl + 1] - s.slice_ptr[sl]) / kSell);
+        double a = 0.0;
+        for (int32_t kk = 0; kk < W; kk++) {
+            const int64_t idx = e0 + kSell * (int64_t)kk;
+            const int32_t nb = s.col[idx];
+            if (nb < 0) break;
+            a = a + s.g[idx] * CG_ZNEW(nb);
+        }
+        CG_NODE_TAIL()
+    })
+    CG_EPILOGUE()
+}
+
+// Ghost entries of a multi-rank context, in the phase of iteration k: the
+// owner's s and r updates (the neighbour's w arrives by the halo).
+__global__ void k_cgcg_ghost(CgArgs g, int64_t lo, int64_t n, const DevCtrl *ctrl)
+{
+    if (ctrl->done) return;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int32_t k = ctrl->k;
+    const bool first = (k == 0);
+    const double alpha = ctrl->alpha, beta = ctrl->beta;
+    const double *wk = g.w[k & 1], *so = g.s[(k + 1) & 1], *rk = g.r[k & 1];
+    const int64_t u = lo + i;
+    const double su = CG_SVAL(u);
+    g.s[k & 1][u] = su;
+    g.r[(k + 1) & 1][u] = rk[u] - alpha * su;
+}
+#undef CG_SVAL
+#undef CG_ZNEW
+#undef CG_NODE_TAIL
+#undef CG_PROLOGUE
+#undef CG_EPILOGUE
+
+// After a CG-CG solve x is final (updated every iteration); only b = 0 needs x = 0.
+__global__ void k_cgcg_finish(VecArgs v, const DevCtrl *ctrl)
+{
+    if (!ctrl->zero_x) return;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < v.n_own; i += (int64_t)gridDim.x * blockDim.x)
+        v.x[i] = 0.0;
+}
+
+void launch_cgcg_finish(const VecArgs &v, const DevCtrl *ctrl, cudaStream_t st)
+{
+    const unsigned nb = (unsigned)std::min<int64_t>(std::max<int64_t>((v.n_own + 255) / 256, 1), 148 * 8);
+    k_cgcg_finish<<<nb, 256, 0, st>>>(v, ctrl);
+}
+
+void launch_stencil_cgcg(const StencilArgs &s, const VecArgs &v, const CgArgs &g, const RedArgs &ra,
+                         const CondArgs &cd, cudaStream_t st)
+{
+    k_cgcg_stencil<<<(unsigned)((v.n_own + kChunk - 1) / kChunk), kThreads, 0, st>>>(s, v, g, ra, cd);
+}
+
+void launch_sell_cgcg(const SellArgs &s, const VecArgs &v, const CgArgs &g, const RedArgs &ra, const CondArgs &cd,
+                      cudaStream_t st)
+{
+    k_cgcg_sell<<<(unsigned)((v.n_own + kChunk - 1) / kChunk), kThreads, 0, st>>>(s, v, g, ra, cd);
+}
+
+void launch_cgcg_ghost(const CgArgs &g, int64_t lo, int64_t n, const DevCtrl *ctrl, cudaStream_t st)
+{
+    if (n > 0) k_cgcg_ghost<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g, lo, n, ctrl);
 }
 
 // Virtual-group "allreduce": dst = sum over ranks (rank order) of src[r].

@@ -144,6 +144,7 @@ template <int WMAX, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) k_sellp_pspmv(SellArgs s, VecArgs v, RedArgs ra, CondArgs cd)
 {
     const DevCtrl *ctrl = ra.ctrl;
+    if (ctrl->done) return;  // CG-CG's w0 pass after a START that stopped
     const int32_t it = ctrl->k;
     const bool first = (it == 0);
     const double beta = ctrl->beta, alpha = ctrl->alpha;
@@ -202,6 +203,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sellp_pspmv(SellArgs s, VecA
     }
     if (c3_chunk_epilogue<1>(acc, v.chunk0 + (int32_t)blockIdx.x, ra) && cd.finalize && threadIdx.x == 0) {
         finalize_pq(ra.ctrl, ra.slots);
+        set_cond3(cd, ra.ctrl);
     }
 }
 

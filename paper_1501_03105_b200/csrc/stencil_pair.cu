@@ -364,6 +364,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_fused(StencilArgs s, Ve
 __global__ void __launch_bounds__(kThreads) k_pair_pspmv(StencilArgs s, VecArgs v, RedArgs ra, CondArgs cd)
 {
     const DevCtrl *ctrl = ra.ctrl;
+    if (ctrl->done) return;  // CG-CG's w0 pass after a START that stopped
     const int32_t k = ctrl->k;
     const bool first = (k == 0);
     const double beta = ctrl->beta, alpha = ctrl->alpha;
@@ -455,6 +456,7 @@ __global__ void __launch_bounds__(kThreads) k_pair_pspmv(StencilArgs s, VecArgs 
     }
     if (c3_chunk_epilogue<1>(acc, v.chunk0 + (int32_t)blockIdx.x, ra) && cd.finalize && threadIdx.x == 0) {
         finalize_pq(ra.ctrl, ra.slots);
+        set_cond2(cd, ra.ctrl);
     }
 }
 

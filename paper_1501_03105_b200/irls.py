@@ -22,13 +22,15 @@ STATUS_NAMES = {0: "IRLS_OK", 1: "IRLS_ERR_INVALID_ARGUMENT", 2: "IRLS_ERR_SOURC
 IRLS_FROM_SCRATCH, IRLS_CONTINUE = 0, 1
 IRLS_NORM_PRECONDITIONED, IRLS_NORM_UNPRECONDITIONED = 0, 1
 IRLS_LOOP_GRAPH, IRLS_LOOP_HOST, IRLS_LOOP_GRAPH_NCCL = 0, 1, 2
+IRLS_CG_HS, IRLS_CG_CG = 0, 1
 KERNEL_PSPMV, KERNEL_AXPY, KERNEL_ASSEMBLE, KERNEL_HALO = 0, 1, 2, 3
 
 
 class irls_options(C.Structure):
     _fields_ = [("eps", C.c_double), ("T", C.c_int32), ("cg_rtol", C.c_double), ("cg_max_iter", C.c_int32),
                 ("cg_norm", C.c_int32), ("warm_start", C.c_int32), ("record_trace", C.c_int32),
-                ("loop_mode", C.c_int32), ("fixed_point_exit", C.c_int32), ("p2p", C.c_int32)]
+                ("loop_mode", C.c_int32), ("fixed_point_exit", C.c_int32), ("p2p", C.c_int32),
+                ("cg_variant", C.c_int32), ("reserved", C.c_int32)]
 
 
 DEVICE_ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
