@@ -198,6 +198,8 @@ def main():
     ap.add_argument("--loop-mode", type=int, default=0)
     ap.add_argument("--no-two-level", action="store_true")
     ap.add_argument("--no-fixed-point-exit", action="store_true")
+    ap.add_argument("--cg-variant", default="hs", choices=["hs", "cg"],
+                    help="PCG form: Hestenes-Stiefel (default) or Chronopoulos-Gear (one reduction per iteration)")
     ap.add_argument("--p2p", type=int, default=0, choices=[0, 1],
                     help="N>1: per-iteration collectives over peer memory (irls_options.p2p) instead of NCCL")
     args = ap.parse_args()
@@ -224,7 +226,8 @@ def main():
 
     spec, wdesc = workload(args.config)
     T = 50
-    opts = I.options(T=T, loop_mode=args.loop_mode, p2p=args.p2p)
+    cgv = I.IRLS_CG_CG if args.cg_variant == "cg" else I.IRLS_CG_HS
+    opts = I.options(T=T, loop_mode=args.loop_mode, p2p=args.p2p, cg_variant=cgv)
     stream = torch.cuda.current_stream()
     uid = None
     if world > 1:
@@ -281,7 +284,7 @@ def main():
     fpx = None
     if not args.no_fixed_point_exit:
         m.close()
-        m = I.MinCut.from_spec(spec, I.options(T=T, loop_mode=args.loop_mode, fixed_point_exit=1, p2p=args.p2p), comm)
+        m = I.MinCut.from_spec(spec, I.options(T=T, loop_mode=args.loop_mode, fixed_point_exit=1, p2p=args.p2p, cg_variant=cgv), comm)
         for _ in range(args.warmup):
             m.irls_solve(I.IRLS_FROM_SCRATCH, T=T, reports=False)
             m.irls_sweep_cut(side=False)
@@ -432,7 +435,8 @@ def main():
                    "l2": "inputs (8.6 GB working set) larger than the 126 MB L2; no flush",
                    "parallelism": f"z-slab x{world}", "cut_value": cut, "k": k,
                    "cg_iter_ms_kernels": cg_iter_ms, "loop_mode": "graph" if (args.loop_mode == 0 and world == 1) or args.loop_mode == 2 else "host",
-                   "collectives": "none (1 rank)" if world == 1 else ("peer memory" if args.p2p else "nccl")},
+                   "collectives": "none (1 rank)" if world == 1 else ("peer memory" if args.p2p else "nccl"),
+                   "cg_variant": "Chronopoulos-Gear" if args.cg_variant == "cg" else "Hestenes-Stiefel"},
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                      "traffic": traffic, "traffic_note": "ncu dram__bytes_read+write per K3 launch "
                      "(profiles/r01_k3_traffic.json) over the live K3 duration, GB/s; algorithmic bytes per launch "

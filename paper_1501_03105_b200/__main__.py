@@ -53,6 +53,8 @@ def main(argv=None):
     ap.add_argument("--norm", choices=["preconditioned", "unpreconditioned"], default=None)
     ap.add_argument("--cold", action="store_true", help="cold-start every CG solve")
     ap.add_argument("--fixed-point-exit", action="store_true")
+    ap.add_argument("--cg-variant", choices=["hs", "cg"], default="hs",
+                    help="Hestenes-Stiefel PCG (default) or Chronopoulos-Gear (one reduction per iteration)")
     ap.add_argument("--rounding", choices=["sweep", "two_level", "both"], default="sweep")
     ap.add_argument("--lambda2", action="store_true", help="Cheeger-type lambda_2 (P:L207-226)")
     ap.add_argument("--exact", action="store_true", help="exact min cut mu* and delta (Eq. 13)")
@@ -69,7 +71,8 @@ def main(argv=None):
     opts = I.options(T=args.T, eps=args.eps, cg_rtol=rtol, cg_max_iter=cap,
                      cg_norm=I.IRLS_NORM_UNPRECONDITIONED if norm == "unpreconditioned" else I.IRLS_NORM_PRECONDITIONED,
                      warm_start=0 if args.cold else 1, fixed_point_exit=1 if args.fixed_point_exit else 0,
-                     record_trace=1 if args.trace else 0)
+                     record_trace=1 if args.trace else 0,
+                     cg_variant=I.IRLS_CG_CG if args.cg_variant == "cg" else I.IRLS_CG_HS)
     t0 = time.perf_counter()
     m = I.MinCut.from_spec(spec, opts)
     st = m.irls_get_stats()

@@ -145,6 +145,8 @@ int launch_pair_assemble(const StencilArgs &s, const VecArgs &v, const RedArgs &
 void launch_pair_pspmv(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
                        cudaStream_t st);
 void launch_pair_axpy(const VecArgs &v, const RedArgs &ra, const CondArgs &cd, cudaStream_t st);
+void launch_pair_cgcg(const StencilArgs &s, const VecArgs &v, const CgArgs &g, const RedArgs &ra, const CondArgs &cd,
+                      cudaStream_t st);
 void launch_pair_finish(const VecArgs &v, DevCtrl *ctrl, cudaStream_t st);
 // sell_pair.cu (widest slice <= 8): false when the generic SELL kernel must run
 bool launch_sellp_assemble(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, int mode,

@@ -645,6 +645,7 @@ void launch_cgcg_finish(const VecArgs &v, const DevCtrl *ctrl, cudaStream_t st)
 void launch_stencil_cgcg(const StencilArgs &s, const VecArgs &v, const CgArgs &g, const RedArgs &ra,
                          const CondArgs &cd, cudaStream_t st)
 {
+    if (s.nx % 2 == 0) return launch_pair_cgcg(s, v, g, ra, cd, st);
     k_cgcg_stencil<<<(unsigned)((v.n_own + kChunk - 1) / kChunk), kThreads, 0, st>>>(s, v, g, ra, cd);
 }
 

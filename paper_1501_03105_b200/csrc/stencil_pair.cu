@@ -513,6 +513,153 @@ __global__ void __launch_bounds__(kThreads) k_pair_axpy(VecArgs v, RedArgs ra, C
     }
 }
 
+// ---------------------------------------------------------------------------
+// Chronopoulos-Gear iteration on node pairs (nx even; O5', A31): the
+// kernels_cg.cu k_cgcg_stencil arithmetic with K3's data movement — every
+// load of the pair first, -x / +x neighbours' new z by shuffle (lanes 0 / 31
+// recompute theirs), -y / +y / -z / +z recomputed from r, w, s_old, Dinv.
+// ---------------------------------------------------------------------------
+struct CgNb {
+    double2 r, w, s, d;
+};
+
+template <int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_cgcg_pair(StencilArgs s, VecArgs v, CgArgs g, RedArgs ra, CondArgs cd)
+{
+    DevCtrl *ctrl = ra.ctrl;
+    if (ctrl->done) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) set_cond2(cd, ctrl);
+        return;
+    }
+    const int32_t k = ctrl->k;
+    const bool first = (k == 0);
+    const double alpha = ctrl->alpha, beta = ctrl->beta;
+    const double *__restrict__ rk = g.r[k & 1];
+    const double *__restrict__ wk = g.w[k & 1];
+    const double *__restrict__ so = g.s[(k + 1) & 1];
+    double *__restrict__ rn = g.r[(k + 1) & 1];
+    double *__restrict__ wn = g.w[(k + 1) & 1];
+    double *__restrict__ sn = g.s[k & 1];
+    const double *__restrict__ di = v.Dinv;
+    const int lane = threadIdx.x & 31;
+    const int64_t base = (int64_t)blockIdx.x * kChunk;
+    const int64_t P = s.P;
+    const double2 zero2 = make_double2(0.0, 0.0);
+    auto ldnb = [&](bool has, int64_t i) {
+        CgNb n{zero2, zero2, zero2, zero2};
+        if (has) {
+            n.r = ldp(rk, i);
+            n.w = ldp(wk, i);
+            if (!first) n.s = ldp(so, i);
+            n.d = ldp(di, i);
+        }
+        return n;
+    };
+    // new z of a neighbour: (r - alpha (w | w + beta s_old)) Dinv
+    auto znew = [&](double r, double w, double so_, double d) {
+        const double sv = first ? w : w + beta * so_;
+        return (r - alpha * sv) * d;
+    };
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 1
+    for (int j = 0; j < 8; j++) {
+        const int64_t u0 = base + 2 * (int64_t)threadIdx.x + 512 * j;
+        const bool valid = u0 < v.n_own;
+        const PairCoord c = pair_coord(s, s.lo + u0);
+        const bool hx = c.x0 > 0, hr = c.x0 + 1 < s.nx - 1;
+        const bool hy = valid && c.y > 0, py = valid && c.y < s.ny - 1;
+        const bool hz = valid && c.z > 0, pz = valid && c.z < s.nz - 1;
+        // ---- own pair first: s, z, p, x, r', z'
+        const CgNb own = ldnb(valid, u0);
+        const double2 po = (valid && !first) ? ldp(g.p, u0) : zero2;
+        const double2 gx2 = valid ? ldp(s.gx, u0) : zero2;
+        const double2 x2 = valid ? ldp_cg(v.x, u0) : zero2;
+        double el_r = 0.0, el_w = 0.0, el_s = 0.0, el_d = 0.0, gxe = 0.0;
+        double er_r = 0.0, er_w = 0.0, er_s = 0.0, er_d = 0.0;
+        if (valid && lane == 0 && hx) {
+            el_r = __ldg(rk + u0 - 1);
+            el_w = __ldg(wk + u0 - 1);
+            if (!first) el_s = __ldg(so + u0 - 1);
+            el_d = __ldg(di + u0 - 1);
+            gxe = __ldg(s.gx + u0 - 1);
+        }
+        if (valid && lane == 31 && hr) {
+            er_r = __ldg(rk + u0 + 2);
+            er_w = __ldg(wk + u0 + 2);
+            if (!first) er_s = __ldg(so + u0 + 2);
+            er_d = __ldg(di + u0 + 2);
+        }
+        const double s0 = first ? own.w.x : own.w.x + beta * own.s.x;
+        const double s1 = first ? own.w.y : own.w.y + beta * own.s.y;
+        const double z0 = own.r.x * own.d.x, z1 = own.r.y * own.d.y;
+        const double p0 = first ? z0 : z0 + beta * po.x;
+        const double p1 = first ? z1 : z1 + beta * po.y;
+        const double r0 = own.r.x - alpha * s0, r1 = own.r.y - alpha * s1;
+        const double zn0 = r0 * own.d.x, zn1 = r1 * own.d.y;
+        double zl = __shfl_up_sync(0xffffffffu, zn1, 1);
+        double zr = __shfl_down_sync(0xffffffffu, zn0, 1);
+        double gxl = __shfl_up_sync(0xffffffffu, gx2.y, 1);
+        if (!valid) continue;
+        if (lane == 0) { zl = znew(el_r, el_w, el_s, el_d); gxl = gxe; }
+        if (lane == 31) zr = znew(er_r, er_w, er_s, er_d);
+        if (!hx) { zl = 0.0; gxl = 0.0; }
+        if (!hr) zr = 0.0;
+        // ---- w' = D z' - sum_asc g z'_nbr (O2: -z, -y, -x, +x, +y, +z), one
+        // neighbour direction at a time (keeps the live state small)
+        auto zpair = [&](const CgNb &n) {
+            return make_double2(znew(n.r.x, n.w.x, n.s.x, n.d.x), znew(n.r.y, n.w.y, n.s.y, n.d.y));
+        };
+        double a = 0.0, b = 0.0;
+        {
+            const double2 gzm = hz ? ldp(s.gz, u0 - P) : zero2;
+            const double2 zz = zpair(ldnb(hz, u0 - P));
+            a = a + gzm.x * zz.x;
+            b = b + gzm.y * zz.y;
+        }
+        {
+            const double2 gym = hy ? ldp(s.gy, u0 - s.nx) : zero2;
+            const double2 zz = zpair(ldnb(hy, u0 - s.nx));
+            a = a + gym.x * zz.x;
+            b = b + gym.y * zz.y;
+        }
+        a = a + gxl * zl;
+        a = a + gx2.x * zn1;
+        b = b + gx2.x * zn0;
+        b = b + gx2.y * zr;
+        {
+            const double2 gy2 = ldp(s.gy, u0);
+            const double2 zz = zpair(ldnb(py, u0 + s.nx));
+            a = a + gy2.x * zz.x;
+            b = b + gy2.y * zz.y;
+        }
+        {
+            const double2 gz2 = ldp(s.gz, u0);
+            const double2 zz = zpair(ldnb(pz, u0 + P));
+            a = a + gz2.x * zz.x;
+            b = b + gz2.y * zz.y;
+        }
+        const double2 D2 = ldp(v.D, u0);
+        const double w0 = D2.x * zn0 - a, w1 = D2.y * zn1 - b;
+        stp(g.p, u0, make_double2(p0, p1));
+        stp(sn, u0, make_double2(s0, s1));
+        stp(v.x, u0, make_double2(x2.x + alpha * p0, x2.y + alpha * p1));
+        stp(rn, u0, make_double2(r0, r1));
+        stp(wn, u0, make_double2(w0, w1));
+        acc[0] = acc[0] + r0 * zn0;
+        acc[1] = acc[1] + zn0 * w0;
+        acc[2] = acc[2] + zn0 * zn0;
+        acc[3] = acc[3] + r0 * r0;
+        acc[0] = acc[0] + r1 * zn1;
+        acc[1] = acc[1] + zn1 * w1;
+        acc[2] = acc[2] + zn1 * zn1;
+        acc[3] = acc[3] + r1 * r1;
+    }
+    if (c3_chunk_epilogue<4>(acc, v.chunk0 + (int32_t)blockIdx.x, ra) && cd.finalize && threadIdx.x == 0) {
+        finalize_cgcg(ctrl, ra.slots);
+        set_cond2(cd, ctrl);
+    }
+}
+
 // After the loop: x += alpha_{k-1} p_{k-1} (or 0 when b = 0); grid-stride over
 // pairs with a small grid, so an idle call (k = 0) costs one short launch.
 __global__ void __launch_bounds__(256) k_pair_finish(VecArgs v, const DevCtrl *ctrl)
@@ -575,6 +722,14 @@ void launch_pair_pspmv(const StencilArgs &s, const VecArgs &v, const RedArgs &ra
 void launch_pair_axpy(const VecArgs &v, const RedArgs &ra, const CondArgs &cd, cudaStream_t st)
 {
     k_pair_axpy<<<nblk(v.n_own), kThreads, 0, st>>>(v, ra, cd);
+}
+
+void launch_pair_cgcg(const StencilArgs &s, const VecArgs &v, const CgArgs &g, const RedArgs &ra, const CondArgs &cd,
+                      cudaStream_t st)
+{
+    // 3 CTAs/SM (80 registers): config 4 282.8 ms per step vs 293.9 (2 CTAs/SM)
+    // and 379.6 (1 CTA/SM, 180 registers); the generic per-node kernel 326.5
+    k_cgcg_pair<3><<<nblk(v.n_own), kThreads, 0, st>>>(s, v, g, ra, cd);
 }
 
 void launch_pair_finish(const VecArgs &v, DevCtrl *ctrl, cudaStream_t st)
