@@ -343,8 +343,8 @@ static irls_status enq_assemble(Ranks &R, int mode, const CondArgs &cd, cudaStre
         for (irls_ctx *c : R) {
             VecArgs v = vec_args(c);
             v.q = c->cg_w[0];
-            if (c->kind == 0) launch_stencil_pspmv(stencil_args(c, false), v, red_args_solve(c), cd, st);
-            else launch_sell_pspmv(sell_args(c), v, red_args_solve(c), cd, st);
+            if (c->kind == 0) launch_stencil_pspmv(stencil_args(c, false), v, red_args_solve(c), cd, st, true);
+            else launch_sell_pspmv(sell_args(c), v, red_args_solve(c), cd, st, true);
             c->launches++;
         }
         if (R[0]->multi) {

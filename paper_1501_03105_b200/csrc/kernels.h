@@ -79,9 +79,9 @@ int launch_sell_assemble_ex(const SellArgs &s, const VecArgs &v, const RedArgs &
                              int mode, double eps, double *gs_out, double *gt_out, cudaStream_t st);
 // K3: p = z + beta p_old (fused), lazy x += alpha p_old, q = L~ p, PQ reduction
 void launch_stencil_pspmv(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
-                          cudaStream_t st);
+                          cudaStream_t st, bool w0 = false);
 void launch_sell_pspmv(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
-                       cudaStream_t st);
+                       cudaStream_t st, bool w0 = false);
 // small.cu: the whole CG loop of a <= one-chunk graph in one block (kind 0
 // stencil, 1 SELL); runs after the assembly, before finish / report
 void small_cg_prepare();  // once per process, outside stream capture (128 KB dynamic shared memory)
@@ -143,7 +143,7 @@ void launch_vminmax(DevCtrl *const *ctrl, int W, cudaStream_t st);
 int launch_pair_assemble(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, int mode,
                           double eps, double *gs_out, double *gt_out, cudaStream_t st);
 void launch_pair_pspmv(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
-                       cudaStream_t st);
+                       cudaStream_t st, bool w0 = false);
 void launch_pair_axpy(const VecArgs &v, const RedArgs &ra, const CondArgs &cd, cudaStream_t st);
 void launch_pair_cgcg(const StencilArgs &s, const VecArgs &v, const CgArgs &g, const RedArgs &ra, const CondArgs &cd,
                       cudaStream_t st);
@@ -151,7 +151,7 @@ void launch_pair_finish(const VecArgs &v, DevCtrl *ctrl, cudaStream_t st);
 // sell_pair.cu (widest slice <= 8): false when the generic SELL kernel must run
 bool launch_sellp_assemble(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, int mode,
                            double eps, double *gs_out, double *gt_out, cudaStream_t st);
-bool launch_sellp_pspmv(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, cudaStream_t st);
+bool launch_sellp_pspmv(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, cudaStream_t st, bool w0 = false);
 
 // ---------------------------------------------------------------------------
 // Sweep cut (K8-K12)

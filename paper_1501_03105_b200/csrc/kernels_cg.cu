@@ -190,10 +190,11 @@ __global__ void __launch_bounds__(kThreads) k_sell_assemble(SellArgs s, VecArgs 
 // its neighbours (O9(ii)); lazy x += alpha_{k-1} p_{k-1}; q = L~ p (O2);
 // PQ reduction.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) k_stencil_pspmv(StencilArgs s, VecArgs v, RedArgs ra, CondArgs cd)
+__global__ void __launch_bounds__(kThreads) k_stencil_pspmv(StencilArgs s, VecArgs v, RedArgs ra, CondArgs cd,
+                                                            bool w0)
 {
     const DevCtrl *ctrl = ra.ctrl;
-    if (ctrl->done) return;  // CG-CG's w0 pass after a START that stopped
+    if (w0 && ctrl->done) return;  // CG-CG's w0 pass after a START that stopped
     const int32_t k = ctrl->k;
     const bool first = (k == 0);
     const double beta = ctrl->beta, alpha = ctrl->alpha;
@@ -222,14 +223,14 @@ __global__ void __launch_bounds__(kThreads) k_stencil_pspmv(StencilArgs s, VecAr
 #undef PVAL
     if (c3_chunk_epilogue<1>(acc, v.chunk0 + (int32_t)blockIdx.x, ra) && cd.finalize && threadIdx.x == 0) {
         finalize_pq(ra.ctrl, ra.slots);
-        set_cond(cd, ra.ctrl);
+        if (w0) set_cond(cd, ra.ctrl);
     }
 }
 
-__global__ void __launch_bounds__(kThreads) k_sell_pspmv(SellArgs s, VecArgs v, RedArgs ra, CondArgs cd)
+__global__ void __launch_bounds__(kThreads) k_sell_pspmv(SellArgs s, VecArgs v, RedArgs ra, CondArgs cd, bool w0)
 {
     const DevCtrl *ctrl = ra.ctrl;
-    if (ctrl->done) return;  // CG-CG's w0 pass after a START that stopped
+    if (w0 && ctrl->done) return;  // CG-CG's w0 pass after a START that stopped
     const int32_t k = ctrl->k;
     const bool first = (k == 0);
     const double beta = ctrl->beta, alpha = ctrl->alpha;
@@ -259,7 +260,7 @@ __global__ void __launch_bounds__(kThreads) k_sell_pspmv(SellArgs s, VecArgs v, 
 #undef PVAL
     if (c3_chunk_epilogue<1>(acc, v.chunk0 + (int32_t)blockIdx.x, ra) && cd.finalize && threadIdx.x == 0) {
         finalize_pq(ra.ctrl, ra.slots);
-        set_cond(cd, ra.ctrl);
+        if (w0) set_cond(cd, ra.ctrl);
     }
 }
 
@@ -739,16 +740,17 @@ int launch_sell_assemble_ex(const SellArgs &s, const VecArgs &v, const RedArgs &
 }
 
 void launch_stencil_pspmv(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
-                          cudaStream_t st)
+                          cudaStream_t st, bool w0)
 {
-    if (s.nx % 2 == 0) return launch_pair_pspmv(s, v, ra, cd, st);
-    k_stencil_pspmv<<<nblocks(v.n_own), kThreads, 0, st>>>(s, v, ra, cd);
+    if (s.nx % 2 == 0) return launch_pair_pspmv(s, v, ra, cd, st, w0);
+    k_stencil_pspmv<<<nblocks(v.n_own), kThreads, 0, st>>>(s, v, ra, cd, w0);
 }
 
-void launch_sell_pspmv(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, cudaStream_t st)
+void launch_sell_pspmv(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, cudaStream_t st,
+                       bool w0)
 {
-    if (launch_sellp_pspmv(s, v, ra, cd, st)) return;
-    k_sell_pspmv<<<nblocks(v.n_own), kThreads, 0, st>>>(s, v, ra, cd);
+    if (launch_sellp_pspmv(s, v, ra, cd, st, w0)) return;
+    k_sell_pspmv<<<nblocks(v.n_own), kThreads, 0, st>>>(s, v, ra, cd, w0);
 }
 
 void launch_ghost_pupdate(const VecArgs &v, int64_t ghost_lo, int64_t ghost_hi, int64_t plane, DevCtrl *ctrl,

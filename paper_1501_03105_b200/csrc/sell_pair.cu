@@ -140,11 +140,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sellp_assemble(SellArgs s, V
     }
 }
 
-template <int WMAX, int MINB>
+template <int WMAX, int MINB, bool W0>
 __global__ void __launch_bounds__(kThreads, MINB) k_sellp_pspmv(SellArgs s, VecArgs v, RedArgs ra, CondArgs cd)
 {
     const DevCtrl *ctrl = ra.ctrl;
-    if (ctrl->done) return;  // CG-CG's w0 pass after a START that stopped
+    if (W0 && ctrl->done) return;  // CG-CG's w0 pass after a START that stopped
     const int32_t it = ctrl->k;
     const bool first = (it == 0);
     const double beta = ctrl->beta, alpha = ctrl->alpha;
@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sellp_pspmv(SellArgs s, VecA
     }
     if (c3_chunk_epilogue<1>(acc, v.chunk0 + (int32_t)blockIdx.x, ra) && cd.finalize && threadIdx.x == 0) {
         finalize_pq(ra.ctrl, ra.slots);
-        set_cond3(cd, ra.ctrl);
+        if (W0) set_cond3(cd, ra.ctrl);
     }
 }
 
@@ -241,12 +241,15 @@ bool launch_sellp_assemble(const SellArgs &s, const VecArgs &v, const RedArgs &r
     return true;
 }
 
-bool launch_sellp_pspmv(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, cudaStream_t st)
+bool launch_sellp_pspmv(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, cudaStream_t st,
+                        bool w0)
 {
     // 3 CTAs/SM (80 registers, 48 B spilled): config 3 0.47 ms vs 0.52 ms at
     // 2 CTAs/SM (105 registers) and 0.49 ms at 4 (64 registers)
-    if (s.wmax <= 4) k_sellp_pspmv<4, 3><<<nblk3(v.n_own), kThreads, 0, st>>>(s, v, ra, cd);
-    else if (s.wmax <= 8) k_sellp_pspmv<8, 1><<<nblk3(v.n_own), kThreads, 0, st>>>(s, v, ra, cd);
+    if (s.wmax <= 4 && w0) k_sellp_pspmv<4, 3, true><<<nblk3(v.n_own), kThreads, 0, st>>>(s, v, ra, cd);
+    else if (s.wmax <= 4) k_sellp_pspmv<4, 3, false><<<nblk3(v.n_own), kThreads, 0, st>>>(s, v, ra, cd);
+    else if (s.wmax <= 8 && w0) k_sellp_pspmv<8, 1, true><<<nblk3(v.n_own), kThreads, 0, st>>>(s, v, ra, cd);
+    else if (s.wmax <= 8) k_sellp_pspmv<8, 1, false><<<nblk3(v.n_own), kThreads, 0, st>>>(s, v, ra, cd);
     else return false;
     return true;
 }

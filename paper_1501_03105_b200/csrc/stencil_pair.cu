@@ -361,10 +361,14 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_fused(StencilArgs s, Ve
 // ---------------------------------------------------------------------------
 // K3: p = z + beta p_old (recomputed for neighbours), lazy x update, q = L~ p
 // ---------------------------------------------------------------------------
+// W0: CG-CG's w0 = A z0 pass (k = 0), which runs after the START stopping
+// test: it returns at once when that test already stopped the solve, and its
+// fused finalize also sets the loop condition (alpha_0 breakdown).
+template <bool W0>
 __global__ void __launch_bounds__(kThreads) k_pair_pspmv(StencilArgs s, VecArgs v, RedArgs ra, CondArgs cd)
 {
     const DevCtrl *ctrl = ra.ctrl;
-    if (ctrl->done) return;  // CG-CG's w0 pass after a START that stopped
+    if (W0 && ctrl->done) return;
     const int32_t k = ctrl->k;
     const bool first = (k == 0);
     const double beta = ctrl->beta, alpha = ctrl->alpha;
@@ -456,7 +460,7 @@ __global__ void __launch_bounds__(kThreads) k_pair_pspmv(StencilArgs s, VecArgs 
     }
     if (c3_chunk_epilogue<1>(acc, v.chunk0 + (int32_t)blockIdx.x, ra) && cd.finalize && threadIdx.x == 0) {
         finalize_pq(ra.ctrl, ra.slots);
-        set_cond2(cd, ra.ctrl);
+        if (W0) set_cond2(cd, ra.ctrl);
     }
 }
 
@@ -714,9 +718,10 @@ int launch_pair_assemble(const StencilArgs &s, const VecArgs &v, const RedArgs &
 }
 
 void launch_pair_pspmv(const StencilArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd,
-                       cudaStream_t st)
+                       cudaStream_t st, bool w0)
 {
-    k_pair_pspmv<<<nblk(v.n_own), kThreads, 0, st>>>(s, v, ra, cd);
+    if (w0) k_pair_pspmv<true><<<nblk(v.n_own), kThreads, 0, st>>>(s, v, ra, cd);
+    else k_pair_pspmv<false><<<nblk(v.n_own), kThreads, 0, st>>>(s, v, ra, cd);
 }
 
 void launch_pair_axpy(const VecArgs &v, const RedArgs &ra, const CondArgs &cd, cudaStream_t st)
