@@ -243,6 +243,14 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    def fresh_comm():
+        """A new NCCL id for every communicator (an id serves one create)."""
+        if world == 1:
+            return comm
+        obj = [I.irls_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return I.comm_desc(world, rank, local, obj[0], stream.cuda_stream, memory=mem)
+
     def max_over_ranks(v):
         if world == 1:
             return v
@@ -284,7 +292,8 @@ def main():
     fpx = None
     if not args.no_fixed_point_exit:
         m.close()
-        m = I.MinCut.from_spec(spec, I.options(T=T, loop_mode=args.loop_mode, fixed_point_exit=1, p2p=args.p2p, cg_variant=cgv), comm)
+        m = I.MinCut.from_spec(spec, I.options(T=T, loop_mode=args.loop_mode, fixed_point_exit=1, p2p=args.p2p,
+                                               cg_variant=cgv), fresh_comm())
         for _ in range(args.warmup):
             m.irls_solve(I.IRLS_FROM_SCRATCH, T=T, reports=False)
             m.irls_sweep_cut(side=False)
@@ -381,11 +390,7 @@ def main():
     import ctypes as C
 
     def e2e_step():
-        nonlocal comm
-        if world > 1:  # a fresh NCCL id per communicator (part of the user's create path)
-            obj = [I.irls_nccl_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(obj, src=0)
-            comm = I.comm_desc(world, rank, local, obj[0], stream.cuda_stream, memory=mem)
+        comm = fresh_comm()  # a fresh NCCL id per communicator (part of the user's create path)
         if csr:
             mm = I.MinCut.irls_mincut_create_csr(spec["n"], pinned["row_ptr"], pinned["col"], pinned["w"], spec["s"],
                                                  spec["t"], opts, comm)
