@@ -368,10 +368,9 @@ static irls_status enq_body_cgcg(Ranks &R, const CondArgs &cd, cudaStream_t st)
     for (int half = 0; half < 2; half++) {
         for (irls_ctx *c : R) {
             const VecArgs v = vec_args(c);
-            const CgArgs g = cg_args(c);
-            if (c->kind == 0) launch_stencil_cgcg(stencil_args(c, false), v, g, red_args_solve(c), cd, st);
-            else launch_sell_cgcg(sell_args(c), v, g, red_args_solve(c), cd, st);
-            c->launches++;
+            CgArgs g = cg_args(c);
+            // ghost s, r first (they only read this iteration's ghost values,
+            // which peers may overwrite once this rank's sums are published)
             if (c->multi && c->kind == 0) {
                 if (c->lo_ghost) launch_cgcg_ghost(g, -c->P, c->P, c->ctrl, st);
                 if (c->hi_ghost) launch_cgcg_ghost(g, c->n_own, c->P, c->ctrl, st);
@@ -380,6 +379,16 @@ static irls_status enq_body_cgcg(Ranks &R, const CondArgs &cd, cudaStream_t st)
                 launch_cgcg_ghost(g, c->npad_own, c->n_ghost, c->ctrl, st);
                 c->launches++;
             }
+            if (c->p2p && c->kind == 0) {  // the w halo fused into the iteration kernel (peer stores)
+                for (int b = 0; b < 2; b++) {
+                    g.wpeer_lo[b] = c->wpeer_lo[b];
+                    g.wpeer_hi[b] = c->wpeer_hi[b];
+                }
+                g.plane = c->P;
+            }
+            if (c->kind == 0) launch_stencil_cgcg(stencil_args(c, false), v, g, red_args_solve(c), cd, st);
+            else launch_sell_cgcg(sell_args(c), v, g, red_args_solve(c), cd, st);
+            c->launches++;
         }
         if (R[0]->multi) {
             if ((s = coll_allreduce(R, 4, st))) return s;
@@ -387,7 +396,8 @@ static irls_status enq_body_cgcg(Ranks &R, const CondArgs &cd, cudaStream_t st)
                 launch_finalize(PH_CG, c->ctrl, c->slots_glob, cd, p2p_wait_args(c), st);
                 c->launches++;
             }
-            if ((s = coll_halo_sel(R, half == 0 ? sel_w1 : sel_w0, st))) return s;
+            if (!(R[0]->p2p && R[0]->kind == 0) && (s = coll_halo_sel(R, half == 0 ? sel_w1 : sel_w0, st)))
+                return s;
         }
     }
     return last_launch(R[0], "cg-cg body");
@@ -400,9 +410,9 @@ static irls_status enq_body(Ranks &R, const CondArgs &cd, cudaStream_t st)
     for (irls_ctx *c : R) {
         const VecArgs v = vec_args(c);
         const RedArgs ra = red_args_solve(c);
-        if (c->kind == 0) launch_stencil_pspmv(stencil_args(c, false), v, ra, cd, st);
-        else launch_sell_pspmv(sell_args(c), v, ra, cd, st);
-        c->launches++;
+        // ghost p first: it reads the ghost z of this iteration, which a
+        // neighbour's K5 may overwrite over peer memory (p2p) as soon as this
+        // rank's K3 has published its group sums
         if (c->multi && c->kind == 0) {
             launch_ghost_pupdate(v, c->lo_ghost, c->hi_ghost, c->P, c->ctrl, st);
             c->launches++;
@@ -410,6 +420,9 @@ static irls_status enq_body(Ranks &R, const CondArgs &cd, cudaStream_t st)
             launch_ghost_range_pupdate(v, c->npad_own, c->n_ghost, c->ctrl, st);
             c->launches++;
         }
+        if (c->kind == 0) launch_stencil_pspmv(stencil_args(c, false), v, ra, cd, st);
+        else launch_sell_pspmv(sell_args(c), v, ra, cd, st);
+        c->launches++;
     }
     if (R[0]->multi) {
         if ((s = coll_allreduce(R, 1, st))) return s;
@@ -1172,6 +1185,16 @@ static irls_status vgroup_create(irls_vgroup **out, int32_t world, int32_t devic
             if (c->kind == 0 && c->hplan.peer_hi >= 0) {
                 irls_ctx *o = g->ranks[c->hplan.peer_hi];
                 c->zpeer_hi = o->z + o->hplan.recv_lo;
+            }
+            for (int b = 0; b < 2 && c->cgcg && c->kind == 0; b++) {
+                if (c->hplan.peer_lo >= 0) {
+                    irls_ctx *o = g->ranks[c->hplan.peer_lo];
+                    c->wpeer_lo[b] = o->cg_w[b] + o->hplan.recv_hi;
+                }
+                if (c->hplan.peer_hi >= 0) {
+                    irls_ctx *o = g->ranks[c->hplan.peer_hi];
+                    c->wpeer_hi[b] = o->cg_w[b] + o->hplan.recv_lo;
+                }
             }
         }
     }

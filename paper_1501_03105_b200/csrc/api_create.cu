@@ -64,20 +64,29 @@ static irls_status alloc_solver(irls_ctx *c, int64_t ghost)
         c->raw_allocs.push_back(p);
         return (double *)p;
     };
+    double *last_base = nullptr;
     auto ghosted = [&](double *&ptr, bool export_) -> bool {
         double *b = export_ ? raw(npad + 2 * gpad) : dalloc<double>(c, npad + 2 * gpad);
         if (!b) return false;
         ptr = b + gpad;
-        if (export_) c->z_base = b;
+        last_base = b;
         return true;
     };
-    if (!ghosted(c->x, false) || !ghosted(c->z, ipc && c->kind == 0) || !ghosted(c->p0, false) ||
-        !ghosted(c->p1, false) || !ghosted(c->r, false) || !ghosted(c->Dinv, false))
+    const bool ipc_z = ipc && c->kind == 0;  // z (and CG-CG's w) planes are stored into by the neighbours
+    if (!ghosted(c->z, ipc_z)) return IRLS_ERR_OOM;
+    if (ipc_z) c->z_base = last_base;
+    if (!ghosted(c->x, false) || !ghosted(c->p0, false) || !ghosted(c->p1, false) || !ghosted(c->r, false) ||
+        !ghosted(c->Dinv, false))
         return IRLS_ERR_OOM;
     c->cgcg = c->opt.cg_variant == IRLS_CG_CG;
-    if (c->cgcg && (!ghosted(c->cg_r2, false) || !ghosted(c->cg_w[0], false) || !ghosted(c->cg_w[1], false) ||
-                    !ghosted(c->cg_s[0], false) || !ghosted(c->cg_s[1], false)))
-        return IRLS_ERR_OOM;
+    if (c->cgcg) {
+        for (int b = 0; b < 2; b++) {
+            if (!ghosted(c->cg_w[b], ipc_z)) return IRLS_ERR_OOM;
+            if (ipc_z) c->w_base[b] = last_base;
+        }
+        if (!ghosted(c->cg_r2, false) || !ghosted(c->cg_s[0], false) || !ghosted(c->cg_s[1], false))
+            return IRLS_ERR_OOM;
+    }
     if (c->p2p) {
         const int64_t nb = 2 * kMaxQ * kGroups + 1;  // slots by parity + the arrival counter
         c->p2p_buf = ipc ? raw(nb) : dalloc<double>(c, nb);
@@ -125,8 +134,8 @@ irls_status p2p_set_peers(irls_ctx *c, const std::vector<double *> &bufs)
 
 // One rank's exported buffers, exchanged with an NCCL all-gather at create.
 struct PeerRec {
-    cudaIpcMemHandle_t hbuf, hz;
-    int64_t zoff_recv_lo, zoff_recv_hi;  // ghost planes, in doubles from z's allocation start
+    cudaIpcMemHandle_t hbuf, hz, hw[2];
+    int64_t zoff_recv_lo, zoff_recv_hi;  // ghost planes, in doubles from the allocation start (z and w alike)
 };
 
 static irls_status p2p_exchange(irls_ctx *c)
@@ -139,6 +148,8 @@ static irls_status p2p_exchange(irls_ctx *c)
         CK(cudaIpcGetMemHandle(&mine.hz, c->z_base));
         mine.zoff_recv_lo = (c->z - c->z_base) + c->hplan.recv_lo;
         mine.zoff_recv_hi = (c->z - c->z_base) + c->hplan.recv_hi;
+        if (c->cgcg)
+            for (int b = 0; b < 2; b++) CK(cudaIpcGetMemHandle(&mine.hw[b], c->w_base[b]));
     }
     std::vector<PeerRec> all(W);
     void *dev = nullptr;
@@ -177,6 +188,16 @@ static irls_status p2p_exchange(irls_ctx *c)
         if (c->hplan.peer_hi >= 0) {
             if ((s = open(all[c->hplan.peer_hi].hz, &b))) return s;
             c->zpeer_hi = b + all[c->hplan.peer_hi].zoff_recv_lo;
+        }
+        for (int w = 0; w < 2 && c->cgcg; w++) {  // same ghosted layout as z
+            if (c->hplan.peer_lo >= 0) {
+                if ((s = open(all[c->hplan.peer_lo].hw[w], &b))) return s;
+                c->wpeer_lo[w] = b + all[c->hplan.peer_lo].zoff_recv_hi;
+            }
+            if (c->hplan.peer_hi >= 0) {
+                if ((s = open(all[c->hplan.peer_hi].hw[w], &b))) return s;
+                c->wpeer_hi[w] = b + all[c->hplan.peer_hi].zoff_recv_lo;
+            }
         }
     }
     return p2p_set_peers(c, bufs);

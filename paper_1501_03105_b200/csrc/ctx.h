@@ -131,6 +131,8 @@ struct irls_ctx {
     unsigned long long **d_pcnt = nullptr;  // device [world]: every rank's arrival counter
     int32_t n_groups_all = 0;     // non-empty C3 groups over all ranks (arrivals per reduction)
     double *zpeer_lo = nullptr, *zpeer_hi = nullptr;  // neighbours' z ghost planes (z-slabs)
+    double *wpeer_lo[2] = {nullptr, nullptr}, *wpeer_hi[2] = {nullptr, nullptr};  // CG-CG: neighbours' w ghost planes
+    double *w_base[2] = {nullptr, nullptr};  // CG-CG w allocations (IPC export)
     double *z_base = nullptr;     // start of z's allocation (IPC export)
     std::vector<void *> raw_allocs;  // cudaMalloc'd, IPC-exportable (multi-process p2p)
     std::vector<void *> ipc_open;    // peers' allocations opened with cudaIpcOpenMemHandle

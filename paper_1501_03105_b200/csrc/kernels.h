@@ -37,6 +37,10 @@ struct VecArgs {
 struct CgArgs {
     double *r[2], *w[2], *s[2];  // ghosted like x
     double *p;
+    // z-slabs with irls_options.p2p: the new w of the first / last owned plane
+    // is also stored into the lower / upper neighbour's ghost plane of w[b]
+    double *wpeer_lo[2] = {nullptr, nullptr}, *wpeer_hi[2] = {nullptr, nullptr};
+    int64_t plane = 0;
 };
 
 struct StencilArgs {

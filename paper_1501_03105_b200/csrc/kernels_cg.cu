@@ -574,6 +574,8 @@ __global__ void __launch_bounds__(kThreads) k_cgcg_stencil(StencilArgs s, VecArg
 {
     CG_PROLOGUE()
     const int64_t P = s.P;
+    double *wl = g.wpeer_lo[(k + 1) & 1], *wh = g.wpeer_hi[(k + 1) & 1];
+    bool peer = false;
     FOR_CHUNK_NODES({
         const Coord c = coord_of(s, s.lo + u);
         double a = 0.0;
@@ -584,7 +586,10 @@ __global__ void __launch_bounds__(kThreads) k_cgcg_stencil(StencilArgs s, VecArg
         if (c.y < s.ny - 1) a = a + s.gy[u] * CG_ZNEW(u + s.nx);
         if (c.z < s.nz - 1) a = a + s.gz[u] * CG_ZNEW(u + P);
         CG_NODE_TAIL()
+        if (wl && u < g.plane) { wl[u] = wu; peer = true; }  // fused w halo (p2p)
+        if (wh && u >= v.n_own - g.plane) { wh[u - (v.n_own - g.plane)] = wu; peer = true; }
     })
+    if (peer) __threadfence_system();
     CG_EPILOGUE()
 }
 

@@ -565,6 +565,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_cgcg_pair(StencilArgs s, Vec
         return (r - alpha * sv) * d;
     };
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    double *wl = g.wpeer_lo[(k + 1) & 1], *wh = g.wpeer_hi[(k + 1) & 1];
+    bool peer = false;
 #pragma unroll 1
     for (int j = 0; j < 8; j++) {
         const int64_t u0 = base + 2 * (int64_t)threadIdx.x + 512 * j;
@@ -649,6 +651,16 @@ __global__ void __launch_bounds__(kThreads, MINB) k_cgcg_pair(StencilArgs s, Vec
         stp(v.x, u0, make_double2(x2.x + alpha * p0, x2.y + alpha * p1));
         stp(rn, u0, make_double2(r0, r1));
         stp(wn, u0, make_double2(w0, w1));
+        if (wl && u0 < g.plane) {  // fused w halo (p2p): first owned plane -> lower neighbour
+            wl[u0] = w0;
+            wl[u0 + 1] = w1;
+            peer = true;
+        }
+        if (wh && u0 >= v.n_own - g.plane) {  // last owned plane -> upper neighbour
+            wh[u0 - (v.n_own - g.plane)] = w0;
+            wh[u0 + 1 - (v.n_own - g.plane)] = w1;
+            peer = true;
+        }
         acc[0] = acc[0] + r0 * zn0;
         acc[1] = acc[1] + zn0 * w0;
         acc[2] = acc[2] + zn0 * zn0;
@@ -658,6 +670,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_cgcg_pair(StencilArgs s, Vec
         acc[2] = acc[2] + zn1 * zn1;
         acc[3] = acc[3] + r1 * r1;
     }
+    if (peer) __threadfence_system();
     if (c3_chunk_epilogue<4>(acc, v.chunk0 + (int32_t)blockIdx.x, ra) && cd.finalize && threadIdx.x == 0) {
         finalize_cgcg(ctrl, ra.slots);
         set_cond2(cd, ctrl);

@@ -144,15 +144,17 @@ def test_vgroup_csr_strips(irls, world, p2p):
     g.close()
 
 
+@pytest.mark.parametrize("p2p", [0, 1])
 @pytest.mark.parametrize("loop_mode", [1, 2])
-def test_nccl_one_rank(irls, loop_mode):
+def test_nccl_one_rank(irls, loop_mode, p2p):
     import torch
     spec = gen.blob_grid(64, 64, 16, seed=3, sigma=(3.0, 8.0))
     T = 10
     S = oracle.Solver(oracle.Graph(spec), T=T, cg_variant=1)
     S.run(record=False)
     comm = irls.comm_desc(1, 0, 0, irls.irls_nccl_unique_id(), torch.cuda.current_stream().cuda_stream)
-    g = irls.MinCut.from_spec(spec, irls.options(T=T, loop_mode=loop_mode, cg_variant=irls.IRLS_CG_CG), comm)
+    g = irls.MinCut.from_spec(spec, irls.options(T=T, loop_mode=loop_mode, cg_variant=irls.IRLS_CG_CG, p2p=p2p),
+                              comm)
     g.irls_solve(irls.IRLS_FROM_SCRATCH, T=T)
     assert np.array_equal(g.irls_get_potentials(), S.x())
     g.close()
