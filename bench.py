@@ -345,6 +345,16 @@ def main():
                                  "bytes_per_node": K1_BYTES_PER_NODE},
     }
     cg_iter_ms = t_k3 + t_k5
+    roof_name = "K3 fused p-update + SpMV + p.q " + ("(SELL-64 CSR)" if csr else "(stencil)")
+    roof_bytes, roof_ms = k3_bytes, t_k3
+    if cgv == I.IRLS_CG_CG:  # the single kernel of a Chronopoulos-Gear iteration
+        t_cg = m.irls_time_kernel(I.KERNEL_CGCG, 20)
+        cg_bytes = (96 * n_own + 12 * ent) if csr else 120 * n_own
+        kernels["CGCG_iteration"] = {"ms": t_cg, "GBps": cg_bytes / (t_cg * 1e-3) / 1e9, "bytes_per_launch": cg_bytes}
+        cg_iter_ms = t_cg
+        roof_name, roof_bytes, roof_ms = "Chronopoulos-Gear iteration (one kernel)", cg_bytes, t_cg
+        ach = roof_bytes / (roof_ms * 1e-3) / 1e9
+        traffic = None
     # ---- N > 1: the z halo against the NVLink roofline (the bytes each rank
     # sends per CG iteration over the measured 770 GB/s per-direction peer
     # bandwidth of B200_PROFILING.md; 900 GB/s nominal)
@@ -445,8 +455,7 @@ def main():
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                      "traffic": traffic, "traffic_note": "ncu dram__bytes_read+write per K3 launch "
                      "(profiles/r01_k3_traffic.json) over the live K3 duration, GB/s; algorithmic bytes per launch "
-                     f"= {k3_bytes / 1e9:.3f} GB", "kernel": "K3 fused p-update + SpMV + p.q "
-                     + ("(SELL-64 CSR)" if csr else "(stencil)"),
+                     f"= {roof_bytes / 1e9:.3f} GB", "kernel": roof_name,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks
                      else "fallback 6650 GB/s (B200_PROFILING.md)",
                      "frac_of_nominal_8TBps": ach / 8000.0, "kernels": kernels},

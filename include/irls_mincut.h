@@ -95,8 +95,9 @@ typedef struct {
                             collectives go over peer memory, fused into the kernels that produce their data
                             (DESIGN.md §6): each group owner stores its C3 slot sums straight into every
                             rank's slot buffer and bumps an arrival counter that the finalize kernel waits
-                            on (no slot allreduce), and on z-slabs K5 also stores z's boundary planes into
-                            the neighbours' ghost planes (no per-iteration halo exchange).  Peer buffers
+                            on (no slot allreduce), and on z-slabs K5 (CG-CG: the iteration kernel) also
+                            stores z's (w's) boundary planes into the neighbours' ghost planes (no
+                            per-iteration halo exchange).  Peer buffers
                             are exchanged at create with CUDA IPC handles over NCCL (allocated with
                             cudaMalloc, outside device_alloc); virtual groups use the other ranks' buffers
                             directly.  Results are bit-identical to p2p = 0.  A wait longer than 10 s
@@ -307,7 +308,9 @@ irls_status irls_get_stats(irls_ctx *ctx, irls_stats *stats);
  * which = 3 (multi-rank NCCL contexts only; COLLECTIVE: every rank calls it
  * with the same reps): the per-CG-iteration z halo exchange (one plane / the
  * packed send lists to each neighbour over NCCL), timed on this rank; it only
- * rewrites z's ghost entries with the values they already hold. */
+ * rewrites z's ghost entries with the values they already hold.
+ * which = 4 (cg_variant = IRLS_CG_CG only): the Chronopoulos-Gear iteration
+ * kernel (one iteration at k = 1; state saved and restored as above). */
 irls_status irls_time_kernel(irls_ctx *ctx, int32_t which, int32_t reps, float *mean_ms);
 
 void irls_mincut_destroy(irls_ctx *ctx);

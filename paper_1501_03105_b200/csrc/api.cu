@@ -989,7 +989,8 @@ extern "C" irls_status irls_get_stats(irls_ctx *c, irls_stats *o)
 extern "C" irls_status irls_time_kernel(irls_ctx *c, int32_t which, int32_t reps, float *mean_ms)
 {
     GUARD(c);
-    if (!mean_ms || reps < 1 || which < 0 || which > 3) return IRLS_ERR_INVALID_ARGUMENT;
+    if (!mean_ms || reps < 1 || which < 0 || which > 4) return IRLS_ERR_INVALID_ARGUMENT;
+    if (which == 4 && !c->cgcg) return fail(c, IRLS_ERR_INVALID_ARGUMENT, "CG-CG kernel timing needs cg_variant 1");
     if (c->state == 0) return fail(c, IRLS_ERR_STATE, "time_kernel needs a solved state");
     cudaStream_t st = c->stream;
     if (which == 3) {  // the z halo (NCCL), collective
@@ -1013,7 +1014,9 @@ extern "C" irls_status irls_time_kernel(irls_ctx *c, int32_t which, int32_t reps
     }
     const int64_t npad = (int64_t)c->nchunks * kChunk;
     // snapshot everything the kernels write
-    double *arrs[] = {c->x, c->q, c->r, c->z, c->p0, c->p1, c->D, c->Dinv};
+    std::vector<double *> arrs = {c->x, c->q, c->r, c->z, c->p0, c->p1, c->D, c->Dinv};
+    if (c->cgcg)
+        for (double *a : {c->cg_r2, c->cg_w[0], c->cg_w[1], c->cg_s[0], c->cg_s[1]}) arrs.push_back(a);
     std::vector<double *> save;
     for (double *a : arrs) {
         double *b = nullptr;
@@ -1055,6 +1058,9 @@ extern "C" irls_status irls_time_kernel(irls_ctx *c, int32_t which, int32_t reps
             else launch_sell_pspmv(sell_args(c), v, ra, cd, st);
         } else if (which == 1) {
             launch_axpy_jacobi(v, ra, cd, st);
+        } else if (which == 4) {
+            if (c->kind == 0) launch_stencil_cgcg(stencil_args(c, false), v, cg_args(c), ra, cd, st);
+            else launch_sell_cgcg(sell_args(c), v, cg_args(c), ra, cd, st);
         } else {
             if (c->kind == 0) launch_stencil_assemble(stencil_args(c, false), v, ra, cd, mode, c->opt.eps, st);
             else launch_sell_assemble(sell_args(c), v, ra, cd, mode, c->opt.eps, st);

@@ -23,7 +23,7 @@ IRLS_FROM_SCRATCH, IRLS_CONTINUE = 0, 1
 IRLS_NORM_PRECONDITIONED, IRLS_NORM_UNPRECONDITIONED = 0, 1
 IRLS_LOOP_GRAPH, IRLS_LOOP_HOST, IRLS_LOOP_GRAPH_NCCL = 0, 1, 2
 IRLS_CG_HS, IRLS_CG_CG = 0, 1
-KERNEL_PSPMV, KERNEL_AXPY, KERNEL_ASSEMBLE, KERNEL_HALO = 0, 1, 2, 3
+KERNEL_PSPMV, KERNEL_AXPY, KERNEL_ASSEMBLE, KERNEL_HALO, KERNEL_CGCG = 0, 1, 2, 3, 4
 
 
 class irls_options(C.Structure):
