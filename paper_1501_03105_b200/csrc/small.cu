@@ -155,19 +155,154 @@ __global__ void __launch_bounds__(kThreads, 1) k_small_cg(StencilArgs s, SellArg
     if (threadIdx.x == 0) *ctrl = cl;
 }
 
+// Grids of at most 512 NJ nodes (config 1: 1,024 = NJ 2): the same loop with
+// each thread's nodes (u = 2t + 512j + e, j < NJ) resolved once per solve —
+// neighbour offsets, conductances in ascending order (C2), D and Dinv held
+// in registers — so an iteration is shared-memory arithmetic, the two C3
+// reductions and the (replicated) scalar finalizers.  Same operations in
+// the same order as k_small_cg<0>.
+template <int NJ>
+__global__ void __launch_bounds__(kThreads, 1) k_small_cg_grid(StencilArgs s, VecArgs v, DevCtrl *ctrl)
+{
+    constexpr int NS = 2 * NJ;
+    extern __shared__ double sm[];  // p | x | r | z, kChunk each
+    double *sp = sm, *sx = sm + kChunk, *sr = sm + 2 * kChunk, *sz = sm + 3 * kChunk;
+    __shared__ double red[kMaxQ * 8];
+    __shared__ double bcast[3];
+    const int64_t n = v.n_own;
+    int g1 = 0;
+    for (int gg = 1; gg < kGroups; gg++)
+        if (0 >= group_lo(gg, 1)) g1 = gg;
+    DevCtrl cl = *ctrl;
+    for (int64_t u = threadIdx.x; u < n; u += blockDim.x) {
+        sx[u] = v.x[u];
+        sr[u] = v.r[u];
+        sz[u] = v.z[u];
+    }
+    // per-solve operator of this thread's nodes
+    int32_t uu[NS], off[NS][6];
+    unsigned mask[NS];
+    double gg6[NS][6], Dd[NS], Di[NS];
+#pragma unroll
+    for (int i = 0; i < NS; i++) {
+        const int32_t u = 2 * (int32_t)threadIdx.x + 512 * (i >> 1) + (i & 1);
+        uu[i] = u;
+        mask[i] = 0u;
+        Dd[i] = Di[i] = 0.0;
+#pragma unroll
+        for (int d = 0; d < 6; d++) { off[i][d] = u; gg6[i][d] = 0.0; }
+        if (u < n) {
+            const uint32_t t1 = fdiv((uint32_t)u, s.fd_nx);
+            const int32_t x = (int32_t)((uint32_t)u - t1 * (uint32_t)s.nx);
+            const uint32_t zz = fdiv(t1, s.fd_ny);
+            const int32_t y = (int32_t)(t1 - zz * (uint32_t)s.ny), z = (int32_t)zz;
+            const int32_t P = (int32_t)s.P;
+            const bool has[6] = {z > 0, y > 0, x > 0, x < s.nx - 1, y < s.ny - 1, z < s.nz - 1};
+            const int32_t o[6] = {u - P, u - s.nx, u - 1, u + 1, u + s.nx, u + P};
+            const int32_t gi[6] = {u - P, u - s.nx, u - 1, u, u, u};
+            const double *ga[6] = {s.gz, s.gy, s.gx, s.gx, s.gy, s.gz};
+#pragma unroll
+            for (int d = 0; d < 6; d++)
+                if (has[d]) {
+                    mask[i] |= 1u << d;
+                    off[i][d] = o[d];
+                    gg6[i][d] = ga[d][gi[d]];
+                }
+            mask[i] |= 1u << 6;  // valid node
+            Dd[i] = v.D[u];
+            Di[i] = v.Dinv[u];
+        }
+    }
+    double q[NS];
+    while (!cl.done) {
+        const bool first = cl.k == 0;
+        const double beta = cl.beta, alpha = cl.alpha;
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < NS; i++)
+            if (mask[i] >> 6) {
+                const int32_t u = uu[i];
+                if (first) {
+                    sp[u] = sz[u];
+                } else {
+                    const double po = sp[u];
+                    sx[u] = sx[u] + alpha * po;
+                    sp[u] = sz[u] + beta * po;
+                }
+            }
+        __syncthreads();
+        double a1[1] = {0.0};
+#pragma unroll
+        for (int i = 0; i < NS; i++) {
+            q[i] = 0.0;
+            if (mask[i] >> 6) {
+                double a = 0.0;
+#pragma unroll
+                for (int d = 0; d < 6; d++)
+                    if (mask[i] & (1u << d)) a = a + gg6[i][d] * sp[off[i][d]];
+                const double pu = sp[uu[i]];
+                const double qu = Dd[i] * pu - a;
+                q[i] = qu;
+                a1[0] = a1[0] + pu * qu;
+            }
+        }
+        c3_block_sum<1>(a1, red);
+        if (threadIdx.x == 0) bcast[0] = a1[0];
+        __syncthreads();
+        finalize_pq_t(&cl, small_total(bcast[0], g1));
+        if (cl.status != ST_OK) break;
+        const double al = cl.alpha;
+        double a3[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int i = 0; i < NS; i++)
+            if (mask[i] >> 6) {
+                const int32_t u = uu[i];
+                const double r = sr[u] - al * q[i];
+                const double z = r * Di[i];
+                sr[u] = r;
+                sz[u] = z;
+                a3[0] = a3[0] + r * z;
+                a3[1] = a3[1] + z * z;
+                a3[2] = a3[2] + r * r;
+            }
+        __syncthreads();  // bcast reuse
+        c3_block_sum<3>(a3, red);
+        if (threadIdx.x == 0) {
+            bcast[0] = a3[0];
+            bcast[1] = a3[1];
+            bcast[2] = a3[2];
+        }
+        __syncthreads();
+        finalize_rz_t(&cl, small_total(bcast[0], g1), small_total(bcast[1], g1), small_total(bcast[2], g1));
+    }
+    __syncthreads();
+    double *plast = (cl.k & 1) ? v.p1 : v.p0;
+    for (int64_t u = threadIdx.x; u < n; u += blockDim.x) {
+        v.x[u] = sx[u];
+        v.r[u] = sr[u];
+        v.z[u] = sz[u];
+        if (cl.k > 0) plast[u] = sp[u];
+    }
+    if (threadIdx.x == 0) *ctrl = cl;
+}
+
 static constexpr size_t kSmallSmem = 4 * sizeof(double) * kChunk;
 
 void small_cg_prepare()
 {
     cudaFuncSetAttribute(k_small_cg<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmallSmem);
     cudaFuncSetAttribute(k_small_cg<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmallSmem);
+    cudaFuncSetAttribute(k_small_cg_grid<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmallSmem);
+    cudaFuncSetAttribute(k_small_cg_grid<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmallSmem);
 }
 
 void launch_small_cg(int kind, const StencilArgs &s, const SellArgs &sl, const VecArgs &v, DevCtrl *ctrl,
                      double *slots, cudaStream_t st)
 {
     (void)slots;
-    if (kind == 0) k_small_cg<0><<<1, kThreads, kSmallSmem, st>>>(s, sl, v, ctrl);
+    if (kind == 0 && v.n_own <= 512) k_small_cg_grid<1><<<1, kThreads, kSmallSmem, st>>>(s, v, ctrl);
+    else if (kind == 0 && v.n_own <= 1024) k_small_cg_grid<2><<<1, kThreads, kSmallSmem, st>>>(s, v, ctrl);
+    else if (kind == 0) k_small_cg<0><<<1, kThreads, kSmallSmem, st>>>(s, sl, v, ctrl);
     else k_small_cg<1><<<1, kThreads, kSmallSmem, st>>>(s, sl, v, ctrl);
 }
 
