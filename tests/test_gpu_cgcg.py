@@ -172,3 +172,24 @@ def test_config2_full_size(irls):
     assert [r["cg_iters"] for r in reps] == [r["cg_iters"] for r in oreps]
     assert np.array_equal(m.irls_get_potentials(), S.x())
     check_sweep(m, S)
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("norm", [0, 1])
+@pytest.mark.parametrize("warm", [True, False])
+@pytest.mark.parametrize("kind", ["grid", "csr"])
+def test_option_matrix(irls, variant, norm, warm, kind):
+    """Every combination of PCG form, residual norm, warm/cold start and
+    graph kind against the oracle, bitwise (reports and x^(T))."""
+    spec = (gen.blob_grid(40, 28, 5, seed=13, sigma=(2.0, 6.0)) if kind == "grid"
+            else gen.random_small_graph(2500, 4000, seed=17))
+    T = 6
+    opts = irls.options(T=T, cg_norm=norm, warm_start=int(warm), cg_variant=variant, cg_rtol=1e-4, cg_max_iter=80)
+    m = irls.MinCut.from_spec(spec, opts)
+    reps, tot = m.irls_solve(irls.IRLS_FROM_SCRATCH, T=T)
+    S = oracle.Solver(oracle.Graph(spec), T=T, cg_norm=norm, warm_start=warm, cg_variant=variant, cg_rtol=1e-4,
+                      cg_max_iter=80)
+    _, oreps = S.run(record=False)
+    assert [r["cg_iters"] for r in reps] == [r["cg_iters"] for r in oreps]
+    assert [r["rel_res"] for r in reps] == [r["rel_res"] for r in oreps]
+    assert np.array_equal(m.irls_get_potentials(), S.x())
