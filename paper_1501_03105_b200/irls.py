@@ -303,10 +303,11 @@ def irls_coarse_maxflow(nc, ptr, col, cap, qs, qt):
 class MinCut:
     """One context (one rank) of the IRLS min-cut library."""
 
-    def __init__(self, h, n, n_total):
+    def __init__(self, h, n, n_total, T=None):
         self.h = h
         self.n = n
         self.n_total = n_total
+        self.T = T  # irls_options.T of the context: irls_solve runs T steps
 
     # -- creation ----------------------------------------------------------
     @classmethod
@@ -322,7 +323,7 @@ class MinCut:
                                               *[_ptr(a) for a in arrs], C.byref(opts))
         if rc:
             raise IrlsError(rc, "irls_mincut_create_stencil")
-        m = cls(h, N, N + 2)
+        m = cls(h, N, N + 2, opts.T)
         m._comm = comm  # keeps a caller allocator's callbacks alive
         return m
 
@@ -338,7 +339,7 @@ class MinCut:
                                           _ptr(ww), s, t, C.byref(opts))
         if rc:
             raise IrlsError(rc, "irls_mincut_create_csr")
-        m = cls(h, n - 2, n)
+        m = cls(h, n - 2, n, opts.T)
         m._comm = comm
         return m
 
@@ -368,6 +369,11 @@ class MinCut:
         return r.as_dict()
 
     def irls_solve(self, mode=IRLS_FROM_SCRATCH, T=None, reports=True):
+        """irls_solve runs the context's irls_options.T steps; `T`, if given,
+        must equal it (it only documents the caller's expectation)."""
+        if T is not None and self.T is not None and T != self.T:
+            raise ValueError(f"irls_solve runs the context's T = {self.T} steps (irls_options.T), not {T}")
+        T = self.T if self.T is not None else T
         nrep = (T + 1 if mode == IRLS_FROM_SCRATCH else T) if T is not None else None
         buf = (irls_step_report * max(nrep, 1))() if (reports and nrep is not None) else None
         total = C.c_int64()
@@ -491,7 +497,10 @@ class VGroup:
             raise IrlsError(rc, "irls_vgroup_create")
 
     def irls_vgroup_solve(self, mode=IRLS_FROM_SCRATCH, T=None):
-        nrep = (T + 1 if mode == IRLS_FROM_SCRATCH else T) if T is not None else None
+        if T is not None and T != self.opts.T:
+            raise ValueError(f"irls_vgroup_solve runs the group's T = {self.opts.T} steps (irls_options.T), not {T}")
+        T = self.opts.T
+        nrep = T + 1 if mode == IRLS_FROM_SCRATCH else T
         buf = (irls_step_report * max(nrep, 1))() if nrep is not None else None
         total = C.c_int64()
         rc = lib().irls_vgroup_solve(self.h, mode, C.cast(buf, C.c_void_p) if buf is not None else None,

@@ -97,3 +97,16 @@ def test_csr_terminal_update_singular(irls):
         m.irls_set_terminal_weights(bad_cs, bad_ct)
     assert e.value.code == 5
     m.irls_set_terminal_weights(cs * 2.0, ct * 3.0)  # still anchored: accepted
+
+
+def test_solve_T_must_match_options(irls):
+    """irls_solve runs irls_options.T steps; the binding sizes the report
+    buffer from the context and refuses a different T (a smaller one used
+    to size the host buffer too small)."""
+    spec = gen.blob_grid(16, 12, 4, seed=3)
+    m = irls.MinCut.from_spec(spec, irls.options(T=5))
+    with pytest.raises(ValueError):
+        m.irls_solve(irls.IRLS_FROM_SCRATCH, T=4)
+    reps, _ = m.irls_solve(irls.IRLS_FROM_SCRATCH)
+    assert len(reps) == 6
+    m.close()
