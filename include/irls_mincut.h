@@ -173,7 +173,8 @@ typedef struct {
     double x_min, x_max; /* record_trace */
     double ref;          /* ||M^-1 b|| or ||b|| */
     float ms;            /* device time of this solve */
-    float reserved2;
+    float ms_assemble;   /* irls_solve's one-graph mode: device time from the previous solve's end to the
+                            end of this solve's assembly (K1 incl. its START reduction); else 0 */
 } irls_step_report;
 
 /* x^(0): W = C, cold CG (Alg. 1 step 2).  report may be NULL. */

@@ -553,55 +553,61 @@ static irls_status capture_solve_body(irls_ctx *c, Ranks &R, int mode, cudaStrea
     return s;
 }
 
+// One solve, captured on `st` (which must be capturing): K1 -> WHILE {body}
+// -> finish -> report, wrapped as gate -> IF (not frozen) {K1 -> WHILE ->
+// finish} -> report when the fixed-point exit is on for this mode.
+static irls_status capture_step(irls_ctx *c, Ranks &R, int mode, cudaStream_t st)
+{
+    const bool gated = c->opt.fixed_point_exit && mode == ASM_REWEIGHT_WARM;
+    if (!gated) {
+        irls_status s = capture_solve_body(c, R, mode, st);
+        if (!s) s = enq_tail(R, mode, st);
+        return s;
+    }
+    irls_status s = IRLS_OK;
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t graph;
+    const cudaGraphNode_t *deps = nullptr;
+    size_t nd = 0;
+    cudaGraphConditionalHandle hif;
+    cudaError_t e = cudaStreamGetCaptureInfo(st, &cs, nullptr, &graph, &deps, &nd);
+    if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&hif, graph, 0, cudaGraphCondAssignDefault);
+    if (e == cudaSuccess) {
+        launch_gate(c->ctrl, hif, st);
+        c->launches++;
+        e = cudaStreamGetCaptureInfo(st, &cs, nullptr, &graph, &deps, &nd);
+    }
+    cudaGraphNodeParams p{};
+    cudaGraphNode_t ifnode;
+    if (e == cudaSuccess) {
+        p.type = cudaGraphNodeTypeConditional;
+        p.conditional.handle = hif;
+        p.conditional.type = cudaGraphCondTypeIf;
+        p.conditional.size = 1;
+        e = cudaGraphAddNode(&ifnode, graph, deps, nd, &p);
+    }
+    if (e == cudaSuccess) e = cudaStreamUpdateCaptureDependencies(st, &ifnode, 1, cudaStreamSetCaptureDependencies);
+    if (e == cudaSuccess)
+        e = cudaStreamBeginCaptureToGraph(c->side_stream2, p.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                          cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return fail(c, IRLS_ERR_CUDA, std::string("gated graph: ") + cudaGetErrorString(e));
+    s = capture_solve_body(c, R, mode, c->side_stream2);
+    if (!s) enq_finish(R, c->side_stream2);
+    cudaGraph_t ifg;
+    e = cudaStreamEndCapture(c->side_stream2, &ifg);
+    if (!s && e != cudaSuccess) s = fail(c, IRLS_ERR_CUDA, std::string("gated graph: ") + cudaGetErrorString(e));
+    if (!s) s = enq_tail(R, mode, st, false);
+    return s;
+}
+
 static irls_status build_graph(irls_ctx *c, int mode)
 {
     cudaStream_t st = c->stream;
     Ranks R{c};
-    const bool gated = c->opt.fixed_point_exit && mode == ASM_REWEIGHT_WARM;
     const int64_t lsave = c->launches;
     c->launches = 0;
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    irls_status s = IRLS_OK;
-    if (!gated) {
-        s = capture_solve_body(c, R, mode, st);
-        if (!s) s = enq_tail(R, mode, st);
-    } else {
-        cudaStreamCaptureStatus cs;
-        cudaGraph_t graph;
-        const cudaGraphNode_t *deps = nullptr;
-        size_t nd = 0;
-        cudaGraphConditionalHandle hif;
-        cudaError_t e = cudaStreamGetCaptureInfo(st, &cs, nullptr, &graph, &deps, &nd);
-        if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&hif, graph, 0, cudaGraphCondAssignDefault);
-        if (e == cudaSuccess) {
-            launch_gate(c->ctrl, hif, st);
-            c->launches++;
-            e = cudaStreamGetCaptureInfo(st, &cs, nullptr, &graph, &deps, &nd);
-        }
-        cudaGraphNodeParams p{};
-        cudaGraphNode_t ifnode;
-        if (e == cudaSuccess) {
-            p.type = cudaGraphNodeTypeConditional;
-            p.conditional.handle = hif;
-            p.conditional.type = cudaGraphCondTypeIf;
-            p.conditional.size = 1;
-            e = cudaGraphAddNode(&ifnode, graph, deps, nd, &p);
-        }
-        if (e == cudaSuccess) e = cudaStreamUpdateCaptureDependencies(st, &ifnode, 1, cudaStreamSetCaptureDependencies);
-        if (e == cudaSuccess)
-            e = cudaStreamBeginCaptureToGraph(c->side_stream2, p.conditional.phGraph_out[0], nullptr, nullptr, 0,
-                                              cudaStreamCaptureModeThreadLocal);
-        if (e != cudaSuccess) {
-            s = fail(c, IRLS_ERR_CUDA, std::string("gated graph: ") + cudaGetErrorString(e));
-        } else {
-            s = capture_solve_body(c, R, mode, c->side_stream2);
-            if (!s) enq_finish(R, c->side_stream2);
-            cudaGraph_t ifg;
-            e = cudaStreamEndCapture(c->side_stream2, &ifg);
-            if (!s && e != cudaSuccess) s = fail(c, IRLS_ERR_CUDA, std::string("gated graph: ") + cudaGetErrorString(e));
-            if (!s) s = enq_tail(R, mode, st, false);
-        }
-    }
+    irls_status s = capture_step(c, R, mode, st);
     cudaGraph_t full = nullptr;
     cudaError_t e = cudaStreamEndCapture(st, &full);
     if (s) { if (full) cudaGraphDestroy(full); c->launches = lsave; return s; }
@@ -723,7 +729,7 @@ static irls_status enqueue_solve(Ranks &R, int mode)
     return enq_tail(R, mode, st);
 }
 
-static void copy_report(const DevReport &d, irls_step_report *o, float ms)
+static void copy_report(const DevReport &d, irls_step_report *o, float ms, float ms_asm)
 {
     o->cg_iters = d.cg_iters;
     o->converged = d.converged;
@@ -738,7 +744,7 @@ static void copy_report(const DevReport &d, irls_step_report *o, float ms)
     o->x_max = d.x_max;
     o->ref = d.ref;
     o->ms = ms;
-    o->reserved2 = 0.f;
+    o->ms_assemble = ms_asm;
 }
 
 // Run `count` solves (first one with mode0, the rest with mode_rest); fill
@@ -806,15 +812,17 @@ irls_status run_solves(Ranks &R, int mode0, int mode_rest, int count, irls_step_
     }
     if (!s) {
         for (int i = 0; i < count; i++) {
-            float ms = 0.f;
+            float ms = 0.f, ms_asm = 0.f;
             if (multi_graph) {
                 const unsigned long long prev = i == 0 ? t0 : h[i - 1].t_end;
                 ms = h[i].t_end > prev ? (float)((double)(h[i].t_end - prev) * 1e-6) : 0.f;
+                ms_asm = h[i].t_asm > prev && h[i].t_asm <= h[i].t_end ? (float)((double)(h[i].t_asm - prev) * 1e-6)
+                                                                       : 0.f;
             } else {
                 cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
             }
             tot += h[i].cg_iters;
-            if (reps) copy_report(h[i], reps + i, ms);
+            if (reps) copy_report(h[i], reps + i, ms, ms_asm);
             if (h[i].status != 0 && !s)
                 s = fail(c, (irls_status)h[i].status,
                          h[i].status == ST_P2P_TIMEOUT ? "peer-memory collective: wait timed out (10 s)"

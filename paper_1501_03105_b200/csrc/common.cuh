@@ -57,6 +57,7 @@ struct DevCtrl {
     uint32_t red_seq;    // peer-memory collectives: reductions consumed so far (slot parity, arrival target)
     unsigned long long xmin_key, xmax_key;
     unsigned long long t_mark;  // %globaltimer (ns) at the start of a solve sequence
+    unsigned long long t_asm;   // %globaltimer (ns) at the last START finalize (end of the assembly)
 };
 
 __device__ __forceinline__ unsigned long long global_ns()
@@ -261,6 +262,7 @@ __device__ inline const double *p2p_wait(DevCtrl *c, const P2PWait &pw)
 // After assembly (phase START): quantities [rz, zz, rr, mbmb, bb].
 __device__ __forceinline__ void finalize_start(DevCtrl *c, const double *slots)
 {
+    c->t_asm = global_ns();
     const double rz = slot_total(slots, 0), zz = slot_total(slots, 1), rr = slot_total(slots, 2);
     const double mbmb = slot_total(slots, 3), bb = slot_total(slots, 4);
     const double ref = sqrt(c->norm == 0 ? mbmb : bb);

@@ -118,6 +118,7 @@ struct DevReport {
     int32_t cg_iters, converged, status, pad;
     double rel_res, true_rel_res, S_eps, flow_value, current_s, x_min, x_max, ref;
     unsigned long long t_end;  // %globaltimer (ns) when the solve's report was written
+    unsigned long long t_asm;  // %globaltimer (ns) when the solve's START reduction was finalized
 };
 // freeze: set DevCtrl::frozen when this (warm reweight) solve ended with 0 CG
 // iterations and x unchanged (fixed_point_exit)

@@ -392,6 +392,7 @@ __global__ void k_report(DevCtrl *ctrl, DevReport *reports, int freeze)
     R.true_rel_res = R.S_eps = R.flow_value = R.current_s = 0.0;
     R.x_min = R.x_max = 0.0;
     R.t_end = global_ns();
+    R.t_asm = ctrl->t_asm;
     ctrl->step = ctrl->step + 1;
     ctrl->xmin_key = ~0ull;
     ctrl->xmax_key = 0ull;

@@ -76,7 +76,7 @@ class irls_step_report(C.Structure):
     _fields_ = [("cg_iters", C.c_int32), ("converged", C.c_int32), ("status", C.c_int32), ("reserved", C.c_int32),
                 ("rel_res", C.c_double), ("true_rel_res", C.c_double), ("S_eps", C.c_double),
                 ("flow_value", C.c_double), ("current_s", C.c_double), ("x_min", C.c_double),
-                ("x_max", C.c_double), ("ref", C.c_double), ("ms", C.c_float), ("reserved2", C.c_float)]
+                ("x_max", C.c_double), ("ref", C.c_double), ("ms", C.c_float), ("ms_assemble", C.c_float)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_ if not k.startswith("reserved")}

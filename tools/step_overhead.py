@@ -1,7 +1,8 @@
 """Where the time of a zero-iteration IRLS step goes (config 4 after the
 fixed point): one irls_step (its own graph: K1 -> WHILE(0) -> finish ->
 report), K1 alone (irls_time_kernel), and the per-step time inside the
-multi-step graph (report timestamps).  usage: python tools/step_overhead.py"""
+multi-step graph (report timestamps; ms_assemble = previous report -> end of
+the assembly).  usage: python tools/step_overhead.py"""
 import os
 import sys
 
@@ -18,6 +19,12 @@ for lm in (0, 1):
     reps, _ = m.irls_solve(I.IRLS_FROM_SCRATCH, T=50)
     reps, _ = m.irls_solve(I.IRLS_FROM_SCRATCH, T=50)
     zero = [r["ms"] for r in reps[1:] if r["cg_iters"] == 0]
+    if lm == 0:
+        za = [r["ms_assemble"] for r in reps[1:] if r["cg_iters"] == 0]
+        one = [(r["ms"], r["ms_assemble"]) for r in reps[1:] if r["cg_iters"] == 1]
+        print(f"graph: zero-iteration steps: previous end -> assembly end {sum(za) / max(len(za), 1):.3f} ms, "
+              f"-> report {sum(zero) / max(len(zero), 1):.3f} ms; one-iteration steps (ms, ms_assemble): {one[:3]}",
+              flush=True)
     s = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
