@@ -96,15 +96,20 @@ __global__ void __launch_bounds__(256) k_tile_hist(const u64 *keys, int64_t n, i
 }
 
 // Stable scatter.  Warp w owns keys [base + 512 w, +512) in 16 rounds of 32.
-// The tile is first ranked (stable, match_any per round) and staged in shared
-// memory in digit order, then written out so that consecutive threads write
-// consecutive positions of one bucket (coalesced runs instead of isolated
-// 8-byte writes).
+// Ranking in ONE pass: per round, the lanes holding the same digit find each
+// other (match_any); the lowest of them advances the warp's counter of that
+// digit with a shared-memory atomic whose old value, broadcast to the group,
+// is the group's start — so every key gets its rank among the warp's keys of
+// its digit, in key order (a warp's shared-memory atomics to one address
+// take effect in issue order), with no dependent read-modify-write chain
+// between rounds.  Then the per-warp digit starts of the tile (digit-major,
+// warp-minor: stable), staging in shared memory in digit order, and a write
+// out in which consecutive threads write consecutive positions of a bucket.
 __global__ void __launch_bounds__(256) k_radix_scatter(const u64 *keys, const int32_t *vals, u64 *okeys,
                                                        int32_t *ovals, int64_t n, int shift,
                                                        const int32_t *tile_off, int64_t ntiles)
 {
-    __shared__ int32_t wh[8][256];     // per-warp digit counts, then per-warp running tile positions
+    __shared__ int32_t wh[8][256];     // per-warp digit counts, then per-warp tile starts
     __shared__ int32_t gdelta[256];    // global start of the bucket minus its tile-local start
     extern __shared__ __align__(16) unsigned char radix_dyn[];  // kTile keys + kTile values
     u64 *skey = reinterpret_cast<u64 *>(radix_dyn);
@@ -116,26 +121,29 @@ __global__ void __launch_bounds__(256) k_radix_scatter(const u64 *keys, const in
     const int64_t base = tbase + w * 512;
     u64 k[16];
     int32_t vv[16];
-    int dig[16];
+    uint32_t dr[16];  // digit << 16 | rank within (warp, digit); 0xffffffff past n
 #pragma unroll
     for (int r = 0; r < 16; r++) {
         const int64_t i = base + r * 32 + lane;
         if (i < n) {
             k[r] = keys[i];
             vv[r] = vals[i];
-            dig[r] = (int)((k[r] >> shift) & 255u);
         } else {
             k[r] = 0;
             vv[r] = 0;
-            dig[r] = -1;
         }
     }
     const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
     for (int r = 0; r < 16; r++) {
-        const unsigned peers = __match_any_sync(0xffffffffu, dig[r]);
-        if (dig[r] >= 0 && (peers & lt) == 0u) wh[w][dig[r]] += __popc(peers);
-        __syncwarp();
+        const int64_t i = base + r * 32 + lane;
+        const int d = i < n ? (int)((k[r] >> shift) & 255u) : 256 + lane;  // past n: a group of one
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const int leader = __ffs(peers) - 1;
+        int old = 0;
+        if (lane == leader && d < 256) old = atomicAdd(&wh[w][d], __popc(peers));
+        old = __shfl_sync(0xffffffffu, old, leader);
+        dr[r] = d < 256 ? ((uint32_t)d << 16) | (uint32_t)(old + __popc(peers & lt)) : 0xffffffffu;
     }
     __syncthreads();
     // digit d (one per thread): tile total, exclusive scan over digits, per-warp starts
@@ -168,17 +176,11 @@ __global__ void __launch_bounds__(256) k_radix_scatter(const u64 *keys, const in
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < 16; r++) {
-        const int dd = dig[r];
-        const unsigned peers = __match_any_sync(0xffffffffu, dd);
-        int32_t pos = 0;
-        if (dd >= 0) pos = wh[w][dd] + __popc(peers & lt);
-        __syncwarp();
-        if (dd >= 0) {
+        if (dr[r] != 0xffffffffu) {
+            const int32_t pos = wh[w][dr[r] >> 16] + (int32_t)(dr[r] & 0xffffu);
             skey[pos] = k[r];
             sval[pos] = vv[r];
-            if ((peers & lt) == 0u) wh[w][dd] += __popc(peers);
         }
-        __syncwarp();
     }
     __syncthreads();
     const int32_t cnt = (int32_t)(n - tbase < kTile ? n - tbase : kTile);
