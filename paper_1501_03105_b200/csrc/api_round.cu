@@ -92,13 +92,13 @@ irls_status sweep_rank0(irls_ctx *c, const double *xfull, uint8_t *side, int32_t
     CK(cudaMemsetAsync(b.flags, 0, sizeof(int32_t) * 4, st));
     sweep_keys(xfull, b, st);
     launches++;
-    int32_t *ord = sweep_sort(b, st, &launches);
-    int32_t hflag = 0;
-    CK(cudaMemcpyAsync(&hflag, b.flags, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (hflag) return fail(c, IRLS_ERR_BAD_POTENTIAL, "NaN in potentials");
-    sweep_rank(ord, b, st);
-    launches++;
+    bool nan = false, rank_done = false;
+    int32_t *ord = sweep_sort(b, st, &launches, &nan, &rank_done);
+    if (nan) return fail(c, IRLS_ERR_BAD_POTENTIAL, "NaN in potentials");
+    if (!rank_done) {  // no radix pass ran (every key equal): rank of the identity order
+        sweep_rank(ord, b, st);
+        launches++;
+    }
     if (c->kind == 0) sweep_delta_stencil(stencil_args(c, true), n, c->F, b, st);
     else sweep_delta_sell(sell_args_full(c), c->F, b, st);
     sweep_delta_order(ord, b, st);

@@ -182,8 +182,9 @@ struct SweepBuffers {
 };
 int64_t sweep_ntiles(int64_t n);
 void sweep_keys(const double *x, SweepBuffers &b, cudaStream_t st);
-// returns pointer to the sorted ids buffer (vals or vals_alt)
-int32_t *sweep_sort(SweepBuffers &b, cudaStream_t st, int *launches);
+// returns pointer to the sorted ids buffer (vals or vals_alt); *nan: a NaN key
+// (nothing sorted); *rank_done: the last radix pass also wrote rank[]
+int32_t *sweep_sort(SweepBuffers &b, cudaStream_t st, int *launches, bool *nan, bool *rank_done);
 void sweep_rank(const int32_t *order, SweepBuffers &b, cudaStream_t st);
 void sweep_delta_stencil(const StencilArgs &s, int64_t N, int32_t F, SweepBuffers &b, cudaStream_t st);
 void sweep_delta_sell(const SellArgs &s, int32_t F, SweepBuffers &b, cudaStream_t st);

@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(256) k_tile_hist(const u64 *keys, int64_t n, i
 // out in which consecutive threads write consecutive positions of a bucket.
 __global__ void __launch_bounds__(256) k_radix_scatter(const u64 *keys, const int32_t *vals, u64 *okeys,
                                                        int32_t *ovals, int64_t n, int shift,
-                                                       const int32_t *tile_off, int64_t ntiles)
+                                                       const int32_t *tile_off, int64_t ntiles, int32_t *rank)
 {
     __shared__ int32_t wh[8][256];     // per-warp digit counts, then per-warp tile starts
     __shared__ int32_t gdelta[256];    // global start of the bucket minus its tile-local start
@@ -190,6 +190,7 @@ __global__ void __launch_bounds__(256) k_radix_scatter(const u64 *keys, const in
         const int64_t g = (int64_t)gdelta[dd] + i;
         okeys[g] = key;
         ovals[g] = sval[i];
+        if (rank) rank[sval[i]] = (int32_t)g;  // last pass: the inverse permutation too
     }
 }
 
@@ -281,25 +282,40 @@ void sweep_keys(const double *x, SweepBuffers &b, cudaStream_t st)
     k_sweep_keys<<<(unsigned)((b.n + 255) / 256), 256, 0, st>>>(x, b.n, b.keys, b.vals, b.flags);
 }
 
-int32_t *sweep_sort(SweepBuffers &b, cudaStream_t st, int *launches)
+int32_t *sweep_sort(SweepBuffers &b, cudaStream_t st, int *launches, bool *nan, bool *rank_done)
 {
     const int64_t n = b.n;
+    *nan = false;
+    *rank_done = false;
     if (n == 0) return b.vals;
     const int64_t nt = sweep_ntiles(n);
     cudaMemsetAsync(b.digit_hist, 0, sizeof(u64) * 8 * 256, st);
     const int nbh = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
     k_hist8<<<nbh, 256, 0, st>>>(b.keys, n, b.digit_hist);
     *launches += 1;
+    // one host round trip: the digit histograms (constant-digit passes are
+    // skipped) and the NaN flag of the keys kernel
     u64 h[8 * 256];
+    int32_t hflag = 0;
     cudaMemcpyAsync(h, b.digit_hist, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(&hflag, b.flags, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
+    if (hflag) {
+        *nan = true;
+        return b.vals;
+    }
+    int last = -1;
+    bool run[8];
+    for (int d = 0; d < 8; d++) {
+        run[d] = true;
+        for (int i = 0; i < 256; i++)
+            if (h[d * 256 + i] == (u64)n) run[d] = false;
+        if (run[d]) last = d;
+    }
     u64 *ka = b.keys, *kb = b.keys_alt;
     int32_t *va = b.vals, *vb = b.vals_alt;
     for (int d = 0; d < 8; d++) {
-        bool trivial = false;
-        for (int i = 0; i < 256; i++)
-            if (h[d * 256 + i] == (u64)n) trivial = true;
-        if (trivial) continue;
+        if (!run[d]) continue;
         k_tile_hist<<<(unsigned)nt, 256, 0, st>>>(ka, n, 8 * d, b.tile_hist, nt);
         exclusive_scan_i32(b.tile_hist, 256 * nt, b.tile_off, (int64_t *)b.scan_tmp, st, launches);
         const int dyn = (int)((sizeof(u64) + sizeof(int32_t)) * kTile);
@@ -308,7 +324,9 @@ int32_t *sweep_sort(SweepBuffers &b, cudaStream_t st, int *launches)
             cudaFuncSetAttribute(k_radix_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
             attr = true;
         }
-        k_radix_scatter<<<(unsigned)nt, 256, dyn, st>>>(ka, va, kb, vb, n, 8 * d, b.tile_off, nt);
+        k_radix_scatter<<<(unsigned)nt, 256, dyn, st>>>(ka, va, kb, vb, n, 8 * d, b.tile_off, nt,
+                                                         d == last ? b.rank : nullptr);
+        if (d == last) *rank_done = true;
         *launches += 2;
         std::swap(ka, kb);
         std::swap(va, vb);
