@@ -383,7 +383,10 @@ __device__ __forceinline__ double rw_g(double c, double d, double eps2)
 __device__ __forceinline__ __int128 qfix(double c, int32_t F)
 {
     if (c == 0.0) return 0;
-    const double v = rint(scalbn(c, F));
+    // c * 2^F with an exact power-of-two factor (the same correctly rounded
+    // value as scalbn; the factor is built from its exponent bits)
+    const double v = (F >= -1022 && F <= 1023) ? rint(c * __longlong_as_double((long long)(F + 1023) << 52))
+                                               : rint(scalbn(c, F));
     const double hi = floor(v * 0x1p-64);
     const double lo = v - hi * 0x1p64;
     return ((__int128)(long long)hi << 64) + (__int128)(unsigned long long)lo;

@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(256) k_tile_hist(const u64 *keys, int64_t n, i
 // between rounds.  Then the per-warp digit starts of the tile (digit-major,
 // warp-minor: stable), staging in shared memory in digit order, and a write
 // out in which consecutive threads write consecutive positions of a bucket.
-__global__ void __launch_bounds__(256) k_radix_scatter(const u64 *keys, const int32_t *vals, u64 *okeys,
+__global__ void __launch_bounds__(256, 3) k_radix_scatter(const u64 *keys, const int32_t *vals, u64 *okeys,
                                                        int32_t *ovals, int64_t n, int shift,
                                                        const int32_t *tile_off, int64_t ntiles, int32_t *rank)
 {
