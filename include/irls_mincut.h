@@ -254,7 +254,10 @@ irls_status irls_exact_min_cut(irls_ctx *ctx, uint8_t *side, irls_two_level_repo
  * b_u = cs_u - ct_u) with the given rtol / cap / norm (irls_cg_norm), then
  * x^T L x and C by C3 (A30).  phi^2/2 <= lambda_2 <= 2 phi with phi =
  * mu_star / C (Theorem 4).  The IRLS state (x, options) is restored afterwards.
- * x_out: the solution v (n~ doubles, host) or NULL.  Single process. */
+ * x_out: the solution v (n~ doubles, host; rank 0) or NULL.  Multi-rank
+ * contexts: collective; the solve runs distributed, the quadratic form on
+ * rank 0 over the gathered v (like the sweep), every rank returns its
+ * values. */
 typedef struct {
     double lambda2, xLx, C, rel_res;
     int32_t cg_iters, converged;

@@ -535,12 +535,11 @@ extern "C" irls_status irls_lambda2(irls_ctx *c, double cg_rtol, int32_t cg_max_
 {
     NvtxRange nvtx_("irls_lambda2");
     GUARD(c);
-    if (c->world > 1) return fail(c, IRLS_ERR_INVALID_ARGUMENT, "irls_lambda2 is single-process");
     if (!(cg_rtol >= 0.0) || cg_max_iter < 0 || (cg_norm != 0 && cg_norm != 1))
         return fail(c, IRLS_ERR_INVALID_ARGUMENT, "lambda2 CG options");
     cudaStream_t st = c->stream;
     const int64_t n = c->n_own;
-    if (n == 0) {  // only s and t: x = (1, -1), x^T L x = 4 c_st, C = 2 c_st
+    if (c->n_glob == 0) {  // only s and t: x = (1, -1), x^T L x = 4 c_st, C = 2 c_st
         if (rep) {
             memset(rep, 0, sizeof(*rep));
             rep->xLx = 4.0 * c->c_st;
@@ -552,7 +551,7 @@ extern "C" irls_status irls_lambda2(irls_ctx *c, double cg_rtol, int32_t cg_max_
     }
     double *xs = dalloc<double>(c, n);
     if (!xs) return fail(c, IRLS_ERR_OOM, "lambda2 x save");
-    CK(cudaMemcpyAsync(xs, c->x, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    if (n > 0) CK(cudaMemcpyAsync(xs, c->x, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     const int state0 = c->state;
     const int64_t iters0 = c->last_cg_iters;
     // the CG options live in the control block: set, solve, restore
@@ -570,24 +569,41 @@ extern "C" irls_status irls_lambda2(irls_ctx *c, double cg_rtol, int32_t cg_max_
     Ranks R{c};
     irls_status s = run_solves(R, ASM_LAMBDA2, ASM_LAMBDA2, 1, &sr, &total);
     const int64_t launches = c->launches;
-    if (!s) {
+    // the quadratic form on rank 0 over the gathered v (P:L303's gather, as
+    // the sweep; every rank holds the full capacities), broadcast to all
+    double *full = c->x;
+    if (!s && c->multi) s = gather_x(c, &full);
+    const int64_t ng = c->n_glob;
+    double msg[2 * kGroups + 1];  // status, then the two quantities' 8 group sums
+    memset(msg, 0, sizeof(msg));
+    if (!s && c->rank == 0) {
         RedArgs ra;
         ra.part = c->part;
         ra.slots = c->slots_local;
         ra.ctrl = c->ctrl;
-        ra.K = c->K;
+        ra.K = (int32_t)((ng + kChunk - 1) / kChunk);
         ra.g0 = 0;
         ra.g1 = 8;
         ra.n_fin = count_nonempty(ra.K, 0, 8);
-        if (c->kind == 0) launch_l2_quad_stencil(stencil_args(c, true), n, c->x, ra, st);
-        else launch_l2_quad_sell(sell_args_full(c), c->x, ra, st);
+        if (c->kind == 0) launch_l2_quad_stencil(stencil_args(c, true), ng, full, ra, st);
+        else launch_l2_quad_sell(sell_args_full(c), full, ra, st);
         s = last_launch(c, "lambda2 quadratic form");
+        if (!s) CK(memcpy_sync(c, msg + 1, c->slots_local, sizeof(double) * 2 * kGroups, cudaMemcpyDeviceToHost));
+        if (!s && x_out) CK(memcpy_sync(c, x_out, full, sizeof(double) * ng, cudaMemcpyDeviceToHost));
     }
-    double slots[2 * kGroups];
-    memset(slots, 0, sizeof(slots));
-    if (!s && n > 0) CK(memcpy_sync(c, slots, c->slots_local, sizeof(slots), cudaMemcpyDeviceToHost));
-    if (!s && x_out && n > 0) CK(memcpy_sync(c, x_out, c->x, sizeof(double) * n, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpyAsync(c->x, xs, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    if (c->multi) {  // every rank returns rank 0's values (and its status)
+        msg[0] = (double)s;
+        double *dmsg = dalloc<double>(c, 2 * kGroups + 1);
+        if (!dmsg) return fail(c, IRLS_ERR_OOM, "lambda2 msg");
+        if (c->rank == 0) CK(cudaMemcpyAsync(dmsg, msg, sizeof(msg), cudaMemcpyHostToDevice, st));
+        NK(ncclBroadcast(dmsg, dmsg, sizeof(msg), ncclUint8, 0, c->nccl, st));
+        CK(cudaMemcpyAsync(msg, dmsg, sizeof(msg), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        CK(dfree(c, dmsg));
+        if (!s && msg[0] != 0.0) s = fail(c, (irls_status)(int)msg[0], "lambda2 failed on rank 0");
+    }
+    double *slots = msg + 1;
+    if (n > 0) CK(cudaMemcpyAsync(c->x, xs, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     CK(set_opts(c->opt.cg_rtol, c->opt.cg_max_iter, c->opt.cg_norm));
     CK(dfree(c, xs));
     CK(cudaStreamSynchronize(st));

@@ -91,3 +91,23 @@ def test_config2_full_size(irls):
     m.irls_solve(irls.IRLS_FROM_SCRATCH, T=50, reports=False)
     _, _, _, cut = m.irls_sweep_cut(side=False)
     assert r["lambda2"] > 0.0
+
+
+@pytest.mark.parametrize("kind", ["grid", "csr"])
+def test_nccl_communicator(irls, kind):
+    """A multi-rank context (a 1-rank NCCL communicator): the distributed
+    solve, the gather to rank 0, the quadratic form there and the broadcast
+    of its values — the same bits as the plain single-GPU call."""
+    import torch
+    spec = gen.blob_grid(48, 40, 6, seed=4, sigma=(3.0, 8.0)) if kind == "grid" else gen.road_graph(90, seed=2, knn=40)
+    m = irls.MinCut.from_spec(spec, irls.options(T=4))
+    r1, x1 = m.irls_lambda2(cg_rtol=1e-10, want_x=True)
+    comm = irls.comm_desc(1, 0, 0, irls.irls_nccl_unique_id(), torch.cuda.current_stream().cuda_stream)
+    g = irls.MinCut.from_spec(spec, irls.options(T=4), comm)
+    g.irls_solve(irls.IRLS_FROM_SCRATCH)
+    x_before = g.irls_get_potentials()
+    r2, x2 = g.irls_lambda2(cg_rtol=1e-10, want_x=True)
+    assert _bitwise(x1, x2) and (r1["lambda2"], r1["xLx"], r1["C"]) == (r2["lambda2"], r2["xLx"], r2["C"])
+    assert _bitwise(g.irls_get_potentials(), x_before)  # the IRLS state is restored
+    g.close()
+    m.close()
