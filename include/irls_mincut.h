@@ -242,7 +242,8 @@ irls_status irls_two_level_cut(irls_ctx *ctx, uint8_t *side, irls_two_level_repo
 /* mu*, the exact minimum cut of G, by the same pipeline with no contraction
  * (gamma0 = -inf, gamma1 = +inf: G_c = G, the no-coarsening limit of S:L384)
  * — the denominator of delta = (mu - mu*) / mu* (Eq. 13).  Needs
- * no solve; single process only; host memory ~60 B per n-link. */
+ * no solve; host memory ~60 B per n-link.  Multi-rank contexts: collective,
+ * computed on rank 0 (which holds the whole graph), report broadcast. */
 irls_status irls_exact_min_cut(irls_ctx *ctx, uint8_t *side, irls_two_level_report *rep);
 
 /* ---- Cheeger-type diagnostic (Theorem 4) ----

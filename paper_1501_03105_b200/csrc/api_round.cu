@@ -420,18 +420,17 @@ struct TwoLevelMsg {
     irls_two_level_report rep;
 };
 
-extern "C" irls_status irls_two_level_cut(irls_ctx *c, uint8_t *side, irls_two_level_report *rep)
+// Two-level rounding (or, exact = true, the no-contraction mu*) on rank 0
+// over the gathered x, its report broadcast to every rank.
+static irls_status two_level_collective(irls_ctx *c, uint8_t *side, irls_two_level_report *rep, bool exact)
 {
-    NvtxRange nvtx_("irls_two_level_cut");
-    GUARD(c);
-    if (c->state == 0) return fail(c, IRLS_ERR_STATE, "two-level rounding before solve");
     double *xfull = nullptr;
-    irls_status s = gather_x(c, &xfull);
+    irls_status s = gather_x(c, &xfull);  // exact: only the length matters (every node is in Sc)
     if (s) return s;
     TwoLevelMsg msg;
     memset(&msg, 0, sizeof(msg));
     if (c->rank == 0) {
-        s = two_level_rank0(c, xfull, side, &msg.rep);
+        s = two_level_rank0(c, xfull, side, &msg.rep, exact);
         msg.status = s;
         if (s && !c->multi) return s;
     }
@@ -449,16 +448,26 @@ extern "C" irls_status irls_two_level_cut(irls_ctx *c, uint8_t *side, irls_two_l
     return IRLS_OK;
 }
 
+extern "C" irls_status irls_two_level_cut(irls_ctx *c, uint8_t *side, irls_two_level_report *rep)
+{
+    NvtxRange nvtx_("irls_two_level_cut");
+    GUARD(c);
+    if (c->state == 0) return fail(c, IRLS_ERR_STATE, "two-level rounding before solve");
+    return two_level_collective(c, side, rep, false);
+}
+
 extern "C" irls_status irls_exact_min_cut(irls_ctx *c, uint8_t *side, irls_two_level_report *rep)
 {
     NvtxRange nvtx_("irls_exact_min_cut");
     GUARD(c);
-    if (c->world > 1) return fail(c, IRLS_ERR_INVALID_ARGUMENT, "irls_exact_min_cut is single-process");
-    irls_two_level_report r;
-    irls_status s = two_level_rank0(c, c->x, side, &r, true);
-    if (s) return s;
-    if (rep) *rep = r;
-    return IRLS_OK;
+    if (!c->multi) {  // no solve needed: x only sizes the classification (every node is in Sc)
+        irls_two_level_report r;
+        irls_status s = two_level_rank0(c, c->x, side, &r, true);
+        if (s) return s;
+        if (rep) *rep = r;
+        return IRLS_OK;
+    }
+    return two_level_collective(c, side, rep, true);
 }
 
 extern "C" irls_status irls_vgroup_two_level_cut(irls_vgroup *g, uint8_t *side, irls_two_level_report *rep)

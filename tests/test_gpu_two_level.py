@@ -174,3 +174,19 @@ def test_config2_full_size(irls):
     assert S.cut_value(side) == pytest.approx(rep["cut_value"], rel=1e-12)
     _, _, _, sweep_cut = m.irls_sweep_cut(side=False)
     assert rep["cut_value"] <= sweep_cut
+
+
+def test_exact_min_cut_on_a_communicator(irls):
+    """mu* (no contraction) on a multi-rank context (1-rank NCCL
+    communicator: gather, rank-0 max-flow, broadcast) equals the plain call,
+    before any solve."""
+    import torch
+    spec = gen.blob_grid(30, 24, 4, seed=6, sigma=(2.0, 6.0))
+    m = irls.MinCut.from_spec(spec, irls.options(T=4))
+    s1, r1 = m.irls_exact_min_cut()
+    comm = irls.comm_desc(1, 0, 0, irls.irls_nccl_unique_id(), torch.cuda.current_stream().cuda_stream)
+    g = irls.MinCut.from_spec(spec, irls.options(T=4), comm)
+    s2, r2 = g.irls_exact_min_cut()
+    assert r1["cut_value"] == r2["cut_value"] and np.array_equal(s1, s2)
+    g.close()
+    m.close()
