@@ -24,7 +24,6 @@ static irls_status alloc_sweep(irls_ctx *c)
     b.scan_tmp = (int32_t *)dalloc<int64_t>(c, (256 * nt + 4095) / 4096 + 1);
     b.digit_hist = dalloc<unsigned long long>(c, 8 * 256);
     b.delta = dalloc<__int128>(c, n + 2);
-    b.delta_id = dalloc<__int128>(c, n);
     b.tile_sum = dalloc<__int128>(c, nt);
     b.tile_min = dalloc<__int128>(c, nt);
     b.tile_argmin = dalloc<int64_t>(c, nt);
@@ -33,7 +32,7 @@ static irls_status alloc_sweep(irls_ctx *c)
     b.side = dalloc<uint8_t>(c, c->n_total);
     c->order_out = dalloc<int32_t>(c, n);
     if (!b.keys || !b.keys_alt || !b.vals || !b.vals_alt || !b.rank || !b.tile_hist || !b.tile_off || !b.scan_tmp ||
-        !b.digit_hist || !b.delta || !b.delta_id || !b.tile_sum || !b.tile_min || !b.tile_argmin || !b.flags || !b.k_out || !b.side ||
+        !b.digit_hist || !b.delta || !b.tile_sum || !b.tile_min || !b.tile_argmin || !b.flags || !b.k_out || !b.side ||
         !c->order_out)
         return fail(c, IRLS_ERR_OOM, "sweep buffers");
     return IRLS_OK;
@@ -101,8 +100,7 @@ irls_status sweep_rank0(irls_ctx *c, const double *xfull, uint8_t *side, int32_t
     }
     if (c->kind == 0) sweep_delta_stencil(stencil_args(c, true), n, c->F, b, st);
     else sweep_delta_sell(sell_args_full(c), c->F, b, st);
-    sweep_delta_order(ord, b, st);
-    launches += 2;
+    launches += 1;
     sweep_scan_argmin(b, qfix_host(c->c_st, c->F), st);
     launches += 4;
     RedArgs ra;

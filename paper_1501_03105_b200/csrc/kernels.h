@@ -171,7 +171,6 @@ struct SweepBuffers {
     int32_t *scan_tmp;       // scan block totals
     unsigned long long *digit_hist;  // [8][256] global histograms
     __int128 *delta;         // [n+2] in sweep order (+ P0, P_k)
-    __int128 *delta_id;      // [n] in id order
     __int128 *tile_sum;      // [ntiles]
     __int128 *tile_min;      // [ntiles]
     int64_t *tile_argmin;    // [ntiles]
@@ -188,7 +187,6 @@ int32_t *sweep_sort(SweepBuffers &b, cudaStream_t st, int *launches, bool *nan, 
 void sweep_rank(const int32_t *order, SweepBuffers &b, cudaStream_t st);
 void sweep_delta_stencil(const StencilArgs &s, int64_t N, int32_t F, SweepBuffers &b, cudaStream_t st);
 void sweep_delta_sell(const SellArgs &s, int32_t F, SweepBuffers &b, cudaStream_t st);
-void sweep_delta_order(const int32_t *order, SweepBuffers &b, cudaStream_t st);
 void sweep_scan_argmin(SweepBuffers &b, __int128 P0, cudaStream_t st);
 void sweep_side_cross_stencil(const StencilArgs &s, int64_t N, SweepBuffers &b, const RedArgs &ra,
                               cudaStream_t st);

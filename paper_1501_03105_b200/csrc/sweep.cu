@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(256) k_delta_stencil(StencilArgs s, int64_t N,
         d += qfix(s.ct[v], F);
         d -= qs;
         qcs += qs;
-        delta[v] = d;  // id order (coalesced); gathered into sweep order later
+        delta[rv] = d;  // straight into sweep order (a scattered 16-byte store; no gather pass)
     }
     tile_sum_i128(qcs, qcs_tile + blockIdx.x);
 }
@@ -419,34 +419,22 @@ __global__ void __launch_bounds__(256) k_delta_sell(SellArgs s, int32_t F, const
         d += qfix(s.ct[v], F);
         d -= qs;
         qcs += qs;
-        delta[v] = d;
+        delta[rv] = d;  // straight into sweep order
     }
     tile_sum_i128(qcs, qcs_tile + blockIdx.x);
 }
 
-// delta in sweep order: ds[i] = delta[order[i]] (random 16-byte reads, coalesced writes)
-__global__ void k_delta_gather(const i128 *delta, const int32_t *order, int64_t n, i128 *ds)
-{
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) ds[i] = delta[order[i]];
-}
-
-void sweep_delta_order(const int32_t *order, SweepBuffers &b, cudaStream_t st)
-{
-    if (b.n == 0) return;
-    k_delta_gather<<<(unsigned)((b.n + 255) / 256), 256, 0, st>>>(b.delta_id, order, b.n, b.delta);
-}
 
 void sweep_delta_stencil(const StencilArgs &s, int64_t N, int32_t F, SweepBuffers &b, cudaStream_t st)
 {
     if (N == 0) return;
-    k_delta_stencil<<<(unsigned)sweep_ntiles(N), 256, 0, st>>>(s, N, F, b.rank, b.delta_id, b.tile_min);
+    k_delta_stencil<<<(unsigned)sweep_ntiles(N), 256, 0, st>>>(s, N, F, b.rank, b.delta, b.tile_min);
 }
 
 void sweep_delta_sell(const SellArgs &s, int32_t F, SweepBuffers &b, cudaStream_t st)
 {
     if (s.n == 0) return;
-    k_delta_sell<<<(unsigned)sweep_ntiles(s.n), 256, 0, st>>>(s, F, b.rank, b.delta_id, b.tile_min);
+    k_delta_sell<<<(unsigned)sweep_ntiles(s.n), 256, 0, st>>>(s, F, b.rank, b.delta, b.tile_min);
 }
 
 // ---------------------------------------------------------------------------
