@@ -491,36 +491,39 @@ __device__ __forceinline__ bool lex_less(i128 a, int64_t ia, i128 b, int64_t ib)
 __global__ void __launch_bounds__(256) k_tile_argmin(const i128 *delta, int64_t n, const i128 *tile_prefix,
                                                      i128 *tile_min, int64_t *tile_arg)
 {
+    // thread t owns the 16 consecutive prefixes base + 16t .. +15: its delta
+    // sum, ONE block-wide exclusive scan of those sums, then a second
+    // (cache-hitting) pass forming P_{i+1} and the first minimum.  Integer
+    // sums are exact, so this order gives the same prefixes as any other.
     __shared__ i128 wsum[8];
     __shared__ i128 smin[8];
     __shared__ int64_t sarg[8];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t base = (int64_t)blockIdx.x * kTile;
-    i128 carry = tile_prefix[blockIdx.x];
+    const int64_t t0 = (int64_t)blockIdx.x * kTile + 16 * (int64_t)threadIdx.x;
+    i128 own = 0;
+#pragma unroll 4
+    for (int q = 0; q < 16; q++)
+        if (t0 + q < n) own += delta[t0 + q];
+    i128 inc = own;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const i128 o = shfl_up_i128(inc, off);
+        if (lane >= off) inc += o;
+    }
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    i128 wpre = 0;
+    for (int k = 0; k < w; k++) wpre += wsum[k];
+    i128 P = tile_prefix[blockIdx.x] + wpre + inc - own;  // P_{t0}
     i128 best = (i128)(((unsigned __int128)1 << 127) - 1);  // +infinity
     int64_t barg = INT64_MAX;
-    for (int r = 0; r < 16; r++) {
-        const int64_t i = base + r * 256 + threadIdx.x;
-        const i128 v = i < n ? delta[i] : (i128)0;
-        i128 inc = v;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const i128 o = shfl_up_i128(inc, off);
-            if (lane >= off) inc += o;
-        }
-        if (lane == 31) wsum[w] = inc;
-        __syncthreads();
-        i128 wpre = 0, tot = 0;
-        for (int k = 0; k < 8; k++) {
-            if (k < w) wpre += wsum[k];
-            tot += wsum[k];
-        }
+#pragma unroll 4
+    for (int q = 0; q < 16; q++) {
+        const int64_t i = t0 + q;
         if (i < n) {
-            const i128 P = carry + wpre + inc;  // P_{i+1}
+            P += delta[i];  // P_{i+1}
             if (lex_less(P, i + 1, best, barg)) { best = P; barg = i + 1; }
         }
-        carry += tot;
-        __syncthreads();
     }
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) {
