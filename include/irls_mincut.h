@@ -96,8 +96,9 @@ typedef struct {
                             (DESIGN.md §6): each group owner stores its C3 slot sums straight into every
                             rank's slot buffer and bumps an arrival counter that the finalize kernel waits
                             on (no slot allreduce), and on z-slabs K5 (CG-CG: the iteration kernel) also
-                            stores z's (w's) boundary planes into the neighbours' ghost planes (no
-                            per-iteration halo exchange).  Peer buffers
+                            stores z's (w's) boundary planes into the neighbours' ghost planes; on CSR
+                            id strips a store kernel writes the send lists' z values into the peers'
+                            ghost blocks before K5's sums are pushed (no per-iteration halo exchange).  Peer buffers
                             are exchanged at create with CUDA IPC handles over NCCL (allocated with
                             cudaMalloc, outside device_alloc); virtual groups use the other ranks' buffers
                             directly.  Results are bit-identical to p2p = 0.  A wait longer than 10 s

@@ -438,8 +438,15 @@ static irls_status enq_body(Ranks &R, const CondArgs &cd, cudaStream_t st)
             v.zpeer_hi = c->zpeer_hi;
             v.plane = c->P;
         }
-        launch_axpy_jacobi(v, red_args_solve(c), cd, st);
+        const bool csr_p2p = c->p2p && c->kind == 1;
+        launch_axpy_jacobi(v, csr_p2p ? red_args(c) : red_args_solve(c), cd, st);
         c->launches++;
+        if (csr_p2p) {  // z halo as peer stores, then the group sums' push (after the stores)
+            launch_p2p_halo_push(c->z, c->send_idx, c->halo_peer_dev, c->halo_pos_dev, c->send_off[c->world],
+                                 c->d_zpeers, c->slots_local, 3, c->g0, c->g1, c->K, c->n_fin, c->d_pslots,
+                                 c->d_pcnt, c->world, c->ctrl, st);
+            c->launches += 2;
+        }
     }
     if (R[0]->multi) {
         if ((s = coll_allreduce(R, 3, st))) return s;
@@ -447,7 +454,7 @@ static irls_status enq_body(Ranks &R, const CondArgs &cd, cudaStream_t st)
             launch_finalize(PH_RZ, c->ctrl, c->slots_glob, cd, p2p_wait_args(c), st);
             c->launches++;
         }
-        if (!(R[0]->p2p && R[0]->kind == 0) && (s = coll_halo(R, true, st))) return s;
+        if (!R[0]->p2p && (s = coll_halo(R, true, st))) return s;
     }
     return last_launch(R[0], "cg body");
 }
@@ -1199,6 +1206,21 @@ static irls_status vgroup_create(irls_vgroup **out, int32_t world, int32_t devic
             if (c->kind == 0 && c->hplan.peer_hi >= 0) {
                 irls_ctx *o = g->ranks[c->hplan.peer_hi];
                 c->zpeer_hi = o->z + o->hplan.recv_lo;
+            }
+            if (c->kind == 1) {  // CSR strips: every rank's z and ghost-block layout
+                std::vector<double *> zp(world);
+                std::vector<int64_t> npad(world);
+                std::vector<std::vector<int64_t>> roff(world);
+                for (int q = 0; q < world; q++) {
+                    zp[q] = g->ranks[q]->z;
+                    npad[q] = g->ranks[q]->npad_own;
+                    roff[q] = g->ranks[q]->recv_off;
+                }
+                s = p2p_set_halo(c, zp, npad, roff);
+                if (s) {
+                    irls_vgroup_destroy(g);
+                    return s;
+                }
             }
             for (int b = 0; b < 2 && c->cgcg && c->kind == 0; b++) {
                 if (c->hplan.peer_lo >= 0) {

@@ -72,7 +72,7 @@ static irls_status alloc_solver(irls_ctx *c, int64_t ghost)
         last_base = b;
         return true;
     };
-    const bool ipc_z = ipc && c->kind == 0;  // z (and CG-CG's w) planes are stored into by the neighbours
+    const bool ipc_z = ipc;  // z (and CG-CG's w on slabs) are stored into by the neighbours
     if (!ghosted(c->z, ipc_z)) return IRLS_ERR_OOM;
     if (ipc_z) c->z_base = last_base;
     if (!ghosted(c->x, false) || !ghosted(c->p0, false) || !ghosted(c->p1, false) || !ghosted(c->r, false) ||
@@ -81,8 +81,8 @@ static irls_status alloc_solver(irls_ctx *c, int64_t ghost)
     c->cgcg = c->opt.cg_variant == IRLS_CG_CG;
     if (c->cgcg) {
         for (int b = 0; b < 2; b++) {
-            if (!ghosted(c->cg_w[b], ipc_z)) return IRLS_ERR_OOM;
-            if (ipc_z) c->w_base[b] = last_base;
+            if (!ghosted(c->cg_w[b], ipc_z && c->kind == 0)) return IRLS_ERR_OOM;
+            if (ipc_z && c->kind == 0) c->w_base[b] = last_base;
         }
         if (!ghosted(c->cg_r2, false) || !ghosted(c->cg_s[0], false) || !ghosted(c->cg_s[1], false))
             return IRLS_ERR_OOM;
@@ -132,10 +132,37 @@ irls_status p2p_set_peers(irls_ctx *c, const std::vector<double *> &bufs)
     return IRLS_OK;
 }
 
+// CSR strips with p2p: where entry i of this rank's send lists lands — rank q
+// (the list's peer) at offset npad_own_q + recv_off_q[me] + (i - send_off[q])
+// of q's z (its ghost block keeps each sender's values contiguous, in the
+// order of the sender's list).
+irls_status p2p_set_halo(irls_ctx *c, const std::vector<double *> &zpeers, const std::vector<int64_t> &peer_npad,
+                         const std::vector<std::vector<int64_t>> &peer_recv_off)
+{
+    const int W = c->world;
+    const int64_t ns = c->send_off[W];
+    std::vector<int32_t> hp(std::max<int64_t>(ns, 1), 0);
+    std::vector<int64_t> pos(std::max<int64_t>(ns, 1), 0);
+    for (int q = 0; q < W; q++)
+        for (int64_t i = c->send_off[q]; i < c->send_off[q + 1]; i++) {
+            hp[i] = q;
+            pos[i] = peer_npad[q] + peer_recv_off[q][c->rank] + (i - c->send_off[q]);
+        }
+    c->halo_peer_dev = dalloc<int32_t>(c, std::max<int64_t>(ns, 1));
+    c->halo_pos_dev = dalloc<int64_t>(c, std::max<int64_t>(ns, 1));
+    c->d_zpeers = (double **)dalloc<double *>(c, W);
+    if (!c->halo_peer_dev || !c->halo_pos_dev || !c->d_zpeers) return fail(c, IRLS_ERR_OOM, "p2p halo");
+    CK(memcpy_sync(c, c->halo_peer_dev, hp.data(), sizeof(int32_t) * hp.size(), cudaMemcpyHostToDevice));
+    CK(memcpy_sync(c, c->halo_pos_dev, pos.data(), sizeof(int64_t) * pos.size(), cudaMemcpyHostToDevice));
+    CK(memcpy_sync(c, c->d_zpeers, zpeers.data(), sizeof(double *) * W, cudaMemcpyHostToDevice));
+    return IRLS_OK;
+}
+
 // One rank's exported buffers, exchanged with an NCCL all-gather at create.
 struct PeerRec {
     cudaIpcMemHandle_t hbuf, hz, hw[2];
     int64_t zoff_recv_lo, zoff_recv_hi;  // ghost planes, in doubles from the allocation start (z and w alike)
+    int64_t zoff_own, npad_own, recv_off[9];  // CSR strips: z's owned start and the ghost block layout
 };
 
 static irls_status p2p_exchange(irls_ctx *c)
@@ -144,12 +171,16 @@ static irls_status p2p_exchange(irls_ctx *c)
     PeerRec mine;
     memset(&mine, 0, sizeof(mine));
     CK(cudaIpcGetMemHandle(&mine.hbuf, c->p2p_buf));
+    CK(cudaIpcGetMemHandle(&mine.hz, c->z_base));
+    mine.zoff_own = c->z - c->z_base;
     if (c->kind == 0) {
-        CK(cudaIpcGetMemHandle(&mine.hz, c->z_base));
         mine.zoff_recv_lo = (c->z - c->z_base) + c->hplan.recv_lo;
         mine.zoff_recv_hi = (c->z - c->z_base) + c->hplan.recv_hi;
         if (c->cgcg)
             for (int b = 0; b < 2; b++) CK(cudaIpcGetMemHandle(&mine.hw[b], c->w_base[b]));
+    } else {
+        mine.npad_own = c->npad_own;
+        for (int q = 0; q <= W && q < 9; q++) mine.recv_off[q] = c->recv_off[q];
     }
     std::vector<PeerRec> all(W);
     void *dev = nullptr;
@@ -178,6 +209,19 @@ static irls_status p2p_exchange(irls_ctx *c)
     for (int w = 0; w < W; w++) {
         if (w == c->rank) bufs[w] = c->p2p_buf;
         else if ((s = open(all[w].hbuf, &bufs[w]))) return s;
+    }
+    if (c->kind == 1) {  // every peer's z (its ghost block receives this rank's send lists)
+        std::vector<double *> zp(W);
+        std::vector<int64_t> npad(W);
+        std::vector<std::vector<int64_t>> roff(W);
+        for (int w = 0; w < W; w++) {
+            double *b = c->z_base;
+            if (w != c->rank && (s = open(all[w].hz, &b))) return s;
+            zp[w] = b + all[w].zoff_own;
+            npad[w] = all[w].npad_own;
+            roff[w].assign(all[w].recv_off, all[w].recv_off + W + 1);
+        }
+        if ((s = p2p_set_halo(c, zp, npad, roff))) return s;
     }
     if (c->kind == 0) {
         double *b;

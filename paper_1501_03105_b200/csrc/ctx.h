@@ -134,6 +134,11 @@ struct irls_ctx {
     double *wpeer_lo[2] = {nullptr, nullptr}, *wpeer_hi[2] = {nullptr, nullptr};  // CG-CG: neighbours' w ghost planes
     double *w_base[2] = {nullptr, nullptr};  // CG-CG w allocations (IPC export)
     double *z_base = nullptr;     // start of z's allocation (IPC export)
+    // CSR strips with p2p: the z halo as peer stores (entry i of the send
+    // lists goes to rank halo_peer[i] at offset halo_pos[i] of its z array)
+    int32_t *halo_peer_dev = nullptr;
+    int64_t *halo_pos_dev = nullptr;
+    double **d_zpeers = nullptr;  // device [world]: every rank's z (owned start)
     std::vector<void *> raw_allocs;  // cudaMalloc'd, IPC-exportable (multi-process p2p)
     std::vector<void *> ipc_open;    // peers' allocations opened with cudaIpcOpenMemHandle
 

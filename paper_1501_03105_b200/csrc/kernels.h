@@ -111,6 +111,12 @@ void launch_sell_cgcg(const SellArgs &s, const VecArgs &v, const CgArgs &g, cons
 // ghost entries [lo, lo + n): s = w + beta s_old, r = r - alpha s (the owner's formulas)
 void launch_cgcg_ghost(const CgArgs &g, int64_t lo, int64_t n, const DevCtrl *ctrl, cudaStream_t st);
 void launch_cgcg_finish(const VecArgs &v, const DevCtrl *ctrl, cudaStream_t st);
+// CSR strips with p2p: the z halo as peer stores, then this rank's group sums
+// (nq quantities of groups [g0, g1)) and arrivals pushed to every rank
+void launch_p2p_halo_push(const double *z, const int32_t *send_idx, const int32_t *peer, const int64_t *pos,
+                          int64_t n, double *const *zpeers, const double *slots, int nq, int g0, int g1, int32_t K,
+                          int n_fin, double *const *pslots, unsigned long long *const *pcnt, int world,
+                          const DevCtrl *ctrl, cudaStream_t st);
 void launch_finalize(int phase, DevCtrl *ctrl, const double *slots, const CondArgs &cd, const P2PWait &pw,
                      cudaStream_t st);
 // write the step report from the control block

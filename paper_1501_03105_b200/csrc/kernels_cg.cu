@@ -667,6 +667,50 @@ void launch_cgcg_ghost(const CgArgs &g, int64_t lo, int64_t n, const DevCtrl *ct
     if (n > 0) k_cgcg_ghost<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g, lo, n, ctrl);
 }
 
+// ---------------------------------------------------------------------------
+// CSR strips with p2p: after K5 (which keeps its group sums local), the z
+// values of the send lists are stored straight into the peers' ghost blocks,
+// then one block publishes this rank's RZ group sums to every rank and bumps
+// their arrival counters — so a peer sees the new ghost z before the arrival
+// it waits on.  Both skip a finished solve (as K5 and the RZ finalize do).
+// ---------------------------------------------------------------------------
+__global__ void k_p2p_halo_store(const double *z, const int32_t *send_idx, const int32_t *peer, const int64_t *pos,
+                                 int64_t n, double *const *zpeers, const DevCtrl *ctrl)
+{
+    if (ctrl->done) return;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        zpeers[peer[i]][pos[i]] = z[send_idx[i]];
+    __threadfence_system();
+}
+
+__global__ void k_p2p_push(const double *slots, int nq, int g0, int g1, int32_t K, int n_fin,
+                           double *const *pslots, unsigned long long *const *pcnt, int world, const DevCtrl *ctrl)
+{
+    if (ctrl->done || threadIdx.x != 0) return;
+    __threadfence_system();
+    const int off = (int)(ctrl->red_seq & 1u) * (kMaxQ * kGroups);
+    for (int w = 0; w < world; w++)
+        for (int q = 0; q < nq; q++)
+            for (int g = g0; g < g1; g++)
+                if (group_lo(g + 1, K) > group_lo(g, K))  // non-empty groups only (empty ones stay +0.0)
+                    pslots[w][off + q * kGroups + g] = slots[q * kGroups + g];
+    __threadfence_system();
+    for (int w = 0; w < world; w++)
+        if (n_fin > 0) atomicAdd_system(pcnt[w], (unsigned long long)n_fin);
+}
+
+void launch_p2p_halo_push(const double *z, const int32_t *send_idx, const int32_t *peer, const int64_t *pos,
+                          int64_t n, double *const *zpeers, const double *slots, int nq, int g0, int g1, int32_t K,
+                          int n_fin, double *const *pslots, unsigned long long *const *pcnt, int world,
+                          const DevCtrl *ctrl, cudaStream_t st)
+{
+    if (n > 0) {
+        const unsigned nb = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 4);
+        k_p2p_halo_store<<<nb, 256, 0, st>>>(z, send_idx, peer, pos, n, zpeers, ctrl);
+    }
+    k_p2p_push<<<1, 32, 0, st>>>(slots, nq, g0, g1, K, n_fin, pslots, pcnt, world, ctrl);
+}
+
 // Virtual-group "allreduce": dst = sum over ranks (rank order) of src[r].
 __global__ void k_vsum(const double *const *src, int W, int n, double *dst)
 {

@@ -198,12 +198,14 @@ def test_vgroup_csr_strips(irls, world, p2p):
 
 
 @pytest.mark.slow
-def test_vgroup_config3_world8(irls):
+@pytest.mark.parametrize("p2p", [0, 1])
+def test_vgroup_config3_world8(irls, p2p):
     """BASELINE config 3 (road-like CSR, 23.7M nodes) as 8 id strips: every
-    step's iteration count, x^(50) and the sweep equal one rank bitwise."""
+    step's iteration count, x^(50) and the sweep equal one rank bitwise
+    (p2p: the strips' z halo as peer stores + pushed group sums)."""
     spec = gen.config3()
     m, reps1, tot1, sw1 = single(irls, spec, irls.options(T=50), 50)
-    g = irls.VGroup(spec, 8, irls.options(T=50))
+    g = irls.VGroup(spec, 8, irls.options(T=50, p2p=p2p))
     reps, tot = g.irls_vgroup_solve(irls.IRLS_FROM_SCRATCH, T=50)
     assert [r["cg_iters"] for r in reps] == [r["cg_iters"] for r in reps1]
     assert np.array_equal(g.irls_vgroup_get_potentials(), m.irls_get_potentials())
