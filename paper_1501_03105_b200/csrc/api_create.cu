@@ -500,7 +500,7 @@ irls_status create_csr_impl(irls_ctx **out, const irls_comm_desc *comm, int64_t 
         std::vector<Ent> tmp;
         for (int64_t u = a; u < b; u++) mptr[u + 1] = merge_row(u, tmp, nullptr, nullptr);
     });
-    for (int64_t u = 0; u < n; u++) mptr[u + 1] += mptr[u];
+    parallel_prefix(mptr.data(), n);
     HostBuf<int32_t> mcol(mptr[n]);
     HostBuf<double> mw(mptr[n]);
     parallel_for(n, [&](int, int64_t a, int64_t b) {
@@ -531,9 +531,11 @@ irls_status create_csr_impl(irls_ctx **out, const irls_comm_desc *comm, int64_t 
         if (u >= hi2) u++;
         return u;
     };
-    std::vector<double> hcs(std::max<int64_t>(nr, 1), 0.0), hct(std::max<int64_t>(nr, 1), 0.0);
-    std::vector<int64_t> orig(std::max<int64_t>(nr, 1), 0);
-    std::vector<int64_t> aptr(nr + 1, 0);
+    // every entry is written by the parallel pass below (no serial zero fill)
+    HostBuf<double> hcs(nr), hct(nr);
+    HostBuf<int64_t> orig(nr);
+    HostBuf<int64_t> aptr(nr + 1);
+    aptr[0] = 0;
     double cst = 0.0;
     for (int64_t e = mptr[s_]; e < mptr[s_ + 1]; e++)
         if (mcol[e] == t_) cst = mw[e];
@@ -541,6 +543,8 @@ irls_status create_csr_impl(irls_ctx **out, const irls_comm_desc *comm, int64_t 
         for (int64_t r = a; r < b; r++) {
             const int64_t u = orig_of(r);
             orig[r] = u;
+            hcs[r] = 0.0;
+            hct[r] = 0.0;
             int64_t k = 0;
             for (int64_t e = mptr[u]; e < mptr[u + 1]; e++) {
                 const int64_t v = mcol[e];
@@ -551,7 +555,7 @@ irls_status create_csr_impl(irls_ctx **out, const irls_comm_desc *comm, int64_t 
             aptr[r + 1] = k;
         }
     });
-    for (int64_t r = 0; r < nr; r++) aptr[r + 1] += aptr[r];
+    parallel_prefix(aptr.data(), nr);
     HostBuf<int32_t> aidx(aptr[nr]);
     HostBuf<double> ac(aptr[nr]);
     std::vector<int64_t> tcnt(host_threads(nr), 0);

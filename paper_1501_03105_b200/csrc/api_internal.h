@@ -263,6 +263,33 @@ static inline void parallel_for(int64_t n, F f)
     for (auto &t : th) t.join();
 }
 
+// p[i + 1] += p[i] for i = 0 .. n - 1 (counts in p[1..n] -> offsets), on the
+// host threads: block sums, their serial scan, then each block adds its
+// offset.  Integer sums: the result does not depend on the thread count.
+static inline void parallel_prefix(int64_t *p, int64_t n)
+{
+    const int nt = host_threads(n);
+    if (nt == 1) {
+        for (int64_t i = 0; i < n; i++) p[i + 1] += p[i];
+        return;
+    }
+    std::vector<int64_t> tot(nt, 0);
+    parallel_for(n, [&](int t, int64_t a, int64_t b) {
+        int64_t acc = 0;
+        for (int64_t i = a; i < b; i++) acc += p[i + 1];
+        tot[t] = acc;
+    });
+    std::vector<int64_t> off(nt, p[0]);
+    for (int t = 1; t < nt; t++) off[t] = off[t - 1] + tot[t - 1];
+    parallel_for(n, [&](int t, int64_t a, int64_t b) {
+        int64_t run = off[t];
+        for (int64_t i = a; i < b; i++) {
+            run += p[i + 1];
+            p[i + 1] = run;
+        }
+    });
+}
+
 // ---- shared between the files
 // api.cu
 irls_status gather_x(irls_ctx *c, double **full);
