@@ -640,12 +640,19 @@ irls_status create_csr_impl(irls_ctx **out, const irls_comm_desc *comm, int64_t 
     const int64_t nsl = (nr + kSell - 1) / kSell;
     std::vector<int64_t> sptr(nsl + 1, 0);
     int64_t sell_wmax = 0;
-    for (int64_t sl = 0; sl < nsl; sl++) {
-        int64_t wmax = 0;
-        for (int64_t r = sl * kSell; r < std::min<int64_t>(nr, sl * kSell + kSell); r++)
-            wmax = std::max(wmax, aptr[r + 1] - aptr[r]);
-        sptr[sl + 1] = sptr[sl] + kSell * wmax;
-        sell_wmax = std::max(sell_wmax, wmax);
+    {
+        std::vector<int64_t> twmax(host_threads(nsl), 0);
+        parallel_for(nsl, [&](int i, int64_t a, int64_t b) {
+            for (int64_t sl = a; sl < b; sl++) {
+                int64_t wmax = 0;
+                for (int64_t r = sl * kSell; r < std::min<int64_t>(nr, sl * kSell + kSell); r++)
+                    wmax = std::max(wmax, aptr[r + 1] - aptr[r]);
+                sptr[sl + 1] = kSell * wmax;
+                twmax[i] = std::max(twmax[i], wmax);
+            }
+        });
+        parallel_prefix(sptr.data(), nsl);
+        for (int64_t wm : twmax) sell_wmax = std::max(sell_wmax, wm);
     }
     const int64_t nent = sptr[nsl];
     HostBuf<int32_t> scol(nent);
