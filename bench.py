@@ -191,7 +191,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--config", default="config4")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-planes", type=int, default=8)
     ap.add_argument("--ref-T", type=int, default=3)
@@ -399,21 +399,31 @@ def main():
     d2h = side_host.shape[0] if rank == 0 else 0
     import ctypes as C
 
-    def e2e_step():
+    phase_ms = {"create": 0.0, "solve": 0.0, "sweep_d2h": 0.0, "destroy": 0.0}
+
+    def e2e_step(record=False):
         comm = fresh_comm()  # a fresh NCCL id per communicator (part of the user's create path)
+        t0 = time.perf_counter()
         if csr:
             mm = I.MinCut.irls_mincut_create_csr(spec["n"], pinned["row_ptr"], pinned["col"], pinned["w"], spec["s"],
                                                  spec["t"], opts, comm)
         else:
             mm = I.MinCut.irls_mincut_create_stencil(spec["nx"], spec["ny"], spec["nz"], pinned["cx"], pinned["cy"],
                                                      pinned["cz"], pinned["cs"], pinned["ct"], opts, comm)
+        t1 = time.perf_counter()
         _, tot = mm.irls_solve(I.IRLS_FROM_SCRATCH, T=T, reports=False)
+        t2 = time.perf_counter()
         kk, cc = C.c_int64(), C.c_double()
         rc = I.lib().irls_sweep_cut(mm.h, side_host.ctypes.data_as(C.c_void_p) if rank == 0 else None, None,
                                     C.byref(kk), C.byref(cc))
         if rc:
             raise I.IrlsError(rc, "irls_sweep_cut")
+        t3 = time.perf_counter()
         mm.close()
+        t4 = time.perf_counter()
+        if record:  # host clock around each (blocking) call: where the end-to-end time goes
+            for key, dt in (("create", t1 - t0), ("solve", t2 - t1), ("sweep_d2h", t3 - t2), ("destroy", t4 - t3)):
+                phase_ms[key] += 1e3 * dt / args.e2e_steps
         return tot
 
     e2e_step()  # warm-up (first-touch of the allocator's blocks for the sweep buffers)
@@ -421,8 +431,14 @@ def main():
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    step_ms = []
     for _ in range(args.e2e_steps):
-        e2e_iters += e2e_step()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        e2e_iters += e2e_step(record=True)
+        s1.record(stream)
+        s1.synchronize()
+        step_ms.append(s0.elapsed_time(s1))
     e1.record(stream)
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1))
@@ -464,7 +480,7 @@ def main():
         "two_level": two_level,
         "fixed_point_exit": fpx,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": e2e_ms / args.e2e_steps,
+                "ms_per_step": e2e_ms / args.e2e_steps, "step_ms": step_ms, "phase_ms_host_clock": phase_ms,
                 "what": "create from pinned host arrays + solve + sweep (side to host) + destroy"},
         "gpu_launches": launches,
         "clocks": clocks,

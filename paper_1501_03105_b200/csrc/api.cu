@@ -1124,7 +1124,7 @@ extern "C" void irls_mincut_destroy(irls_ctx *c)
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (void *p : c->ipc_open) cudaIpcCloseMemHandle(p);
     for (void *p : c->raw_allocs) cudaFree(p);
-    if (c->h_done) cudaFreeHost(c->h_done);
+    pinned_flag_put(c->h_done);
     if (c->nccl) ncclCommDestroy(c->nccl);
     if (c->side_stream) cudaStreamDestroy(c->side_stream);
     if (c->side_stream2) cudaStreamDestroy(c->side_stream2);

@@ -2,11 +2,45 @@
 // inputs (A6-A8), the stencil slab plan, the CSR preparation (duplicate
 // merging, symmetry, terminal split, Prop. 1, SELL-64, id strips with ghost
 // blocks and send lists) on host threads, device allocation and upload.
+#include <mutex>
 #include "api_internal.h"
 
 // Device memory comes from the device's stream-ordered pool with an unbounded
 // release threshold: a create / destroy cycle maps HBM once and then reuses
 // it (sizes here are GBs; cudaMalloc / cudaFree would remap every time).
+// One pinned int per context for the host loop's "done" readback, from a
+// process-wide pinned page (a cudaMallocHost / cudaFreeHost pair per context
+// costs milliseconds and cudaFreeHost synchronises the device).
+static std::mutex g_pin_mu;
+static int *g_pin_page = nullptr;
+static std::vector<int> g_pin_free;
+int *pinned_flag_get()
+{
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    if (!g_pin_page) {
+        constexpr int kSlots = 4096;
+        if (cudaMallocHost(&g_pin_page, sizeof(int) * kSlots) != cudaSuccess) {
+            g_pin_page = nullptr;
+            return nullptr;
+        }
+        for (int i = kSlots - 1; i >= 0; i--) g_pin_free.push_back(i);
+    }
+    if (g_pin_free.empty()) {  // more live contexts than slots: a private pinned int
+        int *p = nullptr;
+        return cudaMallocHost(&p, sizeof(int)) == cudaSuccess ? p : nullptr;
+    }
+    const int i = g_pin_free.back();
+    g_pin_free.pop_back();
+    return g_pin_page + i;
+}
+void pinned_flag_put(int *p)
+{
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    if (g_pin_page && p >= g_pin_page && p < g_pin_page + 4096) g_pin_free.push_back((int)(p - g_pin_page));
+    else cudaFreeHost(p);
+}
+
 static void setup_pool(int device)
 {
     cudaMemPool_t pool;
@@ -45,7 +79,8 @@ static irls_status common_setup(irls_ctx *c, const irls_comm_desc *comm, const i
     }
     CK(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&c->side_stream2, cudaStreamNonBlocking));
-    CK(cudaMallocHost(&c->h_done, sizeof(int)));
+    c->h_done = pinned_flag_get();
+    if (!c->h_done) return IRLS_ERR_OOM;
     setup_pool(c->device);
     small_cg_prepare();
     return IRLS_OK;

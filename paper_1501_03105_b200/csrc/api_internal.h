@@ -308,6 +308,8 @@ bool grid_nonsingular(int32_t nx, int32_t ny, int32_t nz, const double *cx, cons
 irls_status sweep_rank0(irls_ctx *c, const double *xfull, uint8_t *side, int32_t *order, int64_t *k,
                         double *cut_value);
 irls_status p2p_set_peers(irls_ctx *c, const std::vector<double *> &bufs);
+int *pinned_flag_get();
+void pinned_flag_put(int *p);
 irls_status p2p_set_halo(irls_ctx *c, const std::vector<double *> &zpeers, const std::vector<int64_t> &peer_npad,
                          const std::vector<std::vector<int64_t>> &peer_recv_off);
 irls_status two_level_rank0(irls_ctx *c, const double *xfull, uint8_t *side, irls_two_level_report *r,
