@@ -101,7 +101,7 @@ typedef struct {
                             ghost blocks before K5's sums are pushed (no per-iteration halo exchange).  Peer buffers
                             are exchanged at create with CUDA IPC handles over NCCL (allocated with
                             cudaMalloc, outside device_alloc); virtual groups use the other ranks' buffers
-                            directly.  Results are bit-identical to p2p = 0.  A wait longer than 10 s
+                            directly.  Results are bit-identical to p2p = 0.  A wait longer than 120 s
                             ends the solve with IRLS_ERR_NCCL.  Ignored on a single-rank context.
                             Default 0 (NCCL). */
     int32_t cg_variant;  /* irls_cg_variant; default IRLS_CG_HS */

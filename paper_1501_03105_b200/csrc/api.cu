@@ -832,7 +832,7 @@ irls_status run_solves(Ranks &R, int mode0, int mode_rest, int count, irls_step_
             if (reps) copy_report(h[i], reps + i, ms, ms_asm);
             if (h[i].status != 0 && !s)
                 s = fail(c, (irls_status)h[i].status,
-                         h[i].status == ST_P2P_TIMEOUT ? "peer-memory collective: wait timed out (10 s)"
+                         h[i].status == ST_P2P_TIMEOUT ? "peer-memory collective: wait timed out (120 s)"
                                                        : "CG breakdown (p'Ap <= 0 or non-finite scalar)");
         }
         if (c->graph_iters_pending) c->launches += c->gl_body * tot;

@@ -224,7 +224,8 @@ __device__ __forceinline__ double slot_total(const double *slots, int q)
 // Peer-memory slot collective, consumer side (one thread): wait until every
 // non-empty group of this reduction has arrived (counter >= (red_seq + 1) *
 // n_groups), consume it (red_seq + 1) and return its parity buffer.  A wait
-// longer than 10 s (a peer died or the ranks fell out of step) sets status
+// longer than 120 s (a peer died or the ranks fell out of step; ranks may
+// legitimately enter a solve seconds apart) sets status
 // ST_P2P_TIMEOUT, ends the solve and returns nullptr.
 enum { ST_P2P_TIMEOUT = 10 };  // = IRLS_ERR_NCCL (a collective failed)
 struct P2PWait {
@@ -246,7 +247,7 @@ __device__ inline const double *p2p_wait(DevCtrl *c, const P2PWait &pw)
     if (ld_acquire_sys(pw.cnt) < target) {
         const unsigned long long t0 = global_ns();
         while (ld_acquire_sys(pw.cnt) < target) {
-            if (global_ns() - t0 > 10000000000ull) {
+            if (global_ns() - t0 > 120000000000ull) {
                 c->status = ST_P2P_TIMEOUT;
                 c->done = 1;
                 return nullptr;
