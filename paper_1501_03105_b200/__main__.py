@@ -2,6 +2,7 @@
 
     python -m paper_1501_03105_b200 --config 2 --rounding both --trace trace.csv
     python -m paper_1501_03105_b200 --graph g.npz --lambda2 --exact
+    python -m paper_1501_03105_b200 --config 4 --virtual-ranks 8 --p2p
 
 A graph file is an .npz with either a grid (kind="stencil": nx, ny, nz, cx,
 cy, cz, cs, ct) or a CSR graph over all nodes incl. s and t (kind="csr": n,
@@ -60,6 +61,9 @@ def main(argv=None):
     ap.add_argument("--exact", action="store_true", help="exact min cut mu* and delta (Eq. 13)")
     ap.add_argument("--trace", help="write the per-step report as CSV")
     ap.add_argument("--side", help="write the source-side indicator (uint8, one per node) as .npy")
+    ap.add_argument("--virtual-ranks", type=int, default=0,
+                    help="run the W-rank data path (z-slabs / id strips) as a virtual group on this GPU")
+    ap.add_argument("--p2p", action="store_true", help="virtual ranks: peer-memory collectives")
     args = ap.parse_args(argv)
 
     build.build()
@@ -73,6 +77,25 @@ def main(argv=None):
                      warm_start=0 if args.cold else 1, fixed_point_exit=1 if args.fixed_point_exit else 0,
                      record_trace=1 if args.trace else 0,
                      cg_variant=I.IRLS_CG_CG if args.cg_variant == "cg" else I.IRLS_CG_HS)
+    if args.virtual_ranks:
+        opts.p2p = 1 if args.p2p else 0
+        t0 = time.perf_counter()
+        g = I.VGroup(spec, args.virtual_ranks, opts)
+        out = {"graph": what, "virtual_ranks": args.virtual_ranks, "p2p": bool(args.p2p),
+               "create_s": time.perf_counter() - t0}
+        t0 = time.perf_counter()
+        reps, iters = g.irls_vgroup_solve(I.IRLS_FROM_SCRATCH)
+        out.update({"solve_s": time.perf_counter() - t0, "cg_iters": iters})
+        side, _, k, cut = g.irls_vgroup_sweep_cut()
+        out["sweep"] = {"cut": cut, "k": k}
+        if args.rounding in ("two_level", "both"):
+            side2, rep = g.irls_vgroup_two_level_cut()
+            out["two_level"] = {"cut": rep["cut_value"], "coarse_nodes": rep["nc"]}
+        if args.side:
+            np.save(args.side, side)
+        g.close()
+        print(json.dumps(out, indent=1))
+        return
     t0 = time.perf_counter()
     m = I.MinCut.from_spec(spec, opts)
     st = m.irls_get_stats()

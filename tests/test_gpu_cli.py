@@ -56,3 +56,22 @@ def test_cli_graph_file(ready, tmp_path):
     tl = S.two_level()
     assert r["two_level"]["cut"] == tl.cut_value
     assert np.array_equal(np.load(side_path), tl.side)
+
+
+def test_cli_virtual_ranks(tmp_path):
+    """--virtual-ranks W runs the W-rank data path on one GPU: the same cut as
+    the single-rank run."""
+    import json
+    import subprocess
+    import sys
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    single = json.loads(subprocess.run([sys.executable, "-m", "paper_1501_03105_b200", "--config", "2", "--T", "10"],
+                                       check=True, capture_output=True, text=True, cwd=root).stdout)
+    multi = json.loads(subprocess.run([sys.executable, "-m", "paper_1501_03105_b200", "--config", "2", "--T", "10",
+                                       "--virtual-ranks", "4", "--p2p"],
+                                      check=True, capture_output=True, text=True, cwd=root).stdout)
+    assert multi["cg_iters"] == single["cg_iters"]
+    assert multi["sweep"]["cut"] == single["sweep"]["cut"] and multi["sweep"]["k"] == single["sweep"]["k"]
