@@ -328,7 +328,8 @@ static irls_status enq_assemble(Ranks &R, int mode, const CondArgs &cd, cudaStre
             c->launches += launch_stencil_assemble_ex(stencil_args(c, false), v, ra, cd, mode, c->opt.eps, c->gs_diag,
                                                       c->gt_diag, st);
         else
-            c->launches += launch_sell_assemble_ex(sell_args(c), v, ra, cd, mode, c->opt.eps, c->gs_diag, c->gt_diag, st);
+            c->launches += launch_sell_assemble_ex(sell_args(c), v, ra, cd, mode, c->opt.eps, c->gs_diag,
+                                                   c->gt_diag, st);
     }
     if (R[0]->multi) {
         if ((s = coll_allreduce(R, 5, st))) return s;
@@ -675,7 +676,8 @@ static irls_status build_graph_multi(irls_ctx *c, int mode)
         }
         cudaGraph_t bg;
         e = cudaStreamEndCapture(c->side_stream2, &bg);
-        if (!s && e != cudaSuccess) s = fail(c, IRLS_ERR_CUDA, std::string("multi-step graph: ") + cudaGetErrorString(e));
+        if (!s && e != cudaSuccess)
+            s = fail(c, IRLS_ERR_CUDA, std::string("multi-step graph: ") + cudaGetErrorString(e));
     }
     const int64_t per_step = c->launches;
     if (!s && fpx) launch_fill_reports(c->ctrl, c->reports, st);

@@ -788,7 +788,8 @@ irls_status create_csr_impl(irls_ctx **out, const irls_comm_desc *comm, int64_t 
                 const int64_t v = aidx[aptr[gr] + k];
                 const int64_t lv = (v >= lo && v < hi)
                                        ? v - lo
-                                       : c->npad_own + (std::lower_bound(ghosts.begin(), ghosts.end(), (int32_t)v) - ghosts.begin());
+                                       : c->npad_own + (std::lower_bound(ghosts.begin(), ghosts.end(), (int32_t)v) -
+                                                        ghosts.begin());
                 lscol[lsptr[sl] + kSell * k + ln] = (int32_t)lv;
                 lscap[lsptr[sl] + kSell * k + ln] = ac[aptr[gr] + k];
             }
@@ -843,7 +844,8 @@ irls_status create_csr_impl(irls_ctx **out, const irls_comm_desc *comm, int64_t 
                 up(c->lct, hct.data() + c->lo, sizeof(double) * c->n_own);
             }
             up(c->send_idx, lsend.data(), sizeof(int32_t) * lsend.size());
-            if (e != cudaSuccess) st = fail(c, IRLS_ERR_CUDA, std::string("csr strip upload: ") + cudaGetErrorString(e));
+            if (e != cudaSuccess)
+                st = fail(c, IRLS_ERR_CUDA, std::string("csr strip upload: ") + cudaGetErrorString(e));
         }
     }
     if (!st) st = init_nccl(c, comm);

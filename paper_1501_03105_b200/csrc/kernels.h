@@ -162,7 +162,8 @@ void launch_pair_finish(const VecArgs &v, DevCtrl *ctrl, cudaStream_t st);
 // sell_pair.cu (widest slice <= 8): false when the generic SELL kernel must run
 bool launch_sellp_assemble(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, int mode,
                            double eps, double *gs_out, double *gt_out, cudaStream_t st);
-bool launch_sellp_pspmv(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, cudaStream_t st, bool w0 = false);
+bool launch_sellp_pspmv(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, cudaStream_t st,
+                        bool w0 = false);
 
 // ---------------------------------------------------------------------------
 // Sweep cut (K8-K12)

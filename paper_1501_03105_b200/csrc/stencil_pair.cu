@@ -528,7 +528,8 @@ struct CgNb {
 };
 
 template <int MINB>
-__global__ void __launch_bounds__(kThreads, MINB) k_cgcg_pair(StencilArgs s, VecArgs v, CgArgs g, RedArgs ra, CondArgs cd)
+__global__ void __launch_bounds__(kThreads, MINB) k_cgcg_pair(StencilArgs s, VecArgs v, CgArgs g, RedArgs ra,
+                                                           CondArgs cd)
 {
     DevCtrl *ctrl = ra.ctrl;
     if (ctrl->done) {
