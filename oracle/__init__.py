@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "irls_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-CFLAGS = ["-O2", "-std=gnu11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared"]
+CFLAGS = ["-O2", "-std=gnu11", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared"]
 
 
 def build(force: bool = False) -> str:
@@ -59,6 +59,7 @@ def lib():
         L.orc_graph_from_stencil.argtypes = [C.POINTER(P), C.c_int64, C.c_int64, C.c_int64, dp, dp, dp, dp, dp]
         L.orc_graph_from_csr.argtypes = [C.POINTER(P), C.c_int64, i64p, i32p, dp, C.c_int64, C.c_int64]
         L.orc_graph_free.argtypes = [P]
+        L.orc_set_num_threads.argtypes = [C.c_int]; L.orc_set_num_threads.restype = C.c_int
         for f in ("orc_graph_n", "orc_graph_n_total", "orc_graph_nnz"):
             getattr(L, f).argtypes = [P]; getattr(L, f).restype = C.c_int64
         L.orc_graph_c_st.argtypes = [P]; L.orc_graph_c_st.restype = C.c_double
@@ -105,6 +106,12 @@ class OracleError(RuntimeError):
 def _check(rc, where):
     if rc != 0:
         raise OracleError(rc, where)
+
+
+def set_num_threads(n: int = 0) -> int:
+    """OpenMP threads of the oracle (0: keep); returns the count in effect.
+    Results do not depend on it (tests/test_oracle_threads.py)."""
+    return lib().orc_set_num_threads(int(n))
 
 
 def c3_sum(v) -> float:

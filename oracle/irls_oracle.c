@@ -27,8 +27,30 @@
  */
 #include <math.h>
 #include <stdint.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <stdlib.h>
 #include <string.h>
+
+/* Threads (SURVEY §8(d) "OpenMP over C3 chunks"): every parallel loop below
+ * computes elements independently (a node's value from its own inputs in C2
+ * order, a chunk's C3 partial from its own 4096 elements), so the results
+ * are bitwise independent of the thread count (pinned by
+ * tests/test_oracle_threads.py).  Sums across elements happen only in the
+ * fixed C3 tree. */
+#define OMP_FOR _Pragma("omp parallel for schedule(static)")
+
+int orc_set_num_threads(int n)
+{
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+    return omp_get_max_threads();
+#else
+    (void)n;
+    return 1;
+#endif
+}
 
 /* status codes: numerically equal to irls_status in include/irls_mincut.h by
  * specification; deliberately not shared. */
@@ -320,7 +342,7 @@ static double c3_list(double *a, int64_t m)
     if (m == 0) return 0.0;
     while (m > 1) {
         int64_t K = (m + C3_CHUNK - 1) / C3_CHUNK;
-        for (int64_t k = 0; k < K; k++) a[k] = c3_chunk(a, m, k * C3_CHUNK);
+        for (int64_t k = 0; k < K; k++) a[k] = c3_chunk(a, m, k * C3_CHUNK); /* in place: sequential */
         m = K;
     }
     return a[0];
@@ -334,6 +356,7 @@ double orc_c3_sum(const double *v, int64_t n)
     int64_t K = (n + C3_CHUNK - 1) / C3_CHUNK;
     double *part = (double *)malloc(sizeof(double) * (size_t)(K > 0 ? K : 1));
     double gs[C3_GROUPS];
+    OMP_FOR
     for (int64_t k = 0; k < K; k++) part[k] = c3_chunk(v, n, k * C3_CHUNK);
     for (int g = 0; g < C3_GROUPS; g++) {
         int64_t lo = (int64_t)g * K / C3_GROUPS, hi = (int64_t)(g + 1) * K / C3_GROUPS;
@@ -351,6 +374,7 @@ void orc_c3_group_sums(const double *v, int64_t n, double *out8)
 {
     int64_t K = (n + C3_CHUNK - 1) / C3_CHUNK;
     double *part = (double *)malloc(sizeof(double) * (size_t)(K > 0 ? K : 1));
+    OMP_FOR
     for (int64_t k = 0; k < K; k++) part[k] = c3_chunk(v, n, k * C3_CHUNK);
     for (int g = 0; g < C3_GROUPS; g++) {
         int64_t lo = (int64_t)g * K / C3_GROUPS, hi = (int64_t)(g + 1) * K / C3_GROUPS;
@@ -444,6 +468,7 @@ static void assemble(orc_state *S, const double *x)
 {
     const orc_graph *G = S->G;
     double eps2 = S->eps * S->eps;
+    OMP_FOR
     for (int64_t u = 0; u < G->n; u++) {
         double acc = 0.0;
         for (int64_t e = G->adj_ptr[u]; e < G->adj_ptr[u + 1]; e++) {
@@ -466,6 +491,7 @@ static void assemble(orc_state *S, const double *x)
 static void matvec(const orc_state *S, const double *p, double *q)
 {
     const orc_graph *G = S->G;
+    OMP_FOR
     for (int64_t u = 0; u < G->n; u++) {
         double acc = 0.0;
         for (int64_t e = G->adj_ptr[u]; e < G->adj_ptr[u + 1]; e++)
@@ -476,6 +502,7 @@ static void matvec(const orc_state *S, const double *p, double *q)
 
 static double dot_c3(orc_state *S, const double *a, const double *b)
 {
+    OMP_FOR
     for (int64_t u = 0; u < S->G->n; u++) S->tmp[u] = a[u] * b[u];
     return orc_c3_sum(S->tmp, S->G->n);
 }
@@ -492,12 +519,16 @@ static int pcg(orc_state *S, orc_report *rep)
     /* r = b - A x0 */
     matvec(S, x, q);
     const double *b = S->bvec ? S->bvec : S->gs;
+    OMP_FOR
     for (int64_t u = 0; u < n; u++) r[u] = b[u] - q[u];
+    OMP_FOR
     for (int64_t u = 0; u < n; u++) z[u] = r[u] * S->Dinv[u];
+    OMP_FOR
     for (int64_t u = 0; u < n; u++) p[u] = z[u];
     double rho = dot_c3(S, r, z);
     double ref2;
     if (S->cg_norm == 0) {
+        OMP_FOR
         for (int64_t u = 0; u < n; u++) { double mb = b[u] * S->Dinv[u]; S->tmp[u] = mb * mb; }
         ref2 = orc_c3_sum(S->tmp, n);
     } else {
@@ -519,13 +550,17 @@ static int pcg(orc_state *S, orc_report *rep)
         double pi = dot_c3(S, p, q);
         if (!(pi > 0.0) || isinf(pi)) return ORC_ERR_CG_BREAKDOWN;
         double alpha = rho / pi;
+        OMP_FOR
         for (int64_t u = 0; u < n; u++) x[u] = x[u] + alpha * p[u];
+        OMP_FOR
         for (int64_t u = 0; u < n; u++) r[u] = r[u] - alpha * q[u];
+        OMP_FOR
         for (int64_t u = 0; u < n; u++) z[u] = r[u] * S->Dinv[u];
         double rho1 = dot_c3(S, r, z);
         res2 = S->cg_norm == 0 ? dot_c3(S, z, z) : dot_c3(S, r, r);
         res = sqrt(res2);
         double beta = rho1 / rho;
+        OMP_FOR
         for (int64_t u = 0; u < n; u++) p[u] = z[u] + beta * p[u];
         rho = rho1;
         k++;
@@ -557,11 +592,14 @@ static int pcg_cgcg(orc_state *S, orc_report *rep)
     double *x = S->x, *r = S->r, *z = S->z, *p = S->p, *q = S->q, *w = S->w, *sv = S->sv;
     matvec(S, x, q);
     const double *b = S->bvec ? S->bvec : S->gs;
+    OMP_FOR
     for (int64_t u = 0; u < n; u++) r[u] = b[u] - q[u];
+    OMP_FOR
     for (int64_t u = 0; u < n; u++) z[u] = r[u] * S->Dinv[u];
     double rho = dot_c3(S, r, z);
     double ref2;
     if (S->cg_norm == 0) {
+        OMP_FOR
         for (int64_t u = 0; u < n; u++) { double mb = b[u] * S->Dinv[u]; S->tmp[u] = mb * mb; }
         ref2 = orc_c3_sum(S->tmp, n);
     } else {
@@ -585,10 +623,15 @@ static int pcg_cgcg(orc_state *S, orc_report *rep)
     }
     for (;;) {
         if (res <= S->cg_rtol * ref || k == S->cg_max_iter) break;
+        OMP_FOR
         for (int64_t u = 0; u < n; u++) p[u] = k == 0 ? z[u] : z[u] + beta * p[u];
+        OMP_FOR
         for (int64_t u = 0; u < n; u++) sv[u] = k == 0 ? w[u] : w[u] + beta * sv[u];
+        OMP_FOR
         for (int64_t u = 0; u < n; u++) x[u] = x[u] + alpha * p[u];
+        OMP_FOR
         for (int64_t u = 0; u < n; u++) r[u] = r[u] - alpha * sv[u];
+        OMP_FOR
         for (int64_t u = 0; u < n; u++) z[u] = r[u] * S->Dinv[u];
         matvec(S, z, w);
         double gamma = dot_c3(S, r, z);
@@ -626,6 +669,7 @@ static void diagnostics(orc_state *S, orc_report *rep)
     double eps2 = S->eps * S->eps;
     /* Eq. 9: S_eps = sum over edges with c > 0 of w_e; node u
      * owns its higher-id n-links (ascending) then its s- and t-links. */
+    OMP_FOR
     for (int64_t u = 0; u < n; u++) {
         double acc = 0.0;
         for (int64_t e = G->adj_ptr[u]; e < G->adj_ptr[u + 1]; e++) {
@@ -640,6 +684,7 @@ static void diagnostics(orc_state *S, orc_report *rep)
     }
     rep->S_eps = orc_c3_sum(S->tmp, n);
     /* Prop. 3: flow value x^T L^(l) x = sum_e g_e d_e^2 */
+    OMP_FOR
     for (int64_t u = 0; u < n; u++) {
         double acc = 0.0;
         for (int64_t e = G->adj_ptr[u]; e < G->adj_ptr[u + 1]; e++) {
@@ -654,11 +699,13 @@ static void diagnostics(orc_state *S, orc_report *rep)
         S->tmp[u] = acc;
     }
     rep->flow_value = orc_c3_sum(S->tmp, n);
+    OMP_FOR
     for (int64_t u = 0; u < n; u++) S->tmp[u] = S->gs[u] * (1.0 - x[u]);
     rep->current_s = orc_c3_sum(S->tmp, n);
     /* true residual in the stopping norm */
     double *q = S->q;
     matvec(S, x, q);
+    OMP_FOR
     for (int64_t u = 0; u < n; u++) {
         double rr = S->gs[u] - q[u];
         double v = S->cg_norm == 0 ? rr * S->Dinv[u] : rr;
@@ -973,6 +1020,9 @@ int orc_kmeans2(const orc_state *S, const double *x, double *out4, int32_t *roun
     }
     if (r > 100) r = 100;
     out4[0] = c0; out4[1] = c1; out4[2] = c0 + 0.05; out4[3] = c1 - 0.05;
+    /* A26': crossing thresholds (centres less than 0.1 apart) fall back to
+     * gamma = (c0, c1) (the degenerate-threshold reading of SPEC S:L404). */
+    if (!(out4[2] < out4[3])) { out4[2] = c0; out4[3] = c1; }
     *rounds_out = r;
     free(v0); free(v1);
     return ORC_OK;
@@ -1139,6 +1189,17 @@ int orc_two_level(const orc_state *S, const double *x, uint8_t *side, double *cu
     uint8_t *src = (uint8_t *)malloc(N1), *in = (uint8_t *)malloc(N1);
     if (!cls || !cid || !cptr || !ccol || !ccap || !cqs || !cqt || !src || !in) { rc = ORC_ERR_OOM; goto out; }
     int64_t nc;
+    if (!(dinfo[2] < dinfo[3])) {
+        /* A26': still degenerate (c0 >= c1; Lloyd from (0.1, 0.9) keeps
+         * c0 < c1, so only a NaN-free rounding tie reaches this): the sweep
+         * cut of x. */
+        int64_t k;
+        uint64_t pk[2];
+        rc = orc_sweep(S, x, side, NULL, &k, cut_out, F_out, pk);
+        iinfo[0] = rounds; iinfo[1] = iinfo[2] = iinfo[3] = iinfo[4] = 0;
+        flow[0] = flow[1] = 0;
+        goto out;
+    }
     orc_coarsen(S, x, dinfo[2], dinfo[3], cls, cid, &nc, cptr, ccol, ccap, cqs, cqt, cqst, F_out);
     rc = orc_maxflow_coarse(nc, cptr, ccol, ccap, cqs, cqt, cqst, src, flow);
     if (rc) goto out;

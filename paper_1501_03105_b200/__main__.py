@@ -38,14 +38,15 @@ def load_graph(args):
     if root not in sys.path:
         sys.path.insert(0, root)
     from synthetic import generators as gen
-    make = {1: gen.config1, 2: gen.config2, 3: gen.config3, 4: gen.config4, 5: gen.config2}[args.config]
+    make = {1: gen.config1, 2: gen.config2, 3: gen.config3, 4: gen.config4}[args.config]
     return make(), f"BASELINE config {args.config}"
 
 
 def main(argv=None):
     ap = argparse.ArgumentParser(prog="python -m paper_1501_03105_b200", description=__doc__.split("\n\n")[0])
     src = ap.add_mutually_exclusive_group(required=True)
-    src.add_argument("--config", type=int, choices=[1, 2, 3, 4, 5])
+    src.add_argument("--config", type=int, choices=[1, 2, 3, 4],
+                     help="BASELINE configs 1-4 (config 5 is a warm-started sequence: tools/bench_configs.py)")
     src.add_argument("--graph", help=".npz graph file")
     ap.add_argument("--T", type=int, default=50)
     ap.add_argument("--eps", type=float, default=1e-6)
@@ -78,6 +79,10 @@ def main(argv=None):
                      record_trace=1 if args.trace else 0,
                      cg_variant=I.IRLS_CG_CG if args.cg_variant == "cg" else I.IRLS_CG_HS)
     if args.virtual_ranks:
+        unsupported = [f for f, on in (("--lambda2", args.lambda2), ("--exact", args.exact), ("--trace", args.trace))
+                       if on]
+        if unsupported:
+            ap.error(f"--virtual-ranks does not support {', '.join(unsupported)}")
         opts.p2p = 1 if args.p2p else 0
         t0 = time.perf_counter()
         g = I.VGroup(spec, args.virtual_ranks, opts)
@@ -86,11 +91,14 @@ def main(argv=None):
         t0 = time.perf_counter()
         reps, iters = g.irls_vgroup_solve(I.IRLS_FROM_SCRATCH)
         out.update({"solve_s": time.perf_counter() - t0, "cg_iters": iters})
-        side, _, k, cut = g.irls_vgroup_sweep_cut()
-        out["sweep"] = {"cut": cut, "k": k}
+        side = None
+        if args.rounding in ("sweep", "both"):
+            side, _, k, cut = g.irls_vgroup_sweep_cut()
+            out["sweep"] = {"cut": cut, "k": k}
         if args.rounding in ("two_level", "both"):
             side2, rep = g.irls_vgroup_two_level_cut()
             out["two_level"] = {"cut": rep["cut_value"], "coarse_nodes": rep["nc"]}
+            side = side if side is not None else side2
         if args.side:
             np.save(args.side, side)
         g.close()

@@ -938,20 +938,36 @@ extern "C" irls_status irls_set_terminal_weights(irls_ctx *c, const double *cs, 
     }
     // n-link part of F: recomputed from the device copies
     if (c->kind == 0) {
+        // Validate the new weights in scratch buffers: the context's cs/ct
+        // (and F) change only once the weights are accepted, so a rejected
+        // call (SINGULAR is not poisoning) leaves the previous problem intact.
         unsigned long long vo[6];
-        CK(cudaMemcpyAsync(c->cs, cs, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
-        CK(cudaMemcpyAsync(c->ct, ct, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
-        if (validate_stencil(c->nx, c->ny, c->nz, c->cx, c->cy, c->cz, c->cs, c->ct, vo, c->stream))
+        double *scs = nullptr, *sct = nullptr;
+        CK(cudaMallocAsync((void **)&scs, sizeof(double) * std::max<int64_t>(n, 1), c->stream));
+        CK(cudaMallocAsync((void **)&sct, sizeof(double) * std::max<int64_t>(n, 1), c->stream));
+        auto release = [&]() { cudaFreeAsync(scs, c->stream); cudaFreeAsync(sct, c->stream); };
+        CK(cudaMemcpyAsync(scs, cs, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(sct, ct, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+        if (validate_stencil(c->nx, c->ny, c->nz, c->cx, c->cy, c->cz, scs, sct, vo, c->stream)) {
+            release();
             return fail(c, IRLS_ERR_CUDA, "validate");
+        }
         if (vo[1] != 0 || vo[2] == 0) {
             // zero n-links present: full check on the host copy
             std::vector<double> hx(n), hy(n), hz(n);
             memcpy_sync(c, hx.data(), c->cx, sizeof(double) * n, cudaMemcpyDeviceToHost);
             memcpy_sync(c, hy.data(), c->cy, sizeof(double) * n, cudaMemcpyDeviceToHost);
             memcpy_sync(c, hz.data(), c->cz, sizeof(double) * n, cudaMemcpyDeviceToHost);
-            if (!grid_nonsingular(c->nx, c->ny, c->nz, hx.data(), hy.data(), hz.data(), cs, ct))
+            if (!grid_nonsingular(c->nx, c->ny, c->nz, hx.data(), hy.data(), hz.data(), cs, ct)) {
+                release();
+                CK(cudaStreamSynchronize(c->stream));
                 return fail(c, IRLS_ERR_SINGULAR, "terminal weights make L~ singular");
+            }
         }
+        CK(cudaMemcpyAsync(c->cs, scs, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->ct, sct, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+        release();
+        CK(cudaStreamSynchronize(c->stream));
         double m;
         memcpy(&m, &vo[4], sizeof(double));
         c->F = compute_F(m, (int64_t)vo[3]);

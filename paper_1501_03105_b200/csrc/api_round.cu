@@ -276,6 +276,21 @@ irls_status two_level_rank0(irls_ctx *c, const double *xfull, uint8_t *side, irl
     r->gamma0 = exact ? -INFINITY : h.c0 + 0.05;
     r->gamma1 = exact ? INFINITY : h.c1 - 0.05;
     r->kmeans_rounds = h.rounds;
+    if (!exact && !(r->gamma0 < r->gamma1)) {  // A26': crossing thresholds -> (c0, c1)
+        r->gamma0 = h.c0;
+        r->gamma1 = h.c1;
+    }
+    if (!exact && !(r->gamma0 < r->gamma1)) {
+        // A26': still degenerate (c0 >= c1): the sweep cut of x
+        int64_t k = 0;
+        double cut = 0.0;
+        s = sweep_rank0(c, xfull, side, nullptr, &k, &cut);
+        if (s) return s;
+        r->cut_value = cut;
+        r->certified = 1;
+        r->ms_total = (float)std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+        return IRLS_OK;
+    }
     // 2-3. classify, coarse ids / offsets, G_c
     const int64_t nt = tl_ntiles(n);
     int32_t last[4] = {0, 0, 0, 0};

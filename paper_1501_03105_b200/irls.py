@@ -198,6 +198,14 @@ def _f64(a):
     return np.ascontiguousarray(a, dtype=np.float64)
 
 
+def _f64_n(a, n, what):
+    """A host float64 array of exactly n entries (the C side reads n)."""
+    a = _f64(a)
+    if a.ndim != 1 or a.shape[0] != n:
+        raise ValueError(f"{what}: expected {n} float64 values, got shape {a.shape}")
+    return a
+
+
 def options(**kw) -> irls_options:
     o = irls_options()
     lib().irls_options_default(C.byref(o))
@@ -429,7 +437,7 @@ class MinCut:
         return s
 
     def irls_set_terminal_weights(self, cs, ct):
-        a, b = _f64(cs), _f64(ct)
+        a, b = _f64_n(cs, self.n, "cs"), _f64_n(ct, self.n, "ct")
         self._check(lib().irls_set_terminal_weights(self.h, _ptr(a), _ptr(b)), "irls_set_terminal_weights")
 
     def irls_get_potentials(self):
@@ -438,7 +446,7 @@ class MinCut:
         return x[: self.n]
 
     def irls_set_potentials(self, x):
-        a = _f64(x)
+        a = _f64_n(x, self.n, "x")
         self._check(lib().irls_set_potentials(self.h, _ptr(a)), "irls_set_potentials")
 
     def irls_get_stats(self) -> dict:
@@ -534,7 +542,7 @@ class VGroup:
         return x
 
     def irls_vgroup_set_terminal_weights(self, cs, ct):
-        a, b = _f64(cs), _f64(ct)
+        a, b = _f64_n(cs, self.n, "cs"), _f64_n(ct, self.n, "ct")
         rc = lib().irls_vgroup_set_terminal_weights(self.h, _ptr(a), _ptr(b))
         if rc:
             raise IrlsError(rc, "irls_vgroup_set_terminal_weights")

@@ -99,6 +99,33 @@ def test_csr_terminal_update_singular(irls):
     m.irls_set_terminal_weights(cs * 2.0, ct * 3.0)  # still anchored: accepted
 
 
+def test_stencil_terminal_update_singular_leaves_context_intact(irls):
+    """A8 at irls_set_terminal_weights on a grid: a rejected
+    update (IRLS_ERR_SINGULAR) must not reach the device.  The next
+    IRLS_CONTINUE solve runs on the previous weights, bitwise as the oracle
+    continuing without the update."""
+    spec = gen.zero_nlink_grid(8, 8, 1, seed=4)   # every pixel its own component (pin (iii))
+    T = 3
+    m = irls.MinCut.from_spec(spec, irls.options(T=T))
+    m.irls_solve(irls.IRLS_FROM_SCRATCH, T=T)
+    S = oracle.Solver(oracle.Graph(spec), T=T)
+    S.run(record=False)
+    bad_cs, bad_ct = spec["cs"].copy(), spec["ct"].copy()
+    bad_cs[5] = 0.0
+    bad_ct[5] = 0.0                                  # pixel 5 loses both terminal edges: singular
+    with pytest.raises(irls.IrlsError) as e:
+        m.irls_set_terminal_weights(bad_cs, bad_ct)
+    assert e.value.code == 5
+    m.irls_solve(irls.IRLS_CONTINUE, T=T)
+    for _ in range(T):
+        S.step()
+    assert np.array_equal(m.irls_get_potentials(), S.x())
+    side, _, k, cut = m.irls_sweep_cut()
+    sw = S.sweep()
+    assert k == sw.k and cut == sw.cut_value and np.array_equal(side, sw.side)
+    m.close()
+
+
 def test_solve_T_must_match_options(irls):
     """irls_solve runs irls_options.T steps; the binding sizes the report
     buffer from the context and refuses a different T (a smaller one used

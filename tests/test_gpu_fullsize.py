@@ -2,16 +2,26 @@
 and tools/bench_configs.py time (graph loop, T=50, rtol 1e-3 preconditioned,
 cap 50, warm start):
 
-- config 2 (128^3): every x^(l), l = 0..50, and the sweep — bitwise;
-- config 3 (road-like CSR, 23.7M nodes): final x^(50), per-step iteration
-  counts and the sweep — bitwise;
-- config 4 (512x512x256, 67M nodes): x^(0) (the init solve the oracle finishes
-  in minutes) and the sweep of x^(0) — bitwise; the full 50-step trajectory is
-  checked by the invariants that hold at any size (box, sweep cut equals the
-  cut of the returned set), and — with IRLS_FULL_C4=1, ~7 min of oracle time —
-  bitwise: every step's iterations and residual, x^(50) and the sweep
-  (profiles/r01_config4_full_parity.txt).
+- config 2 (128^3): every x^(l), l = 0..50, and the sweep — bitwise against
+  the live oracle, step by step;
+- configs 3, 4 and 5 against golden digests written by the oracle
+  (tools/make_golden.py, which imports only oracle/ and synthetic/; files in
+  tests/golden/*_trajectory.json), so the driver's run does not pay the
+  oracle's minutes of host time:
+  * config 3 (road-like CSR, 23.7M nodes) and config 4 (512x512x256, 67M
+    nodes, the bench workload): through irls_solve (the bench's call) every
+    report's iteration count, converged flag, relative residual and
+    reference norm, x^(50) and the sweep (k, cut value, side[], order[]);
+    and step by step (irls_init / irls_step with record_trace) every x^(l)
+    and every diagnostic of every report;
+  * config 5 (config 2 + 10 cumulative terminal-weight problems, A19): per
+    problem every report, x^(T) and the sweep.
+Floats compare as exact bit patterns (hex), x^(l) by SHA-256 of its bytes.
 """
+import hashlib
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -19,6 +29,10 @@ import oracle
 from synthetic import generators as gen
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+FIELDS = ("cg_iters", "converged", "rel_res", "ref")
+TRACE_FIELDS = FIELDS + ("true_rel_res", "S_eps", "flow_value", "current_s", "x_min", "x_max")
 
 
 @pytest.fixture(scope="module")
@@ -33,6 +47,32 @@ def irls():
 
 def _bitwise(a, b):
     return np.array_equal(np.asarray(a).view(np.uint64), np.asarray(b).view(np.uint64))
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def _golden(name):
+    with open(os.path.join(GOLD, f"{name}_trajectory.json")) as f:
+        return json.load(f)
+
+
+def _rep_equal(got, gold, fields, where):
+    for k in fields:
+        g = gold[k]
+        v = got[k]
+        exp = float.fromhex(g) if isinstance(g, str) else g
+        assert (float(v).hex() if isinstance(g, str) else int(v)) == (g if isinstance(g, str) else int(g)), \
+            f"{where}: {k} = {v!r}, oracle {exp!r}"
+
+
+def _sweep_equal(m, gold, where):
+    side, order, k, cut = m.irls_sweep_cut(order=True)
+    assert k == gold["k"], where
+    assert float(cut).hex() == gold["cut_value"], where
+    assert _sha(side.astype(np.uint8)) == gold["side_sha256"], where
+    assert _sha(order.astype(np.int32)) == gold["order_sha256"], where
 
 
 def test_config2_full_trajectory(irls):
@@ -50,58 +90,79 @@ def test_config2_full_trajectory(irls):
     assert np.array_equal(side, sw.side) and np.array_equal(order.astype(np.int64), sw.order)
 
 
-def test_config3_full_csr(irls):
-    spec = gen.config3()
+def _golden_solve(irls, name, spec):
+    gold = _golden(name)
+    assert gold["policy"]["T"] == 50 and gold["policy"]["cg_rtol"] == 1e-3
     m = irls.MinCut.from_spec(spec, irls.options(T=50))
+    assert m.n == gold["n"]
     reps, total = m.irls_solve(irls.IRLS_FROM_SCRATCH, T=50)
-    S = oracle.Solver(oracle.Graph(spec), T=50)
-    _, oreps = S.run(record=False)
-    assert [r["cg_iters"] for r in reps] == [r["cg_iters"] for r in oreps]
-    assert _bitwise(m.irls_get_potentials(), S.x())
-    side, _, k, cut = m.irls_sweep_cut()
-    sw = S.sweep()
-    assert k == sw.k and cut == sw.cut_value and np.array_equal(side, sw.side)
+    for l, (r, g) in enumerate(zip(reps, gold["solves"])):
+        _rep_equal(r, g["report"], FIELDS, f"{name} solve {l}")
+    assert total == gold["total_cg_iters"]
+    assert _sha(m.irls_get_potentials()) == gold["solves"][-1]["x_sha256"]
+    _sweep_equal(m, gold["sweep"], f"{name} sweep")
+    m.close()
 
 
-def test_config4_init_and_invariants(irls):
-    spec = gen.config4()
-    m = irls.MinCut.from_spec(spec, irls.options(T=50))
-    r0 = m.irls_init()
-    S = oracle.Solver(oracle.Graph(spec), T=0)
-    ro = S.init()
-    assert r0["cg_iters"] == ro["cg_iters"]
-    assert _bitwise(m.irls_get_potentials(), S.x())
-    side, _, k, cut = m.irls_sweep_cut()
-    sw = S.sweep()
-    assert k == sw.k and cut == sw.cut_value and np.array_equal(side, sw.side)
-    del S
-    # full run: invariants at full size
-    reps, total = m.irls_solve(irls.IRLS_FROM_SCRATCH, T=50)
+def _golden_steps(irls, name, spec):
+    gold = _golden(name)
+    m = irls.MinCut.from_spec(spec, irls.options(T=50, record_trace=1))
+    for l, g in enumerate(gold["solves"]):
+        r = m.irls_init() if l == 0 else m.irls_step()
+        _rep_equal(r, g["report"], TRACE_FIELDS, f"{name} step {l}")
+        assert _sha(m.irls_get_potentials()) == g["x_sha256"], f"{name}: x^({l})"
+    m.close()
+
+
+def test_config3_golden_solve(irls):
+    _golden_solve(irls, "config3", gen.config3())
+
+
+def test_config3_golden_every_step(irls):
+    _golden_steps(irls, "config3", gen.config3())
+
+
+def test_config4_golden_solve(irls):
+    """The bench workload: irls_solve as bench.py calls it, 51 solves."""
+    _golden_solve(irls, "config4", gen.config4())
+
+
+def test_config4_golden_every_step(irls):
+    _golden_steps(irls, "config4", gen.config4())
+
+
+def test_config4_invariants(irls):
+    """Properties that hold at any size (A21 box up to the loose tolerance;
+    the sweep's set is {s} + k non-terminals)."""
+    m = irls.MinCut.from_spec(gen.config4(), irls.options(T=50))
+    m.irls_solve(irls.IRLS_FROM_SCRATCH, T=50)
     x = m.irls_get_potentials()
-    assert x.min() > -1e-2 and x.max() < 1 + 1e-2  # box up to the loose CG tolerance (A21)
+    assert x.min() > -1e-2 and x.max() < 1 + 1e-2
     side, _, k, cut = m.irls_sweep_cut()
     assert side[-2] == 1 and side[-1] == 0 and int(side[:-2].sum()) == k
+    m.close()
 
 
-@pytest.mark.skipif(__import__("os").environ.get("IRLS_FULL_C4") != "1",
-                    reason="config 4's full oracle trajectory takes ~7 min of host time; IRLS_FULL_C4=1 runs it "
-                           "(result recorded in profiles/r01_config4_full_parity.txt)")
-def test_config4_full_trajectory(irls):
-    """Config 4 at full size through the bench's configuration: every step's
-    iteration count and relative residual, x^(50) and the sweep — bitwise
-    against the oracle's 51 solves (~7 min on one host core)."""
-    import time
-    spec = gen.config4()
+def test_config5_golden_sequence(irls):
+    """BASELINE configs[4] at full size: config 2, then 10 problems with
+    cumulative U[0.99,1.01] t-link factors, each continued from x^(T) (A19)."""
+    gold = _golden("config5")
+    spec = gen.config2()
     m = irls.MinCut.from_spec(spec, irls.options(T=50))
-    reps, total = m.irls_solve(irls.IRLS_FROM_SCRATCH, T=50)
-    t0 = time.perf_counter()
-    S = oracle.Solver(oracle.Graph(spec), T=50)
-    _, oreps = S.run(record=False)
-    dt = time.perf_counter() - t0
-    assert [r["cg_iters"] for r in reps] == [r["cg_iters"] for r in oreps]
-    assert [r["rel_res"] for r in reps] == [r["rel_res"] for r in oreps]
-    assert _bitwise(m.irls_get_potentials(), S.x())
-    side, _, k, cut = m.irls_sweep_cut()
-    sw = S.sweep()
-    assert k == sw.k and cut == sw.cut_value and np.array_equal(side, sw.side)
-    print(f"config 4 full trajectory bitwise: {total} CG iterations, k = {k}, cut = {cut!r}, oracle {dt:.0f} s")
+    cs, ct = spec["cs"].copy(), spec["ct"].copy()
+    factors = gen.config5_factors(cs.shape[0], n_problems=10, seed=4)
+    for p in gold["problems"]:
+        i = p["problem"]
+        if i == 0:
+            reps, _ = m.irls_solve(irls.IRLS_FROM_SCRATCH, T=50)
+        else:
+            fs, ft = factors[i - 1]
+            cs, ct = cs * fs, ct * ft
+            m.irls_set_terminal_weights(cs, ct)
+            reps, _ = m.irls_solve(irls.IRLS_CONTINUE, T=50)
+        assert len(reps) == len(p["reports"])
+        for l, (r, g) in enumerate(zip(reps, p["reports"])):
+            _rep_equal(r, g, FIELDS, f"config5 problem {i} step {l}")
+        assert _sha(m.irls_get_potentials()) == p["x_sha256"], f"config5 problem {i}"
+        _sweep_equal(m, p["sweep"], f"config5 problem {i} sweep")
+    m.close()

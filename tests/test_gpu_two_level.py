@@ -139,6 +139,20 @@ def test_vgroup_equals_one_rank(irls):
         assert rw["nc"] == r1["nc"] and rw["c0"] == r1["c0"] and rw["c1"] == r1["c1"]
 
 
+def test_crossing_thresholds(irls):
+    """A26': centres < 0.1 apart -> thresholds (c0, c1), bitwise as
+    the oracle (K-means, classes, coarse graph, set, cut)."""
+    spec = gen.random_small_graph(600, 900, seed=77)
+    m = irls.MinCut.from_spec(spec, irls.options(T=2))
+    S = oracle.Solver(oracle.Graph(spec), T=2)
+    rng = np.random.default_rng(5)
+    x = np.where(rng.random(m.n) < 0.5, 0.48, 0.52) + rng.uniform(-0.004, 0.004, m.n)
+    m.irls_set_potentials(x)
+    S.set_x(x)
+    side, rep, r = check_two_level(irls, m, S)
+    assert (rep["gamma0"], rep["gamma1"]) == (rep["c0"], rep["c1"])
+
+
 def test_errors_and_repeat(irls):
     spec = gen.blob_grid(16, 16, 4, seed=2, sigma=(2.0, 5.0))
     m = irls.MinCut.from_spec(spec, irls.options(T=4))

@@ -54,6 +54,30 @@ def test_kmeans_spec_hand_round():
     assert r == 2
 
 
+def test_crossing_thresholds_fall_back_to_centres():
+    """A26' (S:L404): centres less than 0.1 apart make c0 + 0.05 >= c1 - 0.05;
+    the thresholds fall back to (c0, c1).  Hand example: 200 nodes at 0.48 and
+    200 at 0.52 plus x_t = 0, x_s = 1.  Lloyd from (0.1, 0.9): midpoint 0.5
+    splits {0.48 x200, 0} | {0.52 x200, 1}, giving c0 = 96/201, c1 = 105/201
+    (0.0448 apart), after which the assignment is stable."""
+    n_mid = 400
+    spec = line_graph(n_mid, seed=3)
+    x = np.where(np.arange(n_mid) % 2 == 0, 0.48, 0.52)
+    S = solver(spec)
+    (c0, c1, g0, g1), r = S.kmeans2(x)
+    assert c0 == pytest.approx(96.0 / 201.0, rel=1e-14) and c1 == pytest.approx(105.0 / 201.0, rel=1e-14)
+    assert (g0, g1) == (c0, c1)
+    tl = S.two_level(x)
+    assert (tl.gamma0, tl.gamma1) == (c0, c1)
+    # 0.48 > c0 and 0.52 < c1: no node is contracted, G_c = G and the rounding is
+    # the exact minimum cut of the path: its lightest edge
+    assert tl.nc == n_mid and tl.n0 == 0 and tl.n1 == 0
+    n, s_id, t_id, E = H.edge_list(spec)
+    w_min = min(c for _, _, c in E)
+    assert tl.cut_value == pytest.approx(w_min, rel=1e-15)
+    assert H.cut_value(E, tl.side) == pytest.approx(w_min, rel=1e-15)
+
+
 @pytest.mark.parametrize("seed", range(5))
 def test_kmeans_matches_sklearn_lloyd(seed):
     """Lloyd's fixed point from the same initial centres equals scikit-learn's
