@@ -17,7 +17,8 @@ e2e    = the same metric through the C ABI with pinned HOST buffers: create
          destroy inside the timed region;
 roofline = the dominant kernel (K3: fused p-update + SpMV + p.q), timed with
          CUDA events on the library's stream;
-cpu_baseline = the float64 CPU oracle on a bounded sample of the workload.
+cpu_baseline = the float64 CPU oracle (OpenMP, every host core) on the whole
+         workload graph: x^(0) + 3 IRLS steps + the sweep.
 
 `--impl reference` times the oracle (the reference arm of this tier).
 """
@@ -116,42 +117,41 @@ class ClockSampler:
 # oracle (cpu_baseline and the reference arm)
 # ---------------------------------------------------------------------------
 
-def oracle_sample(spec, planes=8, T=3):
-    """The float64 oracle on a bounded sample of the workload: the first
-    `planes` z-planes of the grid, init + T IRLS steps (cap 50, rtol 1e-3).
-    Returns (GEdge/s, seconds, description)."""
+def oracle_sample(spec, planes=None, T=3, sweep=True):
+    """The float64 oracle (OpenMP over C3 chunks and node loops, every host
+    core; bitwise thread-invariant) on the workload: the whole graph
+    (planes=None) or its first `planes` z-planes, init + T IRLS steps (cap 50,
+    rtol 1e-3) + the sweep.  Returns (GEdge/s, seconds, threads, description)."""
     import oracle
-    if spec["kind"] == "csr":  # config 3: the same generator at 1000^2 (a bounded instance of the recipe)
-        from synthetic import generators as gen
-        sub = gen.road_graph(1000, seed=2, knn=200)
-        G = oracle.Graph(sub)
-        S = oracle.Solver(G, T=T)
-        links = G.nnz // 2
-        t0 = time.perf_counter()
-        _, reps = S.run(record=False)
-        S.sweep()
-        dt = time.perf_counter() - t0
-        iters = sum(r["cg_iters"] for r in reps)
-        desc = (f"oracle (plain C, 1 thread) on the config-3 recipe at 1000^2 ({G.n} nodes, {links} n-links), "
-                f"init + {T} IRLS steps + sweep: {iters} CG iterations in {dt:.1f} s")
-        return links * iters / dt / 1e9, dt, desc
-    nx, ny = spec["nx"], spec["ny"]
-    n = nx * ny * planes
-    sub = dict(spec)
-    sub["nz"] = planes
-    for k in ("cx", "cy", "cz", "cs", "ct"):
-        sub[k] = np.ascontiguousarray(spec[k][:n])
+    threads = oracle.set_num_threads(os.cpu_count() or 1)
+    if spec["kind"] == "csr":
+        sub, what = spec, "the whole workload"
+        if planes is not None:  # a bounded instance of the config-3 recipe
+            from synthetic import generators as gen
+            sub, what = gen.road_graph(1000, seed=2, knn=200), "the config-3 recipe at 1000^2"
+    elif planes is None:
+        sub, what = spec, "the whole workload"
+    else:
+        n = spec["nx"] * spec["ny"] * planes
+        sub = dict(spec)
+        sub["nz"] = planes
+        for k in ("cx", "cy", "cz", "cs", "ct"):
+            sub[k] = np.ascontiguousarray(spec[k][:n])
+        what = f"z-planes 0..{planes - 1} of the workload"
+    t0 = time.perf_counter()
     G = oracle.Graph(sub)
     S = oracle.Solver(G, T=T)
     links = G.nnz // 2
-    t0 = time.perf_counter()
+    t1 = time.perf_counter()
     _, reps = S.run(record=False)
-    S.sweep()
-    dt = time.perf_counter() - t0
+    if sweep:
+        S.sweep()
+    dt = time.perf_counter() - t1
     iters = sum(r["cg_iters"] for r in reps)
-    desc = (f"oracle (plain C, 1 thread) on z-planes 0..{planes - 1} of the workload "
-            f"({n} nodes, {links} n-links), init + {T} IRLS steps + sweep: {iters} CG iterations in {dt:.1f} s")
-    return links * iters / dt / 1e9, dt, desc
+    desc = (f"oracle (plain C, OpenMP, {threads} threads) on {what} ({G.n} nodes, {links} n-links): "
+            f"init + {T} IRLS steps{' + sweep' if sweep else ''}, {iters} CG iterations in {dt:.1f} s "
+            f"(graph build {t1 - t0:.1f} s untimed)")
+    return links * iters / dt / 1e9, dt, threads, desc
 
 
 def run_reference(args):
@@ -164,13 +164,12 @@ def run_reference(args):
     for _ in range(args.warmup if args.warmup < 1 else 1):
         oracle_sample(spec, planes=args.ref_planes, T=args.ref_T)
     vals, times = [], []
-    desc = ""
+    desc, cores = "", 1
     for _ in range(args.steps):
-        v, dt, desc = oracle_sample(spec, planes=args.ref_planes, T=args.ref_T)
+        v, dt, cores, desc = oracle_sample(spec, planes=args.ref_planes, T=args.ref_T)
         vals.append(v)
         times.append(dt)
     val = statistics.median(vals)
-    cores = 1
     line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(times), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -193,8 +192,10 @@ def main():
     ap.add_argument("--config", default="config4")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-planes", type=int, default=8)
+    ap.add_argument("--ref-planes", type=int, default=16,
+                    help="reference arm: z-planes of the workload per step (bounded so K steps end in minutes)")
     ap.add_argument("--ref-T", type=int, default=3)
+    ap.add_argument("--cpu-T", type=int, default=3, help="cpu_baseline: IRLS steps after x^(0) on the whole graph")
     ap.add_argument("--loop-mode", type=int, default=0)
     ap.add_argument("--no-two-level", action="store_true")
     ap.add_argument("--no-fixed-point-exit", action="store_true")
@@ -453,8 +454,8 @@ def main():
     # ---- cpu baseline (rank 0, N=1 only) -----------------------------------
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        v, dt, desc = oracle_sample(spec, planes=args.ref_planes, T=args.ref_T)
-        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc}
+        v, dt, threads, desc = oracle_sample(spec, planes=None, T=args.cpu_T)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -45,6 +45,16 @@ def irls():
     return I
 
 
+_SPECS = {}
+
+
+def _spec(name):
+    """Each full-size generator runs once per module (config 4 takes ~13 s)."""
+    if name not in _SPECS:
+        _SPECS[name] = getattr(gen, name)()
+    return _SPECS[name]
+
+
 def _bitwise(a, b):
     return np.array_equal(np.asarray(a).view(np.uint64), np.asarray(b).view(np.uint64))
 
@@ -76,7 +86,7 @@ def _sweep_equal(m, gold, where):
 
 
 def test_config2_full_trajectory(irls):
-    spec = gen.config2()
+    spec = _spec("config2")
     m = irls.MinCut.from_spec(spec, irls.options(T=50))
     S = oracle.Solver(oracle.Graph(spec), T=50)
     for l in range(51):
@@ -115,26 +125,26 @@ def _golden_steps(irls, name, spec):
 
 
 def test_config3_golden_solve(irls):
-    _golden_solve(irls, "config3", gen.config3())
+    _golden_solve(irls, "config3", _spec("config3"))
 
 
 def test_config3_golden_every_step(irls):
-    _golden_steps(irls, "config3", gen.config3())
+    _golden_steps(irls, "config3", _spec("config3"))
 
 
 def test_config4_golden_solve(irls):
     """The bench workload: irls_solve as bench.py calls it, 51 solves."""
-    _golden_solve(irls, "config4", gen.config4())
+    _golden_solve(irls, "config4", _spec("config4"))
 
 
 def test_config4_golden_every_step(irls):
-    _golden_steps(irls, "config4", gen.config4())
+    _golden_steps(irls, "config4", _spec("config4"))
 
 
 def test_config4_invariants(irls):
     """Properties that hold at any size (A21 box up to the loose tolerance;
     the sweep's set is {s} + k non-terminals)."""
-    m = irls.MinCut.from_spec(gen.config4(), irls.options(T=50))
+    m = irls.MinCut.from_spec(_spec("config4"), irls.options(T=50))
     m.irls_solve(irls.IRLS_FROM_SCRATCH, T=50)
     x = m.irls_get_potentials()
     assert x.min() > -1e-2 and x.max() < 1 + 1e-2
@@ -147,7 +157,7 @@ def test_config5_golden_sequence(irls):
     """BASELINE configs[4] at full size: config 2, then 10 problems with
     cumulative U[0.99,1.01] t-link factors, each continued from x^(T) (A19)."""
     gold = _golden("config5")
-    spec = gen.config2()
+    spec = _spec("config2")
     m = irls.MinCut.from_spec(spec, irls.options(T=50))
     cs, ct = spec["cs"].copy(), spec["ct"].copy()
     factors = gen.config5_factors(cs.shape[0], n_problems=10, seed=4)
