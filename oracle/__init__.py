@@ -33,7 +33,7 @@ _lib = None
 class Options(C.Structure):
     _fields_ = [("eps", C.c_double), ("T", C.c_int32), ("cg_rtol", C.c_double),
                 ("cg_max_iter", C.c_int32), ("cg_norm", C.c_int32), ("warm_start", C.c_int32),
-                ("cg_variant", C.c_int32)]
+                ("cg_variant", C.c_int32), ("block_size", C.c_int32)]
 
 
 class Report(C.Structure):
@@ -77,6 +77,10 @@ def lib():
         L.orc_set_terminal_weights.argtypes = [P, dp, dp]
         L.orc_assemble_export.argtypes = [P, P, dp, dp, dp, dp, dp]
         L.orc_irls_run.argtypes = [P, P, P]
+        L.orc_block_count.argtypes = [P]; L.orc_block_count.restype = C.c_int64
+        L.orc_block_env_size.argtypes = [P]; L.orc_block_env_size.restype = C.c_int64
+        L.orc_block_export.argtypes = [P, i64p, i64p, i64p, i64p]
+        L.orc_precond_export.argtypes = [P, P, dp, dp, dp, dp]
         L.orc_sweep.argtypes = [P, dp, u8p, P, C.POINTER(C.c_int64), C.POINTER(C.c_double),
                                 C.POINTER(C.c_int32), u64p]
         L.orc_cut_value.argtypes = [P, u8p]; L.orc_cut_value.restype = C.c_double
@@ -221,9 +225,10 @@ class Solver:
     """IRLS state over a Graph (Algorithm 1)."""
 
     def __init__(self, graph: Graph, eps=1e-6, T=50, cg_rtol=1e-3, cg_max_iter=50,
-                 cg_norm=0, warm_start=True, cg_variant=0):
+                 cg_norm=0, warm_start=True, cg_variant=0, block_size=0):
         self.graph = graph
-        self.opts = Options(eps, T, cg_rtol, cg_max_iter, cg_norm, int(bool(warm_start)), int(cg_variant))
+        self.opts = Options(eps, T, cg_rtol, cg_max_iter, cg_norm, int(bool(warm_start)), int(cg_variant),
+                            int(block_size))
         self.h = lib().orc_state_new(graph.h, C.byref(self.opts))
         if not self.h:
             raise MemoryError("orc_state_new")
@@ -239,6 +244,27 @@ class Solver:
 
     def step(self) -> dict:
         r = Report(); _check(lib().orc_step(self.h, C.byref(r)), "step"); return r.as_dict()
+
+    def blocks(self):
+        """A32 partition: (bptr[nblk+1], bnode[n], bfirst[n], boff[n+1])."""
+        L = lib()
+        nb, n = L.orc_block_count(self.h), self.n
+        bptr = np.zeros(nb + 1, dtype=np.int64); bnode = np.zeros(max(n, 1), dtype=np.int64)
+        bfirst = np.zeros(max(n, 1), dtype=np.int64); boff = np.zeros(n + 1, dtype=np.int64)
+        L.orc_block_export(self.h, bptr, bnode, bfirst, boff)
+        return bptr, bnode[:n], bfirst[:n], boff
+
+    def precond(self, r, x=None):
+        """Assemble at x (None: W = C), factor, and return (z = M^-1 r, L envelope, pivots)."""
+        L = lib()
+        n = self.n
+        r = np.ascontiguousarray(r, dtype=np.float64)
+        z = np.zeros(max(n, 1)); env = np.zeros(max(L.orc_block_env_size(self.h), 1)); Dd = np.zeros(max(n, 1))
+        xp = None
+        if x is not None:
+            x = np.ascontiguousarray(x, dtype=np.float64); xp = x.ctypes.data_as(C.c_void_p)
+        L.orc_precond_export(self.h, xp, r, z, env, Dd)
+        return z[:n], env, Dd[:n]
 
     def x(self) -> np.ndarray:
         out = np.zeros(self.n); lib().orc_get_x(self.h, out); return out

@@ -38,8 +38,8 @@
  * order, a chunk's C3 partial from its own 4096 elements), so the results
  * are bitwise independent of the thread count (pinned by
  * tests/test_oracle_threads.py).  Sums across elements happen only in the
- * fixed C3 tree. */
-#define OMP_FOR _Pragma("omp parallel for schedule(static)")
+ * fixed C3 tree; a block-Jacobi block (A32) is solved by one thread.  Loops
+ * run in parallel only above a size where threads pay for themselves. */
 
 int orc_set_num_threads(int n)
 {
@@ -356,7 +356,7 @@ double orc_c3_sum(const double *v, int64_t n)
     int64_t K = (n + C3_CHUNK - 1) / C3_CHUNK;
     double *part = (double *)malloc(sizeof(double) * (size_t)(K > 0 ? K : 1));
     double gs[C3_GROUPS];
-    OMP_FOR
+#pragma omp parallel for schedule(static) if((K) > 16)
     for (int64_t k = 0; k < K; k++) part[k] = c3_chunk(v, n, k * C3_CHUNK);
     for (int g = 0; g < C3_GROUPS; g++) {
         int64_t lo = (int64_t)g * K / C3_GROUPS, hi = (int64_t)(g + 1) * K / C3_GROUPS;
@@ -374,7 +374,7 @@ void orc_c3_group_sums(const double *v, int64_t n, double *out8)
 {
     int64_t K = (n + C3_CHUNK - 1) / C3_CHUNK;
     double *part = (double *)malloc(sizeof(double) * (size_t)(K > 0 ? K : 1));
-    OMP_FOR
+#pragma omp parallel for schedule(static) if((K) > 16)
     for (int64_t k = 0; k < K; k++) part[k] = c3_chunk(v, n, k * C3_CHUNK);
     for (int g = 0; g < C3_GROUPS; g++) {
         int64_t lo = (int64_t)g * K / C3_GROUPS, hi = (int64_t)(g + 1) * K / C3_GROUPS;
@@ -409,6 +409,16 @@ typedef struct {
     int32_t step;  /* number of solves done (0 = none) */
     double *cs, *ct; /* owned copy of terminal capacities (set_terminal_weights) */
     const double *bvec; /* right-hand side override (lambda2); NULL: b = gs (Eq. 7) */
+    /* block-Jacobi preconditioner (A32; block_size 0 = point Jacobi) */
+    int32_t block_size;
+    int64_t nblk;
+    int64_t *bptr;      /* nblk+1: block b holds positions bptr[b]..bptr[b+1]-1 */
+    int64_t *bnode;     /* n: reduced id at each position (block order) */
+    int64_t *bpos;      /* n: position of each reduced id */
+    int64_t *bfirst;    /* n: first column f_i of the row at each position (block-local index) */
+    int64_t *boff;      /* n+1: start of each row's envelope entries in bL */
+    double *bL, *bDd;   /* envelope of the unit lower factor; pivots (block order) */
+    double *by;         /* scratch (block order) */
 } orc_state;
 
 typedef struct {
@@ -419,6 +429,7 @@ typedef struct {
     int32_t cg_norm;      /* 0 = preconditioned (A9), 1 = unpreconditioned */
     int32_t warm_start;
     int32_t cg_variant;   /* 0 = Hestenes-Stiefel (O5), 1 = Chronopoulos-Gear (O5', A31) */
+    int32_t block_size;   /* 0 = point Jacobi M = diag(L~) (A12); B >= 1: block Jacobi (A32) */
 } orc_options;
 
 typedef struct {
@@ -437,7 +448,154 @@ void orc_state_free(orc_state *S)
     if (!S) return;
     free(S->g); free(S->gs); free(S->gt); free(S->D); free(S->Dinv);
     free(S->x); free(S->r); free(S->z); free(S->p); free(S->q); free(S->w); free(S->sv); free(S->tmp);
-    free(S->cs); free(S->ct); free(S);
+    free(S->cs); free(S->ct);
+    free(S->bptr); free(S->bnode); free(S->bpos); free(S->bfirst); free(S->boff); free(S->bL); free(S->bDd);
+    free(S->by); free(S);
+}
+
+/* ------------------------------------------------------------------------- */
+/* Block-Jacobi preconditioner ("block      */
+/* Jacobi" with "LU" blocks).  Reading A32 in DESIGN.md §2.           */
+/* ------------------------------------------------------------------------- */
+
+/* A32 partition.  For each C3 group g = 0..7 (ids [4096 floor(gK/8),
+ * 4096 floor((g+1)K/8)) clipped to n) and each id u of the group ascending:
+ * if u is unassigned it opens a new block; then the earliest node v of the
+ * block not yet expanded is expanded — its neighbours w (ascending id, c > 0)
+ * inside the group and unassigned are appended in that order — until the
+ * block holds B nodes or all its nodes are expanded.  Block order = append
+ * order.  Writes bptr[nblk+1], bnode[n]; returns nblk (-1 on OOM). */
+int64_t orc_block_partition(const orc_graph *G, int32_t B, int64_t *bptr, int64_t *bnode)
+{
+    int64_t n = G->n, K = (n + C3_CHUNK - 1) / C3_CHUNK, nb = 0, cnt = 0;
+    uint8_t *used = (uint8_t *)calloc((size_t)(n > 0 ? n : 1), 1);
+    if (!used) return -1;
+    for (int g = 0; g < C3_GROUPS; g++) {
+        int64_t lo = (int64_t)g * K / C3_GROUPS * C3_CHUNK, hi = (int64_t)(g + 1) * K / C3_GROUPS * C3_CHUNK;
+        if (lo > n) lo = n;
+        if (hi > n) hi = n;
+        for (int64_t u = lo; u < hi; u++) {
+            if (used[u]) continue;
+            int64_t start = cnt, head = cnt;
+            bptr[nb++] = start;
+            bnode[cnt++] = u;
+            used[u] = 1;
+            while (head < cnt && cnt - start < B) {
+                int64_t v = bnode[head++];
+                for (int64_t e = G->adj_ptr[v]; e < G->adj_ptr[v + 1] && cnt - start < B; e++) {
+                    int64_t w = G->adj_idx[e];
+                    if (w < lo || w >= hi || used[w]) continue;
+                    used[w] = 1;
+                    bnode[cnt++] = w;
+                }
+            }
+        }
+    }
+    bptr[nb] = cnt;
+    free(used);
+    return nb;
+}
+
+/* Envelope of each block row (A32): f_i = the smallest block position among
+ * position i and its in-block neighbours.  Row i of the unit lower factor
+ * lives in columns [f_i, i) (LDL^T fills only inside the envelope). */
+static int block_setup(orc_state *S)
+{
+    const orc_graph *G = S->G;
+    int64_t n = G->n, N1 = n > 0 ? n : 1;
+    S->bptr = (int64_t *)malloc(sizeof(int64_t) * (size_t)(N1 + 1));
+    S->bnode = (int64_t *)malloc(sizeof(int64_t) * (size_t)N1);
+    S->bpos = (int64_t *)malloc(sizeof(int64_t) * (size_t)N1);
+    S->bfirst = (int64_t *)malloc(sizeof(int64_t) * (size_t)N1);
+    S->boff = (int64_t *)malloc(sizeof(int64_t) * (size_t)(N1 + 1));
+    S->bDd = (double *)malloc(sizeof(double) * (size_t)N1);
+    S->by = (double *)malloc(sizeof(double) * (size_t)N1);
+    if (!S->bptr || !S->bnode || !S->bpos || !S->bfirst || !S->boff || !S->bDd || !S->by) return ORC_ERR_OOM;
+    S->nblk = orc_block_partition(G, S->block_size, S->bptr, S->bnode);
+    if (S->nblk < 0) return ORC_ERR_OOM;
+    for (int64_t i = 0; i < n; i++) S->bpos[S->bnode[i]] = i;
+    S->boff[0] = 0;
+    for (int64_t b = 0; b < S->nblk; b++)
+        for (int64_t i = S->bptr[b]; i < S->bptr[b + 1]; i++) {
+            int64_t u = S->bnode[i], f = i;
+            for (int64_t e = G->adj_ptr[u]; e < G->adj_ptr[u + 1]; e++) {
+                int64_t j = S->bpos[G->adj_idx[e]];
+                if (j >= S->bptr[b] && j < f) f = j;
+            }
+            S->bfirst[i] = f - S->bptr[b];
+            S->boff[i + 1] = S->boff[i] + (i - f);
+        }
+    S->bL = (double *)malloc(sizeof(double) * (size_t)(S->boff[n] > 0 ? S->boff[n] : 1));
+    return S->bL ? ORC_OK : ORC_ERR_OOM;
+}
+
+/* A32 factorisation of every block of L~ (after assemble): A_B = L~ restricted
+ * to the block in block order (A_ii = D_u, A_ij = -g_uv for an n-link inside
+ * the block, +0.0 otherwise); LDL^T by rows (Crout), every sum over k
+ * ascending:
+ *   L_ij = (A_ij - sum_k (L_ik * L_jk) * d_k) / d_j,  k in [max(f_i, f_j), j)
+ *   d_i  =  A_ii - sum_k (L_ik * L_ik) * d_k,         k in [f_i, i)
+ * (terms outside the envelope are exact zeros of the dense algorithm, which
+ * leave every sum bitwise unchanged — pinned against a dense factorisation). */
+static void block_factor(orc_state *S)
+{
+    const orc_graph *G = S->G;
+#pragma omp parallel for schedule(static) if((S->nblk) > 64)
+    for (int64_t b = 0; b < S->nblk; b++) {
+        int64_t p0 = S->bptr[b], p1 = S->bptr[b + 1];
+        for (int64_t i = p0; i < p1; i++) {
+            int64_t u = S->bnode[i], fi = S->bfirst[i];
+            double *Li = S->bL + S->boff[i] - fi;           /* Li[j], j in [fi, i - p0) */
+            for (int64_t j = fi; j < i - p0; j++) Li[j] = 0.0;
+            for (int64_t e = G->adj_ptr[u]; e < G->adj_ptr[u + 1]; e++) {
+                int64_t j = S->bpos[G->adj_idx[e]] - p0;
+                if (j >= fi && j < i - p0) Li[j] = -S->g[e];
+            }
+            for (int64_t j = fi; j < i - p0; j++) {
+                int64_t fj = S->bfirst[p0 + j];
+                const double *Lj = S->bL + S->boff[p0 + j] - fj;
+                double acc = Li[j];
+                for (int64_t k = fi > fj ? fi : fj; k < j; k++) acc = acc - (Li[k] * Lj[k]) * S->bDd[p0 + k];
+                Li[j] = acc / S->bDd[p0 + j];
+            }
+            double acc = S->D[u];
+            for (int64_t k = fi; k < i - p0; k++) acc = acc - (Li[k] * Li[k]) * S->bDd[p0 + k];
+            S->bDd[i] = acc;
+        }
+    }
+}
+
+/* z = M^-1 r.  Point Jacobi: z_u = r_u * Dinv_u (O5).  Block Jacobi (A32),
+ * per block: forward y_i = r_i - sum_{k in [f_i, i), ascending} L_ik * y_k;
+ * w_i = y_i / d_i; backward, rows i descending: z_i = w_i after every later
+ * row's updates, then z_k = z_k - L_ik * z_i for k in [f_i, i). */
+static void precond_apply(orc_state *S, const double *r, double *z)
+{
+    int64_t n = S->G->n;
+    if (S->block_size <= 0) {
+#pragma omp parallel for schedule(static) if((n) > 32768)
+        for (int64_t u = 0; u < n; u++) z[u] = r[u] * S->Dinv[u];
+        return;
+    }
+    double *y = S->by;
+#pragma omp parallel for schedule(static) if((S->nblk) > 64)
+    for (int64_t b = 0; b < S->nblk; b++) {
+        int64_t p0 = S->bptr[b], p1 = S->bptr[b + 1];
+        for (int64_t i = p0; i < p1; i++) {
+            int64_t fi = S->bfirst[i];
+            const double *Li = S->bL + S->boff[i] - fi;
+            double acc = r[S->bnode[i]];
+            for (int64_t k = fi; k < i - p0; k++) acc = acc - Li[k] * y[p0 + k];
+            y[i] = acc;
+        }
+        for (int64_t i = p0; i < p1; i++) y[i] = y[i] / S->bDd[i];
+        for (int64_t i = p1 - 1; i >= p0; i--) {
+            int64_t fi = S->bfirst[i];
+            const double *Li = S->bL + S->boff[i] - fi;
+            for (int64_t k = fi; k < i - p0; k++) y[p0 + k] = y[p0 + k] - Li[k] * y[i];
+        }
+        for (int64_t i = p0; i < p1; i++) z[S->bnode[i]] = y[i];
+    }
 }
 
 orc_state *orc_state_new(const orc_graph *G, const orc_options *o)
@@ -458,6 +616,9 @@ orc_state *orc_state_new(const orc_graph *G, const orc_options *o)
     S->eps = o->eps; S->T = o->T; S->cg_rtol = o->cg_rtol; S->cg_max_iter = o->cg_max_iter;
     S->cg_norm = o->cg_norm; S->warm_start = o->warm_start; S->cg_variant = o->cg_variant;
     S->step = 0;
+    S->block_size = o->block_size;
+    if (S->block_size < 0 || (S->block_size > 0 && S->cg_variant != 0)) { orc_state_free(S); return NULL; }
+    if (S->block_size > 0 && block_setup(S) != ORC_OK) { orc_state_free(S); return NULL; }
     return S;
 }
 
@@ -468,7 +629,7 @@ static void assemble(orc_state *S, const double *x)
 {
     const orc_graph *G = S->G;
     double eps2 = S->eps * S->eps;
-    OMP_FOR
+#pragma omp parallel for schedule(static) if((G->n) > 32768)
     for (int64_t u = 0; u < G->n; u++) {
         double acc = 0.0;
         for (int64_t e = G->adj_ptr[u]; e < G->adj_ptr[u + 1]; e++) {
@@ -491,7 +652,7 @@ static void assemble(orc_state *S, const double *x)
 static void matvec(const orc_state *S, const double *p, double *q)
 {
     const orc_graph *G = S->G;
-    OMP_FOR
+#pragma omp parallel for schedule(static) if((G->n) > 32768)
     for (int64_t u = 0; u < G->n; u++) {
         double acc = 0.0;
         for (int64_t e = G->adj_ptr[u]; e < G->adj_ptr[u + 1]; e++)
@@ -502,13 +663,14 @@ static void matvec(const orc_state *S, const double *p, double *q)
 
 static double dot_c3(orc_state *S, const double *a, const double *b)
 {
-    OMP_FOR
+#pragma omp parallel for schedule(static) if((S->G->n) > 32768)
     for (int64_t u = 0; u < S->G->n; u++) S->tmp[u] = a[u] * b[u];
     return orc_c3_sum(S->tmp, S->G->n);
 }
 
 /* O5: Jacobi-preconditioned CG ("preconditioned conjugate gradient")
- * on L~ v = b with M = diag(L~) (A12), Hestenes-Stiefel form, warm start x0
+ * on L~ v = b with M = diag(L~) (A12) or the block-Jacobi M of A32
+ * (z = M^-1 r by precond_apply; ref = ||M^-1 b||), Hestenes-Stiefel form, warm start x0
  * = S->x, stopping test res <= rtol*ref before each iteration (A9,
  * A13). */
 static int pcg(orc_state *S, orc_report *rep)
@@ -519,17 +681,18 @@ static int pcg(orc_state *S, orc_report *rep)
     /* r = b - A x0 */
     matvec(S, x, q);
     const double *b = S->bvec ? S->bvec : S->gs;
-    OMP_FOR
+#pragma omp parallel for schedule(static) if((n) > 32768)
     for (int64_t u = 0; u < n; u++) r[u] = b[u] - q[u];
-    OMP_FOR
-    for (int64_t u = 0; u < n; u++) z[u] = r[u] * S->Dinv[u];
-    OMP_FOR
+    precond_apply(S, r, z);
+#pragma omp parallel for schedule(static) if((n) > 32768)
     for (int64_t u = 0; u < n; u++) p[u] = z[u];
     double rho = dot_c3(S, r, z);
     double ref2;
     if (S->cg_norm == 0) {
-        OMP_FOR
-        for (int64_t u = 0; u < n; u++) { double mb = b[u] * S->Dinv[u]; S->tmp[u] = mb * mb; }
+        double *mb = S->w;                      /* M^-1 b (w is CG-CG's; free here) */
+        precond_apply(S, b, mb);
+#pragma omp parallel for schedule(static) if((n) > 32768)
+        for (int64_t u = 0; u < n; u++) S->tmp[u] = mb[u] * mb[u];
         ref2 = orc_c3_sum(S->tmp, n);
     } else {
         ref2 = dot_c3(S, b, b);
@@ -550,17 +713,16 @@ static int pcg(orc_state *S, orc_report *rep)
         double pi = dot_c3(S, p, q);
         if (!(pi > 0.0) || isinf(pi)) return ORC_ERR_CG_BREAKDOWN;
         double alpha = rho / pi;
-        OMP_FOR
+#pragma omp parallel for schedule(static) if((n) > 32768)
         for (int64_t u = 0; u < n; u++) x[u] = x[u] + alpha * p[u];
-        OMP_FOR
+#pragma omp parallel for schedule(static) if((n) > 32768)
         for (int64_t u = 0; u < n; u++) r[u] = r[u] - alpha * q[u];
-        OMP_FOR
-        for (int64_t u = 0; u < n; u++) z[u] = r[u] * S->Dinv[u];
+        precond_apply(S, r, z);
         double rho1 = dot_c3(S, r, z);
         res2 = S->cg_norm == 0 ? dot_c3(S, z, z) : dot_c3(S, r, r);
         res = sqrt(res2);
         double beta = rho1 / rho;
-        OMP_FOR
+#pragma omp parallel for schedule(static) if((n) > 32768)
         for (int64_t u = 0; u < n; u++) p[u] = z[u] + beta * p[u];
         rho = rho1;
         k++;
@@ -592,14 +754,14 @@ static int pcg_cgcg(orc_state *S, orc_report *rep)
     double *x = S->x, *r = S->r, *z = S->z, *p = S->p, *q = S->q, *w = S->w, *sv = S->sv;
     matvec(S, x, q);
     const double *b = S->bvec ? S->bvec : S->gs;
-    OMP_FOR
+#pragma omp parallel for schedule(static) if((n) > 32768)
     for (int64_t u = 0; u < n; u++) r[u] = b[u] - q[u];
-    OMP_FOR
+#pragma omp parallel for schedule(static) if((n) > 32768)
     for (int64_t u = 0; u < n; u++) z[u] = r[u] * S->Dinv[u];
     double rho = dot_c3(S, r, z);
     double ref2;
     if (S->cg_norm == 0) {
-        OMP_FOR
+#pragma omp parallel for schedule(static) if((n) > 32768)
         for (int64_t u = 0; u < n; u++) { double mb = b[u] * S->Dinv[u]; S->tmp[u] = mb * mb; }
         ref2 = orc_c3_sum(S->tmp, n);
     } else {
@@ -623,15 +785,15 @@ static int pcg_cgcg(orc_state *S, orc_report *rep)
     }
     for (;;) {
         if (res <= S->cg_rtol * ref || k == S->cg_max_iter) break;
-        OMP_FOR
+#pragma omp parallel for schedule(static) if((n) > 32768)
         for (int64_t u = 0; u < n; u++) p[u] = k == 0 ? z[u] : z[u] + beta * p[u];
-        OMP_FOR
+#pragma omp parallel for schedule(static) if((n) > 32768)
         for (int64_t u = 0; u < n; u++) sv[u] = k == 0 ? w[u] : w[u] + beta * sv[u];
-        OMP_FOR
+#pragma omp parallel for schedule(static) if((n) > 32768)
         for (int64_t u = 0; u < n; u++) x[u] = x[u] + alpha * p[u];
-        OMP_FOR
+#pragma omp parallel for schedule(static) if((n) > 32768)
         for (int64_t u = 0; u < n; u++) r[u] = r[u] - alpha * sv[u];
-        OMP_FOR
+#pragma omp parallel for schedule(static) if((n) > 32768)
         for (int64_t u = 0; u < n; u++) z[u] = r[u] * S->Dinv[u];
         matvec(S, z, w);
         double gamma = dot_c3(S, r, z);
@@ -669,7 +831,7 @@ static void diagnostics(orc_state *S, orc_report *rep)
     double eps2 = S->eps * S->eps;
     /* Eq. 9: S_eps = sum over edges with c > 0 of w_e; node u
      * owns its higher-id n-links (ascending) then its s- and t-links. */
-    OMP_FOR
+#pragma omp parallel for schedule(static) if((n) > 32768)
     for (int64_t u = 0; u < n; u++) {
         double acc = 0.0;
         for (int64_t e = G->adj_ptr[u]; e < G->adj_ptr[u + 1]; e++) {
@@ -684,7 +846,7 @@ static void diagnostics(orc_state *S, orc_report *rep)
     }
     rep->S_eps = orc_c3_sum(S->tmp, n);
     /* Prop. 3: flow value x^T L^(l) x = sum_e g_e d_e^2 */
-    OMP_FOR
+#pragma omp parallel for schedule(static) if((n) > 32768)
     for (int64_t u = 0; u < n; u++) {
         double acc = 0.0;
         for (int64_t e = G->adj_ptr[u]; e < G->adj_ptr[u + 1]; e++) {
@@ -699,18 +861,18 @@ static void diagnostics(orc_state *S, orc_report *rep)
         S->tmp[u] = acc;
     }
     rep->flow_value = orc_c3_sum(S->tmp, n);
-    OMP_FOR
+#pragma omp parallel for schedule(static) if((n) > 32768)
     for (int64_t u = 0; u < n; u++) S->tmp[u] = S->gs[u] * (1.0 - x[u]);
     rep->current_s = orc_c3_sum(S->tmp, n);
     /* true residual in the stopping norm */
     double *q = S->q;
     matvec(S, x, q);
-    OMP_FOR
-    for (int64_t u = 0; u < n; u++) {
-        double rr = S->gs[u] - q[u];
-        double v = S->cg_norm == 0 ? rr * S->Dinv[u] : rr;
-        S->tmp[u] = v * v;
-    }
+#pragma omp parallel for schedule(static) if((n) > 32768)
+    for (int64_t u = 0; u < n; u++) q[u] = S->gs[u] - q[u];
+    if (S->cg_norm == 0) precond_apply(S, q, S->w);   /* the stopping norm's M^-1 (b - A x) */
+    const double *mv = S->cg_norm == 0 ? S->w : q;
+#pragma omp parallel for schedule(static) if((n) > 32768)
+    for (int64_t u = 0; u < n; u++) S->tmp[u] = mv[u] * mv[u];
     double tr = sqrt(orc_c3_sum(S->tmp, n));
     rep->true_rel_res = rep->ref > 0.0 ? tr / rep->ref : 0.0;
     double mn = n ? x[0] : 0.0, mx = n ? x[0] : 0.0;
@@ -723,6 +885,7 @@ int orc_init(orc_state *S, orc_report *rep)
 {
     memset(rep, 0, sizeof(*rep));
     assemble(S, NULL);
+    if (S->block_size > 0) block_factor(S);
     for (int64_t u = 0; u < S->G->n; u++) S->x[u] = 0.0;
     int rc = solve(S, rep);
     if (rc != ORC_OK) return rc;
@@ -738,6 +901,7 @@ int orc_step(orc_state *S, orc_report *rep)
     memset(rep, 0, sizeof(*rep));
     if (S->step == 0) return ORC_ERR_STATE;
     assemble(S, S->x);
+    if (S->block_size > 0) block_factor(S);
     if (!S->warm_start)
         for (int64_t u = 0; u < S->G->n; u++) S->x[u] = 0.0;
     int rc = solve(S, rep);
@@ -775,6 +939,31 @@ void orc_assemble_export(orc_state *S, const double *x, double *g, double *gs, d
     const orc_graph *G = S->G;
     for (int64_t e = 0; e < G->adj_ptr[G->n]; e++) g[e] = S->g[e];
     for (int64_t u = 0; u < G->n; u++) { gs[u] = S->gs[u]; gt[u] = S->gt[u]; D[u] = S->D[u]; Dinv[u] = S->Dinv[u]; }
+}
+
+/* For unit pins of A32: the partition (positions -> ids, block starts, first
+ * columns) and, after assemble(x) (x NULL = init) and the factorisation, the
+ * factor (boff-indexed envelope, pivots) and z = M^-1 r. */
+int64_t orc_block_count(const orc_state *S) { return S->block_size > 0 ? S->nblk : 0; }
+int64_t orc_block_env_size(const orc_state *S) { return S->block_size > 0 ? S->boff[S->G->n] : 0; }
+void orc_block_export(const orc_state *S, int64_t *bptr, int64_t *bnode, int64_t *bfirst, int64_t *boff)
+{
+    if (S->block_size <= 0) return;
+    int64_t n = S->G->n;
+    for (int64_t b = 0; b <= S->nblk; b++) bptr[b] = S->bptr[b];
+    for (int64_t i = 0; i < n; i++) { bnode[i] = S->bnode[i]; bfirst[i] = S->bfirst[i]; }
+    for (int64_t i = 0; i <= n; i++) boff[i] = S->boff[i];
+}
+void orc_precond_export(orc_state *S, const double *x, const double *r, double *z, double *L, double *Dd)
+{
+    assemble(S, x);
+    if (S->block_size > 0) block_factor(S);
+    precond_apply(S, r, z);
+    if (S->block_size > 0) {
+        int64_t n = S->G->n;
+        for (int64_t e = 0; e < S->boff[n]; e++) L[e] = S->bL[e];
+        for (int64_t i = 0; i < n; i++) Dd[i] = S->bDd[i];
+    }
 }
 
 /* Run a full solve (init + T steps), optionally recording x^(l) for l=0..T
@@ -1248,6 +1437,8 @@ int orc_lambda2(orc_state *S, double rtol, int32_t max_iter, int32_t norm, doubl
     memcpy(xs, S->x, sizeof(double) * (size_t)n);
     double r0 = S->cg_rtol; int32_t m0 = S->cg_max_iter, n0 = S->cg_norm;
     S->cg_rtol = rtol; S->cg_max_iter = max_iter; S->cg_norm = norm;
+    int32_t bs0 = S->block_size;
+    S->block_size = 0;                 /* lambda_2's solve: point Jacobi (A30) */
     assemble(S, NULL);
     for (int64_t u = 0; u < n; u++) { b[u] = S->gs[u] - S->gt[u]; S->x[u] = 0.0; }
     S->bvec = b;
@@ -1255,6 +1446,7 @@ int orc_lambda2(orc_state *S, double rtol, int32_t max_iter, int32_t norm, doubl
     memset(&rep, 0, sizeof(rep));
     int rc = solve(S, &rep);
     S->bvec = NULL;
+    S->block_size = bs0;
     S->cg_rtol = r0; S->cg_max_iter = m0; S->cg_norm = n0;
     if (rc == ORC_OK) {
         const double *x = S->x;
