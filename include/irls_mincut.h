@@ -105,7 +105,15 @@ typedef struct {
                             ends the solve with IRLS_ERR_NCCL.  Ignored on a single-rank context.
                             Default 0 (NCCL). */
     int32_t cg_variant;  /* irls_cg_variant; default IRLS_CG_HS */
-    int32_t reserved;
+    int32_t block_size;  /* preconditioner (A12 / A32): 0 = point Jacobi M = diag(L~) (default); B in [1, 256]
+                            = block Jacobi with exact block solves (the paper's "block Jacobi" with "LU"
+                            blocks): BFS blocks of at most B nodes
+                            inside one C3 group (so identical for every world size), each factored per IRLS
+                            step as A_B = L D L^T (envelope, by rows, sums ascending) and applied per CG
+                            iteration by forward / backward substitution, bitwise equal to the oracle's
+                            definition (A32).  The partition is built at create.  Not combinable
+                            with cg_variant IRLS_CG_CG, p2p or record_trace (IRLS_ERR_INVALID_ARGUMENT).
+                            irls_lambda2's solve stays point Jacobi (A30). */
 } irls_options;
 
 void irls_options_default(irls_options *opt);

@@ -36,7 +36,7 @@ extern "C" void irls_options_default(irls_options *o)
     o->fixed_point_exit = 0;
     o->p2p = 0;
     o->cg_variant = IRLS_CG_HS;
-    o->reserved = 0;
+    o->block_size = 0;
 }
 
 extern "C" const char *irls_status_string(irls_status st)
@@ -324,12 +324,20 @@ static irls_status enq_assemble(Ranks &R, int mode, const CondArgs &cd, cudaStre
     for (irls_ctx *c : R) {
         const VecArgs v = vec_args(c);
         const RedArgs ra = red_args_solve(c);
+        // block Jacobi (A32): K1 assembles (its Jacobi z0 and START sums are
+        // superseded), then factor, z0 = M^-1 r0, mb = M^-1 b, START sums
+        CondArgs cdk = cd;
+        if (c->blk_on) cdk.finalize = 0;
         if (c->kind == 0)
-            c->launches += launch_stencil_assemble_ex(stencil_args(c, false), v, ra, cd, mode, c->opt.eps, c->gs_diag,
-                                                      c->gt_diag, st);
+            c->launches += launch_stencil_assemble_ex(stencil_args(c, false), v, ra, cdk, mode, c->opt.eps,
+                                                      c->gs_diag, c->gt_diag, st);
         else
-            c->launches += launch_sell_assemble_ex(sell_args(c), v, ra, cd, mode, c->opt.eps, c->gs_diag,
+            c->launches += launch_sell_assemble_ex(sell_args(c), v, ra, cdk, mode, c->opt.eps, c->gs_diag,
                                                    c->gt_diag, st);
+        if (c->blk_on) {
+            c->launches += launch_block_factor(c->blk, c->D, v.frozen, st);
+            c->launches += launch_block_start(c->blk, v, c->gs_diag, ra, cd, st);
+        }
     }
     if (R[0]->multi) {
         if ((s = coll_allreduce(R, 5, st))) return s;
@@ -440,6 +448,10 @@ static irls_status enq_body(Ranks &R, const CondArgs &cd, cudaStream_t st)
             v.plane = c->P;
         }
         const bool csr_p2p = c->p2p && c->kind == 1;
+        if (c->blk_on) {  // block Jacobi (A32): r -= alpha q, z = M^-1 r, RZ sums
+            c->launches += launch_block_iter(c->blk, v, red_args_solve(c), cd, st);
+            continue;
+        }
         launch_axpy_jacobi(v, csr_p2p ? red_args(c) : red_args_solve(c), cd, st);
         c->launches++;
         if (csr_p2p) {  // z halo as peer stores, then the group sums' push (after the stores)
@@ -505,7 +517,16 @@ static irls_status enq_tail(Ranks &R, int mode, cudaStream_t st, bool finish = t
 // wrapped as  gate -> IF (not frozen) { K1 -> WHILE {...} -> finish } ->
 // report: a frozen solve costs one graph launch and two one-thread kernels.
 // One-block CG loop (small.cu) for a single rank whose graph is one C3 chunk.
-static bool small_path(const irls_ctx *c) { return !c->multi && !c->cgcg && c->n_own > 0 && c->n_own <= kChunk; }
+static bool small_path(const irls_ctx *c)
+{
+    return !c->multi && !c->cgcg && !c->blk_on && c->n_own > 0 && c->n_own <= kChunk;
+}
+
+// Block Jacobi (A32) serves every IRLS solve; lambda_2's stays point Jacobi (A30).
+static void set_blk_mode(Ranks &R, int mode)
+{
+    for (irls_ctx *c : R) c->blk_on = c->opt.block_size > 0 && mode != ASM_LAMBDA2;
+}
 
 static void enq_small(irls_ctx *c, cudaStream_t st)
 {
@@ -524,6 +545,7 @@ static irls_status capture_solve_body(irls_ctx *c, Ranks &R, int mode, cudaStrea
     const cudaGraphNode_t *deps = nullptr;
     size_t nd = 0;
     CK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &graph, &deps, &nd));
+    set_blk_mode(R, mode);
     const bool small = small_path(c);
     cudaGraphConditionalHandle h{};
     // default 0 at every launch: the assembly's last block turns the loop on
@@ -721,6 +743,7 @@ static irls_status enqueue_solve(Ranks &R, int mode)
     memset(&cd, 0, sizeof(cd));
     cd.use = 0;
     cd.finalize = c->multi ? 0 : 1;
+    set_blk_mode(R, mode);
     if (mode == ASM_INIT || mode == ASM_LAMBDA2)
         for (irls_ctx *d : R) CK(cudaMemsetAsync(d->x, 0, sizeof(double) * d->n_own, st));
     irls_status s = enq_assemble(R, mode, cd, st);

@@ -408,6 +408,7 @@ irls_status create_stencil_impl(irls_ctx **out, const irls_comm_desc *comm, int3
                 c->n_links = (int64_t)vo[5];  // |E~| with c > 0
             }
         }
+        if (!s) s = block_setup_stencil(c, cx, cy, cz);
         if (!s) s = init_nccl(c, comm);
     }
     if (s) {
@@ -848,6 +849,7 @@ irls_status create_csr_impl(irls_ctx **out, const irls_comm_desc *comm, int64_t 
                 st = fail(c, IRLS_ERR_CUDA, std::string("csr strip upload: ") + cudaGetErrorString(e));
         }
     }
+    if (!st) st = block_setup_csr(c, aptr.data(), aidx.data(), c->multi ? lsptr.data() : sptr.data());
     if (!st) st = init_nccl(c, comm);
     if (!st && nr > 0) {
         cudaError_t e = cudaSuccess;

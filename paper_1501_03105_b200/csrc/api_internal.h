@@ -110,10 +110,17 @@ static inline irls_status check_opts(const irls_options *o)
     if (!(o->eps > 0.0) || isinf(o->eps) || o->T < 0 || !(o->cg_rtol >= 0.0) || o->cg_max_iter < 0 ||
         (o->cg_norm != 0 && o->cg_norm != 1) || (o->loop_mode < 0 || o->loop_mode > 2) ||
         (o->fixed_point_exit != 0 && o->fixed_point_exit != 1) || (o->p2p != 0 && o->p2p != 1) ||
-        (o->cg_variant != IRLS_CG_HS && o->cg_variant != IRLS_CG_CG))
+        (o->cg_variant != IRLS_CG_HS && o->cg_variant != IRLS_CG_CG) || o->block_size < 0 ||
+        o->block_size > 256 ||
+        (o->block_size > 0 && (o->cg_variant != IRLS_CG_HS || o->p2p || o->record_trace)))
         return IRLS_ERR_INVALID_ARGUMENT;
     return IRLS_OK;
 }
+
+// block-Jacobi preconditioner setup at create (api_block.cu; no-op unless
+// opt.block_size > 0): host capacities of the grid / the reduced CSR
+irls_status block_setup_stencil(irls_ctx *c, const double *cx, const double *cy, const double *cz);
+irls_status block_setup_csr(irls_ctx *c, const int64_t *aptr, const int32_t *aidx, const int64_t *lsptr);
 
 static inline int32_t compute_F(double cmax, int64_t cnt)
 {

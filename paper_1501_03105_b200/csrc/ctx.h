@@ -92,6 +92,10 @@ struct irls_ctx {
     std::vector<int64_t> rank_lo;            // [world + 1]: first reduced id owned by every rank
     std::vector<int32_t> comp_root;          // component (root id) of every non-terminal in G~ (host)
 
+    // ---- block-Jacobi preconditioner (opt.block_size > 0, A32)
+    irls::BlockArgs blk{};
+    bool blk_on = false;  // this solve (mode) uses it: every IRLS solve; not lambda_2's (A30)
+
     // ---- sweep fixed point
     int32_t F = 0;
 

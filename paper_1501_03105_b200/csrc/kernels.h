@@ -65,6 +65,21 @@ struct SellArgs {
     int64_t gbase, glow;         // strips: columns >= gbase are ghosts; the first glow ghosts have lower ids
 };
 
+// Block-Jacobi preconditioner (A32, block_jacobi.cu): blocks of positions
+// [bptr[b], bptr[b+1]); position i holds local node bnode[i]; its envelope row
+// (block-local columns [bfirst[i], i)) is L[boff[i] .. boff[i+1]); its
+// in-block lower neighbours are (ecol[e], *eg[e]) for e in [eptr[i], eptr[i+1]).
+struct BlockArgs {
+    int64_t nblk = 0;
+    int32_t m_max = 0;           // largest block
+    int64_t env_max = 0;         // largest block envelope (doubles)
+    const int32_t *bptr = nullptr, *bnode = nullptr, *bfirst = nullptr, *eptr = nullptr, *ecol = nullptr;
+    const int64_t *boff = nullptr;
+    const double *const *eg = nullptr;  // the conductance of each in-block edge (device pointers)
+    double *L = nullptr, *Dd = nullptr;  // factor: envelope of the unit lower L, pivots (block order)
+    double *mb = nullptr;        // M^-1 b (START)
+};
+
 struct CondArgs {
     cudaGraphConditionalHandle handle;
     int32_t use;                 // 1: set the WHILE condition from device code
@@ -97,6 +112,15 @@ void launch_ghost_pupdate(const VecArgs &v, int64_t ghost_lo, int64_t ghost_hi, 
 // CSR multi-rank: ghost block of p updated from the exchanged z; halo packing
 void launch_ghost_range_pupdate(const VecArgs &v, int64_t start, int64_t count, DevCtrl *ctrl, cudaStream_t st);
 void launch_halo_pack(const double *arr, const int32_t *idx, int64_t n, double *out, cudaStream_t st);
+// block Jacobi (A32): KF factor per IRLS step; START: z0 = M^-1 r0, mb = M^-1 b
+// + the 5 START reductions; iteration: r -= alpha q, z = M^-1 r + the 3 RZ
+// reductions.  Return the number of kernels launched.
+size_t block_smem_per_cta(const BlockArgs &b);
+void block_prepare(const BlockArgs &b);  // once per context, outside capture
+int launch_block_factor(const BlockArgs &b, const double *D, const int32_t *frozen, cudaStream_t st);
+int launch_block_start(const BlockArgs &b, const VecArgs &v, const double *gs, const RedArgs &ra,
+                       const CondArgs &cd, cudaStream_t st);
+int launch_block_iter(const BlockArgs &b, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, cudaStream_t st);
 // K5: r -= alpha q, z = Dinv r, RZ reduction
 void launch_axpy_jacobi(const VecArgs &v, const RedArgs &ra, const CondArgs &cd, cudaStream_t st);
 // after the loop: x += alpha p_last (or x = 0 if b = 0)
@@ -173,28 +197,36 @@ struct SweepBuffers {
     unsigned long long *keys, *keys_alt;
     int32_t *vals, *vals_alt;
     int32_t *rank;
-    int32_t *tile_hist;      // [256][ntiles]
+    int32_t *tile_hist;      // [256][ntiles]: the radix passes' look-back words
     int32_t *tile_off;       // [256][ntiles]
     int32_t *scan_tmp;       // scan block totals
     unsigned long long *digit_hist;  // [8][256] global histograms
-    __int128 *delta;         // [n+2] in sweep order (+ P0, P_k)
+    __int128 *delta;         // [n+2] delta_v in id order (+ P0, P_k)
     __int128 *tile_sum;      // [ntiles]
     __int128 *tile_min;      // [ntiles]
     int64_t *tile_argmin;    // [ntiles]
-    int32_t *flags;          // [0] NaN seen
+    int32_t *flags;          // [0] NaN seen, [1] radix tile ticket
     int64_t *k_out;
     double *cross;
     uint8_t *side;           // n_total
 };
 int64_t sweep_ntiles(int64_t n);
-void sweep_keys(const double *x, SweepBuffers &b, cudaStream_t st);
+// prep: keys (x desc), ids, delta_v in id order (exact fixed point), global
+// digit histograms, per-tile Q(cs) sums, NaN flag (digit_hist and flags zeroed
+// by the caller)
+void sweep_prep_stencil(const StencilArgs &s, int64_t N, int32_t F, const double *x, SweepBuffers &b,
+                        cudaStream_t st);
+void sweep_prep_sell(const SellArgs &s, int32_t F, const double *x, SweepBuffers &b, cudaStream_t st);
 // returns pointer to the sorted ids buffer (vals or vals_alt); *nan: a NaN key
-// (nothing sorted); *rank_done: the last radix pass also wrote rank[]
-int32_t *sweep_sort(SweepBuffers &b, cudaStream_t st, int *launches, bool *nan, bool *rank_done);
-void sweep_rank(const int32_t *order, SweepBuffers &b, cudaStream_t st);
-void sweep_delta_stencil(const StencilArgs &s, int64_t N, int32_t F, SweepBuffers &b, cudaStream_t st);
-void sweep_delta_sell(const SellArgs &s, int32_t F, SweepBuffers &b, cudaStream_t st);
-void sweep_scan_argmin(SweepBuffers &b, __int128 P0, cudaStream_t st);
+// (nothing sorted)
+int32_t *sweep_sort(SweepBuffers &b, cudaStream_t st, int *launches, bool *nan);
+void sweep_scan_argmin(SweepBuffers &b, const int32_t *ord, __int128 P0, cudaStream_t st);
+// side + cut of the first k of the order, membership from x (the sweep)
+void sweep_side_cross_x_stencil(const StencilArgs &s, int64_t N, const double *x, const int32_t *ord, SweepBuffers &b,
+                                const RedArgs &ra, cudaStream_t st);
+void sweep_side_cross_x_sell(const SellArgs &s, const double *x, const int32_t *ord, const int64_t *orig,
+                             SweepBuffers &b, const RedArgs &ra, cudaStream_t st);
+// side + cut of {v : rank[v] < k} (two-level lift)
 void sweep_side_cross_stencil(const StencilArgs &s, int64_t N, SweepBuffers &b, const RedArgs &ra,
                               cudaStream_t st);
 void sweep_side_cross_sell(const SellArgs &s, const int64_t *orig, int64_t n_total, SweepBuffers &b,

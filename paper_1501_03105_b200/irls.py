@@ -30,7 +30,7 @@ class irls_options(C.Structure):
     _fields_ = [("eps", C.c_double), ("T", C.c_int32), ("cg_rtol", C.c_double), ("cg_max_iter", C.c_int32),
                 ("cg_norm", C.c_int32), ("warm_start", C.c_int32), ("record_trace", C.c_int32),
                 ("loop_mode", C.c_int32), ("fixed_point_exit", C.c_int32), ("p2p", C.c_int32),
-                ("cg_variant", C.c_int32), ("reserved", C.c_int32)]
+                ("cg_variant", C.c_int32), ("block_size", C.c_int32)]
 
 
 DEVICE_ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
