@@ -18,7 +18,7 @@ static irls_status alloc_sweep(irls_ctx *c)
     b.keys_alt = dalloc<unsigned long long>(c, n);
     b.vals = dalloc<int32_t>(c, n);
     b.vals_alt = dalloc<int32_t>(c, n);
-    b.rank = dalloc<int32_t>(c, n);
+    b.rank = nullptr;  // the sweep forms membership from x (two-level uses its own ranks)
     b.tile_hist = dalloc<int32_t>(c, 256 * nt);
     b.tile_off = dalloc<int32_t>(c, 256 * nt);
     b.scan_tmp = (int32_t *)dalloc<int64_t>(c, (256 * nt + 4095) / 4096 + 1);
@@ -31,7 +31,7 @@ static irls_status alloc_sweep(irls_ctx *c)
     b.k_out = dalloc<int64_t>(c, 1);
     b.side = dalloc<uint8_t>(c, c->n_total);
     c->order_out = dalloc<int32_t>(c, n);
-    if (!b.keys || !b.keys_alt || !b.vals || !b.vals_alt || !b.rank || !b.tile_hist || !b.tile_off || !b.scan_tmp ||
+    if (!b.keys || !b.keys_alt || !b.vals || !b.vals_alt || !b.tile_hist || !b.tile_off || !b.scan_tmp ||
         !b.digit_hist || !b.delta || !b.tile_sum || !b.tile_min || !b.tile_argmin || !b.flags || !b.k_out || !b.side ||
         !c->order_out)
         return fail(c, IRLS_ERR_OOM, "sweep buffers");
@@ -89,19 +89,14 @@ irls_status sweep_rank0(irls_ctx *c, const double *xfull, uint8_t *side, int32_t
     c->launches = 0;
     SweepBuffers &b = c->sb;
     CK(cudaMemsetAsync(b.flags, 0, sizeof(int32_t) * 4, st));
-    sweep_keys(xfull, b, st);
+    CK(cudaMemsetAsync(b.digit_hist, 0, sizeof(unsigned long long) * 8 * 256, st));
+    if (c->kind == 0) sweep_prep_stencil(stencil_args(c, true), n, c->F, xfull, b, st);
+    else sweep_prep_sell(sell_args_full(c), c->F, xfull, b, st);
     launches++;
-    bool nan = false, rank_done = false;
-    int32_t *ord = sweep_sort(b, st, &launches, &nan, &rank_done);
+    bool nan = false;
+    int32_t *ord = sweep_sort(b, st, &launches, &nan);
     if (nan) return fail(c, IRLS_ERR_BAD_POTENTIAL, "NaN in potentials");
-    if (!rank_done) {  // no radix pass ran (every key equal): rank of the identity order
-        sweep_rank(ord, b, st);
-        launches++;
-    }
-    if (c->kind == 0) sweep_delta_stencil(stencil_args(c, true), n, c->F, b, st);
-    else sweep_delta_sell(sell_args_full(c), c->F, b, st);
-    launches += 1;
-    sweep_scan_argmin(b, qfix_host(c->c_st, c->F), st);
+    sweep_scan_argmin(b, ord, qfix_host(c->c_st, c->F), st);
     launches += 4;
     RedArgs ra;
     ra.part = c->part;
@@ -112,10 +107,14 @@ irls_status sweep_rank0(irls_ctx *c, const double *xfull, uint8_t *side, int32_t
     ra.g1 = 8;
     ra.n_fin = count_nonempty(ra.K, 0, 8);
     if (c->kind == 0) {
-        sweep_side_cross_stencil(stencil_args(c, true), n, b, ra, st);
+        if (n > 0) sweep_side_cross_x_stencil(stencil_args(c, true), n, xfull, ord, b, ra, st);
+        else {
+            const uint8_t sd[2] = {1, 0};
+            CK(cudaMemcpyAsync(b.side, sd, 2, cudaMemcpyHostToDevice, st));
+        }
     } else {
         CK(cudaMemsetAsync(b.side, 0, c->n_total, st));
-        sweep_side_cross_sell(sell_args_full(c), c->orig_dev, c->n_total, b, ra, st);
+        sweep_side_cross_x_sell(sell_args_full(c), xfull, ord, c->orig_dev, b, ra, st);
         const uint8_t one = 1;
         CK(cudaMemcpyAsync(b.side + c->s_id, &one, 1, cudaMemcpyHostToDevice, st));
     }

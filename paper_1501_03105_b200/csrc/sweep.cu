@@ -45,79 +45,159 @@ __device__ __forceinline__ i128 shfl_down_i128(i128 v, int off)
     return ((i128)hi << 64) | (i128)lo;
 }
 
-// ---------------------------------------------------------------------------
-// keys
-// ---------------------------------------------------------------------------
-__global__ void k_sweep_keys(const double *x, int64_t n, u64 *keys, int32_t *vals, int32_t *flags)
+__device__ __forceinline__ void tile_sum_i128(i128 v, i128 *out)
 {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    double xv = x[i];
-    if (isnan(xv)) flags[0] = 1;
-    if (xv == 0.0) xv = 0.0;  // -0.0 -> +0.0
-    keys[i] = ~dkey_asc(xv);  // ascending key order = x descending
-    vals[i] = (int32_t)i;     // ties keep ascending id (stable sort)
+    __shared__ i128 sm[8];
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) v += shfl_down_i128(v, off);
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        i128 s = 0;
+        for (int i = 0; i < 8; i++) s += sm[i];
+        *out = s;
+    }
 }
 
 // ---------------------------------------------------------------------------
-// radix sort
+// prep: keys, ids, the exact delta_v in id order, global digit histograms
 // ---------------------------------------------------------------------------
-__global__ void k_hist8(const u64 *keys, int64_t n, u64 *digit_hist)
+// delta_v = sum over neighbours u of (u after v ? +Q(c_uv) : -Q(c_uv)) +
+// Q(ct_v) - Q(cs_v), where "u after v" in the total order (x desc, id asc,
+// A14) is x_u < x_v || (x_u == x_v && u > v) — the same predicate as
+// rank_u > rank_v, evaluated from the potentials, so delta needs no rank
+// array and is written coalesced in id order (the scan gathers it).
+__device__ __forceinline__ double canon(double x) { return x == 0.0 ? 0.0 : x; }  // -0.0 -> +0.0
+
+__device__ __forceinline__ bool after(double xu, int64_t u, double xv, int64_t v)
+{
+    return xu < xv || (xu == xv && u > v);
+}
+
+template <class NB>
+__device__ __forceinline__ void prep_tile(int64_t N, int32_t F, const double *x, u64 *keys, int32_t *vals,
+                                          i128 *delta, u64 *digit_hist, i128 *qcs_tile, int32_t *flags, NB nb)
 {
     __shared__ unsigned h[8][256];
     for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&h[0][0])[i] = 0u;
     __syncthreads();
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const u64 k = keys[i];
+    i128 qcs = 0;
+    bool nan = false;
+    const int64_t base = (int64_t)blockIdx.x * kTile;
+    for (int r = 0; r < 16; r++) {
+        const int64_t v = base + r * 256 + threadIdx.x;
+        if (v >= N) break;
+        const double xr = x[v];
+        nan |= isnan(xr);
+        const double xv = canon(xr);
+        const u64 key = ~dkey_asc(xv);  // ascending key order = x descending
+        keys[v] = key;
+        vals[v] = (int32_t)v;           // ties keep ascending id (stable sort)
 #pragma unroll
-        for (int d = 0; d < 8; d++) atomicAdd(&h[d][(k >> (8 * d)) & 255u], 1u);
+        for (int d = 0; d < 8; d++) atomicAdd(&h[d][(key >> (8 * d)) & 255u], 1u);
+        i128 d = 0, qs = 0;
+        nb(v, xv, d, qs);
+        qcs += qs;
+        delta[v] = d;
     }
+    if (nan) flags[0] = 1;
     __syncthreads();
     for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) {
         const unsigned c = (&h[0][0])[i];
         if (c) atomicAdd(&digit_hist[i], (u64)c);
     }
+    tile_sum_i128(qcs, qcs_tile + blockIdx.x);
 }
 
-__global__ void __launch_bounds__(256) k_tile_hist(const u64 *keys, int64_t n, int shift, int32_t *tile_hist,
-                                                   int64_t ntiles)
+__global__ void __launch_bounds__(256) k_sweep_prep_stencil(StencilArgs s, int64_t N, int32_t F, const double *x,
+                                                            u64 *keys, int32_t *vals, i128 *delta, u64 *digit_hist,
+                                                            i128 *qcs_tile, int32_t *flags)
 {
-    __shared__ unsigned h[256];
-    h[threadIdx.x] = 0u;
-    __syncthreads();
-    const int64_t base = (int64_t)blockIdx.x * kTile;
-#pragma unroll 4
-    for (int r = 0; r < 16; r++) {
-        const int64_t i = base + r * 256 + threadIdx.x;
-        if (i < n) atomicAdd(&h[(keys[i] >> shift) & 255u], 1u);
+    prep_tile(N, F, x, keys, vals, delta, digit_hist, qcs_tile, flags,
+              [&](int64_t v, double xv, i128 &d, i128 &qs) {
+                  const uint32_t uv = (uint32_t)v;
+                  const uint32_t t1 = fdiv(uv, s.fd_nx);
+                  const int32_t xx = (int32_t)(uv - t1 * (uint32_t)s.nx);
+                  const uint32_t zz = fdiv(t1, s.fd_ny);
+                  const int32_t y = (int32_t)(t1 - zz * (uint32_t)s.ny), z = (int32_t)zz;
+#define NB(cond, w, cap)                                                           \
+    if (cond) {                                                                    \
+        const i128 q = qfix(cap, F);                                               \
+        d += after(canon(x[w]), w, xv, v) ? q : -q;                                \
     }
-    __syncthreads();
-    tile_hist[(int64_t)threadIdx.x * ntiles + blockIdx.x] = (int32_t)h[threadIdx.x];
+                  NB(z > 0, v - s.P, s.cz[v - s.P]);
+                  NB(y > 0, v - s.nx, s.cy[v - s.nx]);
+                  NB(xx > 0, v - 1, s.cx[v - 1]);
+                  NB(xx < s.nx - 1, v + 1, s.cx[v]);
+                  NB(y < s.ny - 1, v + s.nx, s.cy[v]);
+                  NB(z < s.nz - 1, v + s.P, s.cz[v]);
+#undef NB
+                  qs = qfix(s.cs[v], F);
+                  d += qfix(s.ct[v], F);
+                  d -= qs;
+              });
 }
 
-// Stable scatter.  Warp w owns keys [base + 512 w, +512) in 16 rounds of 32.
-// Ranking in ONE pass: per round, the lanes holding the same digit find each
-// other (match_any); the lowest of them advances the warp's counter of that
-// digit with a shared-memory atomic whose old value, broadcast to the group,
-// is the group's start — so every key gets its rank among the warp's keys of
-// its digit, in key order (a warp's shared-memory atomics to one address
-// take effect in issue order), with no dependent read-modify-write chain
-// between rounds.  Then the per-warp digit starts of the tile (digit-major,
-// warp-minor: stable), staging in shared memory in digit order, and a write
-// out in which consecutive threads write consecutive positions of a bucket.
-__global__ void __launch_bounds__(256, 3) k_radix_scatter(const u64 *keys, const int32_t *vals, u64 *okeys,
-                                                       int32_t *ovals, int64_t n, int shift,
-                                                       const int32_t *tile_off, int64_t ntiles, int32_t *rank)
+__global__ void __launch_bounds__(256) k_sweep_prep_sell(SellArgs s, int32_t F, const double *x, u64 *keys,
+                                                         int32_t *vals, i128 *delta, u64 *digit_hist, i128 *qcs_tile,
+                                                         int32_t *flags)
+{
+    prep_tile(s.n, F, x, keys, vals, delta, digit_hist, qcs_tile, flags,
+              [&](int64_t v, double xv, i128 &d, i128 &qs) {
+                  const int64_t sl = v / kSell;
+                  const int64_t e0 = s.slice_ptr[sl] + (v % kSell);
+                  const int32_t W = (int32_t)((s.slice_ptr[sl + 1] - s.slice_ptr[sl]) / kSell);
+                  for (int32_t k = 0; k < W; k++) {
+                      const int64_t idx = e0 + kSell * (int64_t)k;
+                      const int32_t u = s.col[idx];
+                      if (u < 0) break;
+                      const i128 q = qfix(s.c[idx], F);
+                      d += after(canon(x[u]), u, xv, v) ? q : -q;
+                  }
+                  qs = qfix(s.cs[v], F);
+                  d += qfix(s.ct[v], F);
+                  d -= qs;
+              });
+}
+
+// ---------------------------------------------------------------------------
+// radix sort: stable LSD, 8-bit digits, one kernel per pass ("onesweep"):
+// tiles taken in ticket order publish their digit counts and find their
+// global offsets by decoupled look-back over the earlier tiles
+// ---------------------------------------------------------------------------
+constexpr uint32_t kStAgg = 1u << 30, kStIncl = 2u << 30, kStMask = (1u << 30) - 1u;
+
+struct GStart {
+    int32_t g[256];  // global start of every digit's bucket in this pass
+};
+
+// Stable scatter of one tile.  Warp w owns keys [base + 512 w, +512) in 16
+// rounds of 32; ranking in ONE pass: per round, the lanes holding the same
+// digit find each other (match_any); the lowest of them advances the warp's
+// counter of that digit with a shared-memory atomic whose old value,
+// broadcast to the group, is the group's start — so every key gets its rank
+// among the warp's keys of its digit, in key order.  Then the tile's digit
+// counts are published (aggregate), the exclusive prefix over earlier tiles
+// found by look-back (inclusive prefix published), the per-warp digit starts
+// formed (digit-major, warp-minor: stable), the keys staged in shared memory
+// in digit order and written out so that consecutive threads write
+// consecutive positions of a bucket.
+__global__ void __launch_bounds__(256, 3) k_onesweep(const u64 *keys, const int32_t *vals, u64 *okeys,
+                                                  int32_t *ovals, int64_t n, int shift, GStart gs, uint32_t *state,
+                                                  int32_t *ticket)
 {
     __shared__ int32_t wh[8][256];     // per-warp digit counts, then per-warp tile starts
     __shared__ int32_t gdelta[256];    // global start of the bucket minus its tile-local start
+    __shared__ int32_t s_tile;
     extern __shared__ __align__(16) unsigned char radix_dyn[];  // kTile keys + kTile values
     u64 *skey = reinterpret_cast<u64 *>(radix_dyn);
     int32_t *sval = reinterpret_cast<int32_t *>(radix_dyn + sizeof(u64) * kTile);
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
     for (int i = threadIdx.x; i < 8 * 256; i += 256) (&wh[0][0])[i] = 0;
     __syncthreads();
-    const int64_t tbase = (int64_t)blockIdx.x * kTile;
+    const int32_t tile = s_tile;
+    const int64_t tbase = (int64_t)tile * kTile;
     const int64_t base = tbase + w * 512;
     u64 k[16];
     int32_t vv[16];
@@ -126,8 +206,8 @@ __global__ void __launch_bounds__(256, 3) k_radix_scatter(const u64 *keys, const
     for (int r = 0; r < 16; r++) {
         const int64_t i = base + r * 32 + lane;
         if (i < n) {
-            k[r] = keys[i];
-            vv[r] = vals[i];
+            k[r] = __ldcs(keys + i);
+            vv[r] = __ldcs(vals + i);
         } else {
             k[r] = 0;
             vv[r] = 0;
@@ -146,11 +226,28 @@ __global__ void __launch_bounds__(256, 3) k_radix_scatter(const u64 *keys, const
         dr[r] = d < 256 ? ((uint32_t)d << 16) | (uint32_t)(old + __popc(peers & lt)) : 0xffffffffu;
     }
     __syncthreads();
-    // digit d (one per thread): tile total, exclusive scan over digits, per-warp starts
+    // digit d (one per thread): tile total, published; look-back; exclusive
+    // scan over digits; per-warp starts
     const int d = threadIdx.x;
     int32_t tot = 0;
 #pragma unroll
     for (int w2 = 0; w2 < 8; w2++) tot += wh[w2][d];
+    volatile uint32_t *vst = state;
+    vst[(int64_t)tile * 256 + d] = (tile == 0 ? kStIncl : kStAgg) | (uint32_t)tot;
+    int32_t excl = 0;
+    if (tile > 0) {
+        int64_t t = tile - 1;
+        for (;;) {
+            uint32_t wv;
+            do {
+                wv = vst[t * 256 + d];
+            } while ((wv & ~kStMask) == 0u);
+            excl += (int32_t)(wv & kStMask);
+            if ((wv & ~kStMask) == kStIncl) break;
+            t--;
+        }
+        vst[(int64_t)tile * 256 + d] = kStIncl | (uint32_t)(excl + tot);
+    }
     {
         int32_t inc = tot;
 #pragma unroll
@@ -164,7 +261,7 @@ __global__ void __launch_bounds__(256, 3) k_radix_scatter(const u64 *keys, const
         int32_t pre = 0;
         for (int i = 0; i < w; i++) pre += wsum[i];
         const int32_t ex = pre + inc - tot;
-        gdelta[d] = tile_off[(int64_t)d * ntiles + blockIdx.x] - ex;
+        gdelta[d] = gs.g[d] + excl - ex;
         int32_t run = ex;
 #pragma unroll
         for (int w2 = 0; w2 < 8; w2++) {
@@ -190,7 +287,6 @@ __global__ void __launch_bounds__(256, 3) k_radix_scatter(const u64 *keys, const
         const int64_t g = (int64_t)gdelta[dd] + i;
         okeys[g] = key;
         ovals[g] = sval[i];
-        if (rank) rank[sval[i]] = (int32_t)g;  // last pass: the inverse permutation too
     }
 }
 
@@ -276,25 +372,29 @@ void exclusive_scan_i32(const int32_t *in, int64_t m, int32_t *out, int64_t *tmp
     *launches += 3;
 }
 
-void sweep_keys(const double *x, SweepBuffers &b, cudaStream_t st)
+void sweep_prep_stencil(const StencilArgs &s, int64_t N, int32_t F, const double *x, SweepBuffers &b,
+                        cudaStream_t st)
 {
-    if (b.n == 0) return;
-    k_sweep_keys<<<(unsigned)((b.n + 255) / 256), 256, 0, st>>>(x, b.n, b.keys, b.vals, b.flags);
+    if (N == 0) return;
+    k_sweep_prep_stencil<<<(unsigned)sweep_ntiles(N), 256, 0, st>>>(s, N, F, x, b.keys, b.vals, b.delta, b.digit_hist,
+                                                                    b.tile_min, b.flags);
 }
 
-int32_t *sweep_sort(SweepBuffers &b, cudaStream_t st, int *launches, bool *nan, bool *rank_done)
+void sweep_prep_sell(const SellArgs &s, int32_t F, const double *x, SweepBuffers &b, cudaStream_t st)
+{
+    if (s.n == 0) return;
+    k_sweep_prep_sell<<<(unsigned)sweep_ntiles(s.n), 256, 0, st>>>(s, F, x, b.keys, b.vals, b.delta, b.digit_hist,
+                                                                  b.tile_min, b.flags);
+}
+
+int32_t *sweep_sort(SweepBuffers &b, cudaStream_t st, int *launches, bool *nan)
 {
     const int64_t n = b.n;
     *nan = false;
-    *rank_done = false;
     if (n == 0) return b.vals;
     const int64_t nt = sweep_ntiles(n);
-    cudaMemsetAsync(b.digit_hist, 0, sizeof(u64) * 8 * 256, st);
-    const int nbh = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
-    k_hist8<<<nbh, 256, 0, st>>>(b.keys, n, b.digit_hist);
-    *launches += 1;
     // one host round trip: the digit histograms (constant-digit passes are
-    // skipped) and the NaN flag of the keys kernel
+    // skipped; the others' bucket starts) and the NaN flag of the prep kernel
     u64 h[8 * 256];
     int32_t hflag = 0;
     cudaMemcpyAsync(h, b.digit_hist, sizeof(h), cudaMemcpyDeviceToHost, st);
@@ -304,149 +404,48 @@ int32_t *sweep_sort(SweepBuffers &b, cudaStream_t st, int *launches, bool *nan, 
         *nan = true;
         return b.vals;
     }
-    int last = -1;
-    bool run[8];
-    for (int d = 0; d < 8; d++) {
-        run[d] = true;
-        for (int i = 0; i < 256; i++)
-            if (h[d * 256 + i] == (u64)n) run[d] = false;
-        if (run[d]) last = d;
-    }
     u64 *ka = b.keys, *kb = b.keys_alt;
     int32_t *va = b.vals, *vb = b.vals_alt;
+    uint32_t *state = reinterpret_cast<uint32_t *>(b.tile_hist);  // [ntiles][256] look-back words
+    int32_t *ticket = b.flags + 1;
+    const int dyn = (int)((sizeof(u64) + sizeof(int32_t)) * kTile);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+        attr = true;
+    }
     for (int d = 0; d < 8; d++) {
-        if (!run[d]) continue;
-        k_tile_hist<<<(unsigned)nt, 256, 0, st>>>(ka, n, 8 * d, b.tile_hist, nt);
-        exclusive_scan_i32(b.tile_hist, 256 * nt, b.tile_off, (int64_t *)b.scan_tmp, st, launches);
-        const int dyn = (int)((sizeof(u64) + sizeof(int32_t)) * kTile);
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_radix_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-            attr = true;
+        bool run = true;
+        for (int i = 0; i < 256; i++)
+            if (h[d * 256 + i] == (u64)n) run = false;
+        if (!run) continue;
+        GStart gs;
+        int64_t acc = 0;
+        for (int i = 0; i < 256; i++) {
+            gs.g[i] = (int32_t)acc;
+            acc += (int64_t)h[d * 256 + i];
         }
-        k_radix_scatter<<<(unsigned)nt, 256, dyn, st>>>(ka, va, kb, vb, n, 8 * d, b.tile_off, nt,
-                                                         d == last ? b.rank : nullptr);
-        if (d == last) *rank_done = true;
-        *launches += 2;
+        cudaMemsetAsync(state, 0, sizeof(uint32_t) * 256 * nt, st);
+        cudaMemsetAsync(ticket, 0, sizeof(int32_t), st);
+        k_onesweep<<<(unsigned)nt, 256, dyn, st>>>(ka, va, kb, vb, n, 8 * d, gs, state, ticket);
+        *launches += 1;
         std::swap(ka, kb);
         std::swap(va, vb);
     }
     return va;
 }
 
-__global__ void k_rank(const int32_t *order, int64_t n, int32_t *rank)
-{
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) rank[order[i]] = (int32_t)i;
-}
-
-void sweep_rank(const int32_t *order, SweepBuffers &b, cudaStream_t st)
-{
-    if (b.n == 0) return;
-    k_rank<<<(unsigned)((b.n + 255) / 256), 256, 0, st>>>(order, b.n, b.rank);
-}
-
-// ---------------------------------------------------------------------------
-// delta (exact fixed point) + per-tile sums of Q(cs) for P_0
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void tile_sum_i128(i128 v, i128 *out)
-{
-    __shared__ i128 sm[8];
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) v += shfl_down_i128(v, off);
-    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = v;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        i128 s = 0;
-        for (int i = 0; i < 8; i++) s += sm[i];
-        *out = s;
-    }
-}
-
-__global__ void __launch_bounds__(256) k_delta_stencil(StencilArgs s, int64_t N, int32_t F, const int32_t *rank,
-                                                       i128 *delta, i128 *qcs_tile)
-{
-    i128 qcs = 0;
-    const int64_t base = (int64_t)blockIdx.x * kTile;
-    for (int r = 0; r < 16; r++) {
-        const int64_t v = base + r * 256 + threadIdx.x;
-        if (v >= N) break;
-        const uint32_t uv = (uint32_t)v;
-        const uint32_t t1 = fdiv(uv, s.fd_nx);
-        const int32_t x = (int32_t)(uv - t1 * (uint32_t)s.nx);
-        const uint32_t zz = fdiv(t1, s.fd_ny);
-        const int32_t y = (int32_t)(t1 - zz * (uint32_t)s.ny), z = (int32_t)zz;
-        const int32_t rv = rank[v];
-        i128 d = 0;
-#define NB(cond, w, cap) if (cond) { const i128 q = qfix(cap, F); d += rank[w] > rv ? q : -q; }
-        NB(z > 0, v - s.P, s.cz[v - s.P]);
-        NB(y > 0, v - s.nx, s.cy[v - s.nx]);
-        NB(x > 0, v - 1, s.cx[v - 1]);
-        NB(x < s.nx - 1, v + 1, s.cx[v]);
-        NB(y < s.ny - 1, v + s.nx, s.cy[v]);
-        NB(z < s.nz - 1, v + s.P, s.cz[v]);
-#undef NB
-        const i128 qs = qfix(s.cs[v], F);
-        d += qfix(s.ct[v], F);
-        d -= qs;
-        qcs += qs;
-        delta[rv] = d;  // straight into sweep order (a scattered 16-byte store; no gather pass)
-    }
-    tile_sum_i128(qcs, qcs_tile + blockIdx.x);
-}
-
-__global__ void __launch_bounds__(256) k_delta_sell(SellArgs s, int32_t F, const int32_t *rank, i128 *delta,
-                                                    i128 *qcs_tile)
-{
-    i128 qcs = 0;
-    const int64_t base = (int64_t)blockIdx.x * kTile;
-    for (int r = 0; r < 16; r++) {
-        const int64_t v = base + r * 256 + threadIdx.x;
-        if (v >= s.n) break;
-        const int64_t sl = v / kSell;
-        const int64_t e0 = s.slice_ptr[sl] + (v % kSell);
-        const int32_t W = (int32_t)((s.slice_ptr[sl + 1] - s.slice_ptr[sl]) / kSell);
-        const int32_t rv = rank[v];
-        i128 d = 0;
-        for (int32_t k = 0; k < W; k++) {
-            const int64_t idx = e0 + kSell * (int64_t)k;
-            const int32_t nb = s.col[idx];
-            if (nb < 0) break;
-            const i128 q = qfix(s.c[idx], F);
-            d += rank[nb] > rv ? q : -q;
-        }
-        const i128 qs = qfix(s.cs[v], F);
-        d += qfix(s.ct[v], F);
-        d -= qs;
-        qcs += qs;
-        delta[rv] = d;  // straight into sweep order
-    }
-    tile_sum_i128(qcs, qcs_tile + blockIdx.x);
-}
-
-
-void sweep_delta_stencil(const StencilArgs &s, int64_t N, int32_t F, SweepBuffers &b, cudaStream_t st)
-{
-    if (N == 0) return;
-    k_delta_stencil<<<(unsigned)sweep_ntiles(N), 256, 0, st>>>(s, N, F, b.rank, b.delta, b.tile_min);
-}
-
-void sweep_delta_sell(const SellArgs &s, int32_t F, SweepBuffers &b, cudaStream_t st)
-{
-    if (s.n == 0) return;
-    k_delta_sell<<<(unsigned)sweep_ntiles(s.n), 256, 0, st>>>(s, F, b.rank, b.delta, b.tile_min);
-}
-
 // ---------------------------------------------------------------------------
 // scan + argmin
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_delta_tile_sum(const i128 *delta, int64_t n, i128 *tile_sum)
+__global__ void __launch_bounds__(256) k_delta_tile_sum(const i128 *delta, const int32_t *ord, int64_t n,
+                                                        i128 *tile_sum)
 {
     i128 acc = 0;
     const int64_t base = (int64_t)blockIdx.x * kTile;
     for (int r = 0; r < 16; r++) {
         const int64_t i = base + r * 256 + threadIdx.x;
-        if (i < n) acc += delta[i];
+        if (i < n) acc += delta[ord[i]];  // delta in id order, gathered in sweep order
     }
     tile_sum_i128(acc, tile_sum + blockIdx.x);
 }
@@ -488,8 +487,8 @@ __device__ __forceinline__ bool lex_less(i128 a, int64_t ia, i128 b, int64_t ib)
 }
 
 // Per tile: inclusive prefixes P_{i+1} = prefix + delta_0..i, first minimum.
-__global__ void __launch_bounds__(256) k_tile_argmin(const i128 *delta, int64_t n, const i128 *tile_prefix,
-                                                     i128 *tile_min, int64_t *tile_arg)
+__global__ void __launch_bounds__(256) k_tile_argmin(const i128 *delta, const int32_t *ord, int64_t n,
+                                                     const i128 *tile_prefix, i128 *tile_min, int64_t *tile_arg)
 {
     // thread t owns the 16 consecutive prefixes base + 16t .. +15: its delta
     // sum, ONE block-wide exclusive scan of those sums, then a second
@@ -500,10 +499,12 @@ __global__ void __launch_bounds__(256) k_tile_argmin(const i128 *delta, int64_t 
     __shared__ int64_t sarg[8];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t t0 = (int64_t)blockIdx.x * kTile + 16 * (int64_t)threadIdx.x;
-    i128 own = 0;
-#pragma unroll 4
-    for (int q = 0; q < 16; q++)
-        if (t0 + q < n) own += delta[t0 + q];
+    i128 own = 0, dl[16];
+#pragma unroll
+    for (int q = 0; q < 16; q++) {
+        dl[q] = t0 + q < n ? delta[ord[t0 + q]] : (i128)0;
+        own += dl[q];
+    }
     i128 inc = own;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -517,11 +518,11 @@ __global__ void __launch_bounds__(256) k_tile_argmin(const i128 *delta, int64_t 
     i128 P = tile_prefix[blockIdx.x] + wpre + inc - own;  // P_{t0}
     i128 best = (i128)(((unsigned __int128)1 << 127) - 1);  // +infinity
     int64_t barg = INT64_MAX;
-#pragma unroll 4
+#pragma unroll
     for (int q = 0; q < 16; q++) {
         const int64_t i = t0 + q;
         if (i < n) {
-            P += delta[i];  // P_{i+1}
+            P += dl[q];  // P_{i+1}
             if (lex_less(P, i + 1, best, barg)) { best = P; barg = i + 1; }
         }
     }
@@ -561,16 +562,17 @@ __global__ void __launch_bounds__(256) k_final_argmin(const i128 *tile_min, cons
     }
 }
 
-void sweep_scan_argmin(SweepBuffers &b, __int128 qcst, cudaStream_t st)
+void sweep_scan_argmin(SweepBuffers &b, const int32_t *ord, __int128 qcst, cudaStream_t st)
 {
     const int64_t n = b.n, nt = sweep_ntiles(n);
-    // b.tile_min holds the per-tile sums of Q(cs) from the delta kernel
+    // b.tile_min holds the per-tile sums of Q(cs) from the prep kernel
     i128 *qcs_tile = b.tile_min;
     i128 *p0 = b.delta + n;        // two spare slots at the end of delta
     i128 *pk = b.delta + n + 1;
-    if (nt > 0) k_delta_tile_sum<<<(unsigned)nt, 256, 0, st>>>(b.delta, n, b.tile_sum);
+    if (nt > 0) k_delta_tile_sum<<<(unsigned)nt, 256, 0, st>>>(b.delta, ord, n, b.tile_sum);
     k_tile_prefix<<<1, 256, 0, st>>>(b.tile_sum, qcs_tile, nt, qcst, p0);
-    if (nt > 0) k_tile_argmin<<<(unsigned)nt, 256, 0, st>>>(b.delta, n, b.tile_sum, b.tile_min, b.tile_argmin);
+    if (nt > 0)
+        k_tile_argmin<<<(unsigned)nt, 256, 0, st>>>(b.delta, ord, n, b.tile_sum, b.tile_min, b.tile_argmin);
     k_final_argmin<<<1, 256, 0, st>>>(b.tile_min, b.tile_argmin, nt, p0, b.k_out, pk);
 }
 
@@ -647,6 +649,111 @@ __global__ void __launch_bounds__(kThreads) k_side_cross_sell(SellArgs s, const 
             acc[0] = acc[0] + cr;
         }
     c3_chunk_epilogue<1>(acc, (int32_t)blockIdx.x, ra);
+}
+
+// The sweep's own side / cut pass: membership straight from the potentials —
+// v is among the first k of the order iff (x_v, v) precedes or equals the
+// k-th element (x*, v*): x_v > x* || (x_v == x* && v <= v*) — no rank array.
+__device__ __forceinline__ bool in_first_k(double xv, int64_t v, bool any, double xs, int64_t vs)
+{
+    return any && (xv > xs || (xv == xs && v <= vs));
+}
+
+__global__ void __launch_bounds__(kThreads) k_side_cross_x_stencil(StencilArgs s, int64_t N, const double *x,
+                                                                   const int32_t *ord, const int64_t *kptr,
+                                                                   uint8_t *side, RedArgs ra)
+{
+    const int64_t k = *kptr;
+    const bool any = k > 0;
+    const int64_t vs = any ? ord[k - 1] : 0;
+    const double xs = any ? canon(x[vs]) : 0.0;
+    double acc[1] = {0.0};
+    const int64_t base = (int64_t)blockIdx.x * kChunk;
+    for (int j = 0; j < 8; j++)
+        for (int e = 0; e < 2; e++) {
+            const int64_t v = base + 2 * (int64_t)threadIdx.x + 512 * j + e;
+            if (v >= N) continue;
+            const bool in = in_first_k(canon(x[v]), v, any, xs, vs);
+            side[v] = in ? 1 : 0;
+            double cr;
+            if (in) {
+                const uint32_t uv = (uint32_t)v;
+                const uint32_t t1 = fdiv(uv, s.fd_nx);
+                const int32_t xx = (int32_t)(uv - t1 * (uint32_t)s.nx);
+                const uint32_t zz = fdiv(t1, s.fd_ny);
+                const int32_t y = (int32_t)(t1 - zz * (uint32_t)s.ny), z = (int32_t)zz;
+                double a = 0.0;
+#define OUT(w) (!in_first_k(canon(x[w]), (w), any, xs, vs))
+                if (z > 0 && OUT(v - s.P)) a = a + s.cz[v - s.P];
+                if (y > 0 && OUT(v - s.nx)) a = a + s.cy[v - s.nx];
+                if (xx > 0 && OUT(v - 1)) a = a + s.cx[v - 1];
+                if (xx < s.nx - 1 && OUT(v + 1)) a = a + s.cx[v];
+                if (y < s.ny - 1 && OUT(v + s.nx)) a = a + s.cy[v];
+                if (z < s.nz - 1 && OUT(v + s.P)) a = a + s.cz[v];
+#undef OUT
+                cr = a + s.ct[v];
+            } else {
+                cr = s.cs[v];
+            }
+            acc[0] = acc[0] + cr;
+        }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        side[N] = 1;
+        side[N + 1] = 0;
+    }
+    c3_chunk_epilogue<1>(acc, (int32_t)blockIdx.x, ra);
+}
+
+__global__ void __launch_bounds__(kThreads) k_side_cross_x_sell(SellArgs s, const double *x, const int32_t *ord,
+                                                                const int64_t *kptr, const int64_t *orig,
+                                                                uint8_t *side, RedArgs ra)
+{
+    const int64_t k = *kptr;
+    const bool any = k > 0;
+    const int64_t vs = any ? ord[k - 1] : 0;
+    const double xs = any ? canon(x[vs]) : 0.0;
+    double acc[1] = {0.0};
+    const int64_t base = (int64_t)blockIdx.x * kChunk;
+    for (int j = 0; j < 8; j++)
+        for (int e = 0; e < 2; e++) {
+            const int64_t v = base + 2 * (int64_t)threadIdx.x + 512 * j + e;
+            if (v >= s.n) continue;
+            const bool in = in_first_k(canon(x[v]), v, any, xs, vs);
+            side[orig[v]] = in ? 1 : 0;
+            double cr;
+            if (in) {
+                const int64_t sl = v / kSell;
+                const int64_t e0 = s.slice_ptr[sl] + (v % kSell);
+                const int32_t W = (int32_t)((s.slice_ptr[sl + 1] - s.slice_ptr[sl]) / kSell);
+                double a = 0.0;
+                for (int32_t kk = 0; kk < W; kk++) {
+                    const int64_t idx = e0 + kSell * (int64_t)kk;
+                    const int32_t u = s.col[idx];
+                    if (u < 0) break;
+                    if (!in_first_k(canon(x[u]), u, any, xs, vs)) a = a + s.c[idx];
+                }
+                cr = a + s.ct[v];
+            } else {
+                cr = s.cs[v];
+            }
+            acc[0] = acc[0] + cr;
+        }
+    c3_chunk_epilogue<1>(acc, (int32_t)blockIdx.x, ra);
+}
+
+void sweep_side_cross_x_stencil(const StencilArgs &s, int64_t N, const double *x, const int32_t *ord, SweepBuffers &b,
+                                const RedArgs &ra, cudaStream_t st)
+{
+    k_side_cross_x_stencil<<<(unsigned)((N + kChunk - 1) / kChunk), kThreads, 0, st>>>(s, N, x, ord, b.k_out,
+                                                                                      b.side, ra);
+}
+
+void sweep_side_cross_x_sell(const SellArgs &s, const double *x, const int32_t *ord, const int64_t *orig,
+                             SweepBuffers &b, const RedArgs &ra, cudaStream_t st)
+{
+    if (s.n == 0) return;
+    k_side_cross_x_sell<<<(unsigned)((s.n + kChunk - 1) / kChunk), kThreads, 0, st>>>(s, x, ord, b.k_out, orig,
+                                                                                     b.side, ra);
 }
 
 void sweep_side_cross_stencil(const StencilArgs &s, int64_t N, SweepBuffers &b, const RedArgs &ra, cudaStream_t st)
