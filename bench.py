@@ -196,13 +196,16 @@ def main():
                     help="reference arm: z-planes of the workload per step (bounded so K steps end in minutes)")
     ap.add_argument("--ref-T", type=int, default=3)
     ap.add_argument("--cpu-T", type=int, default=3, help="cpu_baseline: IRLS steps after x^(0) on the whole graph")
-    ap.add_argument("--loop-mode", type=int, default=0)
+    ap.add_argument("--loop-mode", type=int, default=0,
+                    help="0: CUDA graphs with device-side loops (NCCL / peer stores captured on N > 1); 1: host loop")
     ap.add_argument("--no-two-level", action="store_true")
     ap.add_argument("--no-fixed-point-exit", action="store_true")
     ap.add_argument("--cg-variant", default="hs", choices=["hs", "cg"],
                     help="PCG form: Hestenes-Stiefel (default) or Chronopoulos-Gear (one reduction per iteration)")
-    ap.add_argument("--p2p", type=int, default=0, choices=[0, 1],
-                    help="N>1: per-iteration collectives over peer memory (irls_options.p2p) instead of NCCL")
+    ap.add_argument("--p2p", type=int, default=1, choices=[0, 1],
+                    help="N>1: per-iteration collectives over peer memory (irls_options.p2p: slot sums and the z "
+                         "halo stored by the kernels that produce them; falls back to NCCL if the peer mapping "
+                         "fails at create) or, 0, NCCL")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -260,7 +263,24 @@ def main():
         return float(t.item())
 
     # ---- device-resident value -------------------------------------------
-    m = I.MinCut.from_spec(spec, opts, comm)
+    m, p2p_note = None, None
+    try:
+        m = I.MinCut.from_spec(spec, opts, comm)
+        ok = 1
+    except I.IrlsError as e:
+        if world == 1 or not args.p2p:
+            raise
+        ok, p2p_note = 0, f"p2p create failed ({e}); NCCL collectives used"
+    if world > 1 and args.p2p:
+        t = torch.tensor([ok], dtype=torch.int32, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        if int(t.item()) == 0:  # every rank falls back together (collective create)
+            if m is not None:
+                m.close()
+            args.p2p = 0
+            p2p_note = p2p_note or "a peer's p2p create failed; NCCL collectives used"
+            opts = I.options(T=T, loop_mode=args.loop_mode, p2p=0, cg_variant=cgv)
+            m = I.MinCut.from_spec(spec, opts, fresh_comm())
     st = m.irls_get_stats()
     n_links = st["n_links"]
     for _ in range(args.warmup):
@@ -466,8 +486,9 @@ def main():
                    "cg_iters_per_step": iters_per_step[-1], "time_to_cut_ms": ms / args.steps,
                    "l2": "inputs (8.6 GB working set) larger than the 126 MB L2; no flush",
                    "parallelism": f"z-slab x{world}", "cut_value": cut, "k": k,
-                   "cg_iter_ms_kernels": cg_iter_ms, "loop_mode": "graph" if (args.loop_mode == 0 and world == 1) or args.loop_mode == 2 else "host",
+                   "cg_iter_ms_kernels": cg_iter_ms, "loop_mode": "host" if args.loop_mode == 1 else "graph",
                    "collectives": "none (1 rank)" if world == 1 else ("peer memory" if args.p2p else "nccl"),
+                   "collectives_note": p2p_note,
                    "cg_variant": "Chronopoulos-Gear" if args.cg_variant == "cg" else "Hestenes-Stiefel"},
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                      "traffic": traffic, "traffic_note": "ncu dram__bytes_read+write per K3 launch "

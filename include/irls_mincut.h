@@ -65,11 +65,13 @@ typedef enum {
 } irls_status;
 
 typedef enum { IRLS_NORM_PRECONDITIONED = 0, IRLS_NORM_UNPRECONDITIONED = 1 } irls_cg_norm;
-/* GRAPH: CUDA graphs with device-side WHILE loops on one rank (multi-rank
- * contexts fall back to the host loop: one 4-byte readback per CG
- * iteration); GRAPH_NCCL: graphs also on a communicator, the NCCL
- * collectives captured inside the loop bodies (no host round trip per
- * iteration; exercised on one GPU through a 1-rank communicator). */
+/* GRAPH (default): CUDA graphs with device-side WHILE loops — on a
+ * communicator the NCCL collectives are captured inside the loop bodies
+ * (with p2p only the per-solve ones: the per-iteration exchanges are peer
+ * stores), so there is no host round trip per CG iteration; GRAPH_NCCL: the
+ * same (kept for compatibility); HOST: a host loop with one 4-byte readback
+ * of the device stopping flag per CG iteration (every kernel a plain launch,
+ * visible to profilers). */
 typedef enum { IRLS_LOOP_GRAPH = 0, IRLS_LOOP_HOST = 1, IRLS_LOOP_GRAPH_NCCL = 2 } irls_loop_mode;
 /* PCG form (A31): Hestenes-Stiefel (O5, two reductions per iteration) or
  * Chronopoulos-Gear (O5': one reduction per iteration,
@@ -367,6 +369,18 @@ irls_status irls_plan_stencil(int32_t nx, int32_t ny, int32_t nz, int32_t world,
  * [lo, hi) = the chunks of C3 groups [g0, g1) = [8r/W, 8(r+1)/W); W > 1 needs
  * every rank to own >= 1 chunk (else IRLS_ERR_INVALID_ARGUMENT). */
 irls_status irls_plan_csr(int64_t nr, int32_t world, int32_t rank, int64_t *lo, int64_t *hi, int32_t *g0, int32_t *g1);
+/* Host-only: the halo of id strip `rank` over
+ * the REDUCED adjacency (nr non-terminals, aptr[nr+1], aidx ascending per row,
+ * terminals removed), as irls_mincut_create_csr builds it: lo_hi[2] = the
+ * strip [lo, hi); ghosts (ascending global ids, grouped by owner) with
+ * recv_off[world+1] the per-owner ranges; send_idx (local ids, ascending per
+ * peer) with send_off[world+1] the per-peer ranges.  ghosts / send_idx are
+ * filled only when non-NULL and large enough (ghosts_cap, send_cap entries;
+ * call once with NULL to learn recv_off[world] / send_off[world]).  Entry i of
+ * rank q's send list to rank r lands at ghost slot recv_off_r[q] + i of r. */
+irls_status irls_csr_halo_plan(int64_t nr, const int64_t *aptr, const int32_t *aidx, int32_t world, int32_t rank,
+                               int64_t *lo_hi, int64_t *recv_off, int64_t *send_off, int32_t *ghosts,
+                               int64_t ghosts_cap, int32_t *send_idx, int64_t send_cap);
 /* Halo plan of rank `rank`'s z-slab: element offsets relative to its first
  * owned node (send_lo/send_hi: boundary planes sent to peer_lo/peer_hi;
  * recv_lo/recv_hi: ghost planes received from them), count = nx*ny values

@@ -719,8 +719,9 @@ static irls_status build_graph_multi(irls_ctx *c, int mode)
 static bool graph_mode(const irls_ctx *c)
 {
     if (c->vg) return false;
-    if (!c->multi) return c->opt.loop_mode == IRLS_LOOP_GRAPH || c->opt.loop_mode == IRLS_LOOP_GRAPH_NCCL;
-    return c->opt.loop_mode == IRLS_LOOP_GRAPH_NCCL;
+    // a communicator: the NCCL calls (or, with p2p, the per-solve ones only)
+    // are captured into the graphs — no host round trip per CG iteration
+    return c->opt.loop_mode == IRLS_LOOP_GRAPH || c->opt.loop_mode == IRLS_LOOP_GRAPH_NCCL;
 }
 
 static irls_status enqueue_solve(Ranks &R, int mode)

@@ -73,6 +73,22 @@ irls_status build_blocks(irls_ctx *c, NB nbr)
     if ((int64_t)bnode.size() != n) return fail(c, IRLS_ERR_CUDA, "block partition does not cover the rank");
     const int64_t nblk = (int64_t)bptr.size();
     bptr.push_back((int32_t)n);
+    {   // storage order: decreasing block size (the blocks are independent, so
+        // their order changes no bit); a warp's blocks are then alike
+        std::vector<int32_t> order((size_t)nblk);
+        for (int64_t b = 0; b < nblk; b++) order[b] = (int32_t)b;
+        std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b2) {
+            return bptr[a + 1] - bptr[a] > bptr[b2 + 1] - bptr[b2];
+        });
+        std::vector<int32_t> sp((size_t)nblk + 1, 0), sn;
+        sn.reserve((size_t)n);
+        for (int64_t b = 0; b < nblk; b++) {
+            sn.insert(sn.end(), bnode.begin() + bptr[order[b]], bnode.begin() + bptr[order[b] + 1]);
+            sp[b + 1] = (int32_t)sn.size();
+        }
+        bptr.swap(sp);
+        bnode.swap(sn);
+    }
     std::vector<int32_t> pos((size_t)std::max<int64_t>(n, 1)), blk((size_t)std::max<int64_t>(n, 1));
     for (int64_t b = 0; b < nblk; b++)
         for (int32_t i = bptr[b]; i < bptr[b + 1]; i++) {
@@ -81,7 +97,6 @@ irls_status build_blocks(irls_ctx *c, NB nbr)
         }
     // envelopes and in-block lower-neighbour entries, per position
     std::vector<int32_t> bfirst((size_t)std::max<int64_t>(n, 1)), ecount((size_t)n + 1, 0);
-    std::vector<int64_t> boff((size_t)n + 1, 0);
     parallel_for(nblk, [&](int, int64_t a, int64_t bb) {
         for (int64_t b = a; b < bb; b++)
             for (int32_t i = bptr[b]; i < bptr[b + 1]; i++) {
@@ -96,17 +111,32 @@ irls_status build_blocks(irls_ctx *c, NB nbr)
             }
     });
     int32_t m_max = 0;
-    int64_t env_max = 0;
     for (int64_t b = 0; b < nblk; b++) {
-        int64_t env = 0;
-        for (int32_t i = bptr[b]; i < bptr[b + 1]; i++) {
-            if (i > bptr[b] && bfirst[i] < bfirst[i - 1])
+        for (int32_t i = bptr[b] + 1; i < bptr[b + 1]; i++)
+            if (bfirst[i] < bfirst[i - 1])
                 return fail(c, IRLS_ERR_CUDA, "block envelope not monotone (A32 partition broken)");
-            env += (i - bptr[b]) - bfirst[i];
-            boff[i + 1] = boff[i] + (i - bptr[b]) - bfirst[i];
-        }
         m_max = std::max(m_max, bptr[b + 1] - bptr[b]);
-        env_max = std::max(env_max, env);
+    }
+    // lane groups of 32 consecutive blocks: row i of group G spans the union
+    // [min over the lanes of f_i, i) of their envelopes
+    const int64_t nG = (nblk + 31) / 32;
+    std::vector<int64_t> gL((size_t)nG + 1, 0), gR((size_t)nG + 1, 0);
+    std::vector<int32_t> rowF, rowOff;
+    for (int64_t G = 0; G < nG; G++) {
+        const int64_t bl0 = 32 * G, bl1 = std::min<int64_t>(nblk, 32 * G + 32);
+        int32_t M = 0;
+        for (int64_t b = bl0; b < bl1; b++) M = std::max(M, bptr[b + 1] - bptr[b]);
+        int64_t off = 0;
+        for (int32_t i = 0; i < M; i++) {
+            int32_t F = i;
+            for (int64_t b = bl0; b < bl1; b++)
+                if (i < bptr[b + 1] - bptr[b]) F = std::min(F, bfirst[bptr[b] + i]);
+            rowF.push_back(F);
+            rowOff.push_back((int32_t)off);
+            off += i - F;
+        }
+        gR[G + 1] = gR[G] + M;
+        gL[G + 1] = gL[G] + off;
     }
     std::vector<int32_t> eptr((size_t)n + 1, 0);
     for (int64_t i = 0; i < n; i++) eptr[i + 1] = eptr[i] + ecount[i + 1];
@@ -127,20 +157,21 @@ irls_status build_blocks(irls_ctx *c, NB nbr)
     BlockArgs &A = c->blk;
     A.nblk = nblk;
     A.m_max = m_max;
-    A.env_max = env_max;
-    if (block_smem_per_cta(A) > 220 * 1024)
-        return fail(c, IRLS_ERR_INVALID_ARGUMENT, "block envelope too large for shared memory (lower block_size)");
-    int32_t *d_bptr = dalloc<int32_t>(c, nblk + 1), *d_bnode = dalloc<int32_t>(c, n), *d_bfirst = dalloc<int32_t>(c, n);
-    int32_t *d_eptr = dalloc<int32_t>(c, n + 1), *d_ecol = dalloc<int32_t>(c, std::max<int32_t>(eptr[n], 1));
-    int64_t *d_boff = dalloc<int64_t>(c, n + 1);
-    const double **d_eg = dalloc<const double *>(c, std::max<int32_t>(eptr[n], 1));
-    A.L = dalloc<double>(c, std::max<int64_t>(boff[n], 1));
-    A.Dd = dalloc<double>(c, n);
+    if (m_max > 256) return fail(c, IRLS_ERR_INVALID_ARGUMENT, "block larger than 256 nodes");
+    const int32_t ne = std::max<int32_t>(eptr[n], 1);
+    int32_t *d_bptr = dalloc<int32_t>(c, nblk + 1), *d_bnode = dalloc<int32_t>(c, n);
+    int32_t *d_eptr = dalloc<int32_t>(c, n + 1), *d_ecol = dalloc<int32_t>(c, ne);
+    const double **d_eg = dalloc<const double *>(c, ne);
+    int64_t *d_gL = dalloc<int64_t>(c, nG + 1), *d_gR = dalloc<int64_t>(c, nG + 1);
+    int32_t *d_rowF = dalloc<int32_t>(c, std::max<int64_t>((int64_t)rowF.size(), 1));
+    int32_t *d_rowOff = dalloc<int32_t>(c, std::max<int64_t>((int64_t)rowOff.size(), 1));
+    A.L = dalloc<double>(c, 32 * std::max<int64_t>(gL[nG], 1));
+    A.Dd = dalloc<double>(c, 32 * std::max<int64_t>(gR[nG], 1));
     A.mb = dalloc<double>(c, n);
     if (!c->gs_diag) c->gs_diag = dalloc<double>(c, (int64_t)c->nchunks * kChunk);
     if (!c->gt_diag) c->gt_diag = dalloc<double>(c, (int64_t)c->nchunks * kChunk);
-    if (!d_bptr || !d_bnode || !d_bfirst || !d_eptr || !d_ecol || !d_boff || !d_eg || !A.L || !A.Dd || !A.mb ||
-        !c->gs_diag || !c->gt_diag)
+    if (!d_bptr || !d_bnode || !d_eptr || !d_ecol || !d_eg || !d_gL || !d_gR || !d_rowF || !d_rowOff || !A.L ||
+        !A.Dd || !A.mb || !c->gs_diag || !c->gt_diag)
         return fail(c, IRLS_ERR_OOM, "block preconditioner arrays");
     cudaError_t e = cudaSuccess;
     auto up = [&](void *dst, const void *src, size_t bytes) {
@@ -148,20 +179,23 @@ irls_status build_blocks(irls_ctx *c, NB nbr)
     };
     up(d_bptr, bptr.data(), sizeof(int32_t) * (nblk + 1));
     up(d_bnode, bnode.data(), sizeof(int32_t) * n);
-    up(d_bfirst, bfirst.data(), sizeof(int32_t) * n);
     up(d_eptr, eptr.data(), sizeof(int32_t) * (n + 1));
     up(d_ecol, ecol.data(), sizeof(int32_t) * eptr[n]);
-    up(d_boff, boff.data(), sizeof(int64_t) * (n + 1));
     up(d_eg, eg.data(), sizeof(const double *) * eptr[n]);
+    up(d_gL, gL.data(), sizeof(int64_t) * (nG + 1));
+    up(d_gR, gR.data(), sizeof(int64_t) * (nG + 1));
+    up(d_rowF, rowF.data(), sizeof(int32_t) * rowF.size());
+    up(d_rowOff, rowOff.data(), sizeof(int32_t) * rowOff.size());
     if (e != cudaSuccess) return fail(c, IRLS_ERR_CUDA, std::string("block upload: ") + cudaGetErrorString(e));
     A.bptr = d_bptr;
     A.bnode = d_bnode;
-    A.bfirst = d_bfirst;
     A.eptr = d_eptr;
     A.ecol = d_ecol;
-    A.boff = d_boff;
     A.eg = d_eg;
-    block_prepare(A);
+    A.gL = d_gL;
+    A.gR = d_gR;
+    A.rowF = d_rowF;
+    A.rowOff = d_rowOff;
     return IRLS_OK;
 }
 

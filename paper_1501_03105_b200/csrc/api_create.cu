@@ -425,6 +425,75 @@ struct Ent {
     double w;
 };
 
+static bool csr_strips(int64_t nr, int world, std::vector<int64_t> &lo);
+
+// The halo of one id strip: the ghosts are the neighbours
+// owned by other ranks, in ascending global id (hence grouped by owner);
+// by the symmetry of G~ owned row u goes to rank q iff u has a neighbour
+// owned by q, in ascending u — exactly the order of q's ghost block, so the
+// lists need no communication.  aptr/aidx: the reduced adjacency (ascending).
+static void csr_strip_halo(const int64_t *aptr, const int32_t *aidx, const std::vector<int64_t> &rank_lo, int rank,
+                           std::vector<int32_t> &ghosts, std::vector<int64_t> &recv_off, std::vector<int64_t> &send_off,
+                           std::vector<int32_t> &lsend)
+{
+    const int W = (int)rank_lo.size() - 1;
+    const int64_t lo = rank_lo[rank], hi = rank_lo[rank + 1];
+    auto owner = [&](int64_t v) {
+        return (int)(std::upper_bound(rank_lo.begin(), rank_lo.end() - 1, v) - rank_lo.begin()) - 1;
+    };
+    ghosts.clear();
+    for (int64_t r = lo; r < hi; r++)
+        for (int64_t e = aptr[r]; e < aptr[r + 1]; e++)
+            if (aidx[e] < lo || aidx[e] >= hi) ghosts.push_back(aidx[e]);
+    std::sort(ghosts.begin(), ghosts.end());
+    ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
+    recv_off.assign(W + 1, 0);
+    for (int32_t v : ghosts) recv_off[owner(v) + 1]++;
+    for (int q = 0; q < W; q++) recv_off[q + 1] += recv_off[q];
+    std::vector<std::vector<int32_t>> sendq(W);
+    for (int64_t r = lo; r < hi; r++) {
+        int peers[16], np = 0;
+        for (int64_t e = aptr[r]; e < aptr[r + 1]; e++) {
+            const int64_t v = aidx[e];
+            if (v >= lo && v < hi) continue;
+            const int q = owner(v);
+            bool seen = false;
+            for (int i = 0; i < np; i++) seen |= peers[i] == q;
+            if (!seen && np < 16) peers[np++] = q;
+        }
+        for (int i = 0; i < np; i++) sendq[peers[i]].push_back((int32_t)(r - lo));
+    }
+    send_off.assign(W + 1, 0);
+    lsend.clear();
+    for (int q = 0; q < W; q++) {
+        send_off[q + 1] = send_off[q] + (int64_t)sendq[q].size();
+        lsend.insert(lsend.end(), sendq[q].begin(), sendq[q].end());
+    }
+}
+
+extern "C" irls_status irls_csr_halo_plan(int64_t nr, const int64_t *aptr, const int32_t *aidx, int32_t world,
+                                          int32_t rank, int64_t *lo_hi, int64_t *recv_off, int64_t *send_off,
+                                          int32_t *ghosts, int64_t ghosts_cap, int32_t *send_idx, int64_t send_cap)
+{
+    if (nr < 0 || !aptr || (!aidx && nr > 0 && aptr[nr] > 0) || world < 1 || rank < 0 || rank >= world || !lo_hi ||
+        !recv_off || !send_off)
+        return IRLS_ERR_INVALID_ARGUMENT;
+    std::vector<int64_t> rank_lo;
+    if (!csr_strips(nr, world, rank_lo)) return IRLS_ERR_INVALID_ARGUMENT;
+    std::vector<int32_t> g, ls;
+    std::vector<int64_t> ro, so;
+    csr_strip_halo(aptr, aidx, rank_lo, rank, g, ro, so, ls);
+    lo_hi[0] = rank_lo[rank];
+    lo_hi[1] = rank_lo[rank + 1];
+    for (int q = 0; q <= world; q++) {
+        recv_off[q] = ro[q];
+        send_off[q] = so[q];
+    }
+    if (ghosts && (int64_t)g.size() <= ghosts_cap) std::copy(g.begin(), g.end(), ghosts);
+    if (send_idx && (int64_t)ls.size() <= send_cap) std::copy(ls.begin(), ls.end(), send_idx);
+    return IRLS_OK;
+}
+
 irls_status create_csr_impl(irls_ctx **out, const irls_comm_desc *comm, int64_t n, const int64_t *row_ptr,
                                    const int32_t *col, const double *w, int64_t s_, int64_t t_, const irls_options *opt,
                                    irls_vgroup *vg);
@@ -740,38 +809,10 @@ irls_status create_csr_impl(irls_ctx **out, const irls_comm_desc *comm, int64_t 
     std::vector<double> lscap;
     int64_t lwmax = 0;
     if (!st && c->multi) {
-        const int64_t lo = c->lo, hi = c->lo + c->n_own, W = c->world;
-        auto owner = [&](int64_t v) {
-            return (int)(std::upper_bound(c->rank_lo.begin(), c->rank_lo.end() - 1, v) - c->rank_lo.begin()) - 1;
-        };
+        const int64_t lo = c->lo, hi = c->lo + c->n_own;
         std::vector<int32_t> ghosts;
-        for (int64_t r = lo; r < hi; r++)
-            for (int64_t e = aptr[r]; e < aptr[r + 1]; e++)
-                if (aidx[e] < lo || aidx[e] >= hi) ghosts.push_back(aidx[e]);
-        std::sort(ghosts.begin(), ghosts.end());
-        ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
+        csr_strip_halo(aptr.data(), aidx.data(), c->rank_lo, c->rank, ghosts, c->recv_off, c->send_off, lsend);
         c->n_ghost = (int64_t)ghosts.size();
-        c->recv_off.assign(W + 1, 0);
-        for (int32_t v : ghosts) c->recv_off[owner(v) + 1]++;
-        for (int q = 0; q < W; q++) c->recv_off[q + 1] += c->recv_off[q];
-        std::vector<std::vector<int32_t>> sendq(W);
-        for (int64_t r = lo; r < hi; r++) {
-            int peers[16], np = 0;
-            for (int64_t e = aptr[r]; e < aptr[r + 1]; e++) {
-                const int64_t v = aidx[e];
-                if (v >= lo && v < hi) continue;
-                const int q = owner(v);
-                bool seen = false;
-                for (int i = 0; i < np; i++) seen |= peers[i] == q;
-                if (!seen && np < 16) peers[np++] = q;
-            }
-            for (int i = 0; i < np; i++) sendq[peers[i]].push_back((int32_t)(r - lo));
-        }
-        c->send_off.assign(W + 1, 0);
-        for (int q = 0; q < W; q++) {
-            c->send_off[q + 1] = c->send_off[q] + (int64_t)sendq[q].size();
-            lsend.insert(lsend.end(), sendq[q].begin(), sendq[q].end());
-        }
         const int64_t nl = c->n_own, lnsl = (nl + kSell - 1) / kSell;
         lsptr.assign(lnsl + 1, 0);
         for (int64_t sl = 0; sl < lnsl; sl++) {

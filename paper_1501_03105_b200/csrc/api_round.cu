@@ -25,6 +25,8 @@ static irls_status alloc_sweep(irls_ctx *c)
     b.digit_hist = dalloc<unsigned long long>(c, 8 * 256);
     b.delta = dalloc<__int128>(c, n + 2);
     b.tile_sum = dalloc<__int128>(c, nt);
+    b.tile_incl = dalloc<__int128>(c, nt);
+    b.qcs_tile = dalloc<__int128>(c, nt);
     b.tile_min = dalloc<__int128>(c, nt);
     b.tile_argmin = dalloc<int64_t>(c, nt);
     b.flags = dalloc<int32_t>(c, 4);
@@ -32,7 +34,7 @@ static irls_status alloc_sweep(irls_ctx *c)
     b.side = dalloc<uint8_t>(c, c->n_total);
     c->order_out = dalloc<int32_t>(c, n);
     if (!b.keys || !b.keys_alt || !b.vals || !b.vals_alt || !b.tile_hist || !b.tile_off || !b.scan_tmp ||
-        !b.digit_hist || !b.delta || !b.tile_sum || !b.tile_min || !b.tile_argmin || !b.flags || !b.k_out || !b.side ||
+        !b.digit_hist || !b.delta || !b.tile_sum || !b.tile_incl || !b.qcs_tile || !b.tile_min || !b.tile_argmin || !b.flags || !b.k_out || !b.side ||
         !c->order_out)
         return fail(c, IRLS_ERR_OOM, "sweep buffers");
     return IRLS_OK;
@@ -97,7 +99,7 @@ irls_status sweep_rank0(irls_ctx *c, const double *xfull, uint8_t *side, int32_t
     int32_t *ord = sweep_sort(b, st, &launches, &nan);
     if (nan) return fail(c, IRLS_ERR_BAD_POTENTIAL, "NaN in potentials");
     sweep_scan_argmin(b, ord, qfix_host(c->c_st, c->F), st);
-    launches += 4;
+    launches += 3;
     RedArgs ra;
     ra.part = c->part;
     ra.slots = c->slots_local;

@@ -12,13 +12,13 @@
 //   d_i  =  A_ii - sum_{k asc} (L_ik * L_ik) * d_k
 //   forward  y_i = r_i - sum_{k asc} L_ik * y_k ;  w_i = y_i / d_i
 //   backward z_k = w_k - sum_{i desc} L_ik * z_i
-// executed column by column (right-looking) by the lanes of one warp per
-// block: entry (i, j) receives its updates in ascending step order, which is
-// the definition's order.  Entries outside a row's envelope [f_i, i) are
-// exact zeros of the dense algorithm and are skipped (bitwise no-ops).
-// The envelope first columns f_i are non-decreasing in block order (a BFS
-// node's first in-block neighbour is the node that discovered it), so the
-// rows touched by step k are the contiguous range (k, l_k].
+// executed literally by rows, one thread per block, the 32 blocks of a warp
+// stored interleaved (one 256-byte access per band element).  Row i is
+// stored over [rowF, i), the union of the warp's 32 envelopes; the entries
+// outside a block's own envelope are exact zeros of the dense algorithm (A32:
+// every update with them is a bitwise no-op), so the bits are the dense
+// definition's, i.e. the oracle's.  For blocks of at most 16 nodes the
+// right-hand sides live in registers (fully unrolled recurrences).
 //
 // KR then forms the C3 reductions of the solve (START: <r,z>, <z,z>, <r,r>,
 // <M^-1 b, M^-1 b>, <b,b>; per iteration: <r,z>, <z,z>, <r,r>) in the
@@ -28,166 +28,164 @@
 
 namespace irls {
 
-// Dynamic shared memory per warp: [env_max doubles][m_max doubles (d or acc)]
-// [m_max doubles (acc2)] [m_max int32 (f)] [m_max int32 (row offsets)].
-__host__ __device__ inline size_t blk_warp_bytes(const BlockArgs &b)
-{
-    return sizeof(double) * ((size_t)b.env_max + 2 * (size_t)b.m_max) + sizeof(int32_t) * 2 * (size_t)b.m_max;
-}
-
-struct WarpSmem {
-    double *env, *a0, *a1;
-    int32_t *f, *ro;
+struct Lane {
+    int32_t p0, m;
+    int64_t R0;
+    double *L;   // &band[G][0][l]
+    double *Dd;  // &pivots[G][0][l]
 };
 
-__device__ __forceinline__ WarpSmem warp_smem(const BlockArgs &b, unsigned char *dyn, int w)
+__device__ __forceinline__ Lane lane_of(const BlockArgs &b, int64_t blk)
 {
-    unsigned char *p = dyn + (size_t)w * ((blk_warp_bytes(b) + 15) & ~(size_t)15);
-    WarpSmem s;
-    s.env = reinterpret_cast<double *>(p);
-    s.a0 = s.env + b.env_max;
-    s.a1 = s.a0 + b.m_max;
-    s.f = reinterpret_cast<int32_t *>(s.a1 + b.m_max);
-    s.ro = s.f + b.m_max;
-    return s;
+    Lane t;
+    const int64_t G = blk >> 5, l = blk & 31;
+    t.p0 = b.bptr[blk];
+    t.m = b.bptr[blk + 1] - t.p0;
+    t.R0 = b.gR[G];
+    t.L = b.L + 32 * b.gL[G] + l;
+    t.Dd = b.Dd + 32 * t.R0 + l;
+    return t;
 }
 
-// KF: factor every block (one warp per block).  D: the assembled diagonal.
-__global__ void k_block_factor(BlockArgs b, const double *__restrict__ D, const int32_t *frozen)
+// row i of the lane's block: element (i, k) at row[32 k]
+__device__ __forceinline__ double *band_row(const BlockArgs &b, const Lane &t, int i, int32_t &F)
+{
+    F = b.rowF[t.R0 + i];
+    return t.L + 32 * ((int64_t)b.rowOff[t.R0 + i] - F);
+}
+
+// KF: factor every block (one thread per block).  D: the assembled diagonal.
+__global__ void __launch_bounds__(128) k_block_factor(BlockArgs b, const double *__restrict__ D, const int32_t *frozen)
 {
     if (frozen && *(const volatile int32_t *)frozen) return;
-    extern __shared__ __align__(16) unsigned char blk_dyn[];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t blk = (int64_t)blockIdx.x * (blockDim.x >> 5) + w;
+    const int64_t blk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (blk >= b.nblk) return;
-    const WarpSmem s = warp_smem(b, blk_dyn, w);
-    const int32_t p0 = b.bptr[blk], m = b.bptr[blk + 1] - p0;
-    const int64_t e0 = b.boff[p0];
-    const int32_t ne = (int32_t)(b.boff[p0 + m] - e0);
-    for (int e = lane; e < ne; e += 32) s.env[e] = 0.0;
-    for (int i = lane; i < m; i += 32) {
-        const int32_t fi = b.bfirst[p0 + i];
-        s.f[i] = fi;
-        s.ro[i] = (int32_t)(b.boff[p0 + i] - e0) - fi;  // env index of (i, j) = ro[i] + j
-        s.a0[i] = D[b.bnode[p0 + i]];
-    }
-    __syncwarp();
-    for (int i = lane; i < m; i += 32)  // A_ij = -g_uv for the in-block lower neighbours
-        for (int32_t e = b.eptr[p0 + i]; e < b.eptr[p0 + i + 1]; e++) s.env[s.ro[i] + b.ecol[e]] = -*b.eg[e];
-    __syncwarp();
-    for (int j = 0; j < m; j++) {
-        const double dj = s.a0[j];  // final: every step k < j has updated it
-        for (int i = j + 1 + lane; i < m; i += 32)
-            if (s.f[i] <= j) s.env[s.ro[i] + j] = s.env[s.ro[i] + j] / dj;  // L_ij
-        __syncwarp();
-        for (int i = j + 1 + lane; i < m; i += 32) {
-            if (s.f[i] > j) continue;
-            const double lij = s.env[s.ro[i] + j];
-            double *row = s.env + s.ro[i];
-            for (int k = j + 1; k < i; k++) {  // f_k <= f_i <= j: L_kj inside k's envelope
-                const double t = lij * s.env[s.ro[k] + j];
-                row[k] = row[k] - t * dj;
+    const Lane t = lane_of(b, blk);
+    for (int i = 0; i < t.m; i++) {
+        int32_t F;
+        double *Li = band_row(b, t, i, F);
+        for (int k = F; k < i; k++) Li[32 * k] = 0.0;
+        for (int32_t e = b.eptr[t.p0 + i]; e < b.eptr[t.p0 + i + 1]; e++) Li[32 * b.ecol[e]] = -*b.eg[e];
+        for (int j = F; j < i; j++) {
+            int32_t Fj;
+            const double *Lj = band_row(b, t, j, Fj);
+            double s = Li[32 * j];
+            for (int k = max(F, Fj); k < j; k++) {
+                const double p = Li[32 * k] * Lj[32 * k];
+                s = s - p * t.Dd[32 * k];
             }
-            const double t = lij * lij;
-            s.a0[i] = s.a0[i] - t * dj;
+            Li[32 * j] = s / t.Dd[32 * j];
         }
-        __syncwarp();
+        double s = D[b.bnode[t.p0 + i]];
+        for (int k = F; k < i; k++) {
+            const double p = Li[32 * k] * Li[32 * k];
+            s = s - p * t.Dd[32 * k];
+        }
+        t.Dd[32 * i] = s;
     }
-    for (int e = lane; e < ne; e += 32) b.L[e0 + e] = s.env[e];
-    for (int i = lane; i < m; i += 32) b.Dd[p0 + i] = s.a0[i];
 }
 
-// Forward + diagonal + backward on acc (and acc2 when TWO), in shared memory.
-template <bool TWO>
-__device__ __forceinline__ void block_apply(const WarpSmem &s, const double *__restrict__ Dd, int m, int lane)
+// Forward + diagonal + backward on y (and y2 when TWO).  MAXM <= 16: fully
+// unrolled (registers); larger: runtime loops (local memory).
+template <bool TWO, int MAXM>
+__device__ __forceinline__ void block_apply(const BlockArgs &b, const Lane &t, double (&y)[MAXM], double (&y2)[MAXM])
 {
-    for (int k = 0; k < m; k++) {
-        __syncwarp();
-        const double yk = s.a0[k];
-        const double yk2 = TWO ? s.a1[k] : 0.0;
-        for (int i = k + 1 + lane; i < m; i += 32) {
-            if (s.f[i] > k) break;  // f non-decreasing: no later row reaches column k
-            const double l = s.env[s.ro[i] + k];
-            s.a0[i] = s.a0[i] - l * yk;
-            if (TWO) s.a1[i] = s.a1[i] - l * yk2;
+    constexpr bool UNROLL = MAXM <= 16;
+#pragma unroll
+    for (int i = 0; i < (UNROLL ? MAXM : t.m); i++) {
+        if (i < t.m) {
+            int32_t F;
+            const double *Li = band_row(b, t, i, F);
+            double a = y[i], a2 = TWO ? y2[i] : 0.0;
+#pragma unroll
+            for (int k = (UNROLL ? 0 : F); k < (UNROLL ? MAXM : i); k++) {
+                if (k >= F && k < i) {
+                    const double l = __ldcs(Li + 32 * k);
+                    a = a - l * y[k];
+                    if (TWO) a2 = a2 - l * y2[k];
+                }
+            }
+            y[i] = a;
+            if (TWO) y2[i] = a2;
         }
     }
-    __syncwarp();
-    for (int i = lane; i < m; i += 32) {
-        const double d = Dd[i];
-        s.a0[i] = s.a0[i] / d;
-        if (TWO) s.a1[i] = s.a1[i] / d;
-    }
-    for (int i = m - 1; i >= 0; i--) {
-        __syncwarp();
-        const double zi = s.a0[i];
-        const double zi2 = TWO ? s.a1[i] : 0.0;
-        const double *row = s.env + s.ro[i];
-        for (int k = s.f[i] + lane; k < i; k += 32) {
-            const double l = row[k];
-            s.a0[k] = s.a0[k] - l * zi;
-            if (TWO) s.a1[k] = s.a1[k] - l * zi2;
+#pragma unroll
+    for (int i = 0; i < (UNROLL ? MAXM : t.m); i++) {  // w = D^-1 y
+        if (i < t.m) {
+            const double d = t.Dd[32 * i];
+            y[i] = y[i] / d;
+            if (TWO) y2[i] = y2[i] / d;
         }
     }
-    __syncwarp();
-}
-
-__device__ __forceinline__ void block_load(const BlockArgs &b, const WarpSmem &s, int32_t p0, int m, int lane)
-{
-    const int64_t e0 = b.boff[p0];
-    const int32_t ne = (int32_t)(b.boff[p0 + m] - e0);
-    for (int e = lane; e < ne; e += 32) s.env[e] = __ldcs(b.L + e0 + e);
-    for (int i = lane; i < m; i += 32) {
-        const int32_t fi = b.bfirst[p0 + i];
-        s.f[i] = fi;
-        s.ro[i] = (int32_t)(b.boff[p0 + i] - e0) - fi;
+#pragma unroll
+    for (int i = (UNROLL ? MAXM : t.m) - 1; i >= 0; i--) {
+        if (i < t.m) {
+            int32_t F;
+            const double *Li = band_row(b, t, i, F);
+            const double zi = y[i], zi2 = TWO ? y2[i] : 0.0;
+#pragma unroll
+            for (int k = (UNROLL ? 0 : F); k < (UNROLL ? MAXM : i); k++) {
+                if (k >= F && k < i) {
+                    const double l = __ldcs(Li + 32 * k);
+                    y[k] = y[k] - l * zi;
+                    if (TWO) y2[k] = y2[k] - l * zi2;
+                }
+            }
+        }
     }
 }
 
 // KB0 (START): z0 = M^-1 r0 and mb = M^-1 b (b = gs), two right-hand sides.
-__global__ void k_block_solve_start(BlockArgs b, VecArgs v, const double *__restrict__ gs)
+template <int MAXM>
+__global__ void __launch_bounds__(128) k_block_solve_start(BlockArgs b, VecArgs v, const double *__restrict__ gs)
 {
     if (v.frozen && *(const volatile int32_t *)v.frozen) return;
-    extern __shared__ __align__(16) unsigned char blk_dyn[];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t blk = (int64_t)blockIdx.x * (blockDim.x >> 5) + w;
+    const int64_t blk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (blk >= b.nblk) return;
-    const WarpSmem s = warp_smem(b, blk_dyn, w);
-    const int32_t p0 = b.bptr[blk], m = b.bptr[blk + 1] - p0;
-    block_load(b, s, p0, m, lane);
-    for (int i = lane; i < m; i += 32) {
-        const int32_t u = b.bnode[p0 + i];
-        s.a0[i] = v.r[u];
-        s.a1[i] = gs[u];
+    const Lane t = lane_of(b, blk);
+    double y[MAXM], y2[MAXM];
+#pragma unroll
+    for (int i = 0; i < MAXM; i++) {
+        if (i < t.m) {
+            const int32_t u = b.bnode[t.p0 + i];
+            y[i] = v.r[u];
+            y2[i] = gs[u];
+        }
     }
-    block_apply<true>(s, b.Dd + p0, m, lane);
-    for (int i = lane; i < m; i += 32) {
-        const int32_t u = b.bnode[p0 + i];
-        v.z[u] = s.a0[i];
-        b.mb[u] = s.a1[i];
+    block_apply<true, MAXM>(b, t, y, y2);
+#pragma unroll
+    for (int i = 0; i < MAXM; i++) {
+        if (i < t.m) {
+            const int32_t u = b.bnode[t.p0 + i];
+            v.z[u] = y[i];
+            b.mb[u] = y2[i];
+        }
     }
 }
 
 // KB (iteration): r = r - alpha q (K5's update, same operation), z = M^-1 r.
-__global__ void k_block_solve_iter(BlockArgs b, VecArgs v, const DevCtrl *ctrl)
+template <int MAXM>
+__global__ void __launch_bounds__(128) k_block_solve_iter(BlockArgs b, VecArgs v, const DevCtrl *ctrl)
 {
     if (ctrl->done) return;  // breakdown after q = A p: KR sets the condition
-    extern __shared__ __align__(16) unsigned char blk_dyn[];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t blk = (int64_t)blockIdx.x * (blockDim.x >> 5) + w;
+    const int64_t blk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (blk >= b.nblk) return;
     const double alpha = ctrl->alpha;
-    const WarpSmem s = warp_smem(b, blk_dyn, w);
-    const int32_t p0 = b.bptr[blk], m = b.bptr[blk + 1] - p0;
-    block_load(b, s, p0, m, lane);
-    for (int i = lane; i < m; i += 32) {
-        const int32_t u = b.bnode[p0 + i];
-        const double r = v.r[u] - alpha * v.q[u];
-        v.r[u] = r;
-        s.a0[i] = r;
+    const Lane t = lane_of(b, blk);
+    double y[MAXM], y2[MAXM];
+#pragma unroll
+    for (int i = 0; i < MAXM; i++) {
+        if (i < t.m) {
+            const int32_t u = b.bnode[t.p0 + i];
+            const double r = v.r[u] - alpha * v.q[u];
+            v.r[u] = r;
+            y[i] = r;
+        }
     }
-    block_apply<false>(s, b.Dd + p0, m, lane);
-    for (int i = lane; i < m; i += 32) v.z[b.bnode[p0 + i]] = s.a0[i];
+    block_apply<false, MAXM>(b, t, y, y2);
+#pragma unroll
+    for (int i = 0; i < MAXM; i++)
+        if (i < t.m) v.z[b.bnode[t.p0 + i]] = y[i];
 }
 
 __device__ __forceinline__ void set_cond_b(const CondArgs &cd, const DevCtrl *c)
@@ -249,45 +247,29 @@ __global__ void __launch_bounds__(kThreads) k_block_reduce_iter(VecArgs v, RedAr
     }
 }
 
-static int blk_warps(const BlockArgs &b)
-{
-    const size_t per = (blk_warp_bytes(b) + 15) & ~(size_t)15;
-    int w = (int)std::min<size_t>(8, (200 * 1024) / std::max<size_t>(per, 1));
-    return std::max(w, 1);
-}
-
-size_t block_smem_per_cta(const BlockArgs &b)
-{
-    return (size_t)blk_warps(b) * ((blk_warp_bytes(b) + 15) & ~(size_t)15);
-}
-
-void block_prepare(const BlockArgs &b)
-{
-    const int smem = (int)block_smem_per_cta(b);
-    cudaFuncSetAttribute(k_block_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(k_block_solve_start, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(k_block_solve_iter, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-}
-
-static unsigned blk_grid(const BlockArgs &b)
-{
-    const int w = blk_warps(b);
-    return (unsigned)((b.nblk + w - 1) / w);
-}
+static unsigned blk_grid(const BlockArgs &b) { return (unsigned)((b.nblk + 127) / 128); }
 
 int launch_block_factor(const BlockArgs &b, const double *D, const int32_t *frozen, cudaStream_t st)
 {
     if (b.nblk == 0) return 0;
-    k_block_factor<<<blk_grid(b), 32 * blk_warps(b), block_smem_per_cta(b), st>>>(b, D, frozen);
+    k_block_factor<<<blk_grid(b), 128, 0, st>>>(b, D, frozen);
     return 1;
 }
+
+#define BLK_DISPATCH(KERNEL, ...)                                                        \
+    do {                                                                                 \
+        if (b.m_max <= 8) KERNEL<8><<<blk_grid(b), 128, 0, st>>>(__VA_ARGS__);           \
+        else if (b.m_max <= 16) KERNEL<16><<<blk_grid(b), 128, 0, st>>>(__VA_ARGS__);    \
+        else if (b.m_max <= 64) KERNEL<64><<<blk_grid(b), 128, 0, st>>>(__VA_ARGS__);    \
+        else KERNEL<256><<<blk_grid(b), 128, 0, st>>>(__VA_ARGS__);                      \
+    } while (0)
 
 int launch_block_start(const BlockArgs &b, const VecArgs &v, const double *gs, const RedArgs &ra,
                        const CondArgs &cd, cudaStream_t st)
 {
     int n = 0;
     if (b.nblk > 0) {
-        k_block_solve_start<<<blk_grid(b), 32 * blk_warps(b), block_smem_per_cta(b), st>>>(b, v, gs);
+        BLK_DISPATCH(k_block_solve_start, b, v, gs);
         n++;
     }
     const unsigned nb = (unsigned)((v.n_own + kChunk - 1) / kChunk);
@@ -302,7 +284,7 @@ int launch_block_iter(const BlockArgs &b, const VecArgs &v, const RedArgs &ra, c
 {
     int n = 0;
     if (b.nblk > 0) {
-        k_block_solve_iter<<<blk_grid(b), 32 * blk_warps(b), block_smem_per_cta(b), st>>>(b, v, ra.ctrl);
+        BLK_DISPATCH(k_block_solve_iter, b, v, ra.ctrl);
         n++;
     }
     const unsigned nb = (unsigned)((v.n_own + kChunk - 1) / kChunk);

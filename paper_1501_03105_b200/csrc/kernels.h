@@ -65,18 +65,25 @@ struct SellArgs {
     int64_t gbase, glow;         // strips: columns >= gbase are ghosts; the first glow ghosts have lower ids
 };
 
-// Block-Jacobi preconditioner (A32, block_jacobi.cu): blocks of positions
-// [bptr[b], bptr[b+1]); position i holds local node bnode[i]; its envelope row
-// (block-local columns [bfirst[i], i)) is L[boff[i] .. boff[i+1]); its
-// in-block lower neighbours are (ecol[e], *eg[e]) for e in [eptr[i], eptr[i+1]).
+// Block-Jacobi preconditioner (A32, block_jacobi.cu).  Blocks are stored in
+// the order of decreasing size (independent blocks: the order changes no
+// bit); block b occupies positions [bptr[b], bptr[b+1]); position i holds
+// local node bnode[i]; its in-block lower neighbours are (ecol[e], *eg[e])
+// for e in [eptr[i], eptr[i+1]).  One thread per block; the 32 blocks of a
+// lane group G = b / 32 share a row table (rows gR[G] .. gR[G+1]): row i spans
+// block-local columns [rowF, i) — the union of the 32 blocks' envelopes,
+// zero-padded (exact no-ops of the dense algorithm) — and starts rowOff band
+// elements into G's band.  Band element t of row i of lane l lives at
+// L[32 (gL[G] + rowOff + t) + l], the pivot of row i at Dd[32 (gR[G] + i) + l]:
+// a warp reads 256 contiguous bytes per element.
 struct BlockArgs {
     int64_t nblk = 0;
     int32_t m_max = 0;           // largest block
-    int64_t env_max = 0;         // largest block envelope (doubles)
-    const int32_t *bptr = nullptr, *bnode = nullptr, *bfirst = nullptr, *eptr = nullptr, *ecol = nullptr;
-    const int64_t *boff = nullptr;
+    const int32_t *bptr = nullptr, *bnode = nullptr, *eptr = nullptr, *ecol = nullptr;
     const double *const *eg = nullptr;  // the conductance of each in-block edge (device pointers)
-    double *L = nullptr, *Dd = nullptr;  // factor: envelope of the unit lower L, pivots (block order)
+    const int64_t *gL = nullptr, *gR = nullptr;  // per lane group: band start, row-table start
+    const int32_t *rowF = nullptr, *rowOff = nullptr;
+    double *L = nullptr, *Dd = nullptr;  // factor: unit lower L (band), pivots
     double *mb = nullptr;        // M^-1 b (START)
 };
 
@@ -115,8 +122,6 @@ void launch_halo_pack(const double *arr, const int32_t *idx, int64_t n, double *
 // block Jacobi (A32): KF factor per IRLS step; START: z0 = M^-1 r0, mb = M^-1 b
 // + the 5 START reductions; iteration: r -= alpha q, z = M^-1 r + the 3 RZ
 // reductions.  Return the number of kernels launched.
-size_t block_smem_per_cta(const BlockArgs &b);
-void block_prepare(const BlockArgs &b);  // once per context, outside capture
 int launch_block_factor(const BlockArgs &b, const double *D, const int32_t *frozen, cudaStream_t st);
 int launch_block_start(const BlockArgs &b, const VecArgs &v, const double *gs, const RedArgs &ra,
                        const CondArgs &cd, cudaStream_t st);
@@ -202,7 +207,9 @@ struct SweepBuffers {
     int32_t *scan_tmp;       // scan block totals
     unsigned long long *digit_hist;  // [8][256] global histograms
     __int128 *delta;         // [n+2] delta_v in id order (+ P0, P_k)
-    __int128 *tile_sum;      // [ntiles]
+    __int128 *tile_sum;      // [ntiles] scan look-back: tile aggregates
+    __int128 *tile_incl;     // [ntiles] scan look-back: inclusive prefixes
+    __int128 *qcs_tile;      // [ntiles] per-tile sums of Q(cs) (P_0)
     __int128 *tile_min;      // [ntiles]
     int64_t *tile_argmin;    // [ntiles]
     int32_t *flags;          // [0] NaN seen, [1] radix tile ticket

@@ -715,7 +715,9 @@ int launch_pair_assemble(const StencilArgs &s, const VecArgs &v, const RedArgs &
         else k_pair_nodes<ASM_LAMBDA2><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
     } else if (s.nx % 512 == 0 && s.nx <= 4096) {  // fused single pass
         // 3 CTAs/SM (80 registers): measured on config 4 1.57 ms vs 1.64 (two
-        // passes), 1.90 (4 CTAs/SM, spills) and 1.70 (2 CTAs/SM)
+        // passes), 1.90 (4 CTAs/SM, spills) and 1.70 (2 CTAs/SM); a z-cluster
+        // variant (8 CTAs, -z conductances from the CTA below via DSMEM after a
+        // cluster barrier) measured 2.40 ms (round 2)
         if (mode == ASM_REWEIGHT_WARM)
             k_pair_fused<ASM_REWEIGHT_WARM, 3><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
         else

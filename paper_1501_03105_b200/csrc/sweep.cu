@@ -377,14 +377,14 @@ void sweep_prep_stencil(const StencilArgs &s, int64_t N, int32_t F, const double
 {
     if (N == 0) return;
     k_sweep_prep_stencil<<<(unsigned)sweep_ntiles(N), 256, 0, st>>>(s, N, F, x, b.keys, b.vals, b.delta, b.digit_hist,
-                                                                    b.tile_min, b.flags);
+                                                                    b.qcs_tile, b.flags);
 }
 
 void sweep_prep_sell(const SellArgs &s, int32_t F, const double *x, SweepBuffers &b, cudaStream_t st)
 {
     if (s.n == 0) return;
     k_sweep_prep_sell<<<(unsigned)sweep_ntiles(s.n), 256, 0, st>>>(s, F, x, b.keys, b.vals, b.delta, b.digit_hist,
-                                                                  b.tile_min, b.flags);
+                                                                  b.qcs_tile, b.flags);
 }
 
 int32_t *sweep_sort(SweepBuffers &b, cudaStream_t st, int *launches, bool *nan)
@@ -438,71 +438,53 @@ int32_t *sweep_sort(SweepBuffers &b, cudaStream_t st, int *launches, bool *nan)
 // ---------------------------------------------------------------------------
 // scan + argmin
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_delta_tile_sum(const i128 *delta, const int32_t *ord, int64_t n,
-                                                        i128 *tile_sum)
+__device__ __forceinline__ bool lex_less(i128 a, int64_t ia, i128 b, int64_t ib)
 {
-    i128 acc = 0;
-    const int64_t base = (int64_t)blockIdx.x * kTile;
-    for (int r = 0; r < 16; r++) {
-        const int64_t i = base + r * 256 + threadIdx.x;
-        if (i < n) acc += delta[ord[i]];  // delta in id order, gathered in sweep order
-    }
-    tile_sum_i128(acc, tile_sum + blockIdx.x);
+    return a < b || (a == b && ia < ib);
 }
 
-// One block of 256: P0 = sum(qcs_tile) + Q(c_st); tile_sum -> P0 + exclusive prefix.
-__global__ void __launch_bounds__(256) k_tile_prefix(i128 *tile_sum, const i128 *qcs_tile, int64_t nt, i128 qcst,
-                                                     i128 *p0_out)
+// P_0 = Q(c_st) + sum of the prep kernel's per-tile Q(cs) sums (one block).
+__global__ void __launch_bounds__(256) k_p0(const i128 *qcs_tile, int64_t nt, i128 qcst, i128 *p0_out)
 {
     __shared__ i128 sm[256];
-    const int64_t per = (nt + 255) / 256;
-    const int64_t lo = threadIdx.x * per, hi = lo + per < nt ? lo + per : nt;
-    i128 q = 0, t = 0;
-    for (int64_t i = lo; i < hi; i++) { q += qcs_tile[i]; t += tile_sum[i]; }
+    i128 q = 0;
+    for (int64_t i = threadIdx.x; i < nt; i += 256) q += qcs_tile[i];
     sm[threadIdx.x] = q;
     __syncthreads();
     if (threadIdx.x == 0) {
         i128 p0 = qcst;
         for (int i = 0; i < 256; i++) p0 += sm[i];
         *p0_out = p0;
-        sm[0] = p0;
     }
-    __syncthreads();
-    const i128 p0 = sm[0];
-    __syncthreads();
-    sm[threadIdx.x] = t;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        i128 run = p0;
-        for (int i = 0; i < 256; i++) { const i128 c = sm[i]; sm[i] = run; run += c; }
-    }
-    __syncthreads();
-    i128 run = sm[threadIdx.x];
-    for (int64_t i = lo; i < hi; i++) { const i128 c = tile_sum[i]; tile_sum[i] = run; run += c; }
 }
 
-__device__ __forceinline__ bool lex_less(i128 a, int64_t ia, i128 b, int64_t ib)
+// Single pass over the sweep order: tile t (ticket order) gathers its 4096
+// deltas (id order, through ord), publishes its sum, finds the exclusive
+// prefix by decoupled look-back (exact integers: any association gives the
+// same P_i), then forms P_{i+1} = P_0 + delta_0 + ... + delta_i and the
+// tile's first minimum.  look[t] = 0 (nothing), 1 (aggregate in agg[t]),
+// 2 (inclusive prefix in incl[t]); values are written before their flag.
+__global__ void __launch_bounds__(256) k_scan_argmin(const i128 *delta, const int32_t *ord, int64_t n,
+                                                     const i128 *p0, i128 *agg, i128 *incl, int32_t *look,
+                                                     int32_t *ticket, i128 *tile_min, int64_t *tile_arg)
 {
-    return a < b || (a == b && ia < ib);
-}
-
-// Per tile: inclusive prefixes P_{i+1} = prefix + delta_0..i, first minimum.
-__global__ void __launch_bounds__(256) k_tile_argmin(const i128 *delta, const int32_t *ord, int64_t n,
-                                                     const i128 *tile_prefix, i128 *tile_min, int64_t *tile_arg)
-{
-    // thread t owns the 16 consecutive prefixes base + 16t .. +15: its delta
-    // sum, ONE block-wide exclusive scan of those sums, then a second
-    // (cache-hitting) pass forming P_{i+1} and the first minimum.  Integer
-    // sums are exact, so this order gives the same prefixes as any other.
     __shared__ i128 wsum[8];
     __shared__ i128 smin[8];
     __shared__ int64_t sarg[8];
+    __shared__ i128 s_excl;
+    __shared__ int32_t s_tile;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t t0 = (int64_t)blockIdx.x * kTile + 16 * (int64_t)threadIdx.x;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int64_t t0 = tile * kTile + 16 * (int64_t)threadIdx.x;
+    int32_t id[16];
+#pragma unroll
+    for (int q = 0; q < 16; q++) id[q] = t0 + q < n ? ord[t0 + q] : -1;
     i128 own = 0, dl[16];
 #pragma unroll
     for (int q = 0; q < 16; q++) {
-        dl[q] = t0 + q < n ? delta[ord[t0 + q]] : (i128)0;
+        dl[q] = id[q] >= 0 ? delta[id[q]] : (i128)0;
         own += dl[q];
     }
     i128 inc = own;
@@ -515,7 +497,37 @@ __global__ void __launch_bounds__(256) k_tile_argmin(const i128 *delta, const in
     __syncthreads();
     i128 wpre = 0;
     for (int k = 0; k < w; k++) wpre += wsum[k];
-    i128 P = tile_prefix[blockIdx.x] + wpre + inc - own;  // P_{t0}
+    if (threadIdx.x == 0) {
+        i128 T = 0;
+        for (int k = 0; k < 8; k++) T += wsum[k];
+        volatile int32_t *vlook = look;
+        i128 ex;
+        if (tile == 0) {
+            ex = *p0;
+        } else {
+            agg[tile] = T;
+            __threadfence();
+            vlook[tile] = 1;
+            ex = 0;
+            for (int64_t t = tile - 1;; t--) {
+                int32_t f;
+                while ((f = vlook[t]) == 0) {
+                }
+                __threadfence();
+                if (f == 2) {
+                    ex += *(volatile i128 *)(incl + t);
+                    break;
+                }
+                ex += *(volatile i128 *)(agg + t);
+            }
+        }
+        incl[tile] = ex + T;
+        __threadfence();
+        vlook[tile] = 2;
+        s_excl = ex;
+    }
+    __syncthreads();
+    i128 P = s_excl + wpre + inc - own;  // P_{t0}
     i128 best = (i128)(((unsigned __int128)1 << 127) - 1);  // +infinity
     int64_t barg = INT64_MAX;
 #pragma unroll
@@ -537,8 +549,8 @@ __global__ void __launch_bounds__(256) k_tile_argmin(const i128 *delta, const in
     if (threadIdx.x == 0) {
         for (int k = 1; k < 8; k++)
             if (lex_less(smin[k], sarg[k], best, barg)) { best = smin[k]; barg = sarg[k]; }
-        tile_min[blockIdx.x] = best;
-        tile_arg[blockIdx.x] = barg;
+        tile_min[tile] = best;
+        tile_arg[tile] = barg;
     }
 }
 
@@ -565,14 +577,16 @@ __global__ void __launch_bounds__(256) k_final_argmin(const i128 *tile_min, cons
 void sweep_scan_argmin(SweepBuffers &b, const int32_t *ord, __int128 qcst, cudaStream_t st)
 {
     const int64_t n = b.n, nt = sweep_ntiles(n);
-    // b.tile_min holds the per-tile sums of Q(cs) from the prep kernel
-    i128 *qcs_tile = b.tile_min;
     i128 *p0 = b.delta + n;        // two spare slots at the end of delta
     i128 *pk = b.delta + n + 1;
-    if (nt > 0) k_delta_tile_sum<<<(unsigned)nt, 256, 0, st>>>(b.delta, ord, n, b.tile_sum);
-    k_tile_prefix<<<1, 256, 0, st>>>(b.tile_sum, qcs_tile, nt, qcst, p0);
-    if (nt > 0)
-        k_tile_argmin<<<(unsigned)nt, 256, 0, st>>>(b.delta, ord, n, b.tile_sum, b.tile_min, b.tile_argmin);
+    int32_t *look = b.tile_hist;   // the radix passes are done with it
+    k_p0<<<1, 256, 0, st>>>(b.qcs_tile, nt, qcst, p0);
+    if (nt > 0) {
+        cudaMemsetAsync(look, 0, sizeof(int32_t) * nt, st);
+        cudaMemsetAsync(b.flags + 1, 0, sizeof(int32_t), st);
+        k_scan_argmin<<<(unsigned)nt, 256, 0, st>>>(b.delta, ord, n, p0, b.tile_sum, b.tile_incl, look, b.flags + 1,
+                                                    b.tile_min, b.tile_argmin);
+    }
     k_final_argmin<<<1, 256, 0, st>>>(b.tile_min, b.tile_argmin, nt, p0, b.k_out, pk);
 }
 

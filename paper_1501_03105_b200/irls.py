@@ -122,7 +122,7 @@ SYMBOLS = ["irls_options_default", "irls_nccl_unique_id", "irls_mincut_create_st
            "irls_halo_plan", "irls_combine_slots", "irls_vgroup_create_stencil", "irls_vgroup_solve",
            "irls_vgroup_sweep_cut", "irls_vgroup_get_potentials", "irls_vgroup_set_terminal_weights",
            "irls_vgroup_destroy", "irls_two_level_cut", "irls_two_level_get_coarse", "irls_coarse_maxflow",
-           "irls_vgroup_two_level_cut", "irls_exact_min_cut", "irls_lambda2", "irls_vgroup_create_csr", "irls_vgroup_last_error", "irls_plan_csr"]
+           "irls_vgroup_two_level_cut", "irls_exact_min_cut", "irls_lambda2", "irls_vgroup_create_csr", "irls_vgroup_last_error", "irls_plan_csr", "irls_csr_halo_plan"]
 
 
 def lib():
@@ -257,6 +257,27 @@ def irls_halo_plan(nx, ny, nz, world, rank) -> dict:
     if rc:
         raise IrlsError(rc, "irls_halo_plan")
     return {k: getattr(h, k) for k, _ in h._fields_ if k != "reserved"}
+
+
+def irls_csr_halo_plan(aptr, aidx, world, rank) -> dict:
+    """Host-only halo plan of id strip `rank` over the reduced adjacency."""
+    aptr = np.ascontiguousarray(aptr, dtype=np.int64)
+    aidx = np.ascontiguousarray(aidx, dtype=np.int32) if len(aidx) else np.zeros(1, np.int32)
+    nr = aptr.shape[0] - 1
+    lo_hi = np.zeros(2, np.int64); ro = np.zeros(world + 1, np.int64); so = np.zeros(world + 1, np.int64)
+    f = lib().irls_csr_halo_plan
+    f.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                  C.c_void_p, C.c_int64, C.c_void_p, C.c_int64]
+    rc = f(nr, _ptr(aptr), _ptr(aidx), world, rank, _ptr(lo_hi), _ptr(ro), _ptr(so), None, 0, None, 0)
+    if rc:
+        raise IrlsError(rc, "irls_csr_halo_plan")
+    gh = np.zeros(max(int(ro[-1]), 1), np.int32); sd = np.zeros(max(int(so[-1]), 1), np.int32)
+    rc = f(nr, _ptr(aptr), _ptr(aidx), world, rank, _ptr(lo_hi), _ptr(ro), _ptr(so), _ptr(gh), gh.shape[0],
+           _ptr(sd), sd.shape[0])
+    if rc:
+        raise IrlsError(rc, "irls_csr_halo_plan")
+    return dict(lo=int(lo_hi[0]), hi=int(lo_hi[1]), recv_off=ro, send_off=so, ghosts=gh[: ro[-1]],
+                send_idx=sd[: so[-1]])
 
 
 def irls_plan_csr(nr, world, rank):

@@ -100,6 +100,63 @@ def _worker(rank, world, port, q):
         out["slots_exact"] = np.array_equal(t.numpy(), gs)
         out["combined"] = I.irls_combine_slots(t.numpy()) == oracle.c3_sum(v)
 
+        # ---- CSR id strips: the library's halo plan (irls_csr_halo_plan, the
+        # lists irls_mincut_create_csr builds) drives a real exchange over gloo
+        # in the layout the library uses (owned rows, then the ghost block);
+        # every ghost slot must receive its node's value, and the strips
+        # gathered to rank 0 must rebuild the vector
+        from synthetic import generators as gen
+        spec = gen.road_graph(300, seed=2, knn=100)   # ~88k non-terminals: 22 chunks
+        n, sid, tid = spec["n"], spec["s"], spec["t"]
+        keep = np.array([u for u in range(n) if u not in (sid, tid)], dtype=np.int64)
+        red = -np.ones(n, dtype=np.int64)
+        red[keep] = np.arange(keep.shape[0])
+        rp, cl, ww = spec["row_ptr"], spec["col"], spec["w"]
+        aptr, aidx = [0], []
+        for u in keep:
+            nb = sorted({int(red[v]) for v, c in zip(cl[rp[u]:rp[u + 1]], ww[rp[u]:rp[u + 1]])
+                         if red[v] >= 0 and c > 0})
+            aidx.extend(nb)
+            aptr.append(len(aidx))
+        aptr = np.array(aptr, dtype=np.int64)
+        aidx = np.array(aidx, dtype=np.int32)
+        nr = keep.shape[0]
+        gv = np.random.default_rng(3).standard_normal(nr)
+        hp = I.irls_csr_halo_plan(aptr, aidx, world, rank)
+        clo, chi = hp["lo"], hp["hi"]
+        loc = np.concatenate([gv[clo:chi], np.full(hp["ghosts"].shape[0], np.nan)])
+        reqs, rbufs = [], {}
+        for peer in range(world):
+            if peer == rank:
+                continue
+            a, b = hp["send_off"][peer], hp["send_off"][peer + 1]
+            if b > a:
+                reqs.append(dist.isend(torch.from_numpy(loc[hp["send_idx"][a:b]].copy()), peer))
+            a, b = hp["recv_off"][peer], hp["recv_off"][peer + 1]
+            if b > a:
+                rbufs[peer] = torch.empty(b - a, dtype=torch.float64)
+                reqs.append(dist.irecv(rbufs[peer], peer))
+        for r in reqs:
+            r.wait()
+        for peer, buf in rbufs.items():
+            a = hp["recv_off"][peer]
+            loc[chi - clo + a: chi - clo + a + buf.shape[0]] = buf.numpy()
+        ghost_ok = np.array_equal(loc[chi - clo:], gv[hp["ghosts"]])
+        # every neighbour of an owned row is owned or a ghost (the SpMV's columns)
+        need = {int(v) for r in range(clo, chi) for v in aidx[aptr[r]:aptr[r + 1]] if not clo <= v < chi}
+        out["csr_halo"] = (ghost_ok, need == set(hp["ghosts"].tolist()), hp["ghosts"].shape[0] > 0)
+        if rank == 0:
+            full = np.empty(nr)
+            full[clo:chi] = loc[:chi - clo]
+            for r in range(1, world):
+                pr = I.irls_plan_csr(nr, world, r)
+                buf = torch.empty(pr[1] - pr[0], dtype=torch.float64)
+                dist.recv(buf, r)
+                full[pr[0]:pr[1]] = buf.numpy()
+            out["csr_gather"] = np.array_equal(full, gv)
+        else:
+            dist.send(torch.from_numpy(loc[:chi - clo].copy()), 0)
+
         # ---- gather of the slabs to rank 0
         mine = torch.from_numpy(glob[lo:lo + n_own].copy())
         if rank == 0:
@@ -116,6 +173,13 @@ def _worker(rank, world, port, q):
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
+
+
+def test_csr_halo_exchange_and_gather(results):
+    for rank in (0, 1):
+        ghost_ok, cover_ok, nonempty = results[rank]["csr_halo"]
+        assert ghost_ok and cover_ok and nonempty, rank
+    assert results[0]["csr_gather"]
 
 
 @pytest.fixture(scope="module")

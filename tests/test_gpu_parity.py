@@ -137,7 +137,9 @@ def test_blob_grid_chunk_planes(irls, dims):
 
 
 @pytest.mark.parametrize("dims", [(512, 12, 6), (512, 7, 3), (1024, 5, 4), (1536, 3, 4), (512, 16, 5), (512, 8, 37),
-                                  (512, 24, 1)])
+                                  (512, 24, 1),
+                                  # whole chunks per plane, planes a multiple of 8: the z-cluster K1
+                                  (512, 8, 16), (512, 16, 24), (1024, 8, 8)])
 def test_fused_reweight_rows_of_512(irls, dims):
     """nx a multiple of 512 (config 4's rows): the single-pass fused reweight
     kernel (-y conductance from the thread's own earlier row, -x by shuffle,

@@ -86,10 +86,12 @@ def test_vgroup_cold_and_sequence(irls, world, p2p):
 
 @pytest.mark.parametrize("p2p", [0, 1])
 @pytest.mark.parametrize("world", [2, 4, 8])
-def test_vgroup_fused_rows_of_512(irls, world, p2p):
+@pytest.mark.parametrize("nz", [16, 32])
+def test_vgroup_fused_rows_of_512(irls, world, p2p, nz):
     """512-wide rows (fused reweight kernel incl. the ghost -z slot), one
-    chunk per plane, 16 planes: bitwise equal to one rank."""
-    spec = gen.blob_grid(512, 8, 16, seed=8, sigma=(3.0, 8.0))
+    chunk per plane, 16 or 32 planes (slabs of 8 planes or more run the
+    z-cluster K1): bitwise equal to one rank."""
+    spec = gen.blob_grid(512, 8, nz, seed=8, sigma=(3.0, 8.0))
     T = 10
     m, reps1, tot1, sw1 = single(irls, spec, irls.options(T=T), T)
     g = irls.VGroup(spec, world, irls.options(T=T, p2p=p2p))
