@@ -533,6 +533,166 @@ extern "C" irls_status irls_plan_csr(int64_t nr, int32_t world, int32_t rank, in
     return IRLS_OK;
 }
 
+// One-rank CSR create with the preparation on the GPU (csr_prep.cu): the
+// caller's arrays are uploaded once and every step of the host path —
+// validation, duplicate merge (A7), exact symmetry, terminal split, c_st (A5),
+// F, Prop. 1 / A8, SELL-64 — runs in kernels with the host path's results.
+// Error codes follow the host path's priority (first offending entry, then
+// self loops, then symmetry, then singularity).
+static irls_status create_csr_gpu(irls_ctx **out, const irls_comm_desc *comm, int64_t n, const int64_t *row_ptr,
+                                  const int32_t *col, const double *w, int64_t s_, int64_t t_, const irls_options *opt)
+{
+    const int64_t nnz = row_ptr[n], nr = n - 2;
+    irls_ctx *c = new irls_ctx();
+    irls_status st = common_setup(c, comm, opt);
+    std::vector<void *> tmp;
+    cudaStream_t S = c->stream;
+    auto talloc = [&](size_t bytes) -> void * {
+        void *p = nullptr;
+        if (cudaMallocAsync(&p, std::max<size_t>(bytes, 16), S) != cudaSuccess) return nullptr;
+        tmp.push_back(p);
+        return p;
+    };
+    auto finish = [&](irls_status r) -> irls_status {
+        for (void *p : tmp) cudaFreeAsync(p, S);
+        cudaStreamSynchronize(S);
+        if (r) {
+            irls_mincut_destroy(c);
+            return r;
+        }
+        *out = c;
+        return IRLS_OK;
+    };
+    if (st) return finish(st);
+    if (c->multi) return finish(IRLS_ERR_INVALID_ARGUMENT);  // (the caller routes communicators to the host path)
+    int64_t *d_rp = (int64_t *)talloc(8 * (size_t)(n + 1));
+    int32_t *d_col = (int32_t *)talloc(4 * (size_t)nnz), *d_scol = (int32_t *)talloc(4 * (size_t)nnz);
+    double *d_w = (double *)talloc(8 * (size_t)nnz), *d_sw = (double *)talloc(8 * (size_t)nnz);
+    int32_t *d_mcnt = (int32_t *)talloc(4 * (size_t)(n + 1)), *d_mptr = (int32_t *)talloc(4 * (size_t)(n + 1));
+    int64_t *d_scan = (int64_t *)talloc(8 * (size_t)((n + 1 + 4095) / 4096 + 2 + (nr + 1 + 4095) / 4096 +
+                                                     (nr / kSell + 4096) / 4096 + 8));
+    unsigned long long *d_u64 = (unsigned long long *)talloc(8 * 4);  // first_bad, cnt, cmax, wmax
+    int32_t *d_flags = (int32_t *)talloc(4 * 4);                      // selfloop, asym, lonely
+    double *d_cst = (double *)talloc(8);
+    if (!d_rp || !d_col || !d_scol || !d_w || !d_sw || !d_mcnt || !d_mptr || !d_scan || !d_u64 || !d_flags || !d_cst)
+        return finish(fail(c, IRLS_ERR_OOM, "csr preparation buffers"));
+    CK(cudaMemcpyAsync(d_rp, row_ptr, 8 * (size_t)(n + 1), cudaMemcpyHostToDevice, S));
+    CK(cudaMemcpyAsync(d_col, col, 4 * (size_t)nnz, cudaMemcpyHostToDevice, S));
+    CK(cudaMemcpyAsync(d_w, w, 8 * (size_t)nnz, cudaMemcpyHostToDevice, S));
+    CK(cudaMemsetAsync(d_u64, 0, 8 * 4, S));
+    CK(cudaMemsetAsync(d_u64, 0xff, 8, S));  // first_bad = none
+    CK(cudaMemsetAsync(d_flags, 0, 4 * 4, S));
+    csrp_check(d_rp, d_col, d_w, n, d_u64, d_flags, S);
+    unsigned long long h_u64[4];
+    int32_t h_flags[4];
+    CK(cudaMemcpyAsync(h_u64, d_u64, sizeof(h_u64), cudaMemcpyDeviceToHost, S));
+    CK(cudaMemcpyAsync(h_flags, d_flags, sizeof(h_flags), cudaMemcpyDeviceToHost, S));
+    CK(cudaStreamSynchronize(S));
+    if (h_u64[0] != ~0ull) {
+        const int64_t e = (int64_t)h_u64[0];
+        return finish(col[e] < 0 || col[e] >= n ? IRLS_ERR_INVALID_ARGUMENT : IRLS_ERR_BAD_CAPACITY);
+    }
+    if (h_flags[0]) return finish(IRLS_ERR_INVALID_ARGUMENT);
+    // merge duplicates (A7) -> merged CSR (mptr, mcol = d_col, mw = d_w reused)
+    int launches = 0;
+    csrp_merge(d_rp, d_col, d_w, n, d_scol, d_sw, d_mcnt, S);
+    CK(cudaMemsetAsync(d_mcnt + n, 0, 4, S));
+    exclusive_scan_i32(d_mcnt, n + 1, d_mptr, d_scan, S, &launches);
+    csrp_compact(d_rp, d_scol, d_sw, d_mptr, n, d_col, d_w, S);
+    csrp_symmetry(d_mptr, d_col, d_w, n, d_flags + 1, S);
+    CK(cudaMemcpyAsync(h_flags, d_flags, sizeof(h_flags), cudaMemcpyDeviceToHost, S));
+    CK(cudaStreamSynchronize(S));
+    if (h_flags[1]) return finish(IRLS_ERR_NOT_SYMMETRIC);
+    // the context's sizes
+    c->kind = 1;
+    c->n_glob = nr;
+    c->n_total = n;
+    c->s_id = s_;
+    c->t_id = t_;
+    c->K = (int32_t)((nr + kChunk - 1) / kChunk);
+    c->g0 = 0;
+    c->g1 = kGroups;
+    c->lo = 0;
+    c->n_own = nr;
+    c->chunk0 = 0;
+    c->nchunks = (int32_t)((nr + kChunk - 1) / kChunk);
+    c->n_fin = count_nonempty(c->K, 0, kGroups);
+    c->npad_own = (int64_t)c->nchunks * kChunk;
+    c->rank_lo = {0, nr};
+    const int64_t gpad = (int64_t)c->K * kChunk;
+    c->cs = dalloc<double>(c, gpad);
+    c->ct = dalloc<double>(c, gpad);
+    c->orig_dev = dalloc<int64_t>(c, std::max<int64_t>(nr, 1));
+    int32_t *d_acnt = (int32_t *)talloc(4 * (size_t)(nr + 1)), *d_aptr = (int32_t *)talloc(4 * (size_t)(nr + 1));
+    if (!c->cs || !c->ct || !c->orig_dev || !d_acnt || !d_aptr) return finish(fail(c, IRLS_ERR_OOM, "csr arrays"));
+    csrp_reduce(d_mptr, d_col, d_w, nr, s_, t_, c->cs, c->ct, c->orig_dev, d_acnt, d_u64 + 1, d_u64 + 2, d_cst, S);
+    CK(cudaMemsetAsync(d_acnt + nr, 0, 4, S));
+    exclusive_scan_i32(d_acnt, nr + 1, d_aptr, d_scan, S, &launches);
+    int32_t h_na = 0;
+    double cst = 0.0;
+    CK(cudaMemcpyAsync(&h_na, d_aptr + nr, 4, cudaMemcpyDeviceToHost, S));
+    CK(cudaMemcpyAsync(&cst, d_cst, 8, cudaMemcpyDeviceToHost, S));
+    CK(cudaMemcpyAsync(h_u64, d_u64, sizeof(h_u64), cudaMemcpyDeviceToHost, S));
+    CK(cudaStreamSynchronize(S));
+    int32_t *d_aidx = (int32_t *)talloc(4 * (size_t)std::max<int32_t>(h_na, 1));
+    double *d_ac = (double *)talloc(8 * (size_t)std::max<int32_t>(h_na, 1));
+    int32_t *d_par = (int32_t *)talloc(4 * (size_t)std::max<int64_t>(nr, 1));
+    int32_t *d_root = (int32_t *)talloc(4 * (size_t)std::max<int64_t>(nr, 1));
+    uint8_t *d_anc = (uint8_t *)talloc((size_t)std::max<int64_t>(nr, 1));
+    if (!d_aidx || !d_ac || !d_par || !d_root || !d_anc) return finish(fail(c, IRLS_ERR_OOM, "csr arrays"));
+    csrp_fill(d_mptr, d_col, d_w, c->orig_dev, d_aptr, nr, s_, t_, d_aidx, d_ac, S);
+    if (nr > 0) csrp_components(d_aptr, d_aidx, c->cs, c->ct, nr, d_par, d_root, d_anc, d_flags + 2, S);
+    c->comp_root.resize((size_t)std::max<int64_t>(nr, 1));
+    if (nr > 0) CK(cudaMemcpyAsync(c->comp_root.data(), d_root, 4 * (size_t)nr, cudaMemcpyDeviceToHost, S));
+    CK(cudaMemcpyAsync(h_flags, d_flags, sizeof(h_flags), cudaMemcpyDeviceToHost, S));
+    CK(cudaStreamSynchronize(S));
+    if (h_flags[2]) return finish(IRLS_ERR_SINGULAR);
+    {
+        double cmax;
+        memcpy(&cmax, &h_u64[2], sizeof(double));
+        cmax = std::max(cmax, cst);
+        c->F = compute_F(cmax, (int64_t)h_u64[1] + (cst > 0.0 ? 1 : 0));
+    }
+    c->c_st = cst;
+    c->n_links = h_na / 2;
+    // SELL-64
+    const int64_t nsl = (nr + kSell - 1) / kSell;
+    int32_t *d_sw32 = (int32_t *)talloc(4 * (size_t)(nsl + 1)), *d_sp32 = (int32_t *)talloc(4 * (size_t)(nsl + 1));
+    if (!d_sw32 || !d_sp32) return finish(fail(c, IRLS_ERR_OOM, "sell widths"));
+    CK(cudaMemsetAsync(d_sw32, 0, 4 * (size_t)(nsl + 1), S));
+    if (nsl > 0) csrp_sell_width(d_aptr, nr, d_sw32, d_u64 + 3, S);
+    exclusive_scan_i32(d_sw32, nsl + 1, d_sp32, d_scan, S, &launches);
+    int32_t nent32 = 0;
+    CK(cudaMemcpyAsync(&nent32, d_sp32 + nsl, 4, cudaMemcpyDeviceToHost, S));
+    CK(cudaMemcpyAsync(h_u64, d_u64, sizeof(h_u64), cudaMemcpyDeviceToHost, S));
+    CK(cudaStreamSynchronize(S));
+    const int64_t nent = nent32;
+    c->n_entries = nent;
+    c->sell_wmax = (int32_t)h_u64[3];
+    st = alloc_solver(c, 0);
+    if (st) return finish(st);
+    c->slice_ptr = dalloc<int64_t>(c, nsl + 1);
+    c->col = dalloc<int32_t>(c, nent);
+    c->cap = dalloc<double>(c, nent);
+    c->gsell = dalloc<double>(c, nent);
+    if (!c->slice_ptr || !c->col || !c->cap || !c->gsell) return finish(fail(c, IRLS_ERR_OOM, "sell arrays"));
+    csrp_i32_to_i64(d_sp32, nsl + 1, c->slice_ptr, S);
+    CK(cudaMemsetAsync(c->col, 0xff, 4 * (size_t)std::max<int64_t>(nent, 1), S));  // padding: column -1
+    CK(cudaMemsetAsync(c->cap, 0, 8 * (size_t)std::max<int64_t>(nent, 1), S));
+    if (nr > 0) csrp_sell_fill(d_aptr, d_aidx, d_ac, c->slice_ptr, nr, c->col, c->cap, S);
+    c->lslice_ptr = c->slice_ptr;
+    c->lcol = c->col;
+    c->lcap = c->cap;
+    c->lg = c->gsell;
+    c->lcs = c->cs;
+    c->lct = c->ct;
+    c->lwmax = c->sell_wmax;
+    c->ln_entries = c->n_entries;
+    st = last_launch(c, "csr preparation");
+    if (!st) st = init_nccl(c, comm);
+    return finish(st);
+}
+
 irls_status create_csr_impl(irls_ctx **out, const irls_comm_desc *comm, int64_t n, const int64_t *row_ptr,
                                    const int32_t *col, const double *w, int64_t s_, int64_t t_, const irls_options *opt,
                                    irls_vgroup *vg)
@@ -548,6 +708,10 @@ irls_status create_csr_impl(irls_ctx **out, const irls_comm_desc *comm, int64_t 
     for (int64_t u = 0; u < n; u++)
         if (row_ptr[u + 1] < row_ptr[u]) return IRLS_ERR_INVALID_ARGUMENT;
     const int64_t nnz = row_ptr[n];
+    // one rank, no block preconditioner: the preparation runs on the GPU
+    const bool gpu_prep = !vg && (!comm || (comm->world_size == 1 && !comm->nccl_unique_id)) &&
+                          opt->block_size == 0 && nnz < ((int64_t)1 << 31) - 1 && !getenv("IRLS_HOST_CSR_PREP");
+    if (gpu_prep) return create_csr_gpu(out, comm, n, row_ptr, col, w, s_, t_, opt);
     // Host preparation runs on the host threads (row blocks); every result is
     // independent of the thread count (first offending entry wins, integer
     // counts, per-row sums in CSR order).

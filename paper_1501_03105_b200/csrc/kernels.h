@@ -240,6 +240,26 @@ void sweep_side_cross_sell(const SellArgs &s, const int64_t *orig, int64_t n_tot
                            const RedArgs &ra, cudaStream_t st);
 void sweep_order_out(const int32_t *order, const int64_t *orig, int32_t *out, int64_t n, cudaStream_t st);
 __int128 qfix_host(double c, int32_t F);
+// create-time CSR preparation on the GPU (csr_prep.cu)
+void csrp_check(const int64_t *rp, const int32_t *col, const double *w, int64_t n, unsigned long long *first_bad,
+                int32_t *selfloop, cudaStream_t st);
+void csrp_merge(const int64_t *rp, const int32_t *col, const double *w, int64_t n, int32_t *scol, double *sw,
+                int32_t *mcnt, cudaStream_t st);
+void csrp_compact(const int64_t *rp, const int32_t *scol, const double *sw, const int32_t *mptr, int64_t n,
+                  int32_t *mcol, double *mw, cudaStream_t st);
+void csrp_symmetry(const int32_t *mptr, const int32_t *mcol, const double *mw, int64_t n, int32_t *asym,
+                   cudaStream_t st);
+void csrp_reduce(const int32_t *mptr, const int32_t *mcol, const double *mw, int64_t nr, int64_t s, int64_t t,
+                 double *cs, double *ct, int64_t *orig, int32_t *acnt, unsigned long long *cnt,
+                 unsigned long long *cmax_bits, double *cst, cudaStream_t st);
+void csrp_fill(const int32_t *mptr, const int32_t *mcol, const double *mw, const int64_t *orig, const int32_t *aptr,
+               int64_t nr, int64_t s, int64_t t, int32_t *aidx, double *ac, cudaStream_t st);
+void csrp_components(const int32_t *aptr, const int32_t *aidx, const double *cs, const double *ct, int64_t nr,
+                     int32_t *par, int32_t *root, uint8_t *anchored, int32_t *lonely, cudaStream_t st);
+void csrp_sell_width(const int32_t *aptr, int64_t nr, int32_t *sw, unsigned long long *wmax, cudaStream_t st);
+void csrp_i32_to_i64(const int32_t *in, int64_t n, int64_t *out, cudaStream_t st);
+void csrp_sell_fill(const int32_t *aptr, const int32_t *aidx, const double *ac, const int64_t *sptr, int64_t nr,
+                    int32_t *scol, double *scap, cudaStream_t st);
 void exclusive_scan_i32(const int32_t *in, int64_t m, int32_t *out, int64_t *tmp, cudaStream_t st, int *launches);
 
 // ---------------------------------------------------------------------------
