@@ -169,15 +169,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sellp_pspmv(SellArgs s, VecA
         int2 cl[WMAX];
         double2 gg[WMAX];
 #pragma unroll
-        for (int k = 0; k < WMAX; k++) {
-            if (k < W) {
-                cl[k] = ldi2(s.col, e0 + (int64_t)kSell * k);
-                gg[k] = ldp2(s.g, e0 + (int64_t)kSell * k);
-            } else {
-                cl[k] = make_int2(-1, -1);
-                gg[k] = make_double2(0.0, 0.0);
-            }
-        }
+        for (int k = 0; k < WMAX; k++) cl[k] = k < W ? ldi2(s.col, e0 + (int64_t)kSell * k) : make_int2(-1, -1);
+#pragma unroll
+        for (int k = 0; k < WMAX; k++)  // padding slots of both rows: no conductance load
+            gg[k] = (cl[k].x >= 0 || cl[k].y >= 0) ? ldp2(s.g, e0 + (int64_t)kSell * k) : make_double2(0.0, 0.0);
         double za[WMAX], zb[WMAX], pa[WMAX], pb[WMAX];
 #pragma unroll
         for (int k = 0; k < WMAX; k++) {
