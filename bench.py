@@ -353,7 +353,7 @@ def main():
     ach = k3_bytes / (t_k3 * 1e-3) / 1e9
     traffic = None
     try:  # per-launch DRAM bytes of K3 from the committed ncu --set full capture (same config)
-        tj = json.load(open(os.path.join(ROOT, "profiles", "r01_k3_traffic.json")))
+        tj = json.load(open(os.path.join(ROOT, "profiles", "r02_k3_traffic.json")))
         if args.config == "config4" and world == 1:
             traffic = tj["traffic_GB_per_launch"] / (t_k3 * 1e-3)
     except Exception:
@@ -492,7 +492,7 @@ def main():
                    "cg_variant": "Chronopoulos-Gear" if args.cg_variant == "cg" else "Hestenes-Stiefel"},
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                      "traffic": traffic, "traffic_note": "ncu dram__bytes_read+write per K3 launch "
-                     "(profiles/r01_k3_traffic.json) over the live K3 duration, GB/s; algorithmic bytes per launch "
+                     "(profiles/r02_k3_traffic.json) over the live K3 duration, GB/s; algorithmic bytes per launch "
                      f"= {roof_bytes / 1e9:.3f} GB", "kernel": roof_name,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks
                      else "fallback 6650 GB/s (B200_PROFILING.md)",

@@ -107,32 +107,42 @@ __global__ void k_csr_reduce_rows(const int32_t *mptr, const int32_t *mcol, cons
                                   u64 *cmax_bits)
 {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= nr) return;
-    const int64_t lo2 = min(s, t), hi2 = max(s, t);
-    int64_t u = r;
-    if (u >= lo2) u++;
-    if (u >= hi2) u++;
-    orig[r] = u;
-    double a = 0.0, b = 0.0, cm = 0.0;
-    int32_t k = 0;
     u64 cn = 0;
-    for (int32_t e = mptr[u]; e < mptr[u + 1]; e++) {
-        const int64_t v = mcol[e];
-        const double x = mw[e];
-        if (v == s) a = x;
-        else if (v == t) b = x;
-        else if (x > 0.0) {
-            k++;
-            if (v > u) { cn++; cm = fmax(cm, x); }
+    double cm = 0.0;
+    if (r < nr) {
+        const int64_t lo2 = min(s, t), hi2 = max(s, t);
+        int64_t u = r;
+        if (u >= lo2) u++;
+        if (u >= hi2) u++;
+        orig[r] = u;
+        double a = 0.0, b = 0.0;
+        int32_t k = 0;
+        for (int32_t e = mptr[u]; e < mptr[u + 1]; e++) {
+            const int64_t v = mcol[e];
+            const double x = mw[e];
+            if (v == s) a = x;
+            else if (v == t) b = x;
+            else if (x > 0.0) {
+                k++;
+                if (v > u) { cn++; cm = fmax(cm, x); }
+            }
         }
+        cs[r] = a;
+        ct[r] = b;
+        acnt[r] = k;
+        if (a > 0.0) { cn++; cm = fmax(cm, a); }
+        if (b > 0.0) { cn++; cm = fmax(cm, b); }
     }
-    cs[r] = a;
-    ct[r] = b;
-    acnt[r] = k;
-    if (a > 0.0) { cn++; cm = fmax(cm, a); }
-    if (b > 0.0) { cn++; cm = fmax(cm, b); }
-    if (cn) atomicAdd(cnt, cn);
-    if (cm > 0.0) atomicMax(cmax_bits, (u64)__double_as_longlong(cm));  // c >= 0: bit order = value order
+    // one atomic per warp (integer count; maximum: c >= 0, so bit order = value order)
+    u64 bits = (u64)__double_as_longlong(cm);
+    for (int off = 16; off >= 1; off >>= 1) {
+        cn += __shfl_down_sync(0xffffffffu, cn, off);
+        bits = max(bits, (u64)__shfl_down_sync(0xffffffffu, bits, off));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (cn) atomicAdd(cnt, cn);
+        if (bits) atomicMax(cmax_bits, bits);
+    }
 }
 
 __global__ void k_csr_reduce_fill(const int32_t *mptr, const int32_t *mcol, const double *mw, const int64_t *orig,
@@ -162,11 +172,12 @@ __global__ void k_csr_cst(const int32_t *mptr, const int32_t *mcol, const double
 // ---- union-find (A8)
 __device__ __forceinline__ int32_t uf_find(int32_t *par, int32_t x)
 {
+    volatile int32_t *vp = par;
     for (;;) {
-        const int32_t p = atomicAdd(par + x, 0);
+        const int32_t p = vp[x];
         if (p == x) return x;
-        const int32_t gp = atomicAdd(par + p, 0);
-        if (gp != p) atomicCAS(par + x, p, gp);
+        const int32_t gp = vp[p];
+        if (gp != p) atomicCAS(par + x, p, gp);  // path halving
         x = gp;
     }
 }
