@@ -19,7 +19,7 @@ static irls_status alloc_sweep(irls_ctx *c)
     b.vals = dalloc<int32_t>(c, n);
     b.vals_alt = dalloc<int32_t>(c, n);
     b.rank = nullptr;  // the sweep forms membership from x (two-level uses its own ranks)
-    b.tile_hist = dalloc<int32_t>(c, 256 * nt);
+    b.tile_hist = dalloc<int32_t>(c, 2 * 256 * nt);  // look-back words of radix tiles down to 2048 keys
     b.tile_off = dalloc<int32_t>(c, 256 * nt);
     b.scan_tmp = (int32_t *)dalloc<int64_t>(c, (256 * nt + 4095) / 4096 + 1);
     b.digit_hist = dalloc<unsigned long long>(c, 8 * 256);

@@ -182,28 +182,30 @@ struct GStart {
 // formed (digit-major, warp-minor: stable), the keys staged in shared memory
 // in digit order and written out so that consecutive threads write
 // consecutive positions of a bucket.
-__global__ void __launch_bounds__(256, 3) k_onesweep(const u64 *keys, const int32_t *vals, u64 *okeys,
-                                                  int32_t *ovals, int64_t n, int shift, GStart gs, uint32_t *state,
-                                                  int32_t *ticket)
+template <int KPT, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_onesweep(const u64 *keys, const int32_t *vals, u64 *okeys,
+                                                     int32_t *ovals, int64_t n, int shift, GStart gs, uint32_t *state,
+                                                     int32_t *ticket)
 {
+    constexpr int RT = 256 * KPT;      // keys per tile
     __shared__ int32_t wh[8][256];     // per-warp digit counts, then per-warp tile starts
     __shared__ int32_t gdelta[256];    // global start of the bucket minus its tile-local start
     __shared__ int32_t s_tile;
-    extern __shared__ __align__(16) unsigned char radix_dyn[];  // kTile keys + kTile values
+    extern __shared__ __align__(16) unsigned char radix_dyn[];  // RT keys + RT values
     u64 *skey = reinterpret_cast<u64 *>(radix_dyn);
-    int32_t *sval = reinterpret_cast<int32_t *>(radix_dyn + sizeof(u64) * kTile);
+    int32_t *sval = reinterpret_cast<int32_t *>(radix_dyn + sizeof(u64) * RT);
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
     for (int i = threadIdx.x; i < 8 * 256; i += 256) (&wh[0][0])[i] = 0;
     __syncthreads();
     const int32_t tile = s_tile;
-    const int64_t tbase = (int64_t)tile * kTile;
-    const int64_t base = tbase + w * 512;
-    u64 k[16];
-    int32_t vv[16];
-    uint32_t dr[16];  // digit << 16 | rank within (warp, digit); 0xffffffff past n
+    const int64_t tbase = (int64_t)tile * RT;
+    const int64_t base = tbase + w * 32 * KPT;
+    u64 k[KPT];
+    int32_t vv[KPT];
+    uint32_t dr[KPT];  // digit << 16 | rank within (warp, digit); 0xffffffff past n
 #pragma unroll
-    for (int r = 0; r < 16; r++) {
+    for (int r = 0; r < KPT; r++) {
         const int64_t i = base + r * 32 + lane;
         if (i < n) {
             k[r] = __ldcs(keys + i);
@@ -215,7 +217,7 @@ __global__ void __launch_bounds__(256, 3) k_onesweep(const u64 *keys, const int3
     }
     const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
-    for (int r = 0; r < 16; r++) {
+    for (int r = 0; r < KPT; r++) {
         const int64_t i = base + r * 32 + lane;
         const int d = i < n ? (int)((k[r] >> shift) & 255u) : 256 + lane;  // past n: a group of one
         const unsigned peers = __match_any_sync(0xffffffffu, d);
@@ -236,15 +238,25 @@ __global__ void __launch_bounds__(256, 3) k_onesweep(const u64 *keys, const int3
     vst[(int64_t)tile * 256 + d] = (tile == 0 ? kStIncl : kStAgg) | (uint32_t)tot;
     int32_t excl = 0;
     if (tile > 0) {
+        // four predecessors per round (independent loads): the ready prefix
+        // is consumed up to the first inclusive prefix
         int64_t t = tile - 1;
-        for (;;) {
-            uint32_t wv;
-            do {
-                wv = vst[t * 256 + d];
-            } while ((wv & ~kStMask) == 0u);
-            excl += (int32_t)(wv & kStMask);
-            if ((wv & ~kStMask) == kStIncl) break;
-            t--;
+        for (bool done = false; !done;) {
+            uint32_t wv[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) wv[q] = t - q >= 0 ? vst[(t - q) * 256 + d] : (2u << 30);  // (below tile 0: an empty inclusive prefix)
+            int q = 0;
+            for (; q < 4; q++) {
+                if ((wv[q] & ~kStMask) == 0u) break;
+                excl += (int32_t)(wv[q] & kStMask);
+                if ((wv[q] & ~kStMask) == kStIncl) {
+                    done = true;
+                    break;
+                }
+            }
+            if (done) break;
+            if (q == 0) __nanosleep(32);
+            t -= q;
         }
         vst[(int64_t)tile * 256 + d] = kStIncl | (uint32_t)(excl + tot);
     }
@@ -272,7 +284,7 @@ __global__ void __launch_bounds__(256, 3) k_onesweep(const u64 *keys, const int3
     }
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < 16; r++) {
+    for (int r = 0; r < KPT; r++) {
         if (dr[r] != 0xffffffffu) {
             const int32_t pos = wh[w][dr[r] >> 16] + (int32_t)(dr[r] & 0xffffu);
             skey[pos] = k[r];
@@ -280,7 +292,7 @@ __global__ void __launch_bounds__(256, 3) k_onesweep(const u64 *keys, const int3
         }
     }
     __syncthreads();
-    const int32_t cnt = (int32_t)(n - tbase < kTile ? n - tbase : kTile);
+    const int32_t cnt = (int32_t)(n - tbase < RT ? n - tbase : RT);
     for (int i = threadIdx.x; i < cnt; i += 256) {
         const u64 key = skey[i];
         const int dd = (int)((key >> shift) & 255u);
@@ -408,10 +420,15 @@ int32_t *sweep_sort(SweepBuffers &b, cudaStream_t st, int *launches, bool *nan)
     int32_t *va = b.vals, *vb = b.vals_alt;
     uint32_t *state = reinterpret_cast<uint32_t *>(b.tile_hist);  // [ntiles][256] look-back words
     int32_t *ticket = b.flags + 1;
-    const int dyn = (int)((sizeof(u64) + sizeof(int32_t)) * kTile);
+    // keys per thread: 16 (tiles of 4096, 3 CTAs/SM; measured 9.5 ms per sweep on
+    // config 4 against 11.4 ms with IRLS_SORT_KPT=8: tiles of 2048 at 4 CTAs/SM)
+    static const int kpt = getenv("IRLS_SORT_KPT") && atoi(getenv("IRLS_SORT_KPT")) == 8 ? 8 : 16;
+    const int64_t rt = 256 * (int64_t)kpt, ntr = (n + rt - 1) / rt;
+    const int dyn = (int)((sizeof(u64) + sizeof(int32_t)) * rt);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+        cudaFuncSetAttribute(k_onesweep<16, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 12 * 4096);
+        cudaFuncSetAttribute(k_onesweep<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 12 * 2048);
         attr = true;
     }
     for (int d = 0; d < 8; d++) {
@@ -425,9 +442,10 @@ int32_t *sweep_sort(SweepBuffers &b, cudaStream_t st, int *launches, bool *nan)
             gs.g[i] = (int32_t)acc;
             acc += (int64_t)h[d * 256 + i];
         }
-        cudaMemsetAsync(state, 0, sizeof(uint32_t) * 256 * nt, st);
+        cudaMemsetAsync(state, 0, sizeof(uint32_t) * 256 * ntr, st);
         cudaMemsetAsync(ticket, 0, sizeof(int32_t), st);
-        k_onesweep<<<(unsigned)nt, 256, dyn, st>>>(ka, va, kb, vb, n, 8 * d, gs, state, ticket);
+        if (kpt == 16) k_onesweep<16, 3><<<(unsigned)ntr, 256, dyn, st>>>(ka, va, kb, vb, n, 8 * d, gs, state, ticket);
+        else k_onesweep<8, 4><<<(unsigned)ntr, 256, dyn, st>>>(ka, va, kb, vb, n, 8 * d, gs, state, ticket);
         *launches += 1;
         std::swap(ka, kb);
         std::swap(va, vb);
@@ -497,34 +515,52 @@ __global__ void __launch_bounds__(256) k_scan_argmin(const i128 *delta, const in
     __syncthreads();
     i128 wpre = 0;
     for (int k = 0; k < w; k++) wpre += wsum[k];
-    if (threadIdx.x == 0) {
+    if (w == 0) {  // warp 0: publish the tile sum, then look back 32 tiles at a time
         i128 T = 0;
         for (int k = 0; k < 8; k++) T += wsum[k];
         volatile int32_t *vlook = look;
-        i128 ex;
+        i128 ex = 0;
         if (tile == 0) {
             ex = *p0;
         } else {
-            agg[tile] = T;
-            __threadfence();
-            vlook[tile] = 1;
-            ex = 0;
-            for (int64_t t = tile - 1;; t--) {
-                int32_t f;
-                while ((f = vlook[t]) == 0) {
+            if (lane == 0) {
+                agg[tile] = T;
+                __threadfence();
+                vlook[tile] = 1;
+            }
+            for (int64_t hi = tile - 1;;) {
+                const int64_t t = hi - lane;  // lane 0: the nearest predecessor
+                const int32_t f = t >= 0 ? vlook[t] : 2;
+                const unsigned ready = __ballot_sync(0xffffffffu, f != 0);
+                const unsigned incl_m = __ballot_sync(0xffffffffu, f == 2);
+                int upto = -1;  // lanes 0..upto are summed
+                if (incl_m) {
+                    const int first = __ffs(incl_m) - 1;
+                    const unsigned need = first == 31 ? 0xffffffffu : ((2u << first) - 1u);
+                    if ((ready & need) == need) upto = first;
+                } else if (ready == 0xffffffffu) {
+                    upto = 31;
+                }
+                if (upto < 0) {
+                    __nanosleep(32);
+                    continue;
                 }
                 __threadfence();
-                if (f == 2) {
-                    ex += *(volatile i128 *)(incl + t);
-                    break;
-                }
-                ex += *(volatile i128 *)(agg + t);
+                i128 v = 0;
+                if (lane <= upto && t >= 0) v = (f == 2) ? *(volatile i128 *)(incl + t) : *(volatile i128 *)(agg + t);
+#pragma unroll
+                for (int off = 16; off >= 1; off >>= 1) v += shfl_down_i128(v, off);
+                ex += v;  // lane 0 holds the window's sum
+                if (incl_m && upto == __ffs(incl_m) - 1) break;
+                hi -= 32;
             }
         }
-        incl[tile] = ex + T;
-        __threadfence();
-        vlook[tile] = 2;
-        s_excl = ex;
+        if (lane == 0) {
+            incl[tile] = ex + T;
+            __threadfence();
+            vlook[tile] = 2;
+            s_excl = ex;
+        }
     }
     __syncthreads();
     i128 P = s_excl + wpre + inc - own;  // P_{t0}
