@@ -1,5 +1,6 @@
 """Randomised parity sweep: random grid shapes / CSR graphs, random options
-(PCG form, norm, warm/cold, rtol, cap, loop mode, trace, fixed-point exit),
+(PCG form, norm, warm/cold, rtol, cap, loop mode, trace, fixed-point exit,
+block-Jacobi block size where compatible),
 single rank and virtual groups — every case compared with the oracle
 bitwise (reports, x^(T), sweep).  usage: python tools/fuzz_parity.py [cases] [seed]"""
 import os
@@ -34,11 +35,14 @@ for case in range(cases):
              warm_start=int(rng.integers(0, 2)), cg_rtol=float(rng.choice([1e-3, 1e-6, 1e-10])),
              cg_max_iter=int(rng.choice([5, 50, 500])), loop_mode=int(rng.integers(0, 2)),
              record_trace=int(rng.integers(0, 2)), fixed_point_exit=int(rng.integers(0, 2)))
+    if o["cg_variant"] == 0 and not o["record_trace"] and rng.integers(0, 2):
+        o["block_size"] = int(rng.choice([1, 3, 16, 64, 200]))
     try:
         m = I.MinCut.from_spec(spec, I.options(**o))
         reps, tot = m.irls_solve(I.IRLS_FROM_SCRATCH)
         S = oracle.Solver(oracle.Graph(spec), T=T, cg_norm=o["cg_norm"], warm_start=bool(o["warm_start"]),
-                          cg_rtol=o["cg_rtol"], cg_max_iter=o["cg_max_iter"], cg_variant=o["cg_variant"])
+                          cg_rtol=o["cg_rtol"], cg_max_iter=o["cg_max_iter"], cg_variant=o["cg_variant"],
+                          block_size=o.get("block_size", 0))
         _, oreps = S.run(record=False)
         ok = [r["cg_iters"] for r in reps] == [r["cg_iters"] for r in oreps]
         ok = ok and [r["rel_res"] for r in reps] == [r["rel_res"] for r in oreps]
@@ -46,6 +50,7 @@ for case in range(cases):
         side, order, k, cut = m.irls_sweep_cut(order=True)
         sw = S.sweep()
         ok = ok and k == sw.k and cut == sw.cut_value and np.array_equal(side, sw.side)
+        ok = ok and np.array_equal(order.astype(np.int64), sw.order)
         m.close()
     except Exception as e:  # noqa: BLE001
         ok = False
@@ -69,13 +74,16 @@ for case in range(vcases):
     o = dict(T=T, cg_variant=int(rng.integers(0, 2)), p2p=int(rng.integers(0, 2)),
              record_trace=int(rng.integers(0, 2)), warm_start=int(rng.integers(0, 2)),
              fixed_point_exit=int(rng.integers(0, 2)))
+    if o["cg_variant"] == 0 and not o["p2p"] and not o["record_trace"] and rng.integers(0, 2):
+        o["block_size"] = int(rng.choice([8, 64]))
     try:
         g = I.VGroup(spec, world, I.options(**o))
     except I.IrlsError:
         continue  # an unaligned partition is refused by design
     try:
         reps, tot = g.irls_vgroup_solve(I.IRLS_FROM_SCRATCH)
-        S = oracle.Solver(oracle.Graph(spec), T=T, warm_start=bool(o["warm_start"]), cg_variant=o["cg_variant"])
+        S = oracle.Solver(oracle.Graph(spec), T=T, warm_start=bool(o["warm_start"]), cg_variant=o["cg_variant"],
+                          block_size=o.get("block_size", 0))
         _, oreps = S.run(record=False)
         ok = [r["cg_iters"] for r in reps] == [r["cg_iters"] for r in oreps]
         ok = ok and np.array_equal(g.irls_vgroup_get_potentials().view(np.uint64), S.x().view(np.uint64))

@@ -1,5 +1,4 @@
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_k1.log 2>&1
-echo "== no prefetch"; python tools/kbench.py --config config4 --solves 2
-echo "== prefetch"; IRLS_K1_PREFETCH=1 python tools/kbench.py --config config4 --solves 2
-timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-two-level > gpurun_out/bench_k1.json 2>/dev/null
-python -c "import json; d=json.loads(open('gpurun_out/bench_k1.json').read().strip().splitlines()[-1]); print(d['value'], d['ms_per_step'], d['roofline']['kernels'])"
+for K in 0 2 3; do echo "== IRLS_K1=$K"; IRLS_K1=$K python tools/kbench.py --config config4 --solves 1 | grep -E "K1|solve"; done
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_vgroup.py -x -q -k "512" 2>&1 | tail -2
+IRLS_K1=3 timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "512" 2>&1 | tail -2
