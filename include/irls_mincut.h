@@ -314,6 +314,8 @@ typedef struct {
     int64_t n_nonterminal;   /* n~ (global) */
     int64_t n_links;         /* |E~| with c > 0 (global) */
     int64_t n_local;         /* non-terminals owned by this rank */
+    int64_t sweep_sorted;    /* nodes the last rank-0 sweep radix-sorted: n~ (full sort), or the
+                                candidate buckets' nodes of the branch-and-bound sweep */
 } irls_stats;
 irls_status irls_get_stats(irls_ctx *ctx, irls_stats *stats);
 

@@ -1040,6 +1040,7 @@ extern "C" irls_status irls_get_stats(irls_ctx *c, irls_stats *o)
     o->n_nonterminal = c->n_glob;
     o->n_links = c->n_links;
     o->n_local = c->n_own;
+    o->sweep_sorted = c->sweep_sorted;
     return IRLS_OK;
 }
 

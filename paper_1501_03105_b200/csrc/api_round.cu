@@ -31,10 +31,11 @@ static irls_status alloc_sweep(irls_ctx *c)
     b.tile_argmin = dalloc<int64_t>(c, nt);
     b.flags = dalloc<int32_t>(c, 4);
     b.k_out = dalloc<int64_t>(c, 1);
+    b.lastv = dalloc<int32_t>(c, 1);
     b.side = dalloc<uint8_t>(c, c->n_total);
     c->order_out = dalloc<int32_t>(c, n);
     if (!b.keys || !b.keys_alt || !b.vals || !b.vals_alt || !b.tile_hist || !b.tile_off || !b.scan_tmp ||
-        !b.digit_hist || !b.delta || !b.tile_sum || !b.tile_incl || !b.qcs_tile || !b.tile_min || !b.tile_argmin || !b.flags || !b.k_out || !b.side ||
+        !b.digit_hist || !b.delta || !b.tile_sum || !b.tile_incl || !b.qcs_tile || !b.tile_min || !b.tile_argmin || !b.flags || !b.k_out || !b.lastv || !b.side ||
         !c->order_out)
         return fail(c, IRLS_ERR_OOM, "sweep buffers");
     return IRLS_OK;
@@ -80,6 +81,163 @@ extern "C" irls_status irls_sweep_cut(irls_ctx *c, uint8_t *side, int32_t *order
     return IRLS_OK;
 }
 
+// Branch-and-bound sweep (sweep_bb.cu) for callers that do not need the order:
+// k and the k-th node (x*, v*) of the order, exactly as the full sort's scan
+// finds them (k_out, lastv written on the device).  *done = false (nothing
+// decided) when the bound prunes too little or a buffer is not available;
+// the caller then runs the full sort.
+static irls_status sweep_bb(irls_ctx *c, const double *xfull, int *launches, bool *done)
+{
+    *done = false;
+    cudaStream_t st = c->stream;
+    SweepBuffers &b = c->sb;
+    const int64_t n = c->n_glob;
+    const int32_t nb = 4096, ns = 16384;
+    typedef unsigned long long u64;
+    typedef __int128 i128;
+    const int G = bb_num_ctas();
+    std::vector<void *> tmp;
+    auto talloc = [&](size_t bytes) -> void * {
+        void *p = nullptr;
+        if (cudaMallocAsync(&p, std::max<size_t>(bytes, 16), st) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        tmp.push_back(p);
+        return p;
+    };
+    struct Free {
+        std::vector<void *> *t;
+        cudaStream_t s;
+        ~Free() { for (void *p : *t) cudaFreeAsync(p, s); }
+    } fr{&tmp, st};
+    u64 *skey = (u64 *)talloc(8 * ns), *spk = (u64 *)talloc(8 * nb);
+    int32_t *sid = (int32_t *)talloc(4 * ns), *spi = (int32_t *)talloc(4 * nb);
+    u64 *part = (u64 *)talloc(8 * 4 * (size_t)G * nb);
+    void *table = talloc(bb_table_bytes());
+    i128 *pqcs = (i128 *)talloc(16 * (size_t)G);
+    unsigned *cnt = (unsigned *)talloc(4 * nb);
+    i128 *bsum = (i128 *)talloc(16 * nb), *bneg = (i128 *)talloc(16 * nb), *p0 = (i128 *)talloc(16);
+    int16_t *slot_of = (int16_t *)talloc(2 * nb);
+    if (!skey || !spk || !sid || !spi || !part || !table || !pqcs || !cnt || !bsum || !bneg || !p0 || !slot_of)
+        return IRLS_OK;
+    // buckets, then one pass: counts, exact sums, negative bounds, P_0, NaN flag
+    bb_sample_sort(xfull, n, ns, nb, skey, sid, spk, spi, table, st);
+    if (c->kind == 0)
+        bb_pass_stencil(stencil_args(c, true), n, c->F, xfull, spk, spi, table, nb, part, pqcs, b.flags, st);
+    else bb_pass_sell(sell_args_full(c), c->F, xfull, spk, spi, table, nb, part, pqcs, b.flags, st);
+    bb_reduce(part, pqcs, nb, qfix_host(c->c_st, c->F), cnt, bsum, bneg, p0, st);
+    *launches += 5;
+    std::vector<unsigned> hc(nb);
+    std::vector<i128> hsum(nb), hneg(nb);
+    i128 hp0 = 0;
+    int32_t hflag = 0;
+    CK(cudaMemcpyAsync(hc.data(), cnt, 4 * nb, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hsum.data(), bsum, 16 * nb, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hneg.data(), bneg, 16 * nb, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&hp0, p0, 16, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&hflag, b.flags, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (hflag) return fail(c, IRLS_ERR_BAD_POTENTIAL, "NaN in potentials");
+    std::vector<int64_t> hs(nb + 1, 0);
+    for (int i = 0; i < nb; i++) hs[i + 1] = hs[i] + hc[i];
+    if (hs[nb] != n) return fail(c, IRLS_ERR_CUDA, "sweep buckets do not cover the nodes");
+    // P at the bucket boundaries; the first minimum among them
+    std::vector<i128> Pb(nb + 1);
+    Pb[0] = hp0;
+    for (int i = 0; i < nb; i++) Pb[i + 1] = Pb[i] + hsum[i];
+    i128 best = Pb[0];
+    int64_t barg = 0;
+    int bi_best = 0;
+    for (int i = 1; i <= nb; i++)
+        if (Pb[i] < best) {  // equal values keep the earlier position
+            best = Pb[i];
+            barg = hs[i];
+            bi_best = i;
+        }
+    // candidates: buckets whose lower bound reaches the best boundary value,
+    // and the bucket holding position barg - 1 (for the k-th node)
+    std::vector<int32_t> cand;
+    int holder = -1;
+    if (barg > 0)
+        for (int i = bi_best - 1; i >= 0; i--)
+            if (hc[i] > 0) {
+                holder = i;
+                break;
+            }
+    for (int i = 0; i < nb; i++)
+        if ((hc[i] > 1 && Pb[i] + hneg[i] <= best) || i == holder) cand.push_back(i);
+    const int32_t nc = (int32_t)cand.size();
+    std::vector<int64_t> dst((size_t)nc + 1, 0), cpos(std::max(nc, 1));
+    std::vector<u64> cur(std::max(nc, 1));
+    std::vector<i128> cP(std::max(nc, 1));
+    std::vector<int16_t> hslot(nb, -1);
+    for (int j = 0; j < nc; j++) {
+        dst[j + 1] = dst[j] + hc[cand[j]];
+        cur[j] = (u64)dst[j];
+        cpos[j] = hs[cand[j]];
+        cP[j] = Pb[cand[j]];
+        hslot[cand[j]] = (int16_t)j;
+    }
+    const int64_t C = dst[nc];
+    if (C > n / 4) return IRLS_OK;  // pruning failed: the full path
+    const size_t Cs = (size_t)std::max<int64_t>(C, 1);
+    u64 *ck = (u64 *)talloc(8 * Cs), *k1 = (u64 *)talloc(8 * Cs), *k2 = (u64 *)talloc(8 * Cs);
+    u64 *cursor = (u64 *)talloc(8 * (size_t)std::max(nc, 1));
+    int32_t *cid = (int32_t *)talloc(4 * Cs), *v1 = (int32_t *)talloc(4 * Cs), *v2 = (int32_t *)talloc(4 * Cs);
+    i128 *cdel = (i128 *)talloc(16 * Cs);
+    u64 *dh = (u64 *)talloc(2 * 8 * 8 * 256);
+    int64_t *ddst = (int64_t *)talloc(8 * ((size_t)nc + 1)), *dpos = (int64_t *)talloc(8 * (size_t)std::max(nc, 1));
+    i128 *dP = (i128 *)talloc(16 * (size_t)std::max(nc, 1)), *cmin = (i128 *)talloc(16 * (size_t)std::max(nc, 1));
+    int64_t *carg = (int64_t *)talloc(8 * (size_t)std::max(nc, 1));
+    if (!ck || !k1 || !k2 || !cursor || !cid || !v1 || !v2 || !cdel || !dh || !ddst || !dpos || !dP || !cmin || !carg)
+        return IRLS_OK;
+    CK(cudaMemcpyAsync(slot_of, hslot.data(), 2 * nb, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(cursor, cur.data(), 8 * (size_t)std::max(nc, 1), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ddst, dst.data(), 8 * ((size_t)nc + 1), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dpos, cpos.data(), 8 * (size_t)std::max(nc, 1), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dP, cP.data(), 16 * (size_t)std::max(nc, 1), cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(dh, 0, 2 * 8 * 8 * 256, st));
+    CK(cudaMemsetAsync(b.flags + 2, 0, sizeof(int32_t), st));
+    int32_t *sorted = v1;
+    if (nc > 0) {
+        if (c->kind == 0)
+            bb_extract_stencil(stencil_args(c, true), n, c->F, xfull, spk, spi, table, nb, slot_of, cursor, ck, cid,
+                               cdel, k1, v1, dh, st);
+        else
+            bb_extract_sell(sell_args_full(c), c->F, xfull, spk, spi, table, nb, slot_of, cursor, ck, cid, cdel, k1,
+                            v1, dh, st);
+        // the radix sort of sweep.cu is stable on the key alone; ties must
+        // leave in ascending id, so: (A) sort positions by id, (B) gather
+        // the keys in that order and sort them (values: compact positions)
+        SweepBuffers tb = b;
+        tb.n = C;
+        tb.keys = k1;
+        tb.keys_alt = k2;
+        tb.vals = v1;
+        tb.vals_alt = v2;
+        tb.digit_hist = dh;
+        bool nan = false;
+        const int32_t *perm = sweep_sort(tb, st, launches, &nan);
+        int32_t *pin = perm == v1 ? v2 : v1;  // the other value buffer; k1, k2 are free
+        int32_t *spare = perm == v1 ? v1 : v2;
+        bb_gather(ck, perm, C, k1, pin, dh + 8 * 256, st);
+        tb.keys = k1;
+        tb.keys_alt = k2;
+        tb.vals = pin;
+        tb.vals_alt = spare;
+        tb.digit_hist = dh + 8 * 256;
+        sorted = sweep_sort(tb, st, launches, &nan);
+        bb_cand_scan(cdel, sorted, ddst, dpos, dP, nc, cmin, carg, st);
+        *launches += 4;  // cell flags, extract, gather, candidate scan
+    }
+    bb_finish(cmin, carg, nc, best, barg, ddst, dpos, sorted, cid, b.k_out, b.lastv, b.flags, st);
+    *launches += 1;
+    c->sweep_sorted = C;
+    *done = true;
+    return IRLS_OK;
+}
+
 irls_status sweep_rank0(irls_ctx *c, const double *xfull, uint8_t *side, int32_t *order, int64_t *k,
                                double *cut_value)
 {
@@ -91,15 +249,27 @@ irls_status sweep_rank0(irls_ctx *c, const double *xfull, uint8_t *side, int32_t
     c->launches = 0;
     SweepBuffers &b = c->sb;
     CK(cudaMemsetAsync(b.flags, 0, sizeof(int32_t) * 4, st));
-    CK(cudaMemsetAsync(b.digit_hist, 0, sizeof(unsigned long long) * 8 * 256, st));
-    if (c->kind == 0) sweep_prep_stencil(stencil_args(c, true), n, c->F, xfull, b, st);
-    else sweep_prep_sell(sell_args_full(c), c->F, xfull, b, st);
-    launches++;
-    bool nan = false;
-    int32_t *ord = sweep_sort(b, st, &launches, &nan);
-    if (nan) return fail(c, IRLS_ERR_BAD_POTENTIAL, "NaN in potentials");
-    sweep_scan_argmin(b, ord, qfix_host(c->c_st, c->F), st);
-    launches += 3;
+    // without an order to return, large graphs take the branch-and-bound sweep
+    bool bb_done = false;
+    int32_t *ord = nullptr;
+    c->sweep_sorted = 0;
+    if (!order && n >= (1 << 20) && !getenv("IRLS_SWEEP_FULL")) {
+        s = sweep_bb(c, xfull, &launches, &bb_done);
+        if (s) return s;
+    }
+    if (!bb_done) {
+        CK(cudaMemsetAsync(b.flags, 0, sizeof(int32_t) * 4, st));
+        CK(cudaMemsetAsync(b.digit_hist, 0, sizeof(unsigned long long) * 8 * 256, st));
+        if (c->kind == 0) sweep_prep_stencil(stencil_args(c, true), n, c->F, xfull, b, st);
+        else sweep_prep_sell(sell_args_full(c), c->F, xfull, b, st);
+        launches++;
+        bool nan = false;
+        ord = sweep_sort(b, st, &launches, &nan);
+        if (nan) return fail(c, IRLS_ERR_BAD_POTENTIAL, "NaN in potentials");
+        sweep_scan_argmin(b, ord, qfix_host(c->c_st, c->F), st);
+        launches += 3;
+        c->sweep_sorted = n;
+    }
     RedArgs ra;
     ra.part = c->part;
     ra.slots = c->slots_local;
@@ -127,6 +297,8 @@ irls_status sweep_rank0(irls_ctx *c, const double *xfull, uint8_t *side, int32_t
     int64_t hk = 0;
     if (n > 0) CK(cudaMemcpyAsync(slots, c->slots_local, sizeof(slots), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&hk, b.k_out, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    int32_t hf2 = 0;
+    if (bb_done) CK(cudaMemcpyAsync(&hf2, b.flags + 2, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     if (order && n > 0) {
         sweep_order_out(ord, c->kind == 1 ? c->orig_dev : nullptr, c->order_out, n, st);
         launches++;
@@ -134,6 +306,7 @@ irls_status sweep_rank0(irls_ctx *c, const double *xfull, uint8_t *side, int32_t
     }
     if (side) CK(cudaMemcpyAsync(side, b.side, c->n_total, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (hf2) return fail(c, IRLS_ERR_CUDA, "branch-and-bound sweep: the k-th node is in no candidate");
     if (n == 0) hk = 0;
     c->sweep_k = hk;
     c->sweep_cut = irls_combine_slots(slots) + c->c_st;

@@ -153,6 +153,7 @@ struct irls_ctx {
     bool sweep_valid = false;
     int64_t sweep_k = 0;
     double sweep_cut = 0.0;
+    int64_t sweep_sorted = 0;  // nodes the last sweep radix-sorted
 
     // two-level rounding (rank 0)
     irls::TLBuffers tl{};

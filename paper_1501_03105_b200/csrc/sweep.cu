@@ -12,6 +12,7 @@
 //   side/cut  side[v] = rank[v] < k; cut value recomputed by C3 (+ c_st)
 #include <algorithm>
 #include "kernels.h"
+#include "sweep_delta.cuh"
 
 namespace irls {
 
@@ -60,20 +61,9 @@ __device__ __forceinline__ void tile_sum_i128(i128 v, i128 *out)
 }
 
 // ---------------------------------------------------------------------------
-// prep: keys, ids, the exact delta_v in id order, global digit histograms
+// prep: keys, ids, the exact delta_v in id order (sweep_delta.cuh), global
+// digit histograms; delta is written coalesced in id order (the scan gathers it)
 // ---------------------------------------------------------------------------
-// delta_v = sum over neighbours u of (u after v ? +Q(c_uv) : -Q(c_uv)) +
-// Q(ct_v) - Q(cs_v), where "u after v" in the total order (x desc, id asc,
-// A14) is x_u < x_v || (x_u == x_v && u > v) — the same predicate as
-// rank_u > rank_v, evaluated from the potentials, so delta needs no rank
-// array and is written coalesced in id order (the scan gathers it).
-__device__ __forceinline__ double canon(double x) { return x == 0.0 ? 0.0 : x; }  // -0.0 -> +0.0
-
-__device__ __forceinline__ bool after(double xu, int64_t u, double xv, int64_t v)
-{
-    return xu < xv || (xu == xv && u > v);
-}
-
 template <class NB>
 __device__ __forceinline__ void prep_tile(int64_t N, int32_t F, const double *x, u64 *keys, int32_t *vals,
                                           i128 *delta, u64 *digit_hist, i128 *qcs_tile, int32_t *flags, NB nb)
@@ -90,7 +80,7 @@ __device__ __forceinline__ void prep_tile(int64_t N, int32_t F, const double *x,
         const double xr = x[v];
         nan |= isnan(xr);
         const double xv = canon(xr);
-        const u64 key = ~dkey_asc(xv);  // ascending key order = x descending
+        const u64 key = sweep_key(xv);  // ascending key order = x descending
         keys[v] = key;
         vals[v] = (int32_t)v;           // ties keep ascending id (stable sort)
 #pragma unroll
@@ -114,28 +104,7 @@ __global__ void __launch_bounds__(256) k_sweep_prep_stencil(StencilArgs s, int64
                                                             i128 *qcs_tile, int32_t *flags)
 {
     prep_tile(N, F, x, keys, vals, delta, digit_hist, qcs_tile, flags,
-              [&](int64_t v, double xv, i128 &d, i128 &qs) {
-                  const uint32_t uv = (uint32_t)v;
-                  const uint32_t t1 = fdiv(uv, s.fd_nx);
-                  const int32_t xx = (int32_t)(uv - t1 * (uint32_t)s.nx);
-                  const uint32_t zz = fdiv(t1, s.fd_ny);
-                  const int32_t y = (int32_t)(t1 - zz * (uint32_t)s.ny), z = (int32_t)zz;
-#define NB(cond, w, cap)                                                           \
-    if (cond) {                                                                    \
-        const i128 q = qfix(cap, F);                                               \
-        d += after(canon(x[w]), w, xv, v) ? q : -q;                                \
-    }
-                  NB(z > 0, v - s.P, s.cz[v - s.P]);
-                  NB(y > 0, v - s.nx, s.cy[v - s.nx]);
-                  NB(xx > 0, v - 1, s.cx[v - 1]);
-                  NB(xx < s.nx - 1, v + 1, s.cx[v]);
-                  NB(y < s.ny - 1, v + s.nx, s.cy[v]);
-                  NB(z < s.nz - 1, v + s.P, s.cz[v]);
-#undef NB
-                  qs = qfix(s.cs[v], F);
-                  d += qfix(s.ct[v], F);
-                  d -= qs;
-              });
+              [&](int64_t v, double xv, i128 &d, i128 &qs) { delta_stencil(s, F, x, v, xv, d, qs); });
 }
 
 __global__ void __launch_bounds__(256) k_sweep_prep_sell(SellArgs s, int32_t F, const double *x, u64 *keys,
@@ -143,21 +112,7 @@ __global__ void __launch_bounds__(256) k_sweep_prep_sell(SellArgs s, int32_t F, 
                                                          int32_t *flags)
 {
     prep_tile(s.n, F, x, keys, vals, delta, digit_hist, qcs_tile, flags,
-              [&](int64_t v, double xv, i128 &d, i128 &qs) {
-                  const int64_t sl = v / kSell;
-                  const int64_t e0 = s.slice_ptr[sl] + (v % kSell);
-                  const int32_t W = (int32_t)((s.slice_ptr[sl + 1] - s.slice_ptr[sl]) / kSell);
-                  for (int32_t k = 0; k < W; k++) {
-                      const int64_t idx = e0 + kSell * (int64_t)k;
-                      const int32_t u = s.col[idx];
-                      if (u < 0) break;
-                      const i128 q = qfix(s.c[idx], F);
-                      d += after(canon(x[u]), u, xv, v) ? q : -q;
-                  }
-                  qs = qfix(s.cs[v], F);
-                  d += qfix(s.ct[v], F);
-                  d -= qs;
-              });
+              [&](int64_t v, double xv, i128 &d, i128 &qs) { delta_sell(s, F, x, v, xv, d, qs); });
 }
 
 // ---------------------------------------------------------------------------
@@ -710,12 +665,12 @@ __device__ __forceinline__ bool in_first_k(double xv, int64_t v, bool any, doubl
 }
 
 __global__ void __launch_bounds__(kThreads) k_side_cross_x_stencil(StencilArgs s, int64_t N, const double *x,
-                                                                   const int32_t *ord, const int64_t *kptr,
-                                                                   uint8_t *side, RedArgs ra)
+                                                                   const int32_t *ord, const int32_t *lastv,
+                                                                   const int64_t *kptr, uint8_t *side, RedArgs ra)
 {
     const int64_t k = *kptr;
     const bool any = k > 0;
-    const int64_t vs = any ? ord[k - 1] : 0;
+    const int64_t vs = any ? (ord ? ord[k - 1] : *lastv) : 0;
     const double xs = any ? canon(x[vs]) : 0.0;
     double acc[1] = {0.0};
     const int64_t base = (int64_t)blockIdx.x * kChunk;
@@ -755,12 +710,12 @@ __global__ void __launch_bounds__(kThreads) k_side_cross_x_stencil(StencilArgs s
 }
 
 __global__ void __launch_bounds__(kThreads) k_side_cross_x_sell(SellArgs s, const double *x, const int32_t *ord,
-                                                                const int64_t *kptr, const int64_t *orig,
-                                                                uint8_t *side, RedArgs ra)
+                                                                const int32_t *lastv, const int64_t *kptr,
+                                                                const int64_t *orig, uint8_t *side, RedArgs ra)
 {
     const int64_t k = *kptr;
     const bool any = k > 0;
-    const int64_t vs = any ? ord[k - 1] : 0;
+    const int64_t vs = any ? (ord ? ord[k - 1] : *lastv) : 0;
     const double xs = any ? canon(x[vs]) : 0.0;
     double acc[1] = {0.0};
     const int64_t base = (int64_t)blockIdx.x * kChunk;
@@ -794,16 +749,16 @@ __global__ void __launch_bounds__(kThreads) k_side_cross_x_sell(SellArgs s, cons
 void sweep_side_cross_x_stencil(const StencilArgs &s, int64_t N, const double *x, const int32_t *ord, SweepBuffers &b,
                                 const RedArgs &ra, cudaStream_t st)
 {
-    k_side_cross_x_stencil<<<(unsigned)((N + kChunk - 1) / kChunk), kThreads, 0, st>>>(s, N, x, ord, b.k_out,
-                                                                                      b.side, ra);
+    k_side_cross_x_stencil<<<(unsigned)((N + kChunk - 1) / kChunk), kThreads, 0, st>>>(s, N, x, ord, b.lastv,
+                                                                                      b.k_out, b.side, ra);
 }
 
 void sweep_side_cross_x_sell(const SellArgs &s, const double *x, const int32_t *ord, const int64_t *orig,
                              SweepBuffers &b, const RedArgs &ra, cudaStream_t st)
 {
     if (s.n == 0) return;
-    k_side_cross_x_sell<<<(unsigned)((s.n + kChunk - 1) / kChunk), kThreads, 0, st>>>(s, x, ord, b.k_out, orig,
-                                                                                     b.side, ra);
+    k_side_cross_x_sell<<<(unsigned)((s.n + kChunk - 1) / kChunk), kThreads, 0, st>>>(s, x, ord, b.lastv, b.k_out,
+                                                                                     orig, b.side, ra);
 }
 
 void sweep_side_cross_stencil(const StencilArgs &s, int64_t N, SweepBuffers &b, const RedArgs &ra, cudaStream_t st)

@@ -109,7 +109,8 @@ class irls_lambda2_report(C.Structure):
 
 class irls_stats(C.Structure):
     _fields_ = [("launches", C.c_int64), ("cg_iters", C.c_int64), ("n_nonterminal", C.c_int64),
-                ("n_links", C.c_int64), ("n_local", C.c_int64)]
+                ("n_links", C.c_int64), ("n_local", C.c_int64),
+                ("sweep_sorted", C.c_int64)]
 
 
 _lib = None

@@ -39,7 +39,8 @@ def main():
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     print(json.dumps({"config": a.config, "sweep_ms_median": statistics.median(ts), "sweep_ms": ts, "k": k,
-                      "cut": cut, "launches": m.irls_get_stats()["launches"]}))
+                      "cut": cut, "launches": m.irls_get_stats()["launches"],
+                      "sorted": m.irls_get_stats()["sweep_sorted"]}))
 
 
 if __name__ == "__main__":
