@@ -111,8 +111,8 @@ static irls_status sweep_bb(irls_ctx *c, const double *xfull, int *launches, boo
         cudaStream_t s;
         ~Free() { for (void *p : *t) cudaFreeAsync(p, s); }
     } fr{&tmp, st};
-    u64 *skey = (u64 *)talloc(8 * ns), *spk = (u64 *)talloc(8 * nb);
-    int32_t *sid = (int32_t *)talloc(4 * ns), *spi = (int32_t *)talloc(4 * nb);
+    u64 *skey = (u64 *)talloc(8 * 2 * ns), *spk = (u64 *)talloc(8 * nb);
+    int32_t *sid = (int32_t *)talloc(4 * (2 * ns + (size_t)ns * (ns / 1024))), *spi = (int32_t *)talloc(4 * nb);
     u64 *part = (u64 *)talloc(8 * 4 * (size_t)G * nb);
     void *table = talloc(bb_table_bytes());
     i128 *pqcs = (i128 *)talloc(16 * (size_t)G);
@@ -127,7 +127,7 @@ static irls_status sweep_bb(irls_ctx *c, const double *xfull, int *launches, boo
         bb_pass_stencil(stencil_args(c, true), n, c->F, xfull, spk, spi, table, nb, part, pqcs, b.flags, st);
     else bb_pass_sell(sell_args_full(c), c->F, xfull, spk, spi, table, nb, part, pqcs, b.flags, st);
     bb_reduce(part, pqcs, nb, qfix_host(c->c_st, c->F), cnt, bsum, bneg, p0, st);
-    *launches += 5;
+    *launches += 7;  // sample, rank, rank scatter, splitters, table, pass, reduce
     std::vector<unsigned> hc(nb);
     std::vector<i128> hsum(nb), hneg(nb);
     i128 hp0 = 0;
@@ -207,6 +207,8 @@ static irls_status sweep_bb(irls_ctx *c, const double *xfull, int *launches, boo
         else
             bb_extract_sell(sell_args_full(c), c->F, xfull, spk, spi, table, nb, slot_of, cursor, ck, cid, cdel, k1,
                             v1, dh, st);
+        if (c->kind == 0) bb_cdelta_stencil(stencil_args(c, true), c->F, xfull, cid, C, cdel, st);
+        else bb_cdelta_sell(sell_args_full(c), c->F, xfull, cid, C, cdel, st);
         // the radix sort of sweep.cu is stable on the key alone; ties must
         // leave in ascending id, so: (A) sort positions by id, (B) gather
         // the keys in that order and sort them (values: compact positions)
@@ -229,7 +231,7 @@ static irls_status sweep_bb(irls_ctx *c, const double *xfull, int *launches, boo
         tb.digit_hist = dh + 8 * 256;
         sorted = sweep_sort(tb, st, launches, &nan);
         bb_cand_scan(cdel, sorted, ddst, dpos, dP, nc, cmin, carg, st);
-        *launches += 4;  // cell flags, extract, gather, candidate scan
+        *launches += 5;  // cell flags, extract, deltas, gather, candidate scan
     }
     bb_finish(cmin, carg, nc, best, barg, ddst, dpos, sorted, cid, b.k_out, b.lastv, b.flags, st);
     *launches += 1;

@@ -380,17 +380,24 @@ __device__ __forceinline__ double rw_g(double c, double d, double eps2)
     return (c * c) / w;
 }
 
-// A15 fixed point: Q(c) = rint(c 2^F) as an exact 128-bit integer (c >= 0).
+// A15 fixed point: Q(c) = rint(c 2^F) as an exact 128-bit integer (c >= 0,
+// finite).  Integer arithmetic on the bits of c: c = m 2^(e - 1075) (m with
+// its implicit bit; subnormals e = 1, no implicit bit), so c 2^F = m 2^sh,
+// sh = e - 1075 + F.  sh >= 0: the exact left shift (F is chosen so the
+// result stays below 2^124).  sh < 0: m / 2^-sh rounded half to even — the
+// value rint gives for the exact product c 2^F (a power-of-two scaling,
+// exact in double unless it underflows, where both give 0).  c = 0 gives 0.
 __device__ __forceinline__ __int128 qfix(double c, int32_t F)
 {
-    if (c == 0.0) return 0;
-    // c * 2^F with an exact power-of-two factor (the same correctly rounded
-    // value as scalbn; the factor is built from its exponent bits)
-    const double v = (F >= -1022 && F <= 1023) ? rint(c * __longlong_as_double((long long)(F + 1023) << 52))
-                                               : rint(scalbn(c, F));
-    const double hi = floor(v * 0x1p-64);
-    const double lo = v - hi * 0x1p64;
-    return ((__int128)(long long)hi << 64) + (__int128)(unsigned long long)lo;
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(c);
+    const int e = (int)(bits >> 52) & 0x7ff;
+    const unsigned long long m = (bits & 0xfffffffffffffull) | (e ? (1ull << 52) : 0ull);
+    const int sh = (e ? e : 1) - 1075 + F;
+    if (sh >= 0) return (__int128)m << sh;
+    const int k = -sh;
+    if (k >= 64) return 0;
+    const unsigned long long q = m >> k, rem = m & ((1ull << k) - 1ull), half = 1ull << (k - 1);
+    return (__int128)(q + ((rem > half || (rem == half && (q & 1ull))) ? 1ull : 0ull));
 }
 
 }  // namespace irls

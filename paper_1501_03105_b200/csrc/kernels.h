@@ -251,6 +251,10 @@ void bb_extract_stencil(const StencilArgs &s, int64_t N, int32_t F, const double
 void bb_extract_sell(const SellArgs &s, int32_t F, const double *x, const u64_t *spk, const int32_t *spi, void *table,
                      int32_t nb, const int16_t *slot_of, u64_t *cursor, u64_t *ck, int32_t *cid, __int128 *cdel,
                      u64_t *ida, int32_t *posa, u64_t *digit_hist, cudaStream_t st);
+void bb_cdelta_stencil(const StencilArgs &s, int32_t F, const double *x, const int32_t *cid, int64_t C,
+                       __int128 *cdel, cudaStream_t st);
+void bb_cdelta_sell(const SellArgs &s, int32_t F, const double *x, const int32_t *cid, int64_t C, __int128 *cdel,
+                    cudaStream_t st);
 void bb_gather(const u64_t *ck, const int32_t *perm, int64_t C, u64_t *kb, int32_t *jb, u64_t *digit_hist,
                cudaStream_t st);
 void bb_cand_scan(const __int128 *cdel, const int32_t *sorted, const int64_t *cdst, const int64_t *cpos,

@@ -102,41 +102,53 @@ __global__ void k_bb_sample(const double *x, int64_t n, int32_t ns, u64 *skey, i
     sid[j] = (int32_t)v;
 }
 
-// One CTA of 1024 threads: bitonic sort of ns = 2^p (key, id) pairs in
-// shared memory, then splitter j (j = 1 .. nb - 1) = sample j * ns / nb.
-__global__ void __launch_bounds__(1024) k_bb_sort_samples(const u64 *skey, const int32_t *sid, int32_t ns, int32_t nb,
-                                                         u64 *spk, int32_t *spi)
+// Sample sort by rank: sample i goes to position #{j : (key_j, id_j) <
+// (key_i, id_i)} (the ids are distinct, so the ranks are a permutation).
+// ns^2 comparisons: block (bx, by) counts, for its 256 samples, the samples
+// of slice by (1024 of them, staged in shared memory) below each; the
+// scatter adds the slices' counts.
+constexpr int kRankSlice = 1024;
+
+__global__ void __launch_bounds__(256) k_bb_rank_samples(const u64 *skey, const int32_t *sid, int32_t ns,
+                                                         int32_t *prank)
 {
-    extern __shared__ __align__(16) unsigned char bb_dyn[];
-    u64 *k = reinterpret_cast<u64 *>(bb_dyn);
-    int32_t *id = reinterpret_cast<int32_t *>(bb_dyn + sizeof(u64) * ns);
-    for (int i = threadIdx.x; i < ns; i += blockDim.x) {
-        k[i] = skey[i];
-        id[i] = sid[i];
+    __shared__ u64 tk[kRankSlice];
+    __shared__ int32_t ti[kRankSlice];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t0 = blockIdx.y * kRankSlice;
+    for (int j = threadIdx.x; j < kRankSlice; j += blockDim.x) {
+        tk[j] = t0 + j < ns ? skey[t0 + j] : ~0ull;
+        ti[j] = t0 + j < ns ? sid[t0 + j] : 0x7fffffff;
     }
     __syncthreads();
-    for (int size = 2; size <= ns; size <<= 1)
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            for (int t = threadIdx.x; t < ns / 2; t += blockDim.x) {
-                const int lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
-                const bool up = (lo & size) == 0;
-                const bool sw = up ? kless(k[hi], id[hi], k[lo], id[lo]) : kless(k[lo], id[lo], k[hi], id[hi]);
-                if (sw) {
-                    const u64 tk = k[lo];
-                    k[lo] = k[hi];
-                    k[hi] = tk;
-                    const int32_t ti = id[lo];
-                    id[lo] = id[hi];
-                    id[hi] = ti;
-                }
-            }
-            __syncthreads();
-        }
-    for (int j = threadIdx.x; j < nb - 1; j += blockDim.x) {
-        const int s = (int)(((int64_t)(j + 1) * ns) / nb);
-        spk[j] = k[s];
-        spi[j] = id[s];
-    }
+    if (i >= ns) return;
+    const u64 ki = skey[i];
+    const int32_t ii = sid[i];
+    int r = 0;
+#pragma unroll 16
+    for (int j = 0; j < kRankSlice; j++) r += kless(tk[j], ti[j], ki, ii) ? 1 : 0;
+    prank[(int64_t)blockIdx.y * ns + i] = r;
+}
+
+__global__ void k_bb_rank_scatter(const u64 *skey, const int32_t *sid, const int32_t *prank, int32_t ns,
+                                  int32_t nslices, u64 *okey, int32_t *oid)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ns) return;
+    int r = 0;
+    for (int q = 0; q < nslices; q++) r += prank[(int64_t)q * ns + i];
+    okey[r] = skey[i];
+    oid[r] = sid[i];
+}
+
+// splitter j (j = 1 .. nb - 1) = sorted sample j * ns / nb
+__global__ void k_bb_splitters(const u64 *okey, const int32_t *oid, int32_t ns, int32_t nb, u64 *spk, int32_t *spi)
+{
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= nb - 1) return;
+    const int s = (int)(((int64_t)(j + 1) * ns) / nb);
+    spk[j] = okey[s];
+    spi[j] = oid[s];
 }
 
 __device__ __forceinline__ void load_splitters(const u64 *spk, const int32_t *spi, int nb, u64 *sk, int32_t *si)
@@ -232,19 +244,33 @@ __global__ void __launch_bounds__(kBbThreads, 1) k_bb_pass_sell(SellArgs s, int3
             [&](int64_t v, double xv, i128 &d, i128 &qs) { delta_sell(s, F, x, v, xv, d, qs); });
 }
 
-// per bucket: count, exact sum, negative bound; P_0 = Q(c_st) + sum Q(cs)
+// per bucket: count, exact sum, negative bound; P_0 = Q(c_st) + sum Q(cs).
+// A block takes 32 buckets; its 8 warps split the G partials.
 __global__ void __launch_bounds__(256) k_bb_reduce(const u64 *part, const i128 *pqcs, int G, int nb, i128 qcst,
                                                    unsigned *cnt, i128 *bsum, i128 *bneg, i128 *p0)
 {
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b < nb) {
-        u64 c = 0, ng = 0;
-        i128 sum = 0;
-        for (int k = 0; k < G; k++) {
+    __shared__ u64 sc[8][32], sn[8][32];
+    __shared__ i128 ss[8][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int b = blockIdx.x * 32 + lane;
+    u64 c = 0, ng = 0;
+    i128 sum = 0;
+    if (b < nb)
+        for (int k = w; k < G; k += 8) {
             c += part[((int64_t)0 * G + k) * nb + b];
             sum += (i128)part[((int64_t)1 * G + k) * nb + b];
             sum += (i128)(long long)part[((int64_t)2 * G + k) * nb + b] << 64;
             ng += part[((int64_t)3 * G + k) * nb + b];
+        }
+    sc[w][lane] = c;
+    sn[w][lane] = ng;
+    ss[w][lane] = sum;
+    __syncthreads();
+    if (w == 0 && b < nb) {
+        for (int q = 1; q < 8; q++) {
+            c += sc[q][lane];
+            ng += sn[q][lane];
+            sum += ss[q][lane];
         }
         cnt[b] = (unsigned)c;
         bsum[b] = sum;
@@ -268,10 +294,11 @@ __global__ void k_bb_cellflag(const uint32_t *tabp, const int16_t *slot_of, uint
     cflag[c] = f;
 }
 
-// Candidate extraction (second pass; x only, except for candidates): nodes
-// whose bucket has a slot get (key, id, delta) at their slot's cursor, plus
-// stage A of the candidates' sort (by id: key = id, value = compact
-// position) and its digit histograms.
+// Candidate extraction (second pass, over x only): nodes whose bucket has a
+// slot get (key, id) at their slot's cursor, plus stage A of the candidates'
+// sort (by id: key = id, value = compact position) and its digit histograms.
+// Their deltas follow in k_bb_cdelta_* over the packed candidates (here they
+// would run one lane per warp).
 template <class DL>
 __device__ __forceinline__ void bb_extract(int64_t N, const double *x, const u64 *spk, const int32_t *spi,
                                            const uint32_t *tabp_g, const BbMeta *meta, const uint8_t *cflag_g,
@@ -298,36 +325,41 @@ __device__ __forceinline__ void bb_extract(int64_t N, const double *x, const u64
     const int lane = threadIdx.x & 31;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     unsigned nmine = 0;
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < N; base += stride) {
-        const int64_t v = base + threadIdx.x;
-        int slot = -1;
-        double xv = 0.0;
-        u64 key = 0;
-        if (v < N) {
-            xv = canon(x[v]);
-            key = sweep_key(xv);
-            const u64 c = key < kmin ? 0 : (key - kmin) >> sh;
-            if (key < kmin ? sl[0] >= 0 : (c >= (u64)kCells ? sl[nb - 1] >= 0 : cflag[c] != 0))
-                slot = sl[bucket_fast(key, (int32_t)v, sk, si, tabp, kmin, sh, nb)];
-        }
-        if (__any_sync(0xffffffffu, slot >= 0)) {
-            const unsigned peers = __match_any_sync(0xffffffffu, slot);
-            if (slot >= 0) {
-                const int leader = __ffs(peers) - 1;
-                u64 p0 = 0;
-                if (lane == leader) p0 = atomicAdd(&cursor[slot], (u64)__popc(peers));
-                p0 = __shfl_sync(peers, p0, leader);
-                const int64_t p = (int64_t)p0 + __popc(peers & ((1u << lane) - 1u));
-                i128 d, qs;
-                dl(v, xv, d, qs);
-                ck[p] = key;
-                cid[p] = (int32_t)v;
-                cdel[p] = d;
-                ida[p] = (u64)(uint32_t)v;
-                posa[p] = (int32_t)p;
+    constexpr int U = 4;  // nodes per thread per round: their x loads are in flight together
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x * U; base < N; base += stride * U) {
+        double xr[U];
 #pragma unroll
-                for (int q = 0; q < 4; q++) atomicAdd(&h[q * 256 + (((uint32_t)v >> (8 * q)) & 255u)], 1u);
-                nmine++;
+        for (int q = 0; q < U; q++) {
+            const int64_t v = base + (int64_t)q * blockDim.x + threadIdx.x;
+            xr[q] = v < N ? x[v] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            const int64_t v = base + (int64_t)q * blockDim.x + threadIdx.x;
+            int slot = -1;
+            const double xv = canon(xr[q]);
+            const u64 key = sweep_key(xv);
+            if (v < N) {
+                const u64 c = key < kmin ? 0 : (key - kmin) >> sh;
+                if (key < kmin ? sl[0] >= 0 : (c >= (u64)kCells ? sl[nb - 1] >= 0 : cflag[c] != 0))
+                    slot = sl[bucket_fast(key, (int32_t)v, sk, si, tabp, kmin, sh, nb)];
+            }
+            if (__any_sync(0xffffffffu, slot >= 0)) {
+                const unsigned peers = __match_any_sync(0xffffffffu, slot);
+                if (slot >= 0) {
+                    const int leader = __ffs(peers) - 1;
+                    u64 p0 = 0;
+                    if (lane == leader) p0 = atomicAdd(&cursor[slot], (u64)__popc(peers));
+                    p0 = __shfl_sync(peers, p0, leader);
+                    const int64_t p = (int64_t)p0 + __popc(peers & ((1u << lane) - 1u));
+                    ck[p] = key;
+                    cid[p] = (int32_t)v;
+                    ida[p] = (u64)(uint32_t)v;
+                    posa[p] = (int32_t)p;
+#pragma unroll
+                    for (int b = 0; b < 4; b++) atomicAdd(&h[b * 256 + (((uint32_t)v >> (8 * b)) & 255u)], 1u);
+                    nmine++;
+                }
             }
         }
     }
@@ -363,6 +395,29 @@ __global__ void __launch_bounds__(kBbThreads, 1) k_bb_extract_sell(SellArgs s, i
 {
     bb_extract(s.n, x, spk, spi, tabp, meta, cflag, nb, slot_of, cursor, ck, cid, cdel, ida, posa, digit_hist,
                [&](int64_t v, double xv, i128 &d, i128 &qs) { delta_sell(s, F, x, v, xv, d, qs); });
+}
+
+// delta of every candidate (packed: full warps)
+__global__ void __launch_bounds__(256) k_bb_cdelta_stencil(StencilArgs s, int32_t F, const double *x, const int32_t *cid,
+                                                           int64_t C, i128 *cdel)
+{
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= C) return;
+    const int64_t v = cid[p];
+    i128 d, qs;
+    delta_stencil(s, F, x, v, canon(x[v]), d, qs);
+    cdel[p] = d;
+}
+
+__global__ void __launch_bounds__(256) k_bb_cdelta_sell(SellArgs s, int32_t F, const double *x, const int32_t *cid,
+                                                        int64_t C, i128 *cdel)
+{
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= C) return;
+    const int64_t v = cid[p];
+    i128 d, qs;
+    delta_sell(s, F, x, v, canon(x[v]), d, qs);
+    cdel[p] = d;
 }
 
 // Stage B input: the candidates in ascending id order (perm = stage A's
@@ -522,14 +577,14 @@ size_t bb_table_bytes() { return sizeof(uint32_t) * kCells + sizeof(BbMeta) + kC
 void bb_sample_sort(const double *x, int64_t n, int32_t ns, int32_t nb, u64 *skey, int32_t *sid, u64 *spk,
                     int32_t *spi, void *table, cudaStream_t st)
 {
-    const int dyn = (int)((sizeof(u64) + sizeof(int32_t)) * ns);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_bb_sort_samples, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-    }
+    // skey / sid hold 2 ns entries (the samples, then the sorted samples);
+    // sid also ns * (ns / kRankSlice) slice ranks after them
+    const int nsl = (ns + kRankSlice - 1) / kRankSlice;
+    int32_t *prank = sid + 2 * ns;
     k_bb_sample<<<(ns + 255) / 256, 256, 0, st>>>(x, n, ns, skey, sid);
-    k_bb_sort_samples<<<1, 1024, dyn, st>>>(skey, sid, ns, nb, spk, spi);
+    k_bb_rank_samples<<<dim3((ns + 255) / 256, nsl), 256, 0, st>>>(skey, sid, ns, prank);
+    k_bb_rank_scatter<<<(ns + 255) / 256, 256, 0, st>>>(skey, sid, prank, ns, nsl, skey + ns, sid + ns);
+    k_bb_splitters<<<(nb + 255) / 256, 256, 0, st>>>(skey + ns, sid + ns, ns, nb, spk, spi);
     uint32_t *tabp = reinterpret_cast<uint32_t *>(table);
     BbMeta *meta = reinterpret_cast<BbMeta *>(tabp + kCells);
     k_bb_table<<<kCells / 256, 256, 0, st>>>(spk, nb, tabp, meta);
@@ -573,7 +628,7 @@ void bb_pass_sell(const SellArgs &s, int32_t F, const double *x, const u64 *spk,
 void bb_reduce(const u64 *part, const i128 *pqcs, int32_t nb, i128 qcst, unsigned *cnt, i128 *bsum, i128 *bneg,
                i128 *p0, cudaStream_t st)
 {
-    k_bb_reduce<<<(nb + 255) / 256, 256, 0, st>>>(part, pqcs, bb_num_ctas(), nb, qcst, cnt, bsum, bneg, p0);
+    k_bb_reduce<<<(nb + 31) / 32, 256, 0, st>>>(part, pqcs, bb_num_ctas(), nb, qcst, cnt, bsum, bneg, p0);
 }
 
 void bb_extract_stencil(const StencilArgs &s, int64_t N, int32_t F, const double *x, const u64 *spk,
@@ -585,6 +640,18 @@ void bb_extract_stencil(const StencilArgs &s, int64_t N, int32_t F, const double
     k_bb_extract_stencil<<<bb_num_ctas(), kBbThreads, extract_smem(nb), st>>>(
         s, N, F, x, spk, spi, tab_of(table), meta_of(table), cflag_of(table), nb, slot_of, cursor, ck, cid, cdel, ida,
         posa, digit_hist);
+}
+
+void bb_cdelta_stencil(const StencilArgs &s, int32_t F, const double *x, const int32_t *cid, int64_t C, i128 *cdel,
+                       cudaStream_t st)
+{
+    if (C > 0) k_bb_cdelta_stencil<<<(unsigned)((C + 255) / 256), 256, 0, st>>>(s, F, x, cid, C, cdel);
+}
+
+void bb_cdelta_sell(const SellArgs &s, int32_t F, const double *x, const int32_t *cid, int64_t C, i128 *cdel,
+                    cudaStream_t st)
+{
+    if (C > 0) k_bb_cdelta_sell<<<(unsigned)((C + 255) / 256), 256, 0, st>>>(s, F, x, cid, C, cdel);
 }
 
 void bb_extract_sell(const SellArgs &s, int32_t F, const double *x, const u64 *spk, const int32_t *spi, void *table,

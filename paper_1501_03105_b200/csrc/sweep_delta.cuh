@@ -21,7 +21,10 @@ __device__ __forceinline__ bool after(double xu, int64_t u, double xv, int64_t v
 
 __device__ __forceinline__ unsigned long long sweep_key(double xv) { return ~dkey_asc(xv); }
 
-// delta_v of stencil node v (xv = canon(x[v])); qs = Q(cs_v) (for P_0)
+// delta_v of stencil node v (xv = canon(x[v])); qs = Q(cs_v) (for P_0).
+// Every load is issued up front from clamped indices (absent neighbours read
+// the node itself and get capacity 0, contributing +-Q(0) = 0), so the 15
+// loads of a node are in flight together.
 __device__ __forceinline__ void delta_stencil(const StencilArgs &s, int32_t F, const double *x, int64_t v, double xv,
                                               __int128 &d, __int128 &qs)
 {
@@ -30,21 +33,23 @@ __device__ __forceinline__ void delta_stencil(const StencilArgs &s, int32_t F, c
     const int32_t xx = (int32_t)(uv - t1 * (uint32_t)s.nx);
     const uint32_t zz = fdiv(t1, s.fd_ny);
     const int32_t y = (int32_t)(t1 - zz * (uint32_t)s.ny), z = (int32_t)zz;
+    const bool hz0 = z > 0, hy0 = y > 0, hx0 = xx > 0, hx1 = xx < s.nx - 1, hy1 = y < s.ny - 1, hz1 = z < s.nz - 1;
+    const int64_t wz0 = hz0 ? v - s.P : v, wy0 = hy0 ? v - s.nx : v, wx0 = hx0 ? v - 1 : v;
+    const int64_t wx1 = hx1 ? v + 1 : v, wy1 = hy1 ? v + s.nx : v, wz1 = hz1 ? v + s.P : v;
+    const double c0 = s.cz[wz0], c1 = s.cy[wy0], c2 = s.cx[wx0], c3 = s.cx[v], c4 = s.cy[v], c5 = s.cz[v];
+    const double x0 = x[wz0], x1 = x[wy0], x2 = x[wx0], x3 = x[wx1], x4 = x[wy1], x5 = x[wz1];
+    const double cs = s.cs[v], ct = s.ct[v];
     d = 0;
-#define NB(cond, w, cap)                                                           \
-    if (cond) {                                                                    \
-        const __int128 q = qfix(cap, F);                                           \
-        d += after(canon(x[w]), w, xv, v) ? q : -q;                                \
-    }
-    NB(z > 0, v - s.P, s.cz[v - s.P]);
-    NB(y > 0, v - s.nx, s.cy[v - s.nx]);
-    NB(xx > 0, v - 1, s.cx[v - 1]);
-    NB(xx < s.nx - 1, v + 1, s.cx[v]);
-    NB(y < s.ny - 1, v + s.nx, s.cy[v]);
-    NB(z < s.nz - 1, v + s.P, s.cz[v]);
+#define NB(has, w, xw, cap)                                                            {                                                                                      const __int128 q = qfix((has) ? (cap) : 0.0, F);                                   d += after(canon(xw), w, xv, v) ? q : -q;                                      }
+    NB(hz0, wz0, x0, c0);
+    NB(hy0, wy0, x1, c1);
+    NB(hx0, wx0, x2, c2);
+    NB(hx1, wx1, x3, c3);
+    NB(hy1, wy1, x4, c4);
+    NB(hz1, wz1, x5, c5);
 #undef NB
-    qs = qfix(s.cs[v], F);
-    d += qfix(s.ct[v], F);
+    qs = qfix(cs, F);
+    d += qfix(ct, F);
     d -= qs;
 }
 
