@@ -38,7 +38,7 @@ __device__ __forceinline__ double term_g(double cs, double ct, double x, double 
     return gs;
 }
 
-template <int WMAX, int MODE, int MINB = 1>
+template <int WMAX, int MODE, int MINB = 1, int HALF = WMAX>
 __global__ void __launch_bounds__(kThreads, MINB) k_sellp_assemble(SellArgs s, VecArgs v, RedArgs ra, CondArgs cd,
                                                              double eps2, double *gs_out, double *gt_out)
 {
@@ -59,41 +59,44 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sellp_assemble(SellArgs s, V
         // ---- loads: own, slots, then gathers
         const double2 x2 = HASX ? ldp2(v.x, u0) : make_double2(0.0, 0.0);
         const double2 cs2 = ldp2(s.cs, u0), ct2 = ldp2(s.ct, u0);
-        int2 cl[WMAX];
-        double2 cc[WMAX];
-#pragma unroll
-        for (int k = 0; k < WMAX; k++) {
-            if (k < W) {
-                cl[k] = ldi2(s.col, e0 + (int64_t)kSell * k);
-                cc[k] = ldp2(s.c, e0 + (int64_t)kSell * k);
-            } else {
-                cl[k] = make_int2(-1, -1);
-                cc[k] = make_double2(0.0, 0.0);
-            }
-        }
-        double xa[WMAX], xb[WMAX];
-#pragma unroll
-        for (int k = 0; k < WMAX; k++) {
-            xa[k] = (HASX && cl[k].x >= 0) ? __ldg(v.x + cl[k].x) : 0.0;
-            xb[k] = (HASX && cl[k].y >= 0) ? __ldg(v.x + cl[k].y) : 0.0;
-        }
-        // ---- conductances in slot order
+        // ---- conductances in slot order, HALF slots' loads at a time
         double a0 = 0.0, b0 = 0.0, a1 = 0.0, b1 = 0.0;
 #pragma unroll
-        for (int k = 0; k < WMAX; k++) {
-            if (k < W) {
-                double g0 = 0.0, g1 = 0.0;
-                if (cl[k].x >= 0) {
-                    g0 = INITG ? cc[k].x : rw_g(cc[k].x, x2.x - xa[k], eps2);
-                    a0 = a0 + g0;
-                    if (WARM) b0 = b0 + g0 * xa[k];
+        for (int k0 = 0; k0 < WMAX; k0 += HALF) {
+            int2 cl[HALF];
+            double2 cc[HALF];
+#pragma unroll
+            for (int k = 0; k < HALF; k++) {
+                if (k0 + k < W) {
+                    cl[k] = ldi2(s.col, e0 + (int64_t)kSell * (k0 + k));
+                    cc[k] = ldp2(s.c, e0 + (int64_t)kSell * (k0 + k));
+                } else {
+                    cl[k] = make_int2(-1, -1);
+                    cc[k] = make_double2(0.0, 0.0);
                 }
-                if (cl[k].y >= 0) {
-                    g1 = INITG ? cc[k].y : rw_g(cc[k].y, x2.y - xb[k], eps2);
-                    a1 = a1 + g1;
-                    if (WARM) b1 = b1 + g1 * xb[k];
+            }
+            double xa[HALF], xb[HALF];
+#pragma unroll
+            for (int k = 0; k < HALF; k++) {
+                xa[k] = (HASX && cl[k].x >= 0) ? __ldg(v.x + cl[k].x) : 0.0;
+                xb[k] = (HASX && cl[k].y >= 0) ? __ldg(v.x + cl[k].y) : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < HALF; k++) {
+                if (k0 + k < W) {
+                    double g0 = 0.0, g1 = 0.0;
+                    if (cl[k].x >= 0) {
+                        g0 = INITG ? cc[k].x : rw_g(cc[k].x, x2.x - xa[k], eps2);
+                        a0 = a0 + g0;
+                        if (WARM) b0 = b0 + g0 * xa[k];
+                    }
+                    if (cl[k].y >= 0) {
+                        g1 = INITG ? cc[k].y : rw_g(cc[k].y, x2.y - xb[k], eps2);
+                        a1 = a1 + g1;
+                        if (WARM) b1 = b1 + g1 * xb[k];
+                    }
+                    stp2(s.g, e0 + (int64_t)kSell * (k0 + k), make_double2(g0, g1));
                 }
-                stp2(s.g, e0 + (int64_t)kSell * k, make_double2(g0, g1));
             }
         }
         double2 gs2, gt2;
@@ -140,7 +143,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sellp_assemble(SellArgs s, V
     }
 }
 
-template <int WMAX, int MINB, bool W0>
+template <int WMAX, int MINB, bool W0, int HALF = WMAX>
 __global__ void __launch_bounds__(kThreads, MINB) k_sellp_pspmv(SellArgs s, VecArgs v, RedArgs ra, CondArgs cd)
 {
     const DevCtrl *ctrl = ra.ctrl;
@@ -166,28 +169,35 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sellp_pspmv(SellArgs s, VecA
         const double2 D2 = ldp2(v.D, u0);
         double2 x2 = make_double2(0.0, 0.0);
         if (!first) x2 = *reinterpret_cast<const double2 *>(v.x + u0);
-        int2 cl[WMAX];
-        double2 gg[WMAX];
-#pragma unroll
-        for (int k = 0; k < WMAX; k++) cl[k] = k < W ? ldi2(s.col, e0 + (int64_t)kSell * k) : make_int2(-1, -1);
-#pragma unroll
-        for (int k = 0; k < WMAX; k++)  // padding slots of both rows: no conductance load
-            gg[k] = (cl[k].x >= 0 || cl[k].y >= 0) ? ldp2(s.g, e0 + (int64_t)kSell * k) : make_double2(0.0, 0.0);
-        double za[WMAX], zb[WMAX], pa[WMAX], pb[WMAX];
-#pragma unroll
-        for (int k = 0; k < WMAX; k++) {
-            za[k] = cl[k].x >= 0 ? __ldg(zv + cl[k].x) : 0.0;
-            zb[k] = cl[k].y >= 0 ? __ldg(zv + cl[k].y) : 0.0;
-            pa[k] = (!first && cl[k].x >= 0) ? __ldg(pold + cl[k].x) : 0.0;
-            pb[k] = (!first && cl[k].y >= 0) ? __ldg(pold + cl[k].y) : 0.0;
-        }
         const double p0 = first ? z2.x : z2.x + beta * po.x;
         const double p1 = first ? z2.y : z2.y + beta * po.y;
         double a = 0.0, b = 0.0;
+        // slots in groups of HALF (loads of a group in flight together; fewer
+        // live registers than all WMAX at once)
 #pragma unroll
-        for (int k = 0; k < WMAX; k++) {
-            if (cl[k].x >= 0) a = a + gg[k].x * (first ? za[k] : za[k] + beta * pa[k]);
-            if (cl[k].y >= 0) b = b + gg[k].y * (first ? zb[k] : zb[k] + beta * pb[k]);
+        for (int k0 = 0; k0 < WMAX; k0 += HALF) {
+            int2 cl[HALF];
+            double2 gg[HALF];
+#pragma unroll
+            for (int k = 0; k < HALF; k++)
+                cl[k] = k0 + k < W ? ldi2(s.col, e0 + (int64_t)kSell * (k0 + k)) : make_int2(-1, -1);
+#pragma unroll
+            for (int k = 0; k < HALF; k++)  // padding slots of both rows: no conductance load
+                gg[k] = (cl[k].x >= 0 || cl[k].y >= 0) ? ldp2(s.g, e0 + (int64_t)kSell * (k0 + k))
+                                                        : make_double2(0.0, 0.0);
+            double za[HALF], zb[HALF], pa[HALF], pb[HALF];
+#pragma unroll
+            for (int k = 0; k < HALF; k++) {
+                za[k] = cl[k].x >= 0 ? __ldg(zv + cl[k].x) : 0.0;
+                zb[k] = cl[k].y >= 0 ? __ldg(zv + cl[k].y) : 0.0;
+                pa[k] = (!first && cl[k].x >= 0) ? __ldg(pold + cl[k].x) : 0.0;
+                pb[k] = (!first && cl[k].y >= 0) ? __ldg(pold + cl[k].y) : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < HALF; k++) {
+                if (cl[k].x >= 0) a = a + gg[k].x * (first ? za[k] : za[k] + beta * pa[k]);
+                if (cl[k].y >= 0) b = b + gg[k].y * (first ? zb[k] : zb[k] + beta * pb[k]);
+            }
         }
         const double q0 = D2.x * p0 - a, q1 = v1 ? D2.y * p1 - b : 0.0;
         stp2(pnew, u0, make_double2(p0, v1 ? p1 : 0.0));
@@ -210,6 +220,8 @@ static void asm_w(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const 
 {
     const unsigned nb = nblk3(v.n_own);
     // reweight steps at 3 CTAs/SM: config 3 0.62 ms vs 0.72 ms at 1, 2 or 4
+    // (per-slot loads at 4 CTAs/SM measured 0.676 ms and two slots at a time
+    // 0.682 ms against 0.622 ms for all slots' loads first at 3 CTAs/SM)
     if (WMAX == 4 && mode == ASM_REWEIGHT_WARM) {
         k_sellp_assemble<WMAX, ASM_REWEIGHT_WARM, 3><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
         return;
@@ -239,10 +251,12 @@ bool launch_sellp_assemble(const SellArgs &s, const VecArgs &v, const RedArgs &r
 bool launch_sellp_pspmv(const SellArgs &s, const VecArgs &v, const RedArgs &ra, const CondArgs &cd, cudaStream_t st,
                         bool w0)
 {
-    // 3 CTAs/SM (80 registers, 48 B spilled): config 3 0.47 ms vs 0.52 ms at
-    // 2 CTAs/SM (105 registers) and 0.49 ms at 4 (64 registers)
-    if (s.wmax <= 4 && w0) k_sellp_pspmv<4, 3, true><<<nblk3(v.n_own), kThreads, 0, st>>>(s, v, ra, cd);
-    else if (s.wmax <= 4) k_sellp_pspmv<4, 3, false><<<nblk3(v.n_own), kThreads, 0, st>>>(s, v, ra, cd);
+    // WMAX 4: one slot at a time (HALF = 1: 64 registers, no spill, 4 CTAs/SM;
+    // the unrolled slot loop still keeps the loads in flight): config 3
+    // 0.431 ms against 0.517 ms for all four slots' loads first at 3 CTAs/SM
+    // (80 registers, 48 B spilled) and 0.450 ms for two at a time (same box)
+    if (s.wmax <= 4 && w0) k_sellp_pspmv<4, 4, true, 1><<<nblk3(v.n_own), kThreads, 0, st>>>(s, v, ra, cd);
+    else if (s.wmax <= 4) k_sellp_pspmv<4, 4, false, 1><<<nblk3(v.n_own), kThreads, 0, st>>>(s, v, ra, cd);
     else if (s.wmax <= 8 && w0) k_sellp_pspmv<8, 1, true><<<nblk3(v.n_own), kThreads, 0, st>>>(s, v, ra, cd);
     else if (s.wmax <= 8) k_sellp_pspmv<8, 1, false><<<nblk3(v.n_own), kThreads, 0, st>>>(s, v, ra, cd);
     else return false;
