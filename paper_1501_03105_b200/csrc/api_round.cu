@@ -115,17 +115,18 @@ static irls_status sweep_bb(irls_ctx *c, const double *xfull, int *launches, boo
     int32_t *sid = (int32_t *)talloc(4 * (2 * ns + (size_t)ns * (ns / 1024))), *spi = (int32_t *)talloc(4 * nb);
     u64 *part = (u64 *)talloc(8 * 4 * (size_t)G * nb);
     void *table = talloc(bb_table_bytes());
+    uint16_t *bkt = (uint16_t *)talloc(2 * (size_t)n + 16);
     i128 *pqcs = (i128 *)talloc(16 * (size_t)G);
     unsigned *cnt = (unsigned *)talloc(4 * nb);
     i128 *bsum = (i128 *)talloc(16 * nb), *bneg = (i128 *)talloc(16 * nb), *p0 = (i128 *)talloc(16);
     int16_t *slot_of = (int16_t *)talloc(2 * nb);
-    if (!skey || !spk || !sid || !spi || !part || !table || !pqcs || !cnt || !bsum || !bneg || !p0 || !slot_of)
+    if (!skey || !spk || !sid || !spi || !part || !table || !bkt || !pqcs || !cnt || !bsum || !bneg || !p0 || !slot_of)
         return IRLS_OK;
     // buckets, then one pass: counts, exact sums, negative bounds, P_0, NaN flag
     bb_sample_sort(xfull, n, ns, nb, skey, sid, spk, spi, table, st);
     if (c->kind == 0)
-        bb_pass_stencil(stencil_args(c, true), n, c->F, xfull, spk, spi, table, nb, part, pqcs, b.flags, st);
-    else bb_pass_sell(sell_args_full(c), c->F, xfull, spk, spi, table, nb, part, pqcs, b.flags, st);
+        bb_pass_stencil(stencil_args(c, true), n, c->F, xfull, spk, spi, table, nb, part, pqcs, b.flags, bkt, st);
+    else bb_pass_sell(sell_args_full(c), c->F, xfull, spk, spi, table, nb, part, pqcs, b.flags, bkt, st);
     bb_reduce(part, pqcs, nb, qfix_host(c->c_st, c->F), cnt, bsum, bneg, p0, st);
     *launches += 7;  // sample, rank, rank scatter, splitters, table, pass, reduce
     std::vector<unsigned> hc(nb);
@@ -201,14 +202,7 @@ static irls_status sweep_bb(irls_ctx *c, const double *xfull, int *launches, boo
     CK(cudaMemsetAsync(b.flags + 2, 0, sizeof(int32_t), st));
     int32_t *sorted = v1;
     if (nc > 0) {
-        if (c->kind == 0)
-            bb_extract_stencil(stencil_args(c, true), n, c->F, xfull, spk, spi, table, nb, slot_of, cursor, ck, cid,
-                               cdel, k1, v1, dh, st);
-        else
-            bb_extract_sell(sell_args_full(c), c->F, xfull, spk, spi, table, nb, slot_of, cursor, ck, cid, cdel, k1,
-                            v1, dh, st);
-        if (c->kind == 0) bb_cdelta_stencil(stencil_args(c, true), c->F, xfull, cid, C, cdel, st);
-        else bb_cdelta_sell(sell_args_full(c), c->F, xfull, cid, C, cdel, st);
+        bb_extract(n, xfull, bkt, nb, slot_of, cursor, ck, cid, k1, v1, dh, st);
         // the radix sort of sweep.cu is stable on the key alone; ties must
         // leave in ascending id, so: (A) sort positions by id, (B) gather
         // the keys in that order and sort them (values: compact positions)
@@ -221,6 +215,8 @@ static irls_status sweep_bb(irls_ctx *c, const double *xfull, int *launches, boo
         tb.digit_hist = dh;
         bool nan = false;
         const int32_t *perm = sweep_sort(tb, st, launches, &nan);
+        if (c->kind == 0) bb_cdelta_stencil(stencil_args(c, true), c->F, xfull, cid, perm, C, cdel, st);
+        else bb_cdelta_sell(sell_args_full(c), c->F, xfull, cid, perm, C, cdel, st);
         int32_t *pin = perm == v1 ? v2 : v1;  // the other value buffer; k1, k2 are free
         int32_t *spare = perm == v1 ? v1 : v2;
         bb_gather(ck, perm, C, k1, pin, dh + 8 * 256, st);
@@ -231,7 +227,7 @@ static irls_status sweep_bb(irls_ctx *c, const double *xfull, int *launches, boo
         tb.digit_hist = dh + 8 * 256;
         sorted = sweep_sort(tb, st, launches, &nan);
         bb_cand_scan(cdel, sorted, ddst, dpos, dP, nc, cmin, carg, st);
-        *launches += 5;  // cell flags, extract, deltas, gather, candidate scan
+        *launches += 4;  // extract, deltas, gather, candidate scan
     }
     bb_finish(cmin, carg, nc, best, barg, ddst, dpos, sorted, cid, b.k_out, b.lastv, b.flags, st);
     *launches += 1;

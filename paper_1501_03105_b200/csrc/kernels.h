@@ -235,26 +235,23 @@ void sweep_scan_argmin(SweepBuffers &b, const int32_t *ord, __int128 P0, cudaStr
 // scanned.  Partials: [4][bb_num_ctas()][nb] u64, [bb_num_ctas()] i128.
 typedef unsigned long long u64_t;
 int bb_num_ctas();
-size_t bb_table_bytes();  // splitter cell table + meta + cell flags (one buffer)
+size_t bb_table_bytes();  // splitter cell table + meta (one buffer)
 void bb_sample_sort(const double *x, int64_t n, int32_t ns, int32_t nb, u64_t *skey, int32_t *sid, u64_t *spk,
                     int32_t *spi, void *table, cudaStream_t st);
 void bb_pass_stencil(const StencilArgs &s, int64_t N, int32_t F, const double *x, const u64_t *spk,
                      const int32_t *spi, const void *table, int32_t nb, u64_t *part, __int128 *pqcs, int32_t *flags,
-                     cudaStream_t st);
+                     uint16_t *bkt, cudaStream_t st);
 void bb_pass_sell(const SellArgs &s, int32_t F, const double *x, const u64_t *spk, const int32_t *spi,
-                  const void *table, int32_t nb, u64_t *part, __int128 *pqcs, int32_t *flags, cudaStream_t st);
+                  const void *table, int32_t nb, u64_t *part, __int128 *pqcs, int32_t *flags, uint16_t *bkt,
+                  cudaStream_t st);
 void bb_reduce(const u64_t *part, const __int128 *pqcs, int32_t nb, __int128 qcst, unsigned *cnt, __int128 *bsum,
                __int128 *bneg, __int128 *p0, cudaStream_t st);
-void bb_extract_stencil(const StencilArgs &s, int64_t N, int32_t F, const double *x, const u64_t *spk,
-                        const int32_t *spi, void *table, int32_t nb, const int16_t *slot_of, u64_t *cursor, u64_t *ck,
-                        int32_t *cid, __int128 *cdel, u64_t *ida, int32_t *posa, u64_t *digit_hist, cudaStream_t st);
-void bb_extract_sell(const SellArgs &s, int32_t F, const double *x, const u64_t *spk, const int32_t *spi, void *table,
-                     int32_t nb, const int16_t *slot_of, u64_t *cursor, u64_t *ck, int32_t *cid, __int128 *cdel,
-                     u64_t *ida, int32_t *posa, u64_t *digit_hist, cudaStream_t st);
-void bb_cdelta_stencil(const StencilArgs &s, int32_t F, const double *x, const int32_t *cid, int64_t C,
-                       __int128 *cdel, cudaStream_t st);
-void bb_cdelta_sell(const SellArgs &s, int32_t F, const double *x, const int32_t *cid, int64_t C, __int128 *cdel,
-                    cudaStream_t st);
+void bb_extract(int64_t N, const double *x, const uint16_t *bkt, int32_t nb, const int16_t *slot_of, u64_t *cursor,
+                u64_t *ck, int32_t *cid, u64_t *ida, int32_t *posa, u64_t *digit_hist, cudaStream_t st);
+void bb_cdelta_stencil(const StencilArgs &s, int32_t F, const double *x, const int32_t *cid, const int32_t *perm,
+                       int64_t C, __int128 *cdel, cudaStream_t st);
+void bb_cdelta_sell(const SellArgs &s, int32_t F, const double *x, const int32_t *cid, const int32_t *perm, int64_t C,
+                    __int128 *cdel, cudaStream_t st);
 void bb_gather(const u64_t *ck, const int32_t *perm, int64_t C, u64_t *kb, int32_t *jb, u64_t *digit_hist,
                cudaStream_t st);
 void bb_cand_scan(const __int128 *cdel, const int32_t *sorted, const int64_t *cdst, const int64_t *cpos,

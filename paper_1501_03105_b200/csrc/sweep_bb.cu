@@ -161,11 +161,12 @@ __device__ __forceinline__ void load_splitters(const u64 *spk, const int32_t *sp
 
 // The bucket pass (persistent: one CTA of 1024 threads per SM).  Partials
 // per CTA g: part[(f * G + g) * nb + b] for the fields f = count, low word,
-// high word, negative bound; pqcs[g] = the CTA's sum of Q(cs_v).
+// high word, negative bound; pqcs[g] = the CTA's sum of Q(cs_v); bkt[v] = the
+// bucket of v (2 bytes per node, read back by the extraction).
 template <class DL>
 __device__ __forceinline__ void bb_pass(int64_t N, const double *x, const u64 *spk, const int32_t *spi,
                                         const uint32_t *tabp_g, const BbMeta *meta, int nb, u64 *part, i128 *pqcs,
-                                        int32_t *flags, DL dl)
+                                        int32_t *flags, uint16_t *bkt, DL dl)
 {
     extern __shared__ __align__(16) unsigned char bb_dyn[];
     u64 *alo = reinterpret_cast<u64 *>(bb_dyn);              // [nb]
@@ -196,6 +197,7 @@ __device__ __forceinline__ void bb_pass(int64_t N, const double *x, const u64 *s
         dl(v, xv, d, qs);
         qcs += qs;
         const int b = bucket_fast(sweep_key(xv), (int32_t)v, sk, si, tabp, kmin, sh, nb);
+        bkt[v] = (uint16_t)b;
         const u64 lo = (u64)d;
         atomicAdd(&acnt[b], 1u);
         const u64 old = atomicAdd(&alo[b], lo);
@@ -229,18 +231,18 @@ __global__ void __launch_bounds__(kBbThreads, 1) k_bb_pass_stencil(StencilArgs s
                                                                    const double *x, const u64 *spk,
                                                                    const int32_t *spi, const uint32_t *tabp,
                                                                    const BbMeta *meta, int nb, u64 *part, i128 *pqcs,
-                                                                   int32_t *flags)
+                                                                   int32_t *flags, uint16_t *bkt)
 {
-    bb_pass(N, x, spk, spi, tabp, meta, nb, part, pqcs, flags,
+    bb_pass(N, x, spk, spi, tabp, meta, nb, part, pqcs, flags, bkt,
             [&](int64_t v, double xv, i128 &d, i128 &qs) { delta_stencil(s, F, x, v, xv, d, qs); });
 }
 
 __global__ void __launch_bounds__(kBbThreads, 1) k_bb_pass_sell(SellArgs s, int32_t F, const double *x,
                                                                 const u64 *spk, const int32_t *spi,
                                                                 const uint32_t *tabp, const BbMeta *meta, int nb,
-                                                                u64 *part, i128 *pqcs, int32_t *flags)
+                                                                u64 *part, i128 *pqcs, int32_t *flags, uint16_t *bkt)
 {
-    bb_pass(s.n, x, spk, spi, tabp, meta, nb, part, pqcs, flags,
+    bb_pass(s.n, x, spk, spi, tabp, meta, nb, part, pqcs, flags, bkt,
             [&](int64_t v, double xv, i128 &d, i128 &qs) { delta_sell(s, F, x, v, xv, d, qs); });
 }
 
@@ -283,67 +285,44 @@ __global__ void __launch_bounds__(256) k_bb_reduce(const u64 *part, const i128 *
     }
 }
 
-// cflag[c] = 1 when a bucket that cell c can map to has a slot
-__global__ void k_bb_cellflag(const uint32_t *tabp, const int16_t *slot_of, uint8_t *cflag)
-{
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= kCells) return;
-    const uint32_t p = tabp[c];
-    uint8_t f = 0;
-    for (int b = (int)(p & 0xffffu); b <= (int)(p >> 16); b++) f |= slot_of[b] >= 0;
-    cflag[c] = f;
-}
-
-// Candidate extraction (second pass, over x only): nodes whose bucket has a
-// slot get (key, id) at their slot's cursor, plus stage A of the candidates'
-// sort (by id: key = id, value = compact position) and its digit histograms.
-// Their deltas follow in k_bb_cdelta_* over the packed candidates (here they
-// would run one lane per warp).
-template <class DL>
-__device__ __forceinline__ void bb_extract(int64_t N, const double *x, const u64 *spk, const int32_t *spi,
-                                           const uint32_t *tabp_g, const BbMeta *meta, const uint8_t *cflag_g,
-                                           int nb, const int16_t *slot_of, u64 *cursor, u64 *ck, int32_t *cid,
-                                           i128 *cdel, u64 *ida, int32_t *posa, u64 *digit_hist, DL dl)
+// Candidate extraction (second pass, over the bucket ids: 2 bytes per node,
+// eight per thread and load): nodes whose bucket has a slot get (key, id) at
+// their slot's cursor, plus stage A of the candidates' sort (by id: key = id,
+// value = compact position) and its digit histograms.  Their deltas follow
+// in k_bb_cdelta_* over the candidates in id order (after stage A).
+__global__ void __launch_bounds__(kBbThreads, 1) k_bb_extract(int64_t N, const double *x, const uint16_t *bkt, int nb,
+                                                              const int16_t *slot_of, u64 *cursor, u64 *ck,
+                                                              int32_t *cid, u64 *ida, int32_t *posa, u64 *digit_hist)
 {
     extern __shared__ __align__(16) unsigned char bb_dyn[];
-    u64 *sk = reinterpret_cast<u64 *>(bb_dyn);               // [nb - 1]
-    int32_t *si = reinterpret_cast<int32_t *>(sk + nb);      // [nb - 1]
-    uint32_t *tabp = reinterpret_cast<uint32_t *>(si + nb);  // [kCells]
-    int16_t *sl = reinterpret_cast<int16_t *>(tabp + kCells);  // [nb]
-    uint8_t *cflag = reinterpret_cast<uint8_t *>(sl + nb);    // [kCells]
+    int16_t *sl = reinterpret_cast<int16_t *>(bb_dyn);  // [nb]
     __shared__ unsigned h[4 * 256];
     for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) h[i] = 0u;
     for (int i = threadIdx.x; i < nb; i += blockDim.x) sl[i] = slot_of[i];
-    for (int i = threadIdx.x; i < kCells; i += blockDim.x) {
-        tabp[i] = tabp_g[i];
-        cflag[i] = cflag_g[i];
-    }
-    load_splitters(spk, spi, nb, sk, si);
-    const u64 kmin = meta->kmin;
-    const int sh = (int)meta->shift;
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     unsigned nmine = 0;
-    constexpr int U = 4;  // nodes per thread per round: their x loads are in flight together
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x * U; base < N; base += stride * U) {
-        double xr[U];
+    const int64_t ng = (N + 7) / 8;  // groups of 8 nodes
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t g0 = (int64_t)blockIdx.x * blockDim.x; g0 < ng; g0 += stride) {
+        const int64_t g = g0 + threadIdx.x;
+        uint16_t bb[8];
+        if (g < ng && 8 * g + 8 <= N) {
+            const uint4 w = __ldcs(reinterpret_cast<const uint4 *>(bkt) + g);
+            const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-        for (int q = 0; q < U; q++) {
-            const int64_t v = base + (int64_t)q * blockDim.x + threadIdx.x;
-            xr[q] = v < N ? x[v] : 0.0;
+            for (int q = 0; q < 4; q++) {
+                bb[2 * q] = (uint16_t)(ww[q] & 0xffffu);
+                bb[2 * q + 1] = (uint16_t)(ww[q] >> 16);
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 8; q++) bb[q] = (g < ng && 8 * g + q < N) ? bkt[8 * g + q] : (uint16_t)0xffffu;
         }
 #pragma unroll
-        for (int q = 0; q < U; q++) {
-            const int64_t v = base + (int64_t)q * blockDim.x + threadIdx.x;
-            int slot = -1;
-            const double xv = canon(xr[q]);
-            const u64 key = sweep_key(xv);
-            if (v < N) {
-                const u64 c = key < kmin ? 0 : (key - kmin) >> sh;
-                if (key < kmin ? sl[0] >= 0 : (c >= (u64)kCells ? sl[nb - 1] >= 0 : cflag[c] != 0))
-                    slot = sl[bucket_fast(key, (int32_t)v, sk, si, tabp, kmin, sh, nb)];
-            }
+        for (int q = 0; q < 8; q++) {
+            const int64_t v = 8 * g + q;
+            const int slot = bb[q] != 0xffffu ? (int)sl[bb[q]] : -1;
             if (__any_sync(0xffffffffu, slot >= 0)) {
                 const unsigned peers = __match_any_sync(0xffffffffu, slot);
                 if (slot >= 0) {
@@ -352,7 +331,7 @@ __device__ __forceinline__ void bb_extract(int64_t N, const double *x, const u64
                     if (lane == leader) p0 = atomicAdd(&cursor[slot], (u64)__popc(peers));
                     p0 = __shfl_sync(peers, p0, leader);
                     const int64_t p = (int64_t)p0 + __popc(peers & ((1u << lane) - 1u));
-                    ck[p] = key;
+                    ck[p] = sweep_key(canon(x[v]));
                     cid[p] = (int32_t)v;
                     ida[p] = (u64)(uint32_t)v;
                     posa[p] = (int32_t)p;
@@ -373,36 +352,15 @@ __device__ __forceinline__ void bb_extract(int64_t N, const double *x, const u64
         if (h[i]) atomicAdd(&digit_hist[i], (u64)h[i]);
 }
 
-__global__ void __launch_bounds__(kBbThreads, 1) k_bb_extract_stencil(StencilArgs s, int64_t N, int32_t F,
-                                                                      const double *x, const u64 *spk,
-                                                                      const int32_t *spi, const uint32_t *tabp,
-                                                                      const BbMeta *meta, const uint8_t *cflag, int nb,
-                                                                      const int16_t *slot_of, u64 *cursor, u64 *ck,
-                                                                      int32_t *cid, i128 *cdel, u64 *ida,
-                                                                      int32_t *posa, u64 *digit_hist)
-{
-    bb_extract(N, x, spk, spi, tabp, meta, cflag, nb, slot_of, cursor, ck, cid, cdel, ida, posa, digit_hist,
-               [&](int64_t v, double xv, i128 &d, i128 &qs) { delta_stencil(s, F, x, v, xv, d, qs); });
-}
-
-__global__ void __launch_bounds__(kBbThreads, 1) k_bb_extract_sell(SellArgs s, int32_t F, const double *x,
-                                                                   const u64 *spk, const int32_t *spi,
-                                                                   const uint32_t *tabp, const BbMeta *meta,
-                                                                   const uint8_t *cflag, int nb,
-                                                                   const int16_t *slot_of, u64 *cursor, u64 *ck,
-                                                                   int32_t *cid, i128 *cdel, u64 *ida, int32_t *posa,
-                                                                   u64 *digit_hist)
-{
-    bb_extract(s.n, x, spk, spi, tabp, meta, cflag, nb, slot_of, cursor, ck, cid, cdel, ida, posa, digit_hist,
-               [&](int64_t v, double xv, i128 &d, i128 &qs) { delta_sell(s, F, x, v, xv, d, qs); });
-}
-
-// delta of every candidate (packed: full warps)
+// delta of every candidate (packed: full warps), in ascending id order
+// (perm = stage A's sorted compact positions: neighbouring threads read
+// neighbouring graph data)
 __global__ void __launch_bounds__(256) k_bb_cdelta_stencil(StencilArgs s, int32_t F, const double *x, const int32_t *cid,
-                                                           int64_t C, i128 *cdel)
+                                                           const int32_t *perm, int64_t C, i128 *cdel)
 {
-    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= C) return;
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= C) return;
+    const int64_t p = perm[r];
     const int64_t v = cid[p];
     i128 d, qs;
     delta_stencil(s, F, x, v, canon(x[v]), d, qs);
@@ -410,10 +368,11 @@ __global__ void __launch_bounds__(256) k_bb_cdelta_stencil(StencilArgs s, int32_
 }
 
 __global__ void __launch_bounds__(256) k_bb_cdelta_sell(SellArgs s, int32_t F, const double *x, const int32_t *cid,
-                                                        int64_t C, i128 *cdel)
+                                                        const int32_t *perm, int64_t C, i128 *cdel)
 {
-    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= C) return;
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= C) return;
+    const int64_t p = perm[r];
     const int64_t v = cid[p];
     i128 d, qs;
     delta_sell(s, F, x, v, canon(x[v]), d, qs);
@@ -572,7 +531,7 @@ int bb_num_ctas()
 }
 
 // scratch of the bucket stage: splitters, cell table, meta
-size_t bb_table_bytes() { return sizeof(uint32_t) * kCells + sizeof(BbMeta) + kCells; }
+size_t bb_table_bytes() { return sizeof(uint32_t) * kCells + sizeof(BbMeta); }
 
 void bb_sample_sort(const double *x, int64_t n, int32_t ns, int32_t nb, u64 *skey, int32_t *sid, u64 *spk,
                     int32_t *spi, void *table, cudaStream_t st)
@@ -591,7 +550,6 @@ void bb_sample_sort(const double *x, int64_t n, int32_t ns, int32_t nb, u64 *ske
 }
 
 static size_t pass_smem(int nb) { return (size_t)nb * (3 * 8 + 8 + 4 + 4) + sizeof(uint32_t) * kCells; }
-static size_t extract_smem(int nb) { return (size_t)nb * (8 + 4 + 2) + (sizeof(uint32_t) + 1) * kCells; }
 
 template <class K>
 static void set_smem(K kern, size_t bytes)
@@ -604,25 +562,23 @@ static inline const BbMeta *meta_of(const void *t)
 {
     return reinterpret_cast<const BbMeta *>(reinterpret_cast<const uint32_t *>(t) + kCells);
 }
-static inline uint8_t *cflag_of(void *t)
-{
-    return reinterpret_cast<uint8_t *>(reinterpret_cast<BbMeta *>(reinterpret_cast<uint32_t *>(t) + kCells) + 1);
-}
 
 void bb_pass_stencil(const StencilArgs &s, int64_t N, int32_t F, const double *x, const u64 *spk, const int32_t *spi,
-                     const void *table, int32_t nb, u64 *part, i128 *pqcs, int32_t *flags, cudaStream_t st)
+                     const void *table, int32_t nb, u64 *part, i128 *pqcs, int32_t *flags, uint16_t *bkt,
+                     cudaStream_t st)
 {
     set_smem(k_bb_pass_stencil, pass_smem(nb));
     k_bb_pass_stencil<<<bb_num_ctas(), kBbThreads, pass_smem(nb), st>>>(s, N, F, x, spk, spi, tab_of(table),
-                                                                        meta_of(table), nb, part, pqcs, flags);
+                                                                        meta_of(table), nb, part, pqcs, flags, bkt);
 }
 
 void bb_pass_sell(const SellArgs &s, int32_t F, const double *x, const u64 *spk, const int32_t *spi,
-                  const void *table, int32_t nb, u64 *part, i128 *pqcs, int32_t *flags, cudaStream_t st)
+                  const void *table, int32_t nb, u64 *part, i128 *pqcs, int32_t *flags, uint16_t *bkt,
+                  cudaStream_t st)
 {
     set_smem(k_bb_pass_sell, pass_smem(nb));
     k_bb_pass_sell<<<bb_num_ctas(), kBbThreads, pass_smem(nb), st>>>(s, F, x, spk, spi, tab_of(table),
-                                                                     meta_of(table), nb, part, pqcs, flags);
+                                                                     meta_of(table), nb, part, pqcs, flags, bkt);
 }
 
 void bb_reduce(const u64 *part, const i128 *pqcs, int32_t nb, i128 qcst, unsigned *cnt, i128 *bsum, i128 *bneg,
@@ -631,38 +587,23 @@ void bb_reduce(const u64 *part, const i128 *pqcs, int32_t nb, i128 qcst, unsigne
     k_bb_reduce<<<(nb + 31) / 32, 256, 0, st>>>(part, pqcs, bb_num_ctas(), nb, qcst, cnt, bsum, bneg, p0);
 }
 
-void bb_extract_stencil(const StencilArgs &s, int64_t N, int32_t F, const double *x, const u64 *spk,
-                        const int32_t *spi, void *table, int32_t nb, const int16_t *slot_of, u64 *cursor, u64 *ck,
-                        int32_t *cid, i128 *cdel, u64 *ida, int32_t *posa, u64 *digit_hist, cudaStream_t st)
+void bb_extract(int64_t N, const double *x, const uint16_t *bkt, int32_t nb, const int16_t *slot_of, u64 *cursor,
+                u64 *ck, int32_t *cid, u64 *ida, int32_t *posa, u64 *digit_hist, cudaStream_t st)
 {
-    k_bb_cellflag<<<kCells / 256, 256, 0, st>>>(tab_of(table), slot_of, cflag_of(table));
-    set_smem(k_bb_extract_stencil, extract_smem(nb));
-    k_bb_extract_stencil<<<bb_num_ctas(), kBbThreads, extract_smem(nb), st>>>(
-        s, N, F, x, spk, spi, tab_of(table), meta_of(table), cflag_of(table), nb, slot_of, cursor, ck, cid, cdel, ida,
-        posa, digit_hist);
+    k_bb_extract<<<bb_num_ctas(), kBbThreads, sizeof(int16_t) * nb, st>>>(N, x, bkt, nb, slot_of, cursor, ck, cid, ida,
+                                                                         posa, digit_hist);
 }
 
-void bb_cdelta_stencil(const StencilArgs &s, int32_t F, const double *x, const int32_t *cid, int64_t C, i128 *cdel,
-                       cudaStream_t st)
+void bb_cdelta_stencil(const StencilArgs &s, int32_t F, const double *x, const int32_t *cid, const int32_t *perm,
+                       int64_t C, i128 *cdel, cudaStream_t st)
 {
-    if (C > 0) k_bb_cdelta_stencil<<<(unsigned)((C + 255) / 256), 256, 0, st>>>(s, F, x, cid, C, cdel);
+    if (C > 0) k_bb_cdelta_stencil<<<(unsigned)((C + 255) / 256), 256, 0, st>>>(s, F, x, cid, perm, C, cdel);
 }
 
-void bb_cdelta_sell(const SellArgs &s, int32_t F, const double *x, const int32_t *cid, int64_t C, i128 *cdel,
-                    cudaStream_t st)
+void bb_cdelta_sell(const SellArgs &s, int32_t F, const double *x, const int32_t *cid, const int32_t *perm, int64_t C,
+                    i128 *cdel, cudaStream_t st)
 {
-    if (C > 0) k_bb_cdelta_sell<<<(unsigned)((C + 255) / 256), 256, 0, st>>>(s, F, x, cid, C, cdel);
-}
-
-void bb_extract_sell(const SellArgs &s, int32_t F, const double *x, const u64 *spk, const int32_t *spi, void *table,
-                     int32_t nb, const int16_t *slot_of, u64 *cursor, u64 *ck, int32_t *cid, i128 *cdel, u64 *ida,
-                     int32_t *posa, u64 *digit_hist, cudaStream_t st)
-{
-    k_bb_cellflag<<<kCells / 256, 256, 0, st>>>(tab_of(table), slot_of, cflag_of(table));
-    set_smem(k_bb_extract_sell, extract_smem(nb));
-    k_bb_extract_sell<<<bb_num_ctas(), kBbThreads, extract_smem(nb), st>>>(
-        s, F, x, spk, spi, tab_of(table), meta_of(table), cflag_of(table), nb, slot_of, cursor, ck, cid, cdel, ida,
-        posa, digit_hist);
+    if (C > 0) k_bb_cdelta_sell<<<(unsigned)((C + 255) / 256), 256, 0, st>>>(s, F, x, cid, perm, C, cdel);
 }
 
 void bb_gather(const u64 *ck, const int32_t *perm, int64_t C, u64 *kb, int32_t *jb, u64 *digit_hist, cudaStream_t st)
