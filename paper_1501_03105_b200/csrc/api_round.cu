@@ -181,7 +181,12 @@ static irls_status sweep_bb(irls_ctx *c, const double *xfull, int *launches, boo
         hslot[cand[j]] = (int16_t)j;
     }
     const int64_t C = dst[nc];
-    if (C > n / 4) return IRLS_OK;  // pruning failed: the full path
+    // (IRLS_SWEEP_BB_MAX: a smaller limit on the candidates, for tests)
+    const int64_t cmax = getenv("IRLS_SWEEP_BB_MAX") ? atoll(getenv("IRLS_SWEEP_BB_MAX")) : n / 4;
+    if (C > cmax) {  // pruning failed: the full path, also for the next sweeps
+        c->bb_skip = 8;
+        return IRLS_OK;
+    }
     const size_t Cs = (size_t)std::max<int64_t>(C, 1);
     u64 *ck = (u64 *)talloc(8 * Cs), *k1 = (u64 *)talloc(8 * Cs), *k2 = (u64 *)talloc(8 * Cs);
     u64 *cursor = (u64 *)talloc(8 * (size_t)std::max(nc, 1));
@@ -251,7 +256,12 @@ irls_status sweep_rank0(irls_ctx *c, const double *xfull, uint8_t *side, int32_t
     bool bb_done = false;
     int32_t *ord = nullptr;
     c->sweep_sorted = 0;
-    if (!order && n >= (1 << 20) && !getenv("IRLS_SWEEP_FULL")) {
+    // (after a sweep whose bound pruned too little, the next 8 sweeps of this
+    // context go straight to the full sort: the potentials of consecutive
+    // solves are alike)
+    const bool try_bb = !order && n >= (1 << 20) && !getenv("IRLS_SWEEP_FULL") && c->bb_skip == 0;
+    if (!order && c->bb_skip > 0) c->bb_skip--;
+    if (try_bb) {
         s = sweep_bb(c, xfull, &launches, &bb_done);
         if (s) return s;
     }

@@ -154,6 +154,7 @@ struct irls_ctx {
     int64_t sweep_k = 0;
     double sweep_cut = 0.0;
     int64_t sweep_sorted = 0;  // nodes the last sweep radix-sorted
+    int32_t bb_skip = 0;       // sweeps left that skip the branch-and-bound attempt
 
     // two-level rounding (rank 0)
     irls::TLBuffers tl{};

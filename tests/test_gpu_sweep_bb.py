@@ -34,12 +34,19 @@ def irls():
 
 
 @pytest.fixture(scope="module")
-def grid(irls):
-    """A 128x128x64 blob grid (n~ = 2^20): the GPU context and an oracle
-    solver over the same graph (the oracle only sweeps given potentials)."""
+def shared(irls):
     spec = gen.blob_grid(128, 128, 64, seed=11)
+    return spec, oracle.Solver(oracle.Graph(spec), T=4)
+
+
+@pytest.fixture
+def grid(irls, shared):
+    """A 128x128x64 blob grid (n~ = 2^20): a fresh GPU context per test (a
+    sweep whose bound prunes too little makes the context skip the attempt
+    for its next sweeps) and an oracle solver over the same graph (the oracle
+    only sweeps given potentials)."""
+    spec, S = shared
     m = irls.MinCut.from_spec(spec, irls.options(T=4))
-    S = oracle.Solver(oracle.Graph(spec), T=4)
     yield spec, m, S
     m.close()
 
@@ -91,11 +98,33 @@ def test_ties(irls, grid, levels):
 
 def test_ties_on_solved(irls, grid):
     """Solved potentials rounded to 3 digits: long runs of equal keys inside
-    the candidate buckets."""
+    the candidate buckets (ties leave in ascending id)."""
     spec, m, S = grid
     m.irls_solve(irls.IRLS_FROM_SCRATCH, T=4, reports=False)
     x = np.round(m.irls_get_potentials(), 3)
-    _check(m, S, x, expect_bb=False)
+    assert len(np.unique(x)) < 1100
+    _check(m, S, x, expect_bb=True)
+
+
+def test_skip_after_failed_pruning(irls, grid):
+    """When the bound prunes too little (here: a limit of 1000 candidate
+    nodes), the sweep falls back to the full sort and the next 8 sweeps skip
+    the attempt; then it tries again."""
+    spec, m, S = grid
+    m.irls_solve(irls.IRLS_FROM_SCRATCH, T=4, reports=False)
+    xs = m.irls_get_potentials()
+    os.environ["IRLS_SWEEP_BB_MAX"] = "1000"
+    try:
+        k0 = m.irls_sweep_cut(side=False)[2]
+    finally:
+        os.environ.pop("IRLS_SWEEP_BB_MAX", None)
+    assert m.irls_get_stats()["sweep_sorted"] == m.n
+    for i in range(9):
+        k = m.irls_sweep_cut(side=False)[2]
+        if i < 8:
+            assert m.irls_get_stats()["sweep_sorted"] == m.n
+    assert 0 < m.irls_get_stats()["sweep_sorted"] < m.n // 4
+    assert k == k0 == S.sweep(xs).k
 
 
 def test_uniform_random(irls, grid):
