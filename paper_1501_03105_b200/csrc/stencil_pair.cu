@@ -14,6 +14,7 @@
 // bitwise unchanged (the accumulators are never -0.0), so these kernels give
 // the same bits as the scalar ones and as the oracle.
 #include <algorithm>
+#include <cstdlib>
 #include "kernels.h"
 
 namespace irls {
@@ -351,6 +352,216 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_fused(StencilArgs s, Ve
         acc[2] = acc[2] + r1 * r1;
         acc[3] = acc[3] + mb1 * mb1;
         acc[4] = acc[4] + gs2.y * gs2.y;
+    }
+    if (c3_chunk_epilogue<5>(acc, v.chunk0 + (int32_t)blockIdx.x, ra) && cd.finalize && threadIdx.x == 0) {
+        finalize_start(ra.ctrl, ra.slots);
+        set_cond2(cd, ra.ctrl);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K1 fused, TMA-fed (nx = 512, ny a multiple of 8: config 4's rows).  A chunk
+// is 8 whole rows, iteration j = row y0 + j.  Instead of every thread loading
+// its pair's operands into registers, one thread streams the rows the CTA
+// needs into shared memory with 1-D bulk copies (cp.async.bulk, 4 KB per
+// row) completing on mbarriers, up to two iterations ahead: per iteration x
+// of row j+1 (kept in a 4-row ring, so the +-y neighbours' x come from the
+// rows of the neighbouring iterations), x of the planes above and below, cx,
+// cy, cz, cz of the plane below (cs, ct, used last, are plain loads).  The threads read their operands from shared
+// memory (the -x / +x neighbours too: a row is self-contained) and compute
+// exactly what k_pair_fused computes, in the same order (same bits).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity)
+{
+    // bounded: a phase that never completes (a byte-count bug) traps instead
+    // of hanging the device
+    for (long long spin = 0;; spin++) {
+        uint32_t ok;
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n"
+            "}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (spin > (1ll << 26)) __trap();
+    }
+}
+__device__ __forceinline__ void bulk_row(double *dst, const double *src, uint64_t *bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 4096, [%2];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+constexpr int kTR = 512;  // row length (doubles) of the TMA-fed K1
+
+struct K1Smem {
+    double xr[4][kTR];             // x rows, slot (row + 1) & 3, rows -1 .. 8
+    double st[2][6][kTR];          // per stage: xu, xd, cx, cy, cz, czd
+    double cym0[kTR];              // cy of row -1 (iteration 0's -y conductance)
+    unsigned long long bar[3];     // full[0], full[1], prologue
+};
+
+template <int MODE, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_pair_fused_tma(StencilArgs s, VecArgs v, RedArgs ra, CondArgs cd,
+                                                              double eps2, double *gs_out, double *gt_out)
+{
+    if (v.frozen && *(const volatile int32_t *)v.frozen) return;  // fixed point: this step repeats the last one
+    extern __shared__ __align__(128) unsigned char k1_dyn[];
+    K1Smem &S = *reinterpret_cast<K1Smem *>(k1_dyn);
+    const int lane = threadIdx.x & 31, t = threadIdx.x;
+    const int64_t base = (int64_t)blockIdx.x * kChunk;
+    const int64_t P = s.P;
+    const double2 zero2 = make_double2(0.0, 0.0);
+    constexpr bool WARM = MODE == ASM_REWEIGHT_WARM;
+    // the chunk's rows: y0 .. y0 + 7 of plane z (global coordinates)
+    const PairCoord c0 = pair_coord(s, s.lo + base);
+    const int32_t y0 = c0.y, z = c0.z;
+    const bool hz = z > 0, pz = z < s.nz - 1, ylo = y0 > 0, yhi = y0 + 8 < s.ny;
+    uint64_t *full = reinterpret_cast<uint64_t *>(S.bar);
+    uint64_t *pro = full + 2;
+    auto issue = [&](int j) {  // stage j: x row j+1 and the per-iteration rows of row j
+        const int b = j & 1;
+        const int64_t r = base + (int64_t)kTR * j;
+        const bool xnext = j < 7 || yhi;
+        const unsigned n = 3 + (xnext ? 1 : 0) + (pz ? 1 : 0) + (hz ? 2 : 0);  // cx cy cz + optional rows
+        mbar_expect_tx(&full[b], 4096u * n);
+        if (xnext) bulk_row(S.xr[(j + 2) & 3], v.x + r + kTR, &full[b]);
+        if (pz) bulk_row(S.st[b][0], v.x + r + P, &full[b]);
+        if (hz) {
+            bulk_row(S.st[b][1], v.x + r - P, &full[b]);
+            bulk_row(S.st[b][5], s.cz + r - P, &full[b]);
+        }
+        bulk_row(S.st[b][2], s.cx + r, &full[b]);
+        bulk_row(S.st[b][3], s.cy + r, &full[b]);
+        bulk_row(S.st[b][4], s.cz + r, &full[b]);
+    };
+    if (t == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        mbar_init(pro, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_expect_tx(pro, 4096u * (ylo ? 3u : 1u));
+        bulk_row(S.xr[1], v.x + base, pro);
+        if (ylo) {
+            bulk_row(S.xr[0], v.x + base - kTR, pro);
+            bulk_row(S.cym0, s.cy + base - kTR, pro);
+        }
+        issue(0);
+        issue(1);
+    }
+    __syncthreads();
+    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    double2 gyprev = zero2;  // gy2 of the previous iteration (the -y conductance of this one)
+    mbar_wait(pro, 0);
+#pragma unroll 1
+    for (int j = 0; j < 8; j++) {
+        const int64_t u0 = base + 2 * (int64_t)t + kTR * j;
+        // the terminal capacities straight to registers (used last)
+        const double2 cs2 = ldp(s.cs, u0), ct2 = ldp(s.ct, u0);
+        mbar_wait(&full[j & 1], (j >> 1) & 1);
+        const int b = j & 1;
+        const bool hx = t > 0, hr = t < kThreads - 1;
+        const bool hy = ylo || j > 0, py = yhi || j < 7;
+        const double *xrow = S.xr[(j + 1) & 3];
+        const double2 x2 = *reinterpret_cast<const double2 *>(xrow + 2 * t);
+        const double2 cx2 = *reinterpret_cast<const double2 *>(S.st[b][2] + 2 * t);
+        const double2 cy2 = py ? *reinterpret_cast<const double2 *>(S.st[b][3] + 2 * t) : zero2;
+        const double2 cz2 = pz ? *reinterpret_cast<const double2 *>(S.st[b][4] + 2 * t) : zero2;
+        const double2 xpy = py ? *reinterpret_cast<const double2 *>(S.xr[(j + 2) & 3] + 2 * t) : zero2;
+        const double2 xpz = pz ? *reinterpret_cast<const double2 *>(S.st[b][0] + 2 * t) : zero2;
+        const double2 xmz = hz ? *reinterpret_cast<const double2 *>(S.st[b][1] + 2 * t) : zero2;
+        const double2 czm = hz ? *reinterpret_cast<const double2 *>(S.st[b][5] + 2 * t) : zero2;
+        const double2 xmy = (hy && (WARM || j == 0)) ? *reinterpret_cast<const double2 *>(S.xr[j & 3] + 2 * t) : zero2;
+        const double2 cym = (hy && j == 0) ? *reinterpret_cast<const double2 *>(S.cym0 + 2 * t) : zero2;
+        const double xl = hx ? xrow[2 * t - 1] : 0.0;
+        const double xr = hr ? xrow[2 * t + 2] : 0.0;
+        const double cxl = hx ? S.st[b][2][2 * t - 1] : 0.0;
+        // ---- owned edges (K1a)
+        double2 gx2;
+        gx2.x = rw_g(cx2.x, x2.x - x2.y, eps2);
+        gx2.y = hr ? rw_g(cx2.y, x2.y - xr, eps2) : 0.0;
+        double gxl = __shfl_up_sync(0xffffffffu, gx2.y, 1);
+        if (lane == 0) gxl = hx ? rw_g(cxl, xl - x2.x, eps2) : 0.0;
+        if (!hx) gxl = 0.0;
+        const double2 gy2 = py ? make_double2(rw_g(cy2.x, x2.x - xpy.x, eps2), rw_g(cy2.y, x2.y - xpy.y, eps2)) : zero2;
+        const double2 gz2 = pz ? make_double2(rw_g(cz2.x, x2.x - xpz.x, eps2), rw_g(cz2.y, x2.y - xpz.y, eps2)) : zero2;
+        // ---- lower-neighbour edges: previous iteration (-y), recompute (-z, row 0's -y)
+        double2 gym = zero2;
+        if (hy) gym = j > 0 ? gyprev : make_double2(rw_g(cym.x, xmy.x - x2.x, eps2), rw_g(cym.y, xmy.y - x2.y, eps2));
+        gyprev = gy2;
+        const double2 gzm = hz ? make_double2(rw_g(czm.x, xmz.x - x2.x, eps2), rw_g(czm.y, xmz.y - x2.y, eps2)) : zero2;
+        stp(s.gx, u0, gx2);
+        stp(s.gy, u0, gy2);
+        stp(s.gz, u0, gz2);
+        if (s.lo_ghost && u0 < P) stp(s.gz, u0 - P, gzm);  // the -z edge of the first owned plane (ghost slot)
+        // ---- terminals, D, Dinv, r0, z0 (K1b)
+        double2 gs2, gt2;
+        gs2.x = terminal_g(cs2.x, ct2.x, x2.x, eps2, gt2.x);
+        gs2.y = terminal_g(cs2.y, ct2.y, x2.y, eps2, gt2.y);
+        const double D0 = ((((((0.0 + gzm.x) + gym.x) + gxl) + gx2.x) + gy2.x) + gz2.x + gs2.x) + gt2.x;
+        const double D1 = ((((((0.0 + gzm.y) + gym.y) + gx2.x) + gx2.y) + gy2.y) + gz2.y + gs2.y) + gt2.y;
+        const double Di0 = 1.0 / D0, Di1 = 1.0 / D1;
+        double r0, r1;
+        if (WARM) {
+            double a = 0.0;
+            a = a + gzm.x * xmz.x;
+            a = a + gym.x * xmy.x;
+            a = a + gxl * xl;
+            a = a + gx2.x * x2.y;
+            a = a + gy2.x * xpy.x;
+            a = a + gz2.x * xpz.x;
+            r0 = gs2.x - (D0 * x2.x - a);
+            double bb = 0.0;
+            bb = bb + gzm.y * xmz.y;
+            bb = bb + gym.y * xmy.y;
+            bb = bb + gx2.x * x2.x;
+            bb = bb + gx2.y * xr;
+            bb = bb + gy2.y * xpy.y;
+            bb = bb + gz2.y * xpz.y;
+            r1 = gs2.y - (D1 * x2.y - bb);
+        } else {
+            r0 = gs2.x;
+            r1 = gs2.y;
+        }
+        const double z0 = r0 * Di0, z1 = r1 * Di1;
+        stp(v.D, u0, make_double2(D0, D1));
+        stp(v.Dinv, u0, make_double2(Di0, Di1));
+        stp(v.r, u0, make_double2(r0, r1));
+        stp(v.z, u0, make_double2(z0, z1));
+        if (gs_out) {
+            stp(gs_out, u0, gs2);
+            stp(gt_out, u0, gt2);
+        }
+        const double mb0 = gs2.x * Di0, mb1 = gs2.y * Di1;
+        acc[0] = acc[0] + r0 * z0;
+        acc[1] = acc[1] + z0 * z0;
+        acc[2] = acc[2] + r0 * r0;
+        acc[3] = acc[3] + mb0 * mb0;
+        acc[4] = acc[4] + gs2.x * gs2.x;
+        acc[0] = acc[0] + r1 * z1;
+        acc[1] = acc[1] + z1 * z1;
+        acc[2] = acc[2] + r1 * r1;
+        acc[3] = acc[3] + mb1 * mb1;
+        acc[4] = acc[4] + gs2.y * gs2.y;
+        if (j + 2 < 8) {
+            __syncthreads();  // stage j's buffers and x row j-1 are free
+            if (t == 0) issue(j + 2);
+        }
     }
     if (c3_chunk_epilogue<5>(acc, v.chunk0 + (int32_t)blockIdx.x, ra) && cd.finalize && threadIdx.x == 0) {
         finalize_start(ra.ctrl, ra.slots);
@@ -718,7 +929,27 @@ int launch_pair_assemble(const StencilArgs &s, const VecArgs &v, const RedArgs &
         // passes), 1.90 (4 CTAs/SM, spills) and 1.70 (2 CTAs/SM); a z-cluster
         // variant (8 CTAs, -z conductances from the CTA below via DSMEM after a
         // cluster barrier) measured 2.40 ms (round 2)
-        if (mode == ASM_REWEIGHT_WARM)
+        // TMA-fed variant for rows of exactly 512 in whole 8-row chunks
+        const bool tma = s.nx == 512 && s.ny % 8 == 0 && v.n_own % kChunk == 0 && !getenv("IRLS_K1_NOTMA");
+        if (tma) {
+            // 2 CTAs/SM (108 registers, 68 KB of staging each): config 4 1.485 ms
+            // against 1.55-1.57 ms for k_pair_fused; at 3 CTAs/SM (85
+            // registers) it spills: 1.73 ms
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(k_pair_fused_tma<ASM_REWEIGHT_WARM, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(K1Smem));
+                cudaFuncSetAttribute(k_pair_fused_tma<ASM_REWEIGHT_COLD, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(K1Smem));
+                attr = true;
+            }
+            if (mode == ASM_REWEIGHT_WARM)
+                k_pair_fused_tma<ASM_REWEIGHT_WARM, 2><<<nb, kThreads, sizeof(K1Smem), st>>>(s, v, ra, cd, eps2, gs_out,
+                                                                                             gt_out);
+            else
+                k_pair_fused_tma<ASM_REWEIGHT_COLD, 2><<<nb, kThreads, sizeof(K1Smem), st>>>(s, v, ra, cd, eps2, gs_out,
+                                                                                             gt_out);
+        } else if (mode == ASM_REWEIGHT_WARM)
             k_pair_fused<ASM_REWEIGHT_WARM, 3><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
         else
             k_pair_fused<ASM_REWEIGHT_COLD, 3><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
