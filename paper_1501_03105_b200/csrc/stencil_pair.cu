@@ -409,52 +409,68 @@ __device__ __forceinline__ void bulk_row(double *dst, const double *src, uint64_
 
 constexpr int kTR = 512;  // row length (doubles) of the TMA-fed K1
 
+template <bool ZM>
 struct K1Smem {
     double xr[4][kTR];             // x rows, slot (row + 1) & 3, rows -1 .. 8
     double st[2][6][kTR];          // per stage: xu, xd, cx, cy, cz, czd
     double cym0[kTR];              // cy of row -1 (iteration 0's -y conductance)
+    double gzr[ZM ? 8 : 1][kTR];   // ZM: the previous plane's +z conductances (this plane's -z)
     unsigned long long bar[3];     // full[0], full[1], prologue
 };
 
-template <int MODE, int MINB>
+// ZM (z-march): CTA (chunk column, segment of zp planes) takes the chunks of
+// its column plane after plane; the -z conductance of a node is the +z
+// conductance the same thread computed for the node below in the previous
+// chunk (kept in shared memory), so it is recomputed only in the segment's
+// first plane.  Every chunk keeps its own C3 epilogue.
+template <int MODE, int MINB, bool ZM>
 __global__ void __launch_bounds__(kThreads, MINB) k_pair_fused_tma(StencilArgs s, VecArgs v, RedArgs ra, CondArgs cd,
-                                                              double eps2, double *gs_out, double *gt_out)
+                                                              double eps2, double *gs_out, double *gt_out, int zp)
 {
     if (v.frozen && *(const volatile int32_t *)v.frozen) return;  // fixed point: this step repeats the last one
     extern __shared__ __align__(128) unsigned char k1_dyn[];
-    K1Smem &S = *reinterpret_cast<K1Smem *>(k1_dyn);
+    K1Smem<ZM> &S = *reinterpret_cast<K1Smem<ZM> *>(k1_dyn);
     const int lane = threadIdx.x & 31, t = threadIdx.x;
-    const int64_t base = (int64_t)blockIdx.x * kChunk;
     const int64_t P = s.P;
     const double2 zero2 = make_double2(0.0, 0.0);
     constexpr bool WARM = MODE == ASM_REWEIGHT_WARM;
-    // the chunk's rows: y0 .. y0 + 7 of plane z (global coordinates)
-    const PairCoord c0 = pair_coord(s, s.lo + base);
-    const int32_t y0 = c0.y, z = c0.z;
-    const bool hz = z > 0, pz = z < s.nz - 1, ylo = y0 > 0, yhi = y0 + 8 < s.ny;
+    const int32_t Pc = ZM ? (int32_t)(P / kChunk) : 1;
+    const int32_t cxi = ZM ? (int32_t)blockIdx.x % Pc : (int32_t)blockIdx.x;
+    const int32_t zl0 = ZM ? ((int32_t)blockIdx.x / Pc) * zp : 0;
+    const int32_t zl1 = ZM ? min(zl0 + zp, (int32_t)(v.n_own / P)) : 1;
     uint64_t *full = reinterpret_cast<uint64_t *>(S.bar);
     uint64_t *pro = full + 2;
-    auto issue = [&](int j) {  // stage j: x row j+1 and the per-iteration rows of row j
-        const int b = j & 1;
-        const int64_t r = base + (int64_t)kTR * j;
-        const bool xnext = j < 7 || yhi;
-        const unsigned n = 3 + (xnext ? 1 : 0) + (pz ? 1 : 0) + (hz ? 2 : 0);  // cx cy cz + optional rows
-        mbar_expect_tx(&full[b], 4096u * n);
-        if (xnext) bulk_row(S.xr[(j + 2) & 3], v.x + r + kTR, &full[b]);
-        if (pz) bulk_row(S.st[b][0], v.x + r + P, &full[b]);
-        if (hz) {
-            bulk_row(S.st[b][1], v.x + r - P, &full[b]);
-            bulk_row(S.st[b][5], s.cz + r - P, &full[b]);
-        }
-        bulk_row(S.st[b][2], s.cx + r, &full[b]);
-        bulk_row(S.st[b][3], s.cy + r, &full[b]);
-        bulk_row(S.st[b][4], s.cz + r, &full[b]);
-    };
     if (t == 0) {
         mbar_init(&full[0], 1);
         mbar_init(&full[1], 1);
         mbar_init(pro, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+#pragma unroll 1
+    for (int32_t zl = zl0; zl < zl1; zl++) {
+    const int32_t chunk = ZM ? zl * Pc + cxi : cxi;
+    const int64_t base = (int64_t)chunk * kChunk;
+    const bool zr = ZM && zl > zl0;  // -z conductances from the previous chunk of this CTA
+    // the chunk's rows: y0 .. y0 + 7 of plane z (global coordinates)
+    const PairCoord c0 = pair_coord(s, s.lo + base);
+    const int32_t y0 = c0.y, z = c0.z;
+    const bool hz = z > 0, pz = z < s.nz - 1, ylo = y0 > 0, yhi = y0 + 8 < s.ny;
+    auto issue = [&](int j) {  // stage j: x row j+1 and the per-iteration rows of row j
+        const int b = j & 1;
+        const int64_t r = base + (int64_t)kTR * j;
+        const bool xnext = j < 7 || yhi;
+        const bool czd = hz && !zr;
+        const unsigned n = 3 + (xnext ? 1 : 0) + (pz ? 1 : 0) + (hz ? 1 : 0) + (czd ? 1 : 0);  // cx cy cz + optional
+        mbar_expect_tx(&full[b], 4096u * n);
+        if (xnext) bulk_row(S.xr[(j + 2) & 3], v.x + r + kTR, &full[b]);
+        if (pz) bulk_row(S.st[b][0], v.x + r + P, &full[b]);
+        if (hz) bulk_row(S.st[b][1], v.x + r - P, &full[b]);
+        if (czd) bulk_row(S.st[b][5], s.cz + r - P, &full[b]);
+        bulk_row(S.st[b][2], s.cx + r, &full[b]);
+        bulk_row(S.st[b][3], s.cy + r, &full[b]);
+        bulk_row(S.st[b][4], s.cz + r, &full[b]);
+    };
+    if (t == 0) {  // (the previous chunk's epilogue ended with a block barrier: its buffers are free)
         mbar_expect_tx(pro, 4096u * (ylo ? 3u : 1u));
         bulk_row(S.xr[1], v.x + base, pro);
         if (ylo) {
@@ -467,7 +483,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_fused_tma(StencilArgs s
     __syncthreads();
     double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     double2 gyprev = zero2;  // gy2 of the previous iteration (the -y conductance of this one)
-    mbar_wait(pro, 0);
+    mbar_wait(pro, (unsigned)(zl - zl0) & 1u);
 #pragma unroll 1
     for (int j = 0; j < 8; j++) {
         const int64_t u0 = base + 2 * (int64_t)t + kTR * j;
@@ -485,7 +501,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_fused_tma(StencilArgs s
         const double2 xpy = py ? *reinterpret_cast<const double2 *>(S.xr[(j + 2) & 3] + 2 * t) : zero2;
         const double2 xpz = pz ? *reinterpret_cast<const double2 *>(S.st[b][0] + 2 * t) : zero2;
         const double2 xmz = hz ? *reinterpret_cast<const double2 *>(S.st[b][1] + 2 * t) : zero2;
-        const double2 czm = hz ? *reinterpret_cast<const double2 *>(S.st[b][5] + 2 * t) : zero2;
+        const double2 czm = (hz && !zr) ? *reinterpret_cast<const double2 *>(S.st[b][5] + 2 * t) : zero2;
         const double2 xmy = (hy && (WARM || j == 0)) ? *reinterpret_cast<const double2 *>(S.xr[j & 3] + 2 * t) : zero2;
         const double2 cym = (hy && j == 0) ? *reinterpret_cast<const double2 *>(S.cym0 + 2 * t) : zero2;
         const double xl = hx ? xrow[2 * t - 1] : 0.0;
@@ -504,7 +520,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_fused_tma(StencilArgs s
         double2 gym = zero2;
         if (hy) gym = j > 0 ? gyprev : make_double2(rw_g(cym.x, xmy.x - x2.x, eps2), rw_g(cym.y, xmy.y - x2.y, eps2));
         gyprev = gy2;
-        const double2 gzm = hz ? make_double2(rw_g(czm.x, xmz.x - x2.x, eps2), rw_g(czm.y, xmz.y - x2.y, eps2)) : zero2;
+        double2 gzm = zero2;
+        if (hz)
+            gzm = zr ? *reinterpret_cast<const double2 *>(S.gzr[ZM ? j : 0] + 2 * t)
+                     : make_double2(rw_g(czm.x, xmz.x - x2.x, eps2), rw_g(czm.y, xmz.y - x2.y, eps2));
+        if (ZM) *reinterpret_cast<double2 *>(S.gzr[ZM ? j : 0] + 2 * t) = gz2;
         stp(s.gx, u0, gx2);
         stp(s.gy, u0, gy2);
         stp(s.gz, u0, gz2);
@@ -563,9 +583,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_fused_tma(StencilArgs s
             if (t == 0) issue(j + 2);
         }
     }
-    if (c3_chunk_epilogue<5>(acc, v.chunk0 + (int32_t)blockIdx.x, ra) && cd.finalize && threadIdx.x == 0) {
+    if (c3_chunk_epilogue<5>(acc, v.chunk0 + chunk, ra) && cd.finalize && threadIdx.x == 0) {
         finalize_start(ra.ctrl, ra.slots);
         set_cond2(cd, ra.ctrl);
+    }
+    __syncthreads();  // (ZM) every thread is done with this chunk's buffers
     }
 }
 
@@ -937,18 +959,37 @@ int launch_pair_assemble(const StencilArgs &s, const VecArgs &v, const RedArgs &
             // registers) it spills: 1.73 ms
             static bool attr = false;
             if (!attr) {
-                cudaFuncSetAttribute(k_pair_fused_tma<ASM_REWEIGHT_WARM, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sizeof(K1Smem));
-                cudaFuncSetAttribute(k_pair_fused_tma<ASM_REWEIGHT_COLD, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sizeof(K1Smem));
+                cudaFuncSetAttribute(k_pair_fused_tma<ASM_REWEIGHT_WARM, 2, false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K1Smem<false>));
+                cudaFuncSetAttribute(k_pair_fused_tma<ASM_REWEIGHT_COLD, 2, false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K1Smem<false>));
+                cudaFuncSetAttribute(k_pair_fused_tma<ASM_REWEIGHT_WARM, 2, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K1Smem<true>));
+                cudaFuncSetAttribute(k_pair_fused_tma<ASM_REWEIGHT_COLD, 2, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K1Smem<true>));
                 attr = true;
             }
-            if (mode == ASM_REWEIGHT_WARM)
-                k_pair_fused_tma<ASM_REWEIGHT_WARM, 2><<<nb, kThreads, sizeof(K1Smem), st>>>(s, v, ra, cd, eps2, gs_out,
-                                                                                             gt_out);
+            // z-march segments of 8 planes (2,048 CTAs on config 4): 1.42 ms against
+            // 1.50 ms per chunk (same box); 4 planes 1.46 ms, 16 1.52-1.54, 32 1.59
+            // (fewer CTAs than 7 waves of 296 leave a tail); IRLS_K1_ZP overrides
+            static const int zp_env = getenv("IRLS_K1_ZP") ? atoi(getenv("IRLS_K1_ZP")) : 8;
+            const int64_t nzl = v.n_own / s.P;
+            const bool zm = zp_env > 1 && v.n_own % s.P == 0 && nzl > 1;
+            if (zm) {
+                const int zp = (int)std::min<int64_t>(zp_env, nzl);
+                const unsigned g = (unsigned)((s.P / kChunk) * ((nzl + zp - 1) / zp));
+                if (mode == ASM_REWEIGHT_WARM)
+                    k_pair_fused_tma<ASM_REWEIGHT_WARM, 2, true><<<g, kThreads, sizeof(K1Smem<true>), st>>>(
+                        s, v, ra, cd, eps2, gs_out, gt_out, zp);
+                else
+                    k_pair_fused_tma<ASM_REWEIGHT_COLD, 2, true><<<g, kThreads, sizeof(K1Smem<true>), st>>>(
+                        s, v, ra, cd, eps2, gs_out, gt_out, zp);
+            } else if (mode == ASM_REWEIGHT_WARM)
+                k_pair_fused_tma<ASM_REWEIGHT_WARM, 2, false><<<nb, kThreads, sizeof(K1Smem<false>), st>>>(
+                    s, v, ra, cd, eps2, gs_out, gt_out, 1);
             else
-                k_pair_fused_tma<ASM_REWEIGHT_COLD, 2><<<nb, kThreads, sizeof(K1Smem), st>>>(s, v, ra, cd, eps2, gs_out,
-                                                                                             gt_out);
+                k_pair_fused_tma<ASM_REWEIGHT_COLD, 2, false><<<nb, kThreads, sizeof(K1Smem<false>), st>>>(
+                    s, v, ra, cd, eps2, gs_out, gt_out, 1);
         } else if (mode == ASM_REWEIGHT_WARM)
             k_pair_fused<ASM_REWEIGHT_WARM, 3><<<nb, kThreads, 0, st>>>(s, v, ra, cd, eps2, gs_out, gt_out);
         else
