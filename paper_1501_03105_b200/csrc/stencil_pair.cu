@@ -440,47 +440,61 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_fused_tma(StencilArgs s
     const int32_t zl1 = ZM ? min(zl0 + zp, (int32_t)(v.n_own / P)) : 1;
     uint64_t *full = reinterpret_cast<uint64_t *>(S.bar);
     uint64_t *pro = full + 2;
-    if (t == 0) {
-        mbar_init(&full[0], 1);
-        mbar_init(&full[1], 1);
-        mbar_init(pro, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-#pragma unroll 1
-    for (int32_t zl = zl0; zl < zl1; zl++) {
-    const int32_t chunk = ZM ? zl * Pc + cxi : cxi;
-    const int64_t base = (int64_t)chunk * kChunk;
-    const bool zr = ZM && zl > zl0;  // -z conductances from the previous chunk of this CTA
-    // the chunk's rows: y0 .. y0 + 7 of plane z (global coordinates)
-    const PairCoord c0 = pair_coord(s, s.lo + base);
-    const int32_t y0 = c0.y, z = c0.z;
-    const bool hz = z > 0, pz = z < s.nz - 1, ylo = y0 > 0, yhi = y0 + 8 < s.ny;
-    auto issue = [&](int j) {  // stage j: x row j+1 and the per-iteration rows of row j
+    struct Geo {
+        int64_t base;
+        bool hz, pz, ylo, yhi, zr;
+    };
+    auto geo = [&](int32_t zl_) {
+        Geo g;
+        g.base = (int64_t)(ZM ? zl_ * Pc + cxi : cxi) * kChunk;
+        // the chunk's rows: y0 .. y0 + 7 of plane z (global coordinates)
+        const PairCoord c0 = pair_coord(s, s.lo + g.base);
+        g.hz = c0.z > 0;
+        g.pz = c0.z < s.nz - 1;
+        g.ylo = c0.y > 0;
+        g.yhi = c0.y + 8 < s.ny;
+        g.zr = ZM && zl_ > zl0;  // -z conductances from the previous chunk of this CTA
+        return g;
+    };
+    auto issue = [&](const Geo &g, int j) {  // stage j: x row j+1 and the per-iteration rows of row j
         const int b = j & 1;
-        const int64_t r = base + (int64_t)kTR * j;
-        const bool xnext = j < 7 || yhi;
-        const bool czd = hz && !zr;
-        const unsigned n = 3 + (xnext ? 1 : 0) + (pz ? 1 : 0) + (hz ? 1 : 0) + (czd ? 1 : 0);  // cx cy cz + optional
+        const int64_t r = g.base + (int64_t)kTR * j;
+        const bool xnext = j < 7 || g.yhi;
+        const bool czd = g.hz && !g.zr;
+        const unsigned n = 3 + (xnext ? 1 : 0) + (g.pz ? 1 : 0) + (g.hz ? 1 : 0) + (czd ? 1 : 0);  // cx cy cz + optional
         mbar_expect_tx(&full[b], 4096u * n);
         if (xnext) bulk_row(S.xr[(j + 2) & 3], v.x + r + kTR, &full[b]);
-        if (pz) bulk_row(S.st[b][0], v.x + r + P, &full[b]);
-        if (hz) bulk_row(S.st[b][1], v.x + r - P, &full[b]);
+        if (g.pz) bulk_row(S.st[b][0], v.x + r + P, &full[b]);
+        if (g.hz) bulk_row(S.st[b][1], v.x + r - P, &full[b]);
         if (czd) bulk_row(S.st[b][5], s.cz + r - P, &full[b]);
         bulk_row(S.st[b][2], s.cx + r, &full[b]);
         bulk_row(S.st[b][3], s.cy + r, &full[b]);
         bulk_row(S.st[b][4], s.cz + r, &full[b]);
     };
-    if (t == 0) {  // (the previous chunk's epilogue ended with a block barrier: its buffers are free)
-        mbar_expect_tx(pro, 4096u * (ylo ? 3u : 1u));
-        bulk_row(S.xr[1], v.x + base, pro);
-        if (ylo) {
-            bulk_row(S.xr[0], v.x + base - kTR, pro);
-            bulk_row(S.cym0, s.cy + base - kTR, pro);
+    auto start = [&](const Geo &g) {  // the chunk's prologue rows and its first two stages
+        mbar_expect_tx(pro, 4096u * (g.ylo ? 3u : 1u));
+        bulk_row(S.xr[1], v.x + g.base, pro);
+        if (g.ylo) {
+            bulk_row(S.xr[0], v.x + g.base - kTR, pro);
+            bulk_row(S.cym0, s.cy + g.base - kTR, pro);
         }
-        issue(0);
-        issue(1);
+        issue(g, 0);
+        issue(g, 1);
+    };
+    if (t == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        mbar_init(pro, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        start(geo(zl0));
     }
     __syncthreads();
+#pragma unroll 1
+    for (int32_t zl = zl0; zl < zl1; zl++) {
+    const Geo G = geo(zl);
+    const int32_t chunk = ZM ? zl * Pc + cxi : cxi;
+    const int64_t base = G.base;
+    const bool zr = G.zr, hz = G.hz, pz = G.pz, ylo = G.ylo, yhi = G.yhi;
     double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     double2 gyprev = zero2;  // gy2 of the previous iteration (the -y conductance of this one)
     mbar_wait(pro, (unsigned)(zl - zl0) & 1u);
@@ -580,14 +594,17 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_fused_tma(StencilArgs s
         acc[4] = acc[4] + gs2.y * gs2.y;
         if (j + 2 < 8) {
             __syncthreads();  // stage j's buffers and x row j-1 are free
-            if (t == 0) issue(j + 2);
+            if (t == 0) issue(G, j + 2);
         }
+    }
+    if (ZM && zl + 1 < zl1) {  // the next chunk's rows while this one reduces (-2% against after it)
+        __syncthreads();  // every thread is done with this chunk's staging buffers
+        if (t == 0) start(geo(zl + 1));
     }
     if (c3_chunk_epilogue<5>(acc, v.chunk0 + chunk, ra) && cd.finalize && threadIdx.x == 0) {
         finalize_start(ra.ctrl, ra.slots);
         set_cond2(cd, ra.ctrl);
     }
-    __syncthreads();  // (ZM) every thread is done with this chunk's buffers
     }
 }
 
