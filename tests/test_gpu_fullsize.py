@@ -83,6 +83,11 @@ def _sweep_equal(m, gold, where):
     assert float(cut).hex() == gold["cut_value"], where
     assert _sha(side.astype(np.uint8)) == gold["side_sha256"], where
     assert _sha(order.astype(np.int32)) == gold["order_sha256"], where
+    # without the order: the branch-and-bound sweep (n~ >= 2^20) — same k, cut, side
+    side, _, k, cut = m.irls_sweep_cut(side=True)
+    assert k == gold["k"], where + " (branch and bound)"
+    assert float(cut).hex() == gold["cut_value"], where + " (branch and bound)"
+    assert _sha(side.astype(np.uint8)) == gold["side_sha256"], where + " (branch and bound)"
 
 
 def test_config2_full_trajectory(irls):
@@ -98,6 +103,9 @@ def test_config2_full_trajectory(irls):
     sw = S.sweep()
     assert k == sw.k and cut == sw.cut_value
     assert np.array_equal(side, sw.side) and np.array_equal(order.astype(np.int64), sw.order)
+    side, _, k, cut = m.irls_sweep_cut(side=True)  # branch and bound (no order)
+    assert m.irls_get_stats()["sweep_sorted"] < m.n // 4
+    assert k == sw.k and cut == sw.cut_value and np.array_equal(side, sw.side)
 
 
 def _golden_solve(irls, name, spec):
