@@ -8,35 +8,50 @@
 // ---------------------------------------------------------------------------
 // sweep cut
 // ---------------------------------------------------------------------------
+// Sweep buffers in two parts: what every sweep needs (flags, k, the k-th node,
+// side[], the radix look-back words the candidates' sort reuses), and the
+// n-sized arrays of the full sort (keys, ids, delta, order, tile scans), which
+// the branch-and-bound sweep does not touch (3.2 GB on config 4).
+static irls_status alloc_sweep_base(irls_ctx *c)
+{
+    SweepBuffers &b = c->sb;
+    if (b.flags) return IRLS_OK;
+    const int64_t n = c->n_glob, nt = sweep_ntiles(n);
+    b.n = n;
+    b.rank = nullptr;  // the sweep forms membership from x (two-level uses its own ranks)
+    b.tile_hist = dalloc<int32_t>(c, 2 * 256 * nt);  // look-back words of radix tiles down to 2048 keys
+    b.digit_hist = dalloc<unsigned long long>(c, 8 * 256);
+    b.flags = dalloc<int32_t>(c, 4);
+    b.k_out = dalloc<int64_t>(c, 1);
+    b.lastv = dalloc<int32_t>(c, 1);
+    b.side = dalloc<uint8_t>(c, c->n_total);
+    if (!b.tile_hist || !b.digit_hist || !b.flags || !b.k_out || !b.lastv || !b.side)
+        return fail(c, IRLS_ERR_OOM, "sweep buffers");
+    return IRLS_OK;
+}
+
 static irls_status alloc_sweep(irls_ctx *c)
 {
+    irls_status s = alloc_sweep_base(c);
+    if (s) return s;
     if (c->sb.keys) return IRLS_OK;
     SweepBuffers &b = c->sb;
     const int64_t n = c->n_glob, nt = sweep_ntiles(n);
-    b.n = n;
     b.keys = dalloc<unsigned long long>(c, n);
     b.keys_alt = dalloc<unsigned long long>(c, n);
     b.vals = dalloc<int32_t>(c, n);
     b.vals_alt = dalloc<int32_t>(c, n);
-    b.rank = nullptr;  // the sweep forms membership from x (two-level uses its own ranks)
-    b.tile_hist = dalloc<int32_t>(c, 2 * 256 * nt);  // look-back words of radix tiles down to 2048 keys
     b.tile_off = dalloc<int32_t>(c, 256 * nt);
     b.scan_tmp = (int32_t *)dalloc<int64_t>(c, (256 * nt + 4095) / 4096 + 1);
-    b.digit_hist = dalloc<unsigned long long>(c, 8 * 256);
     b.delta = dalloc<__int128>(c, n + 2);
     b.tile_sum = dalloc<__int128>(c, nt);
     b.tile_incl = dalloc<__int128>(c, nt);
     b.qcs_tile = dalloc<__int128>(c, nt);
     b.tile_min = dalloc<__int128>(c, nt);
     b.tile_argmin = dalloc<int64_t>(c, nt);
-    b.flags = dalloc<int32_t>(c, 4);
-    b.k_out = dalloc<int64_t>(c, 1);
-    b.lastv = dalloc<int32_t>(c, 1);
-    b.side = dalloc<uint8_t>(c, c->n_total);
     c->order_out = dalloc<int32_t>(c, n);
-    if (!b.keys || !b.keys_alt || !b.vals || !b.vals_alt || !b.tile_hist || !b.tile_off || !b.scan_tmp ||
-        !b.digit_hist || !b.delta || !b.tile_sum || !b.tile_incl || !b.qcs_tile || !b.tile_min || !b.tile_argmin || !b.flags || !b.k_out || !b.lastv || !b.side ||
-        !c->order_out)
+    if (!b.keys || !b.keys_alt || !b.vals || !b.vals_alt || !b.tile_off || !b.scan_tmp || !b.delta || !b.tile_sum ||
+        !b.tile_incl || !b.qcs_tile || !b.tile_min || !b.tile_argmin || !c->order_out)
         return fail(c, IRLS_ERR_OOM, "sweep buffers");
     return IRLS_OK;
 }
@@ -246,7 +261,7 @@ irls_status sweep_rank0(irls_ctx *c, const double *xfull, uint8_t *side, int32_t
 {
     cudaStream_t st = c->stream;
     const int64_t n = c->n_glob;
-    irls_status s = alloc_sweep(c);
+    irls_status s = alloc_sweep_base(c);
     if (s) return s;
     int launches = 0;
     c->launches = 0;
@@ -266,6 +281,8 @@ irls_status sweep_rank0(irls_ctx *c, const double *xfull, uint8_t *side, int32_t
         if (s) return s;
     }
     if (!bb_done) {
+        s = alloc_sweep(c);
+        if (s) return s;
         CK(cudaMemsetAsync(b.flags, 0, sizeof(int32_t) * 4, st));
         CK(cudaMemsetAsync(b.digit_hist, 0, sizeof(unsigned long long) * 8 * 256, st));
         if (c->kind == 0) sweep_prep_stencil(stencil_args(c, true), n, c->F, xfull, b, st);
