@@ -190,7 +190,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--config", default="config4")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--e2e-serial", action="store_true", help="e2e: one step after the other (no create/solve overlap)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-planes", type=int, default=16,
@@ -502,7 +502,10 @@ def main():
             rc = I.lib().irls_sweep_cut(mm.h, side_host.ctypes.data_as(C.c_void_p), None, C.byref(kk), C.byref(cc))
             if rc:
                 raise I.IrlsError(rc, "irls_sweep_cut")
+            t1r = time.perf_counter()
+            p_times.append(("sweep_d2h", 1e3 * (t1r - t0r) - p_times[-1][1]))
             mm.close()
+            p_times.append(("destroy", 1e3 * (time.perf_counter() - t1r)))
             return tot
 
         with ThreadPoolExecutor(1) as ex:
@@ -531,8 +534,8 @@ def main():
         e2e_value = n_links * piters / (e2e_ms * 1e-3) / 1e9
         step_ms = None
         e2e_mode = "pipelined"
-        p_phase = {k: statistics.mean([v for kk, v in p_times if kk == k]) for k in ("create", "solve")
-                   if any(kk == k for kk, _ in p_times)}
+        p_phase = {k: statistics.mean([v for kk, v in p_times if kk == k])
+                   for k in ("create", "solve", "sweep_d2h", "destroy") if any(kk == k for kk, _ in p_times)}
 
     if rank != 0:
         if world > 1:
