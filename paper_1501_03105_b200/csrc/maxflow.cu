@@ -16,7 +16,6 @@
 #include <atomic>
 #include <cstdlib>
 #include <climits>
-#include <deque>
 #include <thread>
 #include <vector>
 
@@ -30,29 +29,54 @@ namespace {
 
 constexpr int32_t kNone = -1, kTerm = -2, kOrphan = -3;
 
+// FIFO of node ids with capacity n (a node is in each queue at most once)
+struct Fifo {
+    std::vector<int32_t> buf;
+    size_t head = 0, tail = 0, cnt = 0;
+    void init(int32_t n) { buf.assign((size_t)std::max(n, 1), 0); }
+    bool empty() const { return cnt == 0; }
+    int32_t front() const { return buf[head]; }
+    void push(int32_t v)
+    {
+        buf[tail] = v;
+        tail = tail + 1 == buf.size() ? 0 : tail + 1;
+        cnt++;
+    }
+    void pop()
+    {
+        head = head + 1 == buf.size() ? 0 : head + 1;
+        cnt--;
+    }
+};
+
+// per-node search state, packed (one cache line touch per node visit)
+struct NodeSt {
+    int32_t parent, ts, dist;
+    uint8_t tree, in_active, pad0, pad1;
+};
+
 struct BK {
     int32_t n;
     const int32_t *first, *head;
     std::vector<int32_t> sister;
     std::vector<i128> rc, tr;
-    std::vector<int32_t> parent, ts, dist;
-    std::vector<uint8_t> tree, in_active;
-    std::deque<int32_t> active, orphans;
+    std::vector<NodeSt> nd;
+    Fifo active, orphans;
     int32_t time = 0;
     i128 flow = 0;
     int64_t n_aug = 0, n_orphan = 0;
 
     void activate(int32_t i)
     {
-        if (!in_active[i]) {
-            in_active[i] = 1;
-            active.push_back(i);
+        if (!nd[i].in_active) {
+            nd[i].in_active = 1;
+            active.push(i);
         }
     }
     void make_orphan(int32_t k)
     {
-        parent[k] = kOrphan;
-        orphans.push_back(k);
+        nd[k].parent = kOrphan;
+        orphans.push(k);
         n_orphan++;
     }
 
@@ -62,48 +86,50 @@ struct BK {
     {
         while (!active.empty()) {
             const int32_t i = active.front();
-            if (tree[i] == 0) {
-                active.pop_front();
-                in_active[i] = 0;
+            NodeSt &ni = nd[i];
+            if (ni.tree == 0) {
+                active.pop();
+                ni.in_active = 0;
                 continue;
             }
             for (int32_t a = first[i]; a < first[i + 1]; a++) {
                 const int32_t j = head[a];
-                if (tree[i] == 1) {
+                NodeSt &nj = nd[j];
+                if (ni.tree == 1) {
                     if (rc[a] == 0) continue;
-                    if (tree[j] == 0) {
-                        tree[j] = 1;
-                        parent[j] = sister[a];
-                        ts[j] = ts[i];
-                        dist[j] = dist[i] + 1;
+                    if (nj.tree == 0) {
+                        nj.tree = 1;
+                        nj.parent = sister[a];
+                        nj.ts = ni.ts;
+                        nj.dist = ni.dist + 1;
                         activate(j);
-                    } else if (tree[j] == 2) {
+                    } else if (nj.tree == 2) {
                         return a;
-                    } else if (ts[j] <= ts[i] && dist[j] > dist[i]) {
-                        parent[j] = sister[a];
-                        ts[j] = ts[i];
-                        dist[j] = dist[i] + 1;
+                    } else if (nj.ts <= ni.ts && nj.dist > ni.dist) {
+                        nj.parent = sister[a];
+                        nj.ts = ni.ts;
+                        nj.dist = ni.dist + 1;
                     }
                 } else {
                     const int32_t sa = sister[a];
                     if (rc[sa] == 0) continue;
-                    if (tree[j] == 0) {
-                        tree[j] = 2;
-                        parent[j] = sa;
-                        ts[j] = ts[i];
-                        dist[j] = dist[i] + 1;
+                    if (nj.tree == 0) {
+                        nj.tree = 2;
+                        nj.parent = sa;
+                        nj.ts = ni.ts;
+                        nj.dist = ni.dist + 1;
                         activate(j);
-                    } else if (tree[j] == 1) {
+                    } else if (nj.tree == 1) {
                         return sa;
-                    } else if (ts[j] <= ts[i] && dist[j] > dist[i]) {
-                        parent[j] = sa;
-                        ts[j] = ts[i];
-                        dist[j] = dist[i] + 1;
+                    } else if (nj.ts <= ni.ts && nj.dist > ni.dist) {
+                        nj.parent = sa;
+                        nj.ts = ni.ts;
+                        nj.dist = ni.dist + 1;
                     }
                 }
             }
-            active.pop_front();
-            in_active[i] = 0;
+            active.pop();
+            ni.in_active = 0;
         }
         return -1;
     }
@@ -114,7 +140,7 @@ struct BK {
         const int32_t i = head[sister[a]], j = head[a];
         i128 b = rc[a];
         for (int32_t k = i;;) {
-            const int32_t p = parent[k];
+            const int32_t p = nd[k].parent;
             if (p == kTerm) {
                 if (tr[k] < b) b = tr[k];
                 break;
@@ -123,7 +149,7 @@ struct BK {
             k = head[p];
         }
         for (int32_t k = j;;) {
-            const int32_t p = parent[k];
+            const int32_t p = nd[k].parent;
             if (p == kTerm) {
                 if (-tr[k] < b) b = -tr[k];
                 break;
@@ -134,7 +160,7 @@ struct BK {
         rc[a] -= b;
         rc[sister[a]] += b;
         for (int32_t k = i;;) {
-            const int32_t p = parent[k];
+            const int32_t p = nd[k].parent;
             if (p == kTerm) {
                 tr[k] -= b;
                 if (tr[k] == 0) make_orphan(k);
@@ -147,7 +173,7 @@ struct BK {
             k = nxt;
         }
         for (int32_t k = j;;) {
-            const int32_t p = parent[k];
+            const int32_t p = nd[k].parent;
             if (p == kTerm) {
                 tr[k] += b;
                 if (tr[k] == 0) make_orphan(k);
@@ -169,26 +195,26 @@ struct BK {
     {
         while (!orphans.empty()) {
             const int32_t i = orphans.front();
-            orphans.pop_front();
-            const int t = tree[i];
+            orphans.pop();
+            const int t = nd[i].tree;
             int32_t best = kNone, dmin = INT_MAX;
             for (int32_t a0 = first[i]; a0 < first[i + 1]; a0++) {
                 const int32_t j = head[a0];
-                if (tree[j] != t) continue;
+                if (nd[j].tree != t) continue;
                 if (!(t == 1 ? rc[sister[a0]] > 0 : rc[a0] > 0)) continue;
                 int32_t d = 0, k = j;
                 bool valid;
                 for (;;) {
-                    if (ts[k] == time) {
-                        d += dist[k];
+                    if (nd[k].ts == time) {
+                        d += nd[k].dist;
                         valid = true;
                         break;
                     }
-                    const int32_t p = parent[k];
+                    const int32_t p = nd[k].parent;
                     d++;
                     if (p == kTerm) {
-                        ts[k] = time;
-                        dist[k] = 1;
+                        nd[k].ts = time;
+                        nd[k].dist = 1;
                         valid = true;
                         break;
                     }
@@ -203,26 +229,26 @@ struct BK {
                     best = a0;
                     dmin = d;
                 }
-                for (k = j; ts[k] != time; k = head[parent[k]]) {
-                    ts[k] = time;
-                    dist[k] = d--;
+                for (k = j; nd[k].ts != time; k = head[nd[k].parent]) {
+                    nd[k].ts = time;
+                    nd[k].dist = d--;
                 }
             }
             if (best != kNone) {
-                parent[i] = best;
-                ts[i] = time;
-                dist[i] = dmin + 1;
+                nd[i].parent = best;
+                nd[i].ts = time;
+                nd[i].dist = dmin + 1;
                 continue;
             }
             for (int32_t a0 = first[i]; a0 < first[i + 1]; a0++) {
                 const int32_t j = head[a0];
-                if (tree[j] != t) continue;
+                if (nd[j].tree != t) continue;
                 if (t == 1 ? rc[sister[a0]] > 0 : rc[a0] > 0) activate(j);
-                const int32_t p = parent[j];
+                const int32_t p = nd[j].parent;
                 if (p >= 0 && head[p] == i) make_orphan(j);
             }
-            tree[i] = 0;
-            parent[i] = kNone;
+            nd[i].tree = 0;
+            nd[i].parent = kNone;
         }
     }
 };
@@ -240,11 +266,9 @@ static i128 maxflow_bk_one(int32_t nc, const int32_t *ptr, const int32_t *col, c
     g.sister.assign(m, -1);
     g.rc.assign(cap, cap + m);
     g.tr.resize(nc);
-    g.parent.assign(nc, kNone);
-    g.ts.assign(nc, 0);
-    g.dist.assign(nc, 0);
-    g.tree.assign(nc, 0);
-    g.in_active.assign(nc, 0);
+    g.nd.assign(nc, NodeSt{kNone, 0, 0, 0, 0, 0, 0});
+    g.active.init(nc);
+    g.orphans.init(nc);
     // sister arcs: rows are sorted, so the entries (v, u) with u < v are the
     // leading entries of row v in ascending u
     {
@@ -287,9 +311,9 @@ static i128 maxflow_bk_one(int32_t nc, const int32_t *ptr, const int32_t *col, c
     }
     for (int32_t u = 0; u < nc; u++) {
         if (g.tr[u] != 0) {
-            g.tree[u] = g.tr[u] > 0 ? 1 : 2;
-            g.parent[u] = kTerm;
-            g.dist[u] = 1;
+            g.nd[u].tree = g.tr[u] > 0 ? 1 : 2;
+            g.nd[u].parent = kTerm;
+            g.nd[u].dist = 1;
             g.activate(u);
         }
     }
